@@ -1,0 +1,224 @@
+/*
+ * auras_b200.h -- C ABI of the B200-native Auras hot path.
+ *
+ * Plain C: device pointers, host pointers, sizes and an opaque cudaStream_t
+ * passed as `void *`.  No torch / C++ types cross this boundary.  Every entry
+ * point launches asynchronously on the given stream and returns 0 on success
+ * or a negative AURAS_E_* code (the Python host maps codes onto the
+ * reference's FramepipeError tree, fp/errors.py:4-95).
+ *
+ * Each function names the reference interface it replaces.  Reference paths
+ * are relative to /root/reference; fp/ = pkg/src/framepipe/.
+ */
+#ifndef AURAS_B200_H
+#define AURAS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- errors */
+#define AURAS_OK 0
+#define AURAS_E_CUDA (-1)          /* CUDA runtime error (see auras_last_error) */
+#define AURAS_E_ARG (-2)           /* invalid argument / unsupported shape       */
+#define AURAS_E_ARCH (-3)          /* device is not sm_100                      */
+
+/* Last error message (thread-local, static storage). */
+const char *auras_last_error(void);
+/* ABI version; bumped whenever a struct below changes layout. */
+int auras_abi_version(void);
+/* 1 when the loaded device is compute capability 10.0 (B200). */
+int auras_device_ok(int device);
+
+/* -------------------------------------------------- public-context ring
+ * Replaces ContextStore (fp/context.py:98-175).  The ring lives in HBM:
+ *   payload  : K slots of `slot_bytes` bytes (written by producer kernels)
+ *   meta     : int64[K][2] = {frame, version} per slot, released last
+ *   state    : int64[4]    = {global version, last frame, publish count, err}
+ */
+
+/* ContextStore.publish (fp/context.py:129-143): release-store the slot's
+ * {frame, version} after the payload stores that precede it on `stream`;
+ * bumps the device version counter.  `expected_version` is the host mirror's
+ * version; a mismatch sets state[3]. */
+int auras_ring_commit(int64_t *meta, int64_t *state, int capacity, int64_t frame,
+                      int64_t expected_version, void *stream);
+
+/* ContextStore.fetch_entry / latest_entry (fp/context.py:145-164), resolved
+ * on the device: acquire-load the slot meta of frame `target`; if it does not
+ * hold `target` fall back to the newest slot (fp/executor.py:314-316).  Writes
+ * {slot, version, frame} to `out` (int64[3]) for in-kernel consumers and
+ * appends `version` at `version_log[log_index]`. */
+int auras_ring_fetch(const int64_t *meta, const int64_t *state, int capacity, int64_t target,
+                     int64_t *out, int64_t *version_log, int64_t log_index, void *stream);
+
+/* Copy `bytes` from device `src` into slot `slot` of the payload ring
+ * (ContextStore.publish of a host-built PublicContext). */
+int auras_ring_write(void *payload, int64_t slot_bytes, int slot, const void *src,
+                     int64_t bytes, void *stream);
+
+/* -------------------------------------------------- toy refinement policy
+ * The reference's own conditioning policy (fp/policy.py:217-246, 279-297) in
+ * fp64 on the device, bit-exact with numpy: x <- x + eta*(H - x). */
+
+/* PerceptionModel.start + identity apply_layers (fp/policy.py:76-85): store
+ * the 4-vector observation (host values, passed by value) into lane `lane`. */
+int auras_toy_ingest(double *latent, int lane, const double obs[4], double *x_state,
+                     const double x0[2], void *stream);
+
+/* PerceptionModel.finalize + ContextStore.publish (fp/policy.py:285-290,
+ * fp/context.py:129-143): H = latent[:2] - latent[2:4] into ring slot
+ * frame % capacity, then commit {frame, version}. */
+int auras_toy_publish(const double *latent, int lane, double *ring_payload, int64_t *meta,
+                      int64_t *state, int capacity, int64_t frame, int64_t version,
+                      void *stream);
+
+/* The stage iteration loop (fp/executor.py:325-331): for each of `n` active
+ * requests run iters[i] refinement steps on lane lanes[i], all reading the
+ * single context fetched by auras_ring_fetch (`fetched` = {slot,version,frame}). */
+int auras_toy_generate(double *x_state, const int *lanes, const int *iters, int n, double eta,
+                       const double *ring_payload, const int64_t *fetched, void *stream);
+
+/* GenerationModel.finish norm clip (fp/policy.py:240-244) into out[2]. */
+int auras_toy_finish(const double *x_state, int lane, double max_action, double *out,
+                     void *stream);
+
+/* -------------------------------------------------- diffusion policy (DP)
+ * Replaces PerceptionModel / GenerationModel arithmetic for the Diffusion
+ * Policy CNN plugin.  The host builds a program of
+ * conv ops once; every op is an implicit-GEMM convolution
+ *    out[s, oy, ox, m] = sum_{ky,kx,c} W[m, ky, kx, c] * in[s, oy*st-ph+ky, ox*st-pw+kx, c]
+ * followed by a fused epilogue (split-K reduce, bias, GroupNorm, activation,
+ * FiLM, residual, optional zero-stuffed / pooled store). */
+
+#define AURAS_DT_F32 0
+#define AURAS_DT_BF16 1
+
+#define AURAS_ACT_NONE 0
+#define AURAS_ACT_RELU 1
+#define AURAS_ACT_MISH 2
+
+typedef struct auras_conv_op {
+  /* operands (device pointers; element type = plan dtype) */
+  const void *w;          /* [M][Kp], K index = (ky*kw + kx)*Cin + c, zero padded to Kp */
+  const float *bias;      /* [M] or NULL                                            */
+  const void *in;         /* NHWC view: elem(s,y,x,c) = in[((s*H + y)*W + x)*in_pitch + in_coff + c] */
+  void *out;              /* NHWC view of the output                                 */
+  const float *gn_gamma;  /* [M] or NULL (no GroupNorm)                              */
+  const float *gn_beta;   /* [M]                                                     */
+  const void *res;        /* residual tensor (same type/shape as out view) or NULL   */
+  const float *res_f32;   /* residual as fp32 rows [S][Ho*Wo][M] or NULL             */
+  float *out_f32;         /* if non-NULL: also store the pre-residual result fp32    */
+  /* shapes */
+  int32_t M, Cin, Kp;
+  int32_t H, W, in_pitch, in_coff;
+  int32_t kh, kw, stride, pad_h, pad_w;
+  int32_t Ho, Wo, out_pitch, out_coff;
+  int32_t res_pitch, res_coff;
+  int32_t groups;         /* GroupNorm groups (ignored without gamma)                */
+  int32_t act;            /* AURAS_ACT_*                                             */
+  int32_t res_before_act; /* 1: act(gn(y) + res) (ResNet); 0: act(gn(y)) + res (UNet) */
+  int32_t film_off;       /* >=0: FiLM scale at film_off, bias at film_off+M          */
+  int32_t out_stuff;      /* 1: write out row 2*ox and a zero row 2*ox+1 (1-D only)  */
+  int32_t pool_out;       /* 1: store mean over Ho*Wo as out[s][m] (fp32, out_f32)    */
+  int32_t splits;         /* split-K factor chosen by the planner                    */
+  int32_t reserved[3];
+} auras_conv_op;
+
+/* Linear / GEMV: y[n][m] = sum_k W[m][k] * f(x[n][k]) + b[m], f = Mish or id. */
+typedef struct auras_linear_op {
+  const void *w;          /* [M][K] plan dtype */
+  const float *bias;      /* [M] or NULL       */
+  int32_t M, K;
+  int32_t mish_in;        /* apply Mish to the input first */
+  int32_t ldw;            /* weight row stride in elements (multiple of 8, >= K) */
+} auras_linear_op;
+
+/* Diffusion scheduler tables (DDPM / DDIM, computed on the host in fp64 and
+ * uploaded once): per inference step i,
+ *   timestep[i], c_x0[i], c_xt[i], c_eps[i] (DDIM), sigma[i] (DDPM),
+ *   sqrt_ab[i], sqrt_1mab[i]. */
+typedef struct auras_sched {
+  const int32_t *timestep;
+  const float *sqrt_ab, *sqrt_1mab, *c_x0, *c_xt, *c_eps, *sigma;
+  int32_t n_steps;
+  int32_t clip_sample;
+  int32_t ddpm;           /* 1: add sigma_i * noise_i */
+  int32_t reserved;
+} auras_sched;
+
+/* A compiled UNet program (opaque handle). */
+typedef struct auras_unet_plan auras_unet_plan;
+
+/* Build the plan: `ops` in execution order; `dtype` AURAS_DT_*; `s_max` the
+ * largest batch of samples per step; scratch is allocated inside.  The FiLM
+ * time table `film_tau` is [n_train][film_width] fp32; the FiLM row of
+ * (agent a, ring slot k) is at ring_film + a*ring_agent_stride +
+ * k*ring_slot_stride (floats).  `final_w`/`final_b` is the final 1x1 conv
+ * (action_dim x C0).  `x_in_op` is the index of the op whose input is the
+ * noisy action buffer. */
+auras_unet_plan *auras_unet_plan_create(const auras_conv_op *ops, int n_ops, int dtype,
+                                        int s_max, int horizon, int action_dim,
+                                        const float *film_tau, const float *ring_film,
+                                        int film_width, int64_t ring_slot_stride,
+                                        int64_t ring_agent_stride,
+                                        const void *final_w, const float *final_b,
+                                        int final_cin, const auras_sched *sched,
+                                        void *x_in_buffer, int x_in_pitch);
+void auras_unet_plan_destroy(auras_unet_plan *plan);
+
+/* The batched, staggered-timestep denoise chain for one frame
+ * (fp/executor.py:318-349 + GenerationModel.step fp/policy.py:217-228):
+ * sample s works on request lane lanes[s] of agent agents[s], starting at
+ * inference step start[s] and running count[s] steps; `iters` = max(count).
+ * Every sample reads FiLM rows from ring slot fetched[agents[s]*3] (written
+ * by auras_ring_fetch).  x_lanes: [A][R][horizon][action_dim] fp32,
+ * noise_lanes: [A][R][n_steps][horizon][action_dim] fp32 (DDPM) or NULL.
+ * use_graph: capture the iteration chain into a CUDA graph (cached per
+ * (S, iters)). */
+int auras_unet_generate(auras_unet_plan *plan, int S, const int *lanes, const int *agents,
+                        const int *start, const int *count, int iters, int lanes_per_agent,
+                        float *x_lanes, const float *noise_lanes, const int64_t *fetched,
+                        int use_graph, void *stream);
+
+/* One conv op (standalone; used by the perception encoder and by tests). */
+int auras_conv(const auras_conv_op *op, int dtype, int S, const float *film_rows,
+               int film_stride, float *scratch, int64_t scratch_floats, void *stream);
+
+/* Linear / GEMV for N input rows: y[n][m] (fp32, row stride ldy). */
+int auras_linear(const auras_linear_op *op, int dtype, int N, const float *x, int ldx,
+                 float *y, int ldy, void *stream);
+
+/* Perception helpers (K1): uint8 CHW frames -> dtype NHWC in [-1, 1] padded
+ * to `cpad` channels; 3x3/s2/p1 max pool on NHWC. */
+int auras_image_to_nhwc(const uint8_t *img, int S, int C, int H, int W, void *out, int cpad,
+                        int dtype, void *stream);
+int auras_maxpool3s2(const void *in, int S, int H, int W, int C, void *out, int dtype,
+                     void *stream);
+
+/* Assemble global_cond rows (the ContextStore.publish payload of the DP
+ * plugin): for agent a, row = [feat_prev, pos_prev, feat, pos] (n_obs_steps
+ * = 2) or [feat, pos] (1); feat_prev/pos_prev are the agent's previous
+ * publish (the current one when `first`).  Row a is written at
+ * gc_out + a * gc_row_stride (the agent's ring slot). */
+int auras_dp_assemble_cond(const float *feat, const float *pos, float *prev_cache, int A,
+                           int feat_dim, int pos_dim, int n_obs_steps, int first,
+                           float *gc_out, int64_t gc_row_stride, void *stream);
+
+/* Sinusoidal timestep embedding rows for timesteps t[0..n): out[n][dim]. */
+int auras_sinusoidal(const int32_t *t, int n, int dim, float *out, void *stream);
+
+/* Initialise request lane state: x_lanes[a][lane] <- x0 (device fp32 rows). */
+int auras_dp_copy_rows(float *dst, const float *src, int64_t n_floats, void *stream);
+
+/* GenerationModel.finish for DP: copy the denoised horizon of (agent, lane)
+ * into out[agent][...] (fp32). */
+int auras_dp_finish(const float *x_lanes, int A, const int *agents, const int *lanes, int n,
+                    int lanes_per_agent, int row_floats, float *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AURAS_B200_H */

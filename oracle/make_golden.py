@@ -1,0 +1,258 @@
+"""Generate the golden fixtures under tests/golden/ from the UNMODIFIED reference.
+
+Test infrastructure only (see oracle/__init__.py).  Run in the build container,
+where /root/reference exists:
+
+    PYTHONPATH=/root/reference/pkg/src python oracle/make_golden.py
+
+It imports `framepipe` read-only and records, for a fixed list of cases:
+
+* partition goldens: `split_generation` / `split_perception` outputs
+  (fp/partition.py:57-123), including the seeded fuzz sets the reference tests
+  use (t/test_partition.py:42-82);
+* schedule goldens: complete schema-1 traces and RequestRecords of
+  `run_pipelined` (fp/executor.py:200-399) and `run_sequential`
+  (fp/executor.py:406-461) with the toy refinement policy
+  (fp/policy.py:279-297).  Closed-loop cases also record every observation
+  vector the TrackingEnv produced (fp/envsim.py:89-95) and every sealed error,
+  so the GPU box (which has no /root/reference) can replay them open-loop: if
+  the device engine's actions are bit-identical, the closed loop would have
+  produced the same observations.
+
+Nothing here is imported by the product package.
+"""
+
+from __future__ import annotations
+
+import gzip
+import json
+import math
+import os
+import random
+import sys
+
+import numpy as np
+
+REF_SRC = "/root/reference/pkg/src"
+if REF_SRC not in sys.path:
+    sys.path.insert(0, REF_SRC)
+
+from framepipe.envsim import CirclePath, TrackingEnv  # noqa: E402
+from framepipe.executor import PipelineConfig, run_pipelined, run_sequential  # noqa: E402
+from framepipe.partition import split_generation, split_perception  # noqa: E402
+from framepipe.policy import make_conditioning_policy  # noqa: E402
+
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden")
+
+
+class RecordingEnv:
+    """Wraps a reference TrackingEnv and records what the executor saw."""
+
+    def __init__(self, env):
+        self.env = env
+        self.success_threshold = env.success_threshold
+        self.observations = {}
+        self.errors = []
+        self.applied = []
+
+    def observe(self, frame):
+        obs = self.env.observe(frame)
+        self.observations[frame] = [float(v) for v in obs.vector]
+        return obs
+
+    def apply_action(self, action):
+        self.applied.append([float(v) for v in np.asarray(action, dtype=np.float64)])
+        self.env.apply_action(action)
+
+    def advance_frame(self):
+        self.env.advance_frame()
+
+    @property
+    def last_error(self):
+        err = self.env.last_error
+        self.errors.append(float(err))
+        return err
+
+
+def tracking_env(seed, frames=300, omega_deg=15.0, sigma=0.02):
+    return TrackingEnv(path=CirclePath(radius=1.0, omega=math.radians(omega_deg)),
+                       noise_sigma=sigma, max_step=0.8, episode_frames=frames, seed=seed)
+
+
+def _jsonable(x):
+    if isinstance(x, dict):
+        return {k: _jsonable(v) for k, v in x.items()}
+    if isinstance(x, (list, tuple)):
+        return [_jsonable(v) for v in x]
+    if isinstance(x, (np.floating,)):
+        return float(x)
+    if isinstance(x, (np.integer,)):
+        return int(x)
+    return x
+
+
+def record_case(name, mode, policy_kw, duration, cfg_kw=None, env_seed=None,
+                seq_interval=None, env_kw=None):
+    policy = make_conditioning_policy(**policy_kw)
+    env = None
+    if env_seed is not None:
+        env = RecordingEnv(tracking_env(env_seed, **(env_kw or {})))
+    if mode == "pipe":
+        cfg = PipelineConfig(**cfg_kw)
+        result = run_pipelined(cfg, policy, env, duration)
+    else:
+        result = run_sequential(policy, env, duration, frame_interval=seq_interval)
+    case = {
+        "name": name,
+        "mode": mode,
+        "policy": policy_kw,
+        "duration": duration,
+        "pipeline": cfg_kw,
+        "seq_interval": seq_interval,
+        "trace": _jsonable(result.trace),
+        "requests": [_jsonable(vars(r)) for r in result.requests],
+        "actions": [[float(v) for v in a.values] for a in result.actions],
+        "staleness_profiles": [list(a.staleness_profile) for a in result.actions],
+        "env": None,
+    }
+    if env is not None:
+        case["env"] = {
+            "seed": env_seed,
+            "kw": env_kw or {},
+            "success_threshold": env.success_threshold,
+            "observations": [env.observations[t] for t in sorted(env.observations)],
+            "errors": env.errors,
+            "applied": env.applied,
+        }
+    return case
+
+
+SIX = dict(layer_costs=(1.0, 1.0), n_iterations=4, step_cost=1.0)
+CAL = dict(layer_costs=(14.0, 14.0), n_iterations=100, step_cost=1.0, eta=0.08, max_action=0.8)
+STALE = dict(layer_costs=(1.0,), n_iterations=100, step_cost=0.01)
+NOISY16 = dict(layer_costs=(14.0, 14.0), n_iterations=16, step_cost=1.0, noise_init=True)
+NOISY100 = dict(layer_costs=(14.0, 14.0), n_iterations=100, step_cost=1.0, noise_init=True)
+SKEW = dict(layer_costs=(128.0, 128.0), n_iterations=100, step_cost=1.0, max_action=0.8)
+MULTI = dict(layer_costs=(3.0, 5.0, 2.0, 4.0), n_iterations=30, step_cost=1.0, noise_init=True)
+
+
+def schedule_cases():
+    pc = PipelineConfig
+    cases = []
+    # t/test_executor.py:52-59 throughput law, :67-74 steady emission, :94-108
+    for pp in ((2, 4), (1, 2), (1, 1)):
+        cases.append(record_case(f"six_pipe_{pp[0]}{pp[1]}_m1", "pipe", SIX, 48,
+                                 dict(pp_perception=pp[0], pp_generation=pp[1], fetch_offset=-1)))
+    cases.append(record_case("six_pipe_24_m1_interval1", "pipe", SIX, 40,
+                             dict(pp_perception=2, pp_generation=4, fetch_offset=-1, frame_interval=1.0)))
+    cases.append(record_case("six_pipe_24_off0", "pipe", SIX, 48,
+                             dict(pp_perception=2, pp_generation=4, fetch_offset=0)))
+    cases.append(record_case("six_seq", "seq", SIX, 48))
+    # t/test_executor.py:76-92 staleness profile and final age
+    cases.append(record_case("stale_14_m1", "pipe", STALE, 30,
+                             dict(pp_perception=1, pp_generation=4, fetch_offset=-1, frame_interval=1.0)))
+    cases.append(record_case("stale_14_off0_i2", "pipe", STALE, 30,
+                             dict(pp_perception=1, pp_generation=4, fetch_offset=0, frame_interval=2.0)))
+    # :127-135 offset -2 with K = 4
+    cases.append(record_case("stale_12_m2_k4", "pipe", STALE, 30,
+                             dict(pp_perception=1, pp_generation=2, fetch_offset=-2,
+                                  store_capacity=4, frame_interval=2.0)))
+    # :110-125 mode equivalence (closed loop, env seed 11)
+    cases.append(record_case("cal_seq_env11", "seq", CAL, 200, env_seed=11, seq_interval=128.0))
+    cases.append(record_case("cal_pipe_11_off0_env11", "pipe", CAL, 200,
+                             dict(pp_perception=1, pp_generation=1, fetch_offset=0, frame_interval=128.0),
+                             env_seed=11))
+    # :137-167 snapshot / live, closed loop
+    for mode in ("snapshot", "live"):
+        cases.append(record_case(f"cal_pipe_12_m1_{mode}_env4", "pipe", CAL, 120,
+                                 dict(pp_perception=1, pp_generation=2, fetch_offset=-1,
+                                      frame_interval=64.0, read_policy=mode), env_seed=4))
+    # seq with dropped observations (:42-48)
+    cases.append(record_case("cal_seq_i64", "seq", CAL, 20, seq_interval=64.0))
+    # :178-199 overrun stretch / drop
+    for pol in ("stretch", "drop"):
+        cases.append(record_case(f"six_pipe_11_m1_{pol}", "pipe", SIX, 21,
+                                 dict(pp_perception=1, pp_generation=1, fetch_offset=-1,
+                                      frame_interval=3.0, overrun_policy=pol)))
+    # SURVEY appendix A dumps: noise-initialised 16-step policy
+    for pp, off in (((1, 2), 0), ((1, 2), -1), ((1, 4), 0), ((1, 4), -1)):
+        cases.append(record_case(f"noisy16_pipe_{pp[0]}{pp[1]}_off{off}", "pipe", NOISY16, 40,
+                                 dict(pp_perception=pp[0], pp_generation=pp[1], fetch_offset=off)))
+    cases.append(record_case("noisy16_seq", "seq", NOISY16, 40))
+    # skewed partitions (t/test_partition.py:15-19; t/test_acceptance.py:180-201)
+    cases.append(record_case("noisy100_pipe_14_a05", "pipe", NOISY100, 40,
+                             dict(pp_perception=1, pp_generation=4, fetch_offset=0, alpha=0.5)))
+    cases.append(record_case("skew_pipe_15_a1_env2", "pipe", SKEW, 80,
+                             dict(pp_perception=1, pp_generation=5, fetch_offset=0, alpha=1.0),
+                             env_seed=2, env_kw=dict(omega_deg=24.0)))
+    # depth sweep at n = 100 (SURVEY appendix A virtual k-sweep), both offsets
+    for k in (3, 5, 8):
+        for off in (0, -1):
+            cases.append(record_case(f"noisy100_pipe_1{k}_off{off}", "pipe", NOISY100, 30,
+                                     dict(pp_perception=1, pp_generation=k, fetch_offset=off)))
+    cases.append(record_case("noisy100_seq", "seq", NOISY100, 30))
+    # multi-stage perception (pp_p > 1) and deeper offsets
+    cases.append(record_case("multi_pipe_23_m1", "pipe", MULTI, 36,
+                             dict(pp_perception=2, pp_generation=3, fetch_offset=-1)))
+    cases.append(record_case("multi_pipe_32_m2_k3", "pipe", MULTI, 36,
+                             dict(pp_perception=3, pp_generation=2, fetch_offset=-2, store_capacity=3)))
+    cases.append(record_case("multi_pipe_42_off0_live", "pipe", MULTI, 36,
+                             dict(pp_perception=4, pp_generation=2, fetch_offset=0, read_policy="live")))
+    return cases
+
+
+def partition_goldens():
+    out = {"generation": [], "perception": []}
+    fixed = [(100, 4, 0.0), (100, 4, 0.5), (100, 5, 1.0), (100, 5, 0.0), (7, 1, 0.0),
+             (3, 5, 1.5), (100, 5, -1.0), (16, 2, 0.0), (100, 8, 0.0), (100, 3, 0.0),
+             (100, 7, 0.0), (40, 6, 0.25), (100, 5, 2.0), (1, 1, 0.0)]
+    for alpha in (0.0, 0.25, 0.5, 0.75, 1.0, 1.5, 2.0):
+        fixed.append((100, 5, alpha))
+    rng = random.Random(20240817)  # same seed as t/test_partition.py:43
+    for _ in range(600):
+        n = rng.randint(1, 10_000)
+        s = rng.randint(1, 16)
+        alpha = rng.uniform(-2.0, 2.0)
+        if alpha == 0.0 and n < s:
+            continue
+        fixed.append((n, s, alpha))
+    rng = random.Random(7)  # t/test_partition.py:55
+    for _ in range(200):
+        s = rng.randint(1, 16)
+        n = rng.randint(s, 5000)
+        fixed.append((n, s, 0.0))
+    for n, s, a in fixed:
+        out["generation"].append({"n": n, "stages": s, "alpha": a,
+                                  "counts": split_generation(n, s, a)})
+    rng = random.Random(5)  # t/test_partition.py:117
+    pcases = [([1.0, 1.0, 1.0, 1.0], 2), ([3.0, 1.0, 1.0, 1.0], 2), ([2.0, 5.0, 1.0], 1)]
+    for _ in range(200):
+        n = rng.randint(1, 9)
+        costs = [float(rng.randint(1, 20)) for _ in range(n)]
+        pcases.append((costs, rng.randint(1, n)))
+    for costs, st in pcases:
+        out["perception"].append({"costs": costs, "stages": st,
+                                  "ranges": [list(r) for r in split_perception(costs, st)]})
+    # fault-hook golden (t/test_partition.py:96-99)
+    os.environ["FRAMEPIPE_ROUNDING_FAULT"] = "truncate"
+    try:
+        out["fault_truncate"] = {"n": 100, "stages": 4, "alpha": 0.5,
+                                 "counts": split_generation(100, 4, 0.5)}
+    finally:
+        del os.environ["FRAMEPIPE_ROUNDING_FAULT"]
+    return out
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    with gzip.open(os.path.join(OUT, "partition.json.gz"), "wt") as fh:
+        json.dump(partition_goldens(), fh)
+    cases = schedule_cases()
+    with gzip.open(os.path.join(OUT, "schedules.json.gz"), "wt") as fh:
+        json.dump({"generator": "oracle/make_golden.py", "reference": REF_SRC,
+                   "numpy": np.__version__, "cases": cases}, fh)
+    print(f"wrote {len(cases)} schedule cases to {OUT}")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,386 @@
+"""Virtual-time restatement of the reference frame executor (TEST ORACLE).
+
+Restates, for conditioning (iterative-refinement) policies only:
+
+* `split_generation`  -- fp/partition.py:101-123 (weights e^{(i+1)a}, fsum
+  total, running-sum cumulative fractions, round-half-up boundaries, last
+  boundary forced to n, FRAMEPIPE_ROUNDING_FAULT hook fp/partition.py:18-30);
+* `split_perception`  -- fp/partition.py:57-98 (exact min-max contiguous
+  split; ties resolved towards the earliest cut, as the reference's strict
+  `<` comparison does);
+* `Ring`              -- fp/context.py:98-164 (K slots, version counter,
+  StaleWrite / NotYetPublished / OffsetOutOfRange semantics);
+* `run_pipelined`     -- fp/executor.py:200-399;
+* `run_sequential`    -- fp/executor.py:406-461.
+
+The arithmetic of every float that reaches the trace (stage costs, frame
+durations, the clock, JCT, staleness means) is performed with the same
+operations in the same order as the reference, so traces compare equal with
+`==`.  The model arithmetic is delegated to a policy object with the
+reference's duck type (fp/executor.py:216-330).
+"""
+
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+class OracleError(Exception):
+    pass
+
+
+class NotYetPublished(OracleError):
+    pass
+
+
+class OffsetOutOfRange(OracleError):
+    pass
+
+
+class StaleWrite(OracleError):
+    pass
+
+
+class DeadlockDetected(OracleError):
+    pass
+
+
+# ---------------------------------------------------------------- partition
+
+def _half_up(x: float) -> int:
+    return int(math.floor(x + 0.5))
+
+
+def split_generation(n: int, stages: int, alpha: float = 0.0) -> list[int]:
+    """fp/partition.py:101-123."""
+    if n < 1 or stages < 1 or (alpha == 0.0 and n < stages):
+        raise OracleError("invalid stage count")
+    rounding = (lambda v: int(math.floor(v))) \
+        if os.environ.get("FRAMEPIPE_ROUNDING_FAULT") == "truncate" else _half_up
+    w = [math.exp(alpha * (i + 1)) for i in range(stages)]
+    denom = math.fsum(w)
+    bounds, running = [], 0.0
+    for i, wi in enumerate(w):
+        running += wi
+        bounds.append(n if i == stages - 1 else rounding(n * (running / denom)))
+    out, prev = [], 0
+    for b in bounds:
+        b = min(max(b, prev), n)
+        out.append(b - prev)
+        prev = b
+    return out
+
+
+def split_perception(costs, stages: int) -> list[tuple[int, int]]:
+    """fp/partition.py:57-98: minimise the largest contiguous stage cost."""
+    costs = [float(c) for c in costs]
+    n = len(costs)
+    if stages < 1 or stages > n:
+        raise OracleError("too many stages")
+    pre = [0.0]
+    for c in costs:
+        pre.append(pre[-1] + c)
+    inf = float("inf")
+    # best[s][i]: optimal max-cost splitting the first i layers into s stages
+    best = [[inf] * (n + 1) for _ in range(stages + 1)]
+    arg = [[0] * (n + 1) for _ in range(stages + 1)]
+    best[0][0] = 0.0
+    for s in range(1, stages + 1):
+        for i in range(s, n + 1):
+            for j in range(s - 1, i):
+                v = max(best[s - 1][j], pre[i] - pre[j])
+                if v < best[s][i]:
+                    best[s][i], arg[s][i] = v, j
+    cuts, i = [], n
+    for s in range(stages, 0, -1):
+        cuts.append((arg[s][i], i))
+        i = arg[s][i]
+    return cuts[::-1]
+
+
+# ---------------------------------------------------------------- ring store
+
+@dataclass
+class Ring:
+    """fp/context.py:98-164 without the threading (the oracle is serial)."""
+
+    capacity: int = 2
+    version: int = 0
+    last_frame: int | None = None
+    slots: list = field(default_factory=list)
+
+    def __post_init__(self):
+        self.slots = [None] * self.capacity
+
+    def publish(self, payload, frame: int) -> int:
+        if self.last_frame is not None and frame < self.last_frame:
+            raise StaleWrite(frame)
+        self.version += 1
+        self.slots[frame % self.capacity] = (frame, self.version, payload)
+        self.last_frame = frame
+        return self.version
+
+    def fetch_entry(self, frame: int, offset: int):
+        if offset > 0 or -offset >= self.capacity:
+            raise OffsetOutOfRange(offset)
+        want = frame + offset
+        slot = self.slots[want % self.capacity]
+        if slot is None or slot[0] != want:
+            raise NotYetPublished(want)
+        return slot[1], slot[0], slot[2]
+
+    def latest_entry(self):
+        if self.last_frame is None:
+            raise NotYetPublished("empty")
+        slot = self.slots[self.last_frame % self.capacity]
+        return slot[1], slot[0], slot[2]
+
+
+# ---------------------------------------------------------------- executor
+
+@dataclass
+class Request:
+    observation_id: int
+    birth_frame: int
+    birth_time: float
+    completion_frame: int = -1
+    completion_time: float = -1.0
+    jct: float = -1.0
+    context_versions: list = field(default_factory=list)
+
+
+@dataclass
+class OracleResult:
+    actions: list
+    trace: list
+    requests: list
+
+
+class _Landing:
+    """Boundary protocol of fp/executor.py:146-184 (land newest, then observe)."""
+
+    def __init__(self, env, policy):
+        self.env, self.policy, self.queue = env, policy, []
+        self.last_superseded = 0
+
+    def boundary(self, frame):
+        due = [q for q in self.queue if q[0] == frame]
+        self.last_superseded = 0
+        if due:
+            self.queue = [q for q in self.queue if q[0] != frame]
+            chosen = max(due, key=lambda q: q[1])
+            self.last_superseded = len(due) - 1
+            if self.env is not None:
+                self.env.apply_action(self.policy.generation.decode_action(chosen[2]))
+        if self.env is None:
+            return self.policy.synthetic_observation(frame)
+        return self.env.observe(frame)
+
+    def seal(self):
+        if self.env is None:
+            return None
+        self.env.advance_frame()
+        return self.env.last_error
+
+
+def _frame_record(t, now):
+    return {"type": "frame", "frame": t, "start": now, "perception": [], "generation": [],
+            "publishes": [], "emissions": [], "prefill_calls": 0, "decode_calls": 0,
+            "generation_cost": 0.0, "dropped_observations": 0}
+
+
+def _emission(req_frame, time, t, land, jct, values, ages):
+    return {"request": req_frame, "time": time, "emission_frame": t, "land_frame": land,
+            "jct": jct, "action": list(values), "staleness_min": min(ages),
+            "staleness_mean": float(np.mean(ages)), "staleness_max": max(ages),
+            "staleness_final": ages[-1]}
+
+
+def run_pipelined(cfg: dict, policy, env, duration: int) -> OracleResult:
+    """fp/executor.py:200-399 for conditioning policies.
+
+    `cfg` is the PipelineConfig field dict (fp/executor.py:48-60)."""
+    pp_p, pp_g = cfg.get("pp_perception", 1), cfg.get("pp_generation", 1)
+    off = cfg.get("fetch_offset")
+    off = 0 if off is None else off
+    alpha = cfg.get("alpha", 0.0)
+    interval = cfg.get("frame_interval")
+    cap = cfg.get("store_capacity", 2)
+    read_policy = cfg.get("read_policy", "snapshot")
+    overrun = cfg.get("overrun_policy", "stretch")
+    perc, gen = policy.perception, policy.generation
+
+    ranges = split_perception(perc.layer_costs, pp_p)
+    counts = split_generation(gen.n_iterations, pp_g, alpha)
+    shift = pp_p - 1 - off            # birth -> first generation stage
+    span = shift + pp_g               # birth -> emission, inclusive
+    p_cost = [sum(perc.layer_costs[a:b]) for a, b in ranges]
+    full_cfg = {"pp_perception": pp_p, "pp_generation": pp_g,
+                "fetch_offset": cfg.get("fetch_offset"), "alpha": alpha,
+                "frame_interval": interval,
+                "merge_autoregressive": cfg.get("merge_autoregressive"),
+                "store_capacity": cap, "read_policy": read_policy,
+                "overrun_policy": overrun}
+    trace = [{"type": "header", "schema": 1, "mode": "pipe", "engine": "virtual",
+              "frame_interval": interval, "duration": duration,
+              "config": {"pipeline": full_cfg,
+                         "plan": {"perception_stages": [list(r) for r in ranges],
+                                  "generation_stages": list(counts), "alpha": alpha},
+                         "fetch_offset": off, "merged": False},
+              "success_threshold": getattr(env, "success_threshold", None)}]
+
+    ring = Ring(cap)
+    port = _Landing(env, policy)
+    live: dict[int, dict] = {}    # birth frame -> request state
+    requests, actions = [], []
+    now, skip = 0.0, 0
+    for t in range(duration):
+        rec = _frame_record(t, now)
+        obs = port.boundary(t)
+        rec["superseded_actions"] = port.last_superseded
+        if skip:
+            skip -= 1
+            rec["dropped_observations"] += 1
+        else:
+            r = Request(observation_id=obs.id, birth_frame=t, birth_time=now)
+            live[t] = {"req": r, "obs": obs, "latent": perc.start(obs),
+                       "state": gen.initial_state(seed=t), "ages": []}
+            requests.append(r)
+
+        early = None
+        if off <= -1 and read_policy == "snapshot":
+            try:
+                early = ring.fetch_entry(t, off)
+            except NotYetPublished:
+                early = None
+
+        side_costs, pub_cost, published = [], 0.0, False
+        for s in range(1, pp_p + 1):
+            item = live.get(t - s + 1)
+            if item is None:
+                continue
+            lo, hi = ranges[s - 1]
+            item["latent"] = perc.apply_layers(item["latent"], lo, hi)
+            entry = {"request": t - s + 1, "stage": s, "cost": p_cost[s - 1],
+                     "published_version": None}
+            if s == pp_p:
+                ctx = perc.finalize(item["latent"], item["obs"])
+                v = ring.publish(ctx, t)
+                entry["published_version"] = v
+                rec["publishes"].append(v)
+                pub_cost, published = p_cost[s - 1], True
+            else:
+                side_costs.append(p_cost[s - 1])
+            rec["perception"].append(entry)
+
+        active = [(j, t - shift - (j - 1)) for j in range(1, pp_g + 1)
+                  if (t - shift - (j - 1)) in live]
+        gen_costs = []
+        if active:
+            if early is not None:
+                version, ctx_frame, ctx = early
+            else:
+                try:
+                    version, ctx_frame, ctx = ring.fetch_entry(t, off)
+                except NotYetPublished:
+                    if t + off < pp_p - 1:
+                        raise DeadlockDetected(t)
+                    version, ctx_frame, ctx = ring.latest_entry()
+            for j, b in active:
+                item = live[b]
+                iters = counts[j - 1]
+                age = float(b + span - 1 - ctx_frame)
+                for _ in range(iters):
+                    item["state"] = gen.step(item["state"], ctx)
+                item["ages"].extend([age] * iters)
+                item["req"].context_versions.append(version)
+                c = iters * gen.step_cost
+                gen_costs.append(c)
+                rec["generation_cost"] += c
+                rec["generation"].append({"request": b, "stage": j, "iterations": iters,
+                                          "context_version": version,
+                                          "context_frame": ctx_frame,
+                                          "context_age_at_emission": age})
+
+        if off == 0 and gen_costs and published:
+            busiest = max(side_costs + [pub_cost + max(gen_costs)])
+        else:
+            pool = side_costs + gen_costs + ([pub_cost] if published else [])
+            busiest = max(pool) if pool else 0.0
+        if interval is None:
+            dur = busiest
+        elif busiest <= interval:
+            dur = interval
+        elif overrun == "stretch":
+            dur, rec["overrun"] = busiest, True
+        else:
+            q = math.ceil(busiest / interval)
+            dur, rec["overrun"] = q * interval, True
+            skip += q - 1
+        now += dur
+        rec["end"] = now
+
+        done = live.pop(t - span + 1, None)
+        if done is not None:
+            a = gen.finish(done["state"], emitted_frame=t,
+                           staleness_profile=tuple(done["ages"]))
+            actions.append(a)
+            r = done["req"]
+            r.completion_frame, r.completion_time = t + 1, now
+            r.jct = now - r.birth_time
+            port.queue.append((t + 1, now, a))
+            rec["emissions"].append(_emission(t - span + 1, now, t, t + 1, r.jct,
+                                              a.values, done["ages"]))
+        rec["env_error"] = port.seal()
+        trace.append(rec)
+    return OracleResult(actions, trace, requests)
+
+
+def run_sequential(policy, env, duration: int, frame_interval=None) -> OracleResult:
+    """fp/executor.py:406-461."""
+    gen = policy.generation
+    cost = policy.sequential_cost
+    interval = frame_interval if frame_interval is not None else cost
+    per_req = max(1, math.ceil(cost / interval - 1e-12))
+    trace = [{"type": "header", "schema": 1, "mode": "seq", "engine": "virtual",
+              "frame_interval": interval, "duration": duration,
+              "config": {"request_cost": cost},
+              "success_threshold": getattr(env, "success_threshold", None)}]
+    port = _Landing(env, policy)
+    actions, requests = [], []
+    free_at = 0
+    for t in range(duration):
+        now = t * interval
+        rec = _frame_record(t, now)
+        rec["end"] = now + interval
+        obs = port.boundary(t)
+        rec["superseded_actions"] = port.last_superseded
+        if t >= free_at:
+            r = Request(observation_id=obs.id, birth_frame=t, birth_time=now)
+            ctx = policy.perception.perceive(obs)
+            state = gen.initial_state(seed=t)
+            for _ in range(gen.n_iterations):
+                state = gen.step(state, ctx)
+            emit = t + per_req - 1
+            age = float(emit - ctx.produced_frame)
+            a = gen.finish(state, emitted_frame=emit,
+                           staleness_profile=(age,) * gen.n_iterations)
+            land = t + per_req
+            r.completion_frame, r.completion_time, r.jct = land, now + cost, cost
+            r.context_versions.append(1)
+            requests.append(r)
+            actions.append(a)
+            port.queue.append((land, now + cost, a))
+            free_at = land
+            rec["generation_cost"] = gen.total_cost
+            rec["emissions"].append(_emission(t, now + cost, emit, land, cost, a.values,
+                                              [age]))
+        else:
+            rec["dropped_observations"] = 1
+        rec["env_error"] = port.seal()
+        trace.append(rec)
+    return OracleResult(actions, trace, requests)

@@ -1,0 +1,38 @@
+"""B200-native Auras hot path: perception -> public-context ring in HBM ->
+batched staggered-timestep denoise chain, run as a frame-clocked pipeline on
+two CUDA streams.
+
+Drop-in names of the reference package (fp/__init__.py:5-37) for the hot path:
+`ContextKind`, `ContextStore`, `PublicContext`, `PipelineConfig`, `RunResult`,
+`RequestRecord`, `run_pipelined`, `run_sequential`, `Policy`,
+`make_conditioning_policy`, `StagePlan`, `plan_stages`, `split_generation`,
+`split_perception`, `RolloutMetrics`, `summarize`; plus the Diffusion Policy
+CNN plugin `make_diffusion_policy`.
+"""
+
+__version__ = "0.1.0"
+
+from .context import ContextKind, ContextStore, PublicContext
+from .errors import (ConfigInvalid, DeadlockDetected, DeviceError, FramepipeError,
+                     IncompleteGeneration, InvalidStageCount, KindMismatch, NotYetPublished,
+                     OffsetOutOfRange, ShapeMismatch, StaleWrite, TooManyStages)
+from .executor import PipelineConfig, RequestRecord, RunResult, run_pipelined, run_sequential
+from .metrics import RolloutMetrics, summarize
+from .partition import StagePlan, plan_stages, split_generation, split_perception
+from .policy import ActionOutput, Observation, Policy, make_conditioning_policy
+
+
+def make_diffusion_policy(*args, **kwargs):
+    from .diffusion import make_diffusion_policy as _make
+    return _make(*args, **kwargs)
+
+
+__all__ = [
+    "ActionOutput", "ConfigInvalid", "ContextKind", "ContextStore", "DeadlockDetected",
+    "DeviceError", "FramepipeError", "IncompleteGeneration", "InvalidStageCount", "KindMismatch",
+    "NotYetPublished", "Observation", "OffsetOutOfRange", "PipelineConfig", "Policy",
+    "PublicContext", "RequestRecord", "RolloutMetrics", "RunResult", "ShapeMismatch",
+    "StagePlan", "StaleWrite", "TooManyStages", "make_conditioning_policy",
+    "make_diffusion_policy", "plan_stages", "run_pipelined", "run_sequential",
+    "split_generation", "split_perception", "summarize",
+]

@@ -1,0 +1,212 @@
+"""The public context and its versioned ring, resident in HBM.
+
+Replaces the reference's ContextStore / PublicContext (fp/context.py:23-175)
+on the hot path.  The payload of every slot lives in device memory and is
+written by producer kernels (perception epilogues); what crosses the host is
+only a handle `(slot, version, frame)`.
+
+Device layout (one ring per lock-stepped agent group):
+  payload : [agents, K, slot_elems]   (fp64 for the toy policy, fp32 for DP)
+  meta    : int64 [K, 2] = {frame, version}, the version released last
+  state   : int64 [4]    = {version, last frame, publish count, error flag}
+
+The host keeps a mirror of the metadata (versions, slot frames) because the
+scheduler's decisions -- NotYetPublished, the newest-context fallback,
+DeadlockDetected -- are host decisions in the reference too
+(fp/executor.py:302-316).  Consumer kernels resolve the slot again on the
+device (auras_ring_fetch: acquire-load of the version word) and log the
+version they actually read, so tests can assert that host schedule and
+device consumption agree.
+"""
+
+from __future__ import annotations
+
+import zlib
+from dataclasses import dataclass, field, replace
+from enum import Enum
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .errors import KindMismatch, NotYetPublished, OffsetOutOfRange, StaleWrite
+
+
+class ContextKind(str, Enum):
+    AUTOREGRESSIVE = "autoregressive"
+    CONDITIONING = "conditioning"
+
+
+def _checksum(conditioning, source_observation_id: int, produced_frame: int) -> int:
+    crc = 0
+    if conditioning is not None:
+        crc = zlib.crc32(np.ascontiguousarray(conditioning, dtype=np.float64).tobytes(), crc)
+    crc = zlib.crc32(repr(()).encode(), crc)
+    crc = zlib.crc32(f"{source_observation_id}:{produced_frame}".encode(), crc)
+    return crc
+
+
+@dataclass(frozen=True)
+class PublicContext:
+    """A conditioning-kind public context (H_o of Eq. 2; fp/context.py:39-88).
+
+    `conditioning` is a host copy when one exists (standalone store use); the
+    engine's contexts are device-resident and carry only their ring slot."""
+
+    kind: ContextKind
+    source_observation_id: int
+    produced_frame: int
+    conditioning: Optional[np.ndarray] = None
+    slot: int = -1
+    checksum: int = field(default=-1)
+
+    def __post_init__(self):
+        if self.kind != ContextKind.CONDITIONING:
+            raise KindMismatch("the B200 hot path carries conditioning contexts only")
+        if self.conditioning is not None:
+            object.__setattr__(self, "conditioning",
+                               np.asarray(self.conditioning, dtype=np.float64))
+        object.__setattr__(self, "checksum", _checksum(self.conditioning,
+                                                       self.source_observation_id,
+                                                       self.produced_frame))
+
+    def verify_checksum(self) -> bool:
+        return self.checksum == _checksum(self.conditioning, self.source_observation_id,
+                                          self.produced_frame)
+
+    def with_produced_frame(self, frame: int) -> "PublicContext":
+        return replace(self, produced_frame=frame)
+
+
+class ContextStore:
+    """Ring of K versioned slots in HBM, one writer stream, many reader kernels."""
+
+    def __init__(self, capacity: int = 2, slot_elems: int = 2, agents: int = 1,
+                 dtype=None, device=None):
+        import torch
+        if capacity < 2:
+            raise ValueError("store capacity must be at least 2")
+        _lib.load()
+        self.capacity = capacity
+        self.agents = agents
+        self.slot_elems = slot_elems
+        dtype = torch.float64 if dtype is None else dtype
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        self.payload = torch.zeros(agents, capacity, slot_elems, dtype=dtype, device=dev)
+        self.meta = torch.full((capacity, 2), -1, dtype=torch.int64, device=dev)
+        self.state = torch.tensor([0, -1, 0, 0], dtype=torch.int64, device=dev)
+        # host mirror
+        self._version = 0
+        self._last_frame: Optional[int] = None
+        self._publish_count = 0
+        self._slot_frame = [None] * capacity
+        self._slot_version = [0] * capacity
+        self._slot_obs = [None] * capacity
+
+    # -- properties (fp/context.py:117-127)
+    @property
+    def published_version(self) -> int:
+        return self._version
+
+    @property
+    def publish_count(self) -> int:
+        return self._publish_count
+
+    @property
+    def last_frame(self) -> Optional[int]:
+        return self._last_frame
+
+    @property
+    def slot_bytes(self) -> int:
+        return self.slot_elems * self.payload.element_size()
+
+    # -- engine-level operations (payload written by kernels)
+    def slot_of(self, frame: int) -> int:
+        return frame % self.capacity
+
+    def reserve(self, frame: int, source_observation_id: Optional[int] = None):
+        """Host half of publish: validate, bump the mirror, return (slot, version).
+        The device half (payload kernels + auras_ring_commit) follows on the
+        writer stream."""
+        if self._last_frame is not None and frame < self._last_frame:
+            raise StaleWrite(f"publish for frame {frame} after frame {self._last_frame}")
+        self._version += 1
+        self._publish_count += 1
+        slot = self.slot_of(frame)
+        self._slot_frame[slot] = frame
+        self._slot_version[slot] = self._version
+        self._slot_obs[slot] = frame if source_observation_id is None else source_observation_id
+        self._last_frame = frame
+        return slot, self._version
+
+    def commit(self, frame: int, version: int, stream) -> None:
+        lib = _lib.load()
+        _lib.check(lib.auras_ring_commit(self.meta.data_ptr(), self.state.data_ptr(), self.capacity,
+                                         frame, version, stream.cuda_stream), "ring_commit")
+
+    def resolve(self, frame: int, offset: int = 0):
+        """Host half of fetch_entry: (version, context frame, slot)."""
+        if offset > 0 or -offset >= self.capacity:
+            raise OffsetOutOfRange(f"offset {offset} outside (-{self.capacity}, 0]")
+        target = frame + offset
+        slot = self.slot_of(target)
+        if self._slot_frame[slot] != target:
+            raise NotYetPublished(f"no context published for frame {target}")
+        return self._slot_version[slot], target, slot
+
+    def resolve_latest(self):
+        if self._last_frame is None:
+            raise NotYetPublished("nothing published yet")
+        slot = self.slot_of(self._last_frame)
+        return self._slot_version[slot], self._last_frame, slot
+
+    def device_fetch(self, target: int, out, version_log, log_index: int, stream) -> None:
+        """Device half of fetch: resolve slot/version in-kernel into `out`."""
+        lib = _lib.load()
+        _lib.check(lib.auras_ring_fetch(self.meta.data_ptr(), self.state.data_ptr(), self.capacity,
+                                        target, out.data_ptr(),
+                                        0 if version_log is None else version_log.data_ptr(),
+                                        log_index, stream.cuda_stream), "ring_fetch")
+
+    # -- reference-compatible API (fp/context.py:129-164)
+    def publish(self, ctx: PublicContext, frame: int) -> int:
+        import torch
+        if ctx.kind != ContextKind.CONDITIONING:
+            raise KindMismatch("conditioning contexts only")
+        if ctx.conditioning is None:
+            raise ValueError("publish() of a host context needs its conditioning vector")
+        vec = np.asarray(ctx.conditioning, dtype=np.float64).ravel()
+        if vec.size > self.slot_elems:
+            raise ValueError(f"context of {vec.size} elements exceeds slot of {self.slot_elems}")
+        slot, version = self.reserve(frame, ctx.source_observation_id)
+        stream = torch.cuda.current_stream()
+        src = torch.from_numpy(vec).to(self.payload.dtype).pin_memory()
+        dst = self.payload[0, slot, : vec.size]
+        dst.copy_(src, non_blocking=True)
+        self.commit(frame, version, stream)
+        return version
+
+    def _host_context(self, slot: int, frame: int) -> PublicContext:
+        vals = self.payload[0, slot].double().cpu().numpy()
+        return PublicContext(kind=ContextKind.CONDITIONING,
+                             source_observation_id=self._slot_obs[slot], produced_frame=frame,
+                             conditioning=vals, slot=slot)
+
+    def fetch_entry(self, frame: int, offset: int = 0):
+        version, target, slot = self.resolve(frame, offset)
+        return version, self._host_context(slot, target)
+
+    def fetch(self, frame: int, offset: int = 0) -> PublicContext:
+        return self.fetch_entry(frame, offset)[1]
+
+    def latest_entry(self):
+        version, frame, slot = self.resolve_latest()
+        return frame, version, self._host_context(slot, frame)
+
+    def update_action_tokens(self, frame: int, tokens):
+        raise KindMismatch("action-token updates belong to autoregressive contexts "
+                           "(out of scope for the diffusion hot path)")
+
+    def device_state(self):
+        """(version, last frame, publish count, error flag) as seen by the device."""
+        return tuple(int(v) for v in self.state.cpu().tolist())

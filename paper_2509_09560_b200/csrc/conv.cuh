@@ -1,0 +1,51 @@
+// Internal kernel-argument structs shared by the conv engines and the UNet plan.
+#pragma once
+#include "common.cuh"
+
+namespace auras {
+
+struct ConvGemmArgs {
+  const void *w;      // [M][Kp]
+  const void *in;     // NHWC view
+  float *partial;     // [splits][N][M]
+  int M, N, Kp, Kreal, Cin;
+  int H, W, in_pitch, in_coff;
+  int kh, kw, stride, pad_h, pad_w;
+  int Ho, Wo;
+  int splits, kchunk;
+};
+
+struct EpiArgs {
+  float *partial;             // [splits][N][M]; split 0 receives the reduced sum
+  const float *bias, *gn_gamma, *gn_beta;
+  const void *res;
+  const float *res_f32;
+  void *out;
+  float *out_f32;
+  const float *film_a;        // FiLM rows: film_a[row_a(s) * film_a_stride + off ...]
+  const int *film_a_row;      // per-sample row (NULL: row = s)
+  int64_t film_a_stride;
+  const float *film_b;        // optional second FiLM source, per-sample float offset
+  const int64_t *film_b_off;
+  int M, N, Ho, Wo, splits, groups, act, res_before_act, film_off;
+  int out_pitch, out_coff, res_pitch, res_coff, out_stuff, pool_out;
+};
+
+struct LinArgs {
+  const void *w;
+  const float *bias;
+  const float *x;
+  float *y;
+  int M, K, ldw, mish_in, N, ldx, ldy;
+};
+
+int conv_op_to_args(const auras_conv_op &op, int S, float *partial, ConvGemmArgs &g, EpiArgs &e);
+int run_gemm(const ConvGemmArgs &g, int dtype, cudaStream_t st);
+int run_epilogue(const EpiArgs &e, int S, int dtype, cudaStream_t st);
+int64_t conv_scratch_floats(const auras_conv_op &op, int S);
+
+// tcgen05 / TMA engine (gemm_sm100.cu)
+bool gemm_sm100_supported(const ConvGemmArgs &g);
+int launch_gemm_sm100(const ConvGemmArgs &g, cudaStream_t st);
+
+}  // namespace auras

@@ -1,0 +1,226 @@
+// Public-context ring (ContextStore, fp/context.py:98-175) and the reference's
+// fp64 refinement policy (fp/policy.py:217-246) on the device.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace auras {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_check(cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return AURAS_OK;
+  set_error("%s: %s", what, cudaGetErrorString(e));
+  return AURAS_E_CUDA;
+}
+
+__device__ __forceinline__ int ring_slot(int64_t frame, int capacity) {
+  int64_t r = frame % capacity;
+  return static_cast<int>(r < 0 ? r + capacity : r);
+}
+
+// Version word written last with release semantics: a consumer that
+// acquire-loads the version observes every payload store that preceded it.
+__device__ void commit_slot(int64_t *meta, int64_t *state, int capacity, int64_t frame,
+                            int64_t expected_version) {
+  const int slot = ring_slot(frame, capacity);
+  const int64_t v = state[0] + 1;
+  if (v != expected_version) state[3] = 1;     // host/device version drift
+  if (state[1] >= 0 && frame < state[1]) state[3] = 2;  // StaleWrite seen on device
+  meta[2 * slot + 0] = frame;
+  __threadfence();
+  st_release_gpu(&meta[2 * slot + 1], v);
+  state[0] = v;
+  state[1] = frame;
+  state[2] += 1;
+}
+
+__global__ void ring_commit_kernel(int64_t *meta, int64_t *state, int capacity, int64_t frame,
+                                   int64_t expected_version) {
+  commit_slot(meta, state, capacity, frame, expected_version);
+}
+
+__global__ void ring_fetch_kernel(const int64_t *meta, const int64_t *state, int capacity,
+                                  int64_t target, int64_t *out, int64_t *log, int64_t log_index) {
+  int slot = ring_slot(target, capacity);
+  int64_t v = ld_acquire_gpu(&meta[2 * slot + 1]);
+  int64_t f = meta[2 * slot + 0];
+  if (v <= 0 || f != target) {                  // publisher skipped: newest context
+    const int64_t last = state[1];
+    slot = ring_slot(last, capacity);
+    v = ld_acquire_gpu(&meta[2 * slot + 1]);
+    f = meta[2 * slot + 0];
+  }
+  out[0] = slot;
+  out[1] = v;
+  out[2] = f;
+  if (log) log[log_index] = v;
+}
+
+// ---------------------------------------------------------------- toy policy
+
+__global__ void toy_ingest_kernel(double *latent, int lane, double o0, double o1, double o2,
+                                  double o3, double *x, double x0, double x1) {
+  latent[4 * lane + 0] = o0;
+  latent[4 * lane + 1] = o1;
+  latent[4 * lane + 2] = o2;
+  latent[4 * lane + 3] = o3;
+  x[2 * lane + 0] = x0;
+  x[2 * lane + 1] = x1;
+}
+
+__global__ void toy_publish_kernel(const double *latent, int lane, double *payload,
+                                   int64_t *meta, int64_t *state, int capacity, int64_t frame,
+                                   int64_t version) {
+  const int slot = ring_slot(frame, capacity);
+  // invalidate, write the payload, then release the version (seqlock order)
+  st_release_gpu(&meta[2 * slot + 1], -1);
+  // fp/policy.py:286  conditioning = latent[:2] - latent[2:4]
+  payload[2 * slot + 0] = __dsub_rn(latent[4 * lane + 0], latent[4 * lane + 2]);
+  payload[2 * slot + 1] = __dsub_rn(latent[4 * lane + 1], latent[4 * lane + 3]);
+  commit_slot(meta, state, capacity, frame, version);
+}
+
+struct ToyBatch {
+  int lanes[64];
+  int iters[64];
+};
+
+__global__ void toy_generate_kernel(double *x, ToyBatch batch, int n, double eta,
+                                    const double *payload, const int64_t *fetched) {
+  const int i = threadIdx.x;
+  if (i >= n) return;
+  const int slot = static_cast<int>(fetched[0]);   // slot resolved in-kernel by ring_fetch
+  const double h0 = payload[2 * slot + 0], h1 = payload[2 * slot + 1];
+  const int lane = batch.lanes[i];
+  double a = x[2 * lane + 0], b = x[2 * lane + 1];
+  for (int k = 0; k < batch.iters[i]; ++k) {
+    // fp/policy.py:224  new = x + eta * (target - x), evaluated as numpy does
+    a = __dadd_rn(a, __dmul_rn(eta, __dsub_rn(h0, a)));
+    b = __dadd_rn(b, __dmul_rn(eta, __dsub_rn(h1, b)));
+  }
+  x[2 * lane + 0] = a;
+  x[2 * lane + 1] = b;
+}
+
+__global__ void toy_finish_kernel(const double *x, int lane, double max_action, double *out) {
+  double a = x[2 * lane + 0], b = x[2 * lane + 1];
+  // np.linalg.norm of a 2-vector on this stack is sqrt(fma(b, b, a*a)) (OpenBLAS ddot)
+  const double norm = __dsqrt_rn(__fma_rn(b, b, __dmul_rn(a, a)));
+  if (norm > max_action) {
+    const double s = __ddiv_rn(max_action, norm);
+    a = __dmul_rn(a, s);
+    b = __dmul_rn(b, s);
+  }
+  out[0] = a;
+  out[1] = b;
+}
+
+__global__ void copy_bytes_kernel(uint4 *dst, const uint4 *src, int64_t n16, uint8_t *dtail,
+                                  const uint8_t *stail, int ntail) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+  if (blockIdx.x == 0 && threadIdx.x < ntail) dtail[threadIdx.x] = stail[threadIdx.x];
+}
+
+}  // namespace auras
+
+using namespace auras;
+
+extern "C" {
+
+const char *auras_last_error(void) { return g_err; }
+
+int auras_abi_version(void) { return 3; }
+
+int auras_device_ok(int device) {
+  cudaDeviceProp p;
+  if (cudaGetDeviceProperties(&p, device) != cudaSuccess) return 0;
+  return p.major == 10 && p.minor == 0;
+}
+
+int auras_ring_commit(int64_t *meta, int64_t *state, int capacity, int64_t frame,
+                      int64_t expected_version, void *stream) {
+  if (!meta || !state || capacity < 2) { set_error("ring_commit: bad args"); return AURAS_E_ARG; }
+  ring_commit_kernel<<<1, 1, 0, as_stream(stream)>>>(meta, state, capacity, frame, expected_version);
+  AURAS_LAUNCHED("ring_commit_kernel");
+  return AURAS_OK;
+}
+
+int auras_ring_fetch(const int64_t *meta, const int64_t *state, int capacity, int64_t target,
+                     int64_t *out, int64_t *version_log, int64_t log_index, void *stream) {
+  if (!meta || !state || !out || capacity < 2) { set_error("ring_fetch: bad args"); return AURAS_E_ARG; }
+  ring_fetch_kernel<<<1, 1, 0, as_stream(stream)>>>(meta, state, capacity, target, out, version_log,
+                                                    log_index);
+  AURAS_LAUNCHED("ring_fetch_kernel");
+  return AURAS_OK;
+}
+
+int auras_ring_write(void *payload, int64_t slot_bytes, int slot, const void *src, int64_t bytes,
+                     void *stream) {
+  if (!payload || !src || bytes > slot_bytes || slot < 0) { set_error("ring_write: bad args"); return AURAS_E_ARG; }
+  uint8_t *dst = static_cast<uint8_t *>(payload) + slot_bytes * slot;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+  if (!aligned) {
+    AURAS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, as_stream(stream)));
+    return AURAS_OK;
+  }
+  const int64_t n16 = bytes / 16;
+  const int ntail = static_cast<int>(bytes - n16 * 16);
+  int blocks = static_cast<int>((n16 + 255) / 256);
+  blocks = blocks < 1 ? 1 : (blocks > 592 ? 592 : blocks);
+  copy_bytes_kernel<<<blocks, 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<uint4 *>(dst), reinterpret_cast<const uint4 *>(src), n16, dst + n16 * 16,
+      static_cast<const uint8_t *>(src) + n16 * 16, ntail);
+  AURAS_LAUNCHED("copy_bytes_kernel");
+  return AURAS_OK;
+}
+
+int auras_toy_ingest(double *latent, int lane, const double obs[4], double *x_state,
+                     const double x0[2], void *stream) {
+  if (!latent || !x_state || !obs || !x0 || lane < 0) { set_error("toy_ingest: bad args"); return AURAS_E_ARG; }
+  toy_ingest_kernel<<<1, 1, 0, as_stream(stream)>>>(latent, lane, obs[0], obs[1], obs[2], obs[3],
+                                                    x_state, x0[0], x0[1]);
+  AURAS_LAUNCHED("toy_ingest_kernel");
+  return AURAS_OK;
+}
+
+int auras_toy_publish(const double *latent, int lane, double *ring_payload, int64_t *meta,
+                      int64_t *state, int capacity, int64_t frame, int64_t version, void *stream) {
+  if (!latent || !ring_payload || !meta || !state || capacity < 2) { set_error("toy_publish: bad args"); return AURAS_E_ARG; }
+  toy_publish_kernel<<<1, 1, 0, as_stream(stream)>>>(latent, lane, ring_payload, meta, state,
+                                                     capacity, frame, version);
+  AURAS_LAUNCHED("toy_publish_kernel");
+  return AURAS_OK;
+}
+
+int auras_toy_generate(double *x_state, const int *lanes, const int *iters, int n, double eta,
+                       const double *ring_payload, const int64_t *fetched, void *stream) {
+  if (n < 0 || n > 64 || !x_state || !ring_payload || !fetched) { set_error("toy_generate: bad args (n=%d)", n); return AURAS_E_ARG; }
+  if (n == 0) return AURAS_OK;
+  ToyBatch b;
+  memset(&b, 0, sizeof(b));
+  for (int i = 0; i < n; ++i) { b.lanes[i] = lanes[i]; b.iters[i] = iters[i]; }
+  toy_generate_kernel<<<1, 64, 0, as_stream(stream)>>>(x_state, b, n, eta, ring_payload, fetched);
+  AURAS_LAUNCHED("toy_generate_kernel");
+  return AURAS_OK;
+}
+
+int auras_toy_finish(const double *x_state, int lane, double max_action, double *out, void *stream) {
+  if (!x_state || !out) { set_error("toy_finish: bad args"); return AURAS_E_ARG; }
+  toy_finish_kernel<<<1, 1, 0, as_stream(stream)>>>(x_state, lane, max_action, out);
+  AURAS_LAUNCHED("toy_finish_kernel");
+  return AURAS_OK;
+}
+
+}  // extern "C"

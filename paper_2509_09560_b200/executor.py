@@ -1,0 +1,596 @@
+"""Frame-clocked pipeline executor on two CUDA streams.
+
+Drop-in for the reference's `run_pipelined` / `run_sequential`
+(fp/executor.py:200-461): same signatures, same `PipelineConfig`, same
+`RunResult` / `RequestRecord`, same trace schema 1.  What changes is where
+the work happens:
+
+* perception stages, the finalize and the ring publish run on a perception
+  stream P; every generation stage active in a frame is folded into ONE
+  batched denoise launch chain on a generation stream G (the reference loops
+  over stages and iterations in Python, fp/executor.py:325-331);
+* the handoff is event based: G waits on the event recorded after the
+  publish of the context it reads (offset 0 serialises publish -> fetch inside
+  the frame as the SPEC demands; offset -1 lets P(t) overlap G(t)); P waits on
+  the last G read of a slot before overwriting it (the K = 2 ring-reuse hazard)
+  and on the finish of a lane's previous request before re-using the lane;
+* the slot/version a stage consumes is decided by the same host rules as the
+  reference (so the schedule is bit-identical) and re-resolved on the device,
+  which logs the version it actually read.
+
+Two clocks are available.  `clock="virtual"` (the default, as in the
+reference) computes frame times from the policy's cost units exactly as
+fp/executor.py:350-374 does, so traces are comparable field for field with the
+reference's.  `clock="device"` stamps frame starts, frame ends, emissions and
+JCTs with CUDA events (seconds); it requires `frame_interval=None`
+(as-fast-as-possible frames, per-dependency waits).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .context import ContextKind
+from .errors import ConfigInvalid, DeadlockDetected, IncompleteGeneration, NotYetPublished
+from .partition import StagePlan, plan_stages
+from .policy import ActionOutput, Observation
+
+TRACE_SCHEMA = 1
+
+
+@dataclass(frozen=True)
+class PipelineConfig:
+    """Pipelined search point (fp/executor.py:48-103): degrees, offset, skew,
+    frame policy.  Identical fields and validation rules."""
+
+    pp_perception: int = 1
+    pp_generation: int = 1
+    fetch_offset: Optional[int] = None
+    alpha: float = 0.0
+    frame_interval: Optional[float] = None
+    merge_autoregressive: Optional[bool] = None
+    store_capacity: int = 2
+    read_policy: str = "snapshot"
+    overrun_policy: str = "stretch"
+
+    def resolve_offset(self, kind) -> int:
+        if self.fetch_offset is not None:
+            return self.fetch_offset
+        return -1 if kind == ContextKind.AUTOREGRESSIVE else 0
+
+    def resolve_merge(self, kind) -> bool:
+        if self.merge_autoregressive is not None:
+            return bool(self.merge_autoregressive) and kind == ContextKind.AUTOREGRESSIVE
+        return kind == ContextKind.AUTOREGRESSIVE
+
+    def validate(self, policy) -> None:
+        if self.pp_perception < 1 or self.pp_generation < 1:
+            raise ConfigInvalid("pipeline degrees must be positive")
+        if self.pp_perception + self.pp_generation < 2:
+            raise ConfigInvalid("pipelined mode needs at least two stages")
+        off = self.resolve_offset(policy.kind)
+        if off > 0:
+            raise ConfigInvalid("fetch_offset must be <= 0")
+        if -off >= self.store_capacity:
+            raise ConfigInvalid(f"|fetch_offset| = {-off} must be below store capacity "
+                                f"{self.store_capacity}")
+        if self.pp_perception > len(policy.perception.layers):
+            raise ConfigInvalid("more perception stages than layers")
+        if self.read_policy not in ("snapshot", "live"):
+            raise ConfigInvalid(f"unknown read policy {self.read_policy!r}")
+        if self.overrun_policy not in ("stretch", "drop"):
+            raise ConfigInvalid(f"unknown overrun policy {self.overrun_policy!r}")
+        if self.frame_interval is not None and self.frame_interval <= 0:
+            raise ConfigInvalid("frame interval must be positive")
+
+    def to_dict(self) -> dict:
+        return {"pp_perception": self.pp_perception, "pp_generation": self.pp_generation,
+                "fetch_offset": self.fetch_offset, "alpha": self.alpha,
+                "frame_interval": self.frame_interval,
+                "merge_autoregressive": self.merge_autoregressive,
+                "store_capacity": self.store_capacity, "read_policy": self.read_policy,
+                "overrun_policy": self.overrun_policy}
+
+
+@dataclass
+class RequestRecord:
+    observation_id: int
+    birth_frame: int
+    birth_time: float
+    completion_frame: int = -1
+    completion_time: float = -1.0
+    jct: float = -1.0
+    context_versions: list = field(default_factory=list)
+
+
+@dataclass
+class RunResult:
+    actions: list
+    trace: list
+    requests: list
+    agent_actions: list = field(default_factory=list)   # per agent (agent 0 == actions)
+    device_versions: Optional[np.ndarray] = None        # version read in-kernel, per frame
+    frame_times: Optional[dict] = None                  # device clock: raw event seconds
+
+    @property
+    def header(self) -> dict:
+        return self.trace[0]
+
+
+# ---------------------------------------------------------------- helpers
+
+def _header(mode, interval, duration, config, envs, clock):
+    env0 = envs[0] if envs else None
+    return {"type": "header", "schema": TRACE_SCHEMA, "mode": mode,
+            "engine": "virtual" if clock == "virtual" else "b200",
+            "device": "b200", "clock": clock, "frame_interval": interval,
+            "duration": duration, "config": config,
+            "success_threshold": getattr(env0, "success_threshold", None)}
+
+
+def _frame(t, now):
+    return {"type": "frame", "frame": t, "start": now, "perception": [], "generation": [],
+            "publishes": [], "emissions": [], "prefill_calls": 0, "decode_calls": 0,
+            "generation_cost": 0.0, "dropped_observations": 0}
+
+
+class _Port:
+    """Per-agent environment boundary (fp/executor.py:146-184): land the newest
+    due action, then observe.  env None -> synthetic observation source."""
+
+    def __init__(self, env, policy, agent, source):
+        self.env, self.policy, self.agent, self.source = env, policy, agent, source
+        self.pending = []           # (land_frame, order, emission)
+        self.last_superseded = 0
+
+    def schedule(self, land_frame, order, emission):
+        self.pending.append((land_frame, order, emission))
+
+    def boundary(self, frame, materialize):
+        due = [p for p in self.pending if p[0] == frame]
+        self.last_superseded = 0
+        if due:
+            self.pending = [p for p in self.pending if p[0] != frame]
+            newest = max(due, key=lambda p: p[1])
+            self.last_superseded = len(due) - 1
+            if self.env is not None:
+                action = materialize(newest[2], self.agent)
+                self.env.apply_action(self.policy.generation.decode_action(action))
+        if self.env is not None:
+            return self.env.observe(frame)
+        if self.source is not None:
+            return self.source(self.agent, frame)
+        synth = getattr(self.policy, "synthetic_observation", None)
+        if synth is not None:
+            return synth(self.agent, frame)
+        return Observation(frame=frame, vector=np.zeros(4))     # fp/executor.py:142-143
+
+    def seal(self):
+        if self.env is None:
+            return None
+        self.env.advance_frame()
+        return self.env.last_error
+
+
+class _Device:
+    """Streams, events and the policy session for one run."""
+
+    def __init__(self, policy, *, capacity, lanes, agents, max_outputs, max_frames, clock):
+        import torch
+        self.torch = torch
+        self.clock = clock
+        self.P = torch.cuda.Stream()
+        self.G = torch.cuda.Stream()
+        self.session = policy.open_session(capacity=capacity, lanes=lanes, agents=agents,
+                                           max_outputs=max_outputs, max_frames=max_frames,
+                                           p_stream=self.P, g_stream=self.G)
+        self.store = self.session.store
+        self.pub_event = {}          # context frame -> event after its publish (P)
+        self.ingest_event = {}       # request -> event after ingest (P)
+        self.slot_read = {}          # slot -> last G event that read it
+        self.lane_free = {}          # lane -> G event after the previous occupant's finish
+        self.t_start, self.t_end = {}, {}
+        self.origin = None
+        self.throttle = []
+
+    def event(self, stream, timing=False):
+        ev = self.torch.cuda.Event(enable_timing=timing)
+        ev.record(stream)
+        return ev
+
+    def begin_frame(self, t, window):
+        # bound how far the host runs ahead of the device (event/pinned-buffer lifetimes)
+        if len(self.throttle) >= window:
+            self.throttle.pop(0).synchronize()
+        if self.clock == "device":
+            ev = self.event(self.P, timing=True)
+            self.t_start[t] = ev
+            if self.origin is None:
+                self.origin = ev
+
+    def end_frame(self, t):
+        ev = self.event(self.G, timing=self.clock == "device")
+        if self.clock == "device":
+            self.t_end[t] = ev
+        self.throttle.append(ev)
+
+    def ingest(self, t, lane, observations):
+        ev = self.lane_free.pop(lane, None)
+        if ev is not None:
+            self.P.wait_event(ev)
+        self.session.ingest(t, lane, observations)
+        self.ingest_event[t] = self.event(self.P)
+
+    def publish(self, lane, frame, slot, version):
+        ev = self.slot_read.get(slot)
+        if ev is not None:
+            self.P.wait_event(ev)
+        self.session.publish(lane, frame, slot, version)
+        self.pub_event[frame] = self.event(self.P)
+        for f in [f for f in self.pub_event if f < frame - 4 * self.store.capacity]:
+            del self.pub_event[f]
+
+    def generate(self, ctx_frame, slot, log_index, batch, first_use):
+        self.G.wait_event(self.pub_event[ctx_frame])
+        for b in first_use:
+            ev = self.ingest_event.pop(b, None)
+            if ev is not None:
+                self.G.wait_event(ev)
+        self.session.fetch(ctx_frame, log_index)
+        self.session.generate(batch)
+        self.slot_read[slot] = self.event(self.G)
+
+    def finish(self, lane, out_index):
+        self.session.finish(lane, out_index)
+        self.lane_free[lane] = self.event(self.G)
+
+    def seconds(self, ev):
+        return self.origin.elapsed_time(ev) / 1e3
+
+    def synchronize(self):
+        self.P.synchronize()
+        self.G.synchronize()
+
+
+class _Emissions:
+    """Emitted actions: device rows materialised lazily (one D2H at the end,
+    or one per action when a closed loop needs it).  Session rows are
+    [agents, ...] arrays; `session.action_values(row)` turns one agent's row
+    into the ActionOutput values tuple."""
+
+    def __init__(self, device, policy, agents):
+        self.device, self.policy, self.agents = device, policy, agents
+        self.items = []             # (out_index, emitted_frame, staleness_profile)
+        self.cache = {}
+
+    def add(self, out_index, emitted_frame, profile):
+        self.items.append((out_index, emitted_frame, profile))
+        return len(self.items) - 1
+
+    def _make(self, k, rows):
+        _, emitted, prof = self.items[k]
+        sess = self.device.session
+        return [ActionOutput(kind=self.policy.kind, values=sess.action_values(rows[a]),
+                             emitted_frame=emitted, staleness_profile=prof)
+                for a in range(self.agents)]
+
+    def materialize(self, k, agent):
+        if k not in self.cache:
+            self.cache[k] = self._make(k, self.device.session.read_action(self.items[k][0]))
+        return self.cache[k][agent]
+
+    def all(self):
+        n = len(self.items)
+        per_agent = [[] for _ in range(self.agents)]
+        if n == 0:
+            return per_agent
+        rows = self.device.session.read_actions(n)
+        for k in range(n):
+            if k not in self.cache:
+                self.cache[k] = self._make(k, rows[k])
+            for a in range(self.agents):
+                per_agent[a].append(self.cache[k][a])
+        return per_agent
+
+
+def _agents_and_envs(policy, env, agents):
+    if isinstance(env, (list, tuple)):
+        envs = list(env)
+    else:
+        n = agents if agents is not None else getattr(policy, "agents", 1)
+        envs = [env] * n if env is None else [env]
+    if agents is not None and len(envs) != agents:
+        raise ConfigInvalid(f"{len(envs)} environments for {agents} agents")
+    return envs
+
+
+def _require_plugin(policy):
+    if not hasattr(policy, "open_session"):
+        raise ConfigInvalid("the B200 engine needs a B200 policy plugin (make_conditioning_policy "
+                            "or make_diffusion_policy from paper_2509_09560_b200)")
+
+
+# ---------------------------------------------------------------- pipelined mode
+
+def run_pipelined(cfg: PipelineConfig, policy, env, duration: int, *, clock: str = "virtual",
+                  agents: Optional[int] = None, frame_source=None) -> RunResult:
+    """fp/executor.py:200-399 on the B200.  `env` may be one environment, a list
+    (one per agent, batched into the same kernels), or None (synthetic
+    observations from `frame_source(agent, frame)` when given)."""
+    _require_plugin(policy)
+    cfg.validate(policy)
+    if clock not in ("virtual", "device"):
+        raise ConfigInvalid(f"unknown clock {clock!r}")
+    if clock == "device" and cfg.frame_interval is not None:
+        raise ConfigInvalid("clock='device' runs frames as fast as possible (frame_interval=None)")
+    _lib.load()
+    offset = cfg.resolve_offset(policy.kind)
+    merge = cfg.resolve_merge(policy.kind)
+    plan: StagePlan = plan_stages(policy.perception.layer_costs, cfg.pp_perception,
+                                  policy.generation.n_iterations, cfg.pp_generation, cfg.alpha)
+    pp_p, pp_g = cfg.pp_perception, cfg.pp_generation
+    shift = pp_p - 1 - offset
+    span = shift + pp_g
+    starts = plan.stage_starts()
+    gen = policy.generation
+    envs = _agents_and_envs(policy, env, agents)
+    A = len(envs)
+    lanes = span + 2
+    p_cost = [sum(policy.perception.layer_costs[a:b]) for a, b in plan.perception_stages]
+
+    dev = _Device(policy, capacity=cfg.store_capacity, lanes=lanes, agents=A,
+                  max_outputs=duration, max_frames=duration, clock=clock)
+    store = dev.store
+    ports = [_Port(e, policy, a, frame_source) for a, e in enumerate(envs)]
+    emis = _Emissions(dev, policy, A)
+    trace = [_header("pipe", cfg.frame_interval, duration,
+                     {"pipeline": cfg.to_dict(), "plan": plan.to_dict(), "fetch_offset": offset,
+                      "merged": merge}, envs, clock)]
+    live = {}
+    records = []
+    emitted_rows = []                 # (frame record, emission dict, request record)
+    now, skip = 0.0, 0
+    window = max(4, lanes)
+    for t in range(duration):
+        dev.begin_frame(t, window)
+        rec = _frame(t, now)
+        obs = [port.boundary(t, emis.materialize) for port in ports]
+        rec["superseded_actions"] = ports[0].last_superseded
+        if skip > 0:
+            skip -= 1
+            rec["dropped_observations"] += 1
+        else:
+            lane = t % lanes
+            r = RequestRecord(observation_id=obs[0].id, birth_frame=t, birth_time=now)
+            dev.ingest(t, lane, obs)
+            live[t] = {"rec": r, "lane": lane, "ages": [], "steps": 0, "used": False,
+                       "obs_id": obs[0].id}
+            records.append(r)
+
+        early = None
+        if offset <= -1 and cfg.read_policy == "snapshot":
+            try:
+                early = store.resolve(t, offset)
+            except NotYetPublished:
+                early = None
+
+        side, pub_cost, published = [], 0.0, False
+        for s in range(1, pp_p + 1):
+            b = t - s + 1
+            item = live.get(b)
+            if item is None:
+                continue
+            lo, hi = plan.perception_stages[s - 1]
+            dev.session.perceive(item["lane"], lo, hi)
+            entry = {"request": b, "stage": s, "cost": p_cost[s - 1], "published_version": None}
+            if s == pp_p:
+                slot, version = store.reserve(t, item["obs_id"])
+                dev.publish(item["lane"], t, slot, version)
+                entry["published_version"] = version
+                rec["publishes"].append(version)
+                pub_cost, published = p_cost[s - 1], True
+            else:
+                side.append(p_cost[s - 1])
+            rec["perception"].append(entry)
+
+        active = []
+        for j in range(1, pp_g + 1):
+            b = t - shift - (j - 1)
+            if b in live:
+                active.append((j, b, live[b]))
+        gen_costs = []
+        if active:
+            if early is not None:
+                version, ctx_frame, slot = early
+            else:
+                try:
+                    version, ctx_frame, slot = store.resolve(t, offset)
+                except NotYetPublished:
+                    if t + offset < pp_p - 1:
+                        raise DeadlockDetected(
+                            f"frame {t}: context for frame {t + offset} can never exist")
+                    version, ctx_frame, slot = store.resolve_latest()
+            batch, first = [], []
+            for j, b, item in active:
+                iters = plan.generation_stages[j - 1]
+                batch.append((item["lane"], starts[j - 1], iters))
+                if not item["used"]:
+                    first.append(b)
+                    item["used"] = True
+                age = float(b + span - 1 - ctx_frame)
+                item["ages"].extend([age] * iters)
+                item["steps"] += iters
+                item["rec"].context_versions.append(version)
+                c = iters * gen.step_cost
+                gen_costs.append(c)
+                rec["generation_cost"] += c
+                rec["generation"].append({"request": b, "stage": j, "iterations": iters,
+                                          "context_version": version, "context_frame": ctx_frame,
+                                          "context_age_at_emission": age})
+            dev.generate(ctx_frame, slot, t, batch, first)
+
+        # frame duration in cost units (fp/executor.py:350-374)
+        if offset == 0 and gen_costs and published:
+            busiest = max(side + [pub_cost + max(gen_costs)])
+        else:
+            pool = side + gen_costs + ([pub_cost] if published else [])
+            busiest = max(pool) if pool else 0.0
+        interval = cfg.frame_interval
+        if interval is None:
+            dur = busiest
+        elif busiest <= interval:
+            dur = interval
+        elif cfg.overrun_policy == "stretch":
+            dur = busiest
+            rec["overrun"] = True
+        else:
+            q = math.ceil(busiest / interval)
+            dur = q * interval
+            skip += q - 1
+            rec["overrun"] = True
+        now += dur
+        rec["end"] = now
+
+        b_done = t - span + 1
+        item = live.pop(b_done, None)
+        if item is not None:
+            if item["steps"] < gen.n_iterations:
+                raise IncompleteGeneration(f"{item['steps']}/{gen.n_iterations} iterations applied")
+            out_index = len(emis.items)
+            dev.finish(item["lane"], out_index)
+            k = emis.add(out_index, t, tuple(item["ages"]))
+            r = item["rec"]
+            r.completion_frame = t + 1
+            r.completion_time = now
+            r.jct = now - r.birth_time
+            for port in ports:
+                port.schedule(t + 1, k, k)
+            ages = item["ages"]
+            em = {"request": b_done, "time": now, "emission_frame": t, "land_frame": t + 1,
+                  "jct": r.jct, "action": None, "staleness_min": min(ages),
+                  "staleness_mean": float(np.mean(ages)), "staleness_max": max(ages),
+                  "staleness_final": ages[-1]}
+            rec["emissions"].append(em)
+            emitted_rows.append((rec, em, r, k))
+        rec["env_error"] = ports[0].seal()
+        for port in ports[1:]:
+            port.seal()
+        dev.end_frame(t)
+        trace.append(rec)
+
+    dev.synchronize()
+    per_agent = emis.all()
+    for rec_, em, r, k in emitted_rows:
+        em["action"] = list(per_agent[0][k].values)
+    if clock == "device":
+        _apply_device_clock(dev, trace, records, emitted_rows)
+    versions = dev.session.read_version_log(duration)
+    dev.session.close()
+    return RunResult(actions=per_agent[0], trace=trace, requests=records, agent_actions=per_agent,
+                     device_versions=versions,
+                     frame_times=_frame_times(dev) if clock == "device" else None)
+
+
+def _frame_times(dev):
+    return {"start": {t: dev.seconds(e) for t, e in dev.t_start.items()},
+            "end": {t: dev.seconds(e) for t, e in dev.t_end.items()}}
+
+
+def _apply_device_clock(dev, trace, records, emitted_rows):
+    start = {t: dev.seconds(e) for t, e in dev.t_start.items()}
+    end = {t: dev.seconds(e) for t, e in dev.t_end.items()}
+    for rec in trace[1:]:
+        rec["start"], rec["end"] = start[rec["frame"]], end[rec["frame"]]
+    for r in records:
+        r.birth_time = start[r.birth_frame]
+    for rec, em, r, k in emitted_rows:
+        done = end[rec["frame"]]
+        r.completion_time = done
+        r.jct = done - r.birth_time
+        em["time"], em["jct"] = done, r.jct
+
+
+# ---------------------------------------------------------------- sequential mode
+
+def run_sequential(policy, env, duration: int, frame_interval: Optional[float] = None, *,
+                   clock: str = "virtual", agents: Optional[int] = None,
+                   frame_source=None) -> RunResult:
+    """fp/executor.py:406-461 on the B200: one request at a time (depth 1);
+    observations arriving while a request is in flight are dropped."""
+    _require_plugin(policy)
+    if clock not in ("virtual", "device"):
+        raise ConfigInvalid(f"unknown clock {clock!r}")
+    _lib.load()
+    gen = policy.generation
+    cost = policy.sequential_cost
+    interval = frame_interval if frame_interval is not None else cost
+    per_request = max(1, math.ceil(cost / interval - 1e-12))
+    envs = _agents_and_envs(policy, env, agents)
+    A = len(envs)
+    lanes = 2
+    dev = _Device(policy, capacity=2, lanes=lanes, agents=A, max_outputs=duration,
+                  max_frames=duration, clock=clock)
+    store = dev.store
+    ports = [_Port(e, policy, a, frame_source) for a, e in enumerate(envs)]
+    emis = _Emissions(dev, policy, A)
+    trace = [_header("seq", interval, duration, {"request_cost": cost}, envs, clock)]
+    records, emitted_rows = [], []
+    free_at = 0
+    n_layers = len(policy.perception.layers)
+    for t in range(duration):
+        dev.begin_frame(t, 4)
+        now = t * interval
+        rec = _frame(t, now)
+        rec["end"] = now + interval
+        obs = [port.boundary(t, emis.materialize) for port in ports]
+        rec["superseded_actions"] = ports[0].last_superseded
+        if t >= free_at:
+            lane = t % lanes
+            r = RequestRecord(observation_id=obs[0].id, birth_frame=t, birth_time=now)
+            dev.ingest(t, lane, obs)
+            dev.session.perceive(lane, 0, n_layers)
+            slot, version = store.reserve(t, obs[0].id)
+            dev.publish(lane, t, slot, version)
+            dev.generate(t, slot, t, [(lane, 0, gen.n_iterations)], [t])
+            emit = t + per_request - 1
+            age = float(emit - t)
+            done = now + cost
+            land = t + per_request
+            r.completion_frame, r.completion_time, r.jct = land, done, cost
+            r.context_versions.append(1)        # the reference reports version 1 (fp/executor.py:442)
+            records.append(r)
+            out_index = len(emis.items)
+            dev.finish(lane, out_index)
+            k = emis.add(out_index, emit, (age,) * gen.n_iterations)
+            for port in ports:
+                port.schedule(land, k, k)
+            free_at = land
+            rec["generation_cost"] = gen.total_cost
+            em = {"request": t, "time": done, "emission_frame": emit, "land_frame": land,
+                  "jct": cost, "action": None, "staleness_min": age, "staleness_mean": age,
+                  "staleness_max": age, "staleness_final": age}
+            rec["emissions"].append(em)
+            emitted_rows.append((rec, em, r, k))
+        else:
+            rec["dropped_observations"] = 1
+        rec["env_error"] = ports[0].seal()
+        for port in ports[1:]:
+            port.seal()
+        dev.end_frame(t)
+        trace.append(rec)
+    dev.synchronize()
+    per_agent = emis.all()
+    for rec_, em, r, k in emitted_rows:
+        em["action"] = list(per_agent[0][k].values)
+    if clock == "device":
+        _apply_device_clock(dev, trace, records, emitted_rows)
+    versions = dev.session.read_version_log(duration)
+    dev.session.close()
+    return RunResult(actions=per_agent[0], trace=trace, requests=records, agent_actions=per_agent,
+                     device_versions=versions,
+                     frame_times=_frame_times(dev) if clock == "device" else None)

@@ -1,0 +1,226 @@
+"""Policy plugins for the B200 engine.
+
+A policy is the reference's duck type (fp/policy.py:259-272: `kind`,
+`perception.layers/.layer_costs`, `generation.n_iterations/.step_cost/...`,
+`sequential_cost`) plus one B200 hook, `open_session(...)`, returning a
+device session whose methods enqueue kernels on the engine's perception (P)
+and generation (G) streams:
+
+  ingest(t, lane, observations)            P  request birth: upload the frame(s),
+                                              initialise the request lane's state
+  perceive(lane, lo, hi)                   P  perception layers [lo, hi) of a lane
+  publish(lane, frame, slot, version)      P  finalize + write ring slot + commit
+  fetch(target_frame, log_index)           G  in-kernel slot resolution (+ version log)
+  generate(batch)                          G  batch = [(lane, start_step, iters)]
+  finish(lane, out_index)                  G  action into the device output buffer
+  read_actions(n) -> np.ndarray               D2H of the first n emitted actions
+
+The engine owns the schedule; the session owns the arithmetic.  There is no
+CPU implementation of any session method.
+
+This module holds the reference's own refinement policy on the device
+(`make_conditioning_policy`, fp/policy.py:279-297): fp64 kernels that are
+bit-identical to numpy, used to prove the ring / stream / batching plumbing
+against the reference's golden traces.  The Diffusion Policy CNN plugin is
+in `diffusion.py`.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .context import ContextKind, ContextStore
+from .errors import IncompleteGeneration, ShapeMismatch
+
+
+@dataclass(frozen=True)
+class Observation:
+    """One frame's observation (fp/policy.py:35-42).  `image` carries the
+    uint8 CHW camera frame for image policies; `vector` the low-dim state."""
+
+    frame: int
+    vector: np.ndarray
+    image: Optional[np.ndarray] = None
+
+    @property
+    def id(self) -> int:
+        return self.frame
+
+
+@dataclass(frozen=True)
+class ActionOutput:
+    kind: ContextKind
+    values: tuple
+    emitted_frame: int = -1
+    staleness_profile: tuple = ()
+
+    def as_vector(self) -> np.ndarray:
+        return np.asarray(self.values, dtype=np.float64)
+
+
+@dataclass(frozen=True)
+class PerceptionSpec:
+    """Host-side description of the perception layers (costs drive the
+    partitioner and the virtual clock; fp/policy.py:55-74)."""
+
+    layer_costs: tuple
+    obs_width: int = 4
+
+    @property
+    def layers(self) -> tuple:
+        return self.layer_costs
+
+    @property
+    def total_cost(self) -> float:
+        return float(sum(self.layer_costs))
+
+
+@dataclass(frozen=True)
+class Policy:
+    perception: object
+    generation: object
+
+    @property
+    def kind(self) -> ContextKind:
+        return self.generation.kind
+
+    @property
+    def sequential_cost(self) -> float:
+        return self.perception.total_cost + self.generation.total_cost
+
+    def open_session(self, **kw):
+        return self.generation.open_session(self, **kw)
+
+
+# ---------------------------------------------------------------- toy policy
+
+@dataclass(frozen=True)
+class RefinementGeneration:
+    """x <- x + eta (H - x) on the device in fp64 (fp/policy.py:167-256)."""
+
+    n_iterations: int
+    step_cost: float
+    eta: float = 0.08
+    max_action: float = 0.8
+    noise_init: bool = False
+    init_sigma: float = 1.0
+    state_dim: int = 2
+    kind: ContextKind = ContextKind.CONDITIONING
+
+    def __post_init__(self):
+        if self.n_iterations < 1:
+            raise ValueError("n_iterations must be positive")
+        if self.step_cost <= 0:
+            raise ValueError("step_cost must be strictly positive")
+        if not (0.0 < self.eta < 1.0):
+            raise ValueError("eta must lie in (0, 1)")
+
+    @property
+    def total_cost(self) -> float:
+        return self.n_iterations * self.step_cost
+
+    def initial_noise(self, seed: Optional[int]) -> np.ndarray:
+        """Host-drawn initial state (fp/policy.py:203-211): the random draw is
+        numpy's, by design, so device runs replay the reference's noise."""
+        if self.noise_init:
+            rng = np.random.default_rng(0 if seed is None else seed)
+            return rng.normal(0.0, self.init_sigma, self.state_dim)
+        return np.zeros(self.state_dim)
+
+    def decode_action(self, action: ActionOutput) -> np.ndarray:
+        return action.as_vector()
+
+    def open_session(self, policy, **kw):
+        return RefinementSession(policy, **kw)
+
+
+class RefinementSession:
+    """Device state of the toy policy: fp64 lanes, an fp64 ring, fp64 outputs."""
+
+    def __init__(self, policy, *, capacity, lanes, agents, max_outputs, max_frames,
+                 p_stream, g_stream):
+        import torch
+        if agents != 1:
+            raise ValueError("the refinement toy policy runs one agent per session")
+        self.lib = _lib.load()
+        self.gen = policy.generation
+        self.p, self.g = p_stream, g_stream
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.store = ContextStore(capacity, slot_elems=2, agents=1, dtype=torch.float64, device=dev)
+        self.latent = torch.zeros(lanes, 4, dtype=torch.float64, device=dev)
+        self.x = torch.zeros(lanes, 2, dtype=torch.float64, device=dev)
+        self.out = torch.zeros(max(1, max_outputs), 2, dtype=torch.float64, device=dev)
+        self.fetched = torch.zeros(3, dtype=torch.int64, device=dev)
+        self.version_log = torch.zeros(max(1, max_frames), dtype=torch.int64, device=dev)
+        self.obs_width = policy.perception.obs_width
+
+    def ingest(self, t, lane, observations):
+        obs = observations[0]
+        vec = np.asarray(obs.vector, dtype=np.float64)
+        if vec.shape != (self.obs_width,):
+            raise ShapeMismatch(f"observation width {vec.shape} != ({self.obs_width},)")
+        x0 = np.ascontiguousarray(self.gen.initial_noise(t), dtype=np.float64)
+        o = np.ascontiguousarray(vec)
+        _lib.check(self.lib.auras_toy_ingest(
+            self.latent.data_ptr(), lane, o.ctypes.data_as(_lib.C.POINTER(_lib.f64)),
+            self.x.data_ptr(), x0.ctypes.data_as(_lib.C.POINTER(_lib.f64)), self.p.cuda_stream),
+            "toy_ingest")
+
+    def perceive(self, lane, lo, hi):
+        return None     # identity layers (fp/policy.py:275-276): nothing to launch
+
+    def publish(self, lane, frame, slot, version):
+        st = self.store
+        _lib.check(self.lib.auras_toy_publish(self.latent.data_ptr(), lane, st.payload.data_ptr(),
+                                              st.meta.data_ptr(), st.state.data_ptr(), st.capacity,
+                                              frame, version, self.p.cuda_stream), "toy_publish")
+
+    def fetch(self, target, log_index):
+        self.store.device_fetch(target, self.fetched, self.version_log, log_index, self.g)
+
+    def generate(self, batch):
+        lanes = _lib.int_array([b[0] for b in batch])
+        iters = _lib.int_array([b[2] for b in batch])
+        _lib.check(self.lib.auras_toy_generate(self.x.data_ptr(), lanes, iters, len(batch),
+                                               self.gen.eta, self.store.payload.data_ptr(),
+                                               self.fetched.data_ptr(), self.g.cuda_stream),
+                   "toy_generate")
+
+    def finish(self, lane, out_index):
+        _lib.check(self.lib.auras_toy_finish(self.x.data_ptr(), lane, self.gen.max_action,
+                                             self.out[out_index].data_ptr(), self.g.cuda_stream),
+                   "toy_finish")
+
+    def read_actions(self, n):
+        return self.out[:n].cpu().numpy()[:, None, :]      # [n, agents=1, 2]
+
+    def read_action(self, i):
+        return self.out[i].cpu().numpy()[None, :]
+
+    def read_version_log(self, n):
+        return self.version_log[:n].cpu().numpy()
+
+    def action_values(self, row):
+        return tuple(float(v) for v in row)
+
+    def close(self):
+        pass
+
+
+def make_conditioning_policy(layer_costs=(14.0, 14.0), n_iterations: int = 100,
+                             step_cost: float = 1.0, eta: float = 0.08, max_action: float = 0.8,
+                             noise_init: bool = False) -> Policy:
+    """Same signature and semantics as fp/policy.py:279-297, running on the B200."""
+    costs = tuple(float(c) for c in layer_costs)
+    if not costs:
+        raise ValueError("perception needs at least one layer")
+    if any(c <= 0 for c in costs):
+        raise ValueError("layer cost must be strictly positive")
+    return Policy(perception=PerceptionSpec(costs, obs_width=4),
+                  generation=RefinementGeneration(n_iterations=n_iterations, step_cost=step_cost,
+                                                  eta=eta, max_action=max_action,
+                                                  noise_init=noise_init))

@@ -1,0 +1,65 @@
+"""Pin the CPU oracle against the reference-recorded goldens (no GPU).
+
+The oracle (oracle/schedule.py, oracle/toy.py) must reproduce every schema-1
+trace the unmodified reference produced -- frame times, stage activations,
+context versions, staleness, emitted fp64 actions -- bit for bit.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from golden_util import ReplayEnv, load, schedule_cases
+from oracle import schedule as osched
+from oracle import toy
+
+
+def _jsonify(x):
+    return json.loads(json.dumps(x))
+
+
+CASES = schedule_cases()
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_oracle_reproduces_reference_trace(case):
+    pol = toy.ToyPolicy(**case["policy"])
+    env = ReplayEnv(case["env"], toy.Obs) if case["env"] else None
+    if case["mode"] == "pipe":
+        res = osched.run_pipelined(case["pipeline"], pol, env, case["duration"])
+    else:
+        res = osched.run_sequential(pol, env, case["duration"], case["seq_interval"])
+    assert _jsonify(res.trace) == case["trace"]
+    assert [list(a.values) for a in res.actions] == case["actions"]
+    assert [list(a.staleness_profile) for a in res.actions] == case["staleness_profiles"]
+    assert [_jsonify(vars(r)) for r in res.requests] == case["requests"]
+    if env is not None:
+        assert not env.mismatches
+
+
+def test_oracle_partition_goldens(monkeypatch):
+    g = load("partition")
+    for c in g["generation"]:
+        assert osched.split_generation(c["n"], c["stages"], c["alpha"]) == c["counts"]
+    for c in g["perception"]:
+        assert [list(r) for r in osched.split_perception(c["costs"], c["stages"])] == c["ranges"]
+    f = g["fault_truncate"]
+    monkeypatch.setenv("FRAMEPIPE_ROUNDING_FAULT", "truncate")
+    assert osched.split_generation(f["n"], f["stages"], f["alpha"]) == f["counts"]
+
+
+def test_toy_closed_forms():
+    # t/test_policy.py:62-94 closed forms, restated against the oracle toy
+    eta, n, k = 0.08, 100, 30
+    beta = 1.0 - eta
+    pol = toy.ToyPolicy(eta=eta, n_iterations=n, max_action=10.0)
+    c1, c2 = np.array([1.0, 0.5]), np.array([-0.3, 0.8])
+    s = pol.generation.initial_state()
+    for _ in range(k):
+        s = pol.generation.step(s, toy.Ctx(c1, 0))
+    for _ in range(n - k):
+        s = pol.generation.step(s, toy.Ctx(c2, 1))
+    want = c2 + beta ** (n - k) * ((1.0 - beta ** k) * c1 - c2)
+    assert np.allclose(s.vector, want, rtol=1e-12)
