@@ -105,7 +105,6 @@ int launch_conv_gemm_simt(const ConvGemmArgs &a, cudaStream_t st) {
 template <typename T>
 __global__ void __launch_bounds__(512) conv_epilogue(EpiArgs a) {
   __shared__ float red[32];
-  __shared__ float pool[512];
   const int s = blockIdx.x;
   const bool gn = a.gn_gamma != nullptr;
   const int cg = gn ? a.M / a.groups : min(64, a.M - blockIdx.y * 64);
@@ -114,8 +113,6 @@ __global__ void __launch_bounds__(512) conv_epilogue(EpiArgs a) {
   const int cnt = cg * P;
   float *base = a.partial;
   const int64_t NM = (int64_t)a.N * a.M;
-  if (a.pool_out)
-    for (int i = threadIdx.x; i < cg; i += blockDim.x) pool[i] = 0.f;
 
   float lsum = 0.f;
   for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
@@ -172,7 +169,7 @@ __global__ void __launch_bounds__(512) conv_epilogue(EpiArgs a) {
     if (!a.res_before_act) y += r;
     if (a.out_f32 && !a.pool_out) a.out_f32[row * a.M + c] = y;
     if (a.pool_out) {
-      atomicAdd(&pool[cc], y);
+      base[row * a.M + c] = y;          // staged for the fixed-order pooling below
     } else if (out) {
       const int ox2 = a.out_stuff ? 2 * ox : ox;
       T *dst = out + ((int64_t)(s * a.Ho + oy) * wout + ox2) * a.out_pitch + a.out_coff + c;
@@ -180,10 +177,13 @@ __global__ void __launch_bounds__(512) conv_epilogue(EpiArgs a) {
       if (a.out_stuff) Elem<T>::store(dst + a.out_pitch, 0.f);
     }
   }
-  if (a.pool_out) {
+  if (a.pool_out) {                    // deterministic global average pool
     __syncthreads();
-    for (int i = threadIdx.x; i < cg; i += blockDim.x)
-      a.out_f32[(int64_t)s * a.M + c0 + i] = pool[i] / P;
+    for (int i = threadIdx.x; i < cg; i += blockDim.x) {
+      float acc = 0.f;
+      for (int p = 0; p < P; ++p) acc += base[(int64_t)(s * P + p) * a.M + c0 + i];
+      a.out_f32[(int64_t)s * a.M + c0 + i] = acc / P;
+    }
   }
 }
 
@@ -191,7 +191,7 @@ template <typename T>
 int launch_conv_epilogue(const EpiArgs &a, int S, cudaStream_t st) {
   const bool gn = a.gn_gamma != nullptr;
   if (gn && (a.groups <= 0 || a.M % a.groups)) { set_error("epilogue: M %% groups"); return AURAS_E_ARG; }
-  if (a.pool_out && (!a.out_f32 || (gn ? a.M / a.groups : 64) > 512)) { set_error("epilogue: pool"); return AURAS_E_ARG; }
+  if (a.pool_out && !a.out_f32) { set_error("epilogue: pool without out_f32"); return AURAS_E_ARG; }
   dim3 grid(S, gn ? a.groups : (a.M + 63) / 64);
   conv_epilogue<T><<<grid, 512, 0, st>>>(a);
   AURAS_LAUNCHED("conv_epilogue");

@@ -46,7 +46,7 @@ __global__ void unet_prep(UnetDev *dev, int r, auras_sched sch, int horizon, int
   i = i < sch.n_steps ? i : sch.n_steps - 1;
   if (threadIdx.x == 0) {
     dev->tau_row[s] = sch.timestep[i];
-    const int64_t slot = c.fetched[3 * agent + 0];
+    const int64_t slot = c.fetched[0];   // one ring version schedule per lock-stepped agent group
     dev->film_b_off[s] = agent * ring_agent_stride + slot * ring_slot_stride;
   }
   const float *x = c.x_lanes + ((int64_t)agent * c.lanes_per_agent + lane) * horizon * adim;

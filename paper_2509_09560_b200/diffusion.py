@@ -1,0 +1,887 @@
+"""Diffusion Policy CNN plugin: ResNet-18-GN perception + ConditionalUnet1D
+denoiser with FiLM, DDPM / DDIM, on the B200.
+
+The reference's plugin interface is `Policy(perception, generation)`
+(fp/policy.py:259-272); its conditioning family stands in for a diffusion
+policy with a 2-float contraction (fp/policy.py:220-225).  This module is the
+real network behind the same interface.  Architecture (
+public Diffusion Policy conventions, which the reference does not pin):
+
+* observation encoder: torchvision-style ResNet-18, every BatchNorm replaced
+  by GroupNorm(C/16), fc removed -> 512-d feature per frame, input u8 frames
+  mapped to [-1, 1]; global_cond = n_obs_steps x [feature, agent_pos];
+* ConditionalUnet1D(input_dim=action_dim, down_dims, kernel 5, GN(8),
+  FiLM scale+bias, diffusion-step embedding Sinusoidal -> Linear(d,4d) ->
+  Mish -> Linear(4d,d)), residual 1x1 convs when channels change,
+  Downsample = Conv1d(k3,s2,p1), Upsample = ConvTranspose1d(k4,s2,p1);
+* DDPM (squaredcos_cap_v2 betas, epsilon prediction, clip_sample,
+  fixed_small variance) or DDIM (eta = 0, "leading" spacing, alpha_prev = 1
+  at the last step).
+
+B200 restructuring:
+
+* FiLM is separable: W [Mish(temb); Mish(gc)] + b = (W_t Mish(temb) + b) +
+  W_o Mish(gc).  The first term is tabled for every diffusion timestep at
+  init; the second is computed ONCE PER PUBLISH in the perception epilogue and
+  stored in the public-context ring slot.  Denoise epilogues gather
+  table[timestep] + slot row -- the FiLM Linear never runs in the step loop.
+* Convolutions are implicit GEMMs over NHWC / time-major activations
+  (K = taps x channels); ConvTranspose1d is a conv over a zero-stuffed input
+  written directly by the producing epilogue; channel concats are views into
+  one buffer the producers write at channel offsets.
+* All in-flight requests of all agents are one batch of S samples at
+  staggered timesteps; x_t lives in per-request lanes in HBM.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field, replace
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .context import ContextKind, ContextStore
+from .errors import ConfigInvalid, ShapeMismatch
+from .policy import ActionOutput, Observation, Policy
+
+
+# ---------------------------------------------------------------- configuration
+
+@dataclass(frozen=True)
+class DPConfig:
+    name: str = "pusht"
+    image_hw: int = 96
+    image_channels: int = 3
+    n_obs_steps: int = 2
+    agent_pos_dim: int = 2
+    feat_dim: int = 512
+    down_dims: tuple = (512, 1024, 2048)
+    kernel_size: int = 5
+    n_groups: int = 8
+    dsed: int = 128                 # diffusion step embedding dim
+    horizon: int = 16
+    action_dim: int = 2
+    num_train_timesteps: int = 100
+    num_inference_steps: int = 100
+    scheduler: str = "ddpm"         # "ddpm" | "ddim"
+    clip_sample: bool = True
+    max_action: float = 1.0
+
+    @property
+    def gc_dim(self) -> int:
+        return self.n_obs_steps * (self.feat_dim + self.agent_pos_dim)
+
+    @property
+    def cond_dim(self) -> int:
+        return self.dsed + self.gc_dim
+
+
+PRESETS = {
+    # BASELINE configs[0]: tiny Conv1D-UNet, 16 DDIM steps, 96x96 frames
+    "tiny": DPConfig(name="tiny", n_obs_steps=1, down_dims=(64, 128, 256), dsed=64,
+                     num_inference_steps=16, scheduler="ddim"),
+    # BASELINE configs[1]: DP-CNN PushT image shape, 100-step DDPM
+    "pusht": DPConfig(name="pusht"),
+    # DP default UNet widths (256, 512, 1024)
+    "dp_default": DPConfig(name="dp_default", down_dims=(256, 512, 1024), dsed=256),
+}
+
+
+def unet_blocks(cfg: DPConfig):
+    """Residual blocks in execution order: (name, c_in, c_out, T)."""
+    dims = [cfg.action_dim] + list(cfg.down_dims)
+    pairs = list(zip(dims[:-1], dims[1:]))
+    T = cfg.horizon
+    out = []
+    for i, (ci, co) in enumerate(pairs):
+        out += [(f"down{i}.0", ci, co, T), (f"down{i}.1", co, co, T)]
+        if i < len(pairs) - 1:
+            T //= 2
+    dl = cfg.down_dims[-1]
+    out += [("mid.0", dl, dl, T), ("mid.1", dl, dl, T)]
+    for i, (din, dout) in enumerate(reversed(pairs[1:])):
+        out += [(f"up{i}.0", 2 * dout, din, T), (f"up{i}.1", din, din, T)]
+        T *= 2
+    return out
+
+
+def film_layout(cfg: DPConfig):
+    """Offsets of each block's [scale; bias] rows in the FiLM vector."""
+    offs, acc = {}, 0
+    for name, _, co, _ in unet_blocks(cfg):
+        offs[name] = acc
+        acc += 2 * co
+    return offs, acc
+
+
+RESNET_LAYERS = ((64, 1), (128, 2), (256, 2), (512, 2))   # (channels, first-block stride)
+
+
+# ---------------------------------------------------------------- weights
+
+def init_weights(cfg: DPConfig, seed: int = 0, device="cpu") -> dict:
+    """Deterministic random init in PyTorch layouts (fp32).  Conv / Linear
+    weights and biases ~ U(-1/sqrt(fan_in), 1/sqrt(fan_in)) (PyTorch's default
+    bound); GroupNorm gamma = 1 + 0.1 U(-1,1), beta = 0.1 U(-1,1) so the affine
+    path is exercised.  No checkpoints exist offline: weights are synthetic."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    w = {}
+
+    def uni(shape, bound):
+        return (torch.rand(shape, generator=g, device=device) * 2 - 1) * bound
+
+    def conv(name, co, ci, *k, bias=True, fan_in=None):
+        fan = fan_in if fan_in is not None else ci * int(np.prod(k))
+        b = 1.0 / math.sqrt(fan)
+        w[name + ".w"] = uni((co, ci, *k), b)
+        if bias:
+            w[name + ".b"] = uni((co,), b)
+
+    def gn(name, c):
+        w[name + ".g"] = 1.0 + 0.1 * uni((c,), 1.0)
+        w[name + ".b"] = 0.1 * uni((c,), 1.0)
+
+    # ResNet-18-GN
+    conv("enc.conv1", 64, cfg.image_channels, 7, 7, bias=False)
+    gn("enc.gn1", 64)
+    cin = 64
+    for li, (c, stride) in enumerate(RESNET_LAYERS, start=1):
+        for bi in range(2):
+            p = f"enc.layer{li}.{bi}"
+            s = stride if bi == 0 else 1
+            conv(p + ".conv1", c, cin if bi == 0 else c, 3, 3, bias=False)
+            gn(p + ".gn1", c)
+            conv(p + ".conv2", c, c, 3, 3, bias=False)
+            gn(p + ".gn2", c)
+            if bi == 0 and (s != 1 or cin != c):
+                conv(p + ".ds", c, cin, 1, 1, bias=False)
+                gn(p + ".dsgn", c)
+        cin = c
+    # UNet
+    d = cfg.dsed
+    conv("unet.temb.l1", 4 * d, d)
+    conv("unet.temb.l2", d, 4 * d)
+    k = cfg.kernel_size
+    for name, ci, co, _ in unet_blocks(cfg):
+        p = "unet." + name
+        conv(p + ".c1", co, ci, k)
+        gn(p + ".g1", co)
+        conv(p + ".c2", co, co, k)
+        gn(p + ".g2", co)
+        conv(p + ".film", 2 * co, cfg.cond_dim)
+        if ci != co:
+            conv(p + ".res", co, ci, 1)
+    L = len(cfg.down_dims)
+    for i in range(L - 1):
+        c = cfg.down_dims[i]
+        conv(f"unet.down{i}.ds", c, c, 3)
+    for i in range(L - 1):
+        c = cfg.down_dims[L - 2 - i]
+        # ConvTranspose1d weight layout [in, out, k]; PyTorch fan_in = out * k
+        conv(f"unet.up{i}.us", c, c, 4, fan_in=c * 4)
+    c0 = cfg.down_dims[0]
+    conv("unet.final.c", c0, c0, k)
+    gn("unet.final.g", c0)
+    conv("unet.final.out", cfg.action_dim, c0, 1)
+    return w
+
+
+# ---------------------------------------------------------------- scheduler tables
+
+def scheduler_tables(cfg: DPConfig) -> dict:
+    """Per inference step i: timestep and the coefficients of
+    x_{i+1} = c_x0 * clip((x - s1m * eps) / sab) + c_xt * x + c_eps * eps + sigma * z
+    (diffusers DDPMScheduler / DDIMScheduler conventions, fp64 on the host)."""
+    T = cfg.num_train_timesteps
+
+    def abar(t):
+        return math.cos((t + 0.008) / 1.008 * math.pi / 2) ** 2
+
+    betas = np.array([min(1 - abar((i + 1) / T) / abar(i / T), 0.999) for i in range(T)])
+    ac = np.cumprod(1.0 - betas)
+    n = cfg.num_inference_steps
+    ratio = T // n
+    steps = (np.arange(n) * ratio)[::-1].astype(np.int64)
+    out = {k: np.zeros(n) for k in ("sqrt_ab", "sqrt_1mab", "c_x0", "c_xt", "c_eps", "sigma")}
+    out["timestep"] = steps.astype(np.int32)
+    for i, t in enumerate(steps):
+        prev = t - ratio
+        ab = ac[t]
+        abp = ac[prev] if prev >= 0 else 1.0
+        out["sqrt_ab"][i] = math.sqrt(ab)
+        out["sqrt_1mab"][i] = math.sqrt(1 - ab)
+        if cfg.scheduler == "ddpm":
+            cur_a = ab / abp
+            cur_b = 1 - cur_a
+            out["c_x0"][i] = math.sqrt(abp) * cur_b / (1 - ab)
+            out["c_xt"][i] = math.sqrt(cur_a) * (1 - abp) / (1 - ab)
+            if t > 0:
+                var = max((1 - abp) / (1 - ab) * cur_b, 1e-20)
+                out["sigma"][i] = math.sqrt(var)
+        else:
+            out["c_x0"][i] = math.sqrt(abp)
+            out["c_eps"][i] = math.sqrt(1 - abp)
+    return out
+
+
+def request_noise(cfg: DPConfig, seed_base: int, agent: int, birth_frame: int):
+    """Host-drawn randomness of one request: x_T ~ N(0, I) of (horizon, action_dim)
+    then, for DDPM, one N(0, I) draw per inference step -- numpy
+    default_rng((seed_base, agent, birth_frame)), float32."""
+    rng = np.random.default_rng((seed_base, agent, birth_frame))
+    xT = rng.standard_normal((cfg.horizon, cfg.action_dim)).astype(np.float32)
+    z = None
+    if cfg.scheduler == "ddpm":
+        z = rng.standard_normal((cfg.num_inference_steps, cfg.horizon, cfg.action_dim)).astype(np.float32)
+    return xT, z
+
+
+def synthetic_frame(cfg: DPConfig, seed_base: int, agent: int, frame: int) -> Observation:
+    """A pure function of (seed, agent, frame): u8 CHW image and agent position."""
+    rng = np.random.default_rng((seed_base, agent, frame, 7))
+    img = rng.integers(0, 256, (cfg.image_channels, cfg.image_hw, cfg.image_hw), dtype=np.uint8)
+    pos = rng.uniform(-1.0, 1.0, cfg.agent_pos_dim)
+    return Observation(frame=frame, vector=pos, image=img)
+
+
+def encoder_flops(cfg: DPConfig):
+    """MACs*2 per encoder layer group [stem, layer1..4] at one frame."""
+    hw = cfg.image_hw // 2
+    groups = [2 * 64 * cfg.image_channels * 49 * hw * hw]
+    hw //= 2
+    cin = 64
+    for c, stride in RESNET_LAYERS:
+        ho = hw // stride
+        f = 2 * c * cin * 9 * ho * ho + 3 * 2 * c * c * 9 * ho * ho
+        if stride != 1 or cin != c:
+            f += 2 * c * cin * ho * ho
+        groups.append(f)
+        hw, cin = ho, c
+    return groups
+
+
+def unet_flops_per_sample(cfg: DPConfig) -> float:
+    k = cfg.kernel_size
+    f = 0.0
+    for _, ci, co, T in unet_blocks(cfg):
+        f += 2 * T * (ci * co * k + co * co * k + (ci * co if ci != co else 0))
+    L = len(cfg.down_dims)
+    T = cfg.horizon
+    for i in range(L - 1):
+        T //= 2
+        f += 2 * T * cfg.down_dims[i] ** 2 * 3
+    for i in range(L - 1):
+        c = cfg.down_dims[L - 2 - i]
+        T *= 2
+        f += 2 * T * c * c * 2      # ConvTranspose k4 s2: 2 taps per output
+    c0 = cfg.down_dims[0]
+    f += 2 * cfg.horizon * (c0 * c0 * k + c0 * cfg.action_dim)
+    return f
+
+
+def unet_stream_bytes(cfg: DPConfig, elem_bytes: int = 2) -> int:
+    """Algorithmic weight bytes streamed per denoise step with FiLM tabled:
+    every conv weight as the kernels store it (bf16) plus fp32 bias/GN params."""
+    k = cfg.kernel_size
+    n = 0
+    f32 = 0
+    for _, ci, co, _ in unet_blocks(cfg):
+        n += co * ci * k + co * co * k + (co * ci if ci != co else 0)
+        f32 += 6 * co
+    L = len(cfg.down_dims)
+    for i in range(L - 1):
+        n += cfg.down_dims[i] ** 2 * 3 + cfg.down_dims[L - 2 - i] ** 2 * 4
+    c0 = cfg.down_dims[0]
+    n += c0 * c0 * k
+    return n * elem_bytes + 4 * (f32 + 3 * c0)
+
+
+# ---------------------------------------------------------------- device model
+
+def _round(x, m):
+    return (x + m - 1) // m * m
+
+
+class DeviceModel:
+    """Weights converted once into the kernels' layouts on the device."""
+
+    def __init__(self, cfg: DPConfig, weights: dict, dtype: str):
+        import torch
+        self.torch = torch
+        self.cfg = cfg
+        self.dt = _lib.DT_BF16 if dtype == "bf16" else _lib.DT_F32
+        self.tdtype = torch.bfloat16 if dtype == "bf16" else torch.float32
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.keep = []
+        w = {k: v.to(self.dev, torch.float32) for k, v in weights.items()}
+        self.w = w
+
+    def f32(self, t):
+        t = t.to(self.dev, self.torch.float32).contiguous()
+        self.keep.append(t)
+        return t
+
+    def conv_weight(self, wt, cin_pad=None, transpose_flip=False):
+        """[Co, Ci, (kh,) kw] -> [Co][Kp] with K = (ky*kw + kx)*Cin + c."""
+        torch = self.torch
+        if transpose_flip:       # ConvTranspose1d [in, out, k] -> conv over stuffed input
+            wt = wt.permute(1, 0, 2).flip(-1)
+        if wt.dim() == 3:
+            wt = wt.unsqueeze(2)                       # [Co, Ci, 1, kw]
+        co, ci, kh, kw = wt.shape
+        cp = cin_pad or ci
+        if cp != ci:
+            wt = torch.nn.functional.pad(wt, (0, 0, 0, 0, 0, cp - ci))
+        m = wt.permute(0, 2, 3, 1).reshape(co, kh * kw * cp)
+        kp = _round(m.shape[1], 64)
+        if kp != m.shape[1]:
+            m = torch.nn.functional.pad(m, (0, kp - m.shape[1]))
+        m = m.to(self.tdtype).contiguous()
+        self.keep.append(m)
+        return m, cp, kh, kw, kp
+
+
+def _op(**kw):
+    op = _lib.ConvOp()
+    op.film_off = -1
+    op.splits = 1
+    op.groups = 1
+    for k, v in kw.items():
+        setattr(op, k, v)
+    return op
+
+
+def _splits(M, N, Kp, target_ctas=296):
+    """Split-K factor so the GEMM grid covers the GPU about twice."""
+    tiles = max(1, ((M + 63) // 64) * ((N + 63) // 64))
+    s = max(1, min(Kp // 64, target_ctas // tiles))
+    return s
+
+
+class Encoder:
+    """ResNet-18-GN program for A frames at a time (K1 of SURVEY.md §2.4)."""
+
+    GROUPS = ("stem", "layer1", "layer2", "layer3", "layer4")
+
+    def __init__(self, model: DeviceModel, A: int):
+        torch = model.torch
+        cfg = model.cfg
+        self.m, self.A = model, A
+        dev, td = model.dev, model.tdtype
+        H = cfg.image_hw
+        self.img = torch.zeros(A, cfg.image_channels, H, H, dtype=torch.uint8, device=dev)
+        self.x0 = torch.zeros(A, H, H, 4, dtype=td, device=dev)
+        self.feat = torch.zeros(A, cfg.feat_dim, dtype=torch.float32, device=dev)
+        self.groups = {g: [] for g in self.GROUPS}
+        self.max_scratch = 0
+        w = model.w
+        hs = H // 2
+        stem = torch.zeros(A, hs, hs, 64, dtype=td, device=dev)
+        wm, cp, kh, kw, kp = model.conv_weight(w["enc.conv1.w"], cin_pad=4)
+        self._add("stem", wm, None, self.x0, 4, 0, H, H, cp, kh, kw, 2, 3, stem, 64, 0, hs, hs,
+                  gn=("enc.gn1", 64 // 16), act=_lib.ACT_RELU)
+        hp = (hs - 1) // 2 + 1
+        pooled = torch.zeros(A, hp, hp, 64, dtype=td, device=dev)
+        self.groups["stem"].append(("maxpool", stem, hs, hs, 64, pooled))
+        self.keep = [stem, pooled]
+        x, hw, cin = pooled, hp, 64
+        for li, (c, stride) in enumerate(RESNET_LAYERS, start=1):
+            g = f"layer{li}"
+            for bi in range(2):
+                p = f"enc.layer{li}.{bi}"
+                s = stride if bi == 0 else 1
+                ho = (hw - 1) // s + 1
+                t1 = torch.zeros(A, ho, ho, c, dtype=td, device=dev)
+                out = torch.zeros(A, ho, ho, c, dtype=td, device=dev)
+                self.keep += [t1, out]
+                ci = cin if bi == 0 else c
+                wm, cp, kh, kw, kp = model.conv_weight(w[p + ".conv1.w"])
+                self._add(g, wm, None, x, ci, 0, hw, hw, cp, kh, kw, s, 1, t1, c, 0, ho, ho,
+                          gn=(p + ".gn1", c // 16), act=_lib.ACT_RELU)
+                res = x
+                if p + ".ds.w" in w:
+                    dsb = torch.zeros(A, ho, ho, c, dtype=td, device=dev)
+                    self.keep.append(dsb)
+                    wm, cp, kh, kw, kp = model.conv_weight(w[p + ".ds.w"])
+                    self._add(g, wm, None, x, ci, 0, hw, hw, cp, kh, kw, s, 0, dsb, c, 0, ho, ho,
+                              gn=(p + ".dsgn", c // 16), act=_lib.ACT_NONE)
+                    res = dsb
+                last = li == 4 and bi == 1
+                wm, cp, kh, kw, kp = model.conv_weight(w[p + ".conv2.w"])
+                self._add(g, wm, None, t1, c, 0, ho, ho, cp, kh, kw, 1, 1, out, c, 0, ho, ho,
+                          gn=(p + ".gn2", c // 16), act=_lib.ACT_RELU, res=(res, c, 0),
+                          res_before_act=1, pool=last)
+                x, hw = out, ho
+            cin = c
+        self.scratch = torch.zeros(max(1, self.max_scratch), dtype=torch.float32, device=dev)
+
+    def _add(self, group, wm, bias, inp, in_pitch, in_coff, H, W, cin, kh, kw, stride, pad, out,
+             out_pitch, out_coff, Ho, Wo, gn=None, act=0, res=None, res_before_act=0, pool=False):
+        m = self.m
+        M, kp = wm.shape
+        N = self.A * Ho * Wo
+        op = _op(w=wm.data_ptr(), bias=_lib.ptr(bias), inp=inp.data_ptr(),
+                 out=0 if pool else out.data_ptr(), M=M, Cin=cin, Kp=kp, H=H, W=W,
+                 in_pitch=in_pitch, in_coff=in_coff, kh=kh, kw=kw, stride=stride, pad_h=pad,
+                 pad_w=pad, Ho=Ho, Wo=Wo, out_pitch=out_pitch, out_coff=out_coff, act=act,
+                 res_before_act=res_before_act, splits=_splits(M, N, kp))
+        if gn is not None:
+            name, groups = gn
+            op.gn_gamma = m.f32(m.w[name + ".g"]).data_ptr()
+            op.gn_beta = m.f32(m.w[name + ".b"]).data_ptr()
+            op.groups = groups
+        if res is not None:
+            op.res, op.res_pitch, op.res_coff = res[0].data_ptr(), res[1], res[2]
+        if pool:
+            op.pool_out = 1
+            op.out_f32 = self.feat.data_ptr()
+        kc = _round((kp + op.splits - 1) // op.splits, 64)
+        splits = (kp + kc - 1) // kc
+        self.max_scratch = max(self.max_scratch, splits * N * M)
+        self.groups[group].append(("conv", op))
+
+    def run(self, lo, hi, stream):
+        lib = _lib.load()
+        st = stream.cuda_stream
+        cfg = self.m.cfg
+        for gi in range(lo, hi):
+            g = self.GROUPS[gi]
+            if gi == 0:
+                _lib.check(lib.auras_image_to_nhwc(self.img.data_ptr(), self.A, cfg.image_channels,
+                                                   cfg.image_hw, cfg.image_hw, self.x0.data_ptr(),
+                                                   4, self.m.dt, st), "image_to_nhwc")
+            for item in self.groups[g]:
+                if item[0] == "conv":
+                    _lib.check(lib.auras_conv(_lib.C.byref(item[1]), self.m.dt, self.A, None, 0,
+                                              self.scratch.data_ptr(), self.scratch.numel(), st),
+                               "encoder conv")
+                else:
+                    _, src, h, wd, c, dst = item
+                    _lib.check(lib.auras_maxpool3s2(src.data_ptr(), self.A, h, wd, c, dst.data_ptr(),
+                                                    self.m.dt, st), "maxpool")
+
+
+class Denoiser:
+    """ConditionalUnet1D program over S_max samples (K3-K6 of SURVEY.md §2.4)."""
+
+    def __init__(self, model: DeviceModel, s_max: int, ring: ContextStore, gc_pad: int,
+                 use_graph: bool = True):
+        torch = model.torch
+        cfg = model.cfg
+        self.m, self.s_max, self.use_graph = model, s_max, use_graph
+        dev, td = model.dev, model.tdtype
+        w = model.w
+        self.film_offs, self.F = film_layout(cfg)
+        self.keep = []
+        self.ops = []
+        S = s_max
+        H, k = cfg.horizon, cfg.kernel_size
+        L = len(cfg.down_dims)
+
+        def buf(T, C, dtype=None):
+            t = torch.zeros(S, T, C, dtype=dtype or td, device=dev)
+            self.keep.append(t)
+            return t
+
+        self.xin = buf(H, 64)
+        # channel-concat buffers of the up path: [x | skip]
+        cats = {}
+        T = H
+        for i in range(1, L):
+            T //= 2
+            cats[i] = buf(T, 2 * cfg.down_dims[i])
+        cur, cur_pitch, cur_coff, T = self.xin, 64, 0, H
+        blocks = unet_blocks(cfg)
+        bi = 0
+        for lvl in range(L):
+            for j in range(2):
+                name, ci, co, Tb = blocks[bi]
+                bi += 1
+                last_in_level = j == 1
+                if last_in_level and lvl >= 1:
+                    dst, dpitch, dcoff = cats[lvl], 2 * co, co          # skip h_lvl
+                else:
+                    dst, dpitch, dcoff = buf(T, co), co, 0
+                self._block(name, ci, co, T, cur, cur_pitch, cur_coff, dst, dpitch, dcoff,
+                            cin_pad=64 if (lvl == 0 and j == 0) else None)
+                cur, cur_pitch, cur_coff = dst, dpitch, dcoff
+            if lvl < L - 1:
+                c = cfg.down_dims[lvl]
+                nxt = buf(T // 2, c)
+                wm, cp, kh, kw, kp = model.conv_weight(w[f"unet.down{lvl}.ds.w"])
+                self._conv(wm, model.f32(w[f"unet.down{lvl}.ds.b"]), cur, cur_pitch, cur_coff, T, cp,
+                           kw, 2, 1, nxt, c, 0, T // 2)
+                cur, cur_pitch, cur_coff, T = nxt, c, 0, T // 2
+        # mid: 2 blocks at the deepest level; output into the left half of cats[L-1]
+        dl = cfg.down_dims[-1]
+        mid0 = buf(T, dl)
+        self._block("mid.0", dl, dl, T, cur, cur_pitch, cur_coff, mid0, dl, 0)
+        self._block("mid.1", dl, dl, T, mid0, dl, 0, cats[L - 1], 2 * dl, 0)
+        cur, cur_pitch, cur_coff = cats[L - 1], 2 * dl, 0
+        up_blocks = [b for b in blocks if b[0].startswith("up")]
+        for i in range(L - 1):
+            name0, ci0, co0, _ = up_blocks[2 * i]
+            a = buf(T, co0)
+            self._block(name0, ci0, co0, T, cur, cur_pitch, cur_coff, a, co0, 0)
+            stuffed = buf(2 * T, co0)
+            self._block(up_blocks[2 * i + 1][0], co0, co0, T, a, co0, 0, stuffed, co0, 0, stuff=True)
+            lvl = L - 2 - i
+            if lvl >= 1:
+                dst, dpitch = cats[lvl], 2 * cfg.down_dims[lvl]
+            else:
+                dst, dpitch = buf(2 * T, co0), co0
+            wm, cp, kh, kw, kp = model.conv_weight(w[f"unet.up{i}.us.w"], transpose_flip=True)
+            self._conv(wm, model.f32(w[f"unet.up{i}.us.b"]), stuffed, co0, 0, 2 * T, cp, kw, 1, 2, dst,
+                       dpitch, 0, 2 * T)
+            cur, cur_pitch, cur_coff, T = dst, dpitch, 0, 2 * T
+        c0 = cfg.down_dims[0]
+        fin = buf(H, c0)
+        wm, cp, kh, kw, kp = model.conv_weight(w["unet.final.c.w"])
+        self._conv(wm, model.f32(w["unet.final.c.b"]), cur, cur_pitch, cur_coff, H, cp, kw, 1, k // 2,
+                   fin, c0, 0, H, gn="unet.final.g", act=_lib.ACT_MISH)
+        self.final_w = model.f32(w["unet.final.out.w"].reshape(cfg.action_dim, c0))
+        self.final_b = model.f32(w["unet.final.out.b"])
+        self._build_tables(ring, gc_pad)
+
+    # -- op builders
+    def _conv(self, wm, bias, inp, in_pitch, in_coff, T, cin, kw, stride, pad, out, out_pitch,
+              out_coff, To, gn=None, act=0, res=None, res_f32=None, out_f32=None, film=None,
+              stuff=False):
+        m = self.m
+        M, kp = wm.shape
+        N = self.s_max * To
+        op = _op(w=wm.data_ptr(), bias=_lib.ptr(bias), inp=inp.data_ptr(),
+                 out=0 if out is None else out.data_ptr(), M=M, Cin=cin, Kp=kp, H=1, W=T,
+                 in_pitch=in_pitch, in_coff=in_coff, kh=1, kw=kw, stride=stride, pad_h=0, pad_w=pad,
+                 Ho=1, Wo=To, out_pitch=out_pitch, out_coff=out_coff, act=act,
+                 splits=_splits(M, N, kp), out_stuff=1 if stuff else 0)
+        if gn is not None:
+            op.gn_gamma = m.f32(m.w[gn + ".g"]).data_ptr()
+            op.gn_beta = m.f32(m.w[gn + ".b"]).data_ptr()
+            op.groups = self.m.cfg.n_groups
+        if res is not None:
+            op.res, op.res_pitch, op.res_coff = res[0].data_ptr(), res[1], res[2]
+        if res_f32 is not None:
+            op.res_f32 = res_f32.data_ptr()
+        if out_f32 is not None:
+            op.out_f32 = out_f32.data_ptr()
+        if film is not None:
+            op.film_off = film
+        self.ops.append(op)
+
+    def _block(self, name, ci, co, T, inp, in_pitch, in_coff, out, out_pitch, out_coff,
+               cin_pad=None, stuff=False):
+        """ConditionalResidualBlock1D: conv1-GN-Mish-FiLM, conv2-GN-Mish, + residual."""
+        m, w, k = self.m, self.m.w, self.m.cfg.kernel_size
+        p = "unet." + name
+        a = self.m.torch.zeros(self.s_max, T, co, dtype=m.tdtype, device=m.dev)
+        self.keep.append(a)
+        wm, cp, kh, kw, kp = m.conv_weight(w[p + ".c1.w"], cin_pad=cin_pad)
+        self._conv(wm, m.f32(w[p + ".c1.b"]), inp, in_pitch, in_coff, T, cp, kw, 1, k // 2, a, co, 0, T,
+                   gn=p + ".g1", act=_lib.ACT_MISH, film=self.film_offs[name])
+        res, res_f32 = None, None
+        if ci != co:
+            r32 = self.m.torch.zeros(self.s_max, T, co, dtype=self.m.torch.float32, device=m.dev)
+            self.keep.append(r32)
+            wm, cp, kh, kw, kp = m.conv_weight(w[p + ".res.w"], cin_pad=cin_pad)
+            self._conv(wm, m.f32(w[p + ".res.b"]), inp, in_pitch, in_coff, T, cp, kw, 1, 0, None, co, 0, T,
+                       out_f32=r32)
+            res_f32 = r32
+        else:
+            res = (inp, in_pitch, in_coff)
+        wm, cp, kh, kw, kp = m.conv_weight(w[p + ".c2.w"])
+        self._conv(wm, m.f32(w[p + ".c2.b"]), a, co, 0, T, cp, kw, 1, k // 2, out, out_pitch, out_coff, T,
+                   gn=p + ".g2", act=_lib.ACT_MISH, res=res, res_f32=res_f32, stuff=stuff)
+
+    def _build_tables(self, ring, gc_pad):
+        """FiLM split: W = [W_t | W_o]; table[tau] = W_t Mish(temb(tau)) + b (all taus,
+        once); W_o (bf16/fp32, K padded) is applied per publish into the ring slot."""
+        torch = self.m.torch
+        cfg, m, w = self.m.cfg, self.m, self.m.w
+        lib = _lib.load()
+        names = [b[0] for b in unet_blocks(cfg)]
+        Wf = torch.cat([w[f"unet.{n}.film.w"] for n in names], 0)       # [F, cond_dim]
+        bf = torch.cat([w[f"unet.{n}.film.b"] for n in names], 0)
+        d = cfg.dsed
+        Wt, Wo = Wf[:, :d], Wf[:, d:]
+        self.film_o = torch.nn.functional.pad(Wo, (0, gc_pad - Wo.shape[1])).to(m.tdtype).contiguous()
+        self.keep.append(self.film_o)
+        # time table on the device with the library's own kernels
+        nT = cfg.num_train_timesteps
+        st = torch.cuda.current_stream()
+        taus = torch.arange(nT, dtype=torch.int32, device=m.dev)
+        emb = torch.zeros(nT, d, dtype=torch.float32, device=m.dev)
+        _lib.check(lib.auras_sinusoidal(taus.data_ptr(), nT, d, emb.data_ptr(), st.cuda_stream), "sinusoidal")
+        h = torch.zeros(nT, 4 * d, dtype=torch.float32, device=m.dev)
+        temb = torch.zeros(nT, d, dtype=torch.float32, device=m.dev)
+        self.film_tau = torch.zeros(nT, self.F, dtype=torch.float32, device=m.dev)
+        keep = []
+
+        def lin(W, b, x, y, K, mish):
+            Wp = W.to(m.tdtype)
+            Kp = _round(K, 8)
+            if Kp != K:
+                Wp = torch.nn.functional.pad(Wp, (0, Kp - K))
+            Wp = Wp.contiguous()
+            keep.append(Wp)
+            op = _lib.LinearOp(w=Wp.data_ptr(), bias=_lib.ptr(b), M=W.shape[0], K=K, mish_in=mish, ldw=Kp)
+            _lib.check(lib.auras_linear(_lib.C.byref(op), m.dt, x.shape[0], x.data_ptr(), x.shape[1],
+                                        y.data_ptr(), y.shape[1], st.cuda_stream), "linear")
+
+        lin(w["unet.temb.l1.w"], m.f32(w["unet.temb.l1.b"]), emb, h, d, 0)
+        lin(w["unet.temb.l2.w"], m.f32(w["unet.temb.l2.b"]), h, temb, 4 * d, 1)
+        lin(Wt, m.f32(bf), temb, self.film_tau, d, 1)
+        torch.cuda.synchronize()
+        self.film_tau_ptr = self.film_tau.data_ptr()
+
+
+# ---------------------------------------------------------------- policy objects
+
+@dataclass(frozen=True)
+class DPPerception:
+    layer_costs: tuple
+    obs_width: int = 2
+
+    @property
+    def layers(self):
+        return self.layer_costs
+
+    @property
+    def total_cost(self) -> float:
+        return float(sum(self.layer_costs))
+
+
+@dataclass(frozen=True)
+class DPGeneration:
+    cfg: DPConfig
+    dtype: str
+    seed: int
+    weights: dict = field(repr=False, compare=False, hash=False)
+    step_cost: float = 1.0
+    use_graph: bool = True
+    kind: ContextKind = ContextKind.CONDITIONING
+
+    @property
+    def n_iterations(self) -> int:
+        return self.cfg.num_inference_steps
+
+    @property
+    def total_cost(self) -> float:
+        return self.n_iterations * self.step_cost
+
+    @property
+    def max_action(self) -> float:
+        return self.cfg.max_action
+
+    def decode_action(self, action: ActionOutput) -> np.ndarray:
+        """Environment-facing displacement: horizon row n_obs_steps-1 (the
+        first executed action in Diffusion Policy), norm-clipped to max_action."""
+        cfg = self.cfg
+        hor = np.asarray(action.values, dtype=np.float64).reshape(cfg.horizon, cfg.action_dim)
+        vec = hor[cfg.n_obs_steps - 1].copy()
+        n = float(np.linalg.norm(vec))
+        if n > cfg.max_action:
+            vec *= cfg.max_action / n
+        return vec
+
+    def open_session(self, policy, **kw):
+        return DPSession(policy, **kw)
+
+
+@dataclass(frozen=True)
+class DPPolicy(Policy):
+    agents: int = 1
+
+    def synthetic_observation(self, agent, frame):
+        return synthetic_frame(self.generation.cfg, self.generation.seed, agent, frame)
+
+
+_MODEL_CACHE = {}
+
+
+class DPSession:
+    """Device state of one run: encoder, denoiser plan, HBM ring, request lanes."""
+
+    def __init__(self, policy, *, capacity, lanes, agents, max_outputs, max_frames,
+                 p_stream, g_stream, pp_perception=1):
+        import torch
+        if pp_perception != 1:
+            raise ConfigInvalid("the DP plugin runs its encoder as one perception stage "
+                                "(pp_perception = 1, the paper's depth sweep)")
+        self.torch = torch
+        self.lib = _lib.load()
+        gen: DPGeneration = policy.generation
+        cfg = gen.cfg
+        self.cfg, self.gen = cfg, gen
+        self.p, self.g = p_stream, g_stream
+        self.A, self.R = agents, lanes
+        dev = torch.device("cuda", torch.cuda.current_device())
+        key = (id(gen.weights), gen.dtype)
+        if key not in _MODEL_CACHE:
+            _MODEL_CACHE.clear()
+            _MODEL_CACHE[key] = DeviceModel(cfg, gen.weights, gen.dtype)
+        self.model = _MODEL_CACHE[key]
+        self.gc_pad = _round(cfg.gc_dim, 8)
+        _, F = film_layout(cfg)
+        self.slot_floats = self.gc_pad + F
+        self.store = ContextStore(capacity, slot_elems=self.slot_floats, agents=agents,
+                                  dtype=torch.float32, device=dev)
+        self.encoder = Encoder(self.model, agents)
+        s_max = agents * max(1, lanes)
+        s_max = min(s_max, 64)
+        self.denoiser = Denoiser(self.model, s_max, self.store, self.gc_pad, gen.use_graph)
+        sched = scheduler_tables(cfg)
+        self.sched_t = {k: torch.tensor(v, dtype=torch.int32 if k == "timestep" else torch.float32,
+                                        device=dev) for k, v in sched.items()}
+        sc = _lib.Sched()
+        for k in ("timestep", "sqrt_ab", "sqrt_1mab", "c_x0", "c_xt", "c_eps", "sigma"):
+            setattr(sc, k, self.sched_t[k].data_ptr())
+        sc.n_steps, sc.clip_sample = cfg.num_inference_steps, int(cfg.clip_sample)
+        sc.ddpm = int(cfg.scheduler == "ddpm")
+        ops = (_lib.ConvOp * len(self.denoiser.ops))(*self.denoiser.ops)
+        payload = self.store.payload
+        self.plan = self.lib.auras_unet_plan_create(
+            ops, len(self.denoiser.ops), self.model.dt, s_max, cfg.horizon, cfg.action_dim,
+            self.denoiser.film_tau_ptr, payload.data_ptr() + 4 * self.gc_pad, self.denoiser.F,
+            self.slot_floats, capacity * self.slot_floats, self.denoiser.final_w.data_ptr(),
+            self.denoiser.final_b.data_ptr(), cfg.down_dims[0], _lib.C.byref(sc),
+            self.denoiser.xin.data_ptr(), 64)
+        if not self.plan:
+            _lib.check(-2, "unet_plan_create")
+        self.s_max = s_max
+        hr = cfg.horizon * cfg.action_dim
+        self.row = hr
+        self.x = torch.zeros(agents, lanes, hr, dtype=torch.float32, device=dev)
+        self.noise = None
+        if cfg.scheduler == "ddpm":
+            self.noise = torch.zeros(agents, lanes, cfg.num_inference_steps, hr, dtype=torch.float32,
+                                     device=dev)
+        self.pos = torch.zeros(agents, cfg.agent_pos_dim, dtype=torch.float32, device=dev)
+        self.prev = torch.zeros(agents, cfg.feat_dim + cfg.agent_pos_dim, dtype=torch.float32, device=dev)
+        self.first = True
+        self.out = torch.zeros(max(1, max_outputs), agents, hr, dtype=torch.float32, device=dev)
+        self.fetched = torch.zeros(3, dtype=torch.int64, device=dev)
+        self.version_log = torch.zeros(max(1, max_frames), dtype=torch.int64, device=dev)
+        self.film_op = _lib.LinearOp(w=self.denoiser.film_o.data_ptr(), bias=0, M=self.denoiser.F,
+                                     K=cfg.gc_dim, mish_in=1, ldw=self.gc_pad)
+        self.device_frames = None      # optional [frames, A, C, H, W] u8 resident source
+        torch.cuda.synchronize()
+
+    # -- ingest: frames to HBM, request randomness to its lane
+    def ingest(self, t, lane, observations):
+        torch = self.torch
+        cfg = self.cfg
+        if len(observations) != self.A:
+            raise ShapeMismatch(f"{len(observations)} observations for {self.A} agents")
+        with torch.cuda.stream(self.p):
+            if self.device_frames is not None:
+                self.encoder.img.copy_(self.device_frames[t % self.device_frames.shape[0]], non_blocking=True)
+            else:
+                imgs = np.stack([o.image for o in observations])
+                if imgs.shape[1:] != (cfg.image_channels, cfg.image_hw, cfg.image_hw):
+                    raise ShapeMismatch(f"image shape {imgs.shape[1:]}")
+                self.encoder.img.copy_(torch.from_numpy(imgs).pin_memory(), non_blocking=True)
+            pos = np.stack([np.asarray(o.vector, dtype=np.float32) for o in observations])
+            if pos.shape[1] != cfg.agent_pos_dim:
+                raise ShapeMismatch(f"agent_pos width {pos.shape[1]} != {cfg.agent_pos_dim}")
+            self.pos.copy_(torch.from_numpy(pos).pin_memory(), non_blocking=True)
+            xs, zs = [], []
+            for a in range(self.A):
+                xT, z = request_noise(cfg, self.gen.seed, a, t)
+                xs.append(xT.reshape(-1))
+                if z is not None:
+                    zs.append(z.reshape(cfg.num_inference_steps, -1))
+            self.x[:, lane].copy_(torch.from_numpy(np.stack(xs)).pin_memory(), non_blocking=True)
+            if self.noise is not None:
+                self.noise[:, lane].copy_(torch.from_numpy(np.stack(zs)).pin_memory(), non_blocking=True)
+
+    def perceive(self, lane, lo, hi):
+        self.encoder.run(lo, hi, self.p)
+
+    def publish(self, lane, frame, slot, version):
+        st = self.store
+        payload = st.payload
+        base = payload.data_ptr() + 4 * slot * self.slot_floats
+        agent_stride = st.capacity * self.slot_floats
+        _lib.check(self.lib.auras_dp_assemble_cond(
+            self.encoder.feat.data_ptr(), self.pos.data_ptr(), self.prev.data_ptr(), self.A,
+            self.cfg.feat_dim, self.cfg.agent_pos_dim, self.cfg.n_obs_steps, int(self.first), base,
+            agent_stride, self.p.cuda_stream), "assemble_cond")
+        self.first = False
+        # FiLM projection of the new context, once per publish, into the slot
+        _lib.check(self.lib.auras_linear(_lib.C.byref(self.film_op), self.model.dt, self.A, base,
+                                         agent_stride, base + 4 * self.gc_pad, agent_stride,
+                                         self.p.cuda_stream), "film projection")
+        st.commit(frame, version, self.p)
+
+    def fetch(self, target, log_index):
+        self.store.device_fetch(target, self.fetched, self.version_log, log_index, self.g)
+
+    def generate(self, batch):
+        lanes, agents, start, count = [], [], [], []
+        for a in range(self.A):
+            for lane, s0, n in batch:
+                lanes.append(lane)
+                agents.append(a)
+                start.append(s0)
+                count.append(n)
+        S = len(lanes)
+        if S > self.s_max:
+            raise ConfigInvalid(f"{S} in-flight samples exceed the plan's {self.s_max}")
+        iters = max(count)
+        ia = _lib.int_array
+        _lib.check(self.lib.auras_unet_generate(
+            self.plan, S, ia(lanes), ia(agents), ia(start), ia(count), iters, self.R,
+            self.x.data_ptr(), _lib.ptr(self.noise), self.fetched.data_ptr(),
+            int(self.gen.use_graph), self.g.cuda_stream), "unet_generate")
+
+    def finish(self, lane, out_index):
+        A = self.A
+        _lib.check(self.lib.auras_dp_finish(self.x.data_ptr(), A, _lib.int_array(list(range(A))),
+                                            _lib.int_array([lane] * A), A, self.R, self.row,
+                                            self.out[out_index].data_ptr(), self.g.cuda_stream),
+                   "dp_finish")
+
+    def read_actions(self, n):
+        return self.out[:n].cpu().numpy()
+
+    def read_action(self, i):
+        return self.out[i].cpu().numpy()
+
+    def read_version_log(self, n):
+        return self.version_log[:n].cpu().numpy()
+
+    def action_values(self, row):
+        return tuple(float(v) for v in row)
+
+    def close(self):
+        if self.plan:
+            self.lib.auras_unet_plan_destroy(self.plan)
+            self.plan = None
+
+
+def make_diffusion_policy(config="pusht", dtype: str = "bf16", seed: int = 0, weights=None,
+                          agents: int = 1, use_graph: bool = True, **overrides) -> DPPolicy:
+    """Diffusion Policy CNN on the B200 behind the reference's Policy interface.
+
+    `config`: a preset name ("tiny", "pusht", "dp_default") or a DPConfig.
+    `dtype`: "bf16" (tensor-core path) or "fp32" (reference-precision path).
+    `weights`: a dict from `init_weights` (default: init_weights(cfg, seed))."""
+    cfg = PRESETS[config] if isinstance(config, str) else config
+    if overrides:
+        cfg = replace(cfg, **overrides)
+    if dtype not in ("bf16", "fp32"):
+        raise ConfigInvalid(f"dtype must be bf16 or fp32, not {dtype!r}")
+    if weights is None:
+        import torch
+        weights = init_weights(cfg, seed, device="cuda" if torch.cuda.is_available() else "cpu")
+    gflop = [f / 1e9 for f in encoder_flops(cfg)]
+    step_gflop = unet_flops_per_sample(cfg) / 1e9
+    perception = DPPerception(layer_costs=tuple(gflop), obs_width=cfg.agent_pos_dim)
+    generation = DPGeneration(cfg=cfg, dtype=dtype, seed=seed, weights=weights, step_cost=step_gflop,
+                              use_graph=use_graph)
+    return DPPolicy(perception=perception, generation=generation, agents=agents)

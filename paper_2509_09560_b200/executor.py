@@ -180,7 +180,8 @@ class _Port:
 class _Device:
     """Streams, events and the policy session for one run."""
 
-    def __init__(self, policy, *, capacity, lanes, agents, max_outputs, max_frames, clock):
+    def __init__(self, policy, *, capacity, lanes, agents, max_outputs, max_frames, clock,
+                 pp_perception=1):
         import torch
         self.torch = torch
         self.clock = clock
@@ -188,7 +189,8 @@ class _Device:
         self.G = torch.cuda.Stream()
         self.session = policy.open_session(capacity=capacity, lanes=lanes, agents=agents,
                                            max_outputs=max_outputs, max_frames=max_frames,
-                                           p_stream=self.P, g_stream=self.G)
+                                           p_stream=self.P, g_stream=self.G,
+                                           pp_perception=pp_perception)
         self.store = self.session.store
         self.pub_event = {}          # context frame -> event after its publish (P)
         self.ingest_event = {}       # request -> event after ingest (P)
@@ -344,7 +346,7 @@ def run_pipelined(cfg: PipelineConfig, policy, env, duration: int, *, clock: str
     p_cost = [sum(policy.perception.layer_costs[a:b]) for a, b in plan.perception_stages]
 
     dev = _Device(policy, capacity=cfg.store_capacity, lanes=lanes, agents=A,
-                  max_outputs=duration, max_frames=duration, clock=clock)
+                  max_outputs=duration, max_frames=duration, clock=clock, pp_perception=pp_p)
     store = dev.store
     ports = [_Port(e, policy, a, frame_source) for a, e in enumerate(envs)]
     emis = _Emissions(dev, policy, A)

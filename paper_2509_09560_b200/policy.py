@@ -142,7 +142,7 @@ class RefinementSession:
     """Device state of the toy policy: fp64 lanes, an fp64 ring, fp64 outputs."""
 
     def __init__(self, policy, *, capacity, lanes, agents, max_outputs, max_frames,
-                 p_stream, g_stream):
+                 p_stream, g_stream, pp_perception=1):
         import torch
         if agents != 1:
             raise ValueError("the refinement toy policy runs one agent per session")

@@ -1,0 +1,99 @@
+"""CPU checks of the DP plugin's host-side pieces and of the DP oracle wiring."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import dp_model
+from paper_2509_09560_b200 import diffusion as D
+
+
+def test_unet_layout_tiny_and_pusht():
+    for name in ("tiny", "pusht"):
+        cfg = D.PRESETS[name]
+        blocks = D.unet_blocks(cfg)
+        assert [b[0] for b in blocks] == ["down0.0", "down0.1", "down1.0", "down1.1", "down2.0",
+                                          "down2.1", "mid.0", "mid.1", "up0.0", "up0.1", "up1.0",
+                                          "up1.1"]
+        d0, d1, d2 = cfg.down_dims
+        assert blocks[8][1:] == (2 * d2, d1, 4) and blocks[10][1:] == (2 * d1, d0, 8)
+        offs, F = D.film_layout(cfg)
+        assert F == 2 * sum(b[2] for b in blocks)
+    cfg = D.PRESETS["pusht"]
+    assert cfg.gc_dim == 1028
+    # ~488 MB of bf16 conv weights streamed per step at PushT-img widths
+    assert 480e6 < D.unet_stream_bytes(cfg) < 500e6
+    assert 2.3e9 < D.unet_flops_per_sample(cfg) < 2.45e9
+
+
+@pytest.mark.parametrize("name", ["tiny", "pusht"])
+def test_scheduler_tables_match_oracle(name):
+    cfg = D.PRESETS[name]
+    tab = D.scheduler_tables(cfg)
+    ref = dp_model.Scheduler(cfg)
+    assert list(tab["timestep"]) == ref.timesteps
+    x = torch.randn(16, 2, dtype=torch.float64)
+    eps = torch.randn(16, 2, dtype=torch.float64)
+    z = torch.randn(16, 2, dtype=torch.float64)
+    for i in range(cfg.num_inference_steps):
+        x0 = ((x - tab["sqrt_1mab"][i] * eps) / tab["sqrt_ab"][i]).clamp(-1, 1)
+        got = tab["c_x0"][i] * x0 + tab["c_xt"][i] * x + tab["c_eps"][i] * eps + tab["sigma"][i] * z
+        want = ref.step(i, x, eps, z)
+        assert torch.allclose(got, want, rtol=1e-12, atol=1e-12)
+
+
+def test_request_noise_and_frames_match_oracle():
+    cfg = D.PRESETS["pusht"]
+    xT, z = D.request_noise(cfg, 3, 1, 17)
+    gen = dp_model.OracleGeneration({}, cfg, 3, 1, 1.0)
+    st = gen.initial_state(seed=17)
+    assert np.array_equal(xT, st.x.numpy()) and np.array_equal(z, st.z.numpy())
+    o1 = D.synthetic_frame(cfg, 3, 1, 17)
+    o2 = dp_model.synthetic_frame(cfg, 3, 1, 17)
+    assert np.array_equal(o1.image, o2.image) and np.array_equal(o1.vector, o2.vector)
+
+
+def test_oracle_resnet_trunk_matches_torchvision_wiring():
+    """Cross-check the restated encoder against torchvision's resnet18 with every
+    BatchNorm swapped for GroupNorm(C/16)."""
+    tv = pytest.importorskip("torchvision")
+    cfg = D.PRESETS["tiny"]
+    w = D.init_weights(cfg, seed=1)
+    net = tv.models.resnet18(weights=None)
+    net.fc = torch.nn.Identity()
+
+    def swap(mod):
+        for n, ch in mod.named_children():
+            if isinstance(ch, torch.nn.BatchNorm2d):
+                setattr(mod, n, torch.nn.GroupNorm(ch.num_features // 16, ch.num_features))
+            else:
+                swap(ch)
+    swap(net)
+    sd = {"conv1.weight": w["enc.conv1.w"], "bn1.weight": w["enc.gn1.g"], "bn1.bias": w["enc.gn1.b"]}
+    for li in range(1, 5):
+        for bi in range(2):
+            p, q = f"enc.layer{li}.{bi}", f"layer{li}.{bi}"
+            sd[q + ".conv1.weight"] = w[p + ".conv1.w"]
+            sd[q + ".bn1.weight"], sd[q + ".bn1.bias"] = w[p + ".gn1.g"], w[p + ".gn1.b"]
+            sd[q + ".conv2.weight"] = w[p + ".conv2.w"]
+            sd[q + ".bn2.weight"], sd[q + ".bn2.bias"] = w[p + ".gn2.g"], w[p + ".gn2.b"]
+            if p + ".ds.w" in w:
+                sd[q + ".downsample.0.weight"] = w[p + ".ds.w"]
+                sd[q + ".downsample.1.weight"] = w[p + ".dsgn.g"]
+                sd[q + ".downsample.1.bias"] = w[p + ".dsgn.b"]
+    net.load_state_dict(sd)
+    obs = D.synthetic_frame(cfg, 0, 0, 5)
+    with torch.no_grad():
+        ref = net(torch.from_numpy(obs.image).float()[None] * (2 / 255) - 1)[0]
+        got = dp_model.encode(w, obs.image, obs.vector)
+    assert torch.allclose(got[:512], ref, rtol=1e-4, atol=1e-5)
+
+
+def test_oracle_unet_runs_and_is_deterministic():
+    cfg = D.PRESETS["tiny"]
+    w = D.init_weights(cfg, seed=2)
+    gc = torch.randn(cfg.gc_dim)
+    x = torch.randn(cfg.horizon, cfg.action_dim)
+    e1 = dp_model.unet_eps(w, cfg, x, 42, gc)
+    e2 = dp_model.unet_eps(w, cfg, x, 42, gc)
+    assert e1.shape == (16, 2) and torch.isfinite(e1).all() and torch.equal(e1, e2)
