@@ -695,8 +695,11 @@ class DPGeneration:
 @dataclass(frozen=True)
 class DPPolicy(Policy):
     agents: int = 1
+    resident_frames: int = 0        # >0: synthetic inputs pre-staged in HBM, cycled mod N
 
     def synthetic_observation(self, agent, frame):
+        if self.resident_frames:
+            return Observation(frame=frame, vector=None, image=None)
         return synthetic_frame(self.generation.cfg, self.generation.seed, agent, frame)
 
 
@@ -768,8 +771,33 @@ class DPSession:
         self.version_log = torch.zeros(max(1, max_frames), dtype=torch.int64, device=dev)
         self.film_op = _lib.LinearOp(w=self.denoiser.film_o.data_ptr(), bias=0, M=self.denoiser.F,
                                      K=cfg.gc_dim, mish_in=1, ldw=self.gc_pad)
-        self.device_frames = None      # optional [frames, A, C, H, W] u8 resident source
+        self.resident = None
+        if getattr(policy, "resident_frames", 0):
+            self._stage_resident(policy.resident_frames)
+        self.instrument = False
+        self.gen_events = []
         torch.cuda.synchronize()
+
+    def _stage_resident(self, n):
+        """Pre-stage n frames of synthetic inputs (images, agent positions,
+        request noise) in HBM so a benchmark's timed region starts with its
+        inputs resident; ingest(t) then reads entry t % n."""
+        torch, cfg = self.torch, self.cfg
+        dev = self.x.device
+        imgs, pos, xs, zs = [], [], [], []
+        for f in range(n):
+            obs = [synthetic_frame(cfg, self.gen.seed, a, f) for a in range(self.A)]
+            imgs.append(np.stack([o.image for o in obs]))
+            pos.append(np.stack([np.asarray(o.vector, dtype=np.float32) for o in obs]))
+            noise = [request_noise(cfg, self.gen.seed, a, f) for a in range(self.A)]
+            xs.append(np.stack([x.reshape(-1) for x, _ in noise]))
+            if cfg.scheduler == "ddpm":
+                zs.append(np.stack([z.reshape(cfg.num_inference_steps, -1) for _, z in noise]))
+        self.resident = {"img": torch.from_numpy(np.stack(imgs)).to(dev),
+                         "pos": torch.from_numpy(np.stack(pos)).to(dev),
+                         "x": torch.from_numpy(np.stack(xs)).to(dev),
+                         "z": torch.from_numpy(np.stack(zs)).to(dev) if zs else None,
+                         "n": n}
 
     # -- ingest: frames to HBM, request randomness to its lane
     def ingest(self, t, lane, observations):
@@ -778,13 +806,20 @@ class DPSession:
         if len(observations) != self.A:
             raise ShapeMismatch(f"{len(observations)} observations for {self.A} agents")
         with torch.cuda.stream(self.p):
-            if self.device_frames is not None:
-                self.encoder.img.copy_(self.device_frames[t % self.device_frames.shape[0]], non_blocking=True)
-            else:
-                imgs = np.stack([o.image for o in observations])
-                if imgs.shape[1:] != (cfg.image_channels, cfg.image_hw, cfg.image_hw):
-                    raise ShapeMismatch(f"image shape {imgs.shape[1:]}")
-                self.encoder.img.copy_(torch.from_numpy(imgs).pin_memory(), non_blocking=True)
+            if observations[0].image is None:
+                if self.resident is None:
+                    raise ShapeMismatch("observation without an image and no resident inputs")
+                r, i = self.resident, t % self.resident["n"]
+                self.encoder.img.copy_(r["img"][i], non_blocking=True)
+                self.pos.copy_(r["pos"][i], non_blocking=True)
+                self.x[:, lane].copy_(r["x"][i], non_blocking=True)
+                if self.noise is not None:
+                    self.noise[:, lane].copy_(r["z"][i], non_blocking=True)
+                return
+            imgs = np.stack([o.image for o in observations])
+            if imgs.shape[1:] != (cfg.image_channels, cfg.image_hw, cfg.image_hw):
+                raise ShapeMismatch(f"image shape {imgs.shape[1:]}")
+            self.encoder.img.copy_(torch.from_numpy(imgs).pin_memory(), non_blocking=True)
             pos = np.stack([np.asarray(o.vector, dtype=np.float32) for o in observations])
             if pos.shape[1] != cfg.agent_pos_dim:
                 raise ShapeMismatch(f"agent_pos width {pos.shape[1]} != {cfg.agent_pos_dim}")
@@ -834,10 +869,17 @@ class DPSession:
             raise ConfigInvalid(f"{S} in-flight samples exceed the plan's {self.s_max}")
         iters = max(count)
         ia = _lib.int_array
+        if self.instrument:
+            e0 = self.torch.cuda.Event(enable_timing=True)
+            e0.record(self.g)
         _lib.check(self.lib.auras_unet_generate(
             self.plan, S, ia(lanes), ia(agents), ia(start), ia(count), iters, self.R,
             self.x.data_ptr(), _lib.ptr(self.noise), self.fetched.data_ptr(),
             int(self.gen.use_graph), self.g.cuda_stream), "unet_generate")
+        if self.instrument:
+            e1 = self.torch.cuda.Event(enable_timing=True)
+            e1.record(self.g)
+            self.gen_events.append((e0, e1, iters, S))
 
     def finish(self, lane, out_index):
         A = self.A
@@ -865,7 +907,8 @@ class DPSession:
 
 
 def make_diffusion_policy(config="pusht", dtype: str = "bf16", seed: int = 0, weights=None,
-                          agents: int = 1, use_graph: bool = True, **overrides) -> DPPolicy:
+                          agents: int = 1, use_graph: bool = True, resident_frames: int = 0,
+                          **overrides) -> DPPolicy:
     """Diffusion Policy CNN on the B200 behind the reference's Policy interface.
 
     `config`: a preset name ("tiny", "pusht", "dp_default") or a DPConfig.
@@ -884,4 +927,5 @@ def make_diffusion_policy(config="pusht", dtype: str = "bf16", seed: int = 0, we
     perception = DPPerception(layer_costs=tuple(gflop), obs_width=cfg.agent_pos_dim)
     generation = DPGeneration(cfg=cfg, dtype=dtype, seed=seed, weights=weights, step_cost=step_gflop,
                               use_graph=use_graph)
-    return DPPolicy(perception=perception, generation=generation, agents=agents)
+    return DPPolicy(perception=perception, generation=generation, agents=agents,
+                    resident_frames=resident_frames)

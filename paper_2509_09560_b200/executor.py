@@ -320,7 +320,7 @@ def _require_plugin(policy):
 # ---------------------------------------------------------------- pipelined mode
 
 def run_pipelined(cfg: PipelineConfig, policy, env, duration: int, *, clock: str = "virtual",
-                  agents: Optional[int] = None, frame_source=None) -> RunResult:
+                  agents: Optional[int] = None, frame_source=None, frame_hook=None) -> RunResult:
     """fp/executor.py:200-399 on the B200.  `env` may be one environment, a list
     (one per agent, batched into the same kernels), or None (synthetic
     observations from `frame_source(agent, frame)` when given)."""
@@ -359,6 +359,8 @@ def run_pipelined(cfg: PipelineConfig, policy, env, duration: int, *, clock: str
     now, skip = 0.0, 0
     window = max(4, lanes)
     for t in range(duration):
+        if frame_hook is not None:
+            frame_hook(t, dev, emis)
         dev.begin_frame(t, window)
         rec = _frame(t, now)
         obs = [port.boundary(t, emis.materialize) for port in ports]
@@ -485,6 +487,8 @@ def run_pipelined(cfg: PipelineConfig, policy, env, duration: int, *, clock: str
         dev.end_frame(t)
         trace.append(rec)
 
+    if frame_hook is not None:
+        frame_hook(duration, dev, emis)
     dev.synchronize()
     per_agent = emis.all()
     for rec_, em, r, k in emitted_rows:
@@ -521,7 +525,7 @@ def _apply_device_clock(dev, trace, records, emitted_rows):
 
 def run_sequential(policy, env, duration: int, frame_interval: Optional[float] = None, *,
                    clock: str = "virtual", agents: Optional[int] = None,
-                   frame_source=None) -> RunResult:
+                   frame_source=None, frame_hook=None) -> RunResult:
     """fp/executor.py:406-461 on the B200: one request at a time (depth 1);
     observations arriving while a request is in flight are dropped."""
     _require_plugin(policy)
@@ -545,6 +549,8 @@ def run_sequential(policy, env, duration: int, frame_interval: Optional[float] =
     free_at = 0
     n_layers = len(policy.perception.layers)
     for t in range(duration):
+        if frame_hook is not None:
+            frame_hook(t, dev, emis)
         dev.begin_frame(t, 4)
         now = t * interval
         rec = _frame(t, now)
@@ -585,6 +591,8 @@ def run_sequential(policy, env, duration: int, frame_interval: Optional[float] =
             port.seal()
         dev.end_frame(t)
         trace.append(rec)
+    if frame_hook is not None:
+        frame_hook(duration, dev, emis)
     dev.synchronize()
     per_agent = emis.all()
     for rec_, em, r, k in emitted_rows:
