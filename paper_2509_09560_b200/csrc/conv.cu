@@ -373,7 +373,7 @@ __global__ void dp_finish_kernel(const float *x, FinishBatch b, int n, int lanes
 }
 
 // ------------------------------------------------------------------ dispatch helpers
-int conv_op_to_args(const auras_conv_op &op, int S, float *partial, ConvGemmArgs &g, EpiArgs &e) {
+int conv_op_to_args(const auras_conv_op &op, int S, int dtype, float *partial, ConvGemmArgs &g, EpiArgs &e) {
   if (op.M <= 0 || op.Cin <= 0 || op.Kp <= 0 || op.splits <= 0 || op.kh <= 0 || op.kw <= 0) {
     set_error("conv op: bad shape M=%d Cin=%d Kp=%d splits=%d", op.M, op.Cin, op.Kp, op.splits);
     return AURAS_E_ARG;
@@ -385,10 +385,16 @@ int conv_op_to_args(const auras_conv_op &op, int S, float *partial, ConvGemmArgs
   g.Cin = op.Cin; g.H = op.H; g.W = op.W; g.in_pitch = op.in_pitch; g.in_coff = op.in_coff;
   g.kh = op.kh; g.kw = op.kw; g.stride = op.stride; g.pad_h = op.pad_h; g.pad_w = op.pad_w;
   g.Ho = op.Ho; g.Wo = op.Wo; g.splits = op.splits;
-  int kc = (op.Kp + op.splits - 1) / op.splits;
-  kc = (kc + 63) / 64 * 64;
-  g.kchunk = kc;
-  g.splits = (op.Kp + kc - 1) / kc;
+  if (dtype == AURAS_DT_BF16 && gemm_sm100_supported(g)) {
+    g.engine = 1;
+    g.splits = gemm_sm100_splits(g);
+    g.kchunk = 0;
+  } else {
+    int kc = (op.Kp + op.splits - 1) / op.splits;
+    kc = (kc + 63) / 64 * 64;
+    g.kchunk = kc;
+    g.splits = (op.Kp + kc - 1) / kc;
+  }
   e.partial = partial; e.bias = op.bias; e.gn_gamma = op.gn_gamma; e.gn_beta = op.gn_beta;
   e.res = op.res; e.res_f32 = op.res_f32; e.out = op.out; e.out_f32 = op.out_f32;
   e.M = op.M; e.N = g.N; e.Ho = op.Ho; e.Wo = op.Wo; e.splits = g.splits; e.groups = op.groups;
@@ -399,10 +405,8 @@ int conv_op_to_args(const auras_conv_op &op, int S, float *partial, ConvGemmArgs
 }
 
 int run_gemm(const ConvGemmArgs &g, int dtype, cudaStream_t st) {
-  if (dtype == AURAS_DT_BF16) {
-    if (gemm_sm100_supported(g)) return launch_gemm_sm100(g, st);
-    return launch_conv_gemm_simt<__nv_bfloat16>(g, st);
-  }
+  if (g.engine == 1) return launch_gemm_sm100(g, st);
+  if (dtype == AURAS_DT_BF16) return launch_conv_gemm_simt<__nv_bfloat16>(g, st);
   return launch_conv_gemm_simt<float>(g, st);
 }
 
@@ -411,11 +415,11 @@ int run_epilogue(const EpiArgs &e, int S, int dtype, cudaStream_t st) {
                                 : launch_conv_epilogue<float>(e, S, st);
 }
 
-int64_t conv_scratch_floats(const auras_conv_op &op, int S) {
-  int kc = (op.Kp + op.splits - 1) / op.splits;
-  kc = (kc + 63) / 64 * 64;
-  const int splits = (op.Kp + kc - 1) / kc;
-  return (int64_t)splits * S * op.Ho * op.Wo * op.M;
+int64_t conv_scratch_floats(const auras_conv_op &op, int S, int dtype) {
+  ConvGemmArgs g;
+  EpiArgs e;
+  if (conv_op_to_args(op, S, dtype, nullptr, g, e)) return 0;
+  return (int64_t)g.splits * S * op.Ho * op.Wo * op.M;
 }
 
 }  // namespace auras
@@ -427,10 +431,10 @@ extern "C" {
 int auras_conv(const auras_conv_op *op, int dtype, int S, const float *film_rows, int film_stride,
                float *scratch, int64_t scratch_floats, void *stream) {
   if (!op || !scratch) { set_error("conv: null"); return AURAS_E_ARG; }
-  if (conv_scratch_floats(*op, S) > scratch_floats) { set_error("conv: scratch too small"); return AURAS_E_ARG; }
+  if (conv_scratch_floats(*op, S, dtype) > scratch_floats) { set_error("conv: scratch too small"); return AURAS_E_ARG; }
   ConvGemmArgs g;
   EpiArgs e;
-  int rc = conv_op_to_args(*op, S, scratch, g, e);
+  int rc = conv_op_to_args(*op, S, dtype, scratch, g, e);
   if (rc) return rc;
   if (op->film_off >= 0) {
     if (!film_rows) { set_error("conv: FiLM op without film rows"); return AURAS_E_ARG; }

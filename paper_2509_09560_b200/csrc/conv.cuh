@@ -13,6 +13,7 @@ struct ConvGemmArgs {
   int kh, kw, stride, pad_h, pad_w;
   int Ho, Wo;
   int splits, kchunk;
+  int engine;         // 0 SIMT, 1 tcgen05
 };
 
 struct EpiArgs {
@@ -39,13 +40,14 @@ struct LinArgs {
   int M, K, ldw, mish_in, N, ldx, ldy;
 };
 
-int conv_op_to_args(const auras_conv_op &op, int S, float *partial, ConvGemmArgs &g, EpiArgs &e);
+int conv_op_to_args(const auras_conv_op &op, int S, int dtype, float *partial, ConvGemmArgs &g, EpiArgs &e);
 int run_gemm(const ConvGemmArgs &g, int dtype, cudaStream_t st);
 int run_epilogue(const EpiArgs &e, int S, int dtype, cudaStream_t st);
-int64_t conv_scratch_floats(const auras_conv_op &op, int S);
+int64_t conv_scratch_floats(const auras_conv_op &op, int S, int dtype);
 
 // tcgen05 / TMA engine (gemm_sm100.cu)
 bool gemm_sm100_supported(const ConvGemmArgs &g);
+int gemm_sm100_splits(const ConvGemmArgs &g);
 int launch_gemm_sm100(const ConvGemmArgs &g, cudaStream_t st);
 
 }  // namespace auras

@@ -8,6 +8,7 @@
 // the 1x1 output conv and the DDPM/DDIM update and writes x_{t-1} back to the
 // request lane (GenerationModel.step, fp/policy.py:217-228, for a neural
 // policy).  The chain can be captured once per (S, iters) into a CUDA graph.
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <utility>
@@ -30,17 +31,24 @@ struct UnetCtrl {             // per-frame control, uploaded by value
 
 struct UnetDev {              // device-resident per-sample state
   UnetCtrl ctrl;
+  int r;                      // iteration index within the frame, advanced in-graph
   int tau_row[kMaxS];
   int64_t film_b_off[kMaxS];
 };
 
-__global__ void unet_set_ctrl(UnetDev *dev, UnetCtrl c) { dev->ctrl = c; }
+__global__ void unet_set_ctrl(UnetDev *dev, UnetCtrl c) {
+  dev->ctrl = c;
+  dev->r = 0;
+}
+
+__global__ void unet_advance(UnetDev *dev) { dev->r += 1; }
 
 template <typename T>
-__global__ void unet_prep(UnetDev *dev, int r, auras_sched sch, int horizon, int adim, T *xin,
+__global__ void unet_prep(UnetDev *dev, auras_sched sch, int horizon, int adim, T *xin,
                           int x_pitch, int64_t ring_slot_stride, int64_t ring_agent_stride) {
   const int s = blockIdx.x;
   const UnetCtrl &c = dev->ctrl;
+  const int r = dev->r;
   const int agent = c.agents[s], lane = c.lanes[s];
   int i = c.start[s] + r;
   i = i < sch.n_steps ? i : sch.n_steps - 1;
@@ -59,11 +67,12 @@ __global__ void unet_prep(UnetDev *dev, int r, auras_sched sch, int horizon, int
 
 // eps = W_out . y + b (1x1 conv to action_dim) then the scheduler update.
 template <typename T>
-__global__ void unet_final(UnetDev *dev, int r, auras_sched sch, int horizon, int adim, const T *y,
+__global__ void unet_final(UnetDev *dev, auras_sched sch, int horizon, int adim, const T *y,
                            int y_pitch, int cin, const float *wf, const float *bf) {
   __shared__ float eps[512];
   const int s = blockIdx.x;
   const UnetCtrl &c = dev->ctrl;
+  const int r = dev->r;
   const int lane_id = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int o = wid; o < horizon * adim; o += nw) {
     const int t = o / adim, a = o - t * adim;
@@ -109,24 +118,25 @@ struct auras_unet_plan {
   float *partial = nullptr;
   int64_t partial_floats = 0;
   UnetDev *dev = nullptr;
-  std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
+  std::map<int, cudaGraphExec_t> graphs;     // one denoise step per batch size S
 };
 
-static int unet_launch_chain(auras_unet_plan *p, int S, int iters, cudaStream_t st) {
-  for (int r = 0; r < iters; ++r) {
+// One denoise step for S samples: prep -> (GEMM, epilogue) x ops -> final -> advance.
+static int unet_launch_step(auras_unet_plan *p, int S, cudaStream_t st) {
+  {
     if (p->dtype == AURAS_DT_BF16)
-      unet_prep<__nv_bfloat16><<<S, 128, 0, st>>>(p->dev, r, p->sched, p->horizon, p->adim,
+      unet_prep<__nv_bfloat16><<<S, 128, 0, st>>>(p->dev, p->sched, p->horizon, p->adim,
                                                   static_cast<__nv_bfloat16 *>(p->x_in), p->x_pitch,
                                                   p->ring_slot_stride, p->ring_agent_stride);
     else
-      unet_prep<float><<<S, 128, 0, st>>>(p->dev, r, p->sched, p->horizon, p->adim,
+      unet_prep<float><<<S, 128, 0, st>>>(p->dev, p->sched, p->horizon, p->adim,
                                           static_cast<float *>(p->x_in), p->x_pitch, p->ring_slot_stride,
                                           p->ring_agent_stride);
     AURAS_LAUNCHED("unet_prep");
     for (const auras_conv_op &op : p->ops) {
       ConvGemmArgs g;
       EpiArgs e;
-      int rc = conv_op_to_args(op, S, p->partial, g, e);
+      int rc = conv_op_to_args(op, S, p->dtype, p->partial, g, e);
       if (rc) return rc;
       if (op.film_off >= 0) {
         e.film_a = p->film_tau;
@@ -140,14 +150,16 @@ static int unet_launch_chain(auras_unet_plan *p, int S, int iters, cudaStream_t 
     }
     const auras_conv_op &last = p->ops.back();
     if (p->dtype == AURAS_DT_BF16)
-      unet_final<__nv_bfloat16><<<S, 256, 0, st>>>(p->dev, r, p->sched, p->horizon, p->adim,
+      unet_final<__nv_bfloat16><<<S, 256, 0, st>>>(p->dev, p->sched, p->horizon, p->adim,
                                                    static_cast<const __nv_bfloat16 *>(last.out), last.out_pitch,
                                                    p->final_cin, p->final_w, p->final_b);
     else
-      unet_final<float><<<S, 256, 0, st>>>(p->dev, r, p->sched, p->horizon, p->adim,
+      unet_final<float><<<S, 256, 0, st>>>(p->dev, p->sched, p->horizon, p->adim,
                                            static_cast<const float *>(last.out), last.out_pitch, p->final_cin,
                                            p->final_w, p->final_b);
     AURAS_LAUNCHED("unet_final");
+    unet_advance<<<1, 1, 0, st>>>(p->dev);
+    AURAS_LAUNCHED("unet_advance");
   }
   return AURAS_OK;
 }
@@ -182,7 +194,8 @@ auras_unet_plan *auras_unet_plan_create(const auras_conv_op *ops, int n_ops, int
   p->x_in = x_in_buffer;
   p->x_pitch = x_in_pitch;
   for (const auto &op : p->ops) {
-    const int64_t f = conv_scratch_floats(op, s_max);
+    int64_t f = 0;
+    for (int s = 1; s <= s_max; ++s) f = std::max(f, conv_scratch_floats(op, s, dtype));
     if (f > p->partial_floats) p->partial_floats = f;
   }
   if (cudaMalloc(&p->partial, sizeof(float) * p->partial_floats) != cudaSuccess ||
@@ -232,14 +245,18 @@ int auras_unet_generate(auras_unet_plan *p, int S, const int *lanes, const int *
   c.lanes_per_agent = lanes_per_agent;
   unet_set_ctrl<<<1, 1, 0, st>>>(p->dev, c);
   AURAS_LAUNCHED("unet_set_ctrl");
-  if (!use_graph) return unet_launch_chain(p, S, iters, st);
-
-  auto key = std::make_pair(S, iters);
-  auto it = p->graphs.find(key);
+  if (!use_graph) {
+    for (int r = 0; r < iters; ++r) {
+      int rc = unet_launch_step(p, S, st);
+      if (rc) return rc;
+    }
+    return AURAS_OK;
+  }
+  auto it = p->graphs.find(S);
   if (it == p->graphs.end()) {
     cudaGraph_t g;
     AURAS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    int rc = unet_launch_chain(p, S, iters, st);
+    int rc = unet_launch_step(p, S, st);
     cudaError_t ce = cudaStreamEndCapture(st, &g);
     if (rc) return rc;
     AURAS_CUDA(ce);
@@ -247,9 +264,10 @@ int auras_unet_generate(auras_unet_plan *p, int S, const int *lanes, const int *
     ce = cudaGraphInstantiate(&ge, g, 0);
     cudaGraphDestroy(g);
     AURAS_CUDA(ce);
-    it = p->graphs.emplace(key, ge).first;
+    AURAS_CUDA(cudaGraphUpload(ge, st));
+    it = p->graphs.emplace(S, ge).first;
   }
-  AURAS_CUDA(cudaGraphLaunch(it->second, st));
+  for (int r = 0; r < iters; ++r) AURAS_CUDA(cudaGraphLaunch(it->second, st));
   return AURAS_OK;
 }
 
