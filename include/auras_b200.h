@@ -183,6 +183,12 @@ int auras_unet_generate(auras_unet_plan *plan, int S, const int *lanes, const in
                         float *x_lanes, const float *noise_lanes, const int64_t *fetched,
                         int use_graph, void *stream);
 
+/* Diagnostics: per-task globaltimer trace of the persistent denoise
+ * megakernel for batch size S (trace: int64[n_tasks][8]; tasks_out:
+ * int32[n_tasks][4] task table or NULL).  Returns n_tasks or < 0. */
+int auras_unet_mega_trace(auras_unet_plan *plan, int S, long long *trace, int *tasks_out,
+                          int max_tasks);
+
 /* One conv op (standalone; used by the perception encoder and by tests). */
 int auras_conv(const auras_conv_op *op, int dtype, int S, const float *film_rows,
                int film_stride, float *scratch, int64_t scratch_floats, void *stream);

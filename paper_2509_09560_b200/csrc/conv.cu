@@ -9,11 +9,12 @@
 
 #include "common.cuh"
 #include "conv.cuh"
+#include "epi.cuh"
 
 namespace auras {
 
 // ------------------------------------------------------------------ GEMM (SIMT)
-// partial[split][n][m] = sum_{k in split} W[m][k] * B[n][k]
+// partial[split][m][n] = sum_{k in split} W[m][k] * B[n][k]
 // B[n][k] = in[s, oy*st-ph+ky, ox*st-pw+kx, c]; n=(s,oy,ox), k=((ky*kw+kx)*Cin + c)
 constexpr int SB_M = 64, SB_N = 64, SB_K = 32;
 
@@ -83,7 +84,7 @@ __global__ void __launch_bounds__(256) conv_gemm_simt(ConvGemmArgs a) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int m = m0 + tx * 4 + i;
-      if (m < a.M) out[(int64_t)n * a.M + m] = acc[i][j];
+      if (m < a.M) out[(int64_t)m * a.N + n] = acc[i][j];
     }
   }
 }
@@ -97,94 +98,10 @@ int launch_conv_gemm_simt(const ConvGemmArgs &a, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ epilogue
-// One CTA per (sample, GroupNorm group) -- or per (sample, 64-channel block)
-// without GroupNorm.  Three passes over the L2-resident partials:
-//   1) v = bias + sum_split partial  (written back in place), group sum
-//   2) group variance around the mean
-//   3) normalise, affine, activation, FiLM, residual, store (stuffed/pooled)
 template <typename T>
 __global__ void __launch_bounds__(512) conv_epilogue(EpiArgs a) {
   __shared__ float red[32];
-  const int s = blockIdx.x;
-  const bool gn = a.gn_gamma != nullptr;
-  const int cg = gn ? a.M / a.groups : min(64, a.M - blockIdx.y * 64);
-  const int c0 = gn ? blockIdx.y * cg : blockIdx.y * 64;
-  const int P = a.Ho * a.Wo;
-  const int cnt = cg * P;
-  float *base = a.partial;
-  const int64_t NM = (int64_t)a.N * a.M;
-
-  float lsum = 0.f;
-  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-    const int p = i / cg, c = c0 + (i - p * cg);
-    const int64_t off = (int64_t)(s * P + p) * a.M + c;
-    float v = a.bias ? a.bias[c] : 0.f;
-    for (int z = 0; z < a.splits; ++z) v += base[z * NM + off];
-    base[off] = v;
-    lsum += v;
-  }
-  float mean = 0.f, rstd = 1.f;
-  if (gn) {
-    mean = block_sum(lsum, red) / cnt;
-    float lsq = 0.f;
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-      const int p = i / cg, c = c0 + (i - p * cg);
-      const float d = base[(int64_t)(s * P + p) * a.M + c] - mean;
-      lsq += d * d;
-    }
-    const float var = block_sum(lsq, red) / cnt;
-    rstd = rsqrtf(var + 1e-5f);
-  } else {
-    __syncthreads();
-  }
-
-  T *out = static_cast<T *>(a.out);
-  const T *res = static_cast<const T *>(a.res);
-  const float *fa = nullptr, *fb = nullptr;
-  if (a.film_off >= 0) {
-    const int ra = a.film_a_row ? a.film_a_row[s] : s;
-    fa = a.film_a + (int64_t)ra * a.film_a_stride + a.film_off;
-    if (a.film_b) fb = a.film_b + a.film_b_off[s] + a.film_off;
-  }
-  const int wout = a.out_stuff ? 2 * a.Wo : a.Wo;
-  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-    const int p = i / cg, cc = i - p * cg, c = c0 + cc;
-    const int64_t row = (int64_t)(s * P + p);
-    float y = base[row * a.M + c];
-    if (gn) y = (y - mean) * rstd * a.gn_gamma[c] + a.gn_beta[c];
-    const int oy = p / a.Wo, ox = p - oy * a.Wo;
-    float r = 0.f;
-    if (res) {
-      r = Elem<T>::load(res + ((int64_t)(s * a.Ho + oy) * a.Wo + ox) * a.res_pitch + a.res_coff + c);
-    } else if (a.res_f32) {
-      r = a.res_f32[row * a.M + c];
-    }
-    if (a.res_before_act) y += r;
-    y = activate(y, a.act);
-    if (fa) {
-      float sc = fa[c], bi = fa[a.M + c];
-      if (fb) { sc += fb[c]; bi += fb[a.M + c]; }
-      y = y * sc + bi;
-    }
-    if (!a.res_before_act) y += r;
-    if (a.out_f32 && !a.pool_out) a.out_f32[row * a.M + c] = y;
-    if (a.pool_out) {
-      base[row * a.M + c] = y;          // staged for the fixed-order pooling below
-    } else if (out) {
-      const int ox2 = a.out_stuff ? 2 * ox : ox;
-      T *dst = out + ((int64_t)(s * a.Ho + oy) * wout + ox2) * a.out_pitch + a.out_coff + c;
-      Elem<T>::store(dst, y);
-      if (a.out_stuff) Elem<T>::store(dst + a.out_pitch, 0.f);
-    }
-  }
-  if (a.pool_out) {                    // deterministic global average pool
-    __syncthreads();
-    for (int i = threadIdx.x; i < cg; i += blockDim.x) {
-      float acc = 0.f;
-      for (int p = 0; p < P; ++p) acc += base[(int64_t)(s * P + p) * a.M + c0 + i];
-      a.out_f32[(int64_t)s * a.M + c0 + i] = acc / P;
-    }
-  }
+  epi_unit<T>(a, blockIdx.x, blockIdx.y, threadIdx.x, blockDim.x, red, [] __device__() { __syncthreads(); });
 }
 
 template <typename T>

@@ -1,0 +1,48 @@
+// Host interface of the persistent denoise megakernel (unet_mega.cu).
+#pragma once
+#include <vector>
+
+#include "conv.cuh"
+#include "unet.cuh"
+
+namespace auras {
+
+struct MegaOp;
+struct MegaParams {
+  const MegaOp *ops;
+  const int4 *tasks;
+  const int *cta_begin;
+  int *ctr;
+  int n_ops, S;
+  UnetDev *dev;
+  auras_sched sched;
+  int horizon, adim;
+  __nv_bfloat16 *xin;
+  int x_pitch;
+  int64_t ring_slot_stride, ring_agent_stride;
+  const __nv_bfloat16 *y_final;
+  int y_pitch, final_cin;
+  const float *wf, *bf;
+  long long *trace;         // optional [n_tasks][4] globaltimer stamps (NULL = off)
+};
+
+struct MegaConfig {
+  MegaOp *ops = nullptr;
+  int4 *tasks = nullptr;
+  int *cta_begin = nullptr;
+  int *ctr = nullptr;
+  float *partials = nullptr;
+  int n_ops = 0, n_tasks = 0, grid = 0, S = 0;
+  MegaParams params;
+};
+
+MegaParams mega_base_params(UnetDev *dev, const auras_sched &sched, int horizon, int adim, void *xin, int x_pitch,
+                            int64_t slot_stride, int64_t agent_stride, const void *y_final, int y_pitch, int cin,
+                            const float *wf, const float *bf);
+int mega_build(MegaConfig &mc, const std::vector<auras_conv_op> &ops, int S, const void *x_in, int x_pitch,
+               const MegaParams &base, const float *film_tau, int film_width, const float *ring_film);
+int mega_launch(const MegaConfig &mc, cudaStream_t st);
+int mega_set_trace(MegaConfig &mc, long long *trace);
+void mega_free(MegaConfig &mc);
+
+}  // namespace auras

@@ -9,6 +9,7 @@
 // request lane (GenerationModel.step, fp/policy.py:217-228, for a neural
 // policy).  The chain can be captured once per (S, iters) into a CUDA graph.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <utility>
@@ -16,25 +17,10 @@
 
 #include "common.cuh"
 #include "conv.cuh"
+#include "unet.cuh"
+#include "mega.cuh"
 
 namespace auras {
-
-constexpr int kMaxS = 64;
-
-struct UnetCtrl {             // per-frame control, uploaded by value
-  int lanes[kMaxS], agents[kMaxS], start[kMaxS], count[kMaxS];
-  float *x_lanes;
-  const float *noise_lanes;
-  const int64_t *fetched;
-  int S, lanes_per_agent;
-};
-
-struct UnetDev {              // device-resident per-sample state
-  UnetCtrl ctrl;
-  int r;                      // iteration index within the frame, advanced in-graph
-  int tau_row[kMaxS];
-  int64_t film_b_off[kMaxS];
-};
 
 __global__ void unet_set_ctrl(UnetDev *dev, UnetCtrl c) {
   dev->ctrl = c;
@@ -44,62 +30,18 @@ __global__ void unet_set_ctrl(UnetDev *dev, UnetCtrl c) {
 __global__ void unet_advance(UnetDev *dev) { dev->r += 1; }
 
 template <typename T>
-__global__ void unet_prep(UnetDev *dev, auras_sched sch, int horizon, int adim, T *xin,
-                          int x_pitch, int64_t ring_slot_stride, int64_t ring_agent_stride) {
-  const int s = blockIdx.x;
-  const UnetCtrl &c = dev->ctrl;
-  const int r = dev->r;
-  const int agent = c.agents[s], lane = c.lanes[s];
-  int i = c.start[s] + r;
-  i = i < sch.n_steps ? i : sch.n_steps - 1;
-  if (threadIdx.x == 0) {
-    dev->tau_row[s] = sch.timestep[i];
-    const int64_t slot = c.fetched[0];   // one ring version schedule per lock-stepped agent group
-    dev->film_b_off[s] = agent * ring_agent_stride + slot * ring_slot_stride;
-  }
-  const float *x = c.x_lanes + ((int64_t)agent * c.lanes_per_agent + lane) * horizon * adim;
-  for (int e = threadIdx.x; e < horizon * x_pitch; e += blockDim.x) {
-    const int t = e / x_pitch, ch = e - t * x_pitch;
-    const float v = ch < adim ? x[t * adim + ch] : 0.f;
-    Elem<T>::store(xin + ((int64_t)s * horizon + t) * x_pitch + ch, v);
-  }
+__global__ void unet_prep(UnetDev *dev, auras_sched sch, int horizon, int adim, T *xin, int x_pitch,
+                          int64_t ring_slot_stride, int64_t ring_agent_stride) {
+  prep_body<T>(dev, blockIdx.x, threadIdx.x, blockDim.x, sch, horizon, adim, xin, x_pitch, ring_slot_stride,
+               ring_agent_stride);
 }
 
-// eps = W_out . y + b (1x1 conv to action_dim) then the scheduler update.
 template <typename T>
-__global__ void unet_final(UnetDev *dev, auras_sched sch, int horizon, int adim, const T *y,
-                           int y_pitch, int cin, const float *wf, const float *bf) {
+__global__ void unet_final(UnetDev *dev, auras_sched sch, int horizon, int adim, const T *y, int y_pitch, int cin,
+                           const float *wf, const float *bf) {
   __shared__ float eps[512];
-  const int s = blockIdx.x;
-  const UnetCtrl &c = dev->ctrl;
-  const int r = dev->r;
-  const int lane_id = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int o = wid; o < horizon * adim; o += nw) {
-    const int t = o / adim, a = o - t * adim;
-    const T *yr = y + ((int64_t)s * horizon + t) * y_pitch;
-    float acc = 0.f;
-    for (int k = lane_id; k < cin; k += 32) acc = fmaf(wf[a * cin + k], Elem<T>::load(yr + k), acc);
-    acc = warp_sum(acc);
-    if (lane_id == 0) eps[o] = acc + bf[a];
-  }
-  __syncthreads();
-  if (r >= c.count[s]) return;                        // sample finished its share this frame
-  const int i = c.start[s] + r;
-  const int agent = c.agents[s], lane = c.lanes[s];
-  float *x = c.x_lanes + ((int64_t)agent * c.lanes_per_agent + lane) * horizon * adim;
-  const float *z = c.noise_lanes
-                       ? c.noise_lanes + (((int64_t)agent * c.lanes_per_agent + lane) * sch.n_steps + i) * horizon * adim
-                       : nullptr;
-  const float sab = sch.sqrt_ab[i], s1m = sch.sqrt_1mab[i];
-  const float cx0 = sch.c_x0[i], cxt = sch.c_xt[i], ceps = sch.c_eps[i], sig = sch.sigma[i];
-  for (int e = threadIdx.x; e < horizon * adim; e += blockDim.x) {
-    const float xt = x[e], ep = eps[e];
-    float x0 = (xt - s1m * ep) / sab;
-    if (sch.clip_sample) x0 = fminf(fmaxf(x0, -1.f), 1.f);
-    float nx = cx0 * x0 + cxt * xt + ceps * ep;
-    if (sch.ddpm && z) nx += sig * z[e];
-    x[e] = nx;
-  }
+  final_body<T>(dev, blockIdx.x, threadIdx.x, blockDim.x, sch, horizon, adim, y, y_pitch, cin, wf, bf, eps,
+                [] __device__() { __syncthreads(); });
 }
 
 }  // namespace auras
@@ -119,7 +61,36 @@ struct auras_unet_plan {
   int64_t partial_floats = 0;
   UnetDev *dev = nullptr;
   std::map<int, cudaGraphExec_t> graphs;     // one denoise step per batch size S
+  bool use_mega = false;                     // persistent megakernel (bf16, tcgen05 engine)
+  std::map<int, MegaConfig> mega;
 };
+
+// One denoise step through the persistent megakernel (unet_mega.cu).
+static int unet_mega_step(auras_unet_plan *p, int S, cudaStream_t st) {
+  auto it = p->mega.find(S);
+  if (it == p->mega.end()) { set_error("megakernel config for S=%d not built", S); return AURAS_E_ARG; }
+  int rc = mega_launch(it->second, st);
+  if (rc) return rc;
+  unet_advance<<<1, 1, 0, st>>>(p->dev);
+  AURAS_LAUNCHED("unet_advance");
+  return AURAS_OK;
+}
+
+static int unet_ensure_mega(auras_unet_plan *p, int S) {
+  if (!p->use_mega || p->mega.count(S)) return AURAS_OK;
+  const auras_conv_op &last = p->ops.back();
+  MegaParams base = mega_base_params(p->dev, p->sched, p->horizon, p->adim, p->x_in, p->x_pitch, p->ring_slot_stride,
+                                     p->ring_agent_stride, last.out, last.out_pitch, p->final_cin, p->final_w,
+                                     p->final_b);
+  MegaConfig mc;
+  int rc = mega_build(mc, p->ops, S, p->x_in, p->x_pitch, base, p->film_tau, p->film_width, p->ring_film);
+  if (rc) {
+    mega_free(mc);
+    return rc;
+  }
+  p->mega.emplace(S, mc);
+  return AURAS_OK;
+}
 
 // One denoise step for S samples: prep -> (GEMM, epilogue) x ops -> final -> advance.
 static int unet_launch_step(auras_unet_plan *p, int S, cudaStream_t st) {
@@ -198,6 +169,15 @@ auras_unet_plan *auras_unet_plan_create(const auras_conv_op *ops, int n_ops, int
     for (int s = 1; s <= s_max; ++s) f = std::max(f, conv_scratch_floats(op, s, dtype));
     if (f > p->partial_floats) p->partial_floats = f;
   }
+  p->use_mega = false;
+  if (dtype == AURAS_DT_BF16 && !getenv("AURAS_NO_MEGA")) {
+    p->use_mega = true;
+    for (const auto &op : p->ops) {
+      ConvGemmArgs g;
+      EpiArgs e;
+      if (conv_op_to_args(op, 1, dtype, nullptr, g, e) || g.engine != 1) p->use_mega = false;
+    }
+  }
   if (cudaMalloc(&p->partial, sizeof(float) * p->partial_floats) != cudaSuccess ||
       cudaMalloc(&p->dev, sizeof(UnetDev)) != cudaSuccess ||
       cudaMemset(p->dev, 0, sizeof(UnetDev)) != cudaSuccess) {
@@ -210,6 +190,7 @@ auras_unet_plan *auras_unet_plan_create(const auras_conv_op *ops, int n_ops, int
 
 void auras_unet_plan_destroy(auras_unet_plan *p) {
   if (!p) return;
+  for (auto &kv : p->mega) mega_free(kv.second);
   for (auto &kv : p->graphs) cudaGraphExecDestroy(kv.second);
   if (p->partial) cudaFree(p->partial);
   if (p->dev) cudaFree(p->dev);
@@ -243,11 +224,14 @@ int auras_unet_generate(auras_unet_plan *p, int S, const int *lanes, const int *
   c.fetched = fetched;
   c.S = S;
   c.lanes_per_agent = lanes_per_agent;
+  int rc0 = unet_ensure_mega(p, S);
+  if (rc0) return rc0;
+  auto step = p->use_mega ? unet_mega_step : unet_launch_step;
   unet_set_ctrl<<<1, 1, 0, st>>>(p->dev, c);
   AURAS_LAUNCHED("unet_set_ctrl");
   if (!use_graph) {
     for (int r = 0; r < iters; ++r) {
-      int rc = unet_launch_step(p, S, st);
+      int rc = step(p, S, st);
       if (rc) return rc;
     }
     return AURAS_OK;
@@ -256,7 +240,7 @@ int auras_unet_generate(auras_unet_plan *p, int S, const int *lanes, const int *
   if (it == p->graphs.end()) {
     cudaGraph_t g;
     AURAS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    int rc = unet_launch_step(p, S, st);
+    int rc = step(p, S, st);
     cudaError_t ce = cudaStreamEndCapture(st, &g);
     if (rc) return rc;
     AURAS_CUDA(ce);
@@ -269,6 +253,27 @@ int auras_unet_generate(auras_unet_plan *p, int S, const int *lanes, const int *
   }
   for (int r = 0; r < iters; ++r) AURAS_CUDA(cudaGraphLaunch(it->second, st));
   return AURAS_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// Diagnostics: enable a per-task globaltimer trace for the megakernel of batch
+// size S (buffer: int64[n_tasks][8]); returns n_tasks, copies the task table
+// (int32[n_tasks][4]) to `tasks_out` when non-NULL.  Graphs captured before the
+// call keep their old parameters, so call it before the first generate.
+int auras_unet_mega_trace(auras_unet_plan *p, int S, long long *trace, int *tasks_out, int max_tasks) {
+  if (!p || !p->use_mega) { set_error("megakernel not in use"); return AURAS_E_ARG; }
+  int rc = unet_ensure_mega(p, S);
+  if (rc) return rc;
+  MegaConfig &mc = p->mega[S];
+  if (tasks_out) {
+    if (mc.n_tasks > max_tasks) { set_error("task buffer too small"); return AURAS_E_ARG; }
+    AURAS_CUDA(cudaMemcpy(tasks_out, mc.tasks, sizeof(int4) * mc.n_tasks, cudaMemcpyDeviceToHost));
+  }
+  mega_set_trace(mc, trace);
+  return mc.n_tasks;
 }
 
 }  // extern "C"
