@@ -99,6 +99,9 @@ class ClockSampler:
         self.thread = None
 
     def start(self):
+        if os.environ.get("AURAS_BENCH_NO_CLOCKS") == "1":
+            self.error = "disabled by AURAS_BENCH_NO_CLOCKS"
+            return
         try:
             import pynvml
             pynvml.nvmlInit()

@@ -32,10 +32,13 @@ template <> struct Elem<__nv_bfloat16> {
   static __device__ __forceinline__ void store(__nv_bfloat16 *p, float v) { *p = __float2bfloat16_rn(v); }
 };
 
-// Mish(x) = x * tanh(softplus(x)); softplus with torch's threshold of 20.
+// Mish(x) = x * tanh(softplus(x)).  With e = exp(x):
+// tanh(log(1 + e)) = (e^2 + 2e) / (e^2 + 2e + 2)  -- one exp, one division.
 __device__ __forceinline__ float mish(float x) {
-  float sp = x > 20.f ? x : log1pf(expf(x));
-  return x * tanhf(sp);
+  if (x > 20.f) return x;                     // torch's softplus threshold
+  const float e = __expf(x);
+  const float n = e * (e + 2.f);
+  return x * __fdividef(n, n + 2.f);
 }
 
 __device__ __forceinline__ float activate(float v, int act) {

@@ -27,15 +27,21 @@ __device__ __forceinline__ float unit_sum(float v, float *red, int tid, int nthr
 // load the unit needs -- partials of all splits (float4), bias, GroupNorm
 // affine, FiLM rows, residual -- is issued in one round, statistics come from
 // registers, then one store pass.  Partials are [split][m][n], n = s*P + p.
-template <typename T, typename Sync>
+template <typename T, typename Sync, typename Gate>
 __device__ __forceinline__ void epi_unit_regs(const EpiArgs &a, int s, int gy, int tid, int nthr, float *red,
-                                              Sync sync) {
+                                              Sync sync, Gate gate, long long *stamp = nullptr) {
   constexpr int U = 4;
   const bool gn = a.gn_gamma != nullptr;
   const int cg = gn ? a.M / a.groups : min(64, a.M - gy * 64);
   const int c0 = gn ? gy * cg : gy * 64;
   const int P = a.Ho * a.Wo, P4 = P >> 2;
   const int cnt4 = cg * P4;
+  // R lanes share one float4 vector when there are fewer vectors than threads;
+  // each lane sums every R-th split, a butterfly combines them (fixed order).
+  int R = 1;
+  while (R < 8 && cnt4 * R * 2 <= nthr) R <<= 1;
+  const int lane_r = tid & (R - 1);
+  const int vt = tid / R, vstride = nthr / R;
   const float *base = a.partial;
   const int64_t NM = (int64_t)a.N * a.M;
   const float *fa = nullptr, *fb = nullptr;
@@ -48,16 +54,18 @@ __device__ __forceinline__ void epi_unit_regs(const EpiArgs &a, int s, int gy, i
   float v[U][4], rv[U][4];
   float gam[U], bet[U], sc[U], bi[U];
   int cc_[U], p0_[U];
+  bool ok_[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    const int vi = tid + u * nthr;
+    const int vi = vt + u * vstride;
     const bool ok = vi < cnt4;
+    ok_[u] = ok;
     const int cc = ok ? vi / P4 : 0;
     const int p0 = ok ? (vi - cc * P4) * 4 : 0;
     const int c = c0 + cc;
     cc_[u] = cc;
     p0_[u] = p0;
-    const float b0 = (ok && a.bias) ? a.bias[c] : 0.f;
+    const float b0 = (ok && a.bias && lane_r == 0) ? a.bias[c] : 0.f;
 #pragma unroll
     for (int q = 0; q < 4; ++q) v[u][q] = b0;
     gam[u] = (ok && gn) ? a.gn_gamma[c] : 1.f;
@@ -80,40 +88,71 @@ __device__ __forceinline__ void epi_unit_regs(const EpiArgs &a, int s, int gy, i
       rv[u][q] = r;
     }
   }
-  for (int z = 0; z < a.splits; ++z) {
+  gate();          // everything above is independent of this layer's GEMMs; partials are not
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (tid + u * nthr < cnt4) {
-        const float4 t = *reinterpret_cast<const float4 *>(base + z * NM + (int64_t)(c0 + cc_[u]) * a.N +
-                                                           (int64_t)s * P + p0_[u]);
-        v[u][0] += t.x; v[u][1] += t.y; v[u][2] += t.z; v[u][3] += t.w;
-      }
+  for (int u = 0; u < U; ++u) {
+    if (!ok_[u]) continue;
+    const float *col = base + (int64_t)(c0 + cc_[u]) * a.N + (int64_t)s * P + p0_[u];
+    int z = lane_r;
+    for (; z + 7 * R < a.splits; z += 8 * R) {          // 8 independent float4 loads in flight
+      float4 t[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) t[j] = *reinterpret_cast<const float4 *>(col + (z + j * R) * NM);
+      v[u][0] += ((t[0].x + t[1].x) + (t[2].x + t[3].x)) + ((t[4].x + t[5].x) + (t[6].x + t[7].x));
+      v[u][1] += ((t[0].y + t[1].y) + (t[2].y + t[3].y)) + ((t[4].y + t[5].y) + (t[6].y + t[7].y));
+      v[u][2] += ((t[0].z + t[1].z) + (t[2].z + t[3].z)) + ((t[4].z + t[5].z) + (t[6].z + t[7].z));
+      v[u][3] += ((t[0].w + t[1].w) + (t[2].w + t[3].w)) + ((t[4].w + t[5].w) + (t[6].w + t[7].w));
+    }
+    for (; z + 3 * R < a.splits; z += 4 * R) {
+      const float4 t0 = *reinterpret_cast<const float4 *>(col + z * NM);
+      const float4 t1 = *reinterpret_cast<const float4 *>(col + (z + R) * NM);
+      const float4 t2 = *reinterpret_cast<const float4 *>(col + (z + 2 * R) * NM);
+      const float4 t3 = *reinterpret_cast<const float4 *>(col + (z + 3 * R) * NM);
+      v[u][0] += (t0.x + t1.x) + (t2.x + t3.x);
+      v[u][1] += (t0.y + t1.y) + (t2.y + t3.y);
+      v[u][2] += (t0.z + t1.z) + (t2.z + t3.z);
+      v[u][3] += (t0.w + t1.w) + (t2.w + t3.w);
+    }
+    for (; z < a.splits; z += R) {
+      const float4 t = *reinterpret_cast<const float4 *>(col + z * NM);
+      v[u][0] += t.x; v[u][1] += t.y; v[u][2] += t.z; v[u][3] += t.w;
     }
   }
+  for (int o = 1; o < R; o <<= 1) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[u][q] += __shfl_xor_sync(0xffffffffu, v[u][q], o);
+  }
+  const bool owner = lane_r == 0;
   float mean = 0.f, rstd = 1.f;
   if (gn) {
     float ls = 0.f;
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (tid + u * nthr < cnt4) ls += (v[u][0] + v[u][1]) + (v[u][2] + v[u][3]);
+      if (ok_[u] && owner) ls += (v[u][0] + v[u][1]) + (v[u][2] + v[u][3]);
     const int cnt = cnt4 * 4;
     mean = unit_sum(ls, red, tid, nthr, sync) / cnt;
+    if (stamp && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stamp[0]));
     float lq = 0.f;
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (tid + u * nthr < cnt4)
+      if (ok_[u] && owner)
 #pragma unroll
         for (int q = 0; q < 4; ++q) { const float d = v[u][q] - mean; lq += d * d; }
     rstd = rsqrtf(unit_sum(lq, red, tid, nthr, sync) / cnt + 1e-5f);
+    if (stamp && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stamp[1]));
   }
   T *out = static_cast<T *>(a.out);
   const int wout = a.out_stuff ? 2 * a.Wo : a.Wo;
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    if (tid + u * nthr >= cnt4) continue;
+    if (!ok_[u]) continue;
     const int c = c0 + cc_[u];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
+      if ((q & (R - 1)) != lane_r && R <= 4) continue;       // lanes of a vector split the stores
+      if (R > 4 && !(lane_r < 4 && q == lane_r)) continue;
       const int p = p0_[u] + q;
       float y = v[u][q];
       if (gn) y = (y - mean) * rstd * gam[u] + bet[u];
@@ -131,18 +170,23 @@ __device__ __forceinline__ void epi_unit_regs(const EpiArgs &a, int s, int gy, i
       }
     }
   }
+  if (stamp && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stamp[2]));
+}
+
+// True when the unit takes the register-resident path (epi_unit_regs).
+__device__ __forceinline__ bool epi_fits_regs(const EpiArgs &a, int gy, int nthr) {
+  const bool gn = a.gn_gamma != nullptr;
+  const int cg0 = gn ? a.M / a.groups : min(64, a.M - gy * 64);
+  const int P0 = a.Ho * a.Wo;
+  return !a.pool_out && (P0 & 3) == 0 && cg0 * P0 <= 16 * nthr;
 }
 
 template <typename T, typename Sync>
 __device__ void epi_unit(const EpiArgs &a, int s, int gy, int tid, int nthr, float *red, Sync sync) {
   const bool gn = a.gn_gamma != nullptr;
-  {
-    const int cg0 = gn ? a.M / a.groups : min(64, a.M - gy * 64);
-    const int P0 = a.Ho * a.Wo;
-    if (!a.pool_out && (P0 & 3) == 0 && cg0 * P0 <= 16 * nthr) {
-      epi_unit_regs<T>(a, s, gy, tid, nthr, red, sync);
-      return;
-    }
+  if (epi_fits_regs(a, gy, nthr)) {
+    epi_unit_regs<T>(a, s, gy, tid, nthr, red, sync, [] __device__() {});
+    return;
   }
   const int cg = gn ? a.M / a.groups : min(64, a.M - gy * 64);
   const int c0 = gn ? gy * cg : gy * 64;

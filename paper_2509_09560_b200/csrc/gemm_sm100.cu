@@ -21,29 +21,9 @@
 #include <algorithm>
 #include <cstring>
 
-#include "conv.cuh"
+#include "tc_util.cuh"
 
 namespace auras {
-
-// ---------------------------------------------------------------- host: tensor maps
-typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
-                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
-                                  CUtensorMapFloatOOBfill);
-
-static EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    cudaDriverEntryPointQueryResult q;
-    void *p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
-  return fn;
-}
 
 constexpr int TC_BM = 128, TC_BK = 64;
 constexpr int TC_THREADS = 128;
@@ -88,96 +68,6 @@ bool gemm_sm100_supported(const ConvGemmArgs &g) {
 }
 
 int gemm_sm100_splits(const ConvGemmArgs &g) { return tc_plan(g).splits; }
-
-// ---------------------------------------------------------------- device helpers
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, uint64_t *bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *tm, uint64_t *bar, int c0, int c1, int c2,
-                                            int c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
-      "[%2];" ::"r"(smem_u32(dst)),
-      "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-      : "memory");
-}
-
-// UMMA shared-memory descriptor: K-major operand, 128B swizzle, 8-row atoms
-// 1024 B apart (SBO), version 1 (sm_100).
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);          // start address
-  d |= (uint64_t)(16 >> 4) << 16;                   // LBO (unused for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;                 // SBO
-  d |= (uint64_t)1 << 46;                           // descriptor version
-  d |= (uint64_t)2 << 61;                           // SWIZZLE_128B
-  return d;
-}
-
-// Instruction descriptor: D f32, A/B bf16, both K-major, M = 128, N = n.
-__device__ __forceinline__ uint32_t umma_idesc(int n) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-}
-
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(acc));
-}
-
-__device__ __forceinline__ void umma_commit(uint64_t *bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
 
 struct TcArgs {
   float *partial;
@@ -276,11 +166,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     float v[16];
     tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c, v);
     if (m < a.M) {
+      float *row = out + (int64_t)m * a.N + nbase + c;          // partial[split][m][n]
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int n = c + j;
-        if (n < nvalid) out[(int64_t)(nbase + n) * a.M + m] = nkb > 0 ? v[j] : 0.f;
-      }
+      for (int j = 0; j < 16; j += 4)
+        if (c + j < nvalid)
+          *reinterpret_cast<float4 *>(row + j) = nkb > 0 ? make_float4(v[j], v[j + 1], v[j + 2], v[j + 3])
+                                                       : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -289,33 +180,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 }
 
 int launch_gemm_sm100(const ConvGemmArgs &g, cudaStream_t st) {
-  EncodeTiledFn enc = encode_fn();
-  if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return AURAS_E_CUDA; }
   const TcPlan p = tc_plan(g);
   CUtensorMap tmA, tmB;
-  {
-    cuuint64_t dims[2] = {(cuuint64_t)g.Kp, (cuuint64_t)g.M};
-    cuuint64_t strides[1] = {(cuuint64_t)g.Kp * 2};
-    cuuint32_t box[2] = {TC_BK, TC_BM};
-    cuuint32_t es[2] = {1, 1};
-    CUresult r = enc(&tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(g.w), dims, strides, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) { set_error("tensor map A: CUresult %d", (int)r); return AURAS_E_CUDA; }
-  }
-  {
-    const int S = g.N / g.Wo;
-    const uint8_t *base = static_cast<const uint8_t *>(g.in) + (size_t)g.in_coff * 2;
-    cuuint64_t dims[4] = {(cuuint64_t)g.Cin, (cuuint64_t)g.stride, (cuuint64_t)(g.W / g.stride), (cuuint64_t)S};
-    cuuint64_t strides[3] = {(cuuint64_t)g.in_pitch * 2, (cuuint64_t)g.in_pitch * 2 * g.stride,
-                             (cuuint64_t)g.in_pitch * 2 * g.W};
-    cuuint32_t box[4] = {TC_BK, 1, (cuuint32_t)g.Wo, (cuuint32_t)p.s_box};
-    cuuint32_t es[4] = {1, 1, 1, 1};
-    CUresult r = enc(&tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint8_t *>(base), dims, strides, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) { set_error("tensor map B: CUresult %d", (int)r); return AURAS_E_CUDA; }
-  }
+  int rc = make_weight_map(&tmA, g.w, g.M, g.Kp);
+  if (rc) return rc;
+  rc = make_act_map(&tmB, g.in, g.in_coff, g.Cin, g.in_pitch, g.W, g.stride, g.N / g.Wo, g.Wo, p.s_box);
+  if (rc) return rc;
   static size_t configured = 0;
   if (p.smem > configured) {
     AURAS_CUDA(cudaFuncSetAttribute(conv_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -334,4 +204,3 @@ int launch_gemm_sm100(const ConvGemmArgs &g, cudaStream_t st) {
 
 }  // namespace auras
 
-extern "C" int auras_tc_available(void) { return auras::encode_fn() != nullptr; }

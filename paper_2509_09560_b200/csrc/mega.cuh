@@ -1,5 +1,6 @@
 // Host interface of the persistent denoise megakernel (unet_mega.cu).
 #pragma once
+#include <utility>
 #include <vector>
 
 #include "conv.cuh"
@@ -23,7 +24,10 @@ struct MegaParams {
   const __nv_bfloat16 *y_final;
   int y_pitch, final_cin;
   const float *wf, *bf;
-  long long *trace;         // optional [n_tasks][4] globaltimer stamps (NULL = off)
+  long long *trace;         // optional [n_tasks][8] globaltimer stamps (NULL = off)
+  int spin_ns;              // back-off between counter polls
+  long long *kbtrace;       // optional [grid][1024][3]: per-k-block A ready, B ready, MMA issued
+  int a_depth;              // weight-ring stages actually used (<= MK_NA)
 };
 
 struct MegaConfig {
@@ -39,8 +43,11 @@ struct MegaConfig {
 MegaParams mega_base_params(UnetDev *dev, const auras_sched &sched, int horizon, int adim, void *xin, int x_pitch,
                             int64_t slot_stride, int64_t agent_stride, const void *y_final, int y_pitch, int cin,
                             const float *wf, const float *bf);
+using TiledCache = std::vector<std::pair<const void *, void *>>;   // (row-major weights, tiled copy)
 int mega_build(MegaConfig &mc, const std::vector<auras_conv_op> &ops, int S, const void *x_in, int x_pitch,
-               const MegaParams &base, const float *film_tau, int film_width, const float *ring_film);
+               const MegaParams &base, const float *film_tau, int film_width, const float *ring_film,
+               TiledCache &cache);
+void mega_free_tiled(TiledCache &cache);
 int mega_launch(const MegaConfig &mc, cudaStream_t st);
 int mega_set_trace(MegaConfig &mc, long long *trace);
 void mega_free(MegaConfig &mc);

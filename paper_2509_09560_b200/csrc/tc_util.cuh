@@ -151,6 +151,108 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
 }
 
 
+// ---- warp-uniform variants: every lane executes the call with identical
+// operands; one lane is elected inside the PTX, so descriptors and addresses
+// stay in uniform registers (no per-instruction R2UR/ELECT loops).
+__device__ __forceinline__ void umma_bf16_warp(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                               uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 rx;\n"
+      ".reg .pred px, p;\n"
+      "elect.sync rx|px, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@px tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit_warp(uint64_t *bar) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 rx;\n"
+      ".reg .pred px;\n"
+      "elect.sync rx|px, 0xffffffff;\n"
+      "@px tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d_warp(void *dst, const CUtensorMap *tm, uint64_t *bar, uint32_t bytes,
+                                                 int c0, int c1) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 rx;\n"
+      ".reg .pred px;\n"
+      "elect.sync rx|px, 0xffffffff;\n"
+      "@px mbarrier.arrive.expect_tx.shared::cta.b64 _, [%2], %3;\n"
+      "@px cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%4, %5}], [%2];\n"
+      "}\n" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(smem_u32(bar)), "r"(bytes), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// expect_tx(bytes) once, then one or two 2-D boxes (rows c1a and c1b) into
+// consecutive 16 KB halves of dst.
+__device__ __forceinline__ void tma_load_2d_pair_warp(void *dst, const CUtensorMap *tm, uint64_t *bar, uint32_t bytes,
+                                                      int c0, int c1a, int c1b, int two) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 rx;\n"
+      ".reg .pred px, p2;\n"
+      "elect.sync rx|px, 0xffffffff;\n"
+      "setp.ne.and.b32 p2, %7, 0, px;\n"
+      "@px mbarrier.arrive.expect_tx.shared::cta.b64 _, [%2], %3;\n"
+      "@px cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%4, %5}], [%2];\n"
+      "@p2 cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%8], [%1, {%4, %6}], [%2];\n"
+      "}\n" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(smem_u32(bar)), "r"(bytes), "r"(c0), "r"(c1a), "r"(c1b), "r"(two),
+      "r"(smem_u32(dst) + 16384)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx_warp(uint64_t *bar, uint32_t bytes) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 rx;\n"
+      ".reg .pred px;\n"
+      "elect.sync rx|px, 0xffffffff;\n"
+      "@px mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+
+// TMA only (the barrier's expect_tx was armed separately).
+__device__ __forceinline__ void tma_4d_warp(void *dst, const CUtensorMap *tm, uint64_t *bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 rx;\n"
+      ".reg .pred px;\n"
+      "elect.sync rx|px, 0xffffffff;\n"
+      "@px cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+      "%6}], [%2];\n"
+      "}\n" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d_warp(void *dst, const CUtensorMap *tm, uint64_t *bar, uint32_t bytes,
+                                                 int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 rx;\n"
+      ".reg .pred px;\n"
+      "elect.sync rx|px, 0xffffffff;\n"
+      "@px mbarrier.arrive.expect_tx.shared::cta.b64 _, [%2], %3;\n"
+      "@px cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%4, %5, %6, "
+      "%7}], [%2];\n"
+      "}\n" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(smem_u32(bar)), "r"(bytes), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

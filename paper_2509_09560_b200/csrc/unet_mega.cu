@@ -28,6 +28,7 @@
 // list in layer order and a task only waits on tasks of strictly earlier
 // layers; the grid is one CTA per SM so all CTAs are co-resident.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "epi.cuh"
@@ -39,12 +40,14 @@ namespace auras {
 
 constexpr int MK_THREADS = 384;              // 4 role warps + 8 epilogue warps
 constexpr int MK_EPI = 256;                  // epilogue-unit threads (warps 4-11)
-constexpr int MK_NA = 7;                 // weight stages
-constexpr int MK_NB = 6;                 // activation stages
+constexpr int MK_KS = 2;                 // k-blocks (64 wide) per pipeline stage
+constexpr int MK_NA = 5;                 // weight stages (2 x 16 KB each): 160 KB HBM prefetch depth
 constexpr int MK_BN = 128;               // max N per GEMM task
-constexpr int MK_A_BYTES = 128 * 64 * 2;
-constexpr int MK_B_BYTES = MK_BN * 64 * 2;
-constexpr size_t MK_SMEM = 1024 + (size_t)MK_NA * MK_A_BYTES + (size_t)MK_NB * MK_B_BYTES + 1024 + 4 * 600;
+constexpr int MK_A_BYTES = 128 * 64 * 2;         // one 128 x 64 weight box
+constexpr int MK_A_STAGE = MK_KS * MK_A_BYTES;
+constexpr int MK_B_RING = 48 * 1024;     // activation ring, carved per task into stages of
+constexpr int MK_NBMAX = 12;             //   round_up(bn*128, 1KB) bytes: 3..12 in flight
+constexpr size_t MK_SMEM = 1024 + (size_t)MK_NA * MK_A_STAGE + (size_t)MK_B_RING + 1024 + 4 * 600;
 
 enum { T_GEMM = 0, T_EPI = 1, T_PREP = 2, T_FINAL = 3 };
 
@@ -53,6 +56,7 @@ struct alignas(64) MegaOp {
   CUtensorMap tmB;
   EpiArgs epi;
   int M, N, Cin, Wo, stride, pad, S, s_box, rows, bn, kb_total, kb_per_split, splits, gemm_tasks, epi_units;
+  int bstage, nbst;         // activation-ring stage bytes and stage count for this op
   int gemm_dep[3];          // -1 none, -2 prep
   int epi_dep[2];
 };
@@ -63,21 +67,27 @@ __device__ __forceinline__ long long gtime() {
   return t;
 }
 
+__device__ __forceinline__ void spin_ns(const int *ctr, int target, int ns) {
+  while (ld_acquire_i32(ctr) < target) {
+    if (ns) __nanosleep(ns);
+  }
+}
+
 __device__ __forceinline__ void wait_dep(const MegaParams &P, int *epi_done, int *prep_done, int d) {
-  if (d == -2) spin_until(prep_done, P.S);
-  else if (d >= 0) spin_until(&epi_done[d], P.ops[d].epi_units);
+  if (d == -2) spin_ns(prep_done, P.S, P.spin_ns);
+  else if (d >= 0) spin_ns(&epi_done[d], P.ops[d].epi_units, P.spin_ns);
 }
 
 __global__ void __launch_bounds__(MK_THREADS, 1) unet_mega(const __grid_constant__ MegaParams P) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = smem;
-  uint8_t *sB = sA + MK_NA * MK_A_BYTES;
-  uint64_t *fullA = reinterpret_cast<uint64_t *>(sB + MK_NB * MK_B_BYTES);
+  uint8_t *sB = sA + MK_NA * MK_A_STAGE;
+  uint64_t *fullA = reinterpret_cast<uint64_t *>(sB + MK_B_RING);
   uint64_t *emptyA = fullA + MK_NA;
   uint64_t *fullB = emptyA + MK_NA;
-  uint64_t *emptyB = fullB + MK_NB;
-  uint64_t *tfull = emptyB + MK_NB;
+  uint64_t *emptyB = fullB + MK_NBMAX;
+  uint64_t *tfull = emptyB + MK_NBMAX;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
   float *red = reinterpret_cast<float *>(tmem_slot + 8);
@@ -91,7 +101,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) unet_mega(const __grid_constant
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < MK_NA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], 1); }
-    for (int i = 0; i < MK_NB; ++i) { mbar_init(&fullB[i], 1); mbar_init(&emptyB[i], 1); }
+    for (int i = 0; i < MK_NBMAX; ++i) { mbar_init(&fullB[i], 1); mbar_init(&emptyB[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -107,67 +117,75 @@ __global__ void __launch_bounds__(MK_THREADS, 1) unet_mega(const __grid_constant
 
   if (warp == 0) {
     // ------------------------------------------------ A producer: weights, never blocked on data
-    if (lane == 0) {
-      int ia = 0;
-      for (int t = t0; t < t1; ++t) {
-        const int4 tk = P.tasks[t];
-        if ((tk.x & 0xff) != T_GEMM) continue;
-        const MegaOp *op = &P.ops[tk.x >> 8];
-        const int kps = op->kb_per_split, kbt = op->kb_total;     // snapshot: no reloads in the loop
-        const CUtensorMap *tmA = &op->tmA;
-        const int kb0 = tk.w * kps, kb1 = min(kbt, kb0 + kps);
-        const int row0 = tk.y * 128;
-        for (int kb = kb0; kb < kb1; ++kb, ++ia) {
-          const int st = ia % MK_NA;
-          mbar_wait(&emptyA[st], ((ia / MK_NA) & 1) ^ 1);
-          mbar_expect_tx(&fullA[st], MK_A_BYTES);
-          tma_load_2d(sA + st * MK_A_BYTES, tmA, &fullA[st], kb * 64, row0);
-        }
+    // (warp-uniform loop; one lane elected inside the PTX)
+    int ia = 0;
+    for (int t = t0; t < t1; ++t) {
+      const int4 tk = P.tasks[t];
+      if ((tk.x & 0xff) != T_GEMM) continue;
+      const MegaOp *op = &P.ops[tk.x >> 8];
+      const int kps = op->kb_per_split, kbt = op->kb_total;     // snapshot: no reloads in the loop
+      const CUtensorMap *tmA = &op->tmA;
+      const int kb0 = tk.w * kps, kb1 = min(kbt, kb0 + kps);
+      const int row0 = tk.y * kbt * 128;          // tiled layout [m_tile][k_block][128][64]
+      for (int kb = kb0; kb < kb1; kb += MK_KS, ++ia) {
+        const int st = ia % MK_NA;
+        const int two = kb + 1 < kb1;
+        mbar_wait(&emptyA[st], ((ia / MK_NA) & 1) ^ 1);
+        if (P.a_depth < MK_NA && ia >= P.a_depth)        // optional cap on weights in flight
+          mbar_wait(&emptyA[(ia - P.a_depth) % MK_NA], (((ia - P.a_depth) / MK_NA) & 1));
+        tma_load_2d_pair_warp(sA + st * MK_A_STAGE, tmA, &fullA[st], (1 + two) * MK_A_BYTES, 0, row0 + kb * 128,
+                              row0 + (kb + 1) * 128, two);
       }
     }
-    __syncwarp();
   } else if (warp == 2) {
     // ------------------------------------------------ B producer: activations, after dependencies
-    if (lane == 0) {
-      int ib = 0;
-      for (int t = t0; t < t1; ++t) {
-        const int4 tk = P.tasks[t];
-        if ((tk.x & 0xff) != T_GEMM) continue;
-        const MegaOp *op = &P.ops[tk.x >> 8];
-        const int dep0 = op->gemm_dep[0], dep1 = op->gemm_dep[1], dep2 = op->gemm_dep[2];
-        const int kps = op->kb_per_split, kbt = op->kb_total, Cin = op->Cin, pad = op->pad;
-        const int stride = op->stride, sbox = op->s_box;
-        const uint32_t bbytes = op->rows * 128;
-        const CUtensorMap *tmB = &op->tmB;
+    uint32_t par = 0;                 // per-slot use parity of the activation ring
+    for (int t = t0; t < t1; ++t) {
+      const int4 tk = P.tasks[t];
+      if ((tk.x & 0xff) != T_GEMM) continue;
+      const MegaOp *op = &P.ops[tk.x >> 8];
+      const int bstage = op->bstage, nbst = op->nbst;
+      const int dep0 = op->gemm_dep[0], dep1 = op->gemm_dep[1], dep2 = op->gemm_dep[2];
+      const int kps = op->kb_per_split, kbt = op->kb_total, Cin = op->Cin, pad = op->pad;
+      const int stride = op->stride, sbox = op->s_box;
+      const uint32_t bbytes = op->rows * 128;
+      const CUtensorMap *tmB = &op->tmB;
+      if (lane == 0) {
         wait_dep(P, epi_done, prep_done, dep0);
         wait_dep(P, epi_done, prep_done, dep1);
         wait_dep(P, epi_done, prep_done, dep2);
         fence_proxy_async();
         if (P.trace) P.trace[8 * t + 0] = gtime();
-        const int kb0 = tk.w * kps, kb1 = min(kbt, kb0 + kps);
-        for (int kb = kb0; kb < kb1; ++kb, ++ib) {
-          const int st = ib % MK_NB;
-          mbar_wait(&emptyB[st], ((ib / MK_NB) & 1) ^ 1);
-          const int k = kb * 64;
+      }
+      __syncwarp();
+      const int kb0 = tk.w * kps, kb1 = min(kbt, kb0 + kps);
+      for (int kb = kb0; kb < kb1; kb += MK_KS) {
+        const int st = ((kb - kb0) / MK_KS) % nbst;
+        const int nk = min(MK_KS, kb1 - kb);
+        mbar_wait(&emptyB[st], ((par >> st) & 1) ^ 1);
+        par ^= 1u << st;
+        mbar_expect_tx_warp(&fullB[st], nk * bbytes);
+        for (int i = 0; i < nk; ++i) {
+          const int k = (kb + i) * 64;
           const int tap = k / Cin, c0 = k - tap * Cin;
           const int off = tap - pad;
           const int q = off >= 0 ? off / stride : -((-off + stride - 1) / stride);
           const int h = off - q * stride;
-          mbar_expect_tx(&fullB[st], bbytes);
-          tma_load_4d(sB + st * MK_B_BYTES, tmB, &fullB[st], c0, h, q, tk.z * sbox);
+          tma_4d_warp(sB + st * MK_KS * bstage + i * bstage, tmB, &fullB[st], c0, h, q, tk.z * sbox);
         }
-        if (P.trace) P.trace[8 * t + 1] = gtime();
       }
+      if (lane == 0 && P.trace) P.trace[8 * t + 1] = gtime();
     }
-    __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    int ia = 0, ib = 0, gi = 0;
+    int ia = 0, gi = 0;
+    uint32_t par = 0;
     for (int t = t0; t < t1; ++t) {
       const int4 tk = P.tasks[t];
       if ((tk.x & 0xff) != T_GEMM) continue;
       const MegaOp *op = &P.ops[tk.x >> 8];
       const int kps = op->kb_per_split, kbt = op->kb_total, bn = op->bn;
+      const int bstage = op->bstage, nbst = op->nbst;
       const int buf = gi & 1;
       mbar_wait(&tempty[buf], ((gi >> 1) & 1) ^ 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -175,27 +193,33 @@ __global__ void __launch_bounds__(MK_THREADS, 1) unet_mega(const __grid_constant
       const uint32_t dt = tmem + buf * MK_BN;
       const int kb0 = tk.w * kps, kb1 = min(kbt, kb0 + kps);
       if (P.trace && lane == 0) P.trace[8 * t + 4] = gtime();
-      for (int kb = kb0; kb < kb1; ++kb, ++ia, ++ib) {
-        const int sa = ia % MK_NA, sb = ib % MK_NB;
+      for (int kb = kb0; kb < kb1; kb += MK_KS, ++ia) {
+        const int sa = ia % MK_NA, sb = ((kb - kb0) / MK_KS) % nbst;
+        const int nk = min(MK_KS, kb1 - kb);
         mbar_wait(&fullA[sa], (ia / MK_NA) & 1);
         if (P.trace && lane == 0 && kb == kb0) P.trace[8 * t + 5] = gtime();
-        mbar_wait(&fullB[sb], (ib / MK_NB) & 1);
+        long long *kt = (P.kbtrace && ia < 1024) ? P.kbtrace + ((int64_t)blockIdx.x * 1024 + ia) * 3 : nullptr;
+        if (kt && lane == 0) kt[0] = gtime();
+        mbar_wait(&fullB[sb], (par >> sb) & 1);
+        if (kt && lane == 0) kt[1] = gtime();
+        par ^= 1u << sb;
         if (P.trace && lane == 0 && kb == kb0) P.trace[8 * t + 6] = gtime();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (lane == 0) {
-          const uint32_t a0 = smem_u32(sA + sa * MK_A_BYTES), b0 = smem_u32(sB + sb * MK_B_BYTES);
+        for (int i = 0; i < nk; ++i) {
+          const uint32_t a0 = smem_u32(sA + sa * MK_A_STAGE + i * MK_A_BYTES);
+          const uint32_t b0 = smem_u32(sB + sb * MK_KS * bstage + i * bstage);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            umma_bf16(dt, umma_desc(a0 + kk * 32), umma_desc(b0 + kk * 32), idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
-          umma_commit(&emptyA[sa]);
-          umma_commit(&emptyB[sb]);
+            umma_bf16_warp(dt, umma_desc(a0 + kk * 32), umma_desc(b0 + kk * 32), idesc,
+                           (kb > kb0 || i > 0 || kk > 0) ? 1u : 0u);
         }
+        umma_commit_warp(&emptyA[sa]);
+        umma_commit_warp(&emptyB[sb]);
+        if (kt && lane == 0) kt[2] = gtime();
         __syncwarp();
       }
-      if (lane == 0) {
-        umma_commit(&tfull[buf]);
-        if (P.trace) P.trace[8 * t + 7] = gtime();
-      }
+      umma_commit_warp(&tfull[buf]);
+      if (lane == 0 && P.trace) P.trace[8 * t + 7] = gtime();
       __syncwarp();
       ++gi;
     }
@@ -237,9 +261,9 @@ __global__ void __launch_bounds__(MK_THREADS, 1) unet_mega(const __grid_constant
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
-        __threadfence();
         dsync();
-        if (et == 0) {
+        if (et == 0) {                              // one fence after the barrier releases the CTA's stores
+          __threadfence();
           atomicAdd(&gemm_done[opi], 1);
           if (P.trace) P.trace[8 * t + 3] = gtime();
         }
@@ -247,20 +271,34 @@ __global__ void __launch_bounds__(MK_THREADS, 1) unet_mega(const __grid_constant
       } else if (type == T_EPI) {
         const MegaOp *op = &P.ops[opi];
         const EpiArgs e = op->epi;                  // by value: registers, no reloads after fences
-        if (et == 0) {
-          const int need = op->gemm_tasks, d0 = op->epi_dep[0], d1 = op->epi_dep[1];
-          spin_until(&gemm_done[opi], need);
-          spin_until(prep_done, P.S);
+        const int need = op->gemm_tasks, d0 = op->epi_dep[0], d1 = op->epi_dep[1];
+        if (et == 0) {                              // residual producers + per-sample FiLM rows
+          spin_ns(prep_done, P.S, P.spin_ns);
           wait_dep(P, epi_done, prep_done, d0);
           wait_dep(P, epi_done, prep_done, d1);
         }
         sync();
-        if (P.trace && et == 0) P.trace[8 * t + 0] = gtime();
-        epi_unit<__nv_bfloat16>(e, tk.y, tk.z, et, MK_EPI, red, sync);
+        auto gate = [&] __device__() {              // this layer's GEMM partials
+          if (et == 0) spin_ns(&gemm_done[opi], need, P.spin_ns);
+          sync();
+          if (P.trace && et == 0) P.trace[8 * t + 0] = gtime();
+        };
+        if (epi_fits_regs(e, tk.z, MK_EPI)) {
+          long long st3[3] = {0, 0, 0};
+          epi_unit_regs<__nv_bfloat16>(e, tk.y, tk.z, et, MK_EPI, red, sync, gate, P.trace ? st3 : nullptr);
+          if (P.trace && et == 0) {
+            P.trace[8 * t + 2] = st3[0];
+            P.trace[8 * t + 3] = st3[1];
+            P.trace[8 * t + 4] = st3[2];
+          }
+        } else {
+          gate();
+          epi_unit<__nv_bfloat16>(e, tk.y, tk.z, et, MK_EPI, red, sync);
+        }
         fence_proxy_async();
-        __threadfence();
         sync();
         if (et == 0) {
+          __threadfence();
           atomicAdd(&epi_done[opi], 1);
           if (P.trace) P.trace[8 * t + 1] = gtime();
         }
@@ -268,11 +306,13 @@ __global__ void __launch_bounds__(MK_THREADS, 1) unet_mega(const __grid_constant
         prep_body<__nv_bfloat16>(P.dev, tk.y, et, MK_EPI, P.sched, P.horizon, P.adim, P.xin, P.x_pitch,
                                  P.ring_slot_stride, P.ring_agent_stride);
         fence_proxy_async();
-        __threadfence();
         sync();
-        if (et == 0) atomicAdd(prep_done, 1);
+        if (et == 0) {
+          __threadfence();
+          atomicAdd(prep_done, 1);
+        }
       } else if (type == T_FINAL) {
-        if (et == 0) spin_until(&epi_done[P.n_ops - 1], P.ops[P.n_ops - 1].epi_units);
+        if (et == 0) spin_ns(&epi_done[P.n_ops - 1], P.ops[P.n_ops - 1].epi_units, P.spin_ns);
         sync();
         final_body<__nv_bfloat16>(P.dev, tk.y, et, MK_EPI, P.sched, P.horizon, P.adim, P.y_final, P.y_pitch,
                                   P.final_cin, P.wf, P.bf, eps, sync);
@@ -286,15 +326,69 @@ __global__ void __launch_bounds__(MK_THREADS, 1) unet_mega(const __grid_constant
 
 // ---------------------------------------------------------------- host side
 
+// Weights re-laid out as [m_tile][k_block][128 rows][64] so that every 16 KB
+// TMA box -- and a task's whole run of k-blocks -- is contiguous in HBM.
+__global__ void tile_weights_kernel(const __nv_bfloat16 *__restrict__ src, __nv_bfloat16 *__restrict__ dst, int M,
+                                    int Kp, int m_tiles) {
+  const int KB = Kp / 64;
+  const int64_t total = (int64_t)m_tiles * KB * 128 * 8;     // 16-byte chunks
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int chunk = i & 7;
+    const int64_t rowi = i >> 3;
+    const int r = rowi & 127;
+    const int64_t tile = rowi >> 7;
+    const int kb = tile % KB, mt = tile / KB;
+    const int m = mt * 128 + r;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (m < M) v = *reinterpret_cast<const uint4 *>(src + (int64_t)m * Kp + kb * 64 + chunk * 8);
+    *reinterpret_cast<uint4 *>(dst + rowi * 64 + chunk * 8) = v;
+  }
+}
+
+static int make_tiled_weight_map(CUtensorMap *tm, const void *wt, int rows_total) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return AURAS_E_CUDA; }
+  cuuint64_t dims[2] = {64, (cuuint64_t)rows_total};
+  cuuint64_t strides[1] = {128};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(wt), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("tiled weight map: CUresult %d", (int)r); return AURAS_E_CUDA; }
+  return AURAS_OK;
+}
+
+static int tiled_weights(TiledCache &cache, const auras_conv_op &o, void **out) {
+  for (auto &kv : cache)
+    if (kv.first == o.w) { *out = kv.second; return AURAS_OK; }
+  const int m_tiles = (o.M + 127) / 128;
+  const size_t bytes = (size_t)m_tiles * o.Kp * 128 * 2;
+  void *d = nullptr;
+  AURAS_CUDA(cudaMalloc(&d, bytes));
+  tile_weights_kernel<<<1184, 256>>>(static_cast<const __nv_bfloat16 *>(o.w), static_cast<__nv_bfloat16 *>(d), o.M,
+                                     o.Kp, m_tiles);
+  AURAS_LAUNCHED("tile_weights_kernel");
+  AURAS_CUDA(cudaDeviceSynchronize());
+  cache.emplace_back(o.w, d);
+  *out = d;
+  return AURAS_OK;
+}
+
 static bool same_buffer(const void *a, const void *b) { return a != nullptr && a == b; }
 
 // Build the per-S task table.  `ops` are the plan's conv ops in execution order.
 int mega_build(MegaConfig &mc, const std::vector<auras_conv_op> &ops, int S, const void *x_in, int x_pitch,
-               const MegaParams &base, const float *film_tau, int film_width, const float *ring_film) {
+               const MegaParams &base, const float *film_tau, int film_width, const float *ring_film,
+               TiledCache &cache) {
   const int n = (int)ops.size();
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // leave a few SMs to the perception stream, which runs concurrently
+  const char *rs = getenv("AURAS_MEGA_RESERVE");
+  const int reserve = rs ? atoi(rs) : 8;
+  sms = std::max(16, sms - std::max(0, reserve));
   std::vector<MegaOp> hops(n);
   std::vector<int64_t> part_off(n);
   int64_t part_total = 0;
@@ -312,6 +406,9 @@ int mega_build(MegaConfig &mc, const std::vector<auras_conv_op> &ops, int S, con
     m.rows = m.s_box * o.Wo;
     m.bn = (m.rows + 15) / 16 * 16;
     m.kb_total = o.Kp / 64;
+    m.bstage = (m.bn * 128 + 1023) / 1024 * 1024;
+    m.nbst = std::min(MK_NBMAX, MK_B_RING / (MK_KS * m.bstage));
+    if (m.nbst < 1) { set_error("megakernel: B stage too large"); return AURAS_E_ARG; }
     const int m_tiles = (o.M + 127) / 128, n_tiles = (S + m.s_box - 1) / m.s_box;
     // split-K: enough CTAs to stream big layers at full HBM rate, but at least
     // ~128 KB of weights per task so small layers do not drown in partials
@@ -335,7 +432,9 @@ int mega_build(MegaConfig &mc, const std::vector<auras_conv_op> &ops, int S, con
     }
     part_off[i] = part_total;
     part_total += (int64_t)m.splits * m.N * m.M;
-    if ((rc = make_weight_map(&m.tmA, o.w, o.M, o.Kp))) return rc;
+    void *wt = nullptr;
+    if ((rc = tiled_weights(cache, o, &wt))) return rc;
+    if ((rc = make_tiled_weight_map(&m.tmA, wt, m_tiles * m.kb_total * 128))) return rc;
     if ((rc = make_act_map(&m.tmB, o.in, o.in_coff, o.Cin, o.in_pitch, o.W, o.stride, S, o.Wo, m.s_box))) return rc;
     // dependencies: producers of the input buffer (or the prep), of the residuals
     int nd = 0;
@@ -366,8 +465,10 @@ int mega_build(MegaConfig &mc, const std::vector<auras_conv_op> &ops, int S, con
     const bool gn = ops[i].gn_gamma != nullptr;
     const int gy = gn ? ops[i].groups : (m.M + 63) / 64;
     int u = 0;
-    for (int s = 0; s < S; ++s)
-      for (int g = 0; g < gy; ++g, ++u) per[(rot + u * 7) % sms].push_back(make_int4(T_EPI | (i << 8), s, g, 0));
+    const int units = S * gy;
+    for (int s = 0; s < S; ++s)        // spread the units evenly over the grid (one per CTA when possible)
+      for (int g = 0; g < gy; ++g, ++u)
+        per[(rot + (int)((int64_t)u * sms / units)) % sms].push_back(make_int4(T_EPI | (i << 8), s, g, 0));
     rot = (rot + 1) % sms;
   }
   for (int s = 0; s < S; ++s) per[(rot + s) % sms].push_back(make_int4(T_FINAL, s, 0, 0));
@@ -399,6 +500,10 @@ int mega_build(MegaConfig &mc, const std::vector<auras_conv_op> &ops, int S, con
   mc.params.ctr = mc.ctr;
   mc.params.n_ops = n;
   mc.params.S = S;
+  const char *sn = getenv("AURAS_MEGA_SPIN_NS");
+  mc.params.spin_ns = sn ? atoi(sn) : 0;
+  const char *ad = getenv("AURAS_MEGA_A_DEPTH");
+  mc.params.a_depth = ad ? std::max(1, std::min(MK_NA, atoi(ad))) : MK_NA;
   static bool attr = false;
   if (!attr) {
     AURAS_CUDA(cudaFuncSetAttribute(unet_mega, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MK_SMEM));
@@ -416,7 +521,13 @@ int mega_launch(const MegaConfig &mc, cudaStream_t st) {
 
 int mega_set_trace(MegaConfig &mc, long long *trace) {
   mc.params.trace = trace;
+  mc.params.kbtrace = trace ? trace + (int64_t)mc.n_tasks * 8 : nullptr;
   return AURAS_OK;
+}
+
+void mega_free_tiled(TiledCache &cache) {
+  for (auto &kv : cache) cudaFree(kv.second);
+  cache.clear();
 }
 
 void mega_free(MegaConfig &mc) {

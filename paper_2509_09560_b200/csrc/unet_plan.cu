@@ -63,6 +63,7 @@ struct auras_unet_plan {
   std::map<int, cudaGraphExec_t> graphs;     // one denoise step per batch size S
   bool use_mega = false;                     // persistent megakernel (bf16, tcgen05 engine)
   std::map<int, MegaConfig> mega;
+  TiledCache tiled;                          // tiled weight copies shared by all S
 };
 
 // One denoise step through the persistent megakernel (unet_mega.cu).
@@ -83,7 +84,8 @@ static int unet_ensure_mega(auras_unet_plan *p, int S) {
                                      p->ring_agent_stride, last.out, last.out_pitch, p->final_cin, p->final_w,
                                      p->final_b);
   MegaConfig mc;
-  int rc = mega_build(mc, p->ops, S, p->x_in, p->x_pitch, base, p->film_tau, p->film_width, p->ring_film);
+  int rc = mega_build(mc, p->ops, S, p->x_in, p->x_pitch, base, p->film_tau, p->film_width, p->ring_film,
+                      p->tiled);
   if (rc) {
     mega_free(mc);
     return rc;
@@ -191,6 +193,7 @@ auras_unet_plan *auras_unet_plan_create(const auras_conv_op *ops, int n_ops, int
 void auras_unet_plan_destroy(auras_unet_plan *p) {
   if (!p) return;
   for (auto &kv : p->mega) mega_free(kv.second);
+  mega_free_tiled(p->tiled);
   for (auto &kv : p->graphs) cudaGraphExecDestroy(kv.second);
   if (p->partial) cudaFree(p->partial);
   if (p->dev) cudaFree(p->dev);
@@ -260,7 +263,7 @@ int auras_unet_generate(auras_unet_plan *p, int S, const int *lanes, const int *
 extern "C" {
 
 // Diagnostics: enable a per-task globaltimer trace for the megakernel of batch
-// size S (buffer: int64[n_tasks][8]); returns n_tasks, copies the task table
+// size S (buffer: int64[n_tasks][8] + int64[grid][1024][3]); returns n_tasks, copies the task table
 // (int32[n_tasks][4]) to `tasks_out` when non-NULL.  Graphs captured before the
 // call keep their old parameters, so call it before the first generate.
 int auras_unet_mega_trace(auras_unet_plan *p, int S, long long *trace, int *tasks_out, int max_tasks) {

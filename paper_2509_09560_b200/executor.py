@@ -185,8 +185,15 @@ class _Device:
         import torch
         self.torch = torch
         self.clock = clock
-        self.P = torch.cuda.Stream()
-        self.G = torch.cuda.Stream()
+        # generation gets the higher priority: the persistent denoise kernel needs
+        # all of its CTAs resident, so its pending CTAs must win SMs over the
+        # perception kernels that run concurrently on P
+        lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") \
+            else (0, -1)
+        import os
+        gprio = -1 if os.environ.get("AURAS_G_PRIORITY", "1") == "1" else 0
+        self.P = torch.cuda.Stream(priority=0)
+        self.G = torch.cuda.Stream(priority=gprio)
         self.session = policy.open_session(capacity=capacity, lanes=lanes, agents=agents,
                                            max_outputs=max_outputs, max_frames=max_frames,
                                            p_stream=self.P, g_stream=self.G,
