@@ -81,6 +81,7 @@ _SIGNATURES = {
 
 _lock = threading.Lock()
 _lib = None
+_checked_devices = set()
 
 
 def exported_symbols():
@@ -108,8 +109,10 @@ def load(require_device: bool = True):
         if not torch.cuda.is_available():
             raise DeviceError("the B200 engine needs a CUDA device; none is visible")
         dev = torch.cuda.current_device()
-        if not _lib.auras_device_ok(dev):
-            raise DeviceError(f"device {torch.cuda.get_device_name(dev)} is not sm_100 (B200)")
+        if dev not in _checked_devices:        # cudaGetDeviceProperties costs milliseconds: once per device
+            if not _lib.auras_device_ok(dev):
+                raise DeviceError(f"device {torch.cuda.get_device_name(dev)} is not sm_100 (B200)")
+            _checked_devices.add(dev)
     return _lib
 
 

@@ -36,6 +36,7 @@ B200 restructuring:
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field, replace
 from typing import Optional
 
@@ -776,6 +777,9 @@ class DPSession:
             self._stage_resident(policy.resident_frames)
         self.instrument = False
         self.gen_events = []
+        # perception overlaps generation on the SMs the persistent denoise kernel
+        # leaves free (AURAS_MEGA_RESERVE); measured faster than interleaving
+        self.exclusive = False
         torch.cuda.synchronize()
 
     def _stage_resident(self, n):

@@ -206,6 +206,13 @@ class _Device:
         self.t_start, self.t_end = {}, {}
         self.origin = None
         self.throttle = []
+        # A policy whose denoise step is a whole-GPU persistent kernel asks for
+        # interleaving: perception of frame t+1 is ordered after generation of
+        # frame t (still two streams + events, but no SM contention).
+        import os
+        env = os.environ.get("AURAS_INTERLEAVE_PG")
+        self.interleave = (env == "1") if env is not None else bool(getattr(self.session, "exclusive", False))
+        self.last_gen_end = None
 
     def event(self, stream, timing=False):
         ev = self.torch.cuda.Event(enable_timing=timing)
@@ -216,6 +223,8 @@ class _Device:
         # bound how far the host runs ahead of the device (event/pinned-buffer lifetimes)
         if len(self.throttle) >= window:
             self.throttle.pop(0).synchronize()
+        if self.interleave and self.last_gen_end is not None:
+            self.P.wait_event(self.last_gen_end)
         if self.clock == "device":
             ev = self.event(self.P, timing=True)
             self.t_start[t] = ev
@@ -227,6 +236,7 @@ class _Device:
         if self.clock == "device":
             self.t_end[t] = ev
         self.throttle.append(ev)
+        self.last_gen_end = ev
 
     def ingest(self, t, lane, observations):
         ev = self.lane_free.pop(lane, None)
