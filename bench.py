@@ -63,6 +63,7 @@ class Dist:
         self.pg = None
 
     def init(self, backend):
+        self.backend = backend
         if self.world > 1:
             import torch.distributed as dist
             dist.init_process_group(backend)
@@ -73,11 +74,18 @@ class Dist:
             self.pg.barrier()
 
     def max(self, v):
+        return self._reduce(v, "MAX")
+
+    def sum(self, v):
+        return self._reduce(v, "SUM")
+
+    def _reduce(self, v, op):
         if not self.pg:
             return v
         import torch
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
-        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        dev = "cuda" if getattr(self, "backend", "nccl") == "nccl" else "cpu"
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t, op=getattr(self.pg.ReduceOp, op))
         return float(t.item())
 
 
@@ -202,12 +210,47 @@ def steady_jct_ms(res, t0, K):
 
 # ---------------------------------------------------------------- CPU arms
 
+class _SyntheticImageEnv:
+    """Feeds the synthetic DP frames to an unmodified reference scheduler
+    (which, with env=None, would observe zeros(4) -- no camera image)."""
+
+    success_threshold = None
+
+    def __init__(self, orc):
+        self.orc, self.last_error = orc, 0.0
+
+    def observe(self, frame):
+        return self.orc.synthetic_observation(frame)
+
+    def apply_action(self, action):
+        pass
+
+    def advance_frame(self):
+        pass
+
+
+def _reference_scheduler():
+    """The unmodified reference package installed in baseline/_ref (see
+    DESIGN.md §9); falls back to the restated scheduler in oracle/."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "framepipe")):
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        try:
+            import framepipe.executor as fx
+            return fx.run_sequential, "reference framepipe.run_sequential (baseline/_ref, unmodified)"
+        except Exception:        # noqa: BLE001
+            pass
+    from oracle import schedule as osched
+    return (lambda pol, env, n: osched.run_sequential(pol, env, n)), "oracle/schedule.py run_sequential"
+
+
 def cpu_oracle_sample(cfg_name, seconds, threads=None):
-    """The CPU restatement (oracle/dp_model.py inside the restated reference
-    scheduler) on this host's cores: sequential requests until `seconds`."""
+    """The reference CPU path for this workload on this host's cores: the
+    reference scheduler driving the torch-CPU fp32 oracle network
+    (oracle/dp_model.py), sequential requests until `seconds`."""
     import torch
     from oracle import dp_model
-    from oracle import schedule as osched
     from paper_2509_09560_b200 import diffusion as D
     n = threads or os.cpu_count()
     torch.set_num_threads(n)
@@ -215,6 +258,7 @@ def cpu_oracle_sample(cfg_name, seconds, threads=None):
     w = D.init_weights(cfg, 0, device="cpu")
     costs = tuple(f / 1e9 for f in D.encoder_flops(cfg))
     orc = dp_model.OracleDP(w, cfg, 0, 0, costs, D.unet_flops_per_sample(cfg) / 1e9)
+    run_seq, which = _reference_scheduler()
     # warm-up: one encoder pass and one denoise step
     obs = orc.synthetic_observation(0)
     ctx = orc.perception.perceive(obs)
@@ -223,17 +267,17 @@ def cpu_oracle_sample(cfg_name, seconds, threads=None):
     t0 = time.perf_counter()
     done = 0
     while True:
-        osched.run_sequential(orc, None, 1)
+        run_seq(orc, _SyntheticImageEnv(orc), 1)
         done += 1
         el = time.perf_counter() - t0
         if el >= seconds:
             break
     return {"value": done / el, "unit": "actions/s", "cores": n, "kind": "port",
             "sample": f"{done} request(s) of the {cfg_name} policy (encoder + "
-                      f"{cfg.num_inference_steps} denoise steps each) through oracle/schedule.py "
-                      f"run_sequential with the torch-CPU fp32 oracle network, {el:.1f}s, "
-                      f"torch threads={n}; CPU gets no batching gain from depth k, so this is also "
-                      f"its depth-k rate"}
+                      f"{cfg.num_inference_steps} denoise steps each) through {which} with the "
+                      f"torch-CPU fp32 oracle network (oracle/dp_model.py), {el:.1f}s, torch "
+                      f"threads={n}; the CPU path gets no batching gain from depth k, so this is "
+                      f"also its depth-k rate"}
 
 
 def reference_arm(args, dist):
@@ -244,8 +288,8 @@ def reference_arm(args, dist):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 / base["value"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config} DP-CNN policy, sequential CPU requests "
-                                   f"(reference CPU path: oracle port)",
+            "config": {"workload": f"configs[1]: {args.config} DP-CNN policy on the host CPU -- "
+                                   f"reference scheduler + torch-CPU fp32 network, sequential requests",
                        "depth": args.depth, "fetch_offset": args.offset},
             "cpu_baseline": base,
             "e2e": {"value": base["value"], "unit": "actions/s", "h2d_bytes_per_step": 0,
@@ -305,11 +349,13 @@ def main():
     tflops = S_med * flops_sample / (step_ms / 1e3) / 1e12 if step_ms > 0 else 0.0
     tc_peak = float(peaks.get("bf16_tflops_sustained", 1400.0))
 
-    # kernel launches inside the timed region (per frame, from the programs)
-    n_ops = len(LAST_EVENTS["denoiser_ops"])
+    # our kernel launches inside the timed region, per frame, from the programs:
+    # encoder (+ image convert, pools), cond assembly, FiLM GEMV, ring commit,
+    # ring fetch, per-frame control, per-iteration step kernels, finish
     enc_ops = LAST_EVENTS["encoder_launches"]
+    per_iter = LAST_EVENTS["launches_per_iter"]
     iters_per_frame = max(1, -(-cfg.num_inference_steps // args.depth))
-    per_frame = enc_ops + 3 + 1 + 1 + iters_per_frame * (2 + 2 * n_ops) + 1
+    per_frame = enc_ops + 3 + 1 + 1 + iters_per_frame * per_iter + 1
     launches = per_frame * K
 
     out = {"metric": METRIC, "value": value, "unit": "actions/s", "n_gpus": dist.world,
@@ -391,6 +437,7 @@ def _install_capture():
         if self.gen_events:
             LAST_EVENTS["events"] = list(self.gen_events)
         LAST_EVENTS["denoiser_ops"] = list(self.denoiser.ops)
+        LAST_EVENTS["launches_per_iter"] = int(self.lib.auras_unet_launches_per_iter(self.plan))
         LAST_EVENTS["encoder_launches"] = 1 + sum(
             (2 if item[0] == "conv" else 1) for g in self.encoder.groups.values() for item in g)
         orig_close(self)

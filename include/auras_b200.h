@@ -183,6 +183,11 @@ int auras_unet_generate(auras_unet_plan *plan, int S, const int *lanes, const in
                         float *x_lanes, const float *noise_lanes, const int64_t *fetched,
                         int use_graph, void *stream);
 
+/* Kernel launches one denoise iteration issues (megakernel path: the
+ * persistent step kernel + the iteration advance; layer path: prep, a GEMM and
+ * an epilogue per conv op, final, advance).  Negative on error. */
+int auras_unet_launches_per_iter(const auras_unet_plan *plan);
+
 /* Diagnostics: per-task globaltimer trace of the persistent denoise
  * megakernel for batch size S (trace: int64[n_tasks][8]; tasks_out:
  * int32[n_tasks][4] task table or NULL).  Returns n_tasks or < 0. */

@@ -265,7 +265,10 @@ class OracleGeneration:
 
 
 class OracleDP:
-    """Reference-duck-typed policy for oracle/schedule.py (one agent)."""
+    """Reference-duck-typed policy (one agent) for oracle/schedule.py or the
+    unmodified reference scheduler (fp/executor.py:200-461)."""
+
+    kind = "conditioning"          # compares unequal to ContextKind.AUTOREGRESSIVE
 
     def __init__(self, weights, cfg, seed, agent, layer_costs, step_cost):
         w = {k: v.detach().to("cpu", torch.float32) for k, v in weights.items()}

@@ -15,7 +15,7 @@ import threading
 from .errors import DeviceError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libauras_b200.so")
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 DT_F32, DT_BF16 = 0, 1
 ACT_NONE, ACT_RELU, ACT_MISH = 0, 1, 2
@@ -67,6 +67,7 @@ _SIGNATURES = {
     "auras_unet_generate": (C.c_int, [vp, C.c_int, ip, ip, ip, ip, C.c_int, C.c_int, vp, vp, vp,
                                       C.c_int, vp]),
     "auras_unet_mega_trace": (C.c_int, [vp, C.c_int, vp, vp, C.c_int]),
+    "auras_unet_launches_per_iter": (C.c_int, [vp]),
     "auras_conv": (C.c_int, [C.POINTER(ConvOp), C.c_int, C.c_int, vp, C.c_int, vp, i64, vp]),
     "auras_linear": (C.c_int, [C.POINTER(LinearOp), C.c_int, C.c_int, vp, C.c_int, vp, C.c_int, vp]),
     "auras_image_to_nhwc": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int,

@@ -141,7 +141,7 @@ extern "C" {
 
 const char *auras_last_error(void) { return g_err; }
 
-int auras_abi_version(void) { return 3; }
+int auras_abi_version(void) { return 4; }
 
 int auras_device_ok(int device) {
   cudaDeviceProp p;

@@ -262,6 +262,11 @@ int auras_unet_generate(auras_unet_plan *p, int S, const int *lanes, const int *
 
 extern "C" {
 
+int auras_unet_launches_per_iter(const auras_unet_plan *p) {
+  if (!p) return AURAS_E_ARG;
+  return p->use_mega ? 2 : 3 + 2 * (int)p->ops.size();
+}
+
 // Diagnostics: enable a per-task globaltimer trace for the megakernel of batch
 // size S (buffer: int64[n_tasks][8] + int64[grid][1024][3]); returns n_tasks, copies the task table
 // (int32[n_tasks][4]) to `tasks_out` when non-NULL.  Graphs captured before the
