@@ -5,6 +5,7 @@
 // shapes the tcgen05 engine (gemm_sm100.cu) does not take.  The epilogue is
 // shared by both engines.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -306,6 +307,10 @@ int conv_op_to_args(const auras_conv_op &op, int S, int dtype, float *partial, C
     g.engine = 1;
     g.splits = gemm_sm100_splits(g);
     g.kchunk = 0;
+  } else if (dtype == AURAS_DT_BF16 && gemm_gather_supported(g) && !getenv("AURAS_NO_GATHER")) {
+    g.engine = 2;
+    g.splits = gemm_gather_splits(g);
+    g.kchunk = 0;
   } else {
     int kc = (op.Kp + op.splits - 1) / op.splits;
     kc = (kc + 63) / 64 * 64;
@@ -323,6 +328,7 @@ int conv_op_to_args(const auras_conv_op &op, int S, int dtype, float *partial, C
 
 int run_gemm(const ConvGemmArgs &g, int dtype, cudaStream_t st) {
   if (g.engine == 1) return launch_gemm_sm100(g, st);
+  if (g.engine == 2) return launch_gemm_gather(g, st);
   if (dtype == AURAS_DT_BF16) return launch_conv_gemm_simt<__nv_bfloat16>(g, st);
   return launch_conv_gemm_simt<float>(g, st);
 }

@@ -13,7 +13,7 @@ struct ConvGemmArgs {
   int kh, kw, stride, pad_h, pad_w;
   int Ho, Wo;
   int splits, kchunk;
-  int engine;         // 0 SIMT, 1 tcgen05
+  int engine;         // 0 SIMT, 1 tcgen05 + TMA im2col (1-D), 2 tcgen05 + gathered im2col
 };
 
 struct EpiArgs {
@@ -48,6 +48,10 @@ int64_t conv_scratch_floats(const auras_conv_op &op, int S, int dtype);
 // tcgen05 / TMA engine (gemm_sm100.cu)
 bool gemm_sm100_supported(const ConvGemmArgs &g);
 int gemm_sm100_splits(const ConvGemmArgs &g);
+// tcgen05 engine with a thread-gathered im2col operand (gemm_gather_sm100.cu)
+bool gemm_gather_supported(const ConvGemmArgs &g);
+int gemm_gather_splits(const ConvGemmArgs &g);
+int launch_gemm_gather(const ConvGemmArgs &g, cudaStream_t st);
 int launch_gemm_sm100(const ConvGemmArgs &g, cudaStream_t st);
 
 }  // namespace auras

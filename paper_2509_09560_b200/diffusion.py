@@ -375,15 +375,15 @@ class Encoder:
         dev, td = model.dev, model.tdtype
         H = cfg.image_hw
         self.img = torch.zeros(A, cfg.image_channels, H, H, dtype=torch.uint8, device=dev)
-        self.x0 = torch.zeros(A, H, H, 4, dtype=td, device=dev)
+        self.x0 = torch.zeros(A, H, H, 8, dtype=td, device=dev)      # RGB padded to 8 channels
         self.feat = torch.zeros(A, cfg.feat_dim, dtype=torch.float32, device=dev)
         self.groups = {g: [] for g in self.GROUPS}
         self.max_scratch = 0
         w = model.w
         hs = H // 2
         stem = torch.zeros(A, hs, hs, 64, dtype=td, device=dev)
-        wm, cp, kh, kw, kp = model.conv_weight(w["enc.conv1.w"], cin_pad=4)
-        self._add("stem", wm, None, self.x0, 4, 0, H, H, cp, kh, kw, 2, 3, stem, 64, 0, hs, hs,
+        wm, cp, kh, kw, kp = model.conv_weight(w["enc.conv1.w"], cin_pad=8)
+        self._add("stem", wm, None, self.x0, 8, 0, H, H, cp, kh, kw, 2, 3, stem, 64, 0, hs, hs,
                   gn=("enc.gn1", 64 // 16), act=_lib.ACT_RELU)
         hp = (hs - 1) // 2 + 1
         pooled = torch.zeros(A, hp, hp, 64, dtype=td, device=dev)
@@ -454,7 +454,7 @@ class Encoder:
             if gi == 0:
                 _lib.check(lib.auras_image_to_nhwc(self.img.data_ptr(), self.A, cfg.image_channels,
                                                    cfg.image_hw, cfg.image_hw, self.x0.data_ptr(),
-                                                   4, self.m.dt, st), "image_to_nhwc")
+                                                   8, self.m.dt, st), "image_to_nhwc")
             for item in self.groups[g]:
                 if item[0] == "conv":
                     _lib.check(lib.auras_conv(_lib.C.byref(item[1]), self.m.dt, self.A, None, 0,

@@ -92,3 +92,49 @@ def test_fp32_simt_engine_matches_torch():
     out, ref = run_conv1d(x, w, b, 1, 2, dtype="fp32")
     err = (out - ref).abs().max().item() / ref.abs().max().item()
     assert err < 1e-5, err
+
+
+def run_conv2d(x, w, stride, pad, S_agents=None):
+    """x: [S, H, W, Cin] NHWC; w: [Co, Cin, kh, kw]; bf16 operands, tcgen05 gather engine."""
+    lib = _lib.load()
+    S, H, W, Cin = x.shape
+    Co, _, kh, kw = w.shape
+    buf = x.to(torch.bfloat16).contiguous().cuda()
+    wm = w.permute(0, 2, 3, 1).reshape(Co, kh * kw * Cin)
+    Kp = (kh * kw * Cin + 63) // 64 * 64
+    wm = F.pad(wm, (0, Kp - kh * kw * Cin)).to(torch.bfloat16).contiguous().cuda()
+    Ho, Wo = (H + 2 * pad - kh) // stride + 1, (W + 2 * pad - kw) // stride + 1
+    out = torch.zeros(S, Ho, Wo, Co, dtype=torch.float32, device="cuda")
+    op = _lib.ConvOp(w=wm.data_ptr(), bias=0, inp=buf.data_ptr(), out=0, out_f32=out.data_ptr(), M=Co,
+                     Cin=Cin, Kp=Kp, H=H, W=W, in_pitch=Cin, in_coff=0, kh=kh, kw=kw, stride=stride,
+                     pad_h=pad, pad_w=pad, Ho=Ho, Wo=Wo, out_pitch=Co, out_coff=0, groups=1, act=0,
+                     film_off=-1, splits=1)
+    scratch = torch.zeros(64 * S * Ho * Wo * Co + 1024, dtype=torch.float32, device="cuda")
+    st = torch.cuda.current_stream()
+    _lib.check(lib.auras_conv(C.byref(op), _lib.DT_BF16, S, None, 0, scratch.data_ptr(), scratch.numel(),
+                              st.cuda_stream), "conv2d")
+    torch.cuda.synchronize()
+    ref = F.conv2d(buf.float().permute(0, 3, 1, 2), wm[:, :kh * kw * Cin].float().reshape(Co, kh, kw, Cin)
+                   .permute(0, 3, 1, 2), stride=stride, padding=pad).permute(0, 2, 3, 1)
+    return out, ref
+
+
+CASES_2D = [
+    # (S, H, W, Cin, Co, k, stride, pad): the ResNet-18 encoder's conv shapes
+    (1, 96, 96, 8, 64, 7, 2, 3),      # stem (RGB padded to 8 channels)
+    (2, 24, 24, 64, 64, 3, 1, 1),     # layer1
+    (1, 24, 24, 64, 128, 3, 2, 1),    # layer2 first conv
+    (3, 24, 24, 64, 128, 1, 2, 0),    # layer2 downsample
+    (1, 6, 6, 256, 512, 3, 2, 1),     # layer4 first conv (3x3 output)
+    (2, 3, 3, 512, 512, 3, 1, 1),     # layer4
+]
+
+
+@pytest.mark.parametrize("S,H,W,Cin,Co,k,stride,pad", CASES_2D)
+def test_tcgen05_gather_conv2d_matches_torch(S, H, W, Cin, Co, k, stride, pad):
+    torch.manual_seed(H * 7 + Co)
+    x = torch.randn(S, H, W, Cin)
+    w = torch.randn(Co, Cin, k, k) / (Cin * k * k) ** 0.5
+    out, ref = run_conv2d(x, w, stride, pad)
+    err = (out - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 2e-3, err
