@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also report depths 1..8")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--perception-device", type=int, default=None,
+                    help="disaggregated variant: run perception on this GPU and ship context "
+                         "slots to the generation GPU over P2P (may equal the generation GPU)")
     return ap.parse_args()
 
 
@@ -317,7 +320,7 @@ def main():
     weights = D.init_weights(cfg, seed=0, device="cuda")
     n_res = 64
     pol = D.make_diffusion_policy(cfg, dtype=args.dtype, weights=weights, agents=A,
-                                  resident_frames=n_res)
+                                  resident_frames=n_res, perception_device=args.perception_device)
 
     # --- device-resident timed run at depth k
     win, res, fill = run_window(pol, args.depth, args.offset, A, W, K, dist, dist.local)
@@ -370,7 +373,8 @@ def main():
                       "agents_per_gpu": A, "global_batch": A * dist.world,
                       "samples_per_denoise_step": S_med, "parallelism": f"replicas x{dist.world}",
                       "l2": "inputs larger than L2: 488 MB of UNet weights streamed per denoise step",
-                      "inputs": f"{n_res} synthetic frames + request noise pre-staged in HBM"},
+                      "inputs": f"{n_res} synthetic frames + request noise pre-staged in HBM",
+                      "perception_device": args.perception_device},
            "p99_action_latency_ms": p99, "mean_action_latency_ms": jmean,
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                         "frac": achieved / hbm_peak, "traffic": None,

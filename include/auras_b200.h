@@ -54,6 +54,22 @@ int auras_ring_commit(int64_t *meta, int64_t *state, int capacity, int64_t frame
 int auras_ring_fetch(const int64_t *meta, const int64_t *state, int capacity, int64_t target,
                      int64_t *out, int64_t *version_log, int64_t log_index, void *stream);
 
+/* Disaggregated variant (perception GPU != generation GPU): the same commit
+ * with a system-scope release so a consumer on another GPU (or a peer-mapped
+ * reader) observes the payload before the version. */
+int auras_ring_commit_sys(int64_t *meta, int64_t *state, int capacity, int64_t frame,
+                          int64_t expected_version, void *stream);
+
+/* Enable peer access from `device` to `peer` (idempotent). */
+int auras_enable_peer(int device, int peer);
+
+/* Asynchronous pitched copy of `rows` x `width` bytes between device buffers
+ * that may live on different GPUs (unified addressing; NVLink P2P once
+ * auras_enable_peer was called), enqueued on `stream`.  Used to ship a
+ * perception GPU's staged context slots into the generation GPU's ring. */
+int auras_peer_copy(void *dst, int64_t dst_pitch, const void *src, int64_t src_pitch, int64_t width,
+                    int64_t rows, void *stream);
+
 /* Copy `bytes` from device `src` into slot `slot` of the payload ring
  * (ContextStore.publish of a host-built PublicContext). */
 int auras_ring_write(void *payload, int64_t slot_bytes, int slot, const void *src,

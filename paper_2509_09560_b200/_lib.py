@@ -55,6 +55,9 @@ _SIGNATURES = {
     "auras_device_ok": (C.c_int, [C.c_int]),
     "auras_ring_commit": (C.c_int, [vp, vp, C.c_int, i64, i64, vp]),
     "auras_ring_fetch": (C.c_int, [vp, vp, C.c_int, i64, vp, vp, i64, vp]),
+    "auras_ring_commit_sys": (C.c_int, [vp, vp, C.c_int, i64, i64, vp]),
+    "auras_enable_peer": (C.c_int, [C.c_int, C.c_int]),
+    "auras_peer_copy": (C.c_int, [vp, i64, vp, i64, i64, i64, vp]),
     "auras_ring_write": (C.c_int, [vp, i64, C.c_int, vp, i64, vp]),
     "auras_toy_ingest": (C.c_int, [vp, C.c_int, C.POINTER(f64), vp, C.POINTER(f64), vp]),
     "auras_toy_publish": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_int, i64, i64, vp]),

@@ -139,10 +139,13 @@ class ContextStore:
         self._last_frame = frame
         return slot, self._version
 
-    def commit(self, frame: int, version: int, stream) -> None:
+    def commit(self, frame: int, version: int, stream, system_scope: bool = False) -> None:
+        """Release the slot's version.  `system_scope`: the writer runs on another
+        GPU (disaggregated perception), so the release is st.release.sys."""
         lib = _lib.load()
-        _lib.check(lib.auras_ring_commit(self.meta.data_ptr(), self.state.data_ptr(), self.capacity,
-                                         frame, version, stream.cuda_stream), "ring_commit")
+        fn = lib.auras_ring_commit_sys if system_scope else lib.auras_ring_commit
+        _lib.check(fn(self.meta.data_ptr(), self.state.data_ptr(), self.capacity,
+                      frame, version, stream.cuda_stream), "ring_commit")
 
     def resolve(self, frame: int, offset: int = 0):
         """Host half of fetch_entry: (version, context frame, slot)."""

@@ -27,7 +27,8 @@ struct MegaParams {
   long long *trace;         // optional [n_tasks][8] globaltimer stamps (NULL = off)
   int spin_ns;              // back-off between counter polls
   long long *kbtrace;       // optional [grid][1024][3]: per-k-block A ready, B ready, MMA issued
-  int a_depth;              // weight-ring stages actually used (<= MK_NA)
+  int a_depth;              // weight-ring stages actually used (<= na)
+  int na;                   // weight-ring stages (the rest of the ring smem is activations)
 };
 
 struct MegaConfig {

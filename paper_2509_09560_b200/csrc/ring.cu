@@ -49,6 +49,21 @@ __global__ void ring_commit_kernel(int64_t *meta, int64_t *state, int capacity, 
   commit_slot(meta, state, capacity, frame, expected_version);
 }
 
+// System-scope variant for a ring that lives on another GPU.
+__global__ void ring_commit_sys_kernel(int64_t *meta, int64_t *state, int capacity, int64_t frame,
+                                       int64_t expected_version) {
+  const int slot = ring_slot(frame, capacity);
+  const int64_t v = state[0] + 1;
+  if (v != expected_version) state[3] = 1;
+  if (state[1] >= 0 && frame < state[1]) state[3] = 2;
+  meta[2 * slot + 0] = frame;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(&meta[2 * slot + 1]), "l"(v) : "memory");
+  state[0] = v;
+  state[1] = frame;
+  state[2] += 1;
+}
+
 __global__ void ring_fetch_kernel(const int64_t *meta, const int64_t *state, int capacity,
                                   int64_t target, int64_t *out, int64_t *log, int64_t log_index) {
   int slot = ring_slot(target, capacity);
@@ -154,6 +169,40 @@ int auras_ring_commit(int64_t *meta, int64_t *state, int capacity, int64_t frame
   if (!meta || !state || capacity < 2) { set_error("ring_commit: bad args"); return AURAS_E_ARG; }
   ring_commit_kernel<<<1, 1, 0, as_stream(stream)>>>(meta, state, capacity, frame, expected_version);
   AURAS_LAUNCHED("ring_commit_kernel");
+  return AURAS_OK;
+}
+
+int auras_ring_commit_sys(int64_t *meta, int64_t *state, int capacity, int64_t frame,
+                          int64_t expected_version, void *stream) {
+  if (!meta || !state || capacity < 2) { set_error("ring_commit_sys: bad args"); return AURAS_E_ARG; }
+  ring_commit_sys_kernel<<<1, 1, 0, as_stream(stream)>>>(meta, state, capacity, frame, expected_version);
+  AURAS_LAUNCHED("ring_commit_sys_kernel");
+  return AURAS_OK;
+}
+
+int auras_enable_peer(int device, int peer) {
+  if (device == peer) return AURAS_OK;
+  int prev = 0;
+  AURAS_CUDA(cudaGetDevice(&prev));
+  AURAS_CUDA(cudaSetDevice(device));
+  int can = 0;
+  cudaDeviceCanAccessPeer(&can, device, peer);
+  cudaError_t e = can ? cudaDeviceEnablePeerAccess(peer, 0) : cudaErrorPeerAccessUnsupported;
+  if (e == cudaErrorPeerAccessAlreadyEnabled) e = cudaSuccess;
+  cudaGetLastError();
+  cudaSetDevice(prev);
+  return cuda_check(e, "cudaDeviceEnablePeerAccess");
+}
+
+int auras_peer_copy(void *dst, int64_t dst_pitch, const void *src, int64_t src_pitch, int64_t width,
+                    int64_t rows, void *stream) {
+  if (!dst || !src || width < 0 || rows < 0 || dst_pitch < width || src_pitch < width) {
+    set_error("peer_copy: bad args");
+    return AURAS_E_ARG;
+  }
+  if (width == 0 || rows == 0) return AURAS_OK;
+  AURAS_CUDA(cudaMemcpy2DAsync(dst, (size_t)dst_pitch, src, (size_t)src_pitch, (size_t)width, (size_t)rows,
+                               cudaMemcpyDefault, as_stream(stream)));
   return AURAS_OK;
 }
 

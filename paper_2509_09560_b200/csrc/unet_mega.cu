@@ -41,13 +41,16 @@ namespace auras {
 constexpr int MK_THREADS = 384;              // 4 role warps + 8 epilogue warps
 constexpr int MK_EPI = 256;                  // epilogue-unit threads (warps 4-11)
 constexpr int MK_KS = 2;                 // k-blocks (64 wide) per pipeline stage
-constexpr int MK_NA = 5;                 // weight stages (2 x 16 KB each): 160 KB HBM prefetch depth
-constexpr int MK_BN = 128;               // max N per GEMM task
+constexpr int MK_NA = 5;                 // max weight stages (2 x 16 KB each); runtime P.na <= MK_NA
+constexpr int MK_BN = 256;               // max N per GEMM task (TMEM: 2 buffers x 256 columns)
 constexpr int MK_A_BYTES = 128 * 64 * 2;         // one 128 x 64 weight box
 constexpr int MK_A_STAGE = MK_KS * MK_A_BYTES;
-constexpr int MK_B_RING = 48 * 1024;     // activation ring, carved per task into stages of
-constexpr int MK_NBMAX = 12;             //   round_up(bn*128, 1KB) bytes: 3..12 in flight
-constexpr size_t MK_SMEM = 1024 + (size_t)MK_NA * MK_A_STAGE + (size_t)MK_B_RING + 1024 + 4 * 600;
+// smem holds the weight ring (P.na stages) followed by the activation ring
+// (P.bring bytes, carved per task into stages of KS * round_up(bn*128, 1KB)):
+// 160 KB / 48 KB for batches of <= 128 columns, 128 KB / 96 KB beyond.
+constexpr int MK_RINGS = 208 * 1024;
+constexpr int MK_NBMAX = 12;
+constexpr size_t MK_SMEM = 1024 + (size_t)MK_RINGS + 1024 + 4 * 600;
 
 enum { T_GEMM = 0, T_EPI = 1, T_PREP = 2, T_FINAL = 3 };
 
@@ -82,8 +85,9 @@ __global__ void __launch_bounds__(MK_THREADS, 1) unet_mega(const __grid_constant
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = smem;
-  uint8_t *sB = sA + MK_NA * MK_A_STAGE;
-  uint64_t *fullA = reinterpret_cast<uint64_t *>(sB + MK_B_RING);
+  const int NA = P.na;
+  uint8_t *sB = sA + NA * MK_A_STAGE;
+  uint64_t *fullA = reinterpret_cast<uint64_t *>(sA + MK_RINGS);
   uint64_t *emptyA = fullA + MK_NA;
   uint64_t *fullB = emptyA + MK_NA;
   uint64_t *emptyB = fullB + MK_NBMAX;
@@ -100,14 +104,14 @@ __global__ void __launch_bounds__(MK_THREADS, 1) unet_mega(const __grid_constant
   int *prep_done = P.ctr + 2 * P.n_ops;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < MK_NA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], 1); }
+    for (int i = 0; i < NA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], 1); }
     for (int i = 0; i < MK_NBMAX; ++i) { mbar_init(&fullB[i], 1); mbar_init(&emptyB[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(256));
+                 "r"(2 * MK_BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -128,11 +132,11 @@ __global__ void __launch_bounds__(MK_THREADS, 1) unet_mega(const __grid_constant
       const int kb0 = tk.w * kps, kb1 = min(kbt, kb0 + kps);
       const int row0 = tk.y * kbt * 128;          // tiled layout [m_tile][k_block][128][64]
       for (int kb = kb0; kb < kb1; kb += MK_KS, ++ia) {
-        const int st = ia % MK_NA;
+        const int st = ia % NA;
         const int two = kb + 1 < kb1;
-        mbar_wait(&emptyA[st], ((ia / MK_NA) & 1) ^ 1);
-        if (P.a_depth < MK_NA && ia >= P.a_depth)        // optional cap on weights in flight
-          mbar_wait(&emptyA[(ia - P.a_depth) % MK_NA], (((ia - P.a_depth) / MK_NA) & 1));
+        mbar_wait(&emptyA[st], ((ia / NA) & 1) ^ 1);
+        if (P.a_depth < NA && ia >= P.a_depth)           // optional cap on weights in flight
+          mbar_wait(&emptyA[(ia - P.a_depth) % NA], (((ia - P.a_depth) / NA) & 1));
         tma_load_2d_pair_warp(sA + st * MK_A_STAGE, tmA, &fullA[st], (1 + two) * MK_A_BYTES, 0, row0 + kb * 128,
                               row0 + (kb + 1) * 128, two);
       }
@@ -194,9 +198,9 @@ __global__ void __launch_bounds__(MK_THREADS, 1) unet_mega(const __grid_constant
       const int kb0 = tk.w * kps, kb1 = min(kbt, kb0 + kps);
       if (P.trace && lane == 0) P.trace[8 * t + 4] = gtime();
       for (int kb = kb0; kb < kb1; kb += MK_KS, ++ia) {
-        const int sa = ia % MK_NA, sb = ((kb - kb0) / MK_KS) % nbst;
+        const int sa = ia % NA, sb = ((kb - kb0) / MK_KS) % nbst;
         const int nk = min(MK_KS, kb1 - kb);
-        mbar_wait(&fullA[sa], (ia / MK_NA) & 1);
+        mbar_wait(&fullA[sa], (ia / NA) & 1);
         if (P.trace && lane == 0 && kb == kb0) P.trace[8 * t + 5] = gtime();
         long long *kt = (P.kbtrace && ia < 1024) ? P.kbtrace + ((int64_t)blockIdx.x * 1024 + ia) * 3 : nullptr;
         if (kt && lane == 0) kt[0] = gtime();
@@ -321,7 +325,7 @@ __global__ void __launch_bounds__(MK_THREADS, 1) unet_mega(const __grid_constant
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * MK_BN));
 }
 
 // ---------------------------------------------------------------- host side
@@ -389,6 +393,12 @@ int mega_build(MegaConfig &mc, const std::vector<auras_conv_op> &ops, int S, con
   const char *rs = getenv("AURAS_MEGA_RESERVE");
   const int reserve = rs ? atoi(rs) : 8;
   sms = std::max(16, sms - std::max(0, reserve));
+  // ring split: wide batches (> 128 columns per task) trade weight prefetch for activation stages
+  int rows_max = 0;
+  for (const auto &o : ops) rows_max = std::max(rows_max, std::min(S, MK_BN / o.Wo) * o.Wo);
+  const int bn_max = rows_max > 128 ? MK_BN : 128;
+  const int na = bn_max > 128 ? 4 : MK_NA;
+  const int bring = MK_RINGS - na * MK_A_STAGE;
   std::vector<MegaOp> hops(n);
   std::vector<int64_t> part_off(n);
   int64_t part_total = 0;
@@ -402,12 +412,12 @@ int mega_build(MegaConfig &mc, const std::vector<auras_conv_op> &ops, int S, con
     if (rc) return rc;
     if (!gemm_sm100_supported(g)) { set_error("megakernel: op %d not supported by the tcgen05 engine", i); return AURAS_E_ARG; }
     m.M = o.M; m.N = S * o.Wo; m.Cin = o.Cin; m.Wo = o.Wo; m.stride = o.stride; m.pad = o.pad_w; m.S = S;
-    m.s_box = std::min(S, MK_BN / o.Wo);
+    m.s_box = std::min(S, bn_max / o.Wo);
     m.rows = m.s_box * o.Wo;
     m.bn = (m.rows + 15) / 16 * 16;
     m.kb_total = o.Kp / 64;
     m.bstage = (m.bn * 128 + 1023) / 1024 * 1024;
-    m.nbst = std::min(MK_NBMAX, MK_B_RING / (MK_KS * m.bstage));
+    m.nbst = std::min(MK_NBMAX, bring / (MK_KS * m.bstage));
     if (m.nbst < 1) { set_error("megakernel: B stage too large"); return AURAS_E_ARG; }
     const int m_tiles = (o.M + 127) / 128, n_tiles = (S + m.s_box - 1) / m.s_box;
     // split-K: enough CTAs to stream big layers at full HBM rate, but at least
@@ -503,7 +513,8 @@ int mega_build(MegaConfig &mc, const std::vector<auras_conv_op> &ops, int S, con
   const char *sn = getenv("AURAS_MEGA_SPIN_NS");
   mc.params.spin_ns = sn ? atoi(sn) : 0;
   const char *ad = getenv("AURAS_MEGA_A_DEPTH");
-  mc.params.a_depth = ad ? std::max(1, std::min(MK_NA, atoi(ad))) : MK_NA;
+  mc.params.na = na;
+  mc.params.a_depth = ad ? std::max(1, std::min(na, atoi(ad))) : na;
   static bool attr = false;
   if (!attr) {
     AURAS_CUDA(cudaFuncSetAttribute(unet_mega, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MK_SMEM));

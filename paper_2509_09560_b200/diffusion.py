@@ -310,13 +310,13 @@ def _round(x, m):
 class DeviceModel:
     """Weights converted once into the kernels' layouts on the device."""
 
-    def __init__(self, cfg: DPConfig, weights: dict, dtype: str):
+    def __init__(self, cfg: DPConfig, weights: dict, dtype: str, device=None):
         import torch
         self.torch = torch
         self.cfg = cfg
         self.dt = _lib.DT_BF16 if dtype == "bf16" else _lib.DT_F32
         self.tdtype = torch.bfloat16 if dtype == "bf16" else torch.float32
-        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         self.keep = []
         w = {k: v.to(self.dev, torch.float32) for k, v in weights.items()}
         self.w = w
@@ -664,6 +664,7 @@ class DPGeneration:
     weights: dict = field(repr=False, compare=False, hash=False)
     step_cost: float = 1.0
     use_graph: bool = True
+    perception_device: Optional[int] = None     # disaggregated: encoder on this GPU
     kind: ContextKind = ContextKind.CONDITIONING
 
     @property
@@ -698,6 +699,11 @@ class DPPolicy(Policy):
     agents: int = 1
     resident_frames: int = 0        # >0: synthetic inputs pre-staged in HBM, cycled mod N
 
+    @property
+    def perception_device(self):
+        """GPU running perception when disaggregated (None: same GPU as generation)."""
+        return self.generation.perception_device
+
     def synthetic_observation(self, agent, frame):
         if self.resident_frames:
             return Observation(frame=frame, vector=None, image=None)
@@ -705,6 +711,15 @@ class DPPolicy(Policy):
 
 
 _MODEL_CACHE = {}
+
+
+def _device_model(gen, device):
+    key = (id(gen.weights), gen.dtype, device)
+    if key not in _MODEL_CACHE:
+        for k in [k for k in _MODEL_CACHE if k[:2] != key[:2]]:
+            del _MODEL_CACHE[k]
+        _MODEL_CACHE[key] = DeviceModel(gen.cfg, gen.weights, gen.dtype, device)
+    return _MODEL_CACHE[key]
 
 
 class DPSession:
@@ -723,18 +738,28 @@ class DPSession:
         self.cfg, self.gen = cfg, gen
         self.p, self.g = p_stream, g_stream
         self.A, self.R = agents, lanes
-        dev = torch.device("cuda", torch.cuda.current_device())
-        key = (id(gen.weights), gen.dtype)
-        if key not in _MODEL_CACHE:
-            _MODEL_CACHE.clear()
-            _MODEL_CACHE[key] = DeviceModel(cfg, gen.weights, gen.dtype)
-        self.model = _MODEL_CACHE[key]
+        gd = torch.cuda.current_device()
+        dev = torch.device("cuda", gd)
+        # Disaggregated variant: encoder, FiLM projection and the
+        # slot staging buffer live on the perception GPU; the staged slot is
+        # shipped into this GPU's ring by a P2P copy on the perception stream and
+        # released at system scope.  pd == gd exercises the same code path.
+        self.disagg = gen.perception_device is not None
+        self.gd = gd
+        self.pd = gd if gen.perception_device is None else int(gen.perception_device)
+        pdev = torch.device("cuda", self.pd)
+        if self.disagg and self.pd != gd:
+            _lib.check(self.lib.auras_enable_peer(self.pd, gd), "enable_peer")
+            _lib.check(self.lib.auras_enable_peer(gd, self.pd), "enable_peer")
+        self.model = _device_model(gen, gd)
+        self.pmodel = _device_model(gen, self.pd) if self.pd != gd else self.model
         self.gc_pad = _round(cfg.gc_dim, 8)
         _, F = film_layout(cfg)
         self.slot_floats = self.gc_pad + F
         self.store = ContextStore(capacity, slot_elems=self.slot_floats, agents=agents,
                                   dtype=torch.float32, device=dev)
-        self.encoder = Encoder(self.model, agents)
+        with torch.cuda.device(self.pd):
+            self.encoder = Encoder(self.pmodel, agents)
         s_max = agents * max(1, lanes)
         s_max = min(s_max, 64)
         self.denoiser = Denoiser(self.model, s_max, self.store, self.gc_pad, gen.use_graph)
@@ -764,13 +789,18 @@ class DPSession:
         if cfg.scheduler == "ddpm":
             self.noise = torch.zeros(agents, lanes, cfg.num_inference_steps, hr, dtype=torch.float32,
                                      device=dev)
-        self.pos = torch.zeros(agents, cfg.agent_pos_dim, dtype=torch.float32, device=dev)
-        self.prev = torch.zeros(agents, cfg.feat_dim + cfg.agent_pos_dim, dtype=torch.float32, device=dev)
+        self.pos = torch.zeros(agents, cfg.agent_pos_dim, dtype=torch.float32, device=pdev)
+        self.prev = torch.zeros(agents, cfg.feat_dim + cfg.agent_pos_dim, dtype=torch.float32, device=pdev)
         self.first = True
         self.out = torch.zeros(max(1, max_outputs), agents, hr, dtype=torch.float32, device=dev)
         self.fetched = torch.zeros(3, dtype=torch.int64, device=dev)
         self.version_log = torch.zeros(max(1, max_frames), dtype=torch.int64, device=dev)
-        self.film_op = _lib.LinearOp(w=self.denoiser.film_o.data_ptr(), bias=0, M=self.denoiser.F,
+        self.film_o = self.denoiser.film_o
+        self.stage = None
+        if self.disagg:
+            self.film_o = self.film_o.to(pdev)
+            self.stage = torch.zeros(agents, self.slot_floats, dtype=torch.float32, device=pdev)
+        self.film_op = _lib.LinearOp(w=self.film_o.data_ptr(), bias=0, M=self.denoiser.F,
                                      K=cfg.gc_dim, mish_in=1, ldw=self.gc_pad)
         self.resident = None
         if getattr(policy, "resident_frames", 0):
@@ -797,65 +827,84 @@ class DPSession:
             xs.append(np.stack([x.reshape(-1) for x, _ in noise]))
             if cfg.scheduler == "ddpm":
                 zs.append(np.stack([z.reshape(cfg.num_inference_steps, -1) for _, z in noise]))
-        self.resident = {"img": torch.from_numpy(np.stack(imgs)).to(dev),
-                         "pos": torch.from_numpy(np.stack(pos)).to(dev),
+        pdev = self.pos.device
+        self.resident = {"img": torch.from_numpy(np.stack(imgs)).to(pdev),
+                         "pos": torch.from_numpy(np.stack(pos)).to(pdev),
                          "x": torch.from_numpy(np.stack(xs)).to(dev),
                          "z": torch.from_numpy(np.stack(zs)).to(dev) if zs else None,
                          "n": n}
 
     # -- ingest: frames to HBM, request randomness to its lane
     def ingest(self, t, lane, observations):
+        """Frames -> the perception GPU (P stream); the request's x_T and DDPM
+        noise -> its lane on the generation GPU.  Colocated, everything rides P
+        (the engine orders P after the lane's previous finish); disaggregated,
+        the lane upload rides G, which already runs after that finish."""
         torch = self.torch
         cfg = self.cfg
         if len(observations) != self.A:
             raise ShapeMismatch(f"{len(observations)} observations for {self.A} agents")
-        with torch.cuda.stream(self.p):
-            if observations[0].image is None:
-                if self.resident is None:
-                    raise ShapeMismatch("observation without an image and no resident inputs")
-                r, i = self.resident, t % self.resident["n"]
+        lane_stream = self.g if self.disagg else self.p
+        if observations[0].image is None:
+            if self.resident is None:
+                raise ShapeMismatch("observation without an image and no resident inputs")
+            r, i = self.resident, t % self.resident["n"]
+            with torch.cuda.stream(self.p):
                 self.encoder.img.copy_(r["img"][i], non_blocking=True)
                 self.pos.copy_(r["pos"][i], non_blocking=True)
+            with torch.cuda.stream(lane_stream):
                 self.x[:, lane].copy_(r["x"][i], non_blocking=True)
                 if self.noise is not None:
                     self.noise[:, lane].copy_(r["z"][i], non_blocking=True)
-                return
-            imgs = np.stack([o.image for o in observations])
-            if imgs.shape[1:] != (cfg.image_channels, cfg.image_hw, cfg.image_hw):
-                raise ShapeMismatch(f"image shape {imgs.shape[1:]}")
+            return
+        imgs = np.stack([o.image for o in observations])
+        if imgs.shape[1:] != (cfg.image_channels, cfg.image_hw, cfg.image_hw):
+            raise ShapeMismatch(f"image shape {imgs.shape[1:]}")
+        pos = np.stack([np.asarray(o.vector, dtype=np.float32) for o in observations])
+        if pos.shape[1] != cfg.agent_pos_dim:
+            raise ShapeMismatch(f"agent_pos width {pos.shape[1]} != {cfg.agent_pos_dim}")
+        with torch.cuda.stream(self.p):
             self.encoder.img.copy_(torch.from_numpy(imgs).pin_memory(), non_blocking=True)
-            pos = np.stack([np.asarray(o.vector, dtype=np.float32) for o in observations])
-            if pos.shape[1] != cfg.agent_pos_dim:
-                raise ShapeMismatch(f"agent_pos width {pos.shape[1]} != {cfg.agent_pos_dim}")
             self.pos.copy_(torch.from_numpy(pos).pin_memory(), non_blocking=True)
-            xs, zs = [], []
-            for a in range(self.A):
-                xT, z = request_noise(cfg, self.gen.seed, a, t)
-                xs.append(xT.reshape(-1))
-                if z is not None:
-                    zs.append(z.reshape(cfg.num_inference_steps, -1))
+        xs, zs = [], []
+        for a in range(self.A):
+            xT, z = request_noise(cfg, self.gen.seed, a, t)
+            xs.append(xT.reshape(-1))
+            if z is not None:
+                zs.append(z.reshape(cfg.num_inference_steps, -1))
+        with torch.cuda.stream(lane_stream):
             self.x[:, lane].copy_(torch.from_numpy(np.stack(xs)).pin_memory(), non_blocking=True)
             if self.noise is not None:
                 self.noise[:, lane].copy_(torch.from_numpy(np.stack(zs)).pin_memory(), non_blocking=True)
 
     def perceive(self, lane, lo, hi):
-        self.encoder.run(lo, hi, self.p)
+        with self.torch.cuda.device(self.pd):
+            self.encoder.run(lo, hi, self.p)
 
     def publish(self, lane, frame, slot, version):
         st = self.store
-        payload = st.payload
-        base = payload.data_ptr() + 4 * slot * self.slot_floats
-        agent_stride = st.capacity * self.slot_floats
-        _lib.check(self.lib.auras_dp_assemble_cond(
-            self.encoder.feat.data_ptr(), self.pos.data_ptr(), self.prev.data_ptr(), self.A,
-            self.cfg.feat_dim, self.cfg.agent_pos_dim, self.cfg.n_obs_steps, int(self.first), base,
-            agent_stride, self.p.cuda_stream), "assemble_cond")
-        self.first = False
-        # FiLM projection of the new context, once per publish, into the slot
-        _lib.check(self.lib.auras_linear(_lib.C.byref(self.film_op), self.model.dt, self.A, base,
-                                         agent_stride, base + 4 * self.gc_pad, agent_stride,
-                                         self.p.cuda_stream), "film projection")
-        st.commit(frame, version, self.p)
+        with self.torch.cuda.device(self.pd):
+            ring = st.payload.data_ptr() + 4 * slot * self.slot_floats
+            ring_stride = st.capacity * self.slot_floats
+            if self.disagg:
+                base, stride = self.stage.data_ptr(), self.slot_floats
+            else:
+                base, stride = ring, ring_stride
+            _lib.check(self.lib.auras_dp_assemble_cond(
+                self.encoder.feat.data_ptr(), self.pos.data_ptr(), self.prev.data_ptr(), self.A,
+                self.cfg.feat_dim, self.cfg.agent_pos_dim, self.cfg.n_obs_steps, int(self.first), base,
+                stride, self.p.cuda_stream), "assemble_cond")
+            self.first = False
+            # FiLM projection of the new context, once per publish, into the slot
+            _lib.check(self.lib.auras_linear(_lib.C.byref(self.film_op), self.pmodel.dt, self.A, base,
+                                             stride, base + 4 * self.gc_pad, stride,
+                                             self.p.cuda_stream), "film projection")
+            if self.disagg:
+                # one pitched P2P copy: A staged slots -> slot `slot` of each agent's ring
+                _lib.check(self.lib.auras_peer_copy(ring, 4 * ring_stride, base, 4 * stride,
+                                                    4 * self.slot_floats, self.A, self.p.cuda_stream),
+                           "peer slot copy")
+            st.commit(frame, version, self.p, system_scope=self.disagg)
 
     def fetch(self, target, log_index):
         self.store.device_fetch(target, self.fetched, self.version_log, log_index, self.g)
@@ -912,12 +961,15 @@ class DPSession:
 
 def make_diffusion_policy(config="pusht", dtype: str = "bf16", seed: int = 0, weights=None,
                           agents: int = 1, use_graph: bool = True, resident_frames: int = 0,
-                          **overrides) -> DPPolicy:
+                          perception_device: Optional[int] = None, **overrides) -> DPPolicy:
     """Diffusion Policy CNN on the B200 behind the reference's Policy interface.
 
     `config`: a preset name ("tiny", "pusht", "dp_default") or a DPConfig.
     `dtype`: "bf16" (tensor-core path) or "fp32" (reference-precision path).
-    `weights`: a dict from `init_weights` (default: init_weights(cfg, seed))."""
+    `weights`: a dict from `init_weights` (default: init_weights(cfg, seed)).
+    `perception_device`: run perception on this GPU and ship each context slot
+    into the generation GPU's ring over NVLink P2P (the disaggregated variant);
+    None keeps both stages on the current GPU."""
     cfg = PRESETS[config] if isinstance(config, str) else config
     if overrides:
         cfg = replace(cfg, **overrides)
@@ -930,6 +982,6 @@ def make_diffusion_policy(config="pusht", dtype: str = "bf16", seed: int = 0, we
     step_gflop = unet_flops_per_sample(cfg) / 1e9
     perception = DPPerception(layer_costs=tuple(gflop), obs_width=cfg.agent_pos_dim)
     generation = DPGeneration(cfg=cfg, dtype=dtype, seed=seed, weights=weights, step_cost=step_gflop,
-                              use_graph=use_graph)
+                              use_graph=use_graph, perception_device=perception_device)
     return DPPolicy(perception=perception, generation=generation, agents=agents,
                     resident_frames=resident_frames)

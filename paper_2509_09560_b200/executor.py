@@ -192,7 +192,11 @@ class _Device:
             else (0, -1)
         import os
         gprio = -1 if os.environ.get("AURAS_G_PRIORITY", "1") == "1" else 0
-        self.P = torch.cuda.Stream(priority=0)
+        # disaggregated policies put perception (P) on their own GPU; events carry
+        # the cross-device ordering
+        pd = getattr(policy, "perception_device", None)
+        self.disagg = pd is not None
+        self.P = torch.cuda.Stream(device=pd, priority=0) if self.disagg else torch.cuda.Stream(priority=0)
         self.G = torch.cuda.Stream(priority=gprio)
         self.session = policy.open_session(capacity=capacity, lanes=lanes, agents=agents,
                                            max_outputs=max_outputs, max_frames=max_frames,
@@ -226,7 +230,9 @@ class _Device:
         if self.interleave and self.last_gen_end is not None:
             self.P.wait_event(self.last_gen_end)
         if self.clock == "device":
-            ev = self.event(self.P, timing=True)
+            # frame clocks are G-device events when P lives on another GPU
+            # (elapsed_time needs both events on one device)
+            ev = self.event(self.G if self.disagg else self.P, timing=True)
             self.t_start[t] = ev
             if self.origin is None:
                 self.origin = ev

@@ -105,3 +105,34 @@ def test_pusht_bf16_matches_oracle():
     ref = oracle_run(pol, cfg, 3)
     err = rel_err(res.actions, ref.actions)
     assert err <= TOL["bf16"], err
+
+
+@pytest.mark.parametrize("agents", [1, 3])
+def test_disaggregated_path_matches_colocated(agents):
+    """Disaggregated variant (perception GPU -> P2P slot copy -> system-scope
+    release into the generation GPU's ring), run with both roles on GPU 0
+    (every run here has one GPU): same actions bit for bit, same versions,
+    and within tolerance of the oracle."""
+    w = weights("tiny")
+    cfg = dict(pp_perception=1, pp_generation=3, fetch_offset=-1)
+    kw = dict(dtype="fp32", weights=w, agents=agents)
+    a = run_pipelined(PipelineConfig(**cfg), D.make_diffusion_policy("tiny", **kw), None, 9, agents=agents)
+    b = run_pipelined(PipelineConfig(**cfg), D.make_diffusion_policy("tiny", perception_device=0, **kw),
+                      None, 9, agents=agents)
+    for x, y in zip(a.agent_actions, b.agent_actions):
+        assert np.array_equal(np.array([r.values for r in x]), np.array([r.values for r in y]))
+    assert [r.context_versions for r in a.requests] == [r.context_versions for r in b.requests]
+    assert np.array_equal(a.device_versions, b.device_versions)
+    ref = oracle_run(D.make_diffusion_policy("tiny", **kw), cfg, 9)
+    assert rel_err(b.agent_actions[0], ref.actions) <= TOL["fp32"]
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs")
+def test_disaggregated_two_gpus():
+    w = weights("tiny")
+    cfg = dict(pp_perception=1, pp_generation=2, fetch_offset=0)
+    pol = D.make_diffusion_policy("tiny", dtype="fp32", weights=w, perception_device=1)
+    res = run_pipelined(PipelineConfig(**cfg), pol, None, 8, clock="device")
+    ref = oracle_run(pol, cfg, 8)
+    assert [r.context_versions for r in res.requests] == [r.context_versions for r in ref.requests]
+    assert rel_err(res.actions, ref.actions) <= TOL["fp32"]
