@@ -1,0 +1,126 @@
+// Cluster (DSMEM) helpers and the host interface of the cluster denoise
+// megakernel (unet_cluster.cu).
+#pragma once
+#include <cuda.h>
+
+#include <vector>
+
+#include "conv.cuh"
+#include "mega.cuh"
+#include "tc_util.cuh"
+#include "unet.cuh"
+
+namespace auras {
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+// Whole-cluster barrier; every thread of every CTA must execute it.
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Address of the same shared-memory offset in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+__device__ __forceinline__ void st_cluster_v4_b32(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+
+__device__ __forceinline__ void st_cluster_v2(uint32_t addr, float a, float b) {
+  asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
+}
+
+__device__ __forceinline__ void st_release_i32(int *p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Release-ordered counter increment (prior writes ordered by a CTA barrier
+// become visible before the increment), one instruction instead of
+// __threadfence + atomicAdd.
+__device__ __forceinline__ void red_release_add(int *p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAITC:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONEC;\n"
+      "bra LAB_WAITC;\n"
+      "DONEC:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Barrier among the epilogue warps of all CTAs of the cluster: every warp
+// releases its prior (local and remote) shared-memory writes at cluster scope
+// and arrives once on each CTA's barrier (expected count = 8 CTAs x 8 warps),
+// then waits for its own barrier's phase.
+__device__ __forceinline__ void cluster_barrier_warp(uint64_t *bar, uint32_t parity, int lane) {
+  asm volatile("fence.acq_rel.cluster;" ::: "memory");
+  __syncwarp();
+  if (lane < 8) {
+    const uint32_t r = mapa_shared(smem_u32(bar), lane);
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
+  }
+  mbar_wait_cluster(bar, parity);
+}
+
+// ---------------------------------------------------------------- host interface
+struct ClOp;
+struct ClParams {
+  const ClOp *ops;
+  const int4 *tasks;
+  const int *cl_begin;      // per-cluster task ranges
+  int *ctr;                 // [n_ops] tile completions x 8, [1] prep, then pair flags
+  int *flags;
+  float2 *gstats;           // per tile of a 256-channel GroupNorm: (mean, M2) per sample
+  int n_ops, S, nc, n_tasks;
+  UnetDev *dev;
+  auras_sched sched;
+  int horizon, adim;
+  __nv_bfloat16 *xin;
+  int x_pitch;
+  int64_t ring_slot_stride, ring_agent_stride;
+  const __nv_bfloat16 *y_final;
+  int y_pitch, final_cin;
+  const float *wf, *bf;
+  long long *trace;         // optional [n_tasks][8] globaltimer stamps
+};
+
+struct ClConfig {
+  ClOp *ops = nullptr;
+  int4 *tasks = nullptr;
+  int *cl_begin = nullptr;
+  int *ctr = nullptr;
+  float2 *gstats = nullptr;
+  int ctr_ints = 0, n_ops = 0, n_tasks = 0, nc = 0, S = 0;
+  ClParams params;
+};
+
+int clus_build(ClConfig &cc, const std::vector<auras_conv_op> &ops, int S, const void *x_in,
+               const ClParams &base, const float *film_tau, int film_width, const float *ring_film,
+               TiledCache &cache);
+int clus_launch(const ClConfig &cc, cudaStream_t st);
+int clus_set_trace(ClConfig &cc, long long *trace);
+void clus_free(ClConfig &cc);
+
+}  // namespace auras

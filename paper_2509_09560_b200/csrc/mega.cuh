@@ -1,5 +1,7 @@
 // Host interface of the persistent denoise megakernel (unet_mega.cu).
 #pragma once
+#include <cuda.h>
+
 #include <utility>
 #include <vector>
 
@@ -49,6 +51,9 @@ int mega_build(MegaConfig &mc, const std::vector<auras_conv_op> &ops, int S, con
                const MegaParams &base, const float *film_tau, int film_width, const float *ring_film,
                TiledCache &cache);
 void mega_free_tiled(TiledCache &cache);
+// weights re-laid out as [m_tile][k_block][128][64] (cached per plan) and their tensor map
+int tiled_weights(TiledCache &cache, const auras_conv_op &o, void **out);
+int make_tiled_weight_map(CUtensorMap *tm, const void *wt, int rows_total);
 int mega_launch(const MegaConfig &mc, cudaStream_t st);
 int mega_set_trace(MegaConfig &mc, long long *trace);
 void mega_free(MegaConfig &mc);

@@ -1,0 +1,796 @@
+// Cluster dataflow megakernel: one launch runs a whole denoise step of the
+// ConditionalUnet1D for all S in-flight samples, with
+// split-K reduction and GroupNorm statistics kept on chip.
+//
+// Why a second design (unet_mega.cu is the first): there, split-K partials go
+// through L2 and a separate epilogue unit reduces them, so every layer of the
+// 34-deep dependency chain pays drain -> HBM/L2 round trip -> epilogue ->
+// counter -> next layer, ~12-18 us per layer under a saturated weight stream.
+// Here a thread-block CLUSTER of 8 CTAs owns an output tile (128 channels x
+// up to 64 columns) of one conv; its 8 CTAs split K 8 ways, and
+//
+//   * each CTA's tcgen05 accumulator (TMEM) is pushed row-slice-wise into the
+//     owning CTA's shared memory over DSMEM (reduce-scatter: CTA r owns
+//     channels 16r..16r+15 of the tile);
+//   * the owner sums the 8 slices in a fixed order (deterministic), adds the
+//     bias, and computes GroupNorm statistics of 8-channel atoms; atom
+//     statistics (mean, M2) are exchanged over DSMEM and merged per group
+//     (Chan's formula, fixed order).  Groups of 256 channels span two tiles:
+//     the pair of clusters exchanges tile statistics through global memory;
+//   * GroupNorm affine, Mish/ReLU, FiLM (per-sample rows gathered from the
+//     timestep table and the context ring slot the sample fetched), residual
+//     and the (optionally zero-stuffed) bf16 / fp32 store run in the same
+//     warps, then one release per CTA on the op's completion counter.
+//
+// Warp roles per CTA (384 threads): warp 0 weight TMA producer (never waits on
+// data -- the HBM weight stream runs ahead across layers), warp 1 MMA issuer,
+// warp 2 activation (implicit im2col) TMA producer gated on the producing
+// ops' counters, warps 4-11 epilogue (4-7 also drain TMEM).  Each cluster
+// walks a static list of tile tasks in layer order; the grid is as many
+// clusters as fit co-resident.  Deadlock freedom: tasks only wait on strictly
+// earlier ops, except a GroupNorm pair, which is scheduled on two clusters in
+// the same round (see clus_build).
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "epi.cuh"
+#include "tc_util.cuh"
+#include "unet.cuh"
+#include "mega.cuh"
+#include "cluster.cuh"
+
+#include <cuda_fp16.h>
+
+namespace auras {
+
+constexpr int CL = 8;                     // CTAs per cluster (portable maximum)
+constexpr int CK_THREADS = 384;
+constexpr int CK_EPI = 256;
+constexpr int CK_BN = 64;                 // max columns per tile task (TMEM: 2 x 64 columns)
+constexpr int CK_A_BYTES = 128 * 64 * 2;  // one 128 x 64 weight box
+constexpr int CK_A_STAGE = 2 * CK_A_BYTES;
+constexpr int CK_NA = 4;                  // weight stages (2 k-blocks each)
+constexpr int CK_BRING = 48 * 1024;       // activation ring (1 k-block per stage)
+constexpr int CK_NBMAX = 16;
+constexpr int CK_RSH = 72;                // receive-buffer row stride (halves; 144 B)
+constexpr int CK_OS = 17;                 // staging row stride (floats)
+constexpr int CK_SMAX = 16;               // max samples per tile
+
+constexpr int OFF_B = CK_NA * CK_A_STAGE;
+constexpr int OFF_RECV = OFF_B + CK_BRING;
+constexpr int RECV_BYTES = CL * 16 * CK_RSH * 2;   // one buffer; two alternate by task
+constexpr int OFF_STATS = OFF_RECV + 2 * RECV_BYTES;
+constexpr int OFF_RBUF = OFF_STATS + CL * 2 * CK_SMAX * 8;
+constexpr int OFF_OBUF = OFF_RBUF + CK_BN * CK_OS * 4;
+constexpr int OFF_MR = OFF_OBUF + CK_BN * CK_OS * 4;
+constexpr int OFF_EPS = OFF_MR + 2 * CK_SMAX * 8;
+constexpr int OFF_BAR = OFF_EPS + 512 * 4;
+constexpr int CK_NBARS = 2 * CK_NA + 2 * CK_NBMAX + 2 + 2 + 2;
+constexpr size_t CK_SMEM = 1024 + OFF_BAR + CK_NBARS * 8 + 16;
+
+enum { K_GEMM = 0, K_PREP = 2, K_FINAL = 3 };
+
+struct alignas(64) ClOp {
+  CUtensorMap tmA;
+  CUtensorMap tmB;
+  EpiArgs epi;
+  int M, Cin, Wo, stride, pad, s_box, rows, bn, kb_total, kps, m_tiles, tiles;
+  int bstage, nbst;
+  int gn, cg, pair, flag_base;
+  int lwo, lbn, lsb, lcg;     // log2 of Wo, bn, s_box, cg (all powers of two)
+  int gemm_dep[3], gemm_tgt[3];
+  int epi_dep[2], epi_tgt[2];
+};
+
+__device__ __forceinline__ long long ck_time() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void ck_spin(const int *ctr, int target) {
+  while (ld_acquire_i32(ctr) < target) {
+  }
+}
+
+__device__ __forceinline__ void ck_wait_dep(const ClParams &P, const int *prep_done, int d, int tgt) {
+  if (d == -2) ck_spin(prep_done, P.S);
+  else if (d >= 0) ck_spin(&P.ctr[d], tgt);
+}
+
+// Equal-count merge of k (mean, M2) pairs of n0 values each (fixed order).
+__device__ __forceinline__ float2 merge_equal(const float2 *st, int stride, int k, float n0) {
+  float m = 0.f;
+  for (int i = 0; i < k; ++i) m += st[i * stride].x;
+  m /= (float)k;
+  float q = 0.f, d2 = 0.f;
+  for (int i = 0; i < k; ++i) {
+    q += st[i * stride].y;
+    const float d = st[i * stride].x - m;
+    d2 += d * d;
+  }
+  return make_float2(m, q + n0 * d2);
+}
+
+__global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_constant__ ClParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1 KB alignment by an offset from the __shared__ array itself, so every
+  // derived pointer stays in the shared window (LDS/STS, not generic LD/ST)
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t *sA = smem;
+  uint8_t *sB = smem + OFF_B;
+  __half *recv = reinterpret_cast<__half *>(smem + OFF_RECV);
+  float2 *stats = reinterpret_cast<float2 *>(smem + OFF_STATS);
+  float *rbuf = reinterpret_cast<float *>(smem + OFF_RBUF);
+  float *obuf = reinterpret_cast<float *>(smem + OFF_OBUF);
+  float2 *mr = reinterpret_cast<float2 *>(smem + OFF_MR);
+  float *eps = reinterpret_cast<float *>(smem + OFF_EPS);
+  uint64_t *fullA = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
+  uint64_t *emptyA = fullA + CK_NA;
+  uint64_t *fullB = emptyA + CK_NA;
+  uint64_t *emptyB = fullB + CK_NBMAX;
+  uint64_t *tfull = emptyB + CK_NBMAX;
+  uint64_t *tempty = tfull + 2;
+  uint64_t *cbar = tempty + 2;             // [0] after the accumulator push, [1] after the statistics push
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(cbar + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)cluster_ctarank();
+  const int cid = blockIdx.x / CL;
+  const int t0 = P.cl_begin[cid], t1 = P.cl_begin[cid + 1];
+  int *done = P.ctr;
+  int *prep_done = P.ctr + P.n_ops;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < CK_NA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], 1); }
+    for (int i = 0; i < CK_NBMAX; ++i) { mbar_init(&fullB[i], 1); mbar_init(&emptyB[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    for (int i = 0; i < 2; ++i) mbar_init(&cbar[i], CL * 8);      // 8 epilogue warps of each of 8 CTAs
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * CK_BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync_all();                       // peers' barriers initialised before any remote arrive
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ weights: this CTA's K share of every task
+    int ia = 0;
+    for (int t = t0; t < t1; ++t) {
+      const int4 tk = P.tasks[t];
+      if ((tk.x & 0xff) != K_GEMM) continue;
+      const ClOp *op = &P.ops[tk.x >> 8];
+      const int kps = op->kps, kbt = op->kb_total;
+      const CUtensorMap *tmA = &op->tmA;
+      const int kb0 = rank * kps, kb1 = min(kbt, kb0 + kps);
+      const int row0 = tk.y * kbt * 128;            // tiled layout [m_tile][k_block][128][64]
+      for (int kb = kb0; kb < kb1; kb += 2, ++ia) {
+        const int st = ia % CK_NA;
+        const int two = kb + 1 < kb1;
+        mbar_wait(&emptyA[st], ((ia / CK_NA) & 1) ^ 1);
+        tma_load_2d_pair_warp(sA + st * CK_A_STAGE, tmA, &fullA[st], (1 + two) * CK_A_BYTES, 0, row0 + kb * 128,
+                              row0 + (kb + 1) * 128, two);
+      }
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------ activations: after the producing ops
+    uint32_t par = 0;
+    for (int t = t0; t < t1; ++t) {
+      const int4 tk = P.tasks[t];
+      if ((tk.x & 0xff) != K_GEMM) continue;
+      const ClOp *op = &P.ops[tk.x >> 8];
+      const int bstage = op->bstage, nbst = op->nbst;
+      const int kps = op->kps, kbt = op->kb_total, Cin = op->Cin, pad = op->pad, stride = op->stride;
+      const int sbox = op->s_box;
+      const uint32_t bbytes = op->rows * 128;
+      const CUtensorMap *tmB = &op->tmB;
+      if (lane == 0) {
+        for (int d = 0; d < 3; ++d) ck_wait_dep(P, prep_done, op->gemm_dep[d], op->gemm_tgt[d]);
+        fence_proxy_async();
+        if (P.trace && rank == 0) P.trace[8 * t + 0] = ck_time();
+      }
+      __syncwarp();
+      const int kb0 = rank * kps, kb1 = min(kbt, kb0 + kps);
+      for (int kb = kb0, j = 0; kb < kb1; ++kb, ++j) {
+        const int sb = j % nbst;
+        mbar_wait(&emptyB[sb], ((par >> sb) & 1) ^ 1);
+        par ^= 1u << sb;
+        const int k = kb * 64;
+        const int tap = k / Cin, c0 = k - tap * Cin;
+        const int off = tap - pad;
+        const int q = off >= 0 ? off / stride : -((-off + stride - 1) / stride);
+        const int h = off - q * stride;
+        tma_load_4d_warp(sB + sb * bstage, tmB, &fullB[sb], bbytes, c0, h, q, tk.z * sbox);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    int ia = 0, gi = 0;
+    uint32_t par = 0;
+    for (int t = t0; t < t1; ++t) {
+      const int4 tk = P.tasks[t];
+      if ((tk.x & 0xff) != K_GEMM) continue;
+      const ClOp *op = &P.ops[tk.x >> 8];
+      const int kps = op->kps, kbt = op->kb_total, bn = op->bn, bstage = op->bstage, nbst = op->nbst;
+      const int buf = gi & 1;
+      mbar_wait(&tempty[buf], ((gi >> 1) & 1) ^ 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t idesc = umma_idesc(bn);
+      const uint32_t dt = tmem + buf * CK_BN;
+      const int kb0 = rank * kps, kb1 = min(kbt, kb0 + kps);
+      int j = 0;
+      for (int kb = kb0; kb < kb1; kb += 2, ++ia) {
+        const int sa = ia % CK_NA;
+        mbar_wait(&fullA[sa], (ia / CK_NA) & 1);
+        const int nk = min(2, kb1 - kb);
+        for (int i = 0; i < nk; ++i, ++j) {
+          const int sb = j % nbst;
+          mbar_wait(&fullB[sb], (par >> sb) & 1);
+          par ^= 1u << sb;
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a0 = smem_u32(sA + sa * CK_A_STAGE + i * CK_A_BYTES);
+          const uint32_t b0 = smem_u32(sB + sb * bstage);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            umma_bf16_warp(dt, umma_desc(a0 + kk * 32), umma_desc(b0 + kk * 32), idesc,
+                           (kb > kb0 || i > 0 || kk > 0) ? 1u : 0u);
+          umma_commit_warp(&emptyB[sb]);
+          __syncwarp();
+        }
+        umma_commit_warp(&emptyA[sa]);
+        __syncwarp();
+      }
+      if (kb1 > kb0) umma_commit_warp(&tfull[buf]);
+      else if (lane == 0) mbar_arrive(&tfull[buf]);      // empty K share: the drain pushes zeros
+      __syncwarp();
+      ++gi;
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ epilogue warps
+    const int et = threadIdx.x - 128;
+    const int ew = warp - 4;
+    auto esync = [] __device__() { named_sync(1, CK_EPI); };
+    int gi = 0, gn_i = 0;
+    for (int t = t0; t < t1; ++t) {
+      const int4 tk = P.tasks[t];
+      const int type = tk.x & 0xff, opi = tk.x >> 8;
+      if (type == K_GEMM) {
+        const ClOp *op = &P.ops[opi];
+        const EpiArgs e = op->epi;
+        const int M = op->M, Wo = op->Wo, sbox = op->s_box, rows = op->rows, bn = op->bn;
+        const int kps = op->kps, kbt = op->kb_total, gn = op->gn, cg = op->cg, pair = op->pair;
+        const int mt = tk.y, nt = tk.z, S = P.S;
+        const int lwo = op->lwo, lbn = op->lbn, lsb = op->lsb, lcg = op->lcg;
+        const int nkb = max(0, min(kbt, (rank + 1) * kps) - rank * kps);
+        const bool film = e.film_off >= 0;
+        const bool has_res = e.res != nullptr || e.res_f32 != nullptr;
+        const int buf = gi & 1;
+        const uint32_t cpar = gi & 1;
+        // receive buffers alternate by task: a peer pushing task t+1 has passed
+        // barrier A of task t, so every CTA is done reading task t-1's buffer
+        __half *recvb = recv + buf * (RECV_BYTES / 2);
+        // ---- residual producers and the per-sample FiLM rows (prep) first
+        if (et == 0) {
+          if (film) ck_spin(prep_done, S);
+          for (int d = 0; d < 2; ++d) ck_wait_dep(P, prep_done, op->epi_dep[d], op->epi_tgt[d]);
+        }
+        esync();
+        // ---- element ownership: column col, rows g + k * rstep (k < nv) of this CTA's 16-row slice
+        const int col = et & (bn - 1), g = et >> lbn, rstep = CK_EPI >> lbn, nv = bn >> 4;
+        const int jl = col >> lwo;
+        const int s = nt * sbox + jl;
+        const bool colok = col < rows && s < S;
+        const int chb = mt * 128 + 16 * rank;
+        float bias[4], gam[4], bet[4], sc[4], bi[4], v[4];
+        const float *fa = nullptr, *fb = nullptr;
+        if (film && colok) {
+          fa = e.film_a + (int64_t)e.film_a_row[s] * e.film_a_stride + e.film_off;
+          fb = e.film_b ? e.film_b + e.film_b_off[s] + e.film_off : nullptr;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int ch = chb + g + k * rstep;
+          const bool ok = k < nv && colok && ch < M;
+          bias[k] = (ok && e.bias) ? e.bias[ch] : 0.f;
+          gam[k] = (ok && gn) ? e.gn_gamma[ch] : 1.f;
+          bet[k] = (ok && gn) ? e.gn_beta[ch] : 0.f;
+          sc[k] = 1.f;
+          bi[k] = 0.f;
+          if (ok && fa) {
+            sc[k] = fa[ch] + (fb ? fb[ch] : 0.f);
+            bi[k] = fa[M + ch] + (fb ? fb[M + ch] : 0.f);
+          }
+        }
+        if (has_res) {                                    // residual tile -> rbuf[col][16]
+          const int per = e.res ? 2 : 4;                  // 16-byte chunks per column
+          if (et < per * bn) {
+            const int lper = e.res ? 1 : 2;
+            const int c = et >> lper, h = et & (per - 1);
+            const int j2 = c >> lwo, p2 = c & (Wo - 1), s2 = nt * sbox + j2;
+            const int ch0 = chb + h * (16 >> lper);
+            float tmp[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) tmp[i] = 0.f;
+            const int nvals = 16 >> lper;
+            if (c < rows && s2 < S && ch0 < M) {
+              const int64_t pos = (int64_t)s2 * Wo + p2;
+              if (e.res) {
+                const uint4 u = *reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(e.res) +
+                                                                pos * e.res_pitch + e.res_coff + ch0);
+                const __nv_bfloat162 *b2 = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const float2 f = __bfloat1622float2(b2[i]);
+                  tmp[2 * i] = f.x;
+                  tmp[2 * i + 1] = f.y;
+                }
+              } else {
+                const float4 f = *reinterpret_cast<const float4 *>(e.res_f32 + pos * M + ch0);
+                tmp[0] = f.x; tmp[1] = f.y; tmp[2] = f.z; tmp[3] = f.w;
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (i < nvals) rbuf[c * CK_OS + h * nvals + i] = tmp[i];
+          }
+        }
+        // ---- drain TMEM and push row slices to their owners (reduce-scatter over DSMEM)
+        if (ew < 4) {
+          mbar_wait(&tfull[buf], (gi >> 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 1] = ck_time();
+          const int m = ew * 32 + lane;
+          // fp16 partial sums (K/8 terms each, fp32-accumulated in TMEM): half the
+          // DSMEM traffic; the owner sums the 8 slices in fp32
+          const uint32_t dst = mapa_shared(smem_u32(recvb + (rank * 16 + (m & 15)) * CK_RSH), m >> 4);
+          for (int c = 0; c < bn; c += 16) {
+            float x[16];
+            if (nkb > 0) {
+              tmem_ld16(tmem + buf * CK_BN + c + ((uint32_t)(ew * 32) << 16), x);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) x[i] = 0.f;
+            }
+            uint32_t hw[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const __half2 h2 = __floats2half2_rn(x[2 * i], x[2 * i + 1]);
+              hw[i] = *reinterpret_cast<const uint32_t *>(&h2);
+            }
+            st_cluster_v4_b32(dst + c * 2, hw[0], hw[1], hw[2], hw[3]);
+            st_cluster_v4_b32(dst + c * 2 + 16, hw[4], hw[5], hw[6], hw[7]);
+          }
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[buf]);
+          if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 5] = ck_time();
+        }
+        cluster_barrier_warp(&cbar[0], cpar, lane);
+        if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 2] = ck_time();
+        // ---- fixed-order sum of the 8 K slices + bias; values also staged as obuf[col][row]
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float acc = bias[k];
+          if (k < nv) {
+            const __half *rp = recvb + (g + k * rstep) * CK_RSH + col;
+#pragma unroll
+            for (int src = 0; src < CL; ++src) acc += __half2float(rp[src * 16 * CK_RSH]);
+          }
+          v[k] = acc;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k < nv) obuf[col * CK_OS + g + k * rstep] = v[k];
+        // GroupNorm bookkeeping: (atom a, sample j) pairs, L lanes each (L | 32)
+        const int lL = min(5, 7 - lsb), L = 1 << lL;
+        const int pi = et >> lL, li = et & (L - 1);
+        const int pa = pi >> lsb, pj = pi & (sbox - 1);
+        const bool in_pair = pi < 2 * sbox;
+        const float n0 = 8.f * Wo;
+        const int fi = pair ? op->flag_base + nt * op->m_tiles + mt : 0;
+        if (gn) {
+          esync();
+          // ---- atom statistics: sum and sum of squares over 8 rows x Wo columns, butterfly over L lanes
+          if (in_pair) {
+            float sum = 0.f, sq = 0.f;
+            const int per = (8 * Wo) >> lL;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              if (i < per) {
+                const int idx = li + i * L;
+                const int r8 = idx >> lwo, c = idx & (Wo - 1);
+                const float x = obuf[(pj * Wo + c) * CK_OS + 8 * pa + r8];
+                sum += x;
+                sq += x * x;
+              }
+            }
+            for (int o = 1; o < L; o <<= 1) {
+              sum += __shfl_xor_sync(0xffffffffu, sum, o);
+              sq += __shfl_xor_sync(0xffffffffu, sq, o);
+            }
+            const float mean = sum / n0;
+            const float m2a = fmaxf(sq - sum * mean, 0.f);
+            if (li < CL)                                  // lane li -> CTA li
+              st_cluster_v2(mapa_shared(smem_u32(stats + (rank * 2 + pa) * CK_SMAX + pj), li), mean, m2a);
+            if (pair && li == (CL & (L - 1)))          // the partner tile reads its atoms from L2
+              __stcg(&P.gstats[((int64_t)fi * 16 + rank * 2 + pa) * CK_SMAX + pj], make_float2(mean, m2a));
+          }
+          if (pair) {                                     // published before the cluster barrier
+            esync();
+            if (et == 0) red_release_add(&P.flags[fi], 1);
+          }
+        }
+        if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 6] = ck_time();
+        if (gn) cluster_barrier_warp(&cbar[1], gn_i & 1, lane);      // statistics exchange
+        if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 3] = ck_time();
+        if (gn) {
+          // ---- merge the atoms of each group (butterfly, fixed lane order); 256-channel
+          //      groups merge the 16 atoms of the tile, then the partner tile's statistics
+          float2 gs = make_float2(0.f, 0.f);
+          float ncount = 0.f;
+          if (pair) {                                     // partner tile's 8 CTAs have published
+            if (et == 0) ck_spin(&P.flags[fi ^ 1], CL);
+            esync();
+          }
+          if (in_pair) {
+            int i0 = 0, k = 16;
+            if (!pair) {
+              const int ch0 = chb + 8 * pa;
+              const int gf = (ch0 >> lcg) << lcg;
+              const int lo = max(gf, mt * 128), hi = min(min(gf + cg, mt * 128 + 128), M);
+              i0 = (lo - mt * 128) >> 3;
+              k = (hi - lo) >> 3;
+            }
+            // butterfly merge of k equal-count atoms held two per lane
+            auto merge = [&](float2 a0, float2 a1, bool h0, bool h1) {
+              float m = (h0 ? a0.x : 0.f) + (h1 ? a1.x : 0.f);
+              for (int o = 1; o < L; o <<= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+              m /= (float)k;
+              float q = 0.f;
+              if (h0) { const float d = a0.x - m; q += a0.y + n0 * d * d; }
+              if (h1) { const float d = a1.x - m; q += a1.y + n0 * d * d; }
+              for (int o = 1; o < L; o <<= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+              return make_float2(m, q);
+            };
+            const bool h0 = li < k, h1 = li + L < k;
+            float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+            if (h0) a0 = stats[(i0 + li) * CK_SMAX + pj];
+            if (h1) a1 = stats[(i0 + li + L) * CK_SMAX + pj];
+            gs = merge(a0, a1, h0, h1);
+            ncount = n0 * k;
+            if (pair) {                                   // partner tile (16 atoms), lower tile first
+              const float2 *og = P.gstats + (int64_t)(fi ^ 1) * 16 * CK_SMAX + pj;
+              if (h0) a0 = __ldcg(og + li * CK_SMAX);
+              if (h1) a1 = __ldcg(og + (li + L) * CK_SMAX);
+              const float2 other = merge(a0, a1, h0, h1);
+              const float2 lo2 = (mt & 1) ? other : gs, hi2 = (mt & 1) ? gs : other;
+              const float m = 0.5f * (lo2.x + hi2.x);
+              const float d0 = lo2.x - m, d1 = hi2.x - m;
+              gs = make_float2(m, (lo2.y + hi2.y) + ncount * (d0 * d0 + d1 * d1));
+              ncount *= 2.f;
+            }
+          }
+          if (in_pair && li == 0) mr[pa * CK_SMAX + pj] = make_float2(gs.x, rsqrtf(gs.y / ncount + 1e-5f));
+          esync();
+        }
+        if (P.trace && rank == 0 && et == 0) {
+          P.trace[8 * t + 7] = ck_time();
+          P.trace[8 * (P.n_tasks + t) + 0] = clock64();
+        }
+        // ---- normalise, activate, FiLM, residual -> staging tile (branch-free per element)
+        {
+          const float rba = e.res_before_act ? 1.f : 0.f;
+          const float is_mish = e.act == AURAS_ACT_MISH ? 1.f : 0.f;
+          const float is_relu = e.act == AURAS_ACT_RELU ? 1.f : 0.f;
+          const float is_none = 1.f - is_mish - is_relu;
+          float2 m2[4];
+          float r[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {                   // all shared-memory loads first
+            const int row = g + k * rstep;
+            m2[k] = gn ? mr[(row >> 3) * CK_SMAX + (jl & (CK_SMAX - 1))] : make_float2(0.f, 1.f);
+            r[k] = has_res ? rbuf[col * CK_OS + (row & 15)] : 0.f;
+          }
+          float y[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            float x = (v[k] - m2[k].x) * m2[k].y * gam[k] + bet[k];
+            x += rba * r[k];
+            const float ex = __expf(fminf(x, 20.f));
+            const float nn = ex * (ex + 2.f);
+            const float ratio = __fdividef(nn, nn + 2.f);
+            const float xm = x * (x > 20.f ? 1.f : ratio);
+            x = is_mish * xm + is_relu * fmaxf(x, 0.f) + is_none * x;
+            x = x * sc[k] + bi[k];
+            y[k] = x + (1.f - rba) * r[k];
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (k < nv && colok) obuf[col * CK_OS + g + k * rstep] = y[k];
+        }
+        if (P.trace && rank == 0 && et == 0) {
+          P.trace[8 * (P.n_tasks + t) + 1] = clock64();
+          P.trace[8 * (P.n_tasks + t) + 4] = ck_time();
+        }
+        esync();
+        if (P.trace && rank == 0 && et == 0) P.trace[8 * (P.n_tasks + t) + 5] = ck_time();
+        // ---- vector stores: 8 channels (bf16) / 4 channels (fp32) per thread
+        if (e.out) {
+          if (et < 2 * bn) {
+            const int c = et >> 1, h = et & 1;
+            const int j2 = c >> lwo, p2 = c & (Wo - 1), s2 = nt * sbox + j2;
+            const int ch0 = chb + 8 * h;
+            if (c < rows && s2 < S && ch0 < M) {
+              __nv_bfloat162 b2[4];
+              for (int i = 0; i < 4; ++i)
+                b2[i] = __floats2bfloat162_rn(obuf[c * CK_OS + 8 * h + 2 * i], obuf[c * CK_OS + 8 * h + 2 * i + 1]);
+              const int wout = e.out_stuff ? 2 * Wo : Wo;
+              const int ox2 = e.out_stuff ? 2 * p2 : p2;
+              __nv_bfloat16 *dst = static_cast<__nv_bfloat16 *>(e.out) +
+                                   ((int64_t)s2 * wout + ox2) * e.out_pitch + e.out_coff + ch0;
+              *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>(b2);
+              if (e.out_stuff) *reinterpret_cast<uint4 *>(dst + e.out_pitch) = make_uint4(0, 0, 0, 0);
+            }
+          }
+        }
+        if (e.out_f32) {
+          if (et < 4 * bn) {
+            const int c = et >> 2, h = et & 3;
+            const int j2 = c >> lwo, p2 = c & (Wo - 1), s2 = nt * sbox + j2;
+            const int ch0 = chb + 4 * h;
+            if (c < rows && s2 < S && ch0 < M) {
+              const float *o = obuf + c * CK_OS + 4 * h;
+              *reinterpret_cast<float4 *>(e.out_f32 + ((int64_t)s2 * Wo + p2) * M + ch0) =
+                  make_float4(o[0], o[1], o[2], o[3]);
+            }
+          }
+        }
+        if (P.trace && rank == 0 && et == 0) P.trace[8 * (P.n_tasks + t) + 6] = ck_time();
+        fence_proxy_async();
+        esync();
+        if (P.trace && rank == 0 && et == 0) P.trace[8 * (P.n_tasks + t) + 7] = ck_time();
+        if (et == 0) {
+          red_release_add(&done[opi], 1);
+          if (P.trace && rank == 0) P.trace[8 * t + 4] = ck_time();
+        }
+        ++gi;
+        gn_i += gn;
+      } else if (type == K_PREP) {
+        if (tk.w != rank) continue;
+        prep_body<__nv_bfloat16>(P.dev, tk.y, et, CK_EPI, P.sched, P.horizon, P.adim, P.xin, P.x_pitch,
+                                 P.ring_slot_stride, P.ring_agent_stride);
+        fence_proxy_async();
+        esync();
+        if (et == 0) {
+          __threadfence();
+          atomicAdd(prep_done, 1);
+        }
+      } else if (type == K_FINAL) {
+        if (tk.w != rank) continue;
+        if (et == 0) ck_spin(&done[P.n_ops - 1], P.ops[P.n_ops - 1].tiles * CL);
+        esync();
+        final_body<__nv_bfloat16>(P.dev, tk.y, et, CK_EPI, P.sched, P.horizon, P.adim, P.y_final, P.y_pitch,
+                                  P.final_cin, P.wf, P.bf, eps, esync);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync_all();                       // no CTA leaves while peers may still touch its smem
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * CK_BN));
+}
+
+// ---------------------------------------------------------------- host side
+
+static int pow2_floor(int x) {
+  int p = 1;
+  while (p * 2 <= x) p *= 2;
+  return p;
+}
+
+static bool same_buf(const void *a, const void *b) { return a != nullptr && a == b; }
+
+static int cluster_capacity() {
+  static int cached = -1;
+  if (cached >= 0) return cached;
+  if (cudaFuncSetAttribute(unet_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CK_SMEM) != cudaSuccess) {
+    cudaGetLastError();
+    return cached = 0;
+  }
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(CL * 16);
+  cfg.blockDim = dim3(CK_THREADS);
+  cfg.dynamicSmemBytes = CK_SMEM;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = CL;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, unet_cluster, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  return cached = n;
+}
+
+int clus_build(ClConfig &cc, const std::vector<auras_conv_op> &ops, int S, const void *x_in,
+               const ClParams &base, const float *film_tau, int film_width, const float *ring_film,
+               TiledCache &cache) {
+  const int n = (int)ops.size();
+  int nc = std::min(cluster_capacity(), 16);
+  if (const char *e = getenv("AURAS_CLUSTERS")) nc = std::min(nc, atoi(e));
+  nc &= ~1;                                   // GroupNorm pairs need an even cluster count
+  if (nc < 2) { set_error("cluster kernel: only %d co-resident 8-CTA clusters", nc); return AURAS_E_ARG; }
+  // columns per tile task: narrower tiles mean less DSMEM traffic per CTA and
+  // more clusters per layer, at the cost of re-streaming weights per n-tile
+  int bn_cap = 64;
+  if (const char *e = getenv("AURAS_CL_BN")) bn_cap = std::max(16, std::min(CK_BN, atoi(e)));
+  std::vector<ClOp> hops(n);
+  int n_flags = 0;
+  for (int i = 0; i < n; ++i) {
+    const auras_conv_op &o = ops[i];
+    ClOp &m = hops[i];
+    memset(&m, 0, sizeof(m));
+    ConvGemmArgs g;
+    EpiArgs e;
+    int rc = conv_op_to_args(o, S, AURAS_DT_BF16, nullptr, g, e);
+    if (rc) return rc;
+    if (!gemm_sm100_supported(g) || o.Ho != 1 || o.pool_out) {
+      set_error("cluster kernel: op %d not a 1-D tcgen05 conv", i);
+      return AURAS_E_ARG;
+    }
+    if (o.Wo > 32 || o.Wo < 2 || (o.Wo & (o.Wo - 1)) || o.M % 8) {
+      set_error("cluster kernel: op %d shape", i);
+      return AURAS_E_ARG;
+    }
+    if (o.out && (o.out_pitch % 8 || o.out_coff % 8)) { set_error("cluster kernel: op %d out align", i); return AURAS_E_ARG; }
+    if (o.res && (o.res_pitch % 8 || o.res_coff % 8)) { set_error("cluster kernel: op %d res align", i); return AURAS_E_ARG; }
+    m.gn = o.gn_gamma != nullptr;
+    m.cg = m.gn ? o.M / o.groups : 0;
+    if (m.gn && (o.M % o.groups || m.cg % 8 || (m.cg <= 128 ? 128 % m.cg : m.cg != 256))) {
+      set_error("cluster kernel: op %d GroupNorm of %d channels", i, m.cg);
+      return AURAS_E_ARG;
+    }
+    m.pair = m.gn && m.cg == 256;
+    m.M = o.M; m.Cin = o.Cin; m.Wo = o.Wo; m.stride = o.stride; m.pad = o.pad_w;
+    m.s_box = std::min(CK_SMAX, pow2_floor(std::max(1, std::min(S, bn_cap / o.Wo))));
+    m.rows = m.s_box * o.Wo;
+    m.bn = std::max(16, m.rows);
+    m.kb_total = o.Kp / 64;
+    m.kps = (m.kb_total + CL - 1) / CL;
+    m.m_tiles = (o.M + 127) / 128;
+    const int n_tiles = (S + m.s_box - 1) / m.s_box;
+    m.tiles = m.m_tiles * n_tiles;
+    if (m.pair && (m.m_tiles & 1)) { set_error("cluster kernel: op %d odd tile pair", i); return AURAS_E_ARG; }
+    auto lg = [](int x) { int l = 0; while ((1 << l) < x) ++l; return l; };
+    m.lwo = lg(m.Wo);
+    m.lbn = lg(m.bn);
+    m.lsb = lg(m.s_box);
+    m.lcg = m.gn ? lg(m.cg) : 0;
+    if (m.gn && (1 << m.lcg) != m.cg) { set_error("cluster kernel: op %d group size", i); return AURAS_E_ARG; }
+    m.bstage = m.bn * 128;
+    m.nbst = std::min(CK_NBMAX, CK_BRING / m.bstage);
+    m.epi = e;
+    if (o.film_off >= 0) {
+      m.epi.film_a = film_tau;
+      m.epi.film_a_row = base.dev->tau_row;
+      m.epi.film_a_stride = film_width;
+      m.epi.film_b = ring_film;
+      m.epi.film_b_off = base.dev->film_b_off;
+    }
+    if (m.pair) {
+      m.flag_base = n_flags;
+      n_flags += m.tiles;
+    }
+    void *wt = nullptr;
+    if ((rc = tiled_weights(cache, o, &wt))) return rc;
+    if ((rc = make_tiled_weight_map(&m.tmA, wt, m.m_tiles * m.kb_total * 128))) return rc;
+    if ((rc = make_act_map(&m.tmB, o.in, o.in_coff, o.Cin, o.in_pitch, o.W, o.stride, S, o.Wo, m.s_box))) return rc;
+    for (int d = 0; d < 3; ++d) m.gemm_dep[d] = -1;
+    for (int d = 0; d < 2; ++d) m.epi_dep[d] = -1;
+    int nd = 0;
+    if (o.in == x_in) m.gemm_dep[nd++] = -2;
+    for (int j = i - 1; j >= 0 && nd < 3; --j)
+      if (same_buf(ops[j].out, o.in)) m.gemm_dep[nd++] = j;
+    int ne = 0;
+    for (int j = i - 1; j >= 0 && ne < 2; --j)
+      if (same_buf(ops[j].out, o.res) || same_buf(ops[j].out_f32, o.res_f32)) m.epi_dep[ne++] = j;
+    if (o.res && o.res == x_in) { set_error("cluster kernel: residual from the x buffer"); return AURAS_E_ARG; }
+    for (int d = 0; d < 3; ++d) m.gemm_tgt[d] = m.gemm_dep[d] >= 0 ? hops[m.gemm_dep[d]].tiles * CL : 0;
+    for (int d = 0; d < 2; ++d) m.epi_tgt[d] = m.epi_dep[d] >= 0 ? hops[m.epi_dep[d]].tiles * CL : 0;
+  }
+  // per-cluster task lists, layer order
+  std::vector<std::vector<int4>> per(nc);
+  for (int s = 0; s < S; ++s) per[s % nc].push_back(make_int4(K_PREP, s, 0, (s / nc) % CL));
+  int rot = 0;
+  for (int i = 0; i < n; ++i) {
+    const ClOp &m = hops[i];
+    if (m.pair && (rot & 1)) rot = (rot + 1) % nc;     // pairs land on clusters (2c, 2c+1) in one round
+    const int n_tiles = m.tiles / m.m_tiles;
+    int q = 0;
+    for (int nt = 0; nt < n_tiles; ++nt)
+      for (int mt = 0; mt < m.m_tiles; ++mt, ++q) per[(rot + q) % nc].push_back(make_int4(K_GEMM | (i << 8), mt, nt, 0));
+    rot = (rot + q) % nc;
+  }
+  for (int s = 0; s < S; ++s) per[(rot + s) % nc].push_back(make_int4(K_FINAL, s, 0, (s / nc) % CL));
+  std::vector<int4> flat;
+  std::vector<int> begin(nc + 1, 0);
+  for (int c = 0; c < nc; ++c) {
+    begin[c] = (int)flat.size();
+    flat.insert(flat.end(), per[c].begin(), per[c].end());
+  }
+  begin[nc] = (int)flat.size();
+
+  AURAS_CUDA(cudaMalloc(&cc.ops, sizeof(ClOp) * n));
+  AURAS_CUDA(cudaMalloc(&cc.tasks, sizeof(int4) * flat.size()));
+  AURAS_CUDA(cudaMalloc(&cc.cl_begin, sizeof(int) * (nc + 1)));
+  cc.ctr_ints = n + 1 + std::max(1, n_flags);
+  AURAS_CUDA(cudaMalloc(&cc.ctr, sizeof(int) * cc.ctr_ints));
+  AURAS_CUDA(cudaMalloc(&cc.gstats, sizeof(float2) * 16 * CK_SMAX * std::max(1, n_flags)));
+  AURAS_CUDA(cudaMemcpy(cc.ops, hops.data(), sizeof(ClOp) * n, cudaMemcpyHostToDevice));
+  AURAS_CUDA(cudaMemcpy(cc.tasks, flat.data(), sizeof(int4) * flat.size(), cudaMemcpyHostToDevice));
+  AURAS_CUDA(cudaMemcpy(cc.cl_begin, begin.data(), sizeof(int) * (nc + 1), cudaMemcpyHostToDevice));
+  cc.n_ops = n;
+  cc.n_tasks = (int)flat.size();
+  cc.nc = nc;
+  cc.S = S;
+  cc.params = base;
+  cc.params.ops = cc.ops;
+  cc.params.tasks = cc.tasks;
+  cc.params.cl_begin = cc.cl_begin;
+  cc.params.ctr = cc.ctr;
+  cc.params.flags = cc.ctr + n + 1;
+  cc.params.gstats = cc.gstats;
+  cc.params.n_ops = n;
+  cc.params.S = S;
+  cc.params.nc = nc;
+  cc.params.n_tasks = cc.n_tasks;
+  return AURAS_OK;
+}
+
+int clus_launch(const ClConfig &cc, cudaStream_t st) {
+  AURAS_CUDA(cudaMemsetAsync(cc.ctr, 0, sizeof(int) * cc.ctr_ints, st));
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(CL * cc.nc);
+  cfg.blockDim = dim3(CK_THREADS);
+  cfg.dynamicSmemBytes = CK_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = CL;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  AURAS_CUDA(cudaLaunchKernelEx(&cfg, unet_cluster, cc.params));
+  return AURAS_OK;
+}
+
+int clus_set_trace(ClConfig &cc, long long *trace) {
+  cc.params.trace = trace;
+  return AURAS_OK;
+}
+
+void clus_free(ClConfig &cc) {
+  cudaFree(cc.ops);
+  cudaFree(cc.tasks);
+  cudaFree(cc.cl_begin);
+  cudaFree(cc.ctr);
+  cudaFree(cc.gstats);
+  cc = ClConfig();
+}
+
+}  // namespace auras

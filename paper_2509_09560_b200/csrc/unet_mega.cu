@@ -349,7 +349,7 @@ __global__ void tile_weights_kernel(const __nv_bfloat16 *__restrict__ src, __nv_
   }
 }
 
-static int make_tiled_weight_map(CUtensorMap *tm, const void *wt, int rows_total) {
+int make_tiled_weight_map(CUtensorMap *tm, const void *wt, int rows_total) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return AURAS_E_CUDA; }
   cuuint64_t dims[2] = {64, (cuuint64_t)rows_total};
@@ -363,7 +363,7 @@ static int make_tiled_weight_map(CUtensorMap *tm, const void *wt, int rows_total
   return AURAS_OK;
 }
 
-static int tiled_weights(TiledCache &cache, const auras_conv_op &o, void **out) {
+int tiled_weights(TiledCache &cache, const auras_conv_op &o, void **out) {
   for (auto &kv : cache)
     if (kv.first == o.w) { *out = kv.second; return AURAS_OK; }
   const int m_tiles = (o.M + 127) / 128;

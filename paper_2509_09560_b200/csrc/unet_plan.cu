@@ -19,6 +19,7 @@
 #include "conv.cuh"
 #include "unet.cuh"
 #include "mega.cuh"
+#include "cluster.cuh"
 
 namespace auras {
 
@@ -63,14 +64,23 @@ struct auras_unet_plan {
   std::map<int, cudaGraphExec_t> graphs;     // one denoise step per batch size S
   bool use_mega = false;                     // persistent megakernel (bf16, tcgen05 engine)
   std::map<int, MegaConfig> mega;
+  bool use_cluster = false;                  // cluster megakernel (DSMEM split-K + GroupNorm)
+  std::map<int, ClConfig> clus;
   TiledCache tiled;                          // tiled weight copies shared by all S
 };
 
 // One denoise step through the persistent megakernel (unet_mega.cu).
 static int unet_mega_step(auras_unet_plan *p, int S, cudaStream_t st) {
-  auto it = p->mega.find(S);
-  if (it == p->mega.end()) { set_error("megakernel config for S=%d not built", S); return AURAS_E_ARG; }
-  int rc = mega_launch(it->second, st);
+  int rc;
+  if (p->use_cluster) {
+    auto it = p->clus.find(S);
+    if (it == p->clus.end()) { set_error("cluster config for S=%d not built", S); return AURAS_E_ARG; }
+    rc = clus_launch(it->second, st);
+  } else {
+    auto it = p->mega.find(S);
+    if (it == p->mega.end()) { set_error("megakernel config for S=%d not built", S); return AURAS_E_ARG; }
+    rc = mega_launch(it->second, st);
+  }
   if (rc) return rc;
   unet_advance<<<1, 1, 0, st>>>(p->dev);
   AURAS_LAUNCHED("unet_advance");
@@ -78,11 +88,39 @@ static int unet_mega_step(auras_unet_plan *p, int S, cudaStream_t st) {
 }
 
 static int unet_ensure_mega(auras_unet_plan *p, int S) {
-  if (!p->use_mega || p->mega.count(S)) return AURAS_OK;
+  if (!p->use_mega) return AURAS_OK;
   const auras_conv_op &last = p->ops.back();
   MegaParams base = mega_base_params(p->dev, p->sched, p->horizon, p->adim, p->x_in, p->x_pitch, p->ring_slot_stride,
                                      p->ring_agent_stride, last.out, last.out_pitch, p->final_cin, p->final_w,
                                      p->final_b);
+  if (p->use_cluster) {
+    if (p->clus.count(S)) return AURAS_OK;
+    ClParams cb;
+    memset(&cb, 0, sizeof(cb));
+    cb.dev = base.dev;
+    cb.sched = base.sched;
+    cb.horizon = base.horizon;
+    cb.adim = base.adim;
+    cb.xin = base.xin;
+    cb.x_pitch = base.x_pitch;
+    cb.ring_slot_stride = base.ring_slot_stride;
+    cb.ring_agent_stride = base.ring_agent_stride;
+    cb.y_final = base.y_final;
+    cb.y_pitch = base.y_pitch;
+    cb.final_cin = base.final_cin;
+    cb.wf = base.wf;
+    cb.bf = base.bf;
+    ClConfig cc;
+    int rc = clus_build(cc, p->ops, S, p->x_in, cb, p->film_tau, p->film_width, p->ring_film, p->tiled);
+    if (!rc) {
+      p->clus.emplace(S, cc);
+      return AURAS_OK;
+    }
+    clus_free(cc);
+    if (!p->clus.empty()) return rc;          // shapes are S-independent: a later failure is real
+    p->use_cluster = false;                   // fall back to the split-K-through-L2 megakernel
+  }
+  if (p->mega.count(S)) return AURAS_OK;
   MegaConfig mc;
   int rc = mega_build(mc, p->ops, S, p->x_in, p->x_pitch, base, p->film_tau, p->film_width, p->ring_film,
                       p->tiled);
@@ -180,6 +218,7 @@ auras_unet_plan *auras_unet_plan_create(const auras_conv_op *ops, int n_ops, int
       if (conv_op_to_args(op, 1, dtype, nullptr, g, e) || g.engine != 1) p->use_mega = false;
     }
   }
+  p->use_cluster = p->use_mega && !getenv("AURAS_NO_CLUSTER");
   if (cudaMalloc(&p->partial, sizeof(float) * p->partial_floats) != cudaSuccess ||
       cudaMalloc(&p->dev, sizeof(UnetDev)) != cudaSuccess ||
       cudaMemset(p->dev, 0, sizeof(UnetDev)) != cudaSuccess) {
@@ -193,6 +232,7 @@ auras_unet_plan *auras_unet_plan_create(const auras_conv_op *ops, int n_ops, int
 void auras_unet_plan_destroy(auras_unet_plan *p) {
   if (!p) return;
   for (auto &kv : p->mega) mega_free(kv.second);
+  for (auto &kv : p->clus) clus_free(kv.second);
   mega_free_tiled(p->tiled);
   for (auto &kv : p->graphs) cudaGraphExecDestroy(kv.second);
   if (p->partial) cudaFree(p->partial);
@@ -275,13 +315,24 @@ int auras_unet_mega_trace(auras_unet_plan *p, int S, long long *trace, int *task
   if (!p || !p->use_mega) { set_error("megakernel not in use"); return AURAS_E_ARG; }
   int rc = unet_ensure_mega(p, S);
   if (rc) return rc;
-  MegaConfig &mc = p->mega[S];
-  if (tasks_out) {
-    if (mc.n_tasks > max_tasks) { set_error("task buffer too small"); return AURAS_E_ARG; }
-    AURAS_CUDA(cudaMemcpy(tasks_out, mc.tasks, sizeof(int4) * mc.n_tasks, cudaMemcpyDeviceToHost));
+  const int4 *tasks;
+  int n_tasks;
+  if (p->use_cluster) {
+    ClConfig &cc = p->clus[S];
+    tasks = cc.tasks;
+    n_tasks = cc.n_tasks;
+    clus_set_trace(cc, trace);
+  } else {
+    MegaConfig &mc = p->mega[S];
+    tasks = mc.tasks;
+    n_tasks = mc.n_tasks;
+    mega_set_trace(mc, trace);
   }
-  mega_set_trace(mc, trace);
-  return mc.n_tasks;
+  if (tasks_out) {
+    if (n_tasks > max_tasks) { set_error("task buffer too small"); return AURAS_E_ARG; }
+    AURAS_CUDA(cudaMemcpy(tasks_out, tasks, sizeof(int4) * n_tasks, cudaMemcpyDeviceToHost));
+  }
+  return n_tasks;
 }
 
 }  // extern "C"
