@@ -381,7 +381,8 @@ def main():
                         "kernel": "denoise chain (UNet conv GEMMs + fused epilogues), per step",
                         "step_ms": step_ms, "algorithmic_bytes_per_step": bytes_step + act_bytes,
                         "tensor_tflops": tflops, "tensor_frac": tflops / tc_peak,
-                        "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
+                        "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
+                        "denoise_kernel_by_S": LAST_EVENTS.get("denoise_kernel")},
            "gpu_launches": launches, "clocks": win.clock_info}
 
     # --- depth-1 baseline (the same engine, run_sequential)
@@ -442,6 +443,10 @@ def _install_capture():
             LAST_EVENTS["events"] = list(self.gen_events)
         LAST_EVENTS["denoiser_ops"] = list(self.denoiser.ops)
         LAST_EVENTS["launches_per_iter"] = int(self.lib.auras_unet_launches_per_iter(self.plan))
+        S_seen = sorted({ev[3] for ev in self.gen_events})
+        names = {0: "layer-by-layer", 1: "megakernel (split-K via L2)", 2: "cluster megakernel (DSMEM)"}
+        LAST_EVENTS["denoise_kernel"] = {int(S): names.get(int(self.lib.auras_unet_kernel_for(self.plan, S)), "?")
+                                         for S in S_seen}
         LAST_EVENTS["encoder_launches"] = 1 + sum(
             (2 if item[0] == "conv" else 1) for g in self.encoder.groups.values() for item in g)
         orig_close(self)

@@ -202,6 +202,12 @@ int auras_unet_generate(auras_unet_plan *plan, int S, const int *lanes, const in
 /* Kernel launches one denoise iteration issues (megakernel path: the
  * persistent step kernel + the iteration advance; layer path: prep, a GEMM and
  * an epilogue per conv op, final, advance).  Negative on error. */
+/* Denoise-step engine used for batch size S: 0 layer-by-layer kernels,
+ * 1 persistent megakernel with split-K through L2, 2 cluster megakernel
+ * (DSMEM split-K + GroupNorm), -1 not chosen yet (picked by a timed dry run
+ * of both persistent kernels on the first generate of that S). */
+int auras_unet_kernel_for(const auras_unet_plan *plan, int S);
+
 int auras_unet_launches_per_iter(const auras_unet_plan *plan);
 
 /* Diagnostics: per-task globaltimer trace of the persistent denoise

@@ -70,6 +70,7 @@ _SIGNATURES = {
     "auras_unet_generate": (C.c_int, [vp, C.c_int, ip, ip, ip, ip, C.c_int, C.c_int, vp, vp, vp,
                                       C.c_int, vp]),
     "auras_unet_mega_trace": (C.c_int, [vp, C.c_int, vp, vp, C.c_int]),
+    "auras_unet_kernel_for": (C.c_int, [vp, C.c_int]),
     "auras_unet_launches_per_iter": (C.c_int, [vp]),
     "auras_conv": (C.c_int, [C.POINTER(ConvOp), C.c_int, C.c_int, vp, C.c_int, vp, i64, vp]),
     "auras_linear": (C.c_int, [C.POINTER(LinearOp), C.c_int, C.c_int, vp, C.c_int, vp, C.c_int, vp]),

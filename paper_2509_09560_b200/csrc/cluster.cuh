@@ -94,6 +94,7 @@ struct ClParams {
   int *flags;
   float2 *gstats;           // per tile of a 256-channel GroupNorm: (mean, M2) per sample
   int n_ops, S, nc, n_tasks;
+  int l2_prefetch;          // bulk-prefetch the next task's weights into L2
   UnetDev *dev;
   auras_sched sched;
   int horizon, adim;

@@ -163,10 +163,38 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
 
   if (warp == 0) {
     // ------------------------------------------------ weights: this CTA's K share of every task
+    // The smem ring holds only part of a large task's weights; while this CTA
+    // waits on activations, the rest of the current task and all of the next
+    // one are pulled into L2 (bulk tensor prefetch, one 16 KB box per lane), so
+    // the loads after the dependency resolves hit L2 instead of HBM.
+    auto l2_prefetch = [&](int t) {
+      const int4 tk = P.tasks[t];
+      const ClOp *op = &P.ops[tk.x >> 8];
+      const int kps = op->kps, kbt = op->kb_total;
+      const int kb0 = rank * kps, kb1 = min(kbt, kb0 + kps);
+      const int row0 = tk.y * kbt * 128;
+      for (int kb = kb0 + lane; kb < kb1; kb += 32)
+        asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(&op->tmA), "r"(0),
+                     "r"(row0 + kb * 128)
+                     : "memory");
+    };
+    auto next_gemm = [&](int t) {
+      for (++t; t < t1; ++t)
+        if ((P.tasks[t].x & 0xff) == K_GEMM) return t;
+      return -1;
+    };
     int ia = 0;
+    if (P.l2_prefetch) {
+      const int f = next_gemm(t0 - 1);
+      if (f >= 0) l2_prefetch(f);
+    }
     for (int t = t0; t < t1; ++t) {
       const int4 tk = P.tasks[t];
       if ((tk.x & 0xff) != K_GEMM) continue;
+      if (P.l2_prefetch) {
+        const int nx = next_gemm(t);
+        if (nx >= 0) l2_prefetch(nx);
+      }
       const ClOp *op = &P.ops[tk.x >> 8];
       const int kps = op->kps, kbt = op->kb_total;
       const CUtensorMap *tmA = &op->tmA;
@@ -757,6 +785,10 @@ int clus_build(ClConfig &cc, const std::vector<auras_conv_op> &ops, int S, const
   cc.params.S = S;
   cc.params.nc = nc;
   cc.params.n_tasks = cc.n_tasks;
+  {
+    const char *e = getenv("AURAS_CL_L2PF");
+    cc.params.l2_prefetch = e ? atoi(e) : 1;
+  }
   return AURAS_OK;
 }
 

@@ -66,69 +66,135 @@ struct auras_unet_plan {
   std::map<int, MegaConfig> mega;
   bool use_cluster = false;                  // cluster megakernel (DSMEM split-K + GroupNorm)
   std::map<int, ClConfig> clus;
+  std::map<int, int> use_clus_for;           // per S: 1 cluster kernel, 0 L2 split-K megakernel
+  float *dry_x = nullptr;                    // scratch request lanes for autotuning runs
+  int64_t *dry_fetched = nullptr;
   TiledCache tiled;                          // tiled weight copies shared by all S
 };
 
-// One denoise step through the persistent megakernel (unet_mega.cu).
-static int unet_mega_step(auras_unet_plan *p, int S, cudaStream_t st) {
-  int rc;
-  if (p->use_cluster) {
+static int mega_kernel_launch(auras_unet_plan *p, int S, bool cluster, cudaStream_t st) {
+  if (cluster) {
     auto it = p->clus.find(S);
     if (it == p->clus.end()) { set_error("cluster config for S=%d not built", S); return AURAS_E_ARG; }
-    rc = clus_launch(it->second, st);
-  } else {
-    auto it = p->mega.find(S);
-    if (it == p->mega.end()) { set_error("megakernel config for S=%d not built", S); return AURAS_E_ARG; }
-    rc = mega_launch(it->second, st);
+    return clus_launch(it->second, st);
   }
+  auto it = p->mega.find(S);
+  if (it == p->mega.end()) { set_error("megakernel config for S=%d not built", S); return AURAS_E_ARG; }
+  return mega_launch(it->second, st);
+}
+
+// One denoise step through the persistent megakernel picked for S.
+static int unet_mega_step(auras_unet_plan *p, int S, cudaStream_t st) {
+  int rc = mega_kernel_launch(p, S, p->use_clus_for[S] == 1, st);
   if (rc) return rc;
   unet_advance<<<1, 1, 0, st>>>(p->dev);
   AURAS_LAUNCHED("unet_advance");
   return AURAS_OK;
 }
 
-static int unet_ensure_mega(auras_unet_plan *p, int S) {
-  if (!p->use_mega) return AURAS_OK;
+static int build_cluster_config(auras_unet_plan *p, int S, const MegaParams &base) {
+  ClParams cb;
+  memset(&cb, 0, sizeof(cb));
+  cb.dev = base.dev;
+  cb.sched = base.sched;
+  cb.horizon = base.horizon;
+  cb.adim = base.adim;
+  cb.xin = base.xin;
+  cb.x_pitch = base.x_pitch;
+  cb.ring_slot_stride = base.ring_slot_stride;
+  cb.ring_agent_stride = base.ring_agent_stride;
+  cb.y_final = base.y_final;
+  cb.y_pitch = base.y_pitch;
+  cb.final_cin = base.final_cin;
+  cb.wf = base.wf;
+  cb.bf = base.bf;
+  ClConfig cc;
+  int rc = clus_build(cc, p->ops, S, p->x_in, cb, p->film_tau, p->film_width, p->ring_film, p->tiled);
+  if (rc) {
+    clus_free(cc);
+    return rc;
+  }
+  p->clus.emplace(S, cc);
+  return AURAS_OK;
+}
+
+// Time both persistent kernels on a dry batch of S samples (scratch request
+// lanes; every buffer they write is either scratch or rewritten by the next
+// real step's prep) and keep the faster one for this S.
+static int autotune_mega(auras_unet_plan *p, int S, cudaStream_t st, int *pick) {
+  if (!p->dry_x) {
+    AURAS_CUDA(cudaMalloc(&p->dry_x, sizeof(float) * kMaxS * p->horizon * p->adim));
+    AURAS_CUDA(cudaMemset(p->dry_x, 0, sizeof(float) * kMaxS * p->horizon * p->adim));
+    AURAS_CUDA(cudaMalloc(&p->dry_fetched, sizeof(int64_t) * 4));
+    AURAS_CUDA(cudaMemset(p->dry_fetched, 0, sizeof(int64_t) * 4));
+  }
+  UnetCtrl c;
+  memset(&c, 0, sizeof(c));
+  for (int s = 0; s < S; ++s) {
+    c.lanes[s] = s;
+    c.count[s] = 1;
+  }
+  c.x_lanes = p->dry_x;
+  c.fetched = p->dry_fetched;
+  c.S = S;
+  c.lanes_per_agent = S;
+  unet_set_ctrl<<<1, 1, 0, st>>>(p->dev, c);
+  AURAS_LAUNCHED("unet_set_ctrl");
+  float best[2] = {1e30f, 1e30f};
+  cudaEvent_t e0, e1;
+  AURAS_CUDA(cudaEventCreate(&e0));
+  AURAS_CUDA(cudaEventCreate(&e1));
+  int rc = AURAS_OK;
+  for (int rep = 0; rep < 4 && !rc; ++rep)
+    for (int k = 0; k < 2 && !rc; ++k) {
+      cudaEventRecord(e0, st);
+      rc = mega_kernel_launch(p, S, k == 1, st);
+      cudaEventRecord(e1, st);
+      if (!rc && cudaEventSynchronize(e1) == cudaSuccess) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (rep > 0) best[k] = std::min(best[k], ms);        // rep 0 warms both
+      }
+    }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rc) return rc;
+  AURAS_CUDA(cudaGetLastError());
+  *pick = best[1] < best[0] ? 1 : 0;
+  return AURAS_OK;
+}
+
+static int unet_ensure_mega(auras_unet_plan *p, int S, cudaStream_t st) {
+  if (!p->use_mega || p->use_clus_for.count(S)) return AURAS_OK;
   const auras_conv_op &last = p->ops.back();
   MegaParams base = mega_base_params(p->dev, p->sched, p->horizon, p->adim, p->x_in, p->x_pitch, p->ring_slot_stride,
                                      p->ring_agent_stride, last.out, last.out_pitch, p->final_cin, p->final_w,
                                      p->final_b);
-  if (p->use_cluster) {
-    if (p->clus.count(S)) return AURAS_OK;
-    ClParams cb;
-    memset(&cb, 0, sizeof(cb));
-    cb.dev = base.dev;
-    cb.sched = base.sched;
-    cb.horizon = base.horizon;
-    cb.adim = base.adim;
-    cb.xin = base.xin;
-    cb.x_pitch = base.x_pitch;
-    cb.ring_slot_stride = base.ring_slot_stride;
-    cb.ring_agent_stride = base.ring_agent_stride;
-    cb.y_final = base.y_final;
-    cb.y_pitch = base.y_pitch;
-    cb.final_cin = base.final_cin;
-    cb.wf = base.wf;
-    cb.bf = base.bf;
-    ClConfig cc;
-    int rc = clus_build(cc, p->ops, S, p->x_in, cb, p->film_tau, p->film_width, p->ring_film, p->tiled);
-    if (!rc) {
-      p->clus.emplace(S, cc);
-      return AURAS_OK;
+  // AURAS_MEGA_KERNEL = "cluster" | "l2" forces one kernel; default: autotune per S
+  const char *force = getenv("AURAS_MEGA_KERNEL");
+  bool want_cluster = p->use_cluster && !(force && !strcmp(force, "l2"));
+  bool want_l2 = !(force && !strcmp(force, "cluster") && p->use_cluster);
+  if (want_cluster && build_cluster_config(p, S, base)) {
+    if (force && !strcmp(force, "cluster")) return AURAS_E_ARG;
+    want_cluster = false;                     // shapes the cluster kernel does not cover
+    want_l2 = true;
+  }
+  if (want_l2) {
+    MegaConfig mc;
+    int rc = mega_build(mc, p->ops, S, p->x_in, p->x_pitch, base, p->film_tau, p->film_width, p->ring_film,
+                        p->tiled);
+    if (rc) {
+      mega_free(mc);
+      return rc;
     }
-    clus_free(cc);
-    if (!p->clus.empty()) return rc;          // shapes are S-independent: a later failure is real
-    p->use_cluster = false;                   // fall back to the split-K-through-L2 megakernel
+    p->mega.emplace(S, mc);
   }
-  if (p->mega.count(S)) return AURAS_OK;
-  MegaConfig mc;
-  int rc = mega_build(mc, p->ops, S, p->x_in, p->x_pitch, base, p->film_tau, p->film_width, p->ring_film,
-                      p->tiled);
-  if (rc) {
-    mega_free(mc);
-    return rc;
+  int pick = want_cluster ? 1 : 0;
+  if (want_cluster && want_l2) {
+    int rc = autotune_mega(p, S, st, &pick);
+    if (rc) return rc;
   }
-  p->mega.emplace(S, mc);
+  p->use_clus_for[S] = pick;
   return AURAS_OK;
 }
 
@@ -233,6 +299,8 @@ void auras_unet_plan_destroy(auras_unet_plan *p) {
   if (!p) return;
   for (auto &kv : p->mega) mega_free(kv.second);
   for (auto &kv : p->clus) clus_free(kv.second);
+  if (p->dry_x) cudaFree(p->dry_x);
+  if (p->dry_fetched) cudaFree(p->dry_fetched);
   mega_free_tiled(p->tiled);
   for (auto &kv : p->graphs) cudaGraphExecDestroy(kv.second);
   if (p->partial) cudaFree(p->partial);
@@ -267,7 +335,7 @@ int auras_unet_generate(auras_unet_plan *p, int S, const int *lanes, const int *
   c.fetched = fetched;
   c.S = S;
   c.lanes_per_agent = lanes_per_agent;
-  int rc0 = unet_ensure_mega(p, S);
+  int rc0 = unet_ensure_mega(p, S, st);
   if (rc0) return rc0;
   auto step = p->use_mega ? unet_mega_step : unet_launch_step;
   unet_set_ctrl<<<1, 1, 0, st>>>(p->dev, c);
@@ -302,6 +370,13 @@ int auras_unet_generate(auras_unet_plan *p, int S, const int *lanes, const int *
 
 extern "C" {
 
+int auras_unet_kernel_for(const auras_unet_plan *p, int S) {
+  if (!p) return AURAS_E_ARG;
+  if (!p->use_mega) return 0;
+  auto it = p->use_clus_for.find(S);
+  return it == p->use_clus_for.end() ? -1 : 1 + it->second;
+}
+
 int auras_unet_launches_per_iter(const auras_unet_plan *p) {
   if (!p) return AURAS_E_ARG;
   return p->use_mega ? 2 : 3 + 2 * (int)p->ops.size();
@@ -313,11 +388,11 @@ int auras_unet_launches_per_iter(const auras_unet_plan *p) {
 // call keep their old parameters, so call it before the first generate.
 int auras_unet_mega_trace(auras_unet_plan *p, int S, long long *trace, int *tasks_out, int max_tasks) {
   if (!p || !p->use_mega) { set_error("megakernel not in use"); return AURAS_E_ARG; }
-  int rc = unet_ensure_mega(p, S);
+  int rc = unet_ensure_mega(p, S, nullptr);
   if (rc) return rc;
   const int4 *tasks;
   int n_tasks;
-  if (p->use_cluster) {
+  if (p->use_clus_for[S] == 1) {
     ClConfig &cc = p->clus[S];
     tasks = cc.tasks;
     n_tasks = cc.n_tasks;
