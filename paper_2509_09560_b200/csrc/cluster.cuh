@@ -84,6 +84,21 @@ __device__ __forceinline__ void cluster_barrier_warp(uint64_t *bar, uint32_t par
   mbar_wait_cluster(bar, parity);
 }
 
+__device__ __forceinline__ void tma_load_5d_warp(void *dst, const CUtensorMap *tm, uint64_t *bar, uint32_t bytes,
+                                                 int c0, int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 rx;\n"
+      ".reg .pred px;\n"
+      "elect.sync rx|px, 0xffffffff;\n"
+      "@px mbarrier.arrive.expect_tx.shared::cta.b64 _, [%2], %3;\n"
+      "@px cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%4, %5, %6, %7, "
+      "%8}], [%2];\n"
+      "}\n" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(smem_u32(bar)), "r"(bytes), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+
 // ---------------------------------------------------------------- host interface
 struct ClOp;
 struct ClParams {
@@ -107,7 +122,15 @@ struct ClParams {
   long long *trace;         // optional [n_tasks][8] globaltimer stamps
 };
 
+struct BlockedBuf {           // kernel-owned channel-blocked copy of a plan activation buffer
+  const void *orig = nullptr;
+  __nv_bfloat16 *ptr = nullptr;
+  int T = 0;
+  int64_t plane = 0;          // elements per 64-channel block: S * T * 64
+};
+
 struct ClConfig {
+  std::vector<BlockedBuf> blocked;
   ClOp *ops = nullptr;
   int4 *tasks = nullptr;
   int *cl_begin = nullptr;

@@ -52,23 +52,24 @@ constexpr int CK_BN = 64;                 // max columns per tile task (TMEM: 2 
 constexpr int CK_A_BYTES = 128 * 64 * 2;  // one 128 x 64 weight box
 constexpr int CK_A_STAGE = 2 * CK_A_BYTES;
 constexpr int CK_NA = 4;                  // weight stages (2 k-blocks each)
-constexpr int CK_BRING = 48 * 1024;       // activation ring (1 k-block per stage)
+constexpr int CK_BRING = 44 * 1024;       // activation ring (1 k-block per stage)
 constexpr int CK_NBMAX = 16;
-constexpr int CK_RSH = 72;                // receive-buffer row stride (halves; 144 B)
 constexpr int CK_OS = 17;                 // staging row stride (floats)
 constexpr int CK_SMAX = 16;               // max samples per tile
 
 constexpr int OFF_B = CK_NA * CK_A_STAGE;
 constexpr int OFF_RECV = OFF_B + CK_BRING;
-constexpr int RECV_BYTES = CL * 16 * CK_RSH * 2;   // one buffer; two alternate by task
+constexpr int RECV_BYTES = CL * 32 * 40 * 2;      // one buffer (>= CL x rows x (bn + 8) halves); two alternate
 constexpr int OFF_STATS = OFF_RECV + 2 * RECV_BYTES;
-constexpr int OFF_RBUF = OFF_STATS + CL * 2 * CK_SMAX * 8;
+constexpr int OFF_RBUF = OFF_STATS + CL * 32 * 8;        // stats: CL x (atoms x samples <= 32) float2
 constexpr int OFF_OBUF = OFF_RBUF + CK_BN * CK_OS * 4;
 constexpr int OFF_MR = OFF_OBUF + CK_BN * CK_OS * 4;
-constexpr int OFF_EPS = OFF_MR + 2 * CK_SMAX * 8;
-constexpr int OFF_BAR = OFF_EPS + 512 * 4;
+constexpr int OFF_BAR = OFF_MR + 4 * CK_SMAX * 8;
 constexpr int CK_NBARS = 2 * CK_NA + 2 * CK_NBMAX + 2 + 2 + 2;
 constexpr size_t CK_SMEM = 1024 + OFF_BAR + CK_NBARS * 8 + 16;
+static_assert(CK_SMEM <= 232448, "cluster kernel shared memory");
+static_assert(CL * 16 * (CK_BN + 8) * 2 <= RECV_BYTES, "receive buffer");
+static_assert(32 * 33 <= CK_BN * CK_OS && 512 <= CK_BN * CK_OS, "staging buffer");
 
 enum { K_GEMM = 0, K_PREP = 2, K_FINAL = 3 };
 
@@ -80,6 +81,14 @@ struct alignas(64) ClOp {
   int bstage, nbst;
   int gn, cg, pair, flag_base;
   int lwo, lbn, lsb, lcg;     // log2 of Wo, bn, s_box, cg (all powers of two)
+  int nmt;                    // 128-row m-tiles per task (2: a 256-channel GroupNorm group stays in one cluster)
+  int rsh;                    // receive-buffer row stride (halves)
+  // activation addressing: element (s, t, c) at base + (c >> 6) * plane + (s * T + t) * row + (c & 63)
+  // (channel-blocked [C/64][S][T][64] buffers owned by this kernel, or the plan's [S][T][pitch] layout)
+  __nv_bfloat16 *out_base;
+  const __nv_bfloat16 *res_base;
+  int64_t out_plane, res_plane;
+  int out_row, out_T, res_row, res_T;
   int gemm_dep[3], gemm_tgt[3];
   int epi_dep[2], epi_tgt[2];
 };
@@ -126,7 +135,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
   float *rbuf = reinterpret_cast<float *>(smem + OFF_RBUF);
   float *obuf = reinterpret_cast<float *>(smem + OFF_OBUF);
   float2 *mr = reinterpret_cast<float2 *>(smem + OFF_MR);
-  float *eps = reinterpret_cast<float *>(smem + OFF_EPS);
+  float *eps = obuf;                       // FINAL tasks run after every GEMM epilogue
   uint64_t *fullA = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
   uint64_t *emptyA = fullA + CK_NA;
   uint64_t *fullB = emptyA + CK_NA;
@@ -152,7 +161,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(2 * CK_BN));
+                 "r"(4 * CK_BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -170,13 +179,15 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
     auto l2_prefetch = [&](int t) {
       const int4 tk = P.tasks[t];
       const ClOp *op = &P.ops[tk.x >> 8];
-      const int kps = op->kps, kbt = op->kb_total;
+      const int kps = op->kps, kbt = op->kb_total, nmt = op->nmt;
       const int kb0 = rank * kps, kb1 = min(kbt, kb0 + kps);
-      const int row0 = tk.y * kbt * 128;
-      for (int kb = kb0 + lane; kb < kb1; kb += 32)
-        asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(&op->tmA), "r"(0),
-                     "r"(row0 + kb * 128)
-                     : "memory");
+      for (int u = 0; u < nmt; ++u) {
+        const int row0 = (tk.y * nmt + u) * kbt * 128;
+        for (int kb = kb0 + lane; kb < kb1; kb += 32)
+          asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(&op->tmA), "r"(0),
+                       "r"(row0 + kb * 128)
+                       : "memory");
+      }
     };
     auto next_gemm = [&](int t) {
       for (++t; t < t1; ++t)
@@ -199,13 +210,24 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
       const int kps = op->kps, kbt = op->kb_total;
       const CUtensorMap *tmA = &op->tmA;
       const int kb0 = rank * kps, kb1 = min(kbt, kb0 + kps);
-      const int row0 = tk.y * kbt * 128;            // tiled layout [m_tile][k_block][128][64]
-      for (int kb = kb0; kb < kb1; kb += 2, ++ia) {
-        const int st = ia % CK_NA;
-        const int two = kb + 1 < kb1;
-        mbar_wait(&emptyA[st], ((ia / CK_NA) & 1) ^ 1);
-        tma_load_2d_pair_warp(sA + st * CK_A_STAGE, tmA, &fullA[st], (1 + two) * CK_A_BYTES, 0, row0 + kb * 128,
-                              row0 + (kb + 1) * 128, two);
+      const int nmt = op->nmt;
+      const int row0 = tk.y * nmt * kbt * 128;      // tiled layout [m_tile][k_block][128][64]
+      if (nmt == 1) {                               // stage = 2 k-blocks of one m-tile
+        for (int kb = kb0; kb < kb1; kb += 2, ++ia) {
+          const int st = ia % CK_NA;
+          const int two = kb + 1 < kb1;
+          mbar_wait(&emptyA[st], ((ia / CK_NA) & 1) ^ 1);
+          tma_load_2d_pair_warp(sA + st * CK_A_STAGE, tmA, &fullA[st], (1 + two) * CK_A_BYTES, 0, row0 + kb * 128,
+                                row0 + (kb + 1) * 128, two);
+        }
+      } else {                                      // stage = 1 k-block of both m-tiles
+        const int row1 = row0 + kbt * 128;
+        for (int kb = kb0; kb < kb1; ++kb, ++ia) {
+          const int st = ia % CK_NA;
+          mbar_wait(&emptyA[st], ((ia / CK_NA) & 1) ^ 1);
+          tma_load_2d_pair_warp(sA + st * CK_A_STAGE, tmA, &fullA[st], 2 * CK_A_BYTES, 0, row0 + kb * 128,
+                                row1 + kb * 128, 1);
+        }
       }
     }
   } else if (warp == 2) {
@@ -236,7 +258,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         const int off = tap - pad;
         const int q = off >= 0 ? off / stride : -((-off + stride - 1) / stride);
         const int h = off - q * stride;
-        tma_load_4d_warp(sB + sb * bstage, tmB, &fullB[sb], bbytes, c0, h, q, tk.z * sbox);
+        tma_load_5d_warp(sB + sb * bstage, tmB, &fullB[sb], bbytes, 0, h, q, tk.z * sbox, c0 >> 6);
       }
     }
   } else if (warp == 1) {
@@ -252,16 +274,41 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
       mbar_wait(&tempty[buf], ((gi >> 1) & 1) ^ 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t idesc = umma_idesc(bn);
-      const uint32_t dt = tmem + buf * CK_BN;
+      const uint32_t dt = tmem + buf * 2 * CK_BN;
       const int kb0 = rank * kps, kb1 = min(kbt, kb0 + kps);
       int j = 0;
+      if (op->nmt == 2) {                           // two accumulators: m-tile u at column u * CK_BN
+        for (int kb = kb0; kb < kb1; ++kb, ++ia, ++j) {
+          const int sa = ia % CK_NA, sb = j % nbst;
+          mbar_wait(&fullA[sa], (ia / CK_NA) & 1);
+          mbar_wait(&fullB[sb], (par >> sb) & 1);
+          par ^= 1u << sb;
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a0 = smem_u32(sA + sa * CK_A_STAGE), b0 = smem_u32(sB + sb * bstage);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
+            umma_bf16_warp(dt, umma_desc(a0 + kk * 32), umma_desc(b0 + kk * 32), idesc, acc);
+            umma_bf16_warp(dt + CK_BN, umma_desc(a0 + CK_A_BYTES + kk * 32), umma_desc(b0 + kk * 32), idesc, acc);
+          }
+          umma_commit_warp(&emptyB[sb]);
+          umma_commit_warp(&emptyA[sa]);
+          __syncwarp();
+        }
+      } else
       for (int kb = kb0; kb < kb1; kb += 2, ++ia) {
         const int sa = ia % CK_NA;
+        long long *kt = (P.trace && ia < 1024) ? P.trace + 16 * (int64_t)P.n_tasks +
+                                                     ((int64_t)blockIdx.x * 1024 + ia) * 3
+                                               : nullptr;
+        if (kt && lane == 0) kt[0] = ck_time();
         mbar_wait(&fullA[sa], (ia / CK_NA) & 1);
+        if (kt && lane == 0) kt[1] = ck_time();
         const int nk = min(2, kb1 - kb);
         for (int i = 0; i < nk; ++i, ++j) {
           const int sb = j % nbst;
           mbar_wait(&fullB[sb], (par >> sb) & 1);
+          if (kt && lane == 0 && i == nk - 1) kt[2] = ck_time();
           par ^= 1u << sb;
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a0 = smem_u32(sA + sa * CK_A_STAGE + i * CK_A_BYTES);
@@ -295,8 +342,12 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         const EpiArgs e = op->epi;
         const int M = op->M, Wo = op->Wo, sbox = op->s_box, rows = op->rows, bn = op->bn;
         const int kps = op->kps, kbt = op->kb_total, gn = op->gn, cg = op->cg, pair = op->pair;
-        const int mt = tk.y, nt = tk.z, S = P.S;
+        const int nmt = op->nmt, mt0 = tk.y * nmt, nt = tk.z, S = P.S;
         const int lwo = op->lwo, lbn = op->lbn, lsb = op->lsb, lcg = op->lcg;
+        const int RPC = 16 * nmt;                        // rows (channels) owned by this CTA
+        const int RSH = op->rsh;                         // receive row stride (halves)
+        const int OS = RPC + 1;                          // staging row stride (floats)
+        const int A = 2 * nmt;                           // 8-channel GroupNorm atoms owned
         const int nkb = max(0, min(kbt, (rank + 1) * kps) - rank * kps);
         const bool film = e.film_off >= 0;
         const bool has_res = e.res != nullptr || e.res_f32 != nullptr;
@@ -305,18 +356,19 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         // receive buffers alternate by task: a peer pushing task t+1 has passed
         // barrier A of task t, so every CTA is done reading task t-1's buffer
         __half *recvb = recv + buf * (RECV_BYTES / 2);
+        // channel of owned row r (0..RPC-1): tile r >> 4, row 16 * rank + (r & 15) of that tile
+        auto chan = [&](int r) { return (mt0 + (r >> 4)) * 128 + 16 * rank + (r & 15); };
         // ---- residual producers and the per-sample FiLM rows (prep) first
         if (et == 0) {
           if (film) ck_spin(prep_done, S);
           for (int d = 0; d < 2; ++d) ck_wait_dep(P, prep_done, op->epi_dep[d], op->epi_tgt[d]);
         }
         esync();
-        // ---- element ownership: column col, rows g + k * rstep (k < nv) of this CTA's 16-row slice
-        const int col = et & (bn - 1), g = et >> lbn, rstep = CK_EPI >> lbn, nv = bn >> 4;
+        // ---- element ownership: column col, rows g + k * rstep (k < nv) of the owned slice
+        const int col = et & (bn - 1), g = et >> lbn, rstep = CK_EPI >> lbn, nv = (RPC * bn) >> 8;
         const int jl = col >> lwo;
         const int s = nt * sbox + jl;
         const bool colok = col < rows && s < S;
-        const int chb = mt * 128 + 16 * rank;
         float bias[4], gam[4], bet[4], sc[4], bi[4], v[4];
         const float *fa = nullptr, *fb = nullptr;
         if (film && colok) {
@@ -325,7 +377,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const int ch = chb + g + k * rstep;
+          const int ch = chan(g + k * rstep);
           const bool ok = k < nv && colok && ch < M;
           bias[k] = (ok && e.bias) ? e.bias[ch] : 0.f;
           gam[k] = (ok && gn) ? e.gn_gamma[ch] : 1.f;
@@ -337,22 +389,22 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
             bi[k] = fa[M + ch] + (fb ? fb[M + ch] : 0.f);
           }
         }
-        if (has_res) {                                    // residual tile -> rbuf[col][16]
-          const int per = e.res ? 2 : 4;                  // 16-byte chunks per column
-          if (et < per * bn) {
-            const int lper = e.res ? 1 : 2;
-            const int c = et >> lper, h = et & (per - 1);
+        if (has_res) {                                    // residual tile -> rbuf[col][RPC]
+          const int lper = e.res ? 1 : 2;                 // 8 (bf16) or 4 (fp32) channels per chunk
+          const int cpc = RPC >> (3 - lper + 1);          // chunks per column: RPC/8 or RPC/4
+          if (et < cpc * bn) {
+            const int c = et / cpc, h = et - c * cpc;
             const int j2 = c >> lwo, p2 = c & (Wo - 1), s2 = nt * sbox + j2;
-            const int ch0 = chb + h * (16 >> lper);
+            const int nvals = 16 >> lper;
+            const int r0 = h * nvals;
+            const int ch0 = chan(r0);
             float tmp[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) tmp[i] = 0.f;
-            const int nvals = 16 >> lper;
             if (c < rows && s2 < S && ch0 < M) {
-              const int64_t pos = (int64_t)s2 * Wo + p2;
               if (e.res) {
-                const uint4 u = *reinterpret_cast<const uint4 *>(static_cast<const __nv_bfloat16 *>(e.res) +
-                                                                pos * e.res_pitch + e.res_coff + ch0);
+                const uint4 u = *reinterpret_cast<const uint4 *>(
+                    op->res_base + (ch0 >> 6) * op->res_plane + ((int64_t)s2 * op->res_T + p2) * op->res_row + (ch0 & 63));
                 const __nv_bfloat162 *b2 = reinterpret_cast<const __nv_bfloat162 *>(&u);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
@@ -361,13 +413,13 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
                   tmp[2 * i + 1] = f.y;
                 }
               } else {
-                const float4 f = *reinterpret_cast<const float4 *>(e.res_f32 + pos * M + ch0);
+                const float4 f = *reinterpret_cast<const float4 *>(e.res_f32 + ((int64_t)s2 * Wo + p2) * M + ch0);
                 tmp[0] = f.x; tmp[1] = f.y; tmp[2] = f.z; tmp[3] = f.w;
               }
             }
 #pragma unroll
             for (int i = 0; i < 8; ++i)
-              if (i < nvals) rbuf[c * CK_OS + h * nvals + i] = tmp[i];
+              if (i < nvals) rbuf[c * OS + r0 + i] = tmp[i];
           }
         }
         // ---- drain TMEM and push row slices to their owners (reduce-scatter over DSMEM)
@@ -376,25 +428,27 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 1] = ck_time();
           const int m = ew * 32 + lane;
-          // fp16 partial sums (K/8 terms each, fp32-accumulated in TMEM): half the
-          // DSMEM traffic; the owner sums the 8 slices in fp32
-          const uint32_t dst = mapa_shared(smem_u32(recvb + (rank * 16 + (m & 15)) * CK_RSH), m >> 4);
-          for (int c = 0; c < bn; c += 16) {
-            float x[16];
-            if (nkb > 0) {
-              tmem_ld16(tmem + buf * CK_BN + c + ((uint32_t)(ew * 32) << 16), x);
-            } else {
+          for (int u = 0; u < nmt; ++u) {
+            // fp16 partial sums (K/8 terms each, fp32-accumulated in TMEM): half the
+            // DSMEM traffic; the owner sums the 8 slices in fp32
+            const uint32_t dst = mapa_shared(smem_u32(recvb + (rank * RPC + u * 16 + (m & 15)) * RSH), m >> 4);
+            for (int c = 0; c < bn; c += 16) {
+              float x[16];
+              if (nkb > 0) {
+                tmem_ld16(tmem + buf * 2 * CK_BN + u * CK_BN + c + ((uint32_t)(ew * 32) << 16), x);
+              } else {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) x[i] = 0.f;
-            }
-            uint32_t hw[8];
+                for (int i = 0; i < 16; ++i) x[i] = 0.f;
+              }
+              uint32_t hw[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const __half2 h2 = __floats2half2_rn(x[2 * i], x[2 * i + 1]);
-              hw[i] = *reinterpret_cast<const uint32_t *>(&h2);
+              for (int i = 0; i < 8; ++i) {
+                const __half2 h2 = __floats2half2_rn(x[2 * i], x[2 * i + 1]);
+                hw[i] = *reinterpret_cast<const uint32_t *>(&h2);
+              }
+              st_cluster_v4_b32(dst + c * 2, hw[0], hw[1], hw[2], hw[3]);
+              st_cluster_v4_b32(dst + c * 2 + 16, hw[4], hw[5], hw[6], hw[7]);
             }
-            st_cluster_v4_b32(dst + c * 2, hw[0], hw[1], hw[2], hw[3]);
-            st_cluster_v4_b32(dst + c * 2 + 16, hw[4], hw[5], hw[6], hw[7]);
           }
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
@@ -408,22 +462,22 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         for (int k = 0; k < 4; ++k) {
           float acc = bias[k];
           if (k < nv) {
-            const __half *rp = recvb + (g + k * rstep) * CK_RSH + col;
+            const __half *rp = recvb + (g + k * rstep) * RSH + col;
 #pragma unroll
-            for (int src = 0; src < CL; ++src) acc += __half2float(rp[src * 16 * CK_RSH]);
+            for (int src = 0; src < CL; ++src) acc += __half2float(rp[src * RPC * RSH]);
           }
           v[k] = acc;
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (k < nv) obuf[col * CK_OS + g + k * rstep] = v[k];
+          if (k < nv) obuf[col * OS + g + k * rstep] = v[k];
         // GroupNorm bookkeeping: (atom a, sample j) pairs, L lanes each (L | 32)
-        const int lL = min(5, 7 - lsb), L = 1 << lL;
+        const int lL = min(5, 8 - lsb - nmt), L = 1 << lL;         // L = min(32, 256 / (A * sbox))
         const int pi = et >> lL, li = et & (L - 1);
         const int pa = pi >> lsb, pj = pi & (sbox - 1);
-        const bool in_pair = pi < 2 * sbox;
+        const bool in_pair = pi < A * sbox;
         const float n0 = 8.f * Wo;
-        const int fi = pair ? op->flag_base + nt * op->m_tiles + mt : 0;
+        const int fi = pair ? op->flag_base + nt * op->m_tiles + mt0 : 0;
         if (gn) {
           esync();
           // ---- atom statistics: sum and sum of squares over 8 rows x Wo columns, butterfly over L lanes
@@ -435,7 +489,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
               if (i < per) {
                 const int idx = li + i * L;
                 const int r8 = idx >> lwo, c = idx & (Wo - 1);
-                const float x = obuf[(pj * Wo + c) * CK_OS + 8 * pa + r8];
+                const float x = obuf[(pj * Wo + c) * OS + 8 * pa + r8];
                 sum += x;
                 sq += x * x;
               }
@@ -447,8 +501,8 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
             const float mean = sum / n0;
             const float m2a = fmaxf(sq - sum * mean, 0.f);
             if (li < CL)                                  // lane li -> CTA li
-              st_cluster_v2(mapa_shared(smem_u32(stats + (rank * 2 + pa) * CK_SMAX + pj), li), mean, m2a);
-            if (pair && li == (CL & (L - 1)))          // the partner tile reads its atoms from L2
+              st_cluster_v2(mapa_shared(smem_u32(stats + (rank * A + pa) * sbox + pj), li), mean, m2a);
+            if (pair && li == (CL & (L - 1)))            // the partner tile reads its atoms from L2
               __stcg(&P.gstats[((int64_t)fi * 16 + rank * 2 + pa) * CK_SMAX + pj], make_float2(mean, m2a));
           }
           if (pair) {                                     // published before the cluster barrier
@@ -460,8 +514,9 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         if (gn) cluster_barrier_warp(&cbar[1], gn_i & 1, lane);      // statistics exchange
         if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 3] = ck_time();
         if (gn) {
-          // ---- merge the atoms of each group (butterfly, fixed lane order); 256-channel
-          //      groups merge the 16 atoms of the tile, then the partner tile's statistics
+          // ---- merge the atoms of each group (butterfly, fixed lane order); task atoms are
+          //      numbered in channel order q = tile * 16 + within-tile atom; 256-channel groups
+          //      split over two tasks also merge the partner tile's statistics from L2
           float2 gs = make_float2(0.f, 0.f);
           float ncount = 0.f;
           if (pair) {                                     // partner tile's 8 CTAs have published
@@ -469,37 +524,43 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
             esync();
           }
           if (in_pair) {
-            int i0 = 0, k = 16;
-            if (!pair) {
-              const int ch0 = chb + 8 * pa;
-              const int gf = (ch0 >> lcg) << lcg;
-              const int lo = max(gf, mt * 128), hi = min(min(gf + cg, mt * 128 + 128), M);
-              i0 = (lo - mt * 128) >> 3;
-              k = (hi - lo) >> 3;
-            }
-            // butterfly merge of k equal-count atoms held two per lane
-            auto merge = [&](float2 a0, float2 a1, bool h0, bool h1) {
-              float m = (h0 ? a0.x : 0.f) + (h1 ? a1.x : 0.f);
+            const int ch0 = chan(8 * pa);
+            const int gf = (ch0 >> lcg) << lcg;
+            const int tlo = mt0 * 128, thi = min((mt0 + nmt) * 128, M);
+            const int lo = max(gf, tlo), hi = min(gf + cg, thi);
+            const int q0 = (lo - tlo) >> 3, k = (hi - lo) >> 3;
+            auto atom = [&](const float2 *base, int q) {  // task atom q -> stats entry
+              const int w = q & 15, u = q >> 4;
+              return base[((w >> 1) * A + 2 * u + (w & 1)) * sbox + pj];
+            };
+            // butterfly merge of k equal-count atoms, up to 4 per lane
+            auto merge = [&](const float2 *base, bool global) {
+              float2 at[4];
+              bool hv[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int q = li + i * L;
+                hv[i] = q < k;
+                at[i] = make_float2(0.f, 0.f);
+                if (hv[i]) at[i] = global ? __ldcg(base + (int64_t)(q0 + q) * CK_SMAX + pj) : atom(base, q0 + q);
+              }
+              float m = 0.f;
+#pragma unroll
+              for (int i = 0; i < 4; ++i) m += hv[i] ? at[i].x : 0.f;
               for (int o = 1; o < L; o <<= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
               m /= (float)k;
               float q = 0.f;
-              if (h0) { const float d = a0.x - m; q += a0.y + n0 * d * d; }
-              if (h1) { const float d = a1.x - m; q += a1.y + n0 * d * d; }
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                if (hv[i]) { const float d = at[i].x - m; q += at[i].y + n0 * d * d; }
               for (int o = 1; o < L; o <<= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
               return make_float2(m, q);
             };
-            const bool h0 = li < k, h1 = li + L < k;
-            float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
-            if (h0) a0 = stats[(i0 + li) * CK_SMAX + pj];
-            if (h1) a1 = stats[(i0 + li + L) * CK_SMAX + pj];
-            gs = merge(a0, a1, h0, h1);
+            gs = merge(stats, false);
             ncount = n0 * k;
             if (pair) {                                   // partner tile (16 atoms), lower tile first
-              const float2 *og = P.gstats + (int64_t)(fi ^ 1) * 16 * CK_SMAX + pj;
-              if (h0) a0 = __ldcg(og + li * CK_SMAX);
-              if (h1) a1 = __ldcg(og + (li + L) * CK_SMAX);
-              const float2 other = merge(a0, a1, h0, h1);
-              const float2 lo2 = (mt & 1) ? other : gs, hi2 = (mt & 1) ? gs : other;
+              const float2 other = merge(P.gstats + (int64_t)(fi ^ 1) * 16 * CK_SMAX, true);
+              const float2 lo2 = (mt0 & 1) ? other : gs, hi2 = (mt0 & 1) ? gs : other;
               const float m = 0.5f * (lo2.x + hi2.x);
               const float d0 = lo2.x - m, d1 = hi2.x - m;
               gs = make_float2(m, (lo2.y + hi2.y) + ncount * (d0 * d0 + d1 * d1));
@@ -509,10 +570,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           if (in_pair && li == 0) mr[pa * CK_SMAX + pj] = make_float2(gs.x, rsqrtf(gs.y / ncount + 1e-5f));
           esync();
         }
-        if (P.trace && rank == 0 && et == 0) {
-          P.trace[8 * t + 7] = ck_time();
-          P.trace[8 * (P.n_tasks + t) + 0] = clock64();
-        }
+        if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 7] = ck_time();
         // ---- normalise, activate, FiLM, residual -> staging tile (branch-free per element)
         {
           const float rba = e.res_before_act ? 1.f : 0.f;
@@ -523,9 +581,9 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           float r[4];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {                   // all shared-memory loads first
-            const int row = g + k * rstep;
+            const int row = (g + k * rstep) & (RPC - 1);
             m2[k] = gn ? mr[(row >> 3) * CK_SMAX + (jl & (CK_SMAX - 1))] : make_float2(0.f, 1.f);
-            r[k] = has_res ? rbuf[col * CK_OS + (row & 15)] : 0.f;
+            r[k] = has_res ? rbuf[col * OS + row] : 0.f;
           }
           float y[4];
 #pragma unroll
@@ -542,49 +600,43 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           }
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            if (k < nv && colok) obuf[col * CK_OS + g + k * rstep] = y[k];
-        }
-        if (P.trace && rank == 0 && et == 0) {
-          P.trace[8 * (P.n_tasks + t) + 1] = clock64();
-          P.trace[8 * (P.n_tasks + t) + 4] = ck_time();
+            if (k < nv && colok) obuf[col * OS + g + k * rstep] = y[k];
         }
         esync();
-        if (P.trace && rank == 0 && et == 0) P.trace[8 * (P.n_tasks + t) + 5] = ck_time();
         // ---- vector stores: 8 channels (bf16) / 4 channels (fp32) per thread
         if (e.out) {
-          if (et < 2 * bn) {
-            const int c = et >> 1, h = et & 1;
+          const int cpc = RPC >> 3;
+          if (et < cpc * bn) {
+            const int c = et / cpc, h = et - c * cpc;
             const int j2 = c >> lwo, p2 = c & (Wo - 1), s2 = nt * sbox + j2;
-            const int ch0 = chb + 8 * h;
+            const int ch0 = chan(8 * h);
             if (c < rows && s2 < S && ch0 < M) {
               __nv_bfloat162 b2[4];
               for (int i = 0; i < 4; ++i)
-                b2[i] = __floats2bfloat162_rn(obuf[c * CK_OS + 8 * h + 2 * i], obuf[c * CK_OS + 8 * h + 2 * i + 1]);
-              const int wout = e.out_stuff ? 2 * Wo : Wo;
+                b2[i] = __floats2bfloat162_rn(obuf[c * OS + 8 * h + 2 * i], obuf[c * OS + 8 * h + 2 * i + 1]);
               const int ox2 = e.out_stuff ? 2 * p2 : p2;
-              __nv_bfloat16 *dst = static_cast<__nv_bfloat16 *>(e.out) +
-                                   ((int64_t)s2 * wout + ox2) * e.out_pitch + e.out_coff + ch0;
+              __nv_bfloat16 *dst = op->out_base + (ch0 >> 6) * op->out_plane +
+                                   ((int64_t)s2 * op->out_T + ox2) * op->out_row + (ch0 & 63);
               *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>(b2);
-              if (e.out_stuff) *reinterpret_cast<uint4 *>(dst + e.out_pitch) = make_uint4(0, 0, 0, 0);
+              if (e.out_stuff) *reinterpret_cast<uint4 *>(dst + op->out_row) = make_uint4(0, 0, 0, 0);
             }
           }
         }
         if (e.out_f32) {
-          if (et < 4 * bn) {
-            const int c = et >> 2, h = et & 3;
+          const int cpc = RPC >> 2;
+          if (et < cpc * bn) {
+            const int c = et / cpc, h = et - c * cpc;
             const int j2 = c >> lwo, p2 = c & (Wo - 1), s2 = nt * sbox + j2;
-            const int ch0 = chb + 4 * h;
+            const int ch0 = chan(4 * h);
             if (c < rows && s2 < S && ch0 < M) {
-              const float *o = obuf + c * CK_OS + 4 * h;
+              const float *o = obuf + c * OS + 4 * h;
               *reinterpret_cast<float4 *>(e.out_f32 + ((int64_t)s2 * Wo + p2) * M + ch0) =
                   make_float4(o[0], o[1], o[2], o[3]);
             }
           }
         }
-        if (P.trace && rank == 0 && et == 0) P.trace[8 * (P.n_tasks + t) + 6] = ck_time();
         fence_proxy_async();
         esync();
-        if (P.trace && rank == 0 && et == 0) P.trace[8 * (P.n_tasks + t) + 7] = ck_time();
         if (et == 0) {
           red_release_add(&done[opi], 1);
           if (P.trace && rank == 0) P.trace[8 * t + 4] = ck_time();
@@ -613,7 +665,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   cluster_sync_all();                       // no CTA leaves while peers may still touch its smem
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * CK_BN));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(4 * CK_BN));
 }
 
 // ---------------------------------------------------------------- host side
@@ -653,6 +705,29 @@ static int cluster_capacity() {
   return cached = n;
 }
 
+static BlockedBuf *find_blocked(ClConfig &cc, const void *orig) {
+  for (auto &b : cc.blocked)
+    if (b.orig == orig) return &b;
+  return nullptr;
+}
+
+// 5-D view of a channel-blocked activation buffer: {64 channels, phase (the
+// conv stride), time / stride, sample, channel block}; box {64, 1, Wo, s_box, 1}.
+static int make_act_map_blocked(CUtensorMap *tm, const void *base, int Cin, int T, int stride, int S, int64_t plane,
+                                int Wo, int s_box) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return AURAS_E_CUDA; }
+  cuuint64_t dims[5] = {64, (cuuint64_t)stride, (cuuint64_t)(T / stride), (cuuint64_t)S, (cuuint64_t)(Cin / 64)};
+  cuuint64_t strides[4] = {128, (cuuint64_t)128 * stride, (cuuint64_t)128 * T, (cuuint64_t)plane * 2};
+  cuuint32_t box[5] = {64, 1, (cuuint32_t)Wo, (cuuint32_t)s_box, 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("blocked activation map: CUresult %d", (int)r); return AURAS_E_CUDA; }
+  return AURAS_OK;
+}
+
 int clus_build(ClConfig &cc, const std::vector<auras_conv_op> &ops, int S, const void *x_in,
                const ClParams &base, const float *film_tau, int film_width, const float *ring_film,
                TiledCache &cache) {
@@ -665,6 +740,8 @@ int clus_build(ClConfig &cc, const std::vector<auras_conv_op> &ops, int S, const
   // more clusters per layer, at the cost of re-streaming weights per n-tile
   int bn_cap = 64;
   if (const char *e = getenv("AURAS_CL_BN")) bn_cap = std::max(16, std::min(CK_BN, atoi(e)));
+  const char *de = getenv("AURAS_CL_DUAL");
+  const bool dual = de ? atoi(de) != 0 : true;
   std::vector<ClOp> hops(n);
   int n_flags = 0;
   for (int i = 0; i < n; ++i) {
@@ -691,16 +768,23 @@ int clus_build(ClConfig &cc, const std::vector<auras_conv_op> &ops, int S, const
       set_error("cluster kernel: op %d GroupNorm of %d channels", i, m.cg);
       return AURAS_E_ARG;
     }
-    m.pair = m.gn && m.cg == 256;
     m.M = o.M; m.Cin = o.Cin; m.Wo = o.Wo; m.stride = o.stride; m.pad = o.pad_w;
-    m.s_box = std::min(CK_SMAX, pow2_floor(std::max(1, std::min(S, bn_cap / o.Wo))));
+    m.m_tiles = (o.M + 127) / 128;
+    // two m-tiles per task when the layer has more tiles than there are clusters
+    // (16 tiles of a 2048-channel layer on 14 clusters would take two rounds) or
+    // a GroupNorm group spans two tiles (its statistics then stay in-cluster)
+    m.nmt = (dual && m.m_tiles % 2 == 0 && (m.m_tiles > nc || m.cg == 256)) ? 2 : 1;
+    m.pair = m.gn && m.cg == 256 && m.nmt == 1;
+    const int cap = m.nmt == 2 ? std::min(bn_cap, 32) : bn_cap;
+    m.s_box = std::min(CK_SMAX, pow2_floor(std::max(1, std::min(S, cap / o.Wo))));
     m.rows = m.s_box * o.Wo;
     m.bn = std::max(16, m.rows);
+    if (m.nmt == 2 && (m.bn > 32 || 4 * m.s_box > 32)) { set_error("cluster kernel: op %d dual tile", i); return AURAS_E_ARG; }
+    m.rsh = m.bn + 8;
     m.kb_total = o.Kp / 64;
     m.kps = (m.kb_total + CL - 1) / CL;
-    m.m_tiles = (o.M + 127) / 128;
     const int n_tiles = (S + m.s_box - 1) / m.s_box;
-    m.tiles = m.m_tiles * n_tiles;
+    m.tiles = (m.m_tiles / m.nmt) * n_tiles;
     if (m.pair && (m.m_tiles & 1)) { set_error("cluster kernel: op %d odd tile pair", i); return AURAS_E_ARG; }
     auto lg = [](int x) { int l = 0; while ((1 << l) < x) ++l; return l; };
     m.lwo = lg(m.Wo);
@@ -725,7 +809,64 @@ int clus_build(ClConfig &cc, const std::vector<auras_conv_op> &ops, int S, const
     void *wt = nullptr;
     if ((rc = tiled_weights(cache, o, &wt))) return rc;
     if ((rc = make_tiled_weight_map(&m.tmA, wt, m.m_tiles * m.kb_total * 128))) return rc;
-    if ((rc = make_act_map(&m.tmB, o.in, o.in_coff, o.Cin, o.in_pitch, o.W, o.stride, S, o.Wo, m.s_box))) return rc;
+    // ---- activation buffers: every tensor a later op reads through TMA is re-laid
+    //      out channel-blocked, [C/64][S][T][64], so an im2col box row run is
+    //      contiguous (TMA serves strided 128-byte rows at ~17 GB/s per SM)
+    if (o.in_coff % 64 || o.out_coff % 64 || o.res_coff % 64 || o.Cin % 64) {
+      set_error("cluster kernel: op %d channel offsets not 64-aligned", i);
+      return AURAS_E_ARG;
+    }
+    const __nv_bfloat16 *in_base;
+    int64_t in_plane;
+    int in_T;
+    if (o.in == x_in) {                         // the prep's [S][T][64] input is already blocked (C = 64)
+      if (o.in_pitch != 64 || o.in_coff) { set_error("cluster kernel: x buffer pitch"); return AURAS_E_ARG; }
+      in_base = static_cast<const __nv_bfloat16 *>(o.in);
+      in_T = o.W;
+      in_plane = (int64_t)S * in_T * 64;
+    } else {
+      const BlockedBuf *b = find_blocked(cc, o.in);
+      if (!b || b->T != o.W) { set_error("cluster kernel: op %d input not produced in-kernel", i); return AURAS_E_ARG; }
+      in_base = b->ptr + (o.in_coff >> 6) * b->plane;
+      in_plane = b->plane;
+      in_T = b->T;
+    }
+    if ((rc = make_act_map_blocked(&m.tmB, in_base, o.Cin, in_T, o.stride, S, in_plane, o.Wo, m.s_box))) return rc;
+    if (o.out) {
+      if (i == n - 1) {                         // read by the final 1x1 conv: keep the plan's layout
+        m.out_base = static_cast<__nv_bfloat16 *>(o.out) + o.out_coff;
+        m.out_plane = 64;
+        m.out_row = o.out_pitch;
+        m.out_T = o.out_stuff ? 2 * o.Wo : o.Wo;
+      } else {
+        const int T = o.out_stuff ? 2 * o.Wo : o.Wo;
+        BlockedBuf *b = find_blocked(cc, o.out);
+        if (!b) {
+          BlockedBuf nb;
+          nb.orig = o.out;
+          nb.T = T;
+          nb.plane = (int64_t)S * T * 64;
+          const size_t bytes = (size_t)(o.out_pitch / 64) * nb.plane * 2;
+          AURAS_CUDA(cudaMalloc(&nb.ptr, bytes));
+          AURAS_CUDA(cudaMemset(nb.ptr, 0, bytes));
+          cc.blocked.push_back(nb);
+          b = &cc.blocked.back();
+        }
+        if (b->T != T) { set_error("cluster kernel: op %d output length", i); return AURAS_E_ARG; }
+        m.out_base = b->ptr + (o.out_coff >> 6) * b->plane;
+        m.out_plane = b->plane;
+        m.out_row = 64;
+        m.out_T = T;
+      }
+    }
+    if (o.res) {
+      const BlockedBuf *b = find_blocked(cc, o.res);
+      if (!b) { set_error("cluster kernel: op %d residual not produced in-kernel", i); return AURAS_E_ARG; }
+      m.res_base = b->ptr + (o.res_coff >> 6) * b->plane;
+      m.res_plane = b->plane;
+      m.res_row = 64;
+      m.res_T = b->T;
+    }
     for (int d = 0; d < 3; ++d) m.gemm_dep[d] = -1;
     for (int d = 0; d < 2; ++d) m.epi_dep[d] = -1;
     int nd = 0;
@@ -746,10 +887,10 @@ int clus_build(ClConfig &cc, const std::vector<auras_conv_op> &ops, int S, const
   for (int i = 0; i < n; ++i) {
     const ClOp &m = hops[i];
     if (m.pair && (rot & 1)) rot = (rot + 1) % nc;     // pairs land on clusters (2c, 2c+1) in one round
-    const int n_tiles = m.tiles / m.m_tiles;
+    const int groups = m.m_tiles / m.nmt, n_tiles = m.tiles / groups;
     int q = 0;
     for (int nt = 0; nt < n_tiles; ++nt)
-      for (int mt = 0; mt < m.m_tiles; ++mt, ++q) per[(rot + q) % nc].push_back(make_int4(K_GEMM | (i << 8), mt, nt, 0));
+      for (int mg = 0; mg < groups; ++mg, ++q) per[(rot + q) % nc].push_back(make_int4(K_GEMM | (i << 8), mg, nt, 0));
     rot = (rot + q) % nc;
   }
   for (int s = 0; s < S; ++s) per[(rot + s) % nc].push_back(make_int4(K_FINAL, s, 0, (s / nc) % CL));
@@ -817,6 +958,7 @@ int clus_set_trace(ClConfig &cc, long long *trace) {
 }
 
 void clus_free(ClConfig &cc) {
+  for (auto &b : cc.blocked) cudaFree(b.ptr);
   cudaFree(cc.ops);
   cudaFree(cc.tasks);
   cudaFree(cc.cl_begin);
