@@ -14,7 +14,7 @@ import threading
 
 from .errors import DeviceError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libauras_b200.so")
+LIB_PATH = os.environ.get("AURAS_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libauras_b200.so")
 ABI_VERSION = 4
 
 DT_F32, DT_BF16 = 0, 1

@@ -52,8 +52,10 @@ int mega_build(MegaConfig &mc, const std::vector<auras_conv_op> &ops, int S, con
                TiledCache &cache);
 void mega_free_tiled(TiledCache &cache);
 // weights re-laid out as [m_tile][k_block][128][64] (cached per plan) and their tensor map
-int tiled_weights(TiledCache &cache, const auras_conv_op &o, void **out);
-int make_tiled_weight_map(CUtensorMap *tm, const void *wt, int rows_total);
+// nmt = 2: m-tiles interleaved in pairs per k-block ([pair][kb][2][128][64]);
+// such copies go in their own cache
+int tiled_weights(TiledCache &cache, const auras_conv_op &o, void **out, int nmt = 1);
+int make_tiled_weight_map(CUtensorMap *tm, const void *wt, int rows_total, int box_rows = 128);
 int mega_launch(const MegaConfig &mc, cudaStream_t st);
 int mega_set_trace(MegaConfig &mc, long long *trace);
 void mega_free(MegaConfig &mc);

@@ -88,6 +88,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
+// Wait for an mbarrier phase, backing off between probes: for warps whose
+// wait is not latency critical, so they do not take issue slots from a warp
+// on the same scheduler that is (the MMA issuer).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, int ns = 128) {
+  uint32_t ok;
+  while (true) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(ns);
+  }
+}
+
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, uint64_t *bar, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
@@ -276,4 +296,50 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+
+// One k-block (K = 64) of UMMAs from one elected lane: four K=16 steps along
+// the 128-byte swizzled rows (descriptor start address +32 B = +2 per step).
+// acc = 0 overwrites the accumulator on the first step.  nmt = 2 adds a second
+// M=128 tile whose A rows sit 16 KB (+1024 in descriptor units) further and
+// whose accumulator is `dt2`.
+__device__ __forceinline__ void umma_kblock_warp(uint32_t dt, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 rx;\n"
+      ".reg .pred px, p;\n"
+      ".reg .b64 a1, a2, a3, b1, b2, b3;\n"
+      "elect.sync rx|px, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "add.s64 a1, %1, 2;\n add.s64 a2, %1, 4;\n add.s64 a3, %1, 6;\n"
+      "add.s64 b1, %2, 2;\n add.s64 b2, %2, 4;\n add.s64 b3, %2, 6;\n"
+      "@px tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "@px tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, 1;\n"
+      "@px tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, 1;\n"
+      "@px tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, 1;\n"
+      "}\n" ::"r"(dt),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_kblock2_warp(uint32_t dt, uint32_t dt2, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                                  uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 rx;\n"
+      ".reg .pred px, p;\n"
+      ".reg .b64 a1, a2, a3, c0, c1, c2, c3, b1, b2, b3;\n"
+      "elect.sync rx|px, 0xffffffff;\n"
+      "setp.ne.b32 p, %5, 0;\n"
+      "add.s64 a1, %2, 2;\n add.s64 a2, %2, 4;\n add.s64 a3, %2, 6;\n"
+      "add.s64 c0, %2, 1024;\n add.s64 c1, %2, 1026;\n add.s64 c2, %2, 1028;\n add.s64 c3, %2, 1030;\n"
+      "add.s64 b1, %3, 2;\n add.s64 b2, %3, 4;\n add.s64 b3, %3, 6;\n"
+      "@px tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %4, p;\n"
+      "@px tcgen05.mma.cta_group::1.kind::f16 [%1], c0, %3, %4, p;\n"
+      "@px tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %4, 1;\n"
+      "@px tcgen05.mma.cta_group::1.kind::f16 [%1], c1, b1, %4, 1;\n"
+      "@px tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %4, 1;\n"
+      "@px tcgen05.mma.cta_group::1.kind::f16 [%1], c2, b2, %4, 1;\n"
+      "@px tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %4, 1;\n"
+      "@px tcgen05.mma.cta_group::1.kind::f16 [%1], c3, b3, %4, 1;\n"
+      "}\n" ::"r"(dt),
+      "r"(dt2), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
 }  // namespace auras

@@ -46,7 +46,14 @@
 namespace auras {
 
 constexpr int CL = 8;                     // CTAs per cluster (portable maximum)
-constexpr int CK_THREADS = 384;
+constexpr int CK_THREADS = 512;
+// Warp roles.  One TMA-issuing warp has ~one bulk tensor copy in flight at a
+// time (~0.4 us each, whatever the box size or ring depth; measured,
+// scratch/ubench/tma_w2.cu), so both operand streams are spread over warps.
+constexpr int CK_NWW = 4;                 // weight producer warps 0..3: warp w fills ring stages ia % 4 == w
+constexpr int CK_MMA_WARP = 4;
+constexpr int CK_BW0 = 5, CK_NBW = 3;     // activation TMA warps 5..7: warp 5 + (stage % 3)
+constexpr int CK_EW0 = 8;                 // epilogue warps 8..15 (8..11 also drain TMEM)
 constexpr int CK_EPI = 256;
 constexpr int CK_BN = 64;                 // max columns per tile task (TMEM: 2 x 64 columns)
 constexpr int CK_A_BYTES = 128 * 64 * 2;  // one 128 x 64 weight box
@@ -74,7 +81,8 @@ static_assert(32 * 33 <= CK_BN * CK_OS && 512 <= CK_BN * CK_OS, "staging buffer"
 enum { K_GEMM = 0, K_PREP = 2, K_FINAL = 3 };
 
 struct alignas(64) ClOp {
-  CUtensorMap tmA;
+  CUtensorMap tmA;            // weights, 256-row boxes: one TMA op per 32 KB ring stage
+  CUtensorMap tmA1;           // 128-row boxes (odd tail k-block of a K share)
   CUtensorMap tmB;
   EpiArgs epi;
   int M, Cin, Wo, stride, pad, s_box, rows, bn, kb_total, kps, m_tiles, tiles;
@@ -159,7 +167,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
     for (int i = 0; i < 2; ++i) mbar_init(&cbar[i], CL * 8);      // 8 epilogue warps of each of 8 CTAs
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) {
+  if (warp == CK_MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(4 * CK_BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -170,68 +178,68 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp < CK_NWW) {
     // ------------------------------------------------ weights: this CTA's K share of every task
-    // The smem ring holds only part of a large task's weights; while this CTA
-    // waits on activations, the rest of the current task and all of the next
-    // one are pulled into L2 (bulk tensor prefetch, one 16 KB box per lane), so
-    // the loads after the dependency resolves hit L2 instead of HBM.
+    // Optional L2 prefetch of the next task's share (off by default: measured
+    // +333 MB DRAM reads per step from lines evicted before use).
     auto l2_prefetch = [&](int t) {
       const int4 tk = P.tasks[t];
       const ClOp *op = &P.ops[tk.x >> 8];
       const int kps = op->kps, kbt = op->kb_total, nmt = op->nmt;
       const int kb0 = rank * kps, kb1 = min(kbt, kb0 + kps);
-      for (int u = 0; u < nmt; ++u) {
-        const int row0 = (tk.y * nmt + u) * kbt * 128;
-        for (int kb = kb0 + lane; kb < kb1; kb += 32)
-          asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(&op->tmA), "r"(0),
-                       "r"(row0 + kb * 128)
-                       : "memory");
-      }
+      const int step = 3 - nmt, row0 = tk.y * nmt * kbt * 128;
+      for (int kb = kb0 + step * lane; kb < kb1; kb += 32 * step)
+        asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(&op->tmA), "r"(0),
+                     "r"(row0 + kb * 128 * nmt)
+                     : "memory");
     };
     auto next_gemm = [&](int t) {
       for (++t; t < t1; ++t)
         if ((P.tasks[t].x & 0xff) == K_GEMM) return t;
       return -1;
     };
+    const bool pf = P.l2_prefetch && warp == 0;
     int ia = 0;
-    if (P.l2_prefetch) {
+    if (pf) {
       const int f = next_gemm(t0 - 1);
       if (f >= 0) l2_prefetch(f);
     }
     for (int t = t0; t < t1; ++t) {
       const int4 tk = P.tasks[t];
       if ((tk.x & 0xff) != K_GEMM) continue;
-      if (P.l2_prefetch) {
+      if (pf) {
         const int nx = next_gemm(t);
         if (nx >= 0) l2_prefetch(nx);
       }
       const ClOp *op = &P.ops[tk.x >> 8];
       const int kps = op->kps, kbt = op->kb_total;
-      const CUtensorMap *tmA = &op->tmA;
       const int kb0 = rank * kps, kb1 = min(kbt, kb0 + kps);
       const int nmt = op->nmt;
-      const int row0 = tk.y * nmt * kbt * 128;      // tiled layout [m_tile][k_block][128][64]
+      // tiled layouts: [m_tile][k_block][128][64] (nmt = 1), [pair][k_block][2][128][64] (nmt = 2);
+      // a ring stage (32 KB) is one 256-row box either way
+      const int row0 = tk.y * nmt * kbt * 128;
       if (nmt == 1) {                               // stage = 2 k-blocks of one m-tile
         for (int kb = kb0; kb < kb1; kb += 2, ++ia) {
+          if (ia % CK_NWW != warp) continue;
           const int st = ia % CK_NA;
-          const int two = kb + 1 < kb1;
+          const bool two = kb + 1 < kb1;
           mbar_wait(&emptyA[st], ((ia / CK_NA) & 1) ^ 1);
-          tma_load_2d_pair_warp(sA + st * CK_A_STAGE, tmA, &fullA[st], (1 + two) * CK_A_BYTES, 0, row0 + kb * 128,
-                                row0 + (kb + 1) * 128, two);
+          tma_load_2d_warp(sA + st * CK_A_STAGE, two ? &op->tmA : &op->tmA1, &fullA[st],
+                           two ? CK_A_STAGE : CK_A_BYTES, 0, row0 + kb * 128);
         }
       } else {                                      // stage = 1 k-block of both m-tiles
-        const int row1 = row0 + kbt * 128;
         for (int kb = kb0; kb < kb1; ++kb, ++ia) {
+          if (ia % CK_NWW != warp) continue;
           const int st = ia % CK_NA;
           mbar_wait(&emptyA[st], ((ia / CK_NA) & 1) ^ 1);
-          tma_load_2d_pair_warp(sA + st * CK_A_STAGE, tmA, &fullA[st], 2 * CK_A_BYTES, 0, row0 + kb * 128,
-                                row1 + kb * 128, 1);
+          tma_load_2d_warp(sA + st * CK_A_STAGE, &op->tmA, &fullA[st], CK_A_STAGE, 0, row0 + kb * 256);
         }
       }
     }
-  } else if (warp == 2) {
+  } else if (warp >= CK_BW0 && warp < CK_BW0 + CK_NBW) {
     // ------------------------------------------------ activations: after the producing ops
+    // k-block j of a task goes to ring stage j % nbst, issued by warp 5 + stage % 3
+    const int bw = warp - CK_BW0;
     uint32_t par = 0;
     for (int t = t0; t < t1; ++t) {
       const int4 tk = P.tasks[t];
@@ -251,6 +259,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
       const int kb0 = rank * kps, kb1 = min(kbt, kb0 + kps);
       for (int kb = kb0, j = 0; kb < kb1; ++kb, ++j) {
         const int sb = j % nbst;
+        if (sb % CK_NBW != bw) continue;
         mbar_wait(&emptyB[sb], ((par >> sb) & 1) ^ 1);
         par ^= 1u << sb;
         const int k = kb * 64;
@@ -261,7 +270,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         tma_load_5d_warp(sB + sb * bstage, tmB, &fullB[sb], bbytes, 0, h, q, tk.z * sbox, c0 >> 6);
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == CK_MMA_WARP) {
     // ------------------------------------------------ MMA issuer
     int ia = 0, gi = 0;
     uint32_t par = 0;
@@ -285,12 +294,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           par ^= 1u << sb;
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a0 = smem_u32(sA + sa * CK_A_STAGE), b0 = smem_u32(sB + sb * bstage);
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
-            umma_bf16_warp(dt, umma_desc(a0 + kk * 32), umma_desc(b0 + kk * 32), idesc, acc);
-            umma_bf16_warp(dt + CK_BN, umma_desc(a0 + CK_A_BYTES + kk * 32), umma_desc(b0 + kk * 32), idesc, acc);
-          }
+          umma_kblock2_warp(dt, dt + CK_BN, umma_desc(a0), umma_desc(b0), idesc, kb > kb0 ? 1u : 0u);
           umma_commit_warp(&emptyB[sb]);
           umma_commit_warp(&emptyA[sa]);
           __syncwarp();
@@ -313,10 +317,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a0 = smem_u32(sA + sa * CK_A_STAGE + i * CK_A_BYTES);
           const uint32_t b0 = smem_u32(sB + sb * bstage);
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            umma_bf16_warp(dt, umma_desc(a0 + kk * 32), umma_desc(b0 + kk * 32), idesc,
-                           (kb > kb0 || i > 0 || kk > 0) ? 1u : 0u);
+          umma_kblock_warp(dt, umma_desc(a0), umma_desc(b0), idesc, (kb > kb0 || i > 0) ? 1u : 0u);
           umma_commit_warp(&emptyB[sb]);
           __syncwarp();
         }
@@ -328,10 +329,10 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
       __syncwarp();
       ++gi;
     }
-  } else if (warp >= 4) {
+  } else if (warp >= CK_EW0) {
     // ------------------------------------------------ epilogue warps
-    const int et = threadIdx.x - 128;
-    const int ew = warp - 4;
+    const int et = threadIdx.x - 32 * CK_EW0;
+    const int ew = warp - CK_EW0;
     auto esync = [] __device__() { named_sync(1, CK_EPI); };
     int gi = 0, gn_i = 0;
     for (int t = t0; t < t1; ++t) {
@@ -665,7 +666,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   cluster_sync_all();                       // no CTA leaves while peers may still touch its smem
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(4 * CK_BN));
+  if (warp == CK_MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(4 * CK_BN));
 }
 
 // ---------------------------------------------------------------- host side
@@ -807,8 +808,9 @@ int clus_build(ClConfig &cc, const std::vector<auras_conv_op> &ops, int S, const
       n_flags += m.tiles;
     }
     void *wt = nullptr;
-    if ((rc = tiled_weights(cache, o, &wt))) return rc;
-    if ((rc = make_tiled_weight_map(&m.tmA, wt, m.m_tiles * m.kb_total * 128))) return rc;
+    if ((rc = tiled_weights(cache, o, &wt, m.nmt))) return rc;
+    if ((rc = make_tiled_weight_map(&m.tmA, wt, m.m_tiles * m.kb_total * 128, 256))) return rc;
+    if ((rc = make_tiled_weight_map(&m.tmA1, wt, m.m_tiles * m.kb_total * 128, 128))) return rc;
     // ---- activation buffers: every tensor a later op reads through TMA is re-laid
     //      out channel-blocked, [C/64][S][T][64], so an im2col box row run is
     //      contiguous (TMA serves strided 128-byte rows at ~17 GB/s per SM)
@@ -928,7 +930,7 @@ int clus_build(ClConfig &cc, const std::vector<auras_conv_op> &ops, int S, const
   cc.params.n_tasks = cc.n_tasks;
   {
     const char *e = getenv("AURAS_CL_L2PF");
-    cc.params.l2_prefetch = e ? atoi(e) : 1;
+    cc.params.l2_prefetch = e ? atoi(e) : 0;
   }
   return AURAS_OK;
 }

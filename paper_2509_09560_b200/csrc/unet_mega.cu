@@ -333,14 +333,19 @@ __global__ void __launch_bounds__(MK_THREADS, 1) unet_mega(const __grid_constant
 // Weights re-laid out as [m_tile][k_block][128 rows][64] so that every 16 KB
 // TMA box -- and a task's whole run of k-blocks -- is contiguous in HBM.
 __global__ void tile_weights_kernel(const __nv_bfloat16 *__restrict__ src, __nv_bfloat16 *__restrict__ dst, int M,
-                                    int Kp, int m_tiles) {
+                                    int Kp, int m_tiles, int nmt) {
   const int KB = Kp / 64;
   const int64_t total = (int64_t)m_tiles * KB * 128 * 8;     // 16-byte chunks
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int chunk = i & 7;
     const int64_t rowi = i >> 3;
     const int r = rowi & 127;
-    const int64_t tile = rowi >> 7;
+    int64_t tile = rowi >> 7;
+    if (nmt == 2) {                     // pairs of m-tiles interleaved per k-block: [pair][kb][2][128][64]
+      const int u = tile & 1;
+      const int64_t q = tile >> 1;
+      tile = ((q / KB) * 2 + u) * KB + q % KB;
+    }
     const int kb = tile % KB, mt = tile / KB;
     const int m = mt * 128 + r;
     uint4 v = make_uint4(0, 0, 0, 0);
@@ -349,12 +354,12 @@ __global__ void tile_weights_kernel(const __nv_bfloat16 *__restrict__ src, __nv_
   }
 }
 
-int make_tiled_weight_map(CUtensorMap *tm, const void *wt, int rows_total) {
+int make_tiled_weight_map(CUtensorMap *tm, const void *wt, int rows_total, int box_rows) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return AURAS_E_CUDA; }
   cuuint64_t dims[2] = {64, (cuuint64_t)rows_total};
   cuuint64_t strides[1] = {128};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(wt), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -363,7 +368,7 @@ int make_tiled_weight_map(CUtensorMap *tm, const void *wt, int rows_total) {
   return AURAS_OK;
 }
 
-int tiled_weights(TiledCache &cache, const auras_conv_op &o, void **out) {
+int tiled_weights(TiledCache &cache, const auras_conv_op &o, void **out, int nmt) {
   for (auto &kv : cache)
     if (kv.first == o.w) { *out = kv.second; return AURAS_OK; }
   const int m_tiles = (o.M + 127) / 128;
@@ -371,7 +376,7 @@ int tiled_weights(TiledCache &cache, const auras_conv_op &o, void **out) {
   void *d = nullptr;
   AURAS_CUDA(cudaMalloc(&d, bytes));
   tile_weights_kernel<<<1184, 256>>>(static_cast<const __nv_bfloat16 *>(o.w), static_cast<__nv_bfloat16 *>(d), o.M,
-                                     o.Kp, m_tiles);
+                                     o.Kp, m_tiles, nmt);
   AURAS_LAUNCHED("tile_weights_kernel");
   AURAS_CUDA(cudaDeviceSynchronize());
   cache.emplace_back(o.w, d);

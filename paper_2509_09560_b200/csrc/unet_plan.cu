@@ -70,6 +70,7 @@ struct auras_unet_plan {
   float *dry_x = nullptr;                    // scratch request lanes for autotuning runs
   int64_t *dry_fetched = nullptr;
   TiledCache tiled;                          // tiled weight copies shared by all S
+  TiledCache tiled_cl;                       // the cluster kernel's copies (m-tile pairs interleaved)
 };
 
 static int mega_kernel_launch(auras_unet_plan *p, int S, bool cluster, cudaStream_t st) {
@@ -109,7 +110,7 @@ static int build_cluster_config(auras_unet_plan *p, int S, const MegaParams &bas
   cb.wf = base.wf;
   cb.bf = base.bf;
   ClConfig cc;
-  int rc = clus_build(cc, p->ops, S, p->x_in, cb, p->film_tau, p->film_width, p->ring_film, p->tiled);
+  int rc = clus_build(cc, p->ops, S, p->x_in, cb, p->film_tau, p->film_width, p->ring_film, p->tiled_cl);
   if (rc) {
     clus_free(cc);
     return rc;
@@ -302,6 +303,7 @@ void auras_unet_plan_destroy(auras_unet_plan *p) {
   if (p->dry_x) cudaFree(p->dry_x);
   if (p->dry_fetched) cudaFree(p->dry_fetched);
   mega_free_tiled(p->tiled);
+  mega_free_tiled(p->tiled_cl);
   for (auto &kv : p->graphs) cudaGraphExecDestroy(kv.second);
   if (p->partial) cudaFree(p->partial);
   if (p->dev) cudaFree(p->dev);

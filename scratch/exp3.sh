@@ -1,0 +1,4 @@
+#!/bin/bash
+mkdir -p gpurun_out
+AURAS_MEGA_KERNEL=cluster timeout 300 python scratch/step_time.py 8 pusht trace > gpurun_out/exp3_8.log 2>&1
+python scratch/ctrace.py gpurun_out/ctrace_8.json 2>&1 | head -36 >> gpurun_out/exp3_8.log

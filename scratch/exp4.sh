@@ -1,0 +1,10 @@
+#!/bin/bash
+mkdir -p gpurun_out
+AURAS_MEGA_KERNEL=cluster timeout 600 python -m pytest tests/test_gpu_dp.py -x -q > gpurun_out/exp4_pytest.log 2>&1; echo "rc $?" >> gpurun_out/exp4_pytest.log
+for pf in 1 0; do
+for S in 8 64; do
+echo "pf=$pf" >> gpurun_out/exp4_$S.log
+AURAS_CL_L2PF=$pf AURAS_MEGA_KERNEL=cluster timeout 300 python scratch/step_time.py $S pusht trace >> gpurun_out/exp4_$S.log 2>&1
+python scratch/ctrace.py gpurun_out/ctrace_$S.json 2>&1 | head -36 >> gpurun_out/exp4_$S.log
+done
+done
