@@ -53,7 +53,10 @@ constexpr int CK_THREADS = 512;
 constexpr int CK_NWW = 4;                 // weight producer warps 0..3: warp w fills ring stages ia % 4 == w
 constexpr int CK_MMA_WARP = 4;
 constexpr int CK_BW0 = 5, CK_NBW = 3;     // activation TMA warps 5..7: warp 5 + (stage % 3)
-constexpr int CK_EW0 = 8;                 // epilogue warps 8..15 (8..11 also drain TMEM)
+constexpr int CK_EW0 = 8;
+#ifndef CK_WARP_BAR
+#define CK_WARP_BAR 0                     // 1: every epilogue warp arrives on every peer's cluster barrier
+#endif                 // epilogue warps 8..15 (8..11 also drain TMEM)
 constexpr int CK_EPI = 256;
 constexpr int CK_BN = 64;                 // max columns per tile task (TMEM: 2 x 64 columns)
 constexpr int CK_A_BYTES = 128 * 64 * 2;  // one 128 x 64 weight box
@@ -164,7 +167,11 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
     for (int i = 0; i < CK_NA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], 1); }
     for (int i = 0; i < CK_NBMAX; ++i) { mbar_init(&fullB[i], 1); mbar_init(&emptyB[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+#if CK_WARP_BAR
     for (int i = 0; i < 2; ++i) mbar_init(&cbar[i], CL * 8);      // 8 epilogue warps of each of 8 CTAs
+#else
+    for (int i = 0; i < 2; ++i) mbar_init(&cbar[i], CL);          // one leader thread of each of 8 CTAs
+#endif
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == CK_MMA_WARP) {
@@ -456,7 +463,11 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           if (lane == 0) mbar_arrive(&tempty[buf]);
           if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 5] = ck_time();
         }
+#if CK_WARP_BAR
         cluster_barrier_warp(&cbar[0], cpar, lane);
+#else
+        cluster_barrier_cta(&cbar[0], cpar, ew == 0, lane, esync);
+#endif
         if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 2] = ck_time();
         // ---- fixed-order sum of the 8 K slices + bias; values also staged as obuf[col][row]
 #pragma unroll
@@ -512,7 +523,11 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           }
         }
         if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 6] = ck_time();
+#if CK_WARP_BAR
         if (gn) cluster_barrier_warp(&cbar[1], gn_i & 1, lane);      // statistics exchange
+#else
+        if (gn) cluster_barrier_cta(&cbar[1], gn_i & 1, ew == 0, lane, esync);
+#endif
         if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 3] = ck_time();
         if (gn) {
           // ---- merge the atoms of each group (butterfly, fixed lane order); task atoms are
