@@ -350,6 +350,18 @@ def main():
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     tflops = S_med * flops_sample / (step_ms / 1e3) / 1e12 if step_ms > 0 else 0.0
+    # DRAM bytes per launch of the denoise kernel from the committed ncu --set full
+    # capture (profiles/r1_ncu_unet_cluster.json), for the same S, when it was captured
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "r1_ncu_unet_cluster.json")))
+        dk = LAST_EVENTS.get("denoise_kernel") or {}
+        kern = dk.get(S_med) or dk.get(str(S_med)) or ""
+        if f"S{S_med}" in prof and "cluster" in kern:
+            p_s = prof[f"S{S_med}"]
+            traffic = p_s["dram_read_bytes"] + p_s["dram_write_bytes"]
+    except (OSError, ValueError, KeyError):
+        pass
     tc_peak = float(peaks.get("bf16_tflops_sustained", 1400.0))
 
     # our kernel launches inside the timed region, per frame, from the programs:
@@ -377,7 +389,8 @@ def main():
                       "perception_device": args.perception_device},
            "p99_action_latency_ms": p99, "mean_action_latency_ms": jmean,
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                        "frac": achieved / hbm_peak, "traffic": None,
+                        "frac": achieved / hbm_peak, "traffic": traffic,
+                        "traffic_source": "ncu dram__bytes_read+write per launch, profiles/r1_ncu_unet_cluster.json",
                         "kernel": "denoise chain (UNet conv GEMMs + fused epilogues), per step",
                         "step_ms": step_ms, "algorithmic_bytes_per_step": bytes_step + act_bytes,
                         "tensor_tflops": tflops, "tensor_frac": tflops / tc_peak,
