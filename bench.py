@@ -204,8 +204,11 @@ def run_window(policy, depth, offset, agents, W, K, dist, device, sequential=Fal
 
 
 def steady_jct_ms(res, t0, K):
+    # requests born inside the timed window (steady state) and finished in it: a
+    # request born during fill / warm-up would carry one-time graph capture and
+    # autotuning of the fill-time batch sizes in its JCT
     vals = [r.jct * 1e3 for r in res.requests
-            if r.completion_frame > 0 and t0 <= r.completion_frame - 1 < t0 + K]
+            if r.completion_frame > 0 and r.birth_frame >= t0 and r.completion_frame - 1 < t0 + K]
     if not vals:
         return None, None
     return float(np.percentile(vals, 99)), float(np.mean(vals))
