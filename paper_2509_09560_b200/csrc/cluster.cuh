@@ -41,6 +41,22 @@ __device__ __forceinline__ void st_cluster_v4_b32(uint32_t addr, uint32_t a, uin
                : "memory");
 }
 
+// DSMEM store that also signals `bytes` of completed transaction on an mbarrier
+// of the destination CTA (the receiver waits on its own barrier; no separate
+// release/arrive round trip).
+__device__ __forceinline__ void st_async_v4_b32(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                                uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
+               "r"(a), "r"(b), "r"(c), "r"(d), "r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void st_async_v2_f32(uint32_t addr, float a, float b, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(addr), "f"(a),
+               "f"(b), "r"(bar)
+               : "memory");
+}
+
 __device__ __forceinline__ void st_cluster_v2(uint32_t addr, float a, float b) {
   asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(a), "f"(b) : "memory");
 }

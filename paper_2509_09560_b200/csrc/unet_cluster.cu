@@ -54,6 +54,9 @@ constexpr int CK_NWW = 4;                 // weight producer warps 0..3: warp w 
 constexpr int CK_MMA_WARP = 4;
 constexpr int CK_BW0 = 5, CK_NBW = 3;     // activation TMA warps 5..7: warp 5 + (stage % 3)
 constexpr int CK_EW0 = 8;
+#ifndef CK_TXBAR
+#define CK_TXBAR 1                        // DSMEM pushes signal the receiver's mbarrier (st.async complete_tx)
+#endif
 #ifndef CK_WARP_BAR
 #define CK_WARP_BAR 0                     // 1: every epilogue warp arrives on every peer's cluster barrier
 #endif                 // epilogue warps 8..15 (8..11 also drain TMEM)
@@ -75,7 +78,7 @@ constexpr int OFF_RBUF = OFF_STATS + CL * 32 * 8;        // stats: CL x (atoms x
 constexpr int OFF_OBUF = OFF_RBUF + CK_BN * CK_OS * 4;
 constexpr int OFF_MR = OFF_OBUF + CK_BN * CK_OS * 4;
 constexpr int OFF_BAR = OFF_MR + 4 * CK_SMAX * 8;
-constexpr int CK_NBARS = 2 * CK_NA + 2 * CK_NBMAX + 2 + 2 + 2;
+constexpr int CK_NBARS = 2 * CK_NA + 2 * CK_NBMAX + 2 + 2 + 2 + 4;
 constexpr size_t CK_SMEM = 1024 + OFF_BAR + CK_NBARS * 8 + 16;
 static_assert(CK_SMEM <= 232448, "cluster kernel shared memory");
 static_assert(CL * 16 * (CK_BN + 8) * 2 <= RECV_BYTES, "receive buffer");
@@ -154,7 +157,8 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
   uint64_t *tfull = emptyB + CK_NBMAX;
   uint64_t *tempty = tfull + 2;
   uint64_t *cbar = tempty + 2;             // [0] after the accumulator push, [1] after the statistics push
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(cbar + 2);
+  uint64_t *rbar = cbar + 2;               // transaction barriers: [buf] partials received, [2 + i] statistics received
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rbar + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = (int)cluster_ctarank();
@@ -172,6 +176,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
 #else
     for (int i = 0; i < 2; ++i) mbar_init(&cbar[i], CL);          // one leader thread of each of 8 CTAs
 #endif
+    for (int i = 0; i < 4; ++i) mbar_init(&rbar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == CK_MMA_WARP) {
@@ -368,6 +373,12 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         auto chan = [&](int r) { return (mt0 + (r >> 4)) * 128 + 16 * rank + (r & 15); };
         // ---- residual producers and the per-sample FiLM rows (prep) first
         if (et == 0) {
+#if CK_TXBAR
+          // bytes this CTA will receive: 16 * nmt rows x bn fp16 partials from each of the 8
+          // CTAs; with GroupNorm, (mean, M2) of 2 * nmt atoms x s_box samples from each
+          mbar_expect_tx(&rbar[buf], (uint32_t)(CL * 16 * nmt * bn * 2));
+          if (gn) mbar_expect_tx(&rbar[2 + (gn_i & 1)], (uint32_t)(CL * 2 * nmt * sbox * 8));
+#endif
           if (film) ck_spin(prep_done, S);
           for (int d = 0; d < 2; ++d) ck_wait_dep(P, prep_done, op->epi_dep[d], op->epi_tgt[d]);
         }
@@ -440,6 +451,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
             // fp16 partial sums (K/8 terms each, fp32-accumulated in TMEM): half the
             // DSMEM traffic; the owner sums the 8 slices in fp32
             const uint32_t dst = mapa_shared(smem_u32(recvb + (rank * RPC + u * 16 + (m & 15)) * RSH), m >> 4);
+            const uint32_t rbar_dst = mapa_shared(smem_u32(&rbar[buf]), m >> 4);
             for (int c = 0; c < bn; c += 16) {
               float x[16];
               if (nkb > 0) {
@@ -454,8 +466,13 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
                 const __half2 h2 = __floats2half2_rn(x[2 * i], x[2 * i + 1]);
                 hw[i] = *reinterpret_cast<const uint32_t *>(&h2);
               }
+#if CK_TXBAR
+              st_async_v4_b32(dst + c * 2, hw[0], hw[1], hw[2], hw[3], rbar_dst);
+              st_async_v4_b32(dst + c * 2 + 16, hw[4], hw[5], hw[6], hw[7], rbar_dst);
+#else
               st_cluster_v4_b32(dst + c * 2, hw[0], hw[1], hw[2], hw[3]);
               st_cluster_v4_b32(dst + c * 2 + 16, hw[4], hw[5], hw[6], hw[7]);
+#endif
             }
           }
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -463,7 +480,9 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           if (lane == 0) mbar_arrive(&tempty[buf]);
           if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 5] = ck_time();
         }
-#if CK_WARP_BAR
+#if CK_TXBAR
+        mbar_wait_cluster(&rbar[buf], (gi >> 1) & 1);            // all 8 CTAs' partials have landed
+#elif CK_WARP_BAR
         cluster_barrier_warp(&cbar[0], cpar, lane);
 #else
         cluster_barrier_cta(&cbar[0], cpar, ew == 0, lane, esync);
@@ -512,8 +531,14 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
             }
             const float mean = sum / n0;
             const float m2a = fmaxf(sq - sum * mean, 0.f);
-            if (li < CL)                                  // lane li -> CTA li
+            if (li < CL) {                                // lane li -> CTA li
+#if CK_TXBAR
+              st_async_v2_f32(mapa_shared(smem_u32(stats + (rank * A + pa) * sbox + pj), li), mean, m2a,
+                              mapa_shared(smem_u32(&rbar[2 + (gn_i & 1)]), li));
+#else
               st_cluster_v2(mapa_shared(smem_u32(stats + (rank * A + pa) * sbox + pj), li), mean, m2a);
+#endif
+            }
             if (pair && li == (CL & (L - 1)))            // the partner tile reads its atoms from L2
               __stcg(&P.gstats[((int64_t)fi * 16 + rank * 2 + pa) * CK_SMAX + pj], make_float2(mean, m2a));
           }
@@ -523,7 +548,9 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           }
         }
         if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 6] = ck_time();
-#if CK_WARP_BAR
+#if CK_TXBAR
+        if (gn) mbar_wait_cluster(&rbar[2 + (gn_i & 1)], (gn_i >> 1) & 1);   // every peer's statistics
+#elif CK_WARP_BAR
         if (gn) cluster_barrier_warp(&cbar[1], gn_i & 1, lane);      // statistics exchange
 #else
         if (gn) cluster_barrier_cta(&cbar[1], gn_i & 1, ew == 0, lane, esync);
