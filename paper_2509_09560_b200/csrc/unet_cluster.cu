@@ -383,62 +383,48 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           for (int d = 0; d < 2; ++d) ck_wait_dep(P, prep_done, op->epi_dep[d], op->epi_tgt[d]);
         }
         esync();
-        // ---- element ownership: column col, rows g + k * rstep (k < nv) of the owned slice
-        const int col = et & (bn - 1), g = et >> lbn, rstep = CK_EPI >> lbn, nv = (RPC * bn) >> 8;
-        const int jl = col >> lwo;
-        const int s = nt * sbox + jl;
-        const bool colok = col < rows && s < S;
-        float bias[4], gam[4], bet[4], sc[4], bi[4], v[4];
-        const float *fa = nullptr, *fb = nullptr;
-        if (film && colok) {
-          fa = e.film_a + (int64_t)e.film_a_row[s] * e.film_a_stride + e.film_off;
-          fb = e.film_b ? e.film_b + e.film_b_off[s] + e.film_off : nullptr;
-        }
+        // ---- element ownership.  Thread et belongs to (atom pa, sample pj) pair pi = et / L
+        //      (L lanes per pair, L | 32, L >= 2 Wo); lane li < 2 Wo owns channels 4 hh .. 4 hh + 3
+        //      (hh = li / Wo) of the atom's 8 rows at time tq = li % Wo, i.e. tile column
+        //      col = pj * Wo + tq.  The slice sums, the atom statistics (warp shuffles), the
+        //      group merge and the store all run on these registers: no staging, no CTA barrier.
+        const int lL = min(5, 8 - lsb - nmt), L = 1 << lL;         // L = min(32, 256 / (A * sbox))
+        const int pi = et >> lL, li = et & (L - 1);
+        const int pa = pi >> lsb, pj = pi & (sbox - 1);
+        const bool in_pair = pi < A * sbox;
+        const int hh = li >> lwo, tq = li & (Wo - 1);
+        const int col = pj * Wo + tq;
+        const int s = nt * sbox + pj;
+        const int row0 = 8 * pa + 4 * hh;                  // first owned row (0..RPC-1)
+        const int ch0 = chan(row0);                        // its channel (4 consecutive channels)
+        const bool mine = in_pair && li < 2 * Wo && col < rows && s < S && ch0 < M;
+        float bias[4], gam[4], bet[4], sc[4], bi[4], v[4], r[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const int ch = chan(g + k * rstep);
-          const bool ok = k < nv && colok && ch < M;
-          bias[k] = (ok && e.bias) ? e.bias[ch] : 0.f;
-          gam[k] = (ok && gn) ? e.gn_gamma[ch] : 1.f;
-          bet[k] = (ok && gn) ? e.gn_beta[ch] : 0.f;
-          sc[k] = 1.f;
-          bi[k] = 0.f;
-          if (ok && fa) {
-            sc[k] = fa[ch] + (fb ? fb[ch] : 0.f);
-            bi[k] = fa[M + ch] + (fb ? fb[M + ch] : 0.f);
-          }
+          bias[k] = 0.f; gam[k] = 1.f; bet[k] = 0.f; sc[k] = 1.f; bi[k] = 0.f; r[k] = 0.f;
         }
-        if (has_res) {                                    // residual tile -> rbuf[col][RPC]
-          const int lper = e.res ? 1 : 2;                 // 8 (bf16) or 4 (fp32) channels per chunk
-          const int cpc = RPC >> (3 - lper + 1);          // chunks per column: RPC/8 or RPC/4
-          if (et < cpc * bn) {
-            const int c = et / cpc, h = et - c * cpc;
-            const int j2 = c >> lwo, p2 = c & (Wo - 1), s2 = nt * sbox + j2;
-            const int nvals = 16 >> lper;
-            const int r0 = h * nvals;
-            const int ch0 = chan(r0);
-            float tmp[8];
+        if (mine) {
+          const float *fa = film ? e.film_a + (int64_t)e.film_a_row[s] * e.film_a_stride + e.film_off : nullptr;
+          const float *fb = (film && e.film_b) ? e.film_b + e.film_b_off[s] + e.film_off : nullptr;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) tmp[i] = 0.f;
-            if (c < rows && s2 < S && ch0 < M) {
-              if (e.res) {
-                const uint4 u = *reinterpret_cast<const uint4 *>(
-                    op->res_base + (ch0 >> 6) * op->res_plane + ((int64_t)s2 * op->res_T + p2) * op->res_row + (ch0 & 63));
-                const __nv_bfloat162 *b2 = reinterpret_cast<const __nv_bfloat162 *>(&u);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  const float2 f = __bfloat1622float2(b2[i]);
-                  tmp[2 * i] = f.x;
-                  tmp[2 * i + 1] = f.y;
-                }
-              } else {
-                const float4 f = *reinterpret_cast<const float4 *>(e.res_f32 + ((int64_t)s2 * Wo + p2) * M + ch0);
-                tmp[0] = f.x; tmp[1] = f.y; tmp[2] = f.z; tmp[3] = f.w;
-              }
+          for (int k = 0; k < 4; ++k) {
+            const int ch = ch0 + k;
+            if (e.bias) bias[k] = e.bias[ch];
+            if (gn) { gam[k] = e.gn_gamma[ch]; bet[k] = e.gn_beta[ch]; }
+            if (fa) {
+              sc[k] = fa[ch] + (fb ? fb[ch] : 0.f);
+              bi[k] = fa[M + ch] + (fb ? fb[M + ch] : 0.f);
             }
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (i < nvals) rbuf[c * OS + r0 + i] = tmp[i];
+          }
+          if (e.res) {                                   // 4 bf16 channels of the residual
+            const uint2 u = __ldcg(reinterpret_cast<const uint2 *>(
+                op->res_base + (ch0 >> 6) * op->res_plane + ((int64_t)s * op->res_T + tq) * op->res_row + (ch0 & 63)));
+            const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.x));
+            const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.y));
+            r[0] = f0.x; r[1] = f0.y; r[2] = f1.x; r[3] = f1.y;
+          } else if (e.res_f32) {
+            const float4 f = __ldcg(reinterpret_cast<const float4 *>(e.res_f32 + ((int64_t)s * Wo + tq) * M + ch0));
+            r[0] = f.x; r[1] = f.y; r[2] = f.z; r[3] = f.w;
           }
         }
         // ---- drain TMEM and push row slices to their owners (reduce-scatter over DSMEM)
@@ -488,43 +474,27 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         cluster_barrier_cta(&cbar[0], cpar, ew == 0, lane, esync);
 #endif
         if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 2] = ck_time();
-        // ---- fixed-order sum of the 8 K slices + bias; values also staged as obuf[col][row]
+        // ---- fixed-order sum of the 8 K slices + bias (fp32)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           float acc = bias[k];
-          if (k < nv) {
-            const __half *rp = recvb + (g + k * rstep) * RSH + col;
+          if (mine) {
+            const __half *rp = recvb + (row0 + k) * RSH + col;
 #pragma unroll
             for (int src = 0; src < CL; ++src) acc += __half2float(rp[src * RPC * RSH]);
           }
           v[k] = acc;
         }
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (k < nv) obuf[col * OS + g + k * rstep] = v[k];
-        // GroupNorm bookkeeping: (atom a, sample j) pairs, L lanes each (L | 32)
-        const int lL = min(5, 8 - lsb - nmt), L = 1 << lL;         // L = min(32, 256 / (A * sbox))
-        const int pi = et >> lL, li = et & (L - 1);
-        const int pa = pi >> lsb, pj = pi & (sbox - 1);
-        const bool in_pair = pi < A * sbox;
         const float n0 = 8.f * Wo;
         const int fi = pair ? op->flag_base + nt * op->m_tiles + mt0 : 0;
+        float mean_g = 0.f, rstd_g = 1.f;
         if (gn) {
-          esync();
-          // ---- atom statistics: sum and sum of squares over 8 rows x Wo columns, butterfly over L lanes
+          // ---- atom statistics: 8 rows x Wo columns of (pa, pj), butterfly over the pair's L lanes
           if (in_pair) {
             float sum = 0.f, sq = 0.f;
-            const int per = (8 * Wo) >> lL;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              if (i < per) {
-                const int idx = li + i * L;
-                const int r8 = idx >> lwo, c = idx & (Wo - 1);
-                const float x = obuf[(pj * Wo + c) * OS + 8 * pa + r8];
-                sum += x;
-                sq += x * x;
-              }
-            }
+            for (int k = 0; k < 4; ++k)
+              if (mine) { sum += v[k]; sq += v[k] * v[k]; }
             for (int o = 1; o < L; o <<= 1) {
               sum += __shfl_xor_sync(0xffffffffu, sum, o);
               sq += __shfl_xor_sync(0xffffffffu, sq, o);
@@ -542,7 +512,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
             if (pair && li == (CL & (L - 1)))            // the partner tile reads its atoms from L2
               __stcg(&P.gstats[((int64_t)fi * 16 + rank * 2 + pa) * CK_SMAX + pj], make_float2(mean, m2a));
           }
-          if (pair) {                                     // published before the cluster barrier
+          if (pair) {                                     // published before the exchange
             esync();
             if (et == 0) red_release_add(&P.flags[fi], 1);
           }
@@ -559,31 +529,32 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         if (gn) {
           // ---- merge the atoms of each group (butterfly, fixed lane order); task atoms are
           //      numbered in channel order q = tile * 16 + within-tile atom; 256-channel groups
-          //      split over two tasks also merge the partner tile's statistics from L2
+          //      split over two tasks also merge the partner tile's statistics from L2.  Every
+          //      lane of the pair ends with the group's (mean, rstd).
           float2 gs = make_float2(0.f, 0.f);
-          float ncount = 0.f;
+          float ncount = 1.f;
           if (pair) {                                     // partner tile's 8 CTAs have published
             if (et == 0) ck_spin(&P.flags[fi ^ 1], CL);
             esync();
           }
           if (in_pair) {
-            const int ch0 = chan(8 * pa);
-            const int gf = (ch0 >> lcg) << lcg;
+            const int cha = chan(8 * pa);
+            const int gf = (cha >> lcg) << lcg;
             const int tlo = mt0 * 128, thi = min((mt0 + nmt) * 128, M);
             const int lo = max(gf, tlo), hi = min(gf + cg, thi);
-            const int q0 = (lo - tlo) >> 3, k = (hi - lo) >> 3;
+            const int q0 = (lo - tlo) >> 3, kq = (hi - lo) >> 3;
             auto atom = [&](const float2 *base, int q) {  // task atom q -> stats entry
               const int w = q & 15, u = q >> 4;
               return base[((w >> 1) * A + 2 * u + (w & 1)) * sbox + pj];
             };
-            // butterfly merge of k equal-count atoms, up to 4 per lane
+            // butterfly merge of kq equal-count atoms, up to 4 per lane
             auto merge = [&](const float2 *base, bool global) {
               float2 at[4];
               bool hv[4];
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
                 const int q = li + i * L;
-                hv[i] = q < k;
+                hv[i] = q < kq;
                 at[i] = make_float2(0.f, 0.f);
                 if (hv[i]) at[i] = global ? __ldcg(base + (int64_t)(q0 + q) * CK_SMAX + pj) : atom(base, q0 + q);
               }
@@ -591,7 +562,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
 #pragma unroll
               for (int i = 0; i < 4; ++i) m += hv[i] ? at[i].x : 0.f;
               for (int o = 1; o < L; o <<= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
-              m /= (float)k;
+              m /= (float)kq;
               float q = 0.f;
 #pragma unroll
               for (int i = 0; i < 4; ++i)
@@ -600,7 +571,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
               return make_float2(m, q);
             };
             gs = merge(stats, false);
-            ncount = n0 * k;
+            ncount = n0 * kq;
             if (pair) {                                   // partner tile (16 atoms), lower tile first
               const float2 other = merge(P.gstats + (int64_t)(fi ^ 1) * 16 * CK_SMAX, true);
               const float2 lo2 = (mt0 & 1) ? other : gs, hi2 = (mt0 & 1) ? gs : other;
@@ -610,28 +581,20 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
               ncount *= 2.f;
             }
           }
-          if (in_pair && li == 0) mr[pa * CK_SMAX + pj] = make_float2(gs.x, rsqrtf(gs.y / ncount + 1e-5f));
-          esync();
+          mean_g = gs.x;
+          rstd_g = rsqrtf(gs.y / ncount + 1e-5f);
         }
         if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 7] = ck_time();
-        // ---- normalise, activate, FiLM, residual -> staging tile (branch-free per element)
-        {
+        // ---- normalise, activate, FiLM, residual (registers) and store 4 channels
+        if (mine) {
           const float rba = e.res_before_act ? 1.f : 0.f;
           const float is_mish = e.act == AURAS_ACT_MISH ? 1.f : 0.f;
           const float is_relu = e.act == AURAS_ACT_RELU ? 1.f : 0.f;
           const float is_none = 1.f - is_mish - is_relu;
-          float2 m2[4];
-          float r[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {                   // all shared-memory loads first
-            const int row = (g + k * rstep) & (RPC - 1);
-            m2[k] = gn ? mr[(row >> 3) * CK_SMAX + (jl & (CK_SMAX - 1))] : make_float2(0.f, 1.f);
-            r[k] = has_res ? rbuf[col * OS + row] : 0.f;
-          }
           float y[4];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            float x = (v[k] - m2[k].x) * m2[k].y * gam[k] + bet[k];
+            float x = gn ? (v[k] - mean_g) * rstd_g * gam[k] + bet[k] : v[k];
             x += rba * r[k];
             const float ex = __expf(fminf(x, 20.f));
             const float nn = ex * (ex + 2.f);
@@ -641,42 +604,17 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
             x = x * sc[k] + bi[k];
             y[k] = x + (1.f - rba) * r[k];
           }
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (k < nv && colok) obuf[col * OS + g + k * rstep] = y[k];
-        }
-        esync();
-        // ---- vector stores: 8 channels (bf16) / 4 channels (fp32) per thread
-        if (e.out) {
-          const int cpc = RPC >> 3;
-          if (et < cpc * bn) {
-            const int c = et / cpc, h = et - c * cpc;
-            const int j2 = c >> lwo, p2 = c & (Wo - 1), s2 = nt * sbox + j2;
-            const int ch0 = chan(8 * h);
-            if (c < rows && s2 < S && ch0 < M) {
-              __nv_bfloat162 b2[4];
-              for (int i = 0; i < 4; ++i)
-                b2[i] = __floats2bfloat162_rn(obuf[c * OS + 8 * h + 2 * i], obuf[c * OS + 8 * h + 2 * i + 1]);
-              const int ox2 = e.out_stuff ? 2 * p2 : p2;
-              __nv_bfloat16 *dst = op->out_base + (ch0 >> 6) * op->out_plane +
-                                   ((int64_t)s2 * op->out_T + ox2) * op->out_row + (ch0 & 63);
-              *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>(b2);
-              if (e.out_stuff) *reinterpret_cast<uint4 *>(dst + op->out_row) = make_uint4(0, 0, 0, 0);
-            }
+          if (e.out) {
+            const __nv_bfloat162 b0 = __floats2bfloat162_rn(y[0], y[1]), b1 = __floats2bfloat162_rn(y[2], y[3]);
+            const int ox2 = e.out_stuff ? 2 * tq : tq;
+            __nv_bfloat16 *dst = op->out_base + (ch0 >> 6) * op->out_plane +
+                                 ((int64_t)s * op->out_T + ox2) * op->out_row + (ch0 & 63);
+            *reinterpret_cast<uint2 *>(dst) =
+                make_uint2(*reinterpret_cast<const uint32_t *>(&b0), *reinterpret_cast<const uint32_t *>(&b1));
+            if (e.out_stuff) *reinterpret_cast<uint2 *>(dst + op->out_row) = make_uint2(0, 0);
           }
-        }
-        if (e.out_f32) {
-          const int cpc = RPC >> 2;
-          if (et < cpc * bn) {
-            const int c = et / cpc, h = et - c * cpc;
-            const int j2 = c >> lwo, p2 = c & (Wo - 1), s2 = nt * sbox + j2;
-            const int ch0 = chan(4 * h);
-            if (c < rows && s2 < S && ch0 < M) {
-              const float *o = obuf + c * OS + 4 * h;
-              *reinterpret_cast<float4 *>(e.out_f32 + ((int64_t)s2 * Wo + p2) * M + ch0) =
-                  make_float4(o[0], o[1], o[2], o[3]);
-            }
-          }
+          if (e.out_f32)
+            *reinterpret_cast<float4 *>(e.out_f32 + ((int64_t)s * Wo + tq) * M + ch0) = make_float4(y[0], y[1], y[2], y[3]);
         }
         fence_proxy_async();
         esync();
