@@ -284,8 +284,13 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
     }
   } else if (warp == CK_MMA_WARP) {
     // ------------------------------------------------ MMA issuer
-    int ia = 0, gi = 0;
-    uint32_t par = 0;
+    // One warp issues every UMMA of the CTA; with N = 32..64 its instruction
+    // stream, not the tensor pipe, bounds a k-block, so the loop is kept lean:
+    // ring slots advance incrementally, descriptors come from precomputed
+    // shared-memory addresses, one elected lane issues a whole K = 64 block.
+    int ia = 0, gi = 0, sa = 0;
+    uint32_t par = 0, pa_bits = 0;
+    const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB);
     for (int t = t0; t < t1; ++t) {
       const int4 tk = P.tasks[t];
       if ((tk.x & 0xff) != K_GEMM) continue;
@@ -297,44 +302,39 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
       const uint32_t idesc = umma_idesc(bn);
       const uint32_t dt = tmem + buf * 2 * CK_BN;
       const int kb0 = rank * kps, kb1 = min(kbt, kb0 + kps);
-      int j = 0;
+      int sb = 0;
       if (op->nmt == 2) {                           // two accumulators: m-tile u at column u * CK_BN
-        for (int kb = kb0; kb < kb1; ++kb, ++ia, ++j) {
-          const int sa = ia % CK_NA, sb = j % nbst;
-          mbar_wait(&fullA[sa], (ia / CK_NA) & 1);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&fullA[sa], (pa_bits >> sa) & 1);
           mbar_wait(&fullB[sb], (par >> sb) & 1);
           par ^= 1u << sb;
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t a0 = smem_u32(sA + sa * CK_A_STAGE), b0 = smem_u32(sB + sb * bstage);
-          umma_kblock2_warp(dt, dt + CK_BN, umma_desc(a0), umma_desc(b0), idesc, kb > kb0 ? 1u : 0u);
+          pa_bits ^= 1u << sa;
+          umma_kblock2_warp(dt, dt + CK_BN, umma_desc(sA0 + sa * CK_A_STAGE), umma_desc(sB0 + sb * bstage), idesc,
+                            kb > kb0 ? 1u : 0u);
           umma_commit_warp(&emptyB[sb]);
           umma_commit_warp(&emptyA[sa]);
-          __syncwarp();
+          sb = sb + 1 == nbst ? 0 : sb + 1;
+          sa = (sa + 1) & (CK_NA - 1);
+          ++ia;
         }
-      } else
-      for (int kb = kb0; kb < kb1; kb += 2, ++ia) {
-        const int sa = ia % CK_NA;
-        long long *kt = (P.trace && ia < 1024) ? P.trace + 16 * (int64_t)P.n_tasks +
-                                                     ((int64_t)blockIdx.x * 1024 + ia) * 3
-                                               : nullptr;
-        if (kt && lane == 0) kt[0] = ck_time();
-        mbar_wait(&fullA[sa], (ia / CK_NA) & 1);
-        if (kt && lane == 0) kt[1] = ck_time();
-        const int nk = min(2, kb1 - kb);
-        for (int i = 0; i < nk; ++i, ++j) {
-          const int sb = j % nbst;
-          mbar_wait(&fullB[sb], (par >> sb) & 1);
-          if (kt && lane == 0 && i == nk - 1) kt[2] = ck_time();
-          par ^= 1u << sb;
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t a0 = smem_u32(sA + sa * CK_A_STAGE + i * CK_A_BYTES);
-          const uint32_t b0 = smem_u32(sB + sb * bstage);
-          umma_kblock_warp(dt, umma_desc(a0), umma_desc(b0), idesc, (kb > kb0 || i > 0) ? 1u : 0u);
-          umma_commit_warp(&emptyB[sb]);
-          __syncwarp();
+      } else {
+        for (int kb = kb0; kb < kb1; kb += 2) {
+          mbar_wait(&fullA[sa], (pa_bits >> sa) & 1);
+          pa_bits ^= 1u << sa;
+          const uint32_t a0 = sA0 + sa * CK_A_STAGE;
+          const int nk = min(2, kb1 - kb);
+          for (int i = 0; i < nk; ++i) {
+            mbar_wait(&fullB[sb], (par >> sb) & 1);
+            par ^= 1u << sb;
+            umma_kblock_warp(dt, umma_desc(a0 + i * CK_A_BYTES), umma_desc(sB0 + sb * bstage), idesc,
+                             (kb > kb0 || i > 0) ? 1u : 0u);
+            umma_commit_warp(&emptyB[sb]);
+            sb = sb + 1 == nbst ? 0 : sb + 1;
+          }
+          umma_commit_warp(&emptyA[sa]);
+          sa = (sa + 1) & (CK_NA - 1);
+          ++ia;
         }
-        umma_commit_warp(&emptyA[sa]);
-        __syncwarp();
       }
       if (kb1 > kb0) umma_commit_warp(&tfull[buf]);
       else if (lane == 0) mbar_arrive(&tfull[buf]);      // empty K share: the drain pushes zeros
