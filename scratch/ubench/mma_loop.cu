@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(128, 1) bench(int nkb, int bn, int mode, long 
       for (int i = 0; *stop == 0; ++i) {
         const int st = i & 3;
         if (i >= 4) mbar_wait(&bars[16 + st], ((i >> 2) - 1) & 1);
-        tma_load_2d_warp(sA + (6 + st) * 16384, &tm, &bars[16 + st], 16384, 0, (i * 128) % (1 << 16));
+        tma_load_2d_warp(sA + (6 + st) * 16384, &tm, &bars[16 + st], 16384, 0, (int)(((long long)(blockIdx.x * 5000 + i) * 128) % (1ll << 23)));
       }
     }
     if (mode == 6 && (threadIdx.x & 31) == 0) {
@@ -81,18 +81,18 @@ __global__ void __launch_bounds__(128, 1) bench(int nkb, int bn, int mode, long 
 int main() {
   long long *d; cudaMalloc(&d, 8);
   int *flag; cudaMalloc(&flag, 64); cudaMemset(flag, 0, 64);
-  void *w; cudaMalloc(&w, 1 << 24); cudaMemset(w, 0, 1 << 24);
+  void *w; cudaMalloc(&w, 1ull << 30); cudaMemset(w, 0, 1ull << 30);
   CUtensorMap tm;
   { EncodeTiledFn enc = encode_fn();
-    cuuint64_t dims[2] = {64, 1 << 17}; cuuint64_t str[1] = {128}; cuuint32_t box[2] = {64, 128}; cuuint32_t es[2] = {1, 1};
+    cuuint64_t dims[2] = {64, 1ull << 23}; cuuint64_t str[1] = {128}; cuuint32_t box[2] = {64, 128}; cuuint32_t es[2] = {1, 1};
     enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE); }
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 232000);
-  for (int bn : {32}) for (int mode : {3, 14, 3, 14}) for (int nkb : {2000}) {
+  for (int bn : {32}) for (int grid : {1, 112}) for (int mode : {3, 5, 13}) for (int nkb : {2000}) {
     cudaMemset(flag, 0, 64);
-    bench<<<1, 128, 232000>>>(nkb, bn, mode, d, tm, flag);
+    bench<<<grid, 128, 232000>>>(nkb, bn, mode, d, tm, flag);
     long long h = 0; cudaError_t e = cudaDeviceSynchronize(); cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-    printf("bn=%3d mode=%d nkb=%3d: %lld cycles, %.1f cyc/kb %s\n", bn, mode, nkb, h, (double)h / nkb, e ? cudaGetErrorString(e) : "");
+    printf("grid %3d bn=%3d mode=%d nkb=%3d: %lld cycles, %.1f cyc/kb %s\n", grid, bn, mode, nkb, h, (double)h / nkb, e ? cudaGetErrorString(e) : "");
   }
   return 0;
 }
