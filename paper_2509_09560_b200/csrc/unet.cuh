@@ -13,6 +13,7 @@ struct UnetCtrl {             // per-frame control, uploaded by value
   const float *noise_lanes;
   const int64_t *fetched;
   int S, lanes_per_agent;
+  int iters;                  // denoise iterations this frame (run inside one launch by the cluster kernel)
 };
 
 struct UnetDev {              // device-resident per-sample state
@@ -26,9 +27,9 @@ struct UnetDev {              // device-resident per-sample state
 // its agent fetched in-kernel; load x_t into the conv input (channels padded).
 template <typename T>
 __device__ void prep_body(UnetDev *dev, int s, int tid, int nthr, const auras_sched &sch, int horizon, int adim,
-                          T *xin, int x_pitch, int64_t ring_slot_stride, int64_t ring_agent_stride) {
+                          T *xin, int x_pitch, int64_t ring_slot_stride, int64_t ring_agent_stride, int r_it = -1) {
   const UnetCtrl &c = dev->ctrl;
-  const int r = dev->r;
+  const int r = r_it >= 0 ? r_it : dev->r;
   const int agent = c.agents[s], lane = c.lanes[s];
   int i = c.start[s] + r;
   i = i < sch.n_steps ? i : sch.n_steps - 1;
@@ -51,9 +52,9 @@ __device__ void prep_body(UnetDev *dev, int s, int tid, int nthr, const auras_sc
 template <typename T, typename Sync>
 __device__ void final_body(UnetDev *dev, int s, int tid, int nthr, const auras_sched &sch, int horizon, int adim,
                            const T *y, int y_pitch, int cin, const float *wf, const float *bf, float *eps,
-                           Sync sync) {
+                           Sync sync, int r_it = -1) {
   const UnetCtrl &c = dev->ctrl;
-  const int r = dev->r;
+  const int r = r_it >= 0 ? r_it : dev->r;
   const int lane_id = tid & 31, wid = tid >> 5, nw = nthr >> 5;
   for (int o = wid; o < horizon * adim; o += nw) {
     const int t = o / adim, a = o - t * adim;

@@ -118,9 +118,11 @@ __device__ __forceinline__ void ck_spin(const int *ctr, int target) {
   }
 }
 
-__device__ __forceinline__ void ck_wait_dep(const ClParams &P, const int *prep_done, int d, int tgt) {
-  if (d == -2) ck_spin(prep_done, P.S);
-  else if (d >= 0) ck_spin(&P.ctr[d], tgt);
+// Counters accumulate over the frame's iterations: iteration `it` needs
+// (it + 1) x the per-iteration count.
+__device__ __forceinline__ void ck_wait_dep(const ClParams &P, const int *prep_done, int d, int tgt, int it) {
+  if (d == -2) ck_spin(prep_done, P.S * (it + 1));
+  else if (d >= 0) ck_spin(&P.ctr[d], tgt * (it + 1));
 }
 
 // Equal-count merge of k (mean, M2) pairs of n0 values each (fixed order).
@@ -189,6 +191,10 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
   cluster_sync_all();                       // peers' barriers initialised before any remote arrive
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // the frame's denoise iterations all run in this launch (control word set per frame)
+  const int iters = max(1, P.dev->ctrl.iters), r0 = P.dev->r;
+  if (P.trace && threadIdx.x == 0)
+    P.trace[16 * (int64_t)P.n_tasks + ((int64_t)blockIdx.x * 1024 + 1023) * 3] = ck_time();
 
   if (warp < CK_NWW) {
     // ------------------------------------------------ weights: this CTA's K share of every task
@@ -216,6 +222,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
       const int f = next_gemm(t0 - 1);
       if (f >= 0) l2_prefetch(f);
     }
+    for (int it = 0; it < iters; ++it)
     for (int t = t0; t < t1; ++t) {
       const int4 tk = P.tasks[t];
       if ((tk.x & 0xff) != K_GEMM) continue;
@@ -253,6 +260,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
     // k-block j of a task goes to ring stage j % nbst, issued by warp 5 + stage % 3
     const int bw = warp - CK_BW0;
     uint32_t par = 0;
+    for (int it = 0; it < iters; ++it)
     for (int t = t0; t < t1; ++t) {
       const int4 tk = P.tasks[t];
       if ((tk.x & 0xff) != K_GEMM) continue;
@@ -263,7 +271,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
       const uint32_t bbytes = op->rows * 128;
       const CUtensorMap *tmB = &op->tmB;
       if (lane == 0) {
-        for (int d = 0; d < 3; ++d) ck_wait_dep(P, prep_done, op->gemm_dep[d], op->gemm_tgt[d]);
+        for (int d = 0; d < 3; ++d) ck_wait_dep(P, prep_done, op->gemm_dep[d], op->gemm_tgt[d], it);
         fence_proxy_async();
         if (P.trace && rank == 0) P.trace[8 * t + 0] = ck_time();
       }
@@ -291,6 +299,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
     int ia = 0, gi = 0, sa = 0;
     uint32_t par = 0, pa_bits = 0;
     const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB);
+    for (int it = 0; it < iters; ++it)
     for (int t = t0; t < t1; ++t) {
       const int4 tk = P.tasks[t];
       if ((tk.x & 0xff) != K_GEMM) continue;
@@ -347,6 +356,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
     const int ew = warp - CK_EW0;
     auto esync = [] __device__() { named_sync(1, CK_EPI); };
     int gi = 0, gn_i = 0;
+    for (int it = 0; it < iters; ++it)
     for (int t = t0; t < t1; ++t) {
       const int4 tk = P.tasks[t];
       const int type = tk.x & 0xff, opi = tk.x >> 8;
@@ -379,8 +389,8 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           mbar_expect_tx(&rbar[buf], (uint32_t)(CL * 16 * nmt * bn * 2));
           if (gn) mbar_expect_tx(&rbar[2 + (gn_i & 1)], (uint32_t)(CL * 2 * nmt * sbox * 8));
 #endif
-          if (film) ck_spin(prep_done, S);
-          for (int d = 0; d < 2; ++d) ck_wait_dep(P, prep_done, op->epi_dep[d], op->epi_tgt[d]);
+          if (film) ck_spin(prep_done, S * (it + 1));
+          for (int d = 0; d < 2; ++d) ck_wait_dep(P, prep_done, op->epi_dep[d], op->epi_tgt[d], it);
         }
         esync();
         // ---- element ownership.  Thread et belongs to (atom pa, sample pj) pair pi = et / L
@@ -625,27 +635,46 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         ++gi;
         gn_i += gn;
       } else if (type == K_PREP) {
-        if (tk.w != rank) continue;
+        if (tk.w != rank || it > 0) continue;            // later iterations: prepared by the final task
+        if (P.trace && et == 0) P.trace[8 * t + 0] = ck_time();
         prep_body<__nv_bfloat16>(P.dev, tk.y, et, CK_EPI, P.sched, P.horizon, P.adim, P.xin, P.x_pitch,
-                                 P.ring_slot_stride, P.ring_agent_stride);
+                                 P.ring_slot_stride, P.ring_agent_stride, r0);
         fence_proxy_async();
         esync();
         if (et == 0) {
           __threadfence();
           atomicAdd(prep_done, 1);
+          if (P.trace) P.trace[8 * t + 4] = ck_time();
         }
       } else if (type == K_FINAL) {
         if (tk.w != rank) continue;
-        if (et == 0) ck_spin(&done[P.n_ops - 1], P.ops[P.n_ops - 1].tiles * CL);
+        if (et == 0) ck_spin(&done[P.n_ops - 1], P.ops[P.n_ops - 1].tiles * CL * (it + 1));
+        if (P.trace && et == 0) P.trace[8 * t + 0] = ck_time();
         esync();
         final_body<__nv_bfloat16>(P.dev, tk.y, et, CK_EPI, P.sched, P.horizon, P.adim, P.y_final, P.y_pitch,
-                                  P.final_cin, P.wf, P.bf, eps, esync);
+                                  P.final_cin, P.wf, P.bf, eps, esync, r0 + it);
+        if (it + 1 < iters) {
+          // the sample's next iteration input, from the x this task just wrote (every op of
+          // this iteration has finished: nothing still reads the conv input buffer)
+          esync();
+          prep_body<__nv_bfloat16>(P.dev, tk.y, et, CK_EPI, P.sched, P.horizon, P.adim, P.xin, P.x_pitch,
+                                   P.ring_slot_stride, P.ring_agent_stride, r0 + it + 1);
+          fence_proxy_async();
+          esync();
+          if (et == 0) {
+            __threadfence();
+            atomicAdd(prep_done, 1);
+          }
+        }
+        if (P.trace && et == 0) P.trace[8 * t + 4] = ck_time();
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   cluster_sync_all();                       // no CTA leaves while peers may still touch its smem
+  if (P.trace && threadIdx.x == 0)
+    P.trace[16 * (int64_t)P.n_tasks + ((int64_t)blockIdx.x * 1024 + 1023) * 3 + 1] = ck_time();
   if (warp == CK_MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(4 * CK_BN));
 }
 

@@ -29,6 +29,8 @@ __global__ void unet_set_ctrl(UnetDev *dev, UnetCtrl c) {
 }
 
 __global__ void unet_advance(UnetDev *dev) { dev->r += 1; }
+// after a cluster-kernel launch that ran all of the frame's iterations
+__global__ void unet_advance_iters(UnetDev *dev) { dev->r += max(1, dev->ctrl.iters); }
 
 template <typename T>
 __global__ void unet_prep(UnetDev *dev, auras_sched sch, int horizon, int adim, T *xin, int x_pitch,
@@ -85,11 +87,20 @@ static int mega_kernel_launch(auras_unet_plan *p, int S, bool cluster, cudaStrea
 }
 
 // One denoise step through the persistent megakernel picked for S.
+// One step of the persistent kernels: the L2 split-K megakernel runs one denoise
+// iteration per launch; the cluster kernel runs every iteration of the frame
+// (UnetCtrl::iters) in one launch.
 static int unet_mega_step(auras_unet_plan *p, int S, cudaStream_t st) {
-  int rc = mega_kernel_launch(p, S, p->use_clus_for[S] == 1, st);
+  const bool cl = p->use_clus_for[S] == 1;
+  int rc = mega_kernel_launch(p, S, cl, st);
   if (rc) return rc;
-  unet_advance<<<1, 1, 0, st>>>(p->dev);
-  AURAS_LAUNCHED("unet_advance");
+  if (cl) {
+    unet_advance_iters<<<1, 1, 0, st>>>(p->dev);
+    AURAS_LAUNCHED("unet_advance_iters");
+  } else {
+    unet_advance<<<1, 1, 0, st>>>(p->dev);
+    AURAS_LAUNCHED("unet_advance");
+  }
   return AURAS_OK;
 }
 
@@ -337,13 +348,16 @@ int auras_unet_generate(auras_unet_plan *p, int S, const int *lanes, const int *
   c.fetched = fetched;
   c.S = S;
   c.lanes_per_agent = lanes_per_agent;
+  c.iters = iters;
   int rc0 = unet_ensure_mega(p, S, st);
   if (rc0) return rc0;
+  // launches per frame: one for the cluster kernel (all iterations inside), else one per iteration
+  const int launches = (p->use_mega && p->use_clus_for[S] == 1) ? 1 : iters;
   auto step = p->use_mega ? unet_mega_step : unet_launch_step;
   unet_set_ctrl<<<1, 1, 0, st>>>(p->dev, c);
   AURAS_LAUNCHED("unet_set_ctrl");
   if (!use_graph) {
-    for (int r = 0; r < iters; ++r) {
+    for (int r = 0; r < launches; ++r) {
       int rc = step(p, S, st);
       if (rc) return rc;
     }
@@ -364,7 +378,7 @@ int auras_unet_generate(auras_unet_plan *p, int S, const int *lanes, const int *
     AURAS_CUDA(cudaGraphUpload(ge, st));
     it = p->graphs.emplace(S, ge).first;
   }
-  for (int r = 0; r < iters; ++r) AURAS_CUDA(cudaGraphLaunch(it->second, st));
+  for (int r = 0; r < launches; ++r) AURAS_CUDA(cudaGraphLaunch(it->second, st));
   return AURAS_OK;
 }
 
