@@ -373,7 +373,13 @@ def main():
     enc_ops = LAST_EVENTS["encoder_launches"]
     per_iter = LAST_EVENTS["launches_per_iter"]
     iters_per_frame = max(1, -(-cfg.num_inference_steps // args.depth))
-    per_frame = enc_ops + 3 + 1 + 1 + iters_per_frame * per_iter + 1
+    # the cluster kernel runs all of a frame's iterations in one launch (+1 advance kernel)
+    dk_names = LAST_EVENTS.get("denoise_kernel") or {}
+    if "cluster" in (dk_names.get(S_med) or ""):
+        gen_launches = 2
+    else:
+        gen_launches = iters_per_frame * per_iter
+    per_frame = enc_ops + 3 + 1 + 1 + gen_launches + 1
     launches = per_frame * K
 
     out = {"metric": METRIC, "value": value, "unit": "actions/s", "n_gpus": dist.world,
