@@ -174,6 +174,7 @@ struct ClConfig {
   int *ctr = nullptr;
   float2 *gstats = nullptr;
   int ctr_ints = 0, n_ops = 0, n_tasks = 0, nc = 0, S = 0;
+  int bn_var = 64;            // kernel variant: 64 or 128 columns per tile task (set before clus_build)
   ClParams params;
 };
 

@@ -31,6 +31,7 @@
 // earlier ops, except a GroupNorm pair, which is scheduled on two clusters in
 // the same round (see clus_build).
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -61,28 +62,34 @@ constexpr int CK_EW0 = 8;
 #define CK_WARP_BAR 0                     // 1: every epilogue warp arrives on every peer's cluster barrier
 #endif                 // epilogue warps 8..15 (8..11 also drain TMEM)
 constexpr int CK_EPI = 256;
-constexpr int CK_BN = 64;                 // max columns per tile task (TMEM: 2 x 64 columns)
 constexpr int CK_A_BYTES = 128 * 64 * 2;  // one 128 x 64 weight box
 constexpr int CK_A_STAGE = 2 * CK_A_BYTES;
-constexpr int CK_NA = 4;                  // weight stages (2 k-blocks each)
 constexpr int CK_BRING = 44 * 1024;       // activation ring (1 k-block per stage)
 constexpr int CK_NBMAX = 16;
-constexpr int CK_OS = 17;                 // staging row stride (floats)
 constexpr int CK_SMAX = 16;               // max samples per tile
 
-constexpr int OFF_B = CK_NA * CK_A_STAGE;
-constexpr int OFF_RECV = OFF_B + CK_BRING;
-constexpr int RECV_BYTES = CL * 32 * 40 * 2;      // one buffer (>= CL x rows x (bn + 8) halves); two alternate
-constexpr int OFF_STATS = OFF_RECV + 2 * RECV_BYTES;
-constexpr int OFF_RBUF = OFF_STATS + CL * 32 * 8;        // stats: CL x (atoms x samples <= 32) float2
-constexpr int OFF_OBUF = OFF_RBUF + CK_BN * CK_OS * 4;
-constexpr int OFF_MR = OFF_OBUF + CK_BN * CK_OS * 4;
-constexpr int OFF_BAR = OFF_MR + 4 * CK_SMAX * 8;
-constexpr int CK_NBARS = 2 * CK_NA + 2 * CK_NBMAX + 2 + 2 + 2 + 4;
-constexpr size_t CK_SMEM = 1024 + OFF_BAR + CK_NBARS * 8 + 16;
-static_assert(CK_SMEM <= 232448, "cluster kernel shared memory");
-static_assert(CL * 16 * (CK_BN + 8) * 2 <= RECV_BYTES, "receive buffer");
-static_assert(32 * 33 <= CK_BN * CK_OS && 512 <= CK_BN * CK_OS, "staging buffer");
+// Shared-memory layout of the two kernel variants: BN = 64 columns per tile
+// task (4 weight stages) for small batches, BN = 128 (3 weight stages, wider
+// receive buffers) for many samples per step, where a 64-column tile would
+// re-stream each layer's weights over 4-5 rounds of tasks.
+template <int BN>
+struct ClLay {
+#ifndef CK_NA128
+#define CK_NA128 3
+#endif
+  static constexpr int NA = BN == 64 ? 4 : CK_NA128;          // weight stages (2 k-blocks each)
+  static constexpr int OFF_B = NA * CK_A_STAGE;
+  static constexpr int OFF_RECV = OFF_B + CK_BRING;
+  // one receive buffer (two alternate): >= CL x rows x (bn + 8) halves for rows x bn <= 16 BN
+  static constexpr int RECV_BYTES = BN == 64 ? CL * 32 * 40 * 2 : CL * 32 * 72 * 2;
+  static constexpr int OFF_STATS = OFF_RECV + 2 * RECV_BYTES;
+  static constexpr int OFF_EPS = OFF_STATS + CL * 64 * 8;   // stats: CL x (atoms x samples <= 64) float2
+  static constexpr int OFF_BAR = OFF_EPS + 1024;            // final-task scratch (horizon x adim floats)
+  static constexpr int NBARS = 2 * NA + 2 * CK_NBMAX + 2 + 2 + 2 + 4;
+  static constexpr size_t SMEM = 1024 + OFF_BAR + NBARS * 8 + 16;
+  static_assert(SMEM <= 232448, "cluster kernel shared memory");
+  static_assert(CL * 16 * (BN + 8) * 2 <= RECV_BYTES, "receive buffer");
+};
 
 enum { K_GEMM = 0, K_PREP = 2, K_FINAL = 3 };
 
@@ -139,20 +146,28 @@ __device__ __forceinline__ float2 merge_equal(const float2 *st, int stride, int 
   return make_float2(m, q + n0 * d2);
 }
 
+template <int BN>
 __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_constant__ ClParams P) {
+  using Lay = ClLay<BN>;
+  constexpr int CK_BN = BN;
+  constexpr int CK_NA = Lay::NA;
+  constexpr int RECV_BYTES = Lay::RECV_BYTES;
+  constexpr int VMAX = BN == 64 ? 4 : 8;
+#ifdef CK_TMEM_ALL
+  constexpr int CK_TMEM_COLS = 512;
+#else
+  constexpr int CK_TMEM_COLS = 4 * BN;
+#endif   // values per epilogue thread (8: 128-column tiles)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1 KB alignment by an offset from the __shared__ array itself, so every
   // derived pointer stays in the shared window (LDS/STS, not generic LD/ST)
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sA = smem;
-  uint8_t *sB = smem + OFF_B;
-  __half *recv = reinterpret_cast<__half *>(smem + OFF_RECV);
-  float2 *stats = reinterpret_cast<float2 *>(smem + OFF_STATS);
-  float *rbuf = reinterpret_cast<float *>(smem + OFF_RBUF);
-  float *obuf = reinterpret_cast<float *>(smem + OFF_OBUF);
-  float2 *mr = reinterpret_cast<float2 *>(smem + OFF_MR);
-  float *eps = obuf;                       // FINAL tasks run after every GEMM epilogue
-  uint64_t *fullA = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
+  uint8_t *sB = smem + Lay::OFF_B;
+  __half *recv = reinterpret_cast<__half *>(smem + Lay::OFF_RECV);
+  float2 *stats = reinterpret_cast<float2 *>(smem + Lay::OFF_STATS);
+  float *eps = reinterpret_cast<float *>(smem + Lay::OFF_EPS);
+  uint64_t *fullA = reinterpret_cast<uint64_t *>(smem + Lay::OFF_BAR);
   uint64_t *emptyA = fullA + CK_NA;
   uint64_t *fullB = emptyA + CK_NA;
   uint64_t *emptyB = fullB + CK_NBMAX;
@@ -183,7 +198,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
   }
   if (warp == CK_MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(4 * CK_BN));
+                 "r"(CK_TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -239,8 +254,8 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
       const int row0 = tk.y * nmt * kbt * 128;
       if (nmt == 1) {                               // stage = 2 k-blocks of one m-tile
         for (int kb = kb0; kb < kb1; kb += 2, ++ia) {
-          if (ia % CK_NWW != warp) continue;
           const int st = ia % CK_NA;
+          if (st % CK_NWW != warp) continue;         // a stage always has the same issuing warp
           const bool two = kb + 1 < kb1;
           mbar_wait(&emptyA[st], ((ia / CK_NA) & 1) ^ 1);
           tma_load_2d_warp(sA + st * CK_A_STAGE, two ? &op->tmA : &op->tmA1, &fullA[st],
@@ -248,8 +263,8 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         }
       } else {                                      // stage = 1 k-block of both m-tiles
         for (int kb = kb0; kb < kb1; ++kb, ++ia) {
-          if (ia % CK_NWW != warp) continue;
           const int st = ia % CK_NA;
+          if (st % CK_NWW != warp) continue;         // a stage always has the same issuing warp
           mbar_wait(&emptyA[st], ((ia / CK_NA) & 1) ^ 1);
           tma_load_2d_warp(sA + st * CK_A_STAGE, &op->tmA, &fullA[st], CK_A_STAGE, 0, row0 + kb * 256);
         }
@@ -323,7 +338,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           umma_commit_warp(&emptyB[sb]);
           umma_commit_warp(&emptyA[sa]);
           sb = sb + 1 == nbst ? 0 : sb + 1;
-          sa = (sa + 1) & (CK_NA - 1);
+          sa = sa + 1 == CK_NA ? 0 : sa + 1;
           ++ia;
         }
       } else {
@@ -341,7 +356,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
             sb = sb + 1 == nbst ? 0 : sb + 1;
           }
           umma_commit_warp(&emptyA[sa]);
-          sa = (sa + 1) & (CK_NA - 1);
+          sa = sa + 1 == CK_NA ? 0 : sa + 1;
           ++ia;
         }
       }
@@ -394,30 +409,33 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         }
         esync();
         // ---- element ownership.  Thread et belongs to (atom pa, sample pj) pair pi = et / L
-        //      (L lanes per pair, L | 32, L >= 2 Wo); lane li < 2 Wo owns channels 4 hh .. 4 hh + 3
-        //      (hh = li / Wo) of the atom's 8 rows at time tq = li % Wo, i.e. tile column
+        //      (L lanes per pair, L | 32, L >= Wo).  With L >= 2 Wo (NH = 1) lane li < 2 Wo owns
+        //      channels 4 hh .. 4 hh + 3 (hh = li / Wo) of the atom's 8 rows; with L = Wo (NH = 2,
+        //      128-column tiles) lane li owns all 8 -- at time tq = li % Wo, tile column
         //      col = pj * Wo + tq.  The slice sums, the atom statistics (warp shuffles), the
         //      group merge and the store all run on these registers: no staging, no CTA barrier.
         const int lL = min(5, 8 - lsb - nmt), L = 1 << lL;         // L = min(32, 256 / (A * sbox))
+        const int NH = (VMAX == 4 || L >= 2 * Wo) ? 1 : 2;
         const int pi = et >> lL, li = et & (L - 1);
         const int pa = pi >> lsb, pj = pi & (sbox - 1);
         const bool in_pair = pi < A * sbox;
-        const int hh = li >> lwo, tq = li & (Wo - 1);
+        const int hh = NH == 1 ? li >> lwo : 0, tq = li & (Wo - 1);
         const int col = pj * Wo + tq;
         const int s = nt * sbox + pj;
         const int row0 = 8 * pa + 4 * hh;                  // first owned row (0..RPC-1)
-        const int ch0 = chan(row0);                        // its channel (4 consecutive channels)
-        const bool mine = in_pair && li < 2 * Wo && col < rows && s < S && ch0 < M;
-        float bias[4], gam[4], bet[4], sc[4], bi[4], v[4], r[4];
+        const int ch0 = chan(row0);                        // its channel (4 or 8 consecutive channels)
+        const bool mine = in_pair && li < (2 * Wo) / NH && col < rows && s < S && ch0 < M;
+        float bias[VMAX], gam[VMAX], bet[VMAX], sc[VMAX], bi[VMAX], v[VMAX], r[VMAX];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < VMAX; ++k) {
           bias[k] = 0.f; gam[k] = 1.f; bet[k] = 0.f; sc[k] = 1.f; bi[k] = 0.f; r[k] = 0.f;
         }
         if (mine) {
           const float *fa = film ? e.film_a + (int64_t)e.film_a_row[s] * e.film_a_stride + e.film_off : nullptr;
           const float *fb = (film && e.film_b) ? e.film_b + e.film_b_off[s] + e.film_off : nullptr;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
+          for (int k = 0; k < VMAX; ++k) {
+            if (k >= 4 * NH) break;
             const int ch = ch0 + k;
             if (e.bias) bias[k] = e.bias[ch];
             if (gn) { gam[k] = e.gn_gamma[ch]; bet[k] = e.gn_beta[ch]; }
@@ -426,15 +444,20 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
               bi[k] = fa[M + ch] + (fb ? fb[M + ch] : 0.f);
             }
           }
-          if (e.res) {                                   // 4 bf16 channels of the residual
-            const uint2 u = __ldcg(reinterpret_cast<const uint2 *>(
-                op->res_base + (ch0 >> 6) * op->res_plane + ((int64_t)s * op->res_T + tq) * op->res_row + (ch0 & 63)));
-            const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.x));
-            const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.y));
-            r[0] = f0.x; r[1] = f0.y; r[2] = f1.x; r[3] = f1.y;
-          } else if (e.res_f32) {
-            const float4 f = __ldcg(reinterpret_cast<const float4 *>(e.res_f32 + ((int64_t)s * Wo + tq) * M + ch0));
-            r[0] = f.x; r[1] = f.y; r[2] = f.z; r[3] = f.w;
+#pragma unroll
+          for (int h = 0; h < VMAX / 4; ++h) {
+            if (h >= NH) break;
+            const int c4 = ch0 + 4 * h;
+            if (e.res) {                                 // 4 bf16 channels of the residual
+              const uint2 u = __ldcg(reinterpret_cast<const uint2 *>(
+                  op->res_base + (c4 >> 6) * op->res_plane + ((int64_t)s * op->res_T + tq) * op->res_row + (c4 & 63)));
+              const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.x));
+              const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.y));
+              r[4 * h] = f0.x; r[4 * h + 1] = f0.y; r[4 * h + 2] = f1.x; r[4 * h + 3] = f1.y;
+            } else if (e.res_f32) {
+              const float4 f = __ldcg(reinterpret_cast<const float4 *>(e.res_f32 + ((int64_t)s * Wo + tq) * M + c4));
+              r[4 * h] = f.x; r[4 * h + 1] = f.y; r[4 * h + 2] = f.z; r[4 * h + 3] = f.w;
+            }
           }
         }
         // ---- drain TMEM and push row slices to their owners (reduce-scatter over DSMEM)
@@ -486,9 +509,9 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 2] = ck_time();
         // ---- fixed-order sum of the 8 K slices + bias (fp32)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < VMAX; ++k) {
           float acc = bias[k];
-          if (mine) {
+          if (mine && k < 4 * NH) {
             const __half *rp = recvb + (row0 + k) * RSH + col;
 #pragma unroll
             for (int src = 0; src < CL; ++src) acc += __half2float(rp[src * RPC * RSH]);
@@ -503,20 +526,20 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           if (in_pair) {
             float sum = 0.f, sq = 0.f;
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              if (mine) { sum += v[k]; sq += v[k] * v[k]; }
+            for (int k = 0; k < VMAX; ++k)
+              if (mine && k < 4 * NH) { sum += v[k]; sq += v[k] * v[k]; }
             for (int o = 1; o < L; o <<= 1) {
               sum += __shfl_xor_sync(0xffffffffu, sum, o);
               sq += __shfl_xor_sync(0xffffffffu, sq, o);
             }
             const float mean = sum / n0;
             const float m2a = fmaxf(sq - sum * mean, 0.f);
-            if (li < CL) {                                // lane li -> CTA li
+            for (int dst = li; dst < CL; dst += L) {      // lane li -> CTAs li, li + L, ...
 #if CK_TXBAR
-              st_async_v2_f32(mapa_shared(smem_u32(stats + (rank * A + pa) * sbox + pj), li), mean, m2a,
-                              mapa_shared(smem_u32(&rbar[2 + (gn_i & 1)]), li));
+              st_async_v2_f32(mapa_shared(smem_u32(stats + (rank * A + pa) * sbox + pj), dst), mean, m2a,
+                              mapa_shared(smem_u32(&rbar[2 + (gn_i & 1)]), dst));
 #else
-              st_cluster_v2(mapa_shared(smem_u32(stats + (rank * A + pa) * sbox + pj), li), mean, m2a);
+              st_cluster_v2(mapa_shared(smem_u32(stats + (rank * A + pa) * sbox + pj), dst), mean, m2a);
 #endif
             }
             if (pair && li == (CL & (L - 1)))            // the partner tile reads its atoms from L2
@@ -557,28 +580,23 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
               const int w = q & 15, u = q >> 4;
               return base[((w >> 1) * A + 2 * u + (w & 1)) * sbox + pj];
             };
-            // butterfly merge of kq equal-count atoms, up to 4 per lane
+            // butterfly merge of kq equal-count atoms (lane li takes atoms li, li + L, ...)
             auto merge = [&](const float2 *base, bool global) {
-              float2 at[4];
-              bool hv[4];
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const int q = li + i * L;
-                hv[i] = q < kq;
-                at[i] = make_float2(0.f, 0.f);
-                if (hv[i]) at[i] = global ? __ldcg(base + (int64_t)(q0 + q) * CK_SMAX + pj) : atom(base, q0 + q);
-              }
+              auto get = [&](int q) {
+                return global ? __ldcg(base + (int64_t)(q0 + q) * CK_SMAX + pj) : atom(base, q0 + q);
+              };
               float m = 0.f;
-#pragma unroll
-              for (int i = 0; i < 4; ++i) m += hv[i] ? at[i].x : 0.f;
+              for (int q = li; q < kq; q += L) m += get(q).x;
               for (int o = 1; o < L; o <<= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
               m /= (float)kq;
-              float q = 0.f;
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-                if (hv[i]) { const float d = at[i].x - m; q += at[i].y + n0 * d * d; }
-              for (int o = 1; o < L; o <<= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-              return make_float2(m, q);
+              float qs = 0.f;
+              for (int q = li; q < kq; q += L) {
+                const float2 at = get(q);
+                const float d = at.x - m;
+                qs += at.y + n0 * d * d;
+              }
+              for (int o = 1; o < L; o <<= 1) qs += __shfl_xor_sync(0xffffffffu, qs, o);
+              return make_float2(m, qs);
             };
             gs = merge(stats, false);
             ncount = n0 * kq;
@@ -595,15 +613,15 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           rstd_g = rsqrtf(gs.y / ncount + 1e-5f);
         }
         if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 7] = ck_time();
-        // ---- normalise, activate, FiLM, residual (registers) and store 4 channels
+        // ---- normalise, activate, FiLM, residual (registers) and store 4 channels per half
         if (mine) {
           const float rba = e.res_before_act ? 1.f : 0.f;
           const float is_mish = e.act == AURAS_ACT_MISH ? 1.f : 0.f;
           const float is_relu = e.act == AURAS_ACT_RELU ? 1.f : 0.f;
           const float is_none = 1.f - is_mish - is_relu;
-          float y[4];
+          float y[VMAX];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
+          for (int k = 0; k < VMAX; ++k) {
             float x = gn ? (v[k] - mean_g) * rstd_g * gam[k] + bet[k] : v[k];
             x += rba * r[k];
             const float ex = __expf(fminf(x, 20.f));
@@ -614,17 +632,24 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
             x = x * sc[k] + bi[k];
             y[k] = x + (1.f - rba) * r[k];
           }
-          if (e.out) {
-            const __nv_bfloat162 b0 = __floats2bfloat162_rn(y[0], y[1]), b1 = __floats2bfloat162_rn(y[2], y[3]);
-            const int ox2 = e.out_stuff ? 2 * tq : tq;
-            __nv_bfloat16 *dst = op->out_base + (ch0 >> 6) * op->out_plane +
-                                 ((int64_t)s * op->out_T + ox2) * op->out_row + (ch0 & 63);
-            *reinterpret_cast<uint2 *>(dst) =
-                make_uint2(*reinterpret_cast<const uint32_t *>(&b0), *reinterpret_cast<const uint32_t *>(&b1));
-            if (e.out_stuff) *reinterpret_cast<uint2 *>(dst + op->out_row) = make_uint2(0, 0);
+#pragma unroll
+          for (int h = 0; h < VMAX / 4; ++h) {
+            if (h >= NH) break;
+            const int c4 = ch0 + 4 * h;
+            if (e.out) {
+              const __nv_bfloat162 b0 = __floats2bfloat162_rn(y[4 * h], y[4 * h + 1]);
+              const __nv_bfloat162 b1 = __floats2bfloat162_rn(y[4 * h + 2], y[4 * h + 3]);
+              const int ox2 = e.out_stuff ? 2 * tq : tq;
+              __nv_bfloat16 *dst = op->out_base + (c4 >> 6) * op->out_plane +
+                                   ((int64_t)s * op->out_T + ox2) * op->out_row + (c4 & 63);
+              *reinterpret_cast<uint2 *>(dst) =
+                  make_uint2(*reinterpret_cast<const uint32_t *>(&b0), *reinterpret_cast<const uint32_t *>(&b1));
+              if (e.out_stuff) *reinterpret_cast<uint2 *>(dst + op->out_row) = make_uint2(0, 0);
+            }
+            if (e.out_f32)
+              *reinterpret_cast<float4 *>(e.out_f32 + ((int64_t)s * Wo + tq) * M + c4) =
+                  make_float4(y[4 * h], y[4 * h + 1], y[4 * h + 2], y[4 * h + 3]);
           }
-          if (e.out_f32)
-            *reinterpret_cast<float4 *>(e.out_f32 + ((int64_t)s * Wo + tq) * M + ch0) = make_float4(y[0], y[1], y[2], y[3]);
         }
         fence_proxy_async();
         esync();
@@ -675,7 +700,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
   cluster_sync_all();                       // no CTA leaves while peers may still touch its smem
   if (P.trace && threadIdx.x == 0)
     P.trace[16 * (int64_t)P.n_tasks + ((int64_t)blockIdx.x * 1024 + 1023) * 3 + 1] = ck_time();
-  if (warp == CK_MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(4 * CK_BN));
+  if (warp == CK_MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CK_TMEM_COLS));
 }
 
 // ---------------------------------------------------------------- host side
@@ -688,10 +713,12 @@ static int pow2_floor(int x) {
 
 static bool same_buf(const void *a, const void *b) { return a != nullptr && a == b; }
 
-static int cluster_capacity() {
+template <int BN>
+static int cluster_capacity_t() {
   static int cached = -1;
   if (cached >= 0) return cached;
-  if (cudaFuncSetAttribute(unet_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CK_SMEM) != cudaSuccess) {
+  if (cudaFuncSetAttribute(unet_cluster<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ClLay<BN>::SMEM) !=
+      cudaSuccess) {
     cudaGetLastError();
     return cached = 0;
   }
@@ -699,7 +726,7 @@ static int cluster_capacity() {
   memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3(CL * 16);
   cfg.blockDim = dim3(CK_THREADS);
-  cfg.dynamicSmemBytes = CK_SMEM;
+  cfg.dynamicSmemBytes = ClLay<BN>::SMEM;
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeClusterDimension;
   attr.val.clusterDim.x = CL;
@@ -708,12 +735,14 @@ static int cluster_capacity() {
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, unet_cluster, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, unet_cluster<BN>, &cfg) != cudaSuccess) {
     cudaGetLastError();
     n = 0;
   }
   return cached = n;
 }
+
+static int cluster_capacity(int bn_var) { return bn_var == 128 ? cluster_capacity_t<128>() : cluster_capacity_t<64>(); }
 
 static BlockedBuf *find_blocked(ClConfig &cc, const void *orig) {
   for (auto &b : cc.blocked)
@@ -742,14 +771,16 @@ int clus_build(ClConfig &cc, const std::vector<auras_conv_op> &ops, int S, const
                const ClParams &base, const float *film_tau, int film_width, const float *ring_film,
                TiledCache &cache) {
   const int n = (int)ops.size();
-  int nc = std::min(cluster_capacity(), 16);
+  const int bn_var = cc.bn_var == 128 ? 128 : 64;
+  cc.bn_var = bn_var;
+  int nc = std::min(cluster_capacity(bn_var), 16);
   if (const char *e = getenv("AURAS_CLUSTERS")) nc = std::min(nc, atoi(e));
   nc &= ~1;                                   // GroupNorm pairs need an even cluster count
   if (nc < 2) { set_error("cluster kernel: only %d co-resident 8-CTA clusters", nc); return AURAS_E_ARG; }
   // columns per tile task: narrower tiles mean less DSMEM traffic per CTA and
   // more clusters per layer, at the cost of re-streaming weights per n-tile
-  int bn_cap = 64;
-  if (const char *e = getenv("AURAS_CL_BN")) bn_cap = std::max(16, std::min(CK_BN, atoi(e)));
+  int bn_cap = bn_var;
+  if (const char *e = getenv("AURAS_CL_BN")) bn_cap = std::max(16, std::min(bn_var, atoi(e)));
   const char *de = getenv("AURAS_CL_DUAL");
   const bool dual = de ? atoi(de) != 0 : true;
   std::vector<ClOp> hops(n);
@@ -785,11 +816,21 @@ int clus_build(ClConfig &cc, const std::vector<auras_conv_op> &ops, int S, const
     // a GroupNorm group spans two tiles (its statistics then stay in-cluster)
     m.nmt = (dual && m.m_tiles % 2 == 0 && (m.m_tiles > nc || m.cg == 256)) ? 2 : 1;
     m.pair = m.gn && m.cg == 256 && m.nmt == 1;
-    const int cap = m.nmt == 2 ? std::min(bn_cap, 32) : bn_cap;
+    const int cap = m.nmt == 2 ? bn_cap / 2 : bn_cap;
     m.s_box = std::min(CK_SMAX, pow2_floor(std::max(1, std::min(S, cap / o.Wo))));
     m.rows = m.s_box * o.Wo;
     m.bn = std::max(16, m.rows);
-    if (m.nmt == 2 && (m.bn > 32 || 4 * m.s_box > 32)) { set_error("cluster kernel: op %d dual tile", i); return AURAS_E_ARG; }
+    if (m.nmt == 2 && (m.bn > bn_var / 2 || 4 * m.s_box > 64)) {
+      set_error("cluster kernel: op %d dual tile", i);
+      return AURAS_E_ARG;
+    }
+    {
+      const int lLh = std::min(5, 8 - (int)std::log2((double)m.s_box) - m.nmt);
+      if ((1 << lLh) < o.Wo || (bn_var == 64 && (1 << lLh) < 2 * o.Wo)) {
+        set_error("cluster kernel: op %d epilogue lanes", i);
+        return AURAS_E_ARG;
+      }
+    }
     m.rsh = m.bn + 8;
     m.kb_total = o.Kp / 64;
     m.kps = (m.kb_total + CL - 1) / CL;
@@ -950,7 +991,7 @@ int clus_launch(const ClConfig &cc, cudaStream_t st) {
   memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3(CL * cc.nc);
   cfg.blockDim = dim3(CK_THREADS);
-  cfg.dynamicSmemBytes = CK_SMEM;
+  cfg.dynamicSmemBytes = cc.bn_var == 128 ? ClLay<128>::SMEM : ClLay<64>::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeClusterDimension;
@@ -959,7 +1000,8 @@ int clus_launch(const ClConfig &cc, cudaStream_t st) {
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
-  AURAS_CUDA(cudaLaunchKernelEx(&cfg, unet_cluster, cc.params));
+  if (cc.bn_var == 128) AURAS_CUDA(cudaLaunchKernelEx(&cfg, unet_cluster<128>, cc.params));
+  else AURAS_CUDA(cudaLaunchKernelEx(&cfg, unet_cluster<64>, cc.params));
   return AURAS_OK;
 }
 

@@ -369,8 +369,10 @@ int make_tiled_weight_map(CUtensorMap *tm, const void *wt, int rows_total, int b
 }
 
 int tiled_weights(TiledCache &cache, const auras_conv_op &o, void **out, int nmt) {
+  // the pair-interleaved copy of the same weights is a different entry (odd key)
+  const void *key = nmt == 2 ? static_cast<const void *>(static_cast<const char *>(o.w) + 1) : o.w;
   for (auto &kv : cache)
-    if (kv.first == o.w) { *out = kv.second; return AURAS_OK; }
+    if (kv.first == key) { *out = kv.second; return AURAS_OK; }
   const int m_tiles = (o.M + 127) / 128;
   const size_t bytes = (size_t)m_tiles * o.Kp * 128 * 2;
   void *d = nullptr;
@@ -379,7 +381,7 @@ int tiled_weights(TiledCache &cache, const auras_conv_op &o, void **out, int nmt
                                      o.Kp, m_tiles, nmt);
   AURAS_LAUNCHED("tile_weights_kernel");
   AURAS_CUDA(cudaDeviceSynchronize());
-  cache.emplace_back(o.w, d);
+  cache.emplace_back(key, d);
   *out = d;
   return AURAS_OK;
 }

@@ -17,6 +17,8 @@
 
 #include "common.cuh"
 #include "conv.cuh"
+#include <functional>
+
 #include "unet.cuh"
 #include "mega.cuh"
 #include "cluster.cuh"
@@ -104,7 +106,7 @@ static int unet_mega_step(auras_unet_plan *p, int S, cudaStream_t st) {
   return AURAS_OK;
 }
 
-static int build_cluster_config(auras_unet_plan *p, int S, const MegaParams &base) {
+static int build_cluster_config(auras_unet_plan *p, int S, const MegaParams &base, int bn_var, ClConfig &out) {
   ClParams cb;
   memset(&cb, 0, sizeof(cb));
   cb.dev = base.dev;
@@ -121,19 +123,61 @@ static int build_cluster_config(auras_unet_plan *p, int S, const MegaParams &bas
   cb.wf = base.wf;
   cb.bf = base.bf;
   ClConfig cc;
+  cc.bn_var = bn_var;
   int rc = clus_build(cc, p->ops, S, p->x_in, cb, p->film_tau, p->film_width, p->ring_film, p->tiled_cl);
   if (rc) {
     clus_free(cc);
     return rc;
   }
-  p->clus.emplace(S, cc);
+  out = cc;
+  return AURAS_OK;
+}
+
+static float time_launches(const std::function<int()> &launch, cudaStream_t st, int reps = 3) {
+  cudaEvent_t e0, e1;
+  if (cudaEventCreate(&e0) || cudaEventCreate(&e1)) return 1e30f;
+  float best = 1e30f;
+  for (int r = 0; r <= reps; ++r) {
+    cudaEventRecord(e0, st);
+    if (launch()) { best = 1e30f; break; }
+    cudaEventRecord(e1, st);
+    if (cudaEventSynchronize(e1) != cudaSuccess) { best = 1e30f; break; }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r > 0) best = std::min(best, ms);                 // r = 0 warms up
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return best;
+}
+
+// The cluster kernel for batch S: the 64-column variant, and for S >= 16 also
+// the 128-column one, timed on a dry batch; the faster is kept (AURAS_CL_VARIANT
+// = 64 | 128 forces one).
+static int prepare_dry_batch(auras_unet_plan *p, int S, cudaStream_t st);
+static int choose_cluster_config(auras_unet_plan *p, int S, const MegaParams &base, cudaStream_t st) {
+  const char *fv = getenv("AURAS_CL_VARIANT");
+  const int forced = fv ? atoi(fv) : 0;
+  ClConfig c64, c128;
+  int rc64 = forced == 128 ? AURAS_E_ARG : build_cluster_config(p, S, base, 64, c64);
+  int rc128 = (forced == 64 || (S < 16 && forced != 128)) ? AURAS_E_ARG : build_cluster_config(p, S, base, 128, c128);
+  if (rc64 && rc128) return rc64 ? rc64 : rc128;
+  if (!rc64 && !rc128) {
+    int rc = prepare_dry_batch(p, S, st);
+    if (rc) { clus_free(c64); clus_free(c128); return rc; }
+    const float t64 = time_launches([&] { return clus_launch(c64, st); }, st);
+    const float t128 = time_launches([&] { return clus_launch(c128, st); }, st);
+    if (t128 < t64) { clus_free(c64); rc64 = AURAS_E_ARG; }
+    else { clus_free(c128); rc128 = AURAS_E_ARG; }
+  }
+  p->clus.emplace(S, rc64 ? c128 : c64);
   return AURAS_OK;
 }
 
 // Time both persistent kernels on a dry batch of S samples (scratch request
 // lanes; every buffer they write is either scratch or rewritten by the next
 // real step's prep) and keep the faster one for this S.
-static int autotune_mega(auras_unet_plan *p, int S, cudaStream_t st, int *pick) {
+static int prepare_dry_batch(auras_unet_plan *p, int S, cudaStream_t st) {
   if (!p->dry_x) {
     AURAS_CUDA(cudaMalloc(&p->dry_x, sizeof(float) * kMaxS * p->horizon * p->adim));
     AURAS_CUDA(cudaMemset(p->dry_x, 0, sizeof(float) * kMaxS * p->horizon * p->adim));
@@ -152,6 +196,12 @@ static int autotune_mega(auras_unet_plan *p, int S, cudaStream_t st, int *pick) 
   c.lanes_per_agent = S;
   unet_set_ctrl<<<1, 1, 0, st>>>(p->dev, c);
   AURAS_LAUNCHED("unet_set_ctrl");
+  return AURAS_OK;
+}
+
+static int autotune_mega(auras_unet_plan *p, int S, cudaStream_t st, int *pick) {
+  int rc0 = prepare_dry_batch(p, S, st);
+  if (rc0) return rc0;
   float best[2] = {1e30f, 1e30f};
   cudaEvent_t e0, e1;
   AURAS_CUDA(cudaEventCreate(&e0));
@@ -186,7 +236,7 @@ static int unet_ensure_mega(auras_unet_plan *p, int S, cudaStream_t st) {
   const char *force = getenv("AURAS_MEGA_KERNEL");
   bool want_cluster = p->use_cluster && !(force && !strcmp(force, "l2"));
   bool want_l2 = !(force && !strcmp(force, "cluster") && p->use_cluster);
-  if (want_cluster && build_cluster_config(p, S, base)) {
+  if (want_cluster && choose_cluster_config(p, S, base, st)) {
     if (force && !strcmp(force, "cluster")) return AURAS_E_ARG;
     want_cluster = false;                     // shapes the cluster kernel does not cover
     want_l2 = true;
