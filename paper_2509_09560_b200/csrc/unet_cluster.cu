@@ -946,6 +946,36 @@ int clus_build(ClConfig &cc, const std::vector<auras_conv_op> &ops, int S, const
     rot = (rot + q) % nc;
   }
   for (int s = 0; s < S; ++s) per[(rot + s) % nc].push_back(make_int4(K_FINAL, s, 0, (s / nc) % CL));
+  // The activation ring is re-cut per op (stage = bn x 128 B).  A task whose op
+  // does not depend on the cluster's previous task could load its activations
+  // while that task's UMMAs still read overlapping stages of the old cut, so a
+  // cut change is only allowed across a dependency (always true for the UNets
+  // built here; other shapes fall back to the L2 megakernel).
+  {
+    std::vector<std::vector<char>> dep(n, std::vector<char>(n, 0));   // dep[i][j]: op i waits (transitively) on op j
+    for (int i = 0; i < n; ++i) {
+      for (int d = 0; d < 3; ++d)
+        if (hops[i].gemm_dep[d] >= 0) dep[i][hops[i].gemm_dep[d]] = 1;
+      for (int d = 0; d < 2; ++d)
+        if (hops[i].epi_dep[d] >= 0) dep[i][hops[i].epi_dep[d]] = 1;
+      for (int j = 0; j < i; ++j)
+        if (dep[i][j])
+          for (int k = 0; k < j; ++k)
+            if (dep[j][k]) dep[i][k] = 1;
+    }
+    for (int c = 0; c < nc; ++c) {
+      int prev = -1;
+      for (const int4 &tk : per[c]) {
+        if ((tk.x & 0xff) != K_GEMM) continue;
+        const int cur = tk.x >> 8;
+        if (prev >= 0 && cur != prev && hops[cur].bstage != hops[prev].bstage && !(cur > prev && dep[cur][prev])) {
+          set_error("cluster kernel: ops %d -> %d change the activation ring cut without a dependency", prev, cur);
+          return AURAS_E_ARG;
+        }
+        prev = cur;
+      }
+    }
+  }
   std::vector<int4> flat;
   std::vector<int> begin(nc + 1, 0);
   for (int c = 0; c < nc; ++c) {
