@@ -136,3 +136,27 @@ def test_disaggregated_two_gpus():
     ref = oracle_run(pol, cfg, 8)
     assert [r.context_versions for r in res.requests] == [r.context_versions for r in ref.requests]
     assert rel_err(res.actions, ref.actions) <= TOL["fp32"]
+
+
+_ORC = {}
+
+
+@pytest.mark.parametrize("variant", ["64", "128"])
+def test_cluster_kernel_variants_match_oracle(variant, monkeypatch):
+    """Both cluster-kernel variants (64 / 128 columns per tile task; the per-S
+    autotune may pick either) forced on the pusht shape with 8 lock-stepped
+    agents at depth 2, so one denoise launch runs S = 16 samples over all of
+    the frame's iterations: agents 0 and 7 within the bf16 tolerance of their
+    oracle runs, same context versions."""
+    monkeypatch.setenv("AURAS_MEGA_KERNEL", "cluster")
+    monkeypatch.setenv("AURAS_CL_VARIANT", variant)
+    w = weights("pusht")
+    pol = D.make_diffusion_policy("pusht", dtype="bf16", weights=w, agents=8)
+    cfg = dict(pp_perception=1, pp_generation=2, fetch_offset=0)
+    res = run_pipelined(PipelineConfig(**cfg), pol, None, 3, agents=8)
+    for a in (0, 7):
+        if a not in _ORC:
+            _ORC[a] = oracle_run(pol, cfg, 3, agent=a)
+        ref = _ORC[a]
+        err = rel_err(res.agent_actions[a], ref.actions)
+        assert err <= TOL["bf16"], (variant, a, err)
