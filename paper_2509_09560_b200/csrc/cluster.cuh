@@ -86,41 +86,6 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity
       : "memory");
 }
 
-// Barrier among the epilogue warps of all CTAs of the cluster: every warp
-// releases its prior (local and remote) shared-memory writes at cluster scope
-// and arrives once on each CTA's barrier (expected count = 8 CTAs x 8 warps),
-// then waits for its own barrier's phase.
-__device__ __forceinline__ void cluster_barrier_warp(uint64_t *bar, uint32_t parity, int lane) {
-  asm volatile("fence.acq_rel.cluster;" ::: "memory");
-  __syncwarp();
-  if (lane < 8) {
-    const uint32_t r = mapa_shared(smem_u32(bar), lane);
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
-  }
-  mbar_wait_cluster(bar, parity);
-}
-
-// Cluster barrier among the epilogues of the 8 CTAs with one arriving warp per
-// CTA (expected count 8): the epilogue threads meet at a named barrier, the
-// leader warp releases at cluster scope with lanes 0..7 arriving on the 8 peers'
-// barriers in parallel, waits with acquire, and a second named barrier lets the
-// other warps go.  (A single thread arriving on 8 peers in turn measured ~3.5 us.)
-template <typename Sync>
-__device__ __forceinline__ void cluster_barrier_cta(uint64_t *bar, uint32_t parity, bool leader_warp, int lane,
-                                                    Sync sync) {
-  sync();
-  if (leader_warp) {
-    asm volatile("fence.acq_rel.cluster;" ::: "memory");
-    __syncwarp();
-    if (lane < 8) {
-      const uint32_t a = mapa_shared(smem_u32(bar), lane);
-      asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
-    }
-    mbar_wait_cluster(bar, parity);
-  }
-  sync();
-}
-
 __device__ __forceinline__ void tma_load_5d_warp(void *dst, const CUtensorMap *tm, uint64_t *bar, uint32_t bytes,
                                                  int c0, int c1, int c2, int c3, int c4) {
   asm volatile(

@@ -1,34 +1,39 @@
-// Cluster dataflow megakernel: one launch runs a whole denoise step of the
-// ConditionalUnet1D for all S in-flight samples, with
-// split-K reduction and GroupNorm statistics kept on chip.
+// Cluster dataflow megakernel: one launch runs every denoise iteration of a
+// frame of the ConditionalUnet1D for all S in-flight samples (SURVEY.md §2.4
+// K3-K5), with split-K reduction and GroupNorm statistics kept on chip.
 //
 // Why a second design (unet_mega.cu is the first): there, split-K partials go
 // through L2 and a separate epilogue unit reduces them, so every layer of the
 // 34-deep dependency chain pays drain -> HBM/L2 round trip -> epilogue ->
 // counter -> next layer, ~12-18 us per layer under a saturated weight stream.
-// Here a thread-block CLUSTER of 8 CTAs owns an output tile (128 channels x
-// up to 64 columns) of one conv; its 8 CTAs split K 8 ways, and
+// Here a thread-block CLUSTER of 8 CTAs owns an output tile (128 channels, or
+// 256 for the 2048-channel layers, x up to 64 / 128 columns) of one conv; its
+// 8 CTAs split K 8 ways, and
 //
-//   * each CTA's tcgen05 accumulator (TMEM) is pushed row-slice-wise into the
-//     owning CTA's shared memory over DSMEM (reduce-scatter: CTA r owns
-//     channels 16r..16r+15 of the tile);
+//   * each CTA's tcgen05 accumulator (TMEM) is pushed row-slice-wise as fp16
+//     into the owning CTA's shared memory with st.async, which signals the
+//     owner's transaction mbarrier (reduce-scatter: CTA r owns channels
+//     16r..16r+15 of each 128-channel tile; no cluster barrier);
 //   * the owner sums the 8 slices in a fixed order (deterministic), adds the
-//     bias, and computes GroupNorm statistics of 8-channel atoms; atom
-//     statistics (mean, M2) are exchanged over DSMEM and merged per group
-//     (Chan's formula, fixed order).  Groups of 256 channels span two tiles:
-//     the pair of clusters exchanges tile statistics through global memory;
+//     bias, and computes GroupNorm statistics of 8-channel atoms in registers
+//     (warp shuffles); atom statistics (mean, M2) go to every CTA of the
+//     cluster the same way and are merged per group (Chan's formula, fixed
+//     order).  Groups of 256 channels split over two clusters exchange tile
+//     statistics through global memory;
 //   * GroupNorm affine, Mish/ReLU, FiLM (per-sample rows gathered from the
 //     timestep table and the context ring slot the sample fetched), residual
-//     and the (optionally zero-stuffed) bf16 / fp32 store run in the same
-//     warps, then one release per CTA on the op's completion counter.
+//     and the (optionally zero-stuffed) bf16 / fp32 store run on the same
+//     registers, then one release per CTA on the op's completion counter.
 //
-// Warp roles per CTA (384 threads): warp 0 weight TMA producer (never waits on
-// data -- the HBM weight stream runs ahead across layers), warp 1 MMA issuer,
-// warp 2 activation (implicit im2col) TMA producer gated on the producing
-// ops' counters, warps 4-11 epilogue (4-7 also drain TMEM).  Each cluster
-// walks a static list of tile tasks in layer order; the grid is as many
-// clusters as fit co-resident.  Deadlock freedom: tasks only wait on strictly
-// earlier ops, except a GroupNorm pair, which is scheduled on two clusters in
+// Warp roles per CTA (512 threads): warps 0-3 weight TMA producers (never wait
+// on data -- the HBM weight stream runs ahead across layers and iterations),
+// warp 4 UMMA issuer, warps 5-7 activation (implicit im2col) TMA producers
+// gated on the producing ops' counters, warps 8-15 epilogue (8-11 also drain
+// TMEM).  Each cluster walks a static list of tile tasks in layer order, once
+// per iteration; counters accumulate over the iterations.  The grid is as
+// many clusters as fit co-resident.  Deadlock freedom: tasks only wait on
+// strictly earlier ops (or, across iterations, on the previous iteration's
+// final tasks), except a GroupNorm pair, which is scheduled on two clusters in
 // the same round (see clus_build).
 #include <algorithm>
 #include <cmath>
@@ -55,12 +60,7 @@ constexpr int CK_NWW = 4;                 // weight producer warps 0..3: warp w 
 constexpr int CK_MMA_WARP = 4;
 constexpr int CK_BW0 = 5, CK_NBW = 3;     // activation TMA warps 5..7: warp 5 + (stage % 3)
 constexpr int CK_EW0 = 8;
-#ifndef CK_TXBAR
-#define CK_TXBAR 1                        // DSMEM pushes signal the receiver's mbarrier (st.async complete_tx)
-#endif
-#ifndef CK_WARP_BAR
-#define CK_WARP_BAR 0                     // 1: every epilogue warp arrives on every peer's cluster barrier
-#endif                 // epilogue warps 8..15 (8..11 also drain TMEM)
+                                          // epilogue warps 8..15 (8..11 also drain TMEM)
 constexpr int CK_EPI = 256;
 constexpr int CK_A_BYTES = 128 * 64 * 2;  // one 128 x 64 weight box
 constexpr int CK_A_STAGE = 2 * CK_A_BYTES;
@@ -85,7 +85,7 @@ struct ClLay {
   static constexpr int OFF_STATS = OFF_RECV + 2 * RECV_BYTES;
   static constexpr int OFF_EPS = OFF_STATS + CL * 64 * 8;   // stats: CL x (atoms x samples <= 64) float2
   static constexpr int OFF_BAR = OFF_EPS + 1024;            // final-task scratch (horizon x adim floats)
-  static constexpr int NBARS = 2 * NA + 2 * CK_NBMAX + 2 + 2 + 2 + 4;
+  static constexpr int NBARS = 2 * NA + 2 * CK_NBMAX + 2 + 2 + 4;
   static constexpr size_t SMEM = 1024 + OFF_BAR + NBARS * 8 + 16;
   static_assert(SMEM <= 232448, "cluster kernel shared memory");
   static_assert(CL * 16 * (BN + 8) * 2 <= RECV_BYTES, "receive buffer");
@@ -173,8 +173,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
   uint64_t *emptyB = fullB + CK_NBMAX;
   uint64_t *tfull = emptyB + CK_NBMAX;
   uint64_t *tempty = tfull + 2;
-  uint64_t *cbar = tempty + 2;             // [0] after the accumulator push, [1] after the statistics push
-  uint64_t *rbar = cbar + 2;               // transaction barriers: [buf] partials received, [2 + i] statistics received
+  uint64_t *rbar = tempty + 2;             // transaction barriers: [buf] partials received, [2 + i] statistics received
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rbar + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -188,11 +187,6 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
     for (int i = 0; i < CK_NA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], 1); }
     for (int i = 0; i < CK_NBMAX; ++i) { mbar_init(&fullB[i], 1); mbar_init(&emptyB[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
-#if CK_WARP_BAR
-    for (int i = 0; i < 2; ++i) mbar_init(&cbar[i], CL * 8);      // 8 epilogue warps of each of 8 CTAs
-#else
-    for (int i = 0; i < 2; ++i) mbar_init(&cbar[i], CL);          // one leader thread of each of 8 CTAs
-#endif
     for (int i = 0; i < 4; ++i) mbar_init(&rbar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -381,16 +375,13 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         const int M = op->M, Wo = op->Wo, sbox = op->s_box, rows = op->rows, bn = op->bn;
         const int kps = op->kps, kbt = op->kb_total, gn = op->gn, cg = op->cg, pair = op->pair;
         const int nmt = op->nmt, mt0 = tk.y * nmt, nt = tk.z, S = P.S;
-        const int lwo = op->lwo, lbn = op->lbn, lsb = op->lsb, lcg = op->lcg;
+        const int lwo = op->lwo, lsb = op->lsb, lcg = op->lcg;
         const int RPC = 16 * nmt;                        // rows (channels) owned by this CTA
         const int RSH = op->rsh;                         // receive row stride (halves)
-        const int OS = RPC + 1;                          // staging row stride (floats)
         const int A = 2 * nmt;                           // 8-channel GroupNorm atoms owned
         const int nkb = max(0, min(kbt, (rank + 1) * kps) - rank * kps);
         const bool film = e.film_off >= 0;
-        const bool has_res = e.res != nullptr || e.res_f32 != nullptr;
         const int buf = gi & 1;
-        const uint32_t cpar = gi & 1;
         // receive buffers alternate by task: a peer pushing task t+1 has passed
         // barrier A of task t, so every CTA is done reading task t-1's buffer
         __half *recvb = recv + buf * (RECV_BYTES / 2);
@@ -398,12 +389,10 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         auto chan = [&](int r) { return (mt0 + (r >> 4)) * 128 + 16 * rank + (r & 15); };
         // ---- residual producers and the per-sample FiLM rows (prep) first
         if (et == 0) {
-#if CK_TXBAR
           // bytes this CTA will receive: 16 * nmt rows x bn fp16 partials from each of the 8
           // CTAs; with GroupNorm, (mean, M2) of 2 * nmt atoms x s_box samples from each
           mbar_expect_tx(&rbar[buf], (uint32_t)(CL * 16 * nmt * bn * 2));
           if (gn) mbar_expect_tx(&rbar[2 + (gn_i & 1)], (uint32_t)(CL * 2 * nmt * sbox * 8));
-#endif
           if (film) ck_spin(prep_done, S * (it + 1));
           for (int d = 0; d < 2; ++d) ck_wait_dep(P, prep_done, op->epi_dep[d], op->epi_tgt[d], it);
         }
@@ -485,13 +474,8 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
                 const __half2 h2 = __floats2half2_rn(x[2 * i], x[2 * i + 1]);
                 hw[i] = *reinterpret_cast<const uint32_t *>(&h2);
               }
-#if CK_TXBAR
               st_async_v4_b32(dst + c * 2, hw[0], hw[1], hw[2], hw[3], rbar_dst);
               st_async_v4_b32(dst + c * 2 + 16, hw[4], hw[5], hw[6], hw[7], rbar_dst);
-#else
-              st_cluster_v4_b32(dst + c * 2, hw[0], hw[1], hw[2], hw[3]);
-              st_cluster_v4_b32(dst + c * 2 + 16, hw[4], hw[5], hw[6], hw[7]);
-#endif
             }
           }
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -499,13 +483,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           if (lane == 0) mbar_arrive(&tempty[buf]);
           if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 5] = ck_time();
         }
-#if CK_TXBAR
         mbar_wait_cluster(&rbar[buf], (gi >> 1) & 1);            // all 8 CTAs' partials have landed
-#elif CK_WARP_BAR
-        cluster_barrier_warp(&cbar[0], cpar, lane);
-#else
-        cluster_barrier_cta(&cbar[0], cpar, ew == 0, lane, esync);
-#endif
         if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 2] = ck_time();
         // ---- fixed-order sum of the 8 K slices + bias (fp32)
 #pragma unroll
@@ -535,12 +513,8 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
             const float mean = sum / n0;
             const float m2a = fmaxf(sq - sum * mean, 0.f);
             for (int dst = li; dst < CL; dst += L) {      // lane li -> CTAs li, li + L, ...
-#if CK_TXBAR
               st_async_v2_f32(mapa_shared(smem_u32(stats + (rank * A + pa) * sbox + pj), dst), mean, m2a,
                               mapa_shared(smem_u32(&rbar[2 + (gn_i & 1)]), dst));
-#else
-              st_cluster_v2(mapa_shared(smem_u32(stats + (rank * A + pa) * sbox + pj), dst), mean, m2a);
-#endif
             }
             if (pair && li == (CL & (L - 1)))            // the partner tile reads its atoms from L2
               __stcg(&P.gstats[((int64_t)fi * 16 + rank * 2 + pa) * CK_SMAX + pj], make_float2(mean, m2a));
@@ -551,13 +525,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           }
         }
         if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 6] = ck_time();
-#if CK_TXBAR
         if (gn) mbar_wait_cluster(&rbar[2 + (gn_i & 1)], (gn_i >> 1) & 1);   // every peer's statistics
-#elif CK_WARP_BAR
-        if (gn) cluster_barrier_warp(&cbar[1], gn_i & 1, lane);      // statistics exchange
-#else
-        if (gn) cluster_barrier_cta(&cbar[1], gn_i & 1, ew == 0, lane, esync);
-#endif
         if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 3] = ck_time();
         if (gn) {
           // ---- merge the atoms of each group (butterfly, fixed lane order); task atoms are
