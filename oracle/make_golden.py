@@ -38,7 +38,8 @@ if REF_SRC not in sys.path:
     sys.path.insert(0, REF_SRC)
 
 from framepipe.envsim import CirclePath, TrackingEnv  # noqa: E402
-from framepipe.executor import PipelineConfig, run_pipelined, run_sequential  # noqa: E402
+from framepipe.executor import (PipelineConfig, run_decoupled, run_parallel, run_pipelined,  # noqa: E402
+                                run_sequential)
 from framepipe.partition import split_generation, split_perception  # noqa: E402
 from framepipe.policy import make_conditioning_policy  # noqa: E402
 
@@ -92,7 +93,7 @@ def _jsonable(x):
 
 
 def record_case(name, mode, policy_kw, duration, cfg_kw=None, env_seed=None,
-                seq_interval=None, env_kw=None):
+                seq_interval=None, env_kw=None, workers=None, capacity=1.0):
     policy = make_conditioning_policy(**policy_kw)
     env = None
     if env_seed is not None:
@@ -100,6 +101,10 @@ def record_case(name, mode, policy_kw, duration, cfg_kw=None, env_seed=None,
     if mode == "pipe":
         cfg = PipelineConfig(**cfg_kw)
         result = run_pipelined(cfg, policy, env, duration)
+    elif mode == "par":
+        result = run_parallel(policy, env, workers, duration, frame_interval=seq_interval, capacity=capacity)
+    elif mode == "dec":
+        result = run_decoupled(policy, env, duration, frame_interval=seq_interval)
     else:
         result = run_sequential(policy, env, duration, frame_interval=seq_interval)
     case = {
@@ -109,6 +114,8 @@ def record_case(name, mode, policy_kw, duration, cfg_kw=None, env_seed=None,
         "duration": duration,
         "pipeline": cfg_kw,
         "seq_interval": seq_interval,
+        "workers": workers,
+        "capacity": capacity,
         "trace": _jsonable(result.trace),
         "requests": [_jsonable(vars(r)) for r in result.requests],
         "actions": [[float(v) for v in a.values] for a in result.actions],
@@ -201,6 +208,26 @@ def schedule_cases():
     return cases
 
 
+def baseline_cases():
+    """PAR (fp/executor.py:477-576) and DEC (:583-701), the paper's baselines
+    (SURVEY.md §8(f) row 1), with the same toy policies."""
+    cases = []
+    for w in (1, 2, 4):
+        cases.append(record_case(f"six_par_w{w}", "par", SIX, 40, workers=w))
+    cases.append(record_case("six_par_w3_i2", "par", SIX, 40, workers=3, seq_interval=2.0))
+    cases.append(record_case("six_par_w2_cap2_i3", "par", SIX, 40, workers=2, seq_interval=3.0, capacity=2.0))
+    cases.append(record_case("noisy16_par_w4_i8", "par", NOISY16, 40, workers=4, seq_interval=8.0))
+    cases.append(record_case("noisy100_par_w8_i16", "par", NOISY100, 40, workers=8, seq_interval=16.0))
+    cases.append(record_case("cal_par_w2_i64_env3", "par", CAL, 120, workers=2, seq_interval=64.0, env_seed=3))
+    cases.append(record_case("six_dec", "dec", SIX, 40))
+    cases.append(record_case("six_dec_i1", "dec", SIX, 40, seq_interval=1.0))
+    cases.append(record_case("noisy16_dec_i8", "dec", NOISY16, 40, seq_interval=8.0))
+    cases.append(record_case("noisy100_dec_i16", "dec", NOISY100, 40, seq_interval=16.0))
+    cases.append(record_case("multi_dec_i5", "dec", MULTI, 40, seq_interval=5.0))
+    cases.append(record_case("cal_dec_i64_env5", "dec", CAL, 120, seq_interval=64.0, env_seed=5))
+    return cases
+
+
 def partition_goldens():
     out = {"generation": [], "perception": []}
     fixed = [(100, 4, 0.0), (100, 4, 0.5), (100, 5, 1.0), (100, 5, 0.0), (7, 1, 0.0),
@@ -252,6 +279,11 @@ def main():
         json.dump({"generator": "oracle/make_golden.py", "reference": REF_SRC,
                    "numpy": np.__version__, "cases": cases}, fh)
     print(f"wrote {len(cases)} schedule cases to {OUT}")
+    base = baseline_cases()
+    with gzip.open(os.path.join(OUT, "baselines.json.gz"), "wt") as fh:
+        json.dump({"generator": "oracle/make_golden.py", "reference": REF_SRC,
+                   "numpy": np.__version__, "cases": base}, fh)
+    print(f"wrote {len(base)} PAR/DEC cases to {OUT}")
 
 
 if __name__ == "__main__":

@@ -22,6 +22,7 @@ reference's duck type (fp/executor.py:216-330).
 
 from __future__ import annotations
 
+import dataclasses
 import math
 import os
 from dataclasses import dataclass, field
@@ -381,6 +382,172 @@ def run_sequential(policy, env, duration: int, frame_interval=None) -> OracleRes
                                               [age]))
         else:
             rec["dropped_observations"] = 1
+        rec["env_error"] = port.seal()
+        trace.append(rec)
+    return OracleResult(actions, trace, requests)
+
+
+def _mode_header(mode, interval, duration, config, env):
+    return {"type": "header", "schema": 1, "mode": mode, "engine": "virtual",
+            "frame_interval": interval, "duration": duration, "config": config,
+            "success_threshold": getattr(env, "success_threshold", None)}
+
+
+def run_parallel(policy, env, workers: int, duration: int, frame_interval=None,
+                 capacity: float = 1.0) -> OracleResult:
+    """fp/executor.py:477-576 (PAR): `workers` private requests share one unit of
+    compute by processor sharing; a worker that finishes inside a frame takes
+    that frame's observation again at once (just-in-fit), one that finishes on
+    the boundary waits for the next frame's observation."""
+    if workers < 1:
+        raise ValueError("need at least one worker")
+    gen = policy.generation
+    cost = policy.sequential_cost
+    interval = frame_interval if frame_interval is not None else cost
+    trace = [_mode_header("par", interval, duration,
+                          {"workers": workers, "capacity": capacity, "request_cost": cost}, env)]
+    port = _Landing(env, policy)
+    actions, requests = [], []
+    running = []                        # [worker, obs, birth frame, birth time, work left] per job
+    idle = list(range(workers))
+
+    def complete(job, when, rec):
+        worker, obs, birth, born_at, _ = job
+        ctx = policy.perception.perceive(obs)
+        state = gen.initial_state(seed=birth)
+        for _ in range(gen.n_iterations):
+            state = gen.step(state, ctx)
+        land = int(math.ceil(when / interval - 1e-12))
+        emit = land - 1
+        age = float(emit - ctx.produced_frame)
+        a = gen.finish(state, emitted_frame=emit, staleness_profile=(age,) * gen.n_iterations)
+        r = Request(observation_id=obs.id, birth_frame=birth, birth_time=born_at,
+                    completion_frame=land, completion_time=when, jct=when - born_at)
+        r.context_versions.append(1)
+        requests.append(r)
+        actions.append(a)
+        port.queue.append((land, when, a))
+        rec["emissions"].append(_emission(birth, when, emit, land, r.jct, a.values, [age]))
+
+    for t in range(duration):
+        now = float(t) * interval
+        end = now + interval
+        rec = _frame_record(t, now)
+        rec["end"] = end
+        obs = port.boundary(t)
+        rec["superseded_actions"] = port.last_superseded
+        taken = False
+        if idle:
+            running.append([idle.pop(0), obs, t, now, cost])
+            taken = True
+        clock = now
+        while running and clock < end - 1e-12:
+            rate = capacity / len(running)
+            first = min(running, key=lambda j: j[4])
+            finish_at = clock + first[4] / rate
+            if finish_at > end + 1e-12:             # nobody finishes in this frame
+                for j in running:
+                    j[4] -= (end - clock) * rate
+                clock = end
+                break
+            for j in running:
+                j[4] -= (finish_at - clock) * rate
+            clock = finish_at
+            for j in [j for j in running if j[4] <= 1e-9]:
+                running.remove(j)
+                complete(j, finish_at, rec)
+                if finish_at >= end - 1e-9:
+                    idle.append(j[0])
+                else:
+                    running.append([j[0], obs, t, finish_at, cost])
+                    taken = True
+        if not taken:
+            rec["dropped_observations"] = 1
+        rec["env_error"] = port.seal()
+        trace.append(rec)
+    return OracleResult(actions, trace, requests)
+
+
+def run_decoupled(policy, env, duration: int, frame_interval=None) -> OracleResult:
+    """fp/executor.py:583-701 (DEC): perception free-runs on its own worker,
+    publishing into a 2-slot store; generation starts a full request from the
+    newest context as soon as one derived from an unused observation exists.
+    Event order inside a frame: publish < generation start < generation end."""
+    gen = policy.generation
+    p_cost = policy.perception.total_cost
+    g_cost = gen.total_cost
+    interval = frame_interval if frame_interval is not None else policy.sequential_cost
+    trace = [_mode_header("dec", interval, duration,
+                          {"perception_cost": p_cost, "generation_cost": g_cost}, env)]
+    port = _Landing(env, policy)
+    actions, requests = [], []
+    version, n_pub, latest = 0, 0, None     # latest: (frame, version, ctx, source obs id)
+    used_versions = set()
+    p_start, p_obs = 0.0, None
+    g_free, job = 0.0, None                  # job: (end, start, version, ctx, source, state)
+    last_used_obs, fresh_at = -1, None
+    order = {"publish": 0, "gen_start": 1, "gen_done": 2}
+    for t in range(duration):
+        now = float(t) * interval
+        end = now + interval
+        rec = _frame_record(t, now)
+        rec["end"] = end
+        newest_obs = port.boundary(t)
+        rec["superseded_actions"] = port.last_superseded
+        if p_obs is None:
+            p_obs = newest_obs
+        while True:
+            cands = []
+            pub_at = p_start + p_cost
+            if pub_at < end - 1e-9:
+                cands.append(("publish", pub_at))
+            if job is None and fresh_at is not None:
+                g_at = max(g_free, fresh_at)
+                if g_at < end - 1e-9:
+                    cands.append(("gen_start", g_at))
+            if job is not None and job[0] <= end + 1e-9:
+                cands.append(("gen_done", job[0]))
+            if not cands:
+                break
+            what, when = min(cands, key=lambda c: (c[1], order[c[0]]))
+            if what == "publish":
+                ctx = policy.perception.perceive(p_obs)
+                version += 1
+                n_pub += 1
+                if ctx.produced_frame != t:          # the store stamps the publishing frame
+                    ctx = dataclasses.replace(ctx, produced_frame=t)
+                latest = (t, version, ctx, p_obs.id)
+                rec["publishes"].append(version)
+                rec["perception"].append({"start": p_start, "end": when, "obs": p_obs.id, "version": version})
+                if fresh_at is None and p_obs.id > last_used_obs:
+                    fresh_at = when
+                p_start, p_obs = when, newest_obs
+            elif what == "gen_start":
+                _, ver, ctx, src = latest
+                state = gen.initial_state(seed=int(round(when)))
+                for _ in range(gen.n_iterations):
+                    state = gen.step(state, ctx)
+                used_versions.add(ver)
+                last_used_obs, fresh_at = src, None
+                job = (when + g_cost, when, ver, ctx, src, state)
+                g_free = when + g_cost
+                rec["generation_cost"] += g_cost
+            else:
+                fin, began, ver, ctx, src, state = job
+                land = int(math.ceil(fin / interval - 1e-12))
+                emit = land - 1
+                age = float(emit - ctx.produced_frame)
+                a = gen.finish(state, emitted_frame=emit, staleness_profile=(age,) * gen.n_iterations)
+                actions.append(a)
+                r = Request(observation_id=src, birth_frame=int(began // interval), birth_time=began,
+                            completion_frame=land, completion_time=fin, jct=fin - began)
+                r.context_versions.append(ver)
+                requests.append(r)
+                port.queue.append((land, fin, a))
+                rec["emissions"].append(_emission(src, fin, emit, land, r.jct, a.values, [age]))
+                job = None
+        rec["published_total"] = n_pub
+        rec["consumed_total"] = len(used_versions)
         rec["env_error"] = port.seal()
         trace.append(rec)
     return OracleResult(actions, trace, requests)

@@ -31,6 +31,11 @@ def schedule_cases():
     return load("schedules")["cases"]
 
 
+def baseline_cases():
+    """PAR / DEC traces (fp/executor.py:477-701) recorded from the reference."""
+    return load("baselines")["cases"]
+
+
 def case_by_name(name):
     for c in schedule_cases():
         if c["name"] == name:

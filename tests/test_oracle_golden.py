@@ -11,7 +11,7 @@ import os
 import numpy as np
 import pytest
 
-from golden_util import ReplayEnv, load, schedule_cases
+from golden_util import ReplayEnv, baseline_cases, load, schedule_cases
 from oracle import schedule as osched
 from oracle import toy
 
@@ -31,6 +31,27 @@ def test_oracle_reproduces_reference_trace(case):
         res = osched.run_pipelined(case["pipeline"], pol, env, case["duration"])
     else:
         res = osched.run_sequential(pol, env, case["duration"], case["seq_interval"])
+    assert _jsonify(res.trace) == case["trace"]
+    assert [list(a.values) for a in res.actions] == case["actions"]
+    assert [list(a.staleness_profile) for a in res.actions] == case["staleness_profiles"]
+    assert [_jsonify(vars(r)) for r in res.requests] == case["requests"]
+    if env is not None:
+        assert not env.mismatches
+
+
+BASE = baseline_cases()
+
+
+@pytest.mark.parametrize("case", BASE, ids=[c["name"] for c in BASE])
+def test_oracle_reproduces_reference_par_dec(case):
+    """PAR and DEC baselines restated in the oracle."""
+    pol = toy.ToyPolicy(**case["policy"])
+    env = ReplayEnv(case["env"], toy.Obs) if case["env"] else None
+    if case["mode"] == "par":
+        res = osched.run_parallel(pol, env, case["workers"], case["duration"], case["seq_interval"],
+                                  case["capacity"])
+    else:
+        res = osched.run_decoupled(pol, env, case["duration"], case["seq_interval"])
     assert _jsonify(res.trace) == case["trace"]
     assert [list(a.values) for a in res.actions] == case["actions"]
     assert [list(a.staleness_profile) for a in res.actions] == case["staleness_profiles"]
