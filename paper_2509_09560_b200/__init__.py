@@ -16,7 +16,8 @@ from .context import ContextKind, ContextStore, PublicContext
 from .errors import (ConfigInvalid, DeadlockDetected, DeviceError, FramepipeError,
                      IncompleteGeneration, InvalidStageCount, KindMismatch, NotYetPublished,
                      OffsetOutOfRange, ShapeMismatch, StaleWrite, TooManyStages)
-from .executor import PipelineConfig, RequestRecord, RunResult, run_pipelined, run_sequential
+from .executor import (PipelineConfig, RequestRecord, RunResult, run_decoupled, run_parallel, run_pipelined,
+                       run_sequential)
 from .metrics import RolloutMetrics, summarize
 from .partition import StagePlan, plan_stages, split_generation, split_perception
 from .policy import ActionOutput, Observation, Policy, make_conditioning_policy
@@ -33,6 +34,6 @@ __all__ = [
     "NotYetPublished", "Observation", "OffsetOutOfRange", "PipelineConfig", "Policy",
     "PublicContext", "RequestRecord", "RolloutMetrics", "RunResult", "ShapeMismatch",
     "StagePlan", "StaleWrite", "TooManyStages", "make_conditioning_policy",
-    "make_diffusion_policy", "plan_stages", "run_pipelined", "run_sequential",
+    "make_diffusion_policy", "plan_stages", "run_decoupled", "run_parallel", "run_pipelined", "run_sequential",
     "split_generation", "split_perception", "summarize",
 ]

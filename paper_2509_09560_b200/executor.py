@@ -627,3 +627,272 @@ def run_sequential(policy, env, duration: int, frame_interval: Optional[float] =
     return RunResult(actions=per_agent[0], trace=trace, requests=records, agent_actions=per_agent,
                      device_versions=versions,
                      frame_times=_frame_times(dev) if clock == "device" else None)
+
+
+# ---------------------------------------------------------------- PAR / DEC baselines
+
+def _ingest_keyed(dev, key, seed, lane, observations):
+    """dev.ingest with the request state seeded by `seed` but the ingest event
+    filed under `key` (PAR jobs share dispatch frames; DEC seeds by time)."""
+    ev = dev.lane_free.pop(lane, None)
+    if ev is not None:
+        dev.P.wait_event(ev)
+    dev.session.ingest(seed, lane, observations)
+    dev.ingest_event[key] = dev.event(dev.P)
+
+
+def run_parallel(policy, env, workers: int, duration: int, frame_interval: Optional[float] = None,
+                 capacity: float = 1.0, *, clock: str = "virtual", agents: Optional[int] = None,
+                 frame_source=None, frame_hook=None) -> RunResult:
+    """fp/executor.py:477-576 (PAR) on the B200: `workers` private requests
+    share one compute capacity by processor sharing; a worker finishing inside
+    a frame regrabs that frame's observation (just-in-fit).  The schedule is
+    the reference's own float event loop; every job's perception, context
+    publish, n denoise iterations and finish run on the device when it is
+    dispatched (its context in its own ring slot), so its action is ready by
+    the frame it lands.  With capacity 1 the jobs' device work is sequential
+    -- the processor-sharing model's total throughput."""
+    _require_plugin(policy)
+    if workers < 1:
+        raise ConfigInvalid("need at least one worker")
+    if clock not in ("virtual", "device"):
+        raise ConfigInvalid(f"unknown clock {clock!r}")
+    _lib.load()
+    gen = policy.generation
+    cost = policy.sequential_cost
+    interval = frame_interval if frame_interval is not None else cost
+    envs = _agents_and_envs(policy, env, agents)
+    A = len(envs)
+    lanes = workers + 2
+    max_jobs = duration * (workers + 1) + 8
+    dev = _Device(policy, capacity=max(2, workers + 2), lanes=lanes, agents=A, max_outputs=max_jobs,
+                  max_frames=max_jobs, clock=clock)
+    store = dev.store
+    ports = [_Port(e, policy, a, frame_source) for a, e in enumerate(envs)]
+    emis = _Emissions(dev, policy, A)
+    trace = [_header("par", interval, duration,
+                     {"workers": workers, "capacity": capacity, "request_cost": cost}, envs, clock)]
+    records, emitted_rows = [], []
+    n_layers = len(policy.perception.layers)
+    running = []                 # [worker, job id, obs list, birth frame, birth time, work left]
+    idle = list(range(workers))
+    n_jobs = [0]
+
+    def dispatch(worker, obs, t, when):
+        j = n_jobs[0]
+        n_jobs[0] += 1
+        lane = j % lanes
+        _ingest_keyed(dev, j, t, lane, obs)
+        dev.session.perceive(lane, 0, n_layers)
+        slot, version = store.reserve(j, obs[0].id)
+        dev.publish(lane, j, slot, version)
+        dev.generate(j, slot, j, [(lane, 0, gen.n_iterations)], [j])
+        running.append([worker, j, obs, t, when, cost])
+
+    def complete(job, when, rec):
+        _, j, obs, birth, born_at, _ = job
+        land = int(math.ceil(when / interval - 1e-12))
+        emit = land - 1
+        age = float(emit - birth)                  # the context is produced from the dispatch frame
+        r = RequestRecord(observation_id=obs[0].id, birth_frame=birth, birth_time=born_at,
+                          completion_frame=land, completion_time=when, jct=when - born_at)
+        r.context_versions.append(1)             # the reference reports version 1 (fp/executor.py:520)
+        records.append(r)
+        out_index = len(emis.items)
+        dev.finish(j % lanes, out_index)
+        k = emis.add(out_index, emit, (age,) * gen.n_iterations)
+        for port in ports:
+            port.schedule(land, k, k)
+        em = {"request": birth, "time": when, "emission_frame": emit, "land_frame": land,
+              "jct": r.jct, "action": None, "staleness_min": age, "staleness_mean": age,
+              "staleness_max": age, "staleness_final": age}
+        rec["emissions"].append(em)
+        emitted_rows.append((rec, em, r, k))
+
+    for t in range(duration):
+        if frame_hook is not None:
+            frame_hook(t, dev, emis)
+        dev.begin_frame(t, 4)
+        now = float(t) * interval
+        end = now + interval
+        rec = _frame(t, now)
+        rec["end"] = end
+        obs = [port.boundary(t, emis.materialize) for port in ports]
+        rec["superseded_actions"] = ports[0].last_superseded
+        taken = False
+        if idle:
+            dispatch(idle.pop(0), obs, t, now)
+            taken = True
+        clock_t = now
+        while running and clock_t < end - 1e-12:
+            rate = capacity / len(running)
+            first = min(running, key=lambda jb: jb[5])
+            finish_at = clock_t + first[5] / rate
+            if finish_at > end + 1e-12:
+                for jb in running:
+                    jb[5] -= (end - clock_t) * rate
+                clock_t = end
+                break
+            for jb in running:
+                jb[5] -= (finish_at - clock_t) * rate
+            clock_t = finish_at
+            for jb in [jb for jb in running if jb[5] <= 1e-9]:
+                running.remove(jb)
+                complete(jb, finish_at, rec)
+                if finish_at >= end - 1e-9:
+                    idle.append(jb[0])
+                else:
+                    dispatch(jb[0], obs, t, finish_at)
+                    taken = True
+        if not taken:
+            rec["dropped_observations"] = 1
+        rec["env_error"] = ports[0].seal()
+        for port in ports[1:]:
+            port.seal()
+        dev.end_frame(t)
+        trace.append(rec)
+    if frame_hook is not None:
+        frame_hook(duration, dev, emis)
+    dev.synchronize()
+    per_agent = emis.all()
+    for rec_, em, r, k in emitted_rows:
+        em["action"] = list(per_agent[0][k].values)
+    if clock == "device":
+        _apply_device_clock(dev, trace, records, emitted_rows)
+    versions = dev.session.read_version_log(n_jobs[0])
+    dev.session.close()
+    return RunResult(actions=per_agent[0], trace=trace, requests=records, agent_actions=per_agent,
+                     device_versions=versions,
+                     frame_times=_frame_times(dev) if clock == "device" else None)
+
+
+def run_decoupled(policy, env, duration: int, frame_interval: Optional[float] = None, *,
+                  clock: str = "virtual", agents: Optional[int] = None, frame_source=None,
+                  frame_hook=None) -> RunResult:
+    """fp/executor.py:583-701 (DEC) on the B200: perception free-runs on the P
+    stream, publishing into a 2-slot HBM ring; each generation request (seeded
+    by its start time, as in the reference) fetches the newest context and
+    runs all n denoise iterations on G once a context derived from an unused
+    observation exists.  The event order is the reference's (publish < start
+    < finish at equal times)."""
+    _require_plugin(policy)
+    if clock not in ("virtual", "device"):
+        raise ConfigInvalid(f"unknown clock {clock!r}")
+    _lib.load()
+    gen = policy.generation
+    p_cost = policy.perception.total_cost
+    g_cost = gen.total_cost
+    interval = frame_interval if frame_interval is not None else policy.sequential_cost
+    envs = _agents_and_envs(policy, env, agents)
+    A = len(envs)
+    per_frame = int(math.ceil(interval / max(min(p_cost, g_cost), 1e-9))) + 2
+    max_events = duration * per_frame + 8
+    P_LANE, G_LANE = 0, 1
+    dev = _Device(policy, capacity=2, lanes=2, agents=A, max_outputs=max_events, max_frames=max_events,
+                  clock=clock)
+    store = dev.store
+    ports = [_Port(e, policy, a, frame_source) for a, e in enumerate(envs)]
+    emis = _Emissions(dev, policy, A)
+    trace = [_header("dec", interval, duration,
+                     {"perception_cost": p_cost, "generation_cost": g_cost}, envs, clock)]
+    records, emitted_rows = [], []
+    n_layers = len(policy.perception.layers)
+    latest = None                # (frame, version, slot, source observation id)
+    used_versions = set()
+    p_start, p_obs = 0.0, None
+    g_free, job = 0.0, None      # job: (end, start, version, ctx frame, source obs id)
+    last_used_obs, fresh_at = -1, None
+    n_pub, n_gen, keys = 0, 0, 0
+    order = {"publish": 0, "gen_start": 1, "gen_done": 2}
+    for t in range(duration):
+        if frame_hook is not None:
+            frame_hook(t, dev, emis)
+        dev.begin_frame(t, 4)
+        now = float(t) * interval
+        end = now + interval
+        rec = _frame(t, now)
+        rec["end"] = end
+        newest = [port.boundary(t, emis.materialize) for port in ports]
+        rec["superseded_actions"] = ports[0].last_superseded
+        if p_obs is None:
+            p_obs = newest
+        while True:
+            cands = []
+            pub_at = p_start + p_cost
+            if pub_at < end - 1e-9:
+                cands.append(("publish", pub_at))
+            if job is None and fresh_at is not None:
+                g_at = max(g_free, fresh_at)
+                if g_at < end - 1e-9:
+                    cands.append(("gen_start", g_at))
+            if job is not None and job[0] <= end + 1e-9:
+                cands.append(("gen_done", job[0]))
+            if not cands:
+                break
+            what, when = min(cands, key=lambda c: (c[1], order[c[0]]))
+            if what == "publish":
+                keys += 1
+                _ingest_keyed(dev, ("p", keys), t, P_LANE, p_obs)
+                dev.session.perceive(P_LANE, 0, n_layers)
+                slot, version = store.reserve(t, p_obs[0].id)
+                dev.publish(P_LANE, t, slot, version)
+                n_pub += 1
+                latest = (t, version, slot, p_obs[0].id)
+                rec["publishes"].append(version)
+                rec["perception"].append({"start": p_start, "end": when, "obs": p_obs[0].id,
+                                          "version": version})
+                if fresh_at is None and p_obs[0].id > last_used_obs:
+                    fresh_at = when
+                p_start, p_obs = when, newest
+            elif what == "gen_start":
+                ctx_frame, ver, slot, src = latest
+                seed = int(round(when))
+                keys += 1
+                _ingest_keyed(dev, ("g", keys), seed, G_LANE, newest)
+                dev.generate(ctx_frame, slot, n_gen, [(G_LANE, 0, gen.n_iterations)], [("g", keys)])
+                n_gen += 1
+                used_versions.add(ver)
+                last_used_obs, fresh_at = src, None
+                job = (when + g_cost, when, ver, ctx_frame, src)
+                g_free = when + g_cost
+                rec["generation_cost"] += g_cost
+            else:
+                fin, began, ver, ctx_frame, src = job
+                land = int(math.ceil(fin / interval - 1e-12))
+                emit = land - 1
+                age = float(emit - ctx_frame)
+                r = RequestRecord(observation_id=src, birth_frame=int(began // interval), birth_time=began,
+                                  completion_frame=land, completion_time=fin, jct=fin - began)
+                r.context_versions.append(ver)
+                records.append(r)
+                out_index = len(emis.items)
+                dev.finish(G_LANE, out_index)
+                k = emis.add(out_index, emit, (age,) * gen.n_iterations)
+                for port in ports:
+                    port.schedule(land, k, k)
+                em = {"request": src, "time": fin, "emission_frame": emit, "land_frame": land,
+                      "jct": r.jct, "action": None, "staleness_min": age, "staleness_mean": age,
+                      "staleness_max": age, "staleness_final": age}
+                rec["emissions"].append(em)
+                emitted_rows.append((rec, em, r, k))
+                job = None
+        rec["published_total"] = n_pub
+        rec["consumed_total"] = len(used_versions)
+        rec["env_error"] = ports[0].seal()
+        for port in ports[1:]:
+            port.seal()
+        dev.end_frame(t)
+        trace.append(rec)
+    if frame_hook is not None:
+        frame_hook(duration, dev, emis)
+    dev.synchronize()
+    per_agent = emis.all()
+    for rec_, em, r, k in emitted_rows:
+        em["action"] = list(per_agent[0][k].values)
+    if clock == "device":
+        _apply_device_clock(dev, trace, records, emitted_rows)
+    versions = dev.session.read_version_log(max(1, n_gen))
+    dev.session.close()
+    return RunResult(actions=per_agent[0], trace=trace, requests=records, agent_actions=per_agent,
+                     device_versions=versions,
+                     frame_times=_frame_times(dev) if clock == "device" else None)

@@ -18,7 +18,7 @@ import torch
 
 from oracle import dp_model
 from oracle import schedule as osched
-from paper_2509_09560_b200 import PipelineConfig, run_pipelined, run_sequential
+from paper_2509_09560_b200 import PipelineConfig, run_decoupled, run_parallel, run_pipelined, run_sequential
 from paper_2509_09560_b200 import diffusion as D
 
 pytestmark = pytest.mark.gpu
@@ -160,3 +160,23 @@ def test_cluster_kernel_variants_match_oracle(variant, monkeypatch):
         ref = _ORC[a]
         err = rel_err(res.agent_actions[a], ref.actions)
         assert err <= TOL["bf16"], (variant, a, err)
+
+
+@pytest.mark.parametrize("mode", ["par", "dec"])
+def test_tiny_par_dec_match_oracle(mode):
+    """PAR / DEC baselines with the Diffusion Policy
+    plugin vs the oracle driving the CPU network through the restated
+    schedules: same context versions, fp32 actions within 1e-3."""
+    pol = D.make_diffusion_policy("tiny", dtype="fp32", weights=weights("tiny"))
+    gen = pol.generation
+    orc = dp_model.OracleDP(gen.weights, gen.cfg, gen.seed, 0, pol.perception.layer_costs, gen.step_cost)
+    interval = pol.sequential_cost / 4.0
+    if mode == "par":
+        res = run_parallel(pol, None, 3, 10, interval)
+        ref = osched.run_parallel(orc, None, 3, 10, interval)
+    else:
+        res = run_decoupled(pol, None, 10, interval)
+        ref = osched.run_decoupled(orc, None, 10, interval)
+    assert len(res.actions) == len(ref.actions) > 0
+    assert [r.context_versions for r in res.requests] == [r.context_versions for r in ref.requests]
+    assert rel_err(res.actions, ref.actions) <= TOL["fp32"]

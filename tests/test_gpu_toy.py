@@ -142,3 +142,44 @@ class TestDeviceContextStore:
         assert st.device_state() == (10, 9, 10, 0)
         for off in (0, -1, -2, -3):
             assert st.fetch(9, off).produced_frame == 9 + off
+
+
+# ---------------------------------------------------------------- PAR / DEC baselines
+
+from golden_util import baseline_cases  # noqa: E402
+from paper_2509_09560_b200 import run_decoupled, run_parallel  # noqa: E402
+
+BASE = baseline_cases()
+
+
+@pytest.mark.parametrize("case", BASE, ids=[c["name"] for c in BASE])
+def test_par_dec_bit_exact_vs_reference(case):
+    """PAR and DEC (fp/executor.py:477-701) on the device engine: schedule,
+    versions, ages, virtual times and the device-computed fp64 actions equal
+    the reference's traces bit for bit (closed-loop cases replayed)."""
+    pol = make_conditioning_policy(**case["policy"])
+    env = ReplayEnv(case["env"], lambda f, v: Observation(frame=f, vector=v)) if case["env"] else None
+    if case["mode"] == "par":
+        res = run_parallel(pol, env, case["workers"], case["duration"], case["seq_interval"], case["capacity"])
+    else:
+        res = run_decoupled(pol, env, case["duration"], case["seq_interval"])
+    assert _strip(res.trace) == case["trace"]
+    assert [list(a.values) for a in res.actions] == case["actions"]
+    assert [list(a.staleness_profile) for a in res.actions] == case["staleness_profiles"]
+    assert [_j(vars(r)) for r in res.requests] == case["requests"]
+    if env is not None:
+        assert not env.mismatches
+    if case["mode"] == "dec":
+        got = [int(v) for v in res.device_versions[:len(res.requests)]]
+        assert got == [r["context_versions"][0] for r in case["requests"]][:len(got)]
+
+
+def test_par_dec_device_clock_runs():
+    case = next(c for c in BASE if c["name"] == "noisy16_par_w4_i8")
+    pol = make_conditioning_policy(**case["policy"])
+    res = run_parallel(pol, None, case["workers"], case["duration"], case["seq_interval"], clock="device")
+    assert [list(a.values) for a in res.actions] == case["actions"]
+    case = next(c for c in BASE if c["name"] == "noisy16_dec_i8")
+    res = run_decoupled(make_conditioning_policy(**case["policy"]), None, case["duration"], case["seq_interval"],
+                        clock="device")
+    assert [list(a.values) for a in res.actions] == case["actions"]
