@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-depth1", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also report depths 1..8")
+    ap.add_argument("--baselines", action="store_true",
+                    help="also report the PAR (depth-many workers) and DEC baselines on the device clock")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--perception-device", type=int, default=None,
                     help="disaggregated variant: run perception on this GPU and ship context "
@@ -286,6 +288,40 @@ def cpu_oracle_sample(cfg_name, seconds, threads=None):
                       f"also its depth-k rate"}
 
 
+def baseline_modes(pol, depth, agents, dist):
+    """The paper's baselines on the same policy and device (SURVEY.md §8(f) row
+    1), device clock, frame interval = request cost / depth (the pipelined
+    run's frame rate in virtual units): PAR with `depth` workers (processor
+    sharing of one GPU: each job's device work is one full request at batch 1)
+    and DEC (perception free-running -- re-perceiving the newest frame back to
+    back, the redundant work the paper counts -- beside one generation worker).
+    Rate = actions landed in the second half of the run / its device time;
+    staleness = emission frame - context frame."""
+    from paper_2509_09560_b200 import run_decoupled, run_parallel
+    interval = pol.sequential_cost / depth
+    out = {}
+    for name in ("par", "dec"):
+        # PAR's first jobs finish after depth x request cost (processor sharing): run long
+        # enough for the second half to be steady
+        frames = 3 * depth * depth if name == "par" else 6 * depth
+        if name == "par":
+            res = run_parallel(pol, None, depth, frames, interval, clock="device", agents=agents)
+        else:
+            res = run_decoupled(pol, None, frames, interval, clock="device", agents=agents)
+        ft = res.frame_times
+        h = frames // 2
+        span = ft["end"][frames - 1] - ft["end"][h - 1]
+        n = sum(1 for r in res.requests if h <= r.completion_frame - 1 < frames)
+        ages = [a.staleness_profile[-1] for a in res.actions if h <= a.emitted_frame < frames]
+        jct = [r.jct * 1e3 for r in res.requests if h <= r.completion_frame - 1 < frames]
+        out[name] = {"value": dist.world * agents * n / dist.max(span * 1e3) * 1e3 if span > 0 else 0.0,
+                     "unit": "actions/s", "workers": depth if name == "par" else 1,
+                     "mean_staleness_frames": float(np.mean(ages)) if ages else None,
+                     "mean_jct_ms": float(np.mean(jct)) if jct else None,
+                     "frame_interval_virtual": interval}
+    return out
+
+
 def reference_arm(args, dist):
     if dist.rank != 0:
         return
@@ -331,6 +367,7 @@ def main():
     value = K * A * dist.world / (ms / 1e3)
     t0 = fill + W
     p99, jmean = steady_jct_ms(res, t0, K)
+    ages = [a.staleness_profile[-1] for a in res.actions if t0 <= a.emitted_frame < t0 + K]
 
     # roofline of the denoise chain (all UNet GEMM + epilogue launches of a frame),
     # timed with CUDA events on the generation stream around each frame's chain
@@ -397,6 +434,7 @@ def main():
                       "inputs": f"{n_res} synthetic frames + request noise pre-staged in HBM",
                       "perception_device": args.perception_device},
            "p99_action_latency_ms": p99, "mean_action_latency_ms": jmean,
+           "mean_staleness_final_frames": float(np.mean(ages)) if ages else None,
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                         "frac": achieved / hbm_peak, "traffic": traffic,
                         "traffic_source": "ncu dram__bytes_read+write per launch, profiles/r1_ncu_unet_cluster.json",
@@ -419,6 +457,9 @@ def main():
             wk, rk, fk = run_window(pol, k, 0, A, 3, 12, dist, dist.local)
             sweep[k] = 12 * A * dist.world / (dist.max(wk.ms) / 1e3)
         out["depth_sweep_offset0"] = sweep
+
+    if args.baselines:
+        out["baselines"] = baseline_modes(pol, args.depth, A, dist)
 
     # --- e2e: public API, host inputs each frame, action read back each frame
     if not args.no_e2e:
