@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
   if (threadIdx.x == 0) {
     for (int i = 0; i < CK_NA; ++i) { mbar_init(&fullA[i], 1); mbar_init(&emptyA[i], 1); }
     for (int i = 0; i < CK_NBMAX; ++i) { mbar_init(&fullB[i], 1); mbar_init(&emptyB[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
     for (int i = 0; i < 4; ++i) mbar_init(&rbar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -449,21 +449,26 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
             }
           }
         }
-        // ---- drain TMEM and push row slices to their owners (reduce-scatter over DSMEM)
-        if (ew < 4) {
+        // ---- drain TMEM and push row slices to their owners (reduce-scatter over DSMEM):
+        //      all 8 epilogue warps, warps ew and ew + 4 (same TMEM lane quadrant) taking
+        //      alternate 16-column chunks
+        {
           mbar_wait(&tfull[buf], (gi >> 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 1] = ck_time();
-          const int m = ew * 32 + lane;
-          for (int u = 0; u < nmt; ++u) {
+          const int quad = ew & 3, half = ew >> 2;
+          const int m = quad * 32 + lane;
+          const int cpu = bn >> 4, nch = nmt * cpu;
+          for (int q = half; q < nch; q += 2) {
+            const int u = q / cpu, c = (q - u * cpu) * 16;
             // fp16 partial sums (K/8 terms each, fp32-accumulated in TMEM): half the
             // DSMEM traffic; the owner sums the 8 slices in fp32
             const uint32_t dst = mapa_shared(smem_u32(recvb + (rank * RPC + u * 16 + (m & 15)) * RSH), m >> 4);
             const uint32_t rbar_dst = mapa_shared(smem_u32(&rbar[buf]), m >> 4);
-            for (int c = 0; c < bn; c += 16) {
+            {
               float x[16];
               if (nkb > 0) {
-                tmem_ld16(tmem + buf * 2 * CK_BN + u * CK_BN + c + ((uint32_t)(ew * 32) << 16), x);
+                tmem_ld16(tmem + buf * 2 * CK_BN + u * CK_BN + c + ((uint32_t)(quad * 32) << 16), x);
               } else {
 #pragma unroll
                 for (int i = 0; i < 16; ++i) x[i] = 0.f;
