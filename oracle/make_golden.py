@@ -40,6 +40,7 @@ if REF_SRC not in sys.path:
 from framepipe.envsim import CirclePath, TrackingEnv  # noqa: E402
 from framepipe.executor import (PipelineConfig, run_decoupled, run_parallel, run_pipelined,  # noqa: E402
                                 run_sequential)
+from framepipe.metrics import compare, summarize  # noqa: E402
 from framepipe.partition import split_generation, split_perception  # noqa: E402
 from framepipe.policy import make_conditioning_policy  # noqa: E402
 
@@ -120,6 +121,7 @@ def record_case(name, mode, policy_kw, duration, cfg_kw=None, env_seed=None,
         "requests": [_jsonable(vars(r)) for r in result.requests],
         "actions": [[float(v) for v in a.values] for a in result.actions],
         "staleness_profiles": [list(a.staleness_profile) for a in result.actions],
+        "metrics": json.loads(summarize(result.trace).to_json()),
         "env": None,
     }
     if env is not None:
@@ -280,9 +282,20 @@ def main():
                    "numpy": np.__version__, "cases": cases}, fh)
     print(f"wrote {len(cases)} schedule cases to {OUT}")
     base = baseline_cases()
+    # comparison tables of the reference (fp/metrics.py:181-215) over recorded runs
+    by = {c["name"]: c for c in cases + base}
+    tables = []
+    for names, bl in ((["six_seq", "six_pipe_24_m1", "six_par_w2", "six_dec"], 0),
+                      (["noisy100_seq", "noisy100_pipe_18_off0", "noisy100_par_w8_i16", "noisy100_dec_i16"], 1),
+                      (["cal_seq_env11", "cal_pipe_11_off0_env11"], 0)):
+        from framepipe.metrics import RolloutMetrics
+        runs = [RolloutMetrics.from_dict(by[n]["metrics"]) for n in names]
+        t = compare(runs, names=names, baseline=bl)
+        tables.append({"names": names, "baseline": bl, "json": t.to_json(), "csv": t.to_csv(),
+                       "text": t.to_text()})
     with gzip.open(os.path.join(OUT, "baselines.json.gz"), "wt") as fh:
         json.dump({"generator": "oracle/make_golden.py", "reference": REF_SRC,
-                   "numpy": np.__version__, "cases": base}, fh)
+                   "numpy": np.__version__, "cases": base, "compare_tables": tables}, fh)
     print(f"wrote {len(base)} PAR/DEC cases to {OUT}")
 
 

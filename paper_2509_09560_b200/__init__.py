@@ -13,12 +13,12 @@ CNN plugin `make_diffusion_policy`.
 __version__ = "0.1.0"
 
 from .context import ContextKind, ContextStore, PublicContext
-from .errors import (ConfigInvalid, DeadlockDetected, DeviceError, FramepipeError,
+from .errors import (BaselineMissing, ConfigInvalid, DeadlockDetected, DeviceError, FramepipeError,
                      IncompleteGeneration, InvalidStageCount, KindMismatch, NotYetPublished,
                      OffsetOutOfRange, ShapeMismatch, StaleWrite, TooManyStages)
 from .executor import (PipelineConfig, RequestRecord, RunResult, run_decoupled, run_parallel, run_pipelined,
                        run_sequential)
-from .metrics import RolloutMetrics, summarize
+from .metrics import ComparisonTable, RolloutMetrics, compare, read_metrics, summarize, write_trace_jsonl
 from .partition import StagePlan, plan_stages, split_generation, split_perception
 from .policy import ActionOutput, Observation, Policy, make_conditioning_policy
 
@@ -30,10 +30,11 @@ def make_diffusion_policy(*args, **kwargs):
 
 __all__ = [
     "ActionOutput", "ConfigInvalid", "ContextKind", "ContextStore", "DeadlockDetected",
-    "DeviceError", "FramepipeError", "IncompleteGeneration", "InvalidStageCount", "KindMismatch",
+    "BaselineMissing", "DeviceError", "FramepipeError", "IncompleteGeneration", "InvalidStageCount", "KindMismatch",
     "NotYetPublished", "Observation", "OffsetOutOfRange", "PipelineConfig", "Policy",
     "PublicContext", "RequestRecord", "RolloutMetrics", "RunResult", "ShapeMismatch",
     "StagePlan", "StaleWrite", "TooManyStages", "make_conditioning_policy",
     "make_diffusion_policy", "plan_stages", "run_decoupled", "run_parallel", "run_pipelined", "run_sequential",
-    "split_generation", "split_perception", "summarize",
+    "split_generation", "split_perception", "summarize", "compare", "ComparisonTable", "read_metrics",
+    "write_trace_jsonl",
 ]
