@@ -230,6 +230,32 @@ def baseline_cases():
     return cases
 
 
+TUNE_POLICY = dict(layer_costs=(4.0, 4.0), n_iterations=12, step_cost=1.0, eta=0.3, max_action=0.8)
+TUNE_REQUEST = dict(throughput_requirement=0.06, l_max=4, alpha_grid=(0.0, 0.5), seeds=(0, 1),
+                    throughput_frames=24, accuracy_frames=40)
+
+
+def tuner_golden():
+    """fp/tuner.py grid_search + finetune_alpha on a small request (toy policy,
+    TrackingEnv rollouts), and an infeasible request's evaluation log."""
+    from framepipe.errors import NoFeasibleConfig
+    from framepipe.tuner import TuneRequest, finetune_alpha, grid_search
+    pol = make_conditioning_policy(**TUNE_POLICY)
+    req = TuneRequest(**TUNE_REQUEST)
+    factory = lambda seed: tracking_env(seed, frames=60)  # noqa: E731
+    g = grid_search(pol, factory, req)
+    f = finetune_alpha(pol, factory, g.chosen, req)
+    bad = TuneRequest(**dict(TUNE_REQUEST, throughput_requirement=5.0))
+    try:
+        grid_search(pol, factory, bad)
+        infeasible = None
+    except NoFeasibleConfig as exc:
+        infeasible = {"message": str(exc), "result": exc.result.to_dict()}
+    return {"policy": TUNE_POLICY, "request": {k: list(v) if isinstance(v, tuple) else v
+                                               for k, v in TUNE_REQUEST.items()},
+            "env_frames": 60, "grid": g.to_dict(), "alpha": f.to_dict(), "infeasible": infeasible}
+
+
 def partition_goldens():
     out = {"generation": [], "perception": []}
     fixed = [(100, 4, 0.0), (100, 4, 0.5), (100, 5, 1.0), (100, 5, 0.0), (7, 1, 0.0),
@@ -297,6 +323,9 @@ def main():
         json.dump({"generator": "oracle/make_golden.py", "reference": REF_SRC,
                    "numpy": np.__version__, "cases": base, "compare_tables": tables}, fh)
     print(f"wrote {len(base)} PAR/DEC cases to {OUT}")
+    with gzip.open(os.path.join(OUT, "tuner.json.gz"), "wt") as fh:
+        json.dump(tuner_golden(), fh)
+    print("wrote the tuner golden")
 
 
 if __name__ == "__main__":

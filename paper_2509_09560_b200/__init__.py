@@ -13,13 +13,14 @@ CNN plugin `make_diffusion_policy`.
 __version__ = "0.1.0"
 
 from .context import ContextKind, ContextStore, PublicContext
-from .errors import (BaselineMissing, ConfigInvalid, DeadlockDetected, DeviceError, FramepipeError,
+from .errors import (BaselineMissing, ConfigInvalid, NoFeasibleConfig, DeadlockDetected, DeviceError, FramepipeError,
                      IncompleteGeneration, InvalidStageCount, KindMismatch, NotYetPublished,
                      OffsetOutOfRange, ShapeMismatch, StaleWrite, TooManyStages)
 from .executor import (PipelineConfig, RequestRecord, RunResult, run_decoupled, run_parallel, run_pipelined,
                        run_sequential)
 from .metrics import ComparisonTable, RolloutMetrics, compare, read_metrics, summarize, write_trace_jsonl
 from .partition import StagePlan, plan_stages, split_generation, split_perception
+from .tuner import GridPoint, TuneRequest, TuneResult, finetune_alpha, grid_search
 from .policy import ActionOutput, Observation, Policy, make_conditioning_policy
 
 
@@ -30,11 +31,11 @@ def make_diffusion_policy(*args, **kwargs):
 
 __all__ = [
     "ActionOutput", "ConfigInvalid", "ContextKind", "ContextStore", "DeadlockDetected",
-    "BaselineMissing", "DeviceError", "FramepipeError", "IncompleteGeneration", "InvalidStageCount", "KindMismatch",
+    "BaselineMissing", "NoFeasibleConfig", "DeviceError", "FramepipeError", "IncompleteGeneration", "InvalidStageCount", "KindMismatch",
     "NotYetPublished", "Observation", "OffsetOutOfRange", "PipelineConfig", "Policy",
     "PublicContext", "RequestRecord", "RolloutMetrics", "RunResult", "ShapeMismatch",
     "StagePlan", "StaleWrite", "TooManyStages", "make_conditioning_policy",
     "make_diffusion_policy", "plan_stages", "run_decoupled", "run_parallel", "run_pipelined", "run_sequential",
     "split_generation", "split_perception", "summarize", "compare", "ComparisonTable", "read_metrics",
-    "write_trace_jsonl",
+    "write_trace_jsonl", "TuneRequest", "TuneResult", "GridPoint", "grid_search", "finetune_alpha",
 ]

@@ -84,3 +84,30 @@ def test_toy_closed_forms():
         s = pol.generation.step(s, toy.Ctx(c2, 1))
     want = c2 + beta ** (n - k) * ((1.0 - beta ** k) * c1 - c2)
     assert np.allclose(s.vector, want, rtol=1e-12)
+
+
+
+CLOSED = [c for c in CASES + BASE if c["env"]]
+
+
+@pytest.mark.parametrize("case", CLOSED, ids=[c["name"] for c in CLOSED])
+def test_oracle_env_closes_the_loop_like_the_reference(case):
+    """oracle/envsim.py restates fp/envsim.py: running the oracle schedule in
+    a real closed loop with it (not a replay) reproduces the reference's
+    recorded trace, observations and sealed errors bit for bit."""
+    from oracle import envsim
+    rec = case["env"]
+    env = envsim.tracking_env(rec["seed"], **rec["kw"])
+    assert env.success_threshold == rec["success_threshold"]
+    pol = toy.ToyPolicy(**case["policy"])
+    if case["mode"] == "pipe":
+        res = osched.run_pipelined(case["pipeline"], pol, env, case["duration"])
+    elif case["mode"] == "seq":
+        res = osched.run_sequential(pol, env, case["duration"], case["seq_interval"])
+    elif case["mode"] == "par":
+        res = osched.run_parallel(pol, env, case["workers"], case["duration"], case["seq_interval"],
+                                  case["capacity"])
+    else:
+        res = osched.run_decoupled(pol, env, case["duration"], case["seq_interval"])
+    assert _jsonify(res.trace) == case["trace"]
+    assert env.errors == rec["errors"]
