@@ -101,6 +101,19 @@ int auras_toy_generate(double *x_state, const int *lanes, const int *iters, int 
 int auras_toy_finish(const double *x_state, int lane, double max_action, double *out,
                      void *stream);
 
+/* Scripted token policy (fp/policy.py:110-161, 300-327): tokens[lane][p] for
+ * p in [starts[i], starts[i] + counts[i]) of each request lane, from the
+ * displacement in the fetched ring slot (`fetched` = {slot, version, frame});
+ * replaces GenerationModel.step for autoregressive contexts (:217-228). */
+int auras_ar_generate(int *tokens, int l_a, const int *lanes, const int *starts, const int *counts, int n,
+                      const double *ring_payload, const int64_t *fetched, double max_action, void *stream);
+/* GenerationModel.finish for token policies: the lane's l_a tokens -> out (as doubles). */
+int auras_ar_finish(const int *tokens, int lane, int l_a, double *out, void *stream);
+/* Payload half of ContextStore.update_action_tokens (fp/context.py:166-175):
+ * the newest context's payload re-published into another slot (the version
+ * is released by auras_ring_commit). */
+int auras_ring_copy_slot(double *payload, int elems, int src, int dst, void *stream);
+
 /* -------------------------------------------------- diffusion policy (DP)
  * Replaces PerceptionModel / GenerationModel arithmetic for the Diffusion
  * Policy CNN plugin.  The host builds a program of

@@ -42,7 +42,7 @@ from framepipe.executor import (PipelineConfig, run_decoupled, run_parallel, run
                                 run_sequential)
 from framepipe.metrics import compare, summarize  # noqa: E402
 from framepipe.partition import split_generation, split_perception  # noqa: E402
-from framepipe.policy import make_conditioning_policy  # noqa: E402
+from framepipe.policy import make_autoregressive_policy, make_conditioning_policy  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden")
 
@@ -95,7 +95,9 @@ def _jsonable(x):
 
 def record_case(name, mode, policy_kw, duration, cfg_kw=None, env_seed=None,
                 seq_interval=None, env_kw=None, workers=None, capacity=1.0):
-    policy = make_conditioning_policy(**policy_kw)
+    kw = dict(policy_kw)
+    factory = make_autoregressive_policy if kw.pop("autoregressive", False) else make_conditioning_policy
+    policy = factory(**kw)
     env = None
     if env_seed is not None:
         env = RecordingEnv(tracking_env(env_seed, **(env_kw or {})))
@@ -298,8 +300,51 @@ def partition_goldens():
     return out
 
 
+AR = dict(autoregressive=True, layer_costs=(14.0, 14.0), l_a=7, prefill_cost=10.0, decode_cost=1.0)
+
+
+def autoregressive_cases():
+    """Token policy (fp/policy.py:300-327) through the merged-prefill schedule
+    (fp/executor.py:321-348), sequential (:447-449), PAR and DEC (:670-672):
+    SURVEY.md §8(f) row 3.  Mirrors t/test_executor.py:214-260 and
+    t/test_acceptance.py:230-260, plus closed-loop runs."""
+    cases = []
+    for merge in (True, False):
+        m = "m" if merge else "u"
+        for l_a in (7, 14, 28):
+            kw = dict(AR, l_a=l_a)
+            cases.append(record_case(f"ar{l_a}_pipe_14_{m}", "pipe", kw, 40,
+                                     dict(pp_perception=1, pp_generation=4, fetch_offset=-1,
+                                          merge_autoregressive=merge)))
+        cases.append(record_case(f"ar7_pipe_24_{m}", "pipe", AR, 40,
+                                 dict(pp_perception=2, pp_generation=4, fetch_offset=-1,
+                                      merge_autoregressive=merge)))
+        cases.append(record_case(f"ar14_pipe_13_off0_{m}", "pipe", dict(AR, l_a=14), 40,
+                                 dict(pp_perception=1, pp_generation=3, fetch_offset=0,
+                                      merge_autoregressive=merge)))
+    cases.append(record_case("ar7_pipe_12_snapshot", "pipe", AR, 40,
+                             dict(pp_perception=1, pp_generation=2, fetch_offset=-2, read_policy="snapshot",
+                                  store_capacity=4)))
+    for l_a in (7, 14, 28):
+        cases.append(record_case(f"ar{l_a}_seq", "seq", dict(AR, l_a=l_a), 30))
+    cases.append(record_case("ar7_seq_i16", "seq", AR, 30, seq_interval=16.0))
+    cases.append(record_case("ar7_pipe_14_m_env3", "pipe", AR, 120,
+                             dict(pp_perception=1, pp_generation=4, fetch_offset=-1, merge_autoregressive=True),
+                             env_seed=3))
+    cases.append(record_case("ar7_seq_env3", "seq", AR, 60, env_seed=3))
+    cases.append(record_case("ar7_par_w2_i8", "par", AR, 40, workers=2, seq_interval=8.0))
+    cases.append(record_case("ar7_dec_i8", "dec", AR, 40, seq_interval=8.0))
+    cases.append(record_case("ar7_dec_i32_env5", "dec", AR, 80, seq_interval=32.0, env_seed=5))
+    return cases
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    ar = autoregressive_cases()
+    with gzip.open(os.path.join(OUT, "autoregressive.json.gz"), "wt") as fh:
+        json.dump({"generator": "oracle/make_golden.py", "reference": REF_SRC,
+                   "numpy": np.__version__, "cases": ar}, fh)
+    print(f"wrote {len(ar)} autoregressive cases to {OUT}")
     with gzip.open(os.path.join(OUT, "partition.json.gz"), "wt") as fh:
         json.dump(partition_goldens(), fh)
     cases = schedule_cases()

@@ -21,7 +21,7 @@ from .executor import (PipelineConfig, RequestRecord, RunResult, run_decoupled, 
 from .metrics import ComparisonTable, RolloutMetrics, compare, read_metrics, summarize, write_trace_jsonl
 from .partition import StagePlan, plan_stages, split_generation, split_perception
 from .tuner import GridPoint, TuneRequest, TuneResult, finetune_alpha, grid_search
-from .policy import ActionOutput, Observation, Policy, make_conditioning_policy
+from .policy import make_autoregressive_policy, ActionOutput, Observation, Policy, make_conditioning_policy
 
 
 def make_diffusion_policy(*args, **kwargs):
@@ -34,7 +34,7 @@ __all__ = [
     "BaselineMissing", "NoFeasibleConfig", "DeviceError", "FramepipeError", "IncompleteGeneration", "InvalidStageCount", "KindMismatch",
     "NotYetPublished", "Observation", "OffsetOutOfRange", "PipelineConfig", "Policy",
     "PublicContext", "RequestRecord", "RolloutMetrics", "RunResult", "ShapeMismatch",
-    "StagePlan", "StaleWrite", "TooManyStages", "make_conditioning_policy",
+    "StagePlan", "StaleWrite", "TooManyStages", "make_conditioning_policy", "make_autoregressive_policy",
     "make_diffusion_policy", "plan_stages", "run_decoupled", "run_parallel", "run_pipelined", "run_sequential",
     "split_generation", "split_perception", "summarize", "compare", "ComparisonTable", "read_metrics",
     "write_trace_jsonl", "TuneRequest", "TuneResult", "GridPoint", "grid_search", "finetune_alpha",

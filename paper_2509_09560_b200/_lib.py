@@ -63,6 +63,9 @@ _SIGNATURES = {
     "auras_toy_publish": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_int, i64, i64, vp]),
     "auras_toy_generate": (C.c_int, [vp, ip, ip, C.c_int, f64, vp, vp, vp]),
     "auras_toy_finish": (C.c_int, [vp, C.c_int, f64, vp, vp]),
+    "auras_ar_generate": (C.c_int, [vp, C.c_int, ip, ip, ip, C.c_int, vp, vp, f64, vp]),
+    "auras_ar_finish": (C.c_int, [vp, C.c_int, C.c_int, vp, vp]),
+    "auras_ring_copy_slot": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp]),
     "auras_unet_plan_create": (vp, [C.POINTER(ConvOp), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                     vp, vp, C.c_int, i64, i64, vp, vp, C.c_int, C.POINTER(Sched),
                                     vp, C.c_int]),

@@ -206,9 +206,24 @@ class ContextStore:
         version, frame, slot = self.resolve_latest()
         return frame, version, self._host_context(slot, frame)
 
+    def reserve_token_update(self, frame: int):
+        """Host half of update_action_tokens (fp/context.py:166-175): the newest
+        context, with the new action-token prefix, re-published as `frame`'s
+        context under a new version.  Returns (source slot, slot, version); the
+        device half copies the payload and releases the version.  The token
+        prefix itself lives in the requests' lanes: the scripted token policy
+        reads each request's own prefix (fp/policy.py:226-228), so only the
+        version and the context's frame stamp change here."""
+        if self._last_frame is None:
+            raise NotYetPublished("nothing published yet")
+        src = self.slot_of(self._last_frame)
+        obs = self._slot_obs[src]
+        slot, version = self.reserve(frame, obs)
+        return src, slot, version
+
     def update_action_tokens(self, frame: int, tokens):
-        raise KindMismatch("action-token updates belong to autoregressive contexts "
-                           "(out of scope for the diffusion hot path)")
+        raise KindMismatch("host-side token updates are not supported; the engine updates the "
+                           "device ring (reserve_token_update)")
 
     def device_state(self):
         """(version, last frame, publish count, error flag) as seen by the device."""

@@ -273,3 +273,81 @@ int auras_toy_finish(const double *x_state, int lane, double max_action, double 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- scripted token policy
+// fp/policy.py:110-161: the displacement in the fetched context (vision row 0,
+// the toy ring payload {x, y}) quantised into the 7-token schema
+// (sign, mag / 8, mag % 8) per axis + STOP, repeated cyclically for l_a > 7.
+// Token p of a request depends only on the context it reads and p.
+
+namespace {
+__device__ int ar_token(double dx, double dy, double max_action, int p) {
+  const int k = p % 7;
+  if (k == 6) return 0;                                  // STOP_TOKEN
+  const double raw = k < 3 ? dx : dy;
+  const double width = max_action / 63.0;
+  const double v = fmin(fmax(raw, -max_action), max_action);
+  int mag = (int)floor(fabs(v) / width + 0.5);
+  mag = mag < 63 ? mag : 63;
+  const int sign = mag == 0 ? 0 : (v > 0.0 ? 1 : 2);
+  const int j = k % 3;
+  return j == 0 ? sign : (j == 1 ? mag / 8 : mag % 8);
+}
+
+struct ArBatch {
+  int lanes[64], starts[64], counts[64];
+};
+
+__global__ void ar_generate_kernel(int *tokens, int l_a, ArBatch b, int n, const double *ring_payload,
+                                   const int64_t *fetched, double max_action) {
+  const int64_t slot = fetched[0];
+  const double dx = ring_payload[slot * 2], dy = ring_payload[slot * 2 + 1];
+  for (int r = 0; r < n; ++r)
+    for (int i = threadIdx.x; i < b.counts[r]; i += blockDim.x) {
+      const int p = b.starts[r] + i;
+      if (p < l_a) tokens[b.lanes[r] * l_a + p] = ar_token(dx, dy, max_action, p);
+    }
+}
+
+__global__ void ar_finish_kernel(const int *tokens, int lane, int l_a, double *out) {
+  for (int i = threadIdx.x; i < l_a; i += blockDim.x) out[i] = (double)tokens[lane * l_a + i];
+}
+
+__global__ void ring_copy_slot_kernel(double *payload, int elems, int src, int dst) {
+  for (int i = threadIdx.x; i < elems; i += blockDim.x) payload[dst * elems + i] = payload[src * elems + i];
+}
+}  // namespace
+
+extern "C" {
+
+int auras_ar_generate(int *tokens, int l_a, const int *lanes, const int *starts, const int *counts, int n,
+                      const double *ring_payload, const int64_t *fetched, double max_action, void *stream) {
+  if (n < 0 || n > 64 || l_a < 1 || !tokens || !ring_payload || !fetched) {
+    set_error("ar_generate: bad args (n=%d, l_a=%d)", n, l_a);
+    return AURAS_E_ARG;
+  }
+  if (n == 0) return AURAS_OK;
+  ArBatch b;
+  memset(&b, 0, sizeof(b));
+  for (int i = 0; i < n; ++i) { b.lanes[i] = lanes[i]; b.starts[i] = starts[i]; b.counts[i] = counts[i]; }
+  ar_generate_kernel<<<1, 64, 0, as_stream(stream)>>>(tokens, l_a, b, n, ring_payload, fetched, max_action);
+  AURAS_LAUNCHED("ar_generate_kernel");
+  return AURAS_OK;
+}
+
+int auras_ar_finish(const int *tokens, int lane, int l_a, double *out, void *stream) {
+  if (!tokens || !out || lane < 0 || l_a < 1) { set_error("ar_finish: bad args"); return AURAS_E_ARG; }
+  ar_finish_kernel<<<1, 64, 0, as_stream(stream)>>>(tokens, lane, l_a, out);
+  AURAS_LAUNCHED("ar_finish_kernel");
+  return AURAS_OK;
+}
+
+int auras_ring_copy_slot(double *payload, int elems, int src, int dst, void *stream) {
+  if (!payload || elems < 1 || src < 0 || dst < 0) { set_error("ring_copy_slot: bad args"); return AURAS_E_ARG; }
+  if (src == dst) return AURAS_OK;
+  ring_copy_slot_kernel<<<1, 128, 0, as_stream(stream)>>>(payload, elems, src, dst);
+  AURAS_LAUNCHED("ring_copy_slot_kernel");
+  return AURAS_OK;
+}
+
+}  // extern "C"

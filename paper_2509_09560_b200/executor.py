@@ -274,6 +274,14 @@ class _Device:
         self.session.finish(lane, out_index)
         self.lane_free[lane] = self.event(self.G)
 
+    def republish(self, src_slot, slot, frame, version):
+        """Token-prefix update of the shared context (autoregressive policies)."""
+        ev = self.slot_read.get(slot)
+        if ev is not None:
+            self.P.wait_event(ev)
+        self.session.republish(src_slot, slot, frame, version)
+        self.pub_event[frame] = self.event(self.P)
+
     def seconds(self, ev):
         return self.origin.elapsed_time(ev) / 1e3
 
@@ -442,6 +450,12 @@ def run_pipelined(cfg: PipelineConfig, policy, env, duration: int, *, clock: str
                         raise DeadlockDetected(
                             f"frame {t}: context for frame {t + offset} can never exist")
                     version, ctx_frame, slot = store.resolve_latest()
+            ar = policy.kind == ContextKind.AUTOREGRESSIVE
+            if merge and ar:
+                # one merged prefill over the shared context serves every stage (fp/executor.py:321-324)
+                rec["prefill_calls"] += 1
+                rec["generation_cost"] += gen.prefill_cost
+                gen_costs.append(gen.prefill_cost)
             batch, first = [], []
             for j, b, item in active:
                 iters = plan.generation_stages[j - 1]
@@ -453,13 +467,22 @@ def run_pipelined(cfg: PipelineConfig, policy, env, duration: int, *, clock: str
                 item["ages"].extend([age] * iters)
                 item["steps"] += iters
                 item["rec"].context_versions.append(version)
-                c = iters * gen.step_cost
-                gen_costs.append(c)
-                rec["generation_cost"] += c
+                if not (merge and ar):
+                    c = gen.prefill_cost + max(iters - 1, 0) * gen.decode_cost if ar else iters * gen.step_cost
+                    gen_costs.append(c)
+                    rec["generation_cost"] += c
+                    if ar:
+                        rec["prefill_calls"] += 1
+                        rec["decode_calls"] += max(iters - 1, 0)
                 rec["generation"].append({"request": b, "stage": j, "iterations": iters,
                                           "context_version": version, "context_frame": ctx_frame,
                                           "context_age_at_emission": age})
             dev.generate(ctx_frame, slot, t, batch, first)
+            if ar:
+                # the freshest token prefix goes back into the shared context as a new
+                # version of this frame's context (fp/executor.py:345-348)
+                src, slot2, ver2 = store.reserve_token_update(t)
+                dev.republish(src, slot2, t, ver2)
 
         # frame duration in cost units (fp/executor.py:350-374)
         if offset == 0 and gen_costs and published:
@@ -602,6 +625,9 @@ def run_sequential(policy, env, duration: int, frame_interval: Optional[float] =
                 port.schedule(land, k, k)
             free_at = land
             rec["generation_cost"] = gen.total_cost
+            if policy.kind == ContextKind.AUTOREGRESSIVE:
+                rec["prefill_calls"] = 1
+                rec["decode_calls"] = gen.n_iterations - 1
             em = {"request": t, "time": done, "emission_frame": emit, "land_frame": land,
                   "jct": cost, "action": None, "staleness_min": age, "staleness_mean": age,
                   "staleness_max": age, "staleness_final": age}
@@ -855,6 +881,9 @@ def run_decoupled(policy, env, duration: int, frame_interval: Optional[float] = 
                 last_used_obs, fresh_at = src, None
                 job = (when + g_cost, when, ver, ctx_frame, src)
                 g_free = when + g_cost
+                if policy.kind == ContextKind.AUTOREGRESSIVE:
+                    rec["prefill_calls"] += 1
+                    rec["decode_calls"] += gen.n_iterations - 1
                 rec["generation_cost"] += g_cost
             else:
                 fin, began, ver, ctx_frame, src = job

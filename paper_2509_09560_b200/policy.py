@@ -224,3 +224,115 @@ def make_conditioning_policy(layer_costs=(14.0, 14.0), n_iterations: int = 100,
                   generation=RefinementGeneration(n_iterations=n_iterations, step_cost=step_cost,
                                                   eta=eta, max_action=max_action,
                                                   noise_init=noise_init))
+
+
+# ---------------------------------------------------------------- scripted token policy
+
+ACTION_TOKEN_COUNT = 7
+_MAG_LEVELS = 63
+
+
+def decode_action_tokens(tokens, max_action: float) -> np.ndarray:
+    """fp/policy.py:135-148: the 7-token schema back to a planar displacement."""
+    toks = [int(t) for t in tokens]
+    if len(toks) < ACTION_TOKEN_COUNT:
+        raise ValueError(f"need {ACTION_TOKEN_COUNT} tokens, got {len(toks)}")
+    width = max_action / _MAG_LEVELS
+    out = []
+    for axis in range(2):
+        sign, hi, lo = toks[3 * axis: 3 * axis + 3]
+        s = 0.0 if sign == 0 else (1.0 if sign == 1 else -1.0)
+        out.append(s * (hi * 8 + lo) * width)
+    return np.array(out)
+
+
+@dataclass(frozen=True)
+class TokenGeneration:
+    """Token-sequential generation (fp/policy.py:167-256, autoregressive
+    branch): one token per iteration from the scripted policy, costs a flat
+    prefill per call plus one decode per further token."""
+
+    n_iterations: int
+    step_cost: float
+    prefill_cost: float = 10.0
+    decode_cost: float = 1.0
+    max_action: float = 0.8
+    kind: ContextKind = ContextKind.AUTOREGRESSIVE
+
+    def __post_init__(self):
+        if self.n_iterations < 1:
+            raise ValueError("n_iterations must be positive")
+        if self.step_cost <= 0:
+            raise ValueError("step_cost must be strictly positive")
+
+    @property
+    def total_cost(self) -> float:
+        return self.prefill_cost + (self.n_iterations - 1) * self.decode_cost
+
+    def initial_noise(self, seed: Optional[int]) -> np.ndarray:
+        return np.zeros(2)                      # token states start empty
+
+    def decode_action(self, action: ActionOutput) -> np.ndarray:
+        vec = decode_action_tokens(action.values, self.max_action)
+        norm = float(np.linalg.norm(vec))
+        if norm > self.max_action:
+            vec = vec * (self.max_action / norm)
+        return vec
+
+    def open_session(self, policy, **kw):
+        return TokenSession(policy, **kw)
+
+
+class TokenSession(RefinementSession):
+    """Device state of the scripted token policy: the toy ring (the context's
+    displacement, fp64), int32 token lanes, fp64 token outputs."""
+
+    def __init__(self, policy, **kw):
+        import torch
+        max_outputs = kw.get("max_outputs", 1)
+        super().__init__(policy, **kw)
+        dev = self.x.device
+        self.l_a = policy.generation.n_iterations
+        self.tokens = torch.zeros(self.x.shape[0], self.l_a, dtype=torch.int32, device=dev)
+        self.out = torch.zeros(max(1, max_outputs), self.l_a, dtype=torch.float64, device=dev)
+
+    def generate(self, batch):
+        lanes = _lib.int_array([b[0] for b in batch])
+        starts = _lib.int_array([b[1] for b in batch])
+        counts = _lib.int_array([b[2] for b in batch])
+        _lib.check(self.lib.auras_ar_generate(self.tokens.data_ptr(), self.l_a, lanes, starts, counts,
+                                              len(batch), self.store.payload.data_ptr(),
+                                              self.fetched.data_ptr(), self.gen.max_action, self.g.cuda_stream),
+                   "ar_generate")
+
+    def finish(self, lane, out_index):
+        _lib.check(self.lib.auras_ar_finish(self.tokens.data_ptr(), lane, self.l_a,
+                                            self.out[out_index].data_ptr(), self.g.cuda_stream), "ar_finish")
+
+    def republish(self, src_slot, slot, frame, version):
+        """Device half of an action-token context update (P stream)."""
+        st = self.store
+        _lib.check(self.lib.auras_ring_copy_slot(st.payload.data_ptr(), st.slot_elems, src_slot, slot,
+                                                 self.p.cuda_stream), "ring_copy_slot")
+        st.commit(frame, version, self.p)
+
+    def action_values(self, row):
+        return tuple(int(v) for v in row)
+
+
+def make_autoregressive_policy(layer_costs=(14.0, 14.0), l_a: int = ACTION_TOKEN_COUNT,
+                               prefill_cost: float = 10.0, decode_cost: float = 1.0,
+                               max_action: float = 0.8, vision_len: int = 96, language_len: int = 32,
+                               latent_width: int = 64) -> Policy:
+    """Same signature and semantics as fp/policy.py:300-327 (the scripted token
+    policy whose context mirrors the X_V / X_L / X_A layout), on the B200.  The
+    token policy reads only the displacement in vision row 0, which is what
+    the device ring carries; the long X_V / X_L rows exist in the reference to
+    size the merged prefill and do not change any token."""
+    costs = tuple(float(c) for c in layer_costs)
+    if not costs or any(c <= 0 for c in costs):
+        raise ValueError("layer costs must be positive")
+    return Policy(perception=PerceptionSpec(costs, obs_width=4),
+                  generation=TokenGeneration(n_iterations=l_a, step_cost=decode_cost,
+                                             prefill_cost=prefill_cost, decode_cost=decode_cost,
+                                             max_action=max_action))

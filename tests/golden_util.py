@@ -72,3 +72,14 @@ class ReplayEnv:
 
 def strip_none_keys(trace):
     return json.loads(json.dumps(trace))
+
+
+def autoregressive_cases():
+    """Token-policy traces (fp/policy.py:300-327, merged prefill
+    fp/executor.py:321-348) recorded from the reference."""
+    return load("autoregressive")["cases"]
+
+
+def policy_kwargs(case):
+    kw = dict(case["policy"])
+    return kw.pop("autoregressive", False), kw
