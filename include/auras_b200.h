@@ -114,6 +114,27 @@ int auras_ar_finish(const int *tokens, int lane, int l_a, double *out, void *str
  * is released by auras_ring_commit). */
 int auras_ring_copy_slot(double *payload, int elems, int src, int dst, void *stream);
 
+/* -------------------------------------------------- causal transformer (AR)
+ * fp64 pre-norm causal transformer with its KV cache in HBM
+ * (fp/transformer.py:69-211): the model of the autoregressive merged prefill.
+ * `params` packs, in order: tok_emb [vocab,d], pos_emb [max_len,d], per layer
+ * {ln1_g, ln1_b [d], wq, wk, wv, wo [d,d], ln2_g, ln2_b [d], w1 [d,4d],
+ * b1 [4d], w2 [4d,d], b2 [d]}, lnf_g, lnf_b [d]. */
+int64_t auras_tf_param_count(int d_model, int n_heads, int n_layers, int vocab, int max_len);
+/* Rows [start, start+n) of a sequence whose rows [0, start) are in `kv`
+ * ([layers][2][max_len][d]): prefill (start 0; CausalTransformer.prefill /
+ * prefill_embedded, :106-143), decode (n 1; :147-173) and the merged prefill
+ * (:175-193).  Input rows are token ids (`token_ids`) or embeddings
+ * (`embeddings` [n,d]); `resid`, `qbuf` are [n,d] scratch; `hidden` [n,d]
+ * receives the final-LN hidden states. */
+int auras_tf_forward(const double *params, int d_model, int n_heads, int n_layers, int vocab, int max_len,
+                     const int *token_ids, const double *embeddings, int start, int n,
+                     double *kv, double *resid, double *qbuf, double *hidden, void *stream);
+/* logits = hidden @ tok_emb^T (:207-208) and the greedy token (:210-211);
+ * either output may be NULL. */
+int auras_tf_logits(const double *params, int d_model, int vocab, const double *hidden, int n,
+                    double *logits, int *argmax, void *stream);
+
 /* -------------------------------------------------- diffusion policy (DP)
  * Replaces PerceptionModel / GenerationModel arithmetic for the Diffusion
  * Policy CNN plugin.  The host builds a program of

@@ -26,4 +26,8 @@ Contents
   arithmetic is "parity unpinned" by the reference: the reference pins only
   the schedule that decides which context version each denoise step reads.
   The restatement follows SURVEY.md Appendix B and states every choice.
+* `transformer` -- the reference's float64 causal transformer
+  (fp/transformer.py:58-211) restated in numpy, the checker for the device
+  merged prefill.  PINNED against hidden states, KV rows, logits and greedy
+  tokens recorded from the reference (tests/golden/transformer.json.gz).
 """

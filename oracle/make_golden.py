@@ -300,6 +300,51 @@ def partition_goldens():
     return out
 
 
+def transformer_goldens():
+    """Hidden states, logits and greedy tokens of the reference's float64
+    CausalTransformer (fp/transformer.py:69-211) for the cases its own tests
+    exercise (t/test_transformer.py:34-192, t/test_acceptance.py:61-90):
+    prefills of random token strings over several seeds and shapes, a
+    prefill + decode chain, a merged prefill over an [X_V; X_L; X_A] context."""
+    from framepipe.context import ContextKind, PublicContext
+    from framepipe.transformer import CausalTransformer, TransformerConfig
+    out = {"configs": [], "prefill": [], "decode": [], "merged": []}
+    shapes = [dict(), dict(seed=3), dict(d_model=32, n_heads=2, n_layers=2, vocab_size=50, max_len=64, seed=5),
+              dict(d_model=48, n_heads=4, n_layers=3, vocab_size=40, max_len=96, seed=6)]
+    rng = np.random.default_rng(20240911)
+    for ci, kw in enumerate(shapes):
+        cfg = TransformerConfig(**kw)
+        model = CausalTransformer(cfg)
+        out["configs"].append(kw)
+        for n in (1, 2, 7, 24, 40):
+            n = min(n, cfg.max_len)
+            toks = rng.integers(0, cfg.vocab_size, n)
+            h, cache = model.prefill(toks)
+            out["prefill"].append({"config": ci, "tokens": [int(t) for t in toks], "hidden": h.tolist(),
+                                   "logits_last": model.logits(h[-1]).tolist(),
+                                   "greedy": [model.greedy_token(r) for r in h],
+                                   "k_layer0_last": cache.keys[0][-1].ravel().tolist()})
+        toks = rng.integers(0, cfg.vocab_size, 16)
+        _, cache = model.prefill(toks[:-7])
+        chain = []
+        for t in toks[-7:]:
+            hd, cache = model.decode(int(t), cache)
+            chain.append(hd.tolist())
+        out["decode"].append({"config": ci, "tokens": [int(t) for t in toks], "prefix": 9, "hidden": chain})
+        d = cfg.d_model
+        vision = rng.normal(0.0, 0.05, (16, d))
+        language = rng.normal(0.0, 0.05, (8, d))
+        atoks = tuple(int(x) for x in rng.integers(0, cfg.vocab_size, 5))
+        ctx = PublicContext(kind=ContextKind.AUTOREGRESSIVE, vision_tokens=vision, language_tokens=language,
+                            action_tokens=atoks, source_observation_id=0, produced_frame=0)
+        pos = [24, 26, 28]
+        mg = model.merged_generate(ctx, pos)
+        out["merged"].append({"config": ci, "vision": vision.tolist(), "language": language.tolist(),
+                              "action_tokens": list(atoks), "positions": pos,
+                              "hidden": {str(p): mg[p].tolist() for p in pos}})
+    return out
+
+
 AR = dict(autoregressive=True, layer_costs=(14.0, 14.0), l_a=7, prefill_cost=10.0, decode_cost=1.0)
 
 
@@ -340,6 +385,10 @@ def autoregressive_cases():
 
 def main():
     os.makedirs(OUT, exist_ok=True)
+    with gzip.open(os.path.join(OUT, "transformer.json.gz"), "wt") as fh:
+        json.dump({"generator": "oracle/make_golden.py", "reference": REF_SRC,
+                   "numpy": np.__version__, **transformer_goldens()}, fh)
+    print("wrote the transformer goldens")
     ar = autoregressive_cases()
     with gzip.open(os.path.join(OUT, "autoregressive.json.gz"), "wt") as fh:
         json.dump({"generator": "oracle/make_golden.py", "reference": REF_SRC,

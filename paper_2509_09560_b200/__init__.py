@@ -13,7 +13,7 @@ CNN plugin `make_diffusion_policy`.
 __version__ = "0.1.0"
 
 from .context import ContextKind, ContextStore, PublicContext
-from .errors import (BaselineMissing, ConfigInvalid, NoFeasibleConfig, DeadlockDetected, DeviceError, FramepipeError,
+from .errors import (LengthExceeded, SequenceComplete, BaselineMissing, ConfigInvalid, NoFeasibleConfig, DeadlockDetected, DeviceError, FramepipeError,
                      IncompleteGeneration, InvalidStageCount, KindMismatch, NotYetPublished,
                      OffsetOutOfRange, ShapeMismatch, StaleWrite, TooManyStages)
 from .executor import (PipelineConfig, RequestRecord, RunResult, run_decoupled, run_parallel, run_pipelined,
@@ -29,7 +29,10 @@ def make_diffusion_policy(*args, **kwargs):
     return _make(*args, **kwargs)
 
 
+from .transformer import CausalTransformer, KvCache, TransformerConfig
+
 __all__ = [
+    "CausalTransformer", "KvCache", "TransformerConfig", "LengthExceeded", "SequenceComplete",
     "ActionOutput", "ConfigInvalid", "ContextKind", "ContextStore", "DeadlockDetected",
     "BaselineMissing", "NoFeasibleConfig", "DeviceError", "FramepipeError", "IncompleteGeneration", "InvalidStageCount", "KindMismatch",
     "NotYetPublished", "Observation", "OffsetOutOfRange", "PipelineConfig", "Policy",

@@ -66,6 +66,10 @@ _SIGNATURES = {
     "auras_ar_generate": (C.c_int, [vp, C.c_int, ip, ip, ip, C.c_int, vp, vp, f64, vp]),
     "auras_ar_finish": (C.c_int, [vp, C.c_int, C.c_int, vp, vp]),
     "auras_ring_copy_slot": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp]),
+    "auras_tf_param_count": (i64, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
+    "auras_tf_forward": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, C.c_int,
+                                   vp, vp, vp, vp, vp]),
+    "auras_tf_logits": (C.c_int, [vp, C.c_int, C.c_int, vp, C.c_int, vp, vp, vp]),
     "auras_unet_plan_create": (vp, [C.POINTER(ConvOp), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                     vp, vp, C.c_int, i64, i64, vp, vp, C.c_int, C.POINTER(Sched),
                                     vp, C.c_int]),

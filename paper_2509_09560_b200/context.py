@@ -37,42 +37,67 @@ class ContextKind(str, Enum):
     CONDITIONING = "conditioning"
 
 
-def _checksum(conditioning, source_observation_id: int, produced_frame: int) -> int:
+def _checksum(vision, language, action_tokens, conditioning,
+              source_observation_id: int, produced_frame: int) -> int:
+    """fp/context.py:28-36."""
     crc = 0
-    if conditioning is not None:
-        crc = zlib.crc32(np.ascontiguousarray(conditioning, dtype=np.float64).tobytes(), crc)
-    crc = zlib.crc32(repr(()).encode(), crc)
+    for arr in (vision, language, conditioning):
+        if arr is not None:
+            crc = zlib.crc32(np.ascontiguousarray(arr, dtype=np.float64).tobytes(), crc)
+    crc = zlib.crc32(repr(tuple(action_tokens)).encode(), crc)
     crc = zlib.crc32(f"{source_observation_id}:{produced_frame}".encode(), crc)
     return crc
 
 
 @dataclass(frozen=True)
 class PublicContext:
-    """A conditioning-kind public context (H_o of Eq. 2; fp/context.py:39-88).
+    """The public context (H_o of Eq. 2; fp/context.py:39-88): a conditioning
+    vector for refinement policies, or [X_V; X_L; X_A] for token policies.
 
-    `conditioning` is a host copy when one exists (standalone store use); the
-    engine's contexts are device-resident and carry only their ring slot."""
+    `conditioning` / the token arrays are host copies when one exists
+    (standalone use, the causal transformer's merged prefill); the engine's
+    contexts are device-resident and carry only their ring slot."""
 
     kind: ContextKind
     source_observation_id: int
     produced_frame: int
+    vision_tokens: Optional[np.ndarray] = None
+    language_tokens: Optional[np.ndarray] = None
+    action_tokens: tuple = ()
     conditioning: Optional[np.ndarray] = None
     slot: int = -1
     checksum: int = field(default=-1)
 
     def __post_init__(self):
-        if self.kind != ContextKind.CONDITIONING:
-            raise KindMismatch("the B200 hot path carries conditioning contexts only")
-        if self.conditioning is not None:
-            object.__setattr__(self, "conditioning",
-                               np.asarray(self.conditioning, dtype=np.float64))
-        object.__setattr__(self, "checksum", _checksum(self.conditioning,
-                                                       self.source_observation_id,
-                                                       self.produced_frame))
+        if self.kind == ContextKind.AUTOREGRESSIVE:
+            if self.vision_tokens is None or self.language_tokens is None:
+                raise ValueError("autoregressive context requires vision and language tokens")
+            if self.conditioning is not None:
+                raise ValueError("autoregressive context must not carry a conditioning vector")
+            object.__setattr__(self, "vision_tokens", np.asarray(self.vision_tokens, dtype=np.float64))
+            object.__setattr__(self, "language_tokens", np.asarray(self.language_tokens, dtype=np.float64))
+        elif self.kind == ContextKind.CONDITIONING:
+            if self.vision_tokens is not None or self.language_tokens is not None or self.action_tokens:
+                raise ValueError("conditioning context must not carry token fields")
+            if self.conditioning is not None:
+                object.__setattr__(self, "conditioning",
+                                   np.asarray(self.conditioning, dtype=np.float64))
+        else:
+            raise ValueError(f"unknown context kind: {self.kind!r}")
+        object.__setattr__(self, "action_tokens", tuple(int(t) for t in self.action_tokens))
+        object.__setattr__(self, "checksum", self._compute_checksum())
+
+    def _compute_checksum(self) -> int:
+        return _checksum(self.vision_tokens, self.language_tokens, self.action_tokens,
+                         self.conditioning, self.source_observation_id, self.produced_frame)
 
     def verify_checksum(self) -> bool:
-        return self.checksum == _checksum(self.conditioning, self.source_observation_id,
-                                          self.produced_frame)
+        return self.checksum == self._compute_checksum()
+
+    def with_action_tokens(self, tokens) -> "PublicContext":
+        if self.kind != ContextKind.AUTOREGRESSIVE:
+            raise KindMismatch("action tokens only exist on autoregressive contexts")
+        return replace(self, action_tokens=tuple(tokens))
 
     def with_produced_frame(self, frame: int) -> "PublicContext":
         return replace(self, produced_frame=frame)

@@ -43,3 +43,22 @@ def test_no_cpu_fallback():
         run_pipelined(PipelineConfig(pp_generation=2), six(), None, 4)
     with pytest.raises(DeviceError):
         run_sequential(six(), None, 4)
+
+
+def test_transformer_config_and_ar_context_validation():
+    import numpy as np
+    from paper_2509_09560_b200 import ContextKind, KindMismatch, PublicContext, TransformerConfig
+    with pytest.raises(ValueError):
+        TransformerConfig(d_model=65, n_heads=4)
+    with pytest.raises(ValueError):
+        TransformerConfig(n_layers=0)
+    assert TransformerConfig().head_dim == 16
+    with pytest.raises(ValueError):
+        PublicContext(kind=ContextKind.AUTOREGRESSIVE, source_observation_id=0, produced_frame=0)
+    ctx = PublicContext(kind=ContextKind.AUTOREGRESSIVE, vision_tokens=np.zeros((2, 4)),
+                        language_tokens=np.zeros((1, 4)), source_observation_id=0, produced_frame=0)
+    assert ctx.verify_checksum() and ctx.with_action_tokens([3, 4]).action_tokens == (3, 4)
+    cond = PublicContext(kind=ContextKind.CONDITIONING, conditioning=np.zeros(2),
+                         source_observation_id=0, produced_frame=0)
+    with pytest.raises(KindMismatch):
+        cond.with_action_tokens([1])
