@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--sweep", action="store_true", help="also report depths 1..8")
     ap.add_argument("--baselines", action="store_true",
                     help="also report the PAR (depth-many workers) and DEC baselines on the device clock")
+    ap.add_argument("--merged-prefill", action="store_true",
+                    help="also time the AR merged prefill (csrc/transformer.cu) vs per-stage prefills")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--perception-device", type=int, default=None,
                     help="disaggregated variant: run perception on this GPU and ship context "
@@ -322,6 +324,50 @@ def baseline_modes(pol, depth, agents, dist):
     return out
 
 
+def merged_prefill_bench(pp_g=4, reps=50, vision_len=96, language_len=32, l_a=7):
+    """one causal prefill over [X_V; X_L; X_A] serving
+    the pp_g in-flight requests (fp/transformer.py:175-193) against one prefill
+    per stage (the unmerged schedule), default TransformerConfig, fp64 on the
+    device; the numpy oracle on one host core beside it."""
+    import torch
+    from oracle import transformer as tfo
+    from paper_2509_09560_b200 import CausalTransformer
+    m = CausalTransformer()
+    rng = np.random.default_rng(0)
+    d = m.config.d_model
+    total = vision_len + language_len + l_a
+    emb = torch.from_numpy(rng.normal(0.0, 0.05, (total, d))).cuda()
+    st = torch.cuda.current_stream()
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(reps):
+            fn()
+        b.record(st)
+        b.synchronize()
+        return a.elapsed_time(b) / reps
+
+    merged = timed(lambda: m.prefill_device(embeddings=emb))
+    lens = [total - pp_g + 1 + j for j in range(pp_g)]
+    separate = timed(lambda: [m.prefill_device(embeddings=emb[:n]) for n in lens])
+    _, cache = m.prefill_device(embeddings=emb[:total - 1])
+    dec = timed(lambda: m.decode(3, cache))
+    w = tfo.init_weights()
+    e = emb.cpu().numpy()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        tfo.forward(w, e)
+    cpu_merged = (time.perf_counter() - t0) / 5 * 1e3
+    return {"rows": total, "pp_g": pp_g, "merged_ms": merged, "separate_ms": separate,
+            "merged_speedup": separate / merged, "decode_ms_incl_readback": dec,
+            "launches_per_prefill": m.config.n_layers + 1,
+            "cpu_numpy_merged_ms": cpu_merged, "dtype": "f64",
+            "note": "device time, CUDA events over %d reps; CPU = oracle/transformer.py numpy" % reps}
+
+
 def reference_arm(args, dist):
     if dist.rank != 0:
         return
@@ -460,6 +506,9 @@ def main():
 
     if args.baselines:
         out["baselines"] = baseline_modes(pol, args.depth, A, dist)
+
+    if args.merged_prefill and dist.rank == 0:
+        out["merged_prefill"] = merged_prefill_bench()
 
     # --- e2e: public API, host inputs each frame, action read back each frame
     if not args.no_e2e:

@@ -136,14 +136,14 @@ class CausalTransformer:
             emb.data_ptr() if emb is not None else None,
             start, n, buf.tensor.data_ptr(), resid.data_ptr(), qbuf.data_ptr(), hidden.data_ptr(), stream),
             "tf_forward")
-        self.launches += 2 * self.config.n_layers
+        self.launches += self.config.n_layers + 1
         buf.tip = start + n
         return hidden
 
     def _new_buffer(self):
         import torch
         c = self.config
-        return _KvBuffer(torch.zeros(c.n_layers, 2, c.max_len, c.d_model, dtype=torch.float64,
+        return _KvBuffer(torch.empty(c.n_layers, 2, c.max_len, c.d_model, dtype=torch.float64,
                                      device=self.device))
 
     def _check_len(self, m):
