@@ -17,7 +17,10 @@ Contents
   by oracle/make_golden.py), bit for bit.
 * `toy` -- the reference's fp64 refinement policy x <- x + eta (H - x)
   (fp/policy.py:217-246, 279-297).  PINNED by the same golden traces and by
-  the closed forms of t/test_policy.py:56-152.
+  the closed forms of t/test_policy.py:56-152.  Also the scripted token
+  policy (fp/policy.py:116-165, 300-327) with the merged-prefill accounting
+  and token-update re-publish in `schedule` (fp/executor.py:321-348):
+  PINNED by the 20 autoregressive traces in tests/golden/autoregressive.json.gz.
 * `dp_model` -- a torch-CPU fp32 restatement of the Diffusion Policy CNN
   (ResNet-18-GroupNorm observation encoder, ConditionalUnet1D with FiLM,
   DDPM / DDIM schedulers).  These networks live in third-party code that is

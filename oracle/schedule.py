@@ -206,8 +206,11 @@ def run_pipelined(cfg: dict, policy, env, duration: int) -> OracleResult:
 
     `cfg` is the PipelineConfig field dict (fp/executor.py:48-60)."""
     pp_p, pp_g = cfg.get("pp_perception", 1), cfg.get("pp_generation", 1)
+    ar = getattr(policy, "kind", "conditioning") == "autoregressive"
     off = cfg.get("fetch_offset")
-    off = 0 if off is None else off
+    off = (-1 if ar else 0) if off is None else off          # fp/executor.py:61-65
+    m_cfg = cfg.get("merge_autoregressive")
+    merge = (m_cfg and ar) if m_cfg is not None else ar      # fp/executor.py:66-70
     alpha = cfg.get("alpha", 0.0)
     interval = cfg.get("frame_interval")
     cap = cfg.get("store_capacity", 2)
@@ -231,7 +234,7 @@ def run_pipelined(cfg: dict, policy, env, duration: int) -> OracleResult:
               "config": {"pipeline": full_cfg,
                          "plan": {"perception_stages": [list(r) for r in ranges],
                                   "generation_stages": list(counts), "alpha": alpha},
-                         "fetch_offset": off, "merged": False},
+                         "fetch_offset": off, "merged": bool(merge)},
               "success_threshold": getattr(env, "success_threshold", None)}]
 
     ring = Ring(cap)
@@ -291,6 +294,10 @@ def run_pipelined(cfg: dict, policy, env, duration: int) -> OracleResult:
                     if t + off < pp_p - 1:
                         raise DeadlockDetected(t)
                     version, ctx_frame, ctx = ring.latest_entry()
+            if merge and ar:                     # one merged prefill (fp/executor.py:321-324)
+                rec["prefill_calls"] += 1
+                rec["generation_cost"] += gen.prefill_cost
+                gen_costs.append(gen.prefill_cost)
             for j, b in active:
                 item = live[b]
                 iters = counts[j - 1]
@@ -299,13 +306,23 @@ def run_pipelined(cfg: dict, policy, env, duration: int) -> OracleResult:
                     item["state"] = gen.step(item["state"], ctx)
                 item["ages"].extend([age] * iters)
                 item["req"].context_versions.append(version)
-                c = iters * gen.step_cost
-                gen_costs.append(c)
-                rec["generation_cost"] += c
+                if not (merge and ar):
+                    c = gen.stage_cost(iters) if ar else iters * gen.step_cost
+                    gen_costs.append(c)
+                    rec["generation_cost"] += c
+                    if ar:
+                        rec["prefill_calls"] += 1
+                        rec["decode_calls"] += max(iters - 1, 0)
                 rec["generation"].append({"request": b, "stage": j, "iterations": iters,
                                           "context_version": version,
                                           "context_frame": ctx_frame,
                                           "context_age_at_emission": age})
+            if ar:
+                # the freshest token prefix back into the shared context: the
+                # newest context re-published as this frame's, new version
+                # (fp/executor.py:345-348, fp/context.py:166-175)
+                _, _, newest = ring.latest_entry()
+                ring.publish(newest, t)
 
         if off == 0 and gen_costs and published:
             busiest = max(side_costs + [pub_cost + max(gen_costs)])
@@ -377,6 +394,9 @@ def run_sequential(policy, env, duration: int, frame_interval=None) -> OracleRes
             actions.append(a)
             port.queue.append((land, now + cost, a))
             free_at = land
+            if getattr(policy, "kind", "") == "autoregressive":     # fp/executor.py:447-449
+                rec["prefill_calls"] = 1
+                rec["decode_calls"] = gen.n_iterations - 1
             rec["generation_cost"] = gen.total_cost
             rec["emissions"].append(_emission(t, now + cost, emit, land, cost, a.values,
                                               [age]))
@@ -531,6 +551,9 @@ def run_decoupled(policy, env, duration: int, frame_interval=None) -> OracleResu
                 last_used_obs, fresh_at = src, None
                 job = (when + g_cost, when, ver, ctx, src, state)
                 g_free = when + g_cost
+                if getattr(policy, "kind", "") == "autoregressive":     # fp/executor.py:670-672
+                    rec["prefill_calls"] += 1
+                    rec["decode_calls"] += gen.n_iterations - 1
                 rec["generation_cost"] += g_cost
             else:
                 fin, began, ver, ctx, src, state = job

@@ -111,3 +111,44 @@ def test_oracle_env_closes_the_loop_like_the_reference(case):
         res = osched.run_decoupled(pol, env, case["duration"], case["seq_interval"])
     assert _jsonify(res.trace) == case["trace"]
     assert env.errors == rec["errors"]
+
+
+from golden_util import autoregressive_cases, policy_kwargs  # noqa: E402
+
+AR_CASES = autoregressive_cases()
+
+
+@pytest.mark.parametrize("case", AR_CASES, ids=[c["name"] for c in AR_CASES])
+def test_oracle_reproduces_reference_autoregressive(case):
+    """Token policy through the merged / per-stage prefill schedule, the
+    per-frame token update, sequential, PAR and DEC."""
+    ar, kw = policy_kwargs(case)
+    assert ar
+    pol = toy.TokenPolicy(**kw)
+    env = ReplayEnv(case["env"], toy.Obs) if case["env"] else None
+    if case["mode"] == "pipe":
+        res = osched.run_pipelined(case["pipeline"], pol, env, case["duration"])
+    elif case["mode"] == "par":
+        res = osched.run_parallel(pol, env, case["workers"], case["duration"], case["seq_interval"],
+                                  case["capacity"])
+    elif case["mode"] == "dec":
+        res = osched.run_decoupled(pol, env, case["duration"], case["seq_interval"])
+    else:
+        res = osched.run_sequential(pol, env, case["duration"], case["seq_interval"])
+    assert _jsonify(res.trace) == case["trace"]
+    assert [list(a.values) for a in res.actions] == case["actions"]
+    assert [list(a.staleness_profile) for a in res.actions] == case["staleness_profiles"]
+    assert [_jsonify(vars(r)) for r in res.requests] == case["requests"]
+    if env is not None:
+        assert not env.mismatches
+
+
+def test_token_schema_matches_reference_examples():
+    """t/test_policy.py:150-205: encode / decode round trip within a bucket."""
+    enc = toy.encode_action_tokens((0.25, -0.1), 0.8)
+    assert len(enc) == 7 and enc[6] == 0 and enc[0] == 1 and enc[3] == 2
+    back = toy.decode_action_tokens(enc, 0.8)
+    assert np.allclose(back, [0.25, -0.1], atol=0.8 / 63)
+    assert np.allclose(toy.decode_action_tokens(toy.encode_action_tokens((5.0, -5.0), 0.8), 0.8), [0.8, -0.8])
+    assert toy.encode_action_tokens((0.0, 0.0), 0.8) == (0,) * 7
+    assert toy.encode_action_tokens((0.3, 0.3), 0.8, 14)[7:] == toy.encode_action_tokens((0.3, 0.3), 0.8)
