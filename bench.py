@@ -107,7 +107,7 @@ class ClockSampler:
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "sw_power_cap": 0x4}
 
-    def __init__(self, device, period=0.2):
+    def __init__(self, device, period=0.05):
         self.device, self.period = device, period
         self.samples, self.masks, self.max_mhz = [], [], None
         self.stop_flag = threading.Event()
@@ -150,7 +150,7 @@ class ClockSampler:
         reasons = sorted(n for n, bit in self.REASONS.items() if any(m & bit for m in self.masks))
         return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
                 "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples),
-                "source": "NVML, 200 ms period"}
+                "source": "NVML, 50 ms period"}
 
 
 # ---------------------------------------------------------------- measurement helpers

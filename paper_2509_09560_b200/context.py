@@ -127,6 +127,7 @@ class ContextStore:
         self._slot_frame = [None] * capacity
         self._slot_version = [0] * capacity
         self._slot_obs = [None] * capacity
+        self._slot_host = [None] * capacity     # host copies of token-policy contexts
 
     # -- properties (fp/context.py:117-127)
     @property
@@ -161,6 +162,7 @@ class ContextStore:
         self._slot_frame[slot] = frame
         self._slot_version[slot] = self._version
         self._slot_obs[slot] = frame if source_observation_id is None else source_observation_id
+        self._slot_host[slot] = None
         self._last_frame = frame
         return slot, self._version
 
@@ -198,12 +200,17 @@ class ContextStore:
 
     # -- reference-compatible API (fp/context.py:129-164)
     def publish(self, ctx: PublicContext, frame: int) -> int:
+        """fp/context.py:129-143.  A token-policy context carries its
+        displacement (vision row 0) in the device slot, which is all the
+        scripted token kernels read; the full [X_V; X_L; X_A] stays as a host
+        copy for fetches."""
         import torch
-        if ctx.kind != ContextKind.CONDITIONING:
-            raise KindMismatch("conditioning contexts only")
-        if ctx.conditioning is None:
+        if ctx.kind == ContextKind.AUTOREGRESSIVE:
+            vec = np.asarray(ctx.vision_tokens, dtype=np.float64)[0, :2].ravel()
+        elif ctx.conditioning is None:
             raise ValueError("publish() of a host context needs its conditioning vector")
-        vec = np.asarray(ctx.conditioning, dtype=np.float64).ravel()
+        else:
+            vec = np.asarray(ctx.conditioning, dtype=np.float64).ravel()
         if vec.size > self.slot_elems:
             raise ValueError(f"context of {vec.size} elements exceeds slot of {self.slot_elems}")
         slot, version = self.reserve(frame, ctx.source_observation_id)
@@ -212,9 +219,14 @@ class ContextStore:
         dst = self.payload[0, slot, : vec.size]
         dst.copy_(src, non_blocking=True)
         self.commit(frame, version, stream)
+        if ctx.kind == ContextKind.AUTOREGRESSIVE:
+            self._slot_host[slot] = ctx
         return version
 
     def _host_context(self, slot: int, frame: int) -> PublicContext:
+        host = self._slot_host[slot]
+        if host is not None:                 # the store stamps the publishing frame
+            return replace(host, produced_frame=frame, slot=slot)
         vals = self.payload[0, slot].double().cpu().numpy()
         return PublicContext(kind=ContextKind.CONDITIONING,
                              source_observation_id=self._slot_obs[slot], produced_frame=frame,
@@ -246,9 +258,23 @@ class ContextStore:
         slot, version = self.reserve(frame, obs)
         return src, slot, version
 
-    def update_action_tokens(self, frame: int, tokens):
-        raise KindMismatch("host-side token updates are not supported; the engine updates the "
-                           "device ring (reserve_token_update)")
+    def update_action_tokens(self, frame: int, tokens) -> int:
+        """fp/context.py:166-175: the latest context with `tokens` as its
+        action tokens, re-published as `frame`'s context under a new version
+        (device copy + release on the current stream)."""
+        import torch
+        if self._last_frame is None:
+            raise NotYetPublished("nothing published yet")
+        host = self._slot_host[self.slot_of(self._last_frame)]
+        if host is None:
+            raise KindMismatch("latest context is not autoregressive")
+        src, slot, version = self.reserve_token_update(frame)
+        stream = torch.cuda.current_stream()
+        _lib.check(_lib.load().auras_ring_copy_slot(self.payload.data_ptr(), self.slot_elems, src, slot,
+                                                    stream.cuda_stream), "ring_copy_slot")
+        self.commit(frame, version, stream)
+        self._slot_host[slot] = host.with_action_tokens(tokens)
+        return version
 
     def device_state(self):
         """(version, last frame, publish count, error flag) as seen by the device."""

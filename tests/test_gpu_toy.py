@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 
 from golden_util import ReplayEnv, schedule_cases
-from paper_2509_09560_b200 import (ContextKind, ContextStore, NotYetPublished, OffsetOutOfRange,
+from paper_2509_09560_b200 import (ContextKind, ContextStore, KindMismatch, NotYetPublished, OffsetOutOfRange,
                                    PipelineConfig, PublicContext, StaleWrite,
                                    make_conditioning_policy, run_pipelined, run_sequential,
                                    summarize)
@@ -142,6 +142,30 @@ class TestDeviceContextStore:
         assert st.device_state() == (10, 9, 10, 0)
         for off in (0, -1, -2, -3):
             assert st.fetch(9, off).produced_frame == 9 + off
+
+    def test_update_action_tokens(self):
+        """t/test_context_store.py token-update cases (fp/context.py:166-175)."""
+        st = ContextStore(capacity=2)
+        with pytest.raises(NotYetPublished):
+            st.update_action_tokens(0, [1])
+        st.publish(self.ctx(0), 0)
+        with pytest.raises(KindMismatch):
+            st.update_action_tokens(0, [1])
+        vis = np.zeros((4, 8))
+        vis[0, :2] = [0.25, -0.5]
+        ar = PublicContext(kind=ContextKind.AUTOREGRESSIVE, source_observation_id=1, produced_frame=1,
+                           vision_tokens=vis, language_tokens=np.zeros((2, 8)))
+        v1 = st.publish(ar, 1)
+        v2 = st.update_action_tokens(2, [3, 4, 5])
+        assert v2 == v1 + 1
+        got = st.fetch(2, 0)
+        assert got.kind == ContextKind.AUTOREGRESSIVE and got.action_tokens == (3, 4, 5)
+        assert got.produced_frame == 2 and got.source_observation_id == 1
+        assert list(st.payload[0, st.slot_of(2)].cpu().numpy()) == [0.25, -0.5]
+        assert st.fetch(2, -1).action_tokens == ()
+        assert st.device_state()[:3] == (v2, 2, 3)
+        with pytest.raises(StaleWrite):
+            st.update_action_tokens(1, [1])
 
 
 # ---------------------------------------------------------------- PAR / DEC baselines
