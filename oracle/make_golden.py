@@ -93,6 +93,13 @@ def _jsonable(x):
     return x
 
 
+def _metrics_or_error(trace):
+    try:
+        return json.loads(summarize(trace).to_json())
+    except Exception as e:                           # noqa: BLE001 -- EmptyTrace on 0-frame runs
+        return {"error": type(e).__name__}
+
+
 def record_case(name, mode, policy_kw, duration, cfg_kw=None, env_seed=None,
                 seq_interval=None, env_kw=None, workers=None, capacity=1.0):
     kw = dict(policy_kw)
@@ -123,7 +130,7 @@ def record_case(name, mode, policy_kw, duration, cfg_kw=None, env_seed=None,
         "requests": [_jsonable(vars(r)) for r in result.requests],
         "actions": [[float(v) for v in a.values] for a in result.actions],
         "staleness_profiles": [list(a.staleness_profile) for a in result.actions],
-        "metrics": json.loads(summarize(result.trace).to_json()),
+        "metrics": _metrics_or_error(result.trace),
         "env": None,
     }
     if env is not None:
@@ -345,6 +352,50 @@ def transformer_goldens():
     return out
 
 
+def edge_goldens():
+    """Boundary runs the reference's tests touch (empty and one-frame runs in
+    every mode, live reads, drop on overrun, alpha outside [0, 1]) and the
+    configuration errors PipelineConfig.validate raises (fp/executor.py:72-92)."""
+    cases = []
+    for d in (0, 1, 2):
+        cases.append(record_case(f"six_pipe_22_d{d}", "pipe", SIX, d, dict(pp_perception=2, pp_generation=2)))
+        cases.append(record_case(f"six_seq_d{d}", "seq", SIX, d))
+        cases.append(record_case(f"six_par_w2_d{d}", "par", SIX, d, workers=2))
+        cases.append(record_case(f"six_dec_d{d}", "dec", SIX, d))
+        cases.append(record_case(f"ar7_pipe_14_d{d}", "pipe", AR, d, dict(pp_perception=1, pp_generation=4)))
+    cases.append(record_case("noisy16_pipe_14_live_m1", "pipe", NOISY16, 30,
+                             dict(pp_perception=1, pp_generation=4, fetch_offset=-1, read_policy="live")))
+    cases.append(record_case("noisy16_pipe_22_live_m2_k3", "pipe", NOISY16, 30,
+                             dict(pp_perception=2, pp_generation=2, fetch_offset=-2, read_policy="live",
+                                  store_capacity=3)))
+    cases.append(record_case("multi_pipe_33_drop_i12", "pipe", MULTI, 40,
+                             dict(pp_perception=3, pp_generation=3, frame_interval=12.0, overrun_policy="drop")))
+    cases.append(record_case("multi_pipe_33_stretch_i12", "pipe", MULTI, 40,
+                             dict(pp_perception=3, pp_generation=3, frame_interval=12.0)))
+    cases.append(record_case("six_pipe_12_alpha1.5", "pipe", SIX, 20, dict(pp_perception=1, pp_generation=2, alpha=1.5)))
+    cases.append(record_case("noisy16_pipe_14_alpha-0.5", "pipe", NOISY16, 30,
+                             dict(pp_perception=1, pp_generation=4, alpha=-0.5)))
+    errors = []
+    for kw in (dict(pp_perception=1, pp_generation=2, fetch_offset=-2),
+               dict(pp_perception=3, pp_generation=2),
+               dict(pp_perception=1, pp_generation=5),
+               dict(pp_perception=1, pp_generation=2, fetch_offset=1),
+               dict(pp_perception=0, pp_generation=2),
+               dict(pp_perception=1, pp_generation=0),
+               dict(pp_perception=1, pp_generation=2, overrun_policy="skip"),
+               dict(pp_perception=1, pp_generation=2, frame_interval=-1.0),
+               dict(pp_perception=1, pp_generation=2, frame_interval=0.0),
+               dict(pp_perception=1, pp_generation=2, store_capacity=1),
+               dict(pp_perception=1, pp_generation=2, read_policy="bogus"),
+               dict(pp_perception=1, pp_generation=2, fetch_offset=-3, store_capacity=3)):
+        try:
+            run_pipelined(PipelineConfig(**kw), make_conditioning_policy(**SIX), None, 4)
+            errors.append({"pipeline": kw, "error": None})
+        except Exception as e:                       # noqa: BLE001 -- recording the class
+            errors.append({"pipeline": kw, "error": type(e).__name__})
+    return {"cases": cases, "errors": errors}
+
+
 AR = dict(autoregressive=True, layer_costs=(14.0, 14.0), l_a=7, prefill_cost=10.0, decode_cost=1.0)
 
 
@@ -389,6 +440,10 @@ def main():
         json.dump({"generator": "oracle/make_golden.py", "reference": REF_SRC,
                    "numpy": np.__version__, **transformer_goldens()}, fh)
     print("wrote the transformer goldens")
+    with gzip.open(os.path.join(OUT, "edge.json.gz"), "wt") as fh:
+        json.dump({"generator": "oracle/make_golden.py", "reference": REF_SRC,
+                   "numpy": np.__version__, **edge_goldens()}, fh)
+    print("wrote the edge-case goldens")
     ar = autoregressive_cases()
     with gzip.open(os.path.join(OUT, "autoregressive.json.gz"), "wt") as fh:
         json.dump({"generator": "oracle/make_golden.py", "reference": REF_SRC,

@@ -83,3 +83,9 @@ def autoregressive_cases():
 def policy_kwargs(case):
     kw = dict(case["policy"])
     return kw.pop("autoregressive", False), kw
+
+
+def edge_goldens():
+    """Empty / one-frame runs, live reads, drop on overrun, alpha outside
+    [0, 1], and PipelineConfig errors, recorded from the reference."""
+    return load("edge")

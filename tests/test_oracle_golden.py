@@ -152,3 +152,62 @@ def test_token_schema_matches_reference_examples():
     assert np.allclose(toy.decode_action_tokens(toy.encode_action_tokens((5.0, -5.0), 0.8), 0.8), [0.8, -0.8])
     assert toy.encode_action_tokens((0.0, 0.0), 0.8) == (0,) * 7
     assert toy.encode_action_tokens((0.3, 0.3), 0.8, 14)[7:] == toy.encode_action_tokens((0.3, 0.3), 0.8)
+
+
+from golden_util import edge_goldens  # noqa: E402
+
+EDGE = edge_goldens()
+
+
+def _oracle_run(case):
+    ar, kw = policy_kwargs(case)
+    pol = toy.TokenPolicy(**kw) if ar else toy.ToyPolicy(**kw)
+    env = ReplayEnv(case["env"], toy.Obs) if case["env"] else None
+    if case["mode"] == "pipe":
+        return osched.run_pipelined(case["pipeline"], pol, env, case["duration"]), env
+    if case["mode"] == "par":
+        return osched.run_parallel(pol, env, case["workers"], case["duration"], case["seq_interval"],
+                                   case["capacity"]), env
+    if case["mode"] == "dec":
+        return osched.run_decoupled(pol, env, case["duration"], case["seq_interval"]), env
+    return osched.run_sequential(pol, env, case["duration"], case["seq_interval"]), env
+
+
+@pytest.mark.parametrize("case", EDGE["cases"], ids=[c["name"] for c in EDGE["cases"]])
+def test_oracle_edge_cases(case):
+    res, env = _oracle_run(case)
+    assert _jsonify(res.trace) == case["trace"]
+    assert [list(a.values) for a in res.actions] == case["actions"]
+    assert [_jsonify(vars(r)) for r in res.requests] == case["requests"]
+
+
+@pytest.mark.parametrize("case", EDGE["cases"], ids=[c["name"] for c in EDGE["cases"]])
+def test_summarize_edge_cases(case):
+    """summarize on the reference's own traces, incl. EmptyTrace on 0-frame runs."""
+    from paper_2509_09560_b200 import summarize
+    from paper_2509_09560_b200.errors import EmptyTrace
+    if "error" in case["metrics"]:
+        assert case["metrics"]["error"] == "EmptyTrace"
+        with pytest.raises(EmptyTrace):
+            summarize(case["trace"])
+    else:
+        got = json.loads(summarize(case["trace"]).to_json())
+        for k, v in case["metrics"].items():
+            assert got[k] == v, k
+
+
+@pytest.mark.parametrize("err", EDGE["errors"], ids=[str(i) for i in range(len(EDGE["errors"]))])
+def test_config_errors_match_reference(err):
+    """PipelineConfig.validate + the partitioner raise the reference's error
+    class (fp/executor.py:72-92, fp/partition.py); the store-capacity
+    ValueError comes from the device ring and is checked on the GPU."""
+    from paper_2509_09560_b200 import PipelineConfig, errors, make_conditioning_policy, plan_stages
+    if err["pipeline"].get("store_capacity") == 1:
+        pytest.skip("raised by the device ContextStore (tests/test_gpu_edge.py)")
+    pol = make_conditioning_policy(layer_costs=(1.0, 1.0), n_iterations=4, step_cost=1.0)
+    cls = getattr(errors, err["error"])
+    with pytest.raises(cls):
+        cfg = PipelineConfig(**err["pipeline"])
+        cfg.validate(pol)
+        plan_stages(pol.perception.layer_costs, cfg.pp_perception, pol.generation.n_iterations,
+                    cfg.pp_generation, cfg.alpha)
