@@ -218,6 +218,18 @@ def steady_jct_ms(res, t0, K):
     return float(np.percentile(vals, 99)), float(np.mean(vals))
 
 
+def emission_jitter(res, lo, hi):
+    """Population CV of the intervals between action-ready times (device clock)
+    for requests completing in frames [lo, hi): the jitter of fp/metrics.py:81
+    (JITTER_DEFINITION) measured on the GPU."""
+    t = sorted(r.completion_time for r in res.requests
+               if r.completion_frame > 0 and lo <= r.completion_frame - 1 < hi)
+    if len(t) < 3:
+        return None
+    d = np.diff(t)
+    return float(np.std(d) / np.mean(d)) if np.mean(d) > 0 else None
+
+
 # ---------------------------------------------------------------- CPU arms
 
 class _SyntheticImageEnv:
@@ -318,6 +330,7 @@ def baseline_modes(pol, depth, agents, dist):
         jct = [r.jct * 1e3 for r in res.requests if h <= r.completion_frame - 1 < frames]
         out[name] = {"value": dist.world * agents * n / dist.max(span * 1e3) * 1e3 if span > 0 else 0.0,
                      "unit": "actions/s", "workers": depth if name == "par" else 1,
+                     "jitter": emission_jitter(res, h, frames),
                      "mean_staleness_frames": float(np.mean(ages)) if ages else None,
                      "mean_jct_ms": float(np.mean(jct)) if jct else None,
                      "frame_interval_virtual": interval}
@@ -480,6 +493,7 @@ def main():
                       "inputs": f"{n_res} synthetic frames + request noise pre-staged in HBM",
                       "perception_device": args.perception_device},
            "p99_action_latency_ms": p99, "mean_action_latency_ms": jmean,
+           "jitter": emission_jitter(res, t0, t0 + K),
            "mean_staleness_final_frames": float(np.mean(ages)) if ages else None,
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                         "frac": achieved / hbm_peak, "traffic": traffic,
