@@ -149,6 +149,7 @@ int auras_tf_logits(const double *params, int d_model, int vocab, const double *
 #define AURAS_ACT_NONE 0
 #define AURAS_ACT_RELU 1
 #define AURAS_ACT_MISH 2
+#define AURAS_ACT_GELU 3          /* exact erf GELU (ViT MLP)                                */
 
 typedef struct auras_conv_op {
   /* operands (device pointers; element type = plan dtype) */
@@ -254,6 +255,10 @@ int auras_unet_mega_trace(auras_unet_plan *plan, int S, long long *trace, int *t
 int auras_conv(const auras_conv_op *op, int dtype, int S, const float *film_rows,
                int film_stride, float *scratch, int64_t scratch_floats, void *stream);
 
+/* fp32 scratch floats auras_conv needs for this op at batch S (the engine
+ * picks its own split-K factor). */
+int64_t auras_conv_scratch_floats(const auras_conv_op *op, int dtype, int S);
+
 /* Linear / GEMV for N input rows: y[n][m] (fp32, row stride ldy). */
 int auras_linear(const auras_linear_op *op, int dtype, int N, const float *x, int ldx,
                  float *y, int ldy, void *stream);
@@ -264,6 +269,18 @@ int auras_image_to_nhwc(const uint8_t *img, int S, int C, int H, int W, void *ou
                         int dtype, void *stream);
 int auras_maxpool3s2(const void *in, int S, int H, int W, int C, void *out, int dtype,
                      void *stream);
+
+/* ViT-B/16 perception (BASELINE configs[3]): the non-GEMM
+ * parts of a pre-norm block.  Patch embedding and linear layers use auras_conv
+ * (16x16/s16 and 1x1 kernels over the token axis).  Token rows are bf16
+ * [S][N][C]; q|k|v rows [S][N][3C] in timm's (3, heads, dh) order. */
+int auras_vit_tokens(const void *patches, const float *cls, const float *pos, void *x, int S, int N, int C,
+                     void *stream);
+/* Per-row LayerNorm with fp32 statistics; out bf16 (out_f32 = 0) or fp32. */
+int auras_layernorm(const void *in, int64_t ldi, void *out, int64_t ldo, int out_f32, const float *gamma,
+                    const float *beta, int rows, int C, float eps, void *stream);
+/* softmax(q k^T / sqrt(dh)) v for every (image, head); dh <= 64. */
+int auras_vit_attention(const void *qkv, void *out, int S, int N, int heads, int dh, void *stream);
 
 /* Assemble global_cond rows (the ContextStore.publish payload of the DP
  * plugin): for agent a, row = [feat_prev, pos_prev, feat, pos] (n_obs_steps

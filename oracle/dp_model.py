@@ -51,8 +51,38 @@ def _gn(x, w, name, groups):
 
 # ---------------------------------------------------------------- perception
 
+def encode_vit(w, img_u8: np.ndarray, pos) -> torch.Tensor:
+    """ViT-B/16 in timm's layout (BASELINE configs[3] perception; parity
+    unpinned by the reference, which has no vision model): patch conv 16/16,
+    [CLS; patches] + position embedding, 12 pre-norm blocks (LayerNorm eps
+    1e-6, softmax(q k^T / sqrt(dh)) v over 12 heads, exact-GELU MLP), final
+    LayerNorm; feature = the CLS row -> [768 feature, agent_pos]."""
+    x = torch.from_numpy(np.asarray(img_u8)).float()[None] * (2.0 / 255.0) - 1.0
+    D = w["vit.cls"].numel()
+    x = F.conv2d(x, w["vit.patch.w"], w["vit.patch.b"], stride=w["vit.patch.w"].shape[-1])
+    x = x.flatten(2).transpose(1, 2)                                # [1, n, D]
+    x = torch.cat([w["vit.cls"].reshape(1, 1, D), x], dim=1) + w["vit.pos"][None]
+    N = x.shape[1]
+    depth = sum(1 for k in w if k.startswith("vit.b") and k.endswith(".qkv.w"))
+    heads = 12
+    for i in range(depth):
+        p = f"vit.b{i}"
+        a = F.layer_norm(x, (D,), w[p + ".ln1.g"], w[p + ".ln1.b"], eps=1e-6)
+        qkv = F.linear(a, w[p + ".qkv.w"], w[p + ".qkv.b"]).reshape(1, N, 3, heads, D // heads).permute(2, 0, 3, 1, 4)
+        q, k, v = qkv[0], qkv[1], qkv[2]
+        att = torch.softmax((q * (D // heads) ** -0.5) @ k.transpose(-2, -1), dim=-1) @ v
+        x = x + F.linear(att.transpose(1, 2).reshape(1, N, D), w[p + ".proj.w"], w[p + ".proj.b"])
+        a = F.layer_norm(x, (D,), w[p + ".ln2.g"], w[p + ".ln2.b"], eps=1e-6)
+        x = x + F.linear(F.gelu(F.linear(a, w[p + ".fc1.w"], w[p + ".fc1.b"])), w[p + ".fc2.w"], w[p + ".fc2.b"])
+    x = F.layer_norm(x, (D,), w["vit.norm.g"], w["vit.norm.b"], eps=1e-6)
+    return torch.cat([x[0, 0], torch.as_tensor(np.asarray(pos, dtype=np.float32))])
+
+
 def encode(w, img_u8: np.ndarray, pos) -> torch.Tensor:
-    """ResNet-18 with GroupNorm(C/16) and no fc -> [512 feature, agent_pos]."""
+    """ResNet-18 with GroupNorm(C/16) and no fc -> [512 feature, agent_pos]
+    (the ViT-B/16 encoder when the weights hold one)."""
+    if "vit.patch.w" in w:
+        return encode_vit(w, img_u8, pos)
     x = torch.from_numpy(np.asarray(img_u8)).float()[None] * (2.0 / 255.0) - 1.0
     x = F.relu(_gn(F.conv2d(x, w["enc.conv1.w"], stride=2, padding=3), w, "enc.gn1", 4))
     x = F.max_pool2d(x, 3, 2, 1)

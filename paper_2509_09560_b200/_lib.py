@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("AURAS_LIB") or os.path.join(os.path.dirname(os.path.a
 ABI_VERSION = 4
 
 DT_F32, DT_BF16 = 0, 1
-ACT_NONE, ACT_RELU, ACT_MISH = 0, 1, 2
+ACT_NONE, ACT_RELU, ACT_MISH, ACT_GELU = 0, 1, 2, 3
 
 vp = C.c_void_p
 i32, i64, f64 = C.c_int32, C.c_int64, C.c_double
@@ -66,6 +66,10 @@ _SIGNATURES = {
     "auras_ar_generate": (C.c_int, [vp, C.c_int, ip, ip, ip, C.c_int, vp, vp, f64, vp]),
     "auras_ar_finish": (C.c_int, [vp, C.c_int, C.c_int, vp, vp]),
     "auras_ring_copy_slot": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp]),
+    "auras_conv_scratch_floats": (i64, [C.POINTER(ConvOp), C.c_int, C.c_int]),
+    "auras_vit_tokens": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp]),
+    "auras_layernorm": (C.c_int, [vp, i64, vp, i64, C.c_int, vp, vp, C.c_int, C.c_int, C.c_float, vp]),
+    "auras_vit_attention": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp]),
     "auras_tf_param_count": (i64, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
     "auras_tf_forward": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, C.c_int,
                                    vp, vp, vp, vp, vp]),

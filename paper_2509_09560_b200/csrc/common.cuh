@@ -44,6 +44,7 @@ __device__ __forceinline__ float mish(float x) {
 __device__ __forceinline__ float activate(float v, int act) {
   if (act == AURAS_ACT_RELU) return v > 0.f ? v : 0.f;
   if (act == AURAS_ACT_MISH) return mish(v);
+  if (act == AURAS_ACT_GELU) return 0.5f * v * (1.f + erff(v * 0.70710678118654752f));   // exact (erf) GELU
   return v;
 }
 

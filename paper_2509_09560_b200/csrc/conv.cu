@@ -349,6 +349,10 @@ int64_t conv_scratch_floats(const auras_conv_op &op, int S, int dtype) {
 
 using namespace auras;
 
+extern "C" int64_t auras_conv_scratch_floats(const auras_conv_op *op, int dtype, int S) {
+  return op ? conv_scratch_floats(*op, S, dtype) : -1;
+}
+
 extern "C" {
 
 int auras_conv(const auras_conv_op *op, int dtype, int S, const float *film_rows, int film_stride,

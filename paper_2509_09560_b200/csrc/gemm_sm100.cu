@@ -62,6 +62,7 @@ bool gemm_sm100_supported(const ConvGemmArgs &g) {
   if (g.Cin % TC_BK || g.Kp % TC_BK || g.Kp < g.Kreal) return false;
   if (g.stride < 1 || g.stride > 2 || g.W % g.stride) return false;
   if (g.Wo > 256 || g.Wo < 1) return false;
+  if (g.Wo % 4) return false;                               // epilogue stores 4 positions at a time
   if (g.in_pitch % 8 || g.in_coff % 8) return false;
   if ((reinterpret_cast<uintptr_t>(g.w) & 15) || (reinterpret_cast<uintptr_t>(g.in) & 15)) return false;
   return true;

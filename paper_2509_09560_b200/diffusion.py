@@ -69,6 +69,11 @@ class DPConfig:
     scheduler: str = "ddpm"         # "ddpm" | "ddim"
     clip_sample: bool = True
     max_action: float = 1.0
+    encoder: str = "resnet18"       # "resnet18" | "vit_b16"
+    vit_depth: int = 12
+    vit_heads: int = 12
+    vit_mlp: int = 3072
+    vit_patch: int = 16
 
     @property
     def gc_dim(self) -> int:
@@ -87,6 +92,11 @@ PRESETS = {
     "pusht": DPConfig(name="pusht"),
     # DP default UNet widths (256, 512, 1024)
     "dp_default": DPConfig(name="dp_default", down_dims=(256, 512, 1024), dsed=256),
+    # BASELINE configs[3], perception half: ViT-B/16 at 224x224, 7-DoF actions, bf16;
+    # the denoiser is the DP-default ConditionalUnet1D (the DP-T transformer
+    # denoiser of that config is not built yet)
+    "vit": DPConfig(name="vit", encoder="vit_b16", image_hw=224, feat_dim=768, action_dim=7,
+                    down_dims=(256, 512, 1024), dsed=256),
 }
 
 
@@ -146,6 +156,41 @@ def init_weights(cfg: DPConfig, seed: int = 0, device="cpu") -> dict:
         w[name + ".g"] = 1.0 + 0.1 * uni((c,), 1.0)
         w[name + ".b"] = 0.1 * uni((c,), 1.0)
 
+    if cfg.encoder == "vit_b16":
+        _vit_weights(cfg, w, conv, uni, g, device)
+    else:
+        _resnet_weights(cfg, w, conv, gn)
+    _unet_weights(cfg, w, conv, gn)
+    return w
+
+
+def _vit_weights(cfg, w, conv, uni, g, device):
+    """ViT-B/16 (timm layout): patch conv, CLS token, position embedding
+    (N(0, 0.02)), pre-norm blocks (LayerNorm gamma 1 + 0.1 U, beta 0.1 U),
+    final LayerNorm."""
+    import torch
+    D, P = cfg.feat_dim, cfg.vit_patch
+    n_tok = (cfg.image_hw // P) ** 2 + 1
+    conv("vit.patch", D, cfg.image_channels, P, P)
+    w["vit.cls"] = torch.randn((D,), generator=g, device=device) * 0.02
+    w["vit.pos"] = torch.randn((n_tok, D), generator=g, device=device) * 0.02
+
+    def ln(name):
+        w[name + ".g"] = 1.0 + 0.1 * uni((D,), 1.0)
+        w[name + ".b"] = 0.1 * uni((D,), 1.0)
+
+    for i in range(cfg.vit_depth):
+        p = f"vit.b{i}"
+        ln(p + ".ln1")
+        conv(p + ".qkv", 3 * D, D)
+        conv(p + ".proj", D, D)
+        ln(p + ".ln2")
+        conv(p + ".fc1", cfg.vit_mlp, D)
+        conv(p + ".fc2", D, cfg.vit_mlp)
+    ln("vit.norm")
+
+
+def _resnet_weights(cfg, w, conv, gn):
     # ResNet-18-GN
     conv("enc.conv1", 64, cfg.image_channels, 7, 7, bias=False)
     gn("enc.gn1", 64)
@@ -162,7 +207,9 @@ def init_weights(cfg: DPConfig, seed: int = 0, device="cpu") -> dict:
                 conv(p + ".ds", c, cin, 1, 1, bias=False)
                 gn(p + ".dsgn", c)
         cin = c
-    # UNet
+
+
+def _unet_weights(cfg, w, conv, gn):
     d = cfg.dsed
     conv("unet.temb.l1", 4 * d, d)
     conv("unet.temb.l2", d, 4 * d)
@@ -188,7 +235,6 @@ def init_weights(cfg: DPConfig, seed: int = 0, device="cpu") -> dict:
     conv("unet.final.c", c0, c0, k)
     gn("unet.final.g", c0)
     conv("unet.final.out", cfg.action_dim, c0, 1)
-    return w
 
 
 # ---------------------------------------------------------------- scheduler tables
@@ -250,7 +296,15 @@ def synthetic_frame(cfg: DPConfig, seed_base: int, agent: int, frame: int) -> Ob
 
 
 def encoder_flops(cfg: DPConfig):
-    """MACs*2 per encoder layer group [stem, layer1..4] at one frame."""
+    """MACs*2 per encoder layer group at one frame: [stem, layer1..4] for
+    ResNet-18; [patch embedding, blocks 0-2, 3-5, 6-8, 9-11] for ViT-B/16."""
+    if cfg.encoder == "vit_b16":
+        D, F = cfg.feat_dim, cfg.vit_mlp
+        n = (cfg.image_hw // cfg.vit_patch) ** 2
+        N = n + 1
+        block = 2 * N * D * (3 * D + D + 2 * F) + 2 * 2 * N * N * D
+        per = cfg.vit_depth // 4
+        return [2 * n * D * cfg.image_channels * cfg.vit_patch ** 2] + [per * block] * 4
     hw = cfg.image_hw // 2
     groups = [2 * 64 * cfg.image_channels * 49 * hw * hw]
     hw //= 2
@@ -464,6 +518,119 @@ class Encoder:
                     _, src, h, wd, c, dst = item
                     _lib.check(lib.auras_maxpool3s2(src.data_ptr(), self.A, h, wd, c, dst.data_ptr(),
                                                     self.m.dt, st), "maxpool")
+
+
+class ViTEncoder:
+    """ViT-B/16 program for A frames at a time (BASELINE configs[3]; SURVEY.md
+    §2.4 K7), same interface as Encoder.  Patch embedding and every linear
+    layer are tcgen05 implicit-GEMM conv ops (16x16/s16 over the image, 1x1
+    over the token axis) with bias / GELU / residual in the epilogue;
+    LayerNorm, token assembly and attention are the vit.cu kernels.  The
+    residual stream is bf16 [A][197][768] ping-ponged between two buffers.
+    Groups (perception stages): patch embedding, then blocks in four thirds."""
+
+    GROUPS = ("embed", "blocks0", "blocks1", "blocks2", "blocks3")
+
+    def __init__(self, model: DeviceModel, A: int):
+        torch = model.torch
+        cfg = model.cfg
+        if model.dt != _lib.DT_BF16:
+            raise ConfigInvalid("the ViT-B/16 encoder runs in bf16 only")
+        self.m, self.A = model, A
+        dev, td = model.dev, model.tdtype
+        H, P, D = cfg.image_hw, cfg.vit_patch, cfg.feat_dim
+        g = H // P
+        self.n_tok = N = g * g + 1
+        self.heads = cfg.vit_heads
+        self.img = torch.zeros(A, cfg.image_channels, H, H, dtype=torch.uint8, device=dev)
+        self.x0 = torch.zeros(A, H, H, 8, dtype=td, device=dev)
+        self.feat = torch.zeros(A, D, dtype=torch.float32, device=dev)
+        self.patches = torch.zeros(A, g, g, D, dtype=td, device=dev)
+        self.xa = torch.zeros(A, N, D, dtype=td, device=dev)
+        self.xb = torch.zeros(A, N, D, dtype=td, device=dev)
+        self.ln = torch.zeros(A, N, D, dtype=td, device=dev)
+        self.qkv = torch.zeros(A, N, 3 * D, dtype=td, device=dev)
+        self.att = torch.zeros(A, N, D, dtype=td, device=dev)
+        self.hid = torch.zeros(A, N, cfg.vit_mlp, dtype=td, device=dev)
+        self.groups = {gname: [] for gname in self.GROUPS}
+        self.max_scratch = 0
+        w = model.w
+        self.cls = model.f32(w["vit.cls"])
+        self.pos = model.f32(w["vit.pos"])
+        wm, cp, kh, kw, kp = model.conv_weight(w["vit.patch.w"], cin_pad=8)
+        self._conv("embed", wm, model.f32(w["vit.patch.b"]), self.x0, 8, H, H, cp, kh, kw, P,
+                   self.patches, D, g, g)
+        self.groups["embed"].append(("tokens",))
+        per = cfg.vit_depth // 4
+        for i in range(cfg.vit_depth):
+            gname = f"blocks{min(i // per, 3)}"
+            p = f"vit.b{i}"
+            lin = lambda name: model.conv_weight(w[name + ".w"].reshape(*w[name + ".w"].shape, 1, 1))  # noqa: E731
+            self.groups[gname].append(("ln", self.xa, self.ln, model.f32(w[p + ".ln1.g"]),
+                                       model.f32(w[p + ".ln1.b"])))
+            wm, cp, _, _, _ = lin(p + ".qkv")
+            self._conv(gname, wm, model.f32(w[p + ".qkv.b"]), self.ln, D, 1, N, cp, 1, 1, 1, self.qkv, 3 * D, 1, N)
+            self.groups[gname].append(("attn",))
+            wm, cp, _, _, _ = lin(p + ".proj")
+            self._conv(gname, wm, model.f32(w[p + ".proj.b"]), self.att, D, 1, N, cp, 1, 1, 1, self.xb, D, 1, N,
+                       res=self.xa)
+            self.groups[gname].append(("ln", self.xb, self.ln, model.f32(w[p + ".ln2.g"]),
+                                       model.f32(w[p + ".ln2.b"])))
+            wm, cp, _, _, _ = lin(p + ".fc1")
+            self._conv(gname, wm, model.f32(w[p + ".fc1.b"]), self.ln, D, 1, N, cp, 1, 1, 1, self.hid, cfg.vit_mlp,
+                       1, N, act=_lib.ACT_GELU)
+            wm, cp, _, _, _ = lin(p + ".fc2")
+            self._conv(gname, wm, model.f32(w[p + ".fc2.b"]), self.hid, cfg.vit_mlp, 1, N, cp, 1, 1, 1, self.xa,
+                       D, 1, N, res=self.xb)
+        self.norm = (model.f32(w["vit.norm.g"]), model.f32(w["vit.norm.b"]))
+        self.groups["blocks3"].append(("final",))
+        self.scratch = torch.zeros(max(1, self.max_scratch), dtype=torch.float32, device=dev)
+
+    def _conv(self, group, wm, bias, inp, in_pitch, H, W, cin, kh, kw, stride, out, out_pitch, Ho, Wo,
+              act=0, res=None):
+        M, kp = wm.shape
+        N = self.A * Ho * Wo
+        op = _op(w=wm.data_ptr(), bias=bias.data_ptr(), inp=inp.data_ptr(), out=out.data_ptr(), M=M, Cin=cin,
+                 Kp=kp, H=H, W=W, in_pitch=in_pitch, in_coff=0, kh=kh, kw=kw, stride=stride, pad_h=0, pad_w=0,
+                 Ho=Ho, Wo=Wo, out_pitch=out_pitch, out_coff=0, act=act, res_before_act=0,
+                 splits=_splits(M, N, kp))
+        if res is not None:
+            op.res, op.res_pitch, op.res_coff = res.data_ptr(), out_pitch, 0
+        need = _lib.load().auras_conv_scratch_floats(_lib.C.byref(op), self.m.dt, self.A)
+        self.max_scratch = max(self.max_scratch, int(need))
+        self.groups[group].append(("conv", op))
+
+    def run(self, lo, hi, stream):
+        lib = _lib.load()
+        st = stream.cuda_stream
+        cfg = self.m.cfg
+        D, N = cfg.feat_dim, self.n_tok
+        for gi in range(lo, hi):
+            gname = self.GROUPS[gi]
+            if gi == 0:
+                _lib.check(lib.auras_image_to_nhwc(self.img.data_ptr(), self.A, cfg.image_channels,
+                                                   cfg.image_hw, cfg.image_hw, self.x0.data_ptr(),
+                                                   8, self.m.dt, st), "image_to_nhwc")
+            for item in self.groups[gname]:
+                kind = item[0]
+                if kind == "conv":
+                    _lib.check(lib.auras_conv(_lib.C.byref(item[1]), self.m.dt, self.A, None, 0,
+                                              self.scratch.data_ptr(), self.scratch.numel(), st), "vit conv")
+                elif kind == "tokens":
+                    _lib.check(lib.auras_vit_tokens(self.patches.data_ptr(), self.cls.data_ptr(),
+                                                    self.pos.data_ptr(), self.xa.data_ptr(), self.A, N, D, st),
+                               "vit_tokens")
+                elif kind == "ln":
+                    _, src, dst, gam, bet = item
+                    _lib.check(lib.auras_layernorm(src.data_ptr(), D, dst.data_ptr(), D, 0, gam.data_ptr(),
+                                                   bet.data_ptr(), self.A * N, D, 1e-6, st), "layernorm")
+                elif kind == "attn":
+                    _lib.check(lib.auras_vit_attention(self.qkv.data_ptr(), self.att.data_ptr(), self.A, N,
+                                                       self.heads, D // self.heads, st), "vit_attention")
+                else:                                     # final LayerNorm of the CLS rows -> feat (fp32)
+                    _lib.check(lib.auras_layernorm(self.xa.data_ptr(), N * D, self.feat.data_ptr(), D, 1,
+                                                   self.norm[0].data_ptr(), self.norm[1].data_ptr(), self.A, D,
+                                                   1e-6, st), "layernorm")
 
 
 class Denoiser:
@@ -759,7 +926,7 @@ class DPSession:
         self.store = ContextStore(capacity, slot_elems=self.slot_floats, agents=agents,
                                   dtype=torch.float32, device=dev)
         with torch.cuda.device(self.pd):
-            self.encoder = Encoder(self.pmodel, agents)
+            self.encoder = (ViTEncoder if cfg.encoder == "vit_b16" else Encoder)(self.pmodel, agents)
         s_max = agents * max(1, lanes)
         s_max = min(s_max, 64)
         self.denoiser = Denoiser(self.model, s_max, self.store, self.gc_pad, gen.use_graph)
