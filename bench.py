@@ -456,7 +456,7 @@ def main():
         prof = json.load(open(os.path.join(ROOT, "profiles", "r1_ncu_unet_cluster.json")))
         dk = LAST_EVENTS.get("denoise_kernel") or {}
         kern = dk.get(S_med) or dk.get(str(S_med)) or ""
-        if f"S{S_med}" in prof and "cluster" in kern:
+        if f"S{S_med}" in prof and "cluster" in kern and args.config == prof.get("config", "pusht"):
             p_s = prof[f"S{S_med}"]
             traffic = p_s["dram_read_bytes"] + p_s["dram_write_bytes"]
     except (OSError, ValueError, KeyError):
@@ -481,10 +481,12 @@ def main():
     out = {"metric": METRIC, "value": value, "unit": "actions/s", "n_gpus": dist.world,
            "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-           "config": {"workload": f"configs[1]: Diffusion Policy CNN ({cfg.name}: ResNet-18-GN "
+           "config": {"workload": f"{'configs[3] (perception half)' if cfg.encoder == 'vit_b16' else 'configs[1]'}: "
+                                  f"Diffusion Policy ({cfg.name}: "
+                                  f"{'ViT-B/16' if cfg.encoder == 'vit_b16' else 'ResNet-18-GN'} "
                                   f"encoder, UNet {list(cfg.down_dims)}, {cfg.num_inference_steps}-step "
                                   f"{cfg.scheduler.upper()}, horizon {cfg.horizon}, action dim "
-                                  f"{cfg.action_dim}, 96x96 frames) on 1 B200 per rank",
+                                  f"{cfg.action_dim}, {cfg.image_hw}x{cfg.image_hw} frames) on 1 B200 per rank",
                       "model": f"dp-cnn-{cfg.name}", "depth": args.depth,
                       "pp": [1, args.depth], "fetch_offset": args.offset, "alpha": 0.0,
                       "agents_per_gpu": A, "global_batch": A * dist.world,

@@ -175,7 +175,8 @@ typedef struct auras_conv_op {
   int32_t out_stuff;      /* 1: write out row 2*ox and a zero row 2*ox+1 (1-D only)  */
   int32_t pool_out;       /* 1: store mean over Ho*Wo as out[s][m] (fp32, out_f32)    */
   int32_t splits;         /* split-K factor chosen by the planner                    */
-  int32_t reserved[3];
+  int32_t cta_target;     /* gathered-im2col engine: CTAs to aim for (0 = 32)        */
+  int32_t reserved[2];
 } auras_conv_op;
 
 /* Linear / GEMV: y[n][m] = sum_k W[m][k] * f(x[n][k]) + b[m], f = Mish or id. */

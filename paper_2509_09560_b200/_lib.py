@@ -35,7 +35,7 @@ class ConvOp(C.Structure):
         ("Ho", i32), ("Wo", i32), ("out_pitch", i32), ("out_coff", i32),
         ("res_pitch", i32), ("res_coff", i32),
         ("groups", i32), ("act", i32), ("res_before_act", i32), ("film_off", i32),
-        ("out_stuff", i32), ("pool_out", i32), ("splits", i32), ("reserved", i32 * 3),
+        ("out_stuff", i32), ("pool_out", i32), ("splits", i32), ("cta_target", i32), ("reserved", i32 * 2),
     ]
 
 

@@ -116,6 +116,40 @@ int launch_conv_epilogue(const EpiArgs &a, int S, cudaStream_t st) {
   return AURAS_OK;
 }
 
+// Token-wise epilogue for 1-row convolutions without GroupNorm / FiLM / pooling
+// (the ViT linear layers, op.cta_target > 0): the split-K partials are
+// [split][m][n] and the output rows [n][pitch], so a 32 x 32 tile is summed
+// with n-contiguous reads, transposed through shared memory and stored with
+// m-contiguous writes.  bias -> act -> + residual, as epi_unit.
+template <typename T>
+__global__ void __launch_bounds__(256) tok_epilogue(EpiArgs a) {
+  __shared__ float tile[32][33];
+  const int m0 = blockIdx.x * 32, n0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t NM = (int64_t)a.N * a.M;
+  for (int i = ty; i < 32; i += 8) {
+    const int m = m0 + i, n = n0 + tx;
+    float v = 0.f;
+    if (m < a.M && n < a.N) {
+      v = a.bias ? a.bias[m] : 0.f;
+      for (int z = 0; z < a.splits; ++z) v += a.partial[z * NM + (int64_t)m * a.N + n];
+      v = activate(v, a.act);
+    }
+    tile[i][tx] = v;
+  }
+  __syncthreads();
+  const T *res = static_cast<const T *>(a.res);
+  T *out = static_cast<T *>(a.out);
+  for (int i = ty; i < 32; i += 8) {
+    const int n = n0 + i, m = m0 + tx;
+    if (m < a.M && n < a.N) {
+      float v = tile[tx][i];
+      if (res) v += Elem<T>::load(res + (int64_t)n * a.res_pitch + a.res_coff + m);
+      Elem<T>::store(out + (int64_t)n * a.out_pitch + a.out_coff + m, v);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ linear / GEMV
 // y[n][m] = sum_k W[m][k] * f(x[n][k]) + b[m]; one warp per output row m,
 // x staged in shared memory; weights streamed once with 16-byte loads.
@@ -302,7 +336,7 @@ int conv_op_to_args(const auras_conv_op &op, int S, int dtype, float *partial, C
   g.M = op.M; g.N = S * op.Ho * op.Wo; g.Kp = op.Kp; g.Kreal = op.kh * op.kw * op.Cin;
   g.Cin = op.Cin; g.H = op.H; g.W = op.W; g.in_pitch = op.in_pitch; g.in_coff = op.in_coff;
   g.kh = op.kh; g.kw = op.kw; g.stride = op.stride; g.pad_h = op.pad_h; g.pad_w = op.pad_w;
-  g.Ho = op.Ho; g.Wo = op.Wo; g.splits = op.splits;
+  g.Ho = op.Ho; g.Wo = op.Wo; g.splits = op.splits; g.cta_target = op.cta_target;
   if (dtype == AURAS_DT_BF16 && gemm_sm100_supported(g)) {
     g.engine = 1;
     g.splits = gemm_sm100_splits(g);
@@ -370,6 +404,14 @@ int auras_conv(const auras_conv_op *op, int dtype, int S, const float *film_rows
   }
   cudaStream_t st = as_stream(stream);
   if ((rc = run_gemm(g, dtype, st))) return rc;
+  if (op->cta_target > 0 && !e.gn_gamma && !e.pool_out && e.film_off < 0 && !e.out_stuff && !e.out_f32 &&
+      !e.res_f32 && op->Ho == 1 && e.out) {
+    dim3 grid((e.M + 31) / 32, (e.N + 31) / 32);
+    if (dtype == AURAS_DT_BF16) tok_epilogue<__nv_bfloat16><<<grid, 256, 0, st>>>(e);
+    else tok_epilogue<float><<<grid, 256, 0, st>>>(e);
+    AURAS_LAUNCHED("tok_epilogue");
+    return AURAS_OK;
+  }
   return run_epilogue(e, S, dtype, st);
 }
 

@@ -14,6 +14,7 @@ struct ConvGemmArgs {
   int Ho, Wo;
   int splits, kchunk;
   int engine;         // 0 SIMT, 1 tcgen05 + TMA im2col (1-D), 2 tcgen05 + gathered im2col
+  int cta_target;     // engine 2: CTAs to aim for (0: a 32-CTA slice of the GPU)
 };
 
 struct EpiArgs {

@@ -42,8 +42,10 @@ static GatherPlan gather_plan(const ConvGemmArgs &g) {
   p.m_tiles = (g.M + GG_BM - 1) / GG_BM;
   p.n_tiles = (g.N + GG_BN - 1) / GG_BN;
   p.kb_total = g.Kp / GG_BK;
-  // enough CTAs to occupy a slice of the GPU, but keep >= 4 k-blocks per CTA
-  int want = std::max(1, 32 / (p.m_tiles * p.n_tiles));
+  // enough CTAs to occupy a slice of the GPU (or the op's cta_target when the
+  // caller runs it alone), but keep >= 4 k-blocks per CTA
+  const int target = g.cta_target > 0 ? g.cta_target : 32;
+  int want = std::max(1, target / (p.m_tiles * p.n_tiles));
   want = std::min(want, std::max(1, p.kb_total / 4));
   p.kb_per_split = (p.kb_total + want - 1) / want;
   p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;

@@ -71,7 +71,7 @@ __global__ void layernorm_kernel(const __nv_bfloat16 *__restrict__ in, int64_t l
 }
 
 constexpr int ATT_THREADS = 256;
-constexpr int ATT_QB = 32;          // queries per CTA
+constexpr int ATT_QB = 8;           // queries per CTA: one per warp, many CTAs
 
 // grid (S * heads, ceil(N / ATT_QB)); dh <= 64 (two head columns per lane).
 __global__ void __launch_bounds__(ATT_THREADS) vit_attention_kernel(const __nv_bfloat16 *__restrict__ qkv,

@@ -569,36 +569,49 @@ class ViTEncoder:
             self.groups[gname].append(("ln", self.xa, self.ln, model.f32(w[p + ".ln1.g"]),
                                        model.f32(w[p + ".ln1.b"])))
             wm, cp, _, _, _ = lin(p + ".qkv")
-            self._conv(gname, wm, model.f32(w[p + ".qkv.b"]), self.ln, D, 1, N, cp, 1, 1, 1, self.qkv, 3 * D, 1, N)
+            self._tok(gname, wm, model.f32(w[p + ".qkv.b"]), self.ln, D, cp, self.qkv, 3 * D)
             self.groups[gname].append(("attn",))
             wm, cp, _, _, _ = lin(p + ".proj")
-            self._conv(gname, wm, model.f32(w[p + ".proj.b"]), self.att, D, 1, N, cp, 1, 1, 1, self.xb, D, 1, N,
-                       res=self.xa)
+            self._tok(gname, wm, model.f32(w[p + ".proj.b"]), self.att, D, cp, self.xb, D, res=self.xa)
             self.groups[gname].append(("ln", self.xb, self.ln, model.f32(w[p + ".ln2.g"]),
                                        model.f32(w[p + ".ln2.b"])))
             wm, cp, _, _, _ = lin(p + ".fc1")
-            self._conv(gname, wm, model.f32(w[p + ".fc1.b"]), self.ln, D, 1, N, cp, 1, 1, 1, self.hid, cfg.vit_mlp,
-                       1, N, act=_lib.ACT_GELU)
+            self._tok(gname, wm, model.f32(w[p + ".fc1.b"]), self.ln, D, cp, self.hid, cfg.vit_mlp,
+                      act=_lib.ACT_GELU)
             wm, cp, _, _, _ = lin(p + ".fc2")
-            self._conv(gname, wm, model.f32(w[p + ".fc2.b"]), self.hid, cfg.vit_mlp, 1, N, cp, 1, 1, 1, self.xa,
-                       D, 1, N, res=self.xb)
+            self._tok(gname, wm, model.f32(w[p + ".fc2.b"]), self.hid, cfg.vit_mlp, cp, self.xa, D, res=self.xb)
         self.norm = (model.f32(w["vit.norm.g"]), model.f32(w["vit.norm.b"]))
         self.groups["blocks3"].append(("final",))
         self.scratch = torch.zeros(max(1, self.max_scratch), dtype=torch.float32, device=dev)
 
+    def _tok(self, group, wm, bias, inp, in_pitch, cin, out, out_pitch, act=0, res=None):
+        """A token-wise linear layer: every token is a 1x1 'image' (S = A * N),
+        so the GEMM's N and the epilogue grid span all tokens, and the
+        gathered-im2col engine may spread over the whole GPU (perception runs
+        alone while the denoise kernel is not resident)."""
+        import os
+        if os.environ.get("AURAS_VIT_TOKROWS") == "1":
+            self._conv(group, wm, bias, inp, in_pitch, 1, 1, cin, 1, 1, 1, out, out_pitch, 1, 1, act=act, res=res,
+                       S=self.A * self.n_tok, cta_target=int(os.environ.get("AURAS_VIT_CTAS", "148")))
+        else:
+            N = self.n_tok
+            self._conv(group, wm, bias, inp, in_pitch, 1, N, cin, 1, 1, 1, out, out_pitch, 1, N, act=act, res=res,
+                       cta_target=int(os.environ.get("AURAS_VIT_CTAS", "148")))
+
     def _conv(self, group, wm, bias, inp, in_pitch, H, W, cin, kh, kw, stride, out, out_pitch, Ho, Wo,
-              act=0, res=None):
+              act=0, res=None, S=None, cta_target=0):
         M, kp = wm.shape
-        N = self.A * Ho * Wo
+        S = self.A if S is None else S
+        N = S * Ho * Wo
         op = _op(w=wm.data_ptr(), bias=bias.data_ptr(), inp=inp.data_ptr(), out=out.data_ptr(), M=M, Cin=cin,
                  Kp=kp, H=H, W=W, in_pitch=in_pitch, in_coff=0, kh=kh, kw=kw, stride=stride, pad_h=0, pad_w=0,
                  Ho=Ho, Wo=Wo, out_pitch=out_pitch, out_coff=0, act=act, res_before_act=0,
-                 splits=_splits(M, N, kp))
+                 splits=_splits(M, N, kp), cta_target=cta_target)
         if res is not None:
             op.res, op.res_pitch, op.res_coff = res.data_ptr(), out_pitch, 0
-        need = _lib.load().auras_conv_scratch_floats(_lib.C.byref(op), self.m.dt, self.A)
+        need = _lib.load().auras_conv_scratch_floats(_lib.C.byref(op), self.m.dt, S)
         self.max_scratch = max(self.max_scratch, int(need))
-        self.groups[group].append(("conv", op))
+        self.groups[group].append(("conv", op, S))
 
     def run(self, lo, hi, stream):
         lib = _lib.load()
@@ -614,7 +627,7 @@ class ViTEncoder:
             for item in self.groups[gname]:
                 kind = item[0]
                 if kind == "conv":
-                    _lib.check(lib.auras_conv(_lib.C.byref(item[1]), self.m.dt, self.A, None, 0,
+                    _lib.check(lib.auras_conv(_lib.C.byref(item[1]), self.m.dt, item[2], None, 0,
                                               self.scratch.data_ptr(), self.scratch.numel(), st), "vit conv")
                 elif kind == "tokens":
                     _lib.check(lib.auras_vit_tokens(self.patches.data_ptr(), self.cls.data_ptr(),
