@@ -132,7 +132,13 @@ __global__ void __launch_bounds__(256) tok_epilogue(EpiArgs a) {
     float v = 0.f;
     if (m < a.M && n < a.N) {
       v = a.bias ? a.bias[m] : 0.f;
-      for (int z = 0; z < a.splits; ++z) v += a.partial[z * NM + (int64_t)m * a.N + n];
+      const float *pp = a.partial + (int64_t)m * a.N + n;
+      int z = 0;
+      for (; z + 4 <= a.splits; z += 4) {          // four split loads in flight
+        const float t0 = pp[z * NM], t1 = pp[(z + 1) * NM], t2 = pp[(z + 2) * NM], t3 = pp[(z + 3) * NM];
+        v += (t0 + t1) + (t2 + t3);
+      }
+      for (; z < a.splits; ++z) v += pp[z * NM];
       v = activate(v, a.act);
     }
     tile[i][tx] = v;

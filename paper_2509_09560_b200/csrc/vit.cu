@@ -46,6 +46,8 @@ __global__ void vit_tokens_kernel(const __nv_bfloat16 *__restrict__ patches, con
 }
 
 // One warp per row: two-pass mean / biased variance in fp32 (torch's LayerNorm).
+// Rows up to 32 * LN_MAXV elements stay in registers after one read.
+constexpr int LN_MAXV = 32;
 template <typename TO>
 __global__ void layernorm_kernel(const __nv_bfloat16 *__restrict__ in, int64_t ldi, TO *__restrict__ out,
                                  int64_t ldo, const float *__restrict__ g, const float *__restrict__ b, int rows,
@@ -53,20 +55,32 @@ __global__ void layernorm_kernel(const __nv_bfloat16 *__restrict__ in, int64_t l
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= rows) return;
   const __nv_bfloat16 *xr = in + warp * ldi;
+  float xv[LN_MAXV];
   float s = 0.f;
-  for (int c = lane; c < C; c += 32) s += __bfloat162float(xr[c]);
+#pragma unroll
+  for (int u = 0; u < LN_MAXV; ++u) {
+    const int c = lane + 32 * u;
+    xv[u] = c < C ? __bfloat162float(xr[c]) : 0.f;
+    s += xv[u];
+  }
   const float mu = warp_sum_f(s) / C;
   float q = 0.f;
-  for (int c = lane; c < C; c += 32) {
-    const float d = __bfloat162float(xr[c]) - mu;
+#pragma unroll
+  for (int u = 0; u < LN_MAXV; ++u) {
+    const int c = lane + 32 * u;
+    const float d = c < C ? xv[u] - mu : 0.f;
     q += d * d;
   }
   const float rstd = rsqrtf(warp_sum_f(q) / C + eps);
   TO *yr = out + warp * ldo;
-  for (int c = lane; c < C; c += 32) {
-    const float v = (__bfloat162float(xr[c]) - mu) * rstd * g[c] + b[c];
-    if constexpr (sizeof(TO) == 4) yr[c] = v;
-    else yr[c] = __float2bfloat16_rn(v);
+#pragma unroll
+  for (int u = 0; u < LN_MAXV; ++u) {
+    const int c = lane + 32 * u;
+    if (c < C) {
+      const float v = (xv[u] - mu) * rstd * g[c] + b[c];
+      if constexpr (sizeof(TO) == 4) yr[c] = v;
+      else yr[c] = __float2bfloat16_rn(v);
+    }
   }
 }
 
@@ -86,10 +100,44 @@ __global__ void __launch_bounds__(ATT_THREADS) vit_attention_kernel(const __nv_b
   float *qs = ps + (ATT_THREADS / 32) * N;        // [warps][dh]
   const int s = blockIdx.x / H, h = blockIdx.x % H;
   const __nv_bfloat16 *base = qkv + (int64_t)s * N * 3 * C;
-  for (int i = threadIdx.x; i < N * dh; i += ATT_THREADS) {
-    const int n = i / dh, e = i % dh;
-    ks[n * kp + e] = __bfloat162float(base[(int64_t)n * 3 * C + C + h * dh + e]);
-    vs[n * dh + e] = __bfloat162float(base[(int64_t)n * 3 * C + 2 * C + h * dh + e]);
+  if ((dh & 7) == 0) {
+    // 16-byte loads, 4 rows' worth in flight per thread: an L2 round trip is
+    // long enough here that a scalar loop over 2 x 12.6 K elements costs tens of us
+    const int cpr = dh >> 3;                      // 8-element chunks per row
+    const int total = N * cpr;
+    for (int i0 = threadIdx.x; i0 < total; i0 += 4 * ATT_THREADS) {
+      uint4 kq[4], vq[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * ATT_THREADS;
+        if (i < total) {
+          const int n = i / cpr, j = i % cpr;
+          const __nv_bfloat16 *row = base + (int64_t)n * 3 * C + h * dh + 8 * j;
+          kq[u] = *reinterpret_cast<const uint4 *>(row + C);
+          vq[u] = *reinterpret_cast<const uint4 *>(row + 2 * C);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * ATT_THREADS;
+        if (i < total) {
+          const int n = i / cpr, j = i % cpr;
+          const __nv_bfloat16 *kb = reinterpret_cast<const __nv_bfloat16 *>(&kq[u]);
+          const __nv_bfloat16 *vb = reinterpret_cast<const __nv_bfloat16 *>(&vq[u]);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            ks[n * kp + 8 * j + t] = __bfloat162float(kb[t]);
+            vs[n * dh + 8 * j + t] = __bfloat162float(vb[t]);
+          }
+        }
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < N * dh; i += ATT_THREADS) {
+      const int n = i / dh, e = i % dh;
+      ks[n * kp + e] = __bfloat162float(base[(int64_t)n * 3 * C + C + h * dh + e]);
+      vs[n * dh + e] = __bfloat162float(base[(int64_t)n * 3 * C + 2 * C + h * dh + e]);
+    }
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -148,8 +196,8 @@ extern "C" int auras_vit_tokens(const void *patches, const float *cls, const flo
 
 extern "C" int auras_layernorm(const void *in, int64_t ldi, void *out, int64_t ldo, int out_f32, const float *gamma,
                                const float *beta, int rows, int C, float eps, void *stream) {
-  if (rows < 1 || C < 1) {
-    set_error("layernorm: bad sizes rows=%d C=%d", rows, C);
+  if (rows < 1 || C < 1 || C > 32 * LN_MAXV) {
+    set_error("layernorm: bad sizes rows=%d C=%d (C <= %d)", rows, C, 32 * LN_MAXV);
     return AURAS_E_ARG;
   }
   const int grid = (rows * 32 + 255) / 256;

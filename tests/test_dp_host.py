@@ -97,3 +97,17 @@ def test_oracle_unet_runs_and_is_deterministic():
     e1 = dp_model.unet_eps(w, cfg, x, 42, gc)
     e2 = dp_model.unet_eps(w, cfg, x, 42, gc)
     assert e1.shape == (16, 2) and torch.isfinite(e1).all() and torch.equal(e1, e2)
+
+
+def test_vit_preset_matches_survey_sizes():
+    """configs[3] perception: ViT-B/16 at 224x224 is 85.8 M parameters and
+    about 35.1 GFLOP per frame."""
+    from paper_2509_09560_b200 import diffusion as D
+    cfg = D.PRESETS["vit"]
+    w = D.init_weights(cfg, 0)
+    n_vit = sum(v.numel() for k, v in w.items() if k.startswith("vit."))
+    assert abs(n_vit / 1e6 - 85.8) < 0.1
+    assert abs(sum(D.encoder_flops(cfg)) / 1e9 - 35.1) < 0.1
+    assert cfg.action_dim == 7 and cfg.image_hw == 224 and cfg.feat_dim == 768
+    assert len(D.encoder_flops(cfg)) == len(D.ViTEncoder.GROUPS)
+    assert not any(k.startswith("enc.") for k in w)          # no ResNet weights in this preset
