@@ -274,14 +274,16 @@ int auras_maxpool3s2(const void *in, int S, int H, int W, int C, void *out, int 
 /* ViT-B/16 perception (BASELINE configs[3]): the non-GEMM
  * parts of a pre-norm block.  Patch embedding and linear layers use auras_conv
  * (16x16/s16 and 1x1 kernels over the token axis).  Token rows are bf16
- * [S][N][C]; q|k|v rows [S][N][3C] in timm's (3, heads, dh) order. */
-int auras_vit_tokens(const void *patches, const float *cls, const float *pos, void *x, int S, int N, int C,
-                     void *stream);
+ * [S][N][C] (rows n_valid..N-1 of an image are zero padding); q|k|v rows
+ * [S][N][3C] in timm's (3, heads, dh) order. */
+int auras_vit_tokens(const void *patches, const float *cls, const float *pos, void *x, int S, int N, int n_valid,
+                     int C, void *stream);
 /* Per-row LayerNorm with fp32 statistics; out bf16 (out_f32 = 0) or fp32. */
 int auras_layernorm(const void *in, int64_t ldi, void *out, int64_t ldo, int out_f32, const float *gamma,
                     const float *beta, int rows, int C, float eps, void *stream);
-/* softmax(q k^T / sqrt(dh)) v for every (image, head); dh <= 64. */
-int auras_vit_attention(const void *qkv, void *out, int S, int N, int heads, int dh, void *stream);
+/* softmax(q k^T / sqrt(dh)) v for every (image, head) over the first n_valid
+ * of N token rows (the rest are padding); dh <= 64. */
+int auras_vit_attention(const void *qkv, void *out, int S, int N, int n_valid, int heads, int dh, void *stream);
 
 /* Assemble global_cond rows (the ContextStore.publish payload of the DP
  * plugin): for agent a, row = [feat_prev, pos_prev, feat, pos] (n_obs_steps

@@ -67,9 +67,9 @@ _SIGNATURES = {
     "auras_ar_finish": (C.c_int, [vp, C.c_int, C.c_int, vp, vp]),
     "auras_ring_copy_slot": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp]),
     "auras_conv_scratch_floats": (i64, [C.POINTER(ConvOp), C.c_int, C.c_int]),
-    "auras_vit_tokens": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp]),
+    "auras_vit_tokens": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp]),
     "auras_layernorm": (C.c_int, [vp, i64, vp, i64, C.c_int, vp, vp, C.c_int, C.c_int, C.c_float, vp]),
-    "auras_vit_attention": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp]),
+    "auras_vit_attention": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp]),
     "auras_tf_param_count": (i64, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
     "auras_tf_forward": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, C.c_int,
                                    vp, vp, vp, vp, vp]),

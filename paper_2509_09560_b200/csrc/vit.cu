@@ -32,7 +32,7 @@ __device__ __forceinline__ float warp_max_f(float v) {
 
 __global__ void vit_tokens_kernel(const __nv_bfloat16 *__restrict__ patches, const float *__restrict__ cls,
                                   const float *__restrict__ pos, __nv_bfloat16 *__restrict__ x, int S, int N,
-                                  int C) {
+                                  int nv, int C) {
   const int64_t total = (int64_t)S * N * C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -40,7 +40,11 @@ __global__ void vit_tokens_kernel(const __nv_bfloat16 *__restrict__ patches, con
     const int64_t r = i / C;
     const int n = (int)(r % N);
     const int64_t s = r / N;
-    const float v = n == 0 ? cls[c] : __bfloat162float(patches[(s * (N - 1) + (n - 1)) * C + c]);
+    if (n >= nv) {                                 // pad row
+      x[i] = __float2bfloat16_rn(0.f);
+      continue;
+    }
+    const float v = n == 0 ? cls[c] : __bfloat162float(patches[(s * (nv - 1) + (n - 1)) * C + c]);
     x[i] = __float2bfloat16_rn(v + pos[(int64_t)n * C + c]);
   }
 }
@@ -90,7 +94,7 @@ constexpr int ATT_QB = 8;           // queries per CTA: one per warp, many CTAs
 // grid (S * heads, ceil(N / ATT_QB)); dh <= 64 (two head columns per lane).
 __global__ void __launch_bounds__(ATT_THREADS) vit_attention_kernel(const __nv_bfloat16 *__restrict__ qkv,
                                                                     __nv_bfloat16 *__restrict__ out, int N,
-                                                                    int H, int dh, float scale) {
+                                                                    int nv, int H, int dh, float scale) {
   extern __shared__ float sm[];
   const int C = H * dh;
   const int kp = dh + 1;                          // padded row pitch (floats): conflict-free key reads
@@ -145,11 +149,11 @@ __global__ void __launch_bounds__(ATT_THREADS) vit_attention_kernel(const __nv_b
   float *q = qs + warp * dh;
   for (int qi = warp; qi < ATT_QB; qi += ATT_THREADS / 32) {
     const int n = blockIdx.y * ATT_QB + qi;
-    if (n >= N) break;                            // warp-uniform
+    if (n >= nv) break;                           // warp-uniform; pad rows are not queries
     for (int e = lane; e < dh; e += 32) q[e] = __bfloat162float(base[(int64_t)n * 3 * C + h * dh + e]) * scale;
     __syncwarp();
     float mx = -INFINITY;
-    for (int k = lane; k < N; k += 32) {
+    for (int k = lane; k < nv; k += 32) {
       const float *kr = ks + k * kp;
       float a = 0.f;
       for (int e = 0; e < dh; ++e) a = fmaf(q[e], kr[e], a);
@@ -158,7 +162,7 @@ __global__ void __launch_bounds__(ATT_THREADS) vit_attention_kernel(const __nv_b
     }
     mx = warp_max_f(mx);
     float sum = 0.f;
-    for (int k = lane; k < N; k += 32) {
+    for (int k = lane; k < nv; k += 32) {
       const float e = __expf(p[k] - mx);
       p[k] = e;
       sum += e;
@@ -168,7 +172,7 @@ __global__ void __launch_bounds__(ATT_THREADS) vit_attention_kernel(const __nv_b
     __syncwarp();
     for (int e = lane; e < dh; e += 32) {
       float a = 0.f;
-      for (int k = 0; k < N; ++k) a = fmaf(p[k], vs[k * dh + e], a);
+      for (int k = 0; k < nv; ++k) a = fmaf(p[k], vs[k * dh + e], a);
       out[((int64_t)s * N + n) * C + h * dh + e] = __float2bfloat16_rn(a * inv);
     }
     __syncwarp();
@@ -181,15 +185,15 @@ __global__ void __launch_bounds__(ATT_THREADS) vit_attention_kernel(const __nv_b
 using namespace auras;
 
 extern "C" int auras_vit_tokens(const void *patches, const float *cls, const float *pos, void *x, int S, int N,
-                                int C, void *stream) {
-  if (S < 1 || N < 2 || C < 1) {
+                                int n_valid, int C, void *stream) {
+  if (S < 1 || n_valid < 2 || N < n_valid || C < 1) {
     set_error("vit_tokens: bad sizes S=%d N=%d C=%d", S, N, C);
     return AURAS_E_ARG;
   }
   const int64_t total = (int64_t)S * N * C;
   const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
   vit_tokens_kernel<<<grid, 256, 0, as_stream(stream)>>>(static_cast<const __nv_bfloat16 *>(patches), cls, pos,
-                                                         static_cast<__nv_bfloat16 *>(x), S, N, C);
+                                                         static_cast<__nv_bfloat16 *>(x), S, N, n_valid, C);
   AURAS_LAUNCHED("vit_tokens");
   return AURAS_OK;
 }
@@ -212,8 +216,9 @@ extern "C" int auras_layernorm(const void *in, int64_t ldi, void *out, int64_t l
   return AURAS_OK;
 }
 
-extern "C" int auras_vit_attention(const void *qkv, void *out, int S, int N, int heads, int dh, void *stream) {
-  if (S < 1 || N < 1 || heads < 1 || dh < 1 || dh > 64) {
+extern "C" int auras_vit_attention(const void *qkv, void *out, int S, int N, int n_valid, int heads, int dh,
+                                   void *stream) {
+  if (S < 1 || n_valid < 1 || N < n_valid || heads < 1 || dh < 1 || dh > 64) {
     set_error("vit_attention: bad sizes S=%d N=%d heads=%d dh=%d", S, N, heads, dh);
     return AURAS_E_ARG;
   }
@@ -228,9 +233,9 @@ extern "C" int auras_vit_attention(const void *qkv, void *out, int S, int N, int
     AURAS_CUDA(cudaFuncSetAttribute(vit_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = smem;
   }
-  dim3 grid(S * heads, (N + ATT_QB - 1) / ATT_QB);
+  dim3 grid(S * heads, (n_valid + ATT_QB - 1) / ATT_QB);
   vit_attention_kernel<<<grid, ATT_THREADS, smem, as_stream(stream)>>>(
-      static_cast<const __nv_bfloat16 *>(qkv), static_cast<__nv_bfloat16 *>(out), N, heads, dh,
+      static_cast<const __nv_bfloat16 *>(qkv), static_cast<__nv_bfloat16 *>(out), N, n_valid, heads, dh,
       1.f / sqrtf((float)dh));
   AURAS_LAUNCHED("vit_attention");
   return AURAS_OK;

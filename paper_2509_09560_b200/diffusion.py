@@ -540,7 +540,11 @@ class ViTEncoder:
         dev, td = model.dev, model.tdtype
         H, P, D = cfg.image_hw, cfg.vit_patch, cfg.feat_dim
         g = H // P
-        self.n_tok = N = g * g + 1
+        self.n_valid = g * g + 1
+        # token rows padded to a multiple of 8 (env AURAS_VIT_PAD=0 keeps 197):
+        # pad rows are zero at entry, never attended to, never read back
+        import os
+        self.n_tok = N = _round(self.n_valid, 8) if os.environ.get("AURAS_VIT_PAD", "1") == "1" else self.n_valid
         self.heads = cfg.vit_heads
         self.img = torch.zeros(A, cfg.image_channels, H, H, dtype=torch.uint8, device=dev)
         self.x0 = torch.zeros(A, H, H, 8, dtype=td, device=dev)
@@ -585,18 +589,14 @@ class ViTEncoder:
         self.scratch = torch.zeros(max(1, self.max_scratch), dtype=torch.float32, device=dev)
 
     def _tok(self, group, wm, bias, inp, in_pitch, cin, out, out_pitch, act=0, res=None):
-        """A token-wise linear layer: every token is a 1x1 'image' (S = A * N),
-        so the GEMM's N and the epilogue grid span all tokens, and the
-        gathered-im2col engine may spread over the whole GPU (perception runs
-        alone while the denoise kernel is not resident)."""
-        import os
-        if os.environ.get("AURAS_VIT_TOKROWS") == "1":
-            self._conv(group, wm, bias, inp, in_pitch, 1, 1, cin, 1, 1, 1, out, out_pitch, 1, 1, act=act, res=res,
-                       S=self.A * self.n_tok, cta_target=int(os.environ.get("AURAS_VIT_CTAS", "148")))
-        else:
-            N = self.n_tok
-            self._conv(group, wm, bias, inp, in_pitch, 1, N, cin, 1, 1, 1, out, out_pitch, 1, N, act=act, res=res,
-                       cta_target=int(os.environ.get("AURAS_VIT_CTAS", "148")))
+        """A token-wise linear layer as a 1-row convolution over the (padded)
+        token axis: with N a multiple of 8 it takes the TMA 1-D tcgen05 path;
+        the epilogue is the token-wise transposing one (cta_target > 0), which
+        also lets the gathered-im2col engine spread over the whole GPU
+        (perception runs alone while the denoise kernel is not resident)."""
+        N = self.n_tok
+        self._conv(group, wm, bias, inp, in_pitch, 1, N, cin, 1, 1, 1, out, out_pitch, 1, N, act=act, res=res,
+                   cta_target=148)
 
     def _conv(self, group, wm, bias, inp, in_pitch, H, W, cin, kh, kw, stride, out, out_pitch, Ho, Wo,
               act=0, res=None, S=None, cta_target=0):
@@ -631,15 +631,16 @@ class ViTEncoder:
                                               self.scratch.data_ptr(), self.scratch.numel(), st), "vit conv")
                 elif kind == "tokens":
                     _lib.check(lib.auras_vit_tokens(self.patches.data_ptr(), self.cls.data_ptr(),
-                                                    self.pos.data_ptr(), self.xa.data_ptr(), self.A, N, D, st),
-                               "vit_tokens")
+                                                    self.pos.data_ptr(), self.xa.data_ptr(), self.A, N,
+                                                    self.n_valid, D, st), "vit_tokens")
                 elif kind == "ln":
                     _, src, dst, gam, bet = item
                     _lib.check(lib.auras_layernorm(src.data_ptr(), D, dst.data_ptr(), D, 0, gam.data_ptr(),
                                                    bet.data_ptr(), self.A * N, D, 1e-6, st), "layernorm")
                 elif kind == "attn":
                     _lib.check(lib.auras_vit_attention(self.qkv.data_ptr(), self.att.data_ptr(), self.A, N,
-                                                       self.heads, D // self.heads, st), "vit_attention")
+                                                       self.n_valid, self.heads, D // self.heads, st),
+                               "vit_attention")
                 else:                                     # final LayerNorm of the CLS rows -> feat (fp32)
                     _lib.check(lib.auras_layernorm(self.xa.data_ptr(), N * D, self.feat.data_ptr(), D, 1,
                                                    self.norm[0].data_ptr(), self.norm[1].data_ptr(), self.A, D,

@@ -48,13 +48,29 @@ def test_layernorm_kernel():
     assert (o32 - ref).abs().max().item() <= 1e-4
 
 
+def test_attention_ignores_pad_rows():
+    """Rows n_valid..N-1 are padding: neither keys nor queries."""
+    lib = _lib.load()
+    S, N, nv, H, dh = 2, 200, 197, 12, 64
+    C = H * dh
+    qkv = torch.randn(S, N, 3 * C, device="cuda").to(torch.bfloat16)
+    out = torch.zeros(S, N, C, device="cuda", dtype=torch.bfloat16)
+    _lib.check(lib.auras_vit_attention(qkv.data_ptr(), out.data_ptr(), S, N, nv, H, dh,
+                                       torch.cuda.current_stream().cuda_stream), "attn")
+    q, k, v = qkv[:, :nv].float().reshape(S, nv, 3, H, dh).permute(2, 0, 3, 1, 4)
+    ref = (torch.softmax((q * dh ** -0.5) @ k.transpose(-2, -1), dim=-1) @ v).transpose(1, 2).reshape(S, nv, C)
+    torch.cuda.synchronize()
+    assert (out[:, :nv].float() - ref).abs().max().item() <= 2e-2
+    assert out[:, nv:].abs().max().item() == 0
+
+
 @pytest.mark.parametrize("S,N,H,dh", [(2, 197, 12, 64), (3, 50, 4, 32), (1, 7, 2, 16)])
 def test_attention_kernel(S, N, H, dh):
     lib = _lib.load()
     C = H * dh
     qkv = torch.randn(S, N, 3 * C, device="cuda").to(torch.bfloat16)
     out = torch.empty(S, N, C, device="cuda", dtype=torch.bfloat16)
-    _lib.check(lib.auras_vit_attention(qkv.data_ptr(), out.data_ptr(), S, N, H, dh,
+    _lib.check(lib.auras_vit_attention(qkv.data_ptr(), out.data_ptr(), S, N, N, H, dh,
                                        torch.cuda.current_stream().cuda_stream), "attn")
     q, k, v = qkv.float().reshape(S, N, 3, H, dh).permute(2, 0, 3, 1, 4)
     ref = (torch.softmax((q * dh ** -0.5) @ k.transpose(-2, -1), dim=-1) @ v).transpose(1, 2).reshape(S, N, C)
@@ -69,7 +85,8 @@ def test_tokens_kernel():
     cls = torch.randn(C, device="cuda")
     pos = torch.randn(n + 1, C, device="cuda")
     x = torch.empty(S, n + 1, C, device="cuda", dtype=torch.bfloat16)
-    _lib.check(lib.auras_vit_tokens(patches.data_ptr(), cls.data_ptr(), pos.data_ptr(), x.data_ptr(), S, n + 1, C,
+    _lib.check(lib.auras_vit_tokens(patches.data_ptr(), cls.data_ptr(), pos.data_ptr(), x.data_ptr(), S, n + 1, n + 1,
+                                    C,
                                     torch.cuda.current_stream().cuda_stream), "tokens")
     ref = torch.cat([cls.expand(S, 1, C), patches.float()], dim=1) + pos
     torch.cuda.synchronize()
