@@ -53,7 +53,9 @@ def _gn(x, w, name, groups):
 
 def encode_vit(w, img_u8: np.ndarray, pos) -> torch.Tensor:
     """ViT-B/16 in timm's layout (BASELINE configs[3] perception; parity
-    unpinned by the reference, which has no vision model): patch conv 16/16,
+    unpinned by the reference, which has no vision model; the block wiring is
+    pinned against torch's nn.TransformerEncoderLayer in
+    tests/test_dp_host.py): patch conv 16/16,
     [CLS; patches] + position embedding, 12 pre-norm blocks (LayerNorm eps
     1e-6, softmax(q k^T / sqrt(dh)) v over 12 heads, exact-GELU MLP), final
     LayerNorm; feature = the CLS row -> [768 feature, agent_pos]."""

@@ -111,3 +111,39 @@ def test_vit_preset_matches_survey_sizes():
     assert cfg.action_dim == 7 and cfg.image_hw == 224 and cfg.feat_dim == 768
     assert len(D.encoder_flops(cfg)) == len(D.ViTEncoder.GROUPS)
     assert not any(k.startswith("enc.") for k in w)          # no ResNet weights in this preset
+
+
+def test_oracle_vit_matches_torch_transformer_layers():
+    """Pins the ViT-B/16 restatement (oracle/dp_model.py encode_vit) against
+    torch's own pre-norm nn.TransformerEncoderLayer (exact GELU, LayerNorm
+    eps 1e-6, fused in_proj in q|k|v order = timm's qkv layout) loaded with
+    the same weights, on a 2-block, 112x112 variant to keep it fast."""
+    import numpy as np
+    import torch
+    from oracle import dp_model
+    from paper_2509_09560_b200 import diffusion as D
+    cfg = D.DPConfig(name="vit_small_test", encoder="vit_b16", image_hw=112, feat_dim=768, vit_depth=2)
+    w = D.init_weights(cfg, 1)
+    img = np.random.default_rng(0).integers(0, 256, (3, 112, 112), dtype=np.uint8)
+    got = dp_model.encode_vit(w, img, np.zeros(2))[:768]
+    x = torch.from_numpy(img).float()[None] * (2.0 / 255.0) - 1.0
+    x = torch.nn.functional.conv2d(x, w["vit.patch.w"], w["vit.patch.b"], stride=16).flatten(2).transpose(1, 2)
+    x = torch.cat([w["vit.cls"].reshape(1, 1, 768), x], dim=1) + w["vit.pos"][None]
+    for i in range(2):
+        p = f"vit.b{i}"
+        layer = torch.nn.TransformerEncoderLayer(768, 12, 3072, dropout=0.0, activation="gelu", layer_norm_eps=1e-6,
+                                                 batch_first=True, norm_first=True)
+        with torch.no_grad():
+            layer.self_attn.in_proj_weight.copy_(w[p + ".qkv.w"])
+            layer.self_attn.in_proj_bias.copy_(w[p + ".qkv.b"])
+            layer.self_attn.out_proj.weight.copy_(w[p + ".proj.w"])
+            layer.self_attn.out_proj.bias.copy_(w[p + ".proj.b"])
+            layer.norm1.weight.copy_(w[p + ".ln1.g"]), layer.norm1.bias.copy_(w[p + ".ln1.b"])
+            layer.norm2.weight.copy_(w[p + ".ln2.g"]), layer.norm2.bias.copy_(w[p + ".ln2.b"])
+            layer.linear1.weight.copy_(w[p + ".fc1.w"]), layer.linear1.bias.copy_(w[p + ".fc1.b"])
+            layer.linear2.weight.copy_(w[p + ".fc2.w"]), layer.linear2.bias.copy_(w[p + ".fc2.b"])
+        layer.eval()
+        with torch.no_grad():
+            x = layer(x)
+    want = torch.nn.functional.layer_norm(x, (768,), w["vit.norm.g"], w["vit.norm.b"], eps=1e-6)[0, 0]
+    assert torch.allclose(got, want, atol=1e-4, rtol=1e-4), float((got - want).abs().max())
