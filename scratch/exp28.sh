@@ -1,0 +1,3 @@
+#!/bin/bash
+AURAS_MEGA_KERNEL=cluster timeout 300 python scratch/step_time.py 8 pusht trace > gpurun_out/exp28_8.log 2>&1
+python scratch/headtail.py gpurun_out/ctrace_8.json gpurun_out/kbtrace_8.npy >> gpurun_out/exp28_8.log 2>&1

@@ -5,12 +5,12 @@ __global__ void k(int *p) { if (p) p[blockIdx.x] = 1; }
 int main() {
   cudaDeviceProp pr; cudaGetDeviceProperties(&pr, 0);
   printf("SMs %d\n", pr.multiProcessorCount);
-  for (int smem : {100 * 1024, 200 * 1024, 231 * 1024}) {
+  for (int smem : {200 * 1024, 224 * 1024}) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    for (int cs : {1, 2, 4, 8, 16}) {
+    for (int cs : {4, 6, 7, 8}) {
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(cs * 16); cfg.blockDim = dim3(384); cfg.dynamicSmemBytes = smem;
+      cfg.gridDim = dim3(cs * 16); cfg.blockDim = dim3(512); cfg.dynamicSmemBytes = smem;
       cudaLaunchAttribute a; a.id = cudaLaunchAttributeClusterDimension; a.val.clusterDim.x = cs; a.val.clusterDim.y = 1; a.val.clusterDim.z = 1;
       cfg.attrs = &a; cfg.numAttrs = 1;
       int n = -1; cudaError_t e = cudaOccupancyMaxActiveClusters(&n, k, &cfg);
