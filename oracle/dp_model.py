@@ -151,6 +151,56 @@ def unet_eps(w, cfg, x: torch.Tensor, timestep: int, gc: torch.Tensor) -> torch.
     return h[0].T
 
 
+def _mha(q_in, kv_in, w_in, b_in, w_out, b_out, heads, mask):
+    """nn.MultiheadAttention's math: packed q|k|v in-projection, scaled dot
+    product per head, additive -inf mask, out-projection."""
+    E = q_in.shape[-1]
+    q = F.linear(q_in, w_in[:E], b_in[:E])
+    k = F.linear(kv_in, w_in[E:2 * E], b_in[E:2 * E])
+    v = F.linear(kv_in, w_in[2 * E:], b_in[2 * E:])
+    dh = E // heads
+    q = q.reshape(-1, heads, dh).transpose(0, 1)
+    k = k.reshape(-1, heads, dh).transpose(0, 1)
+    v = v.reshape(-1, heads, dh).transpose(0, 1)
+    att = torch.softmax(q @ k.transpose(-2, -1) / math.sqrt(dh) + mask, dim=-1) @ v
+    return F.linear(att.transpose(0, 1).reshape(-1, E), w_out, b_out)
+
+
+def dpt_masks(T: int, t_cond: int):
+    """TransformerForDiffusion's masks: causal self-attention; action t sees
+    cond token s (time token first) iff t >= s - 1."""
+    causal = torch.full((T, T), float("-inf")).triu(1)
+    t, s_ = torch.meshgrid(torch.arange(T), torch.arange(t_cond), indexing="ij")
+    mem = torch.zeros(T, t_cond).masked_fill(~(t >= s_ - 1), float("-inf"))
+    return causal, mem
+
+
+def dpt_eps(w, cfg, x: torch.Tensor, timestep: int, gc: torch.Tensor) -> torch.Tensor:
+    """Diffusion Policy's TransformerForDiffusion (time_as_cond, obs_as_cond,
+    causal_attn, n_cond_layers = 0) in eval mode: x (horizon, action_dim) ->
+    eps.  Parity unpinned by the reference (no network there); the layer
+    wiring is pinned against torch's nn.TransformerDecoderLayer in
+    tests/test_dp_host.py."""
+    E, H, L = cfg.dpt_emb, cfg.dpt_heads, cfg.dpt_layers
+    n_obs = cfg.n_obs_steps
+    temb = _sinusoidal(timestep, E)                                      # [1, E]
+    cond = F.linear(gc.reshape(n_obs, -1), w["dpt.cond_obs.w"], w["dpt.cond_obs.b"])
+    c = torch.cat([temb, cond], dim=0) + w["dpt.cond_pos"]
+    mem = F.linear(_mish(F.linear(c, w["dpt.enc1.w"], w["dpt.enc1.b"])), w["dpt.enc2.w"], w["dpt.enc2.b"])
+    h = F.linear(x, w["dpt.input.w"], w["dpt.input.b"]) + w["dpt.pos"]
+    causal, mmask = dpt_masks(x.shape[0], 1 + n_obs)
+    for l in range(L):
+        p = f"dpt.l{l}"
+        a = F.layer_norm(h, (E,), w[p + ".ln1.g"], w[p + ".ln1.b"])
+        h = h + _mha(a, a, w[p + ".sa_in.w"], w[p + ".sa_in.b"], w[p + ".sa_out.w"], w[p + ".sa_out.b"], H, causal)
+        a = F.layer_norm(h, (E,), w[p + ".ln2.g"], w[p + ".ln2.b"])
+        h = h + _mha(a, mem, w[p + ".ca_in.w"], w[p + ".ca_in.b"], w[p + ".ca_out.w"], w[p + ".ca_out.b"], H, mmask)
+        a = F.layer_norm(h, (E,), w[p + ".ln3.g"], w[p + ".ln3.b"])
+        h = h + F.linear(F.gelu(F.linear(a, w[p + ".ff1.w"], w[p + ".ff1.b"])), w[p + ".ff2.w"], w[p + ".ff2.b"])
+    h = F.layer_norm(h, (E,), w["dpt.lnf.g"], w["dpt.lnf.b"])
+    return F.linear(h, w["dpt.head.w"], w["dpt.head.b"])
+
+
 # ---------------------------------------------------------------- scheduler
 
 class Scheduler:
@@ -283,7 +333,8 @@ class OracleGeneration:
     def step(self, state, ctx):
         i = state.steps
         with torch.no_grad():
-            eps = unet_eps(self.w, self.cfg, state.x, self.sched.timesteps[i], ctx.payload)
+            fn = dpt_eps if "dpt.input.w" in self.w else unet_eps
+            eps = fn(self.w, self.cfg, state.x, self.sched.timesteps[i], ctx.payload)
             x = self.sched.step(i, state.x, eps, None if state.z is None else state.z[i])
         return State(x, state.z, i + 1)
 

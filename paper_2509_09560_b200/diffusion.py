@@ -70,6 +70,10 @@ class DPConfig:
     clip_sample: bool = True
     max_action: float = 1.0
     encoder: str = "resnet18"       # "resnet18" | "vit_b16"
+    denoiser: str = "unet"          # "unet" (ConditionalUnet1D) | "transformer" (DP-T)
+    dpt_layers: int = 8
+    dpt_heads: int = 4
+    dpt_emb: int = 256
     vit_depth: int = 12
     vit_heads: int = 12
     vit_mlp: int = 3072
@@ -160,7 +164,10 @@ def init_weights(cfg: DPConfig, seed: int = 0, device="cpu") -> dict:
         _vit_weights(cfg, w, conv, uni, g, device)
     else:
         _resnet_weights(cfg, w, conv, gn)
-    _unet_weights(cfg, w, conv, gn)
+    if cfg.denoiser == "transformer":
+        _dpt_weights(cfg, w, conv, uni, g, device)
+    else:
+        _unet_weights(cfg, w, conv, gn)
     return w
 
 
@@ -188,6 +195,40 @@ def _vit_weights(cfg, w, conv, uni, g, device):
         conv(p + ".fc1", cfg.vit_mlp, D)
         conv(p + ".fc2", D, cfg.vit_mlp)
     ln("vit.norm")
+
+
+def _dpt_weights(cfg, w, conv, uni, g, device):
+    """Diffusion Policy's TransformerForDiffusion (obs and time as cond tokens,
+    causal attention, MLP cond encoder): input / cond-obs embeddings, position
+    embeddings N(0, 0.02), dpt_layers pre-norm decoder layers (self-attention,
+    cross-attention to the cond tokens, GELU MLP), final LayerNorm and head."""
+    import torch
+    E, T = cfg.dpt_emb, cfg.horizon
+    t_cond = 1 + cfg.n_obs_steps
+    conv("dpt.input", E, cfg.action_dim)
+    w["dpt.pos"] = torch.randn((T, E), generator=g, device=device) * 0.02
+    conv("dpt.cond_obs", E, cfg.feat_dim + cfg.agent_pos_dim)
+    w["dpt.cond_pos"] = torch.randn((t_cond, E), generator=g, device=device) * 0.02
+    conv("dpt.enc1", 4 * E, E)
+    conv("dpt.enc2", E, 4 * E)
+
+    def ln(name):
+        w[name + ".g"] = 1.0 + 0.1 * uni((E,), 1.0)
+        w[name + ".b"] = 0.1 * uni((E,), 1.0)
+
+    for l in range(cfg.dpt_layers):
+        p = f"dpt.l{l}"
+        ln(p + ".ln1")
+        conv(p + ".sa_in", 3 * E, E)
+        conv(p + ".sa_out", E, E)
+        ln(p + ".ln2")
+        conv(p + ".ca_in", 3 * E, E)
+        conv(p + ".ca_out", E, E)
+        ln(p + ".ln3")
+        conv(p + ".ff1", 4 * E, E)
+        conv(p + ".ff2", E, 4 * E)
+    ln("dpt.lnf")
+    conv("dpt.head", cfg.action_dim, E)
 
 
 def _resnet_weights(cfg, w, conv, gn):

@@ -147,3 +147,51 @@ def test_oracle_vit_matches_torch_transformer_layers():
             x = layer(x)
     want = torch.nn.functional.layer_norm(x, (768,), w["vit.norm.g"], w["vit.norm.b"], eps=1e-6)[0, 0]
     assert torch.allclose(got, want, atol=1e-4, rtol=1e-4), float((got - want).abs().max())
+
+
+def test_oracle_dpt_matches_torch_decoder_layers():
+    """Pins the DP-T denoiser restatement (oracle/dp_model.py dpt_eps) against
+    torch's nn.TransformerDecoderLayer (pre-norm, GELU, batch_first) with the
+    same weights and DP's causal / memory masks."""
+    import numpy as np
+    import torch
+    from oracle import dp_model
+    from paper_2509_09560_b200 import diffusion as D
+    cfg = D.DPConfig(name="dpt_test", encoder="vit_b16", image_hw=32, feat_dim=768, action_dim=7,
+                     denoiser="transformer", dpt_layers=2, vit_depth=1)
+    w = D.init_weights(cfg, 2)
+    rng = np.random.default_rng(0)
+    x = torch.from_numpy(rng.standard_normal((16, 7)).astype(np.float32))
+    gc = torch.from_numpy(rng.standard_normal(cfg.gc_dim).astype(np.float32))
+    got = dp_model.dpt_eps(w, cfg, x, 37, gc)
+    E = cfg.dpt_emb
+    temb = dp_model._sinusoidal(37, E)
+    cond = torch.nn.functional.linear(gc.reshape(2, -1), w["dpt.cond_obs.w"], w["dpt.cond_obs.b"])
+    c = torch.cat([temb, cond]) + w["dpt.cond_pos"]
+    mem = torch.nn.functional.linear(torch.nn.functional.mish(torch.nn.functional.linear(c, w["dpt.enc1.w"],
+                                                                                          w["dpt.enc1.b"])),
+                                     w["dpt.enc2.w"], w["dpt.enc2.b"])[None]
+    h = (torch.nn.functional.linear(x, w["dpt.input.w"], w["dpt.input.b"]) + w["dpt.pos"])[None]
+    causal, mmask = dp_model.dpt_masks(16, 3)
+    for l in range(2):
+        p = f"dpt.l{l}"
+        layer = torch.nn.TransformerDecoderLayer(E, 4, 4 * E, dropout=0.0, activation="gelu", batch_first=True,
+                                                 norm_first=True)
+        with torch.no_grad():
+            layer.self_attn.in_proj_weight.copy_(w[p + ".sa_in.w"]), layer.self_attn.in_proj_bias.copy_(w[p + ".sa_in.b"])
+            layer.self_attn.out_proj.weight.copy_(w[p + ".sa_out.w"]), layer.self_attn.out_proj.bias.copy_(w[p + ".sa_out.b"])
+            layer.multihead_attn.in_proj_weight.copy_(w[p + ".ca_in.w"])
+            layer.multihead_attn.in_proj_bias.copy_(w[p + ".ca_in.b"])
+            layer.multihead_attn.out_proj.weight.copy_(w[p + ".ca_out.w"])
+            layer.multihead_attn.out_proj.bias.copy_(w[p + ".ca_out.b"])
+            for i in (1, 2, 3):
+                getattr(layer, f"norm{i}").weight.copy_(w[p + f".ln{i}.g"])
+                getattr(layer, f"norm{i}").bias.copy_(w[p + f".ln{i}.b"])
+            layer.linear1.weight.copy_(w[p + ".ff1.w"]), layer.linear1.bias.copy_(w[p + ".ff1.b"])
+            layer.linear2.weight.copy_(w[p + ".ff2.w"]), layer.linear2.bias.copy_(w[p + ".ff2.b"])
+        layer.eval()
+        with torch.no_grad():
+            h = layer(h, mem, tgt_mask=causal, memory_mask=mmask)
+    h = torch.nn.functional.layer_norm(h[0], (E,), w["dpt.lnf.g"], w["dpt.lnf.b"])
+    want = torch.nn.functional.linear(h, w["dpt.head.w"], w["dpt.head.b"])
+    assert torch.allclose(got, want, atol=1e-4, rtol=1e-4), float((got - want).abs().max())
