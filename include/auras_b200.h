@@ -285,6 +285,22 @@ int auras_layernorm(const void *in, int64_t ldi, void *out, int64_t ldo, int out
  * of N token rows (the rest are padding); dh <= 64. */
 int auras_vit_attention(const void *qkv, void *out, int S, int N, int n_valid, int heads, int dh, void *stream);
 
+/* DP-T denoiser (TransformerForDiffusion; BASELINE configs[3]): the pieces
+ * around the conv-path GEMMs.  Samples are (agent, lane, inference step);
+ * x lanes / noise lanes / scheduler tables as for the UNet plan. */
+int auras_dpt_prep(const int *agents, const int *lanes, const int *steps, int S, const float *x_lanes,
+                   int lanes_per_agent, int horizon, int adim, void *xin, const float *ring,
+                   int64_t ring_agent_stride, int slot_floats, const int64_t *fetched, int tok_w, int n_obs,
+                   void *gcbuf, int gpad, const float *temb, int E, void *c, const float *cond_pos, void *stream);
+int auras_dpt_cond(const void *cobs, void *c, const float *cond_pos, int S, int n_obs, int E, void *stream);
+/* softmax(q k^T / sqrt(dh) + mask) v, key j visible to query n iff
+ * j <= n + mask_off; rows (s * Nq + n) * ld + head * dh; Nk <= 32. */
+int auras_attention(const void *q, int ldq, const void *k, int ldk, const void *v, int ldv, void *out, int ldo,
+                    int S, int Nq, int Nk, int heads, int dh, int mask_off, void *stream);
+int auras_dpt_update(const float *eps, int eps_pitch, const int *agents, const int *lanes, const int *steps, int S,
+                     float *x_lanes, const float *noise_lanes, int lanes_per_agent, int horizon, int adim,
+                     const auras_sched *sched, void *stream);
+
 /* Assemble global_cond rows (the ContextStore.publish payload of the DP
  * plugin): for agent a, row = [feat_prev, pos_prev, feat, pos] (n_obs_steps
  * = 2) or [feat, pos] (1); feat_prev/pos_prev are the agent's previous

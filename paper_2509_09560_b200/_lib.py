@@ -67,6 +67,13 @@ _SIGNATURES = {
     "auras_ar_finish": (C.c_int, [vp, C.c_int, C.c_int, vp, vp]),
     "auras_ring_copy_slot": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp]),
     "auras_conv_scratch_floats": (i64, [C.POINTER(ConvOp), C.c_int, C.c_int]),
+    "auras_dpt_prep": (C.c_int, [vp, vp, vp, C.c_int, vp, C.c_int, C.c_int, C.c_int, vp, vp, i64, C.c_int, vp,
+                                 C.c_int, C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, vp]),
+    "auras_dpt_cond": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, vp]),
+    "auras_attention": (C.c_int, [vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, C.c_int, C.c_int, C.c_int, C.c_int,
+                                  C.c_int, C.c_int, C.c_int, vp]),
+    "auras_dpt_update": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_int, vp, vp, C.c_int, C.c_int, C.c_int,
+                                   C.POINTER(Sched), vp]),
     "auras_vit_tokens": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp]),
     "auras_layernorm": (C.c_int, [vp, i64, vp, i64, C.c_int, vp, vp, C.c_int, C.c_int, C.c_float, vp]),
     "auras_vit_attention": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp]),

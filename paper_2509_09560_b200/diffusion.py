@@ -688,6 +688,151 @@ class ViTEncoder:
                                                    1e-6, st), "layernorm")
 
 
+class DPTDenoiser:
+    """DP-T denoiser program (Diffusion Policy's TransformerForDiffusion;
+    BASELINE configs[3]) over up to S_max samples at their own inference
+    steps.  Every linear layer is a tcgen05 conv-path GEMM over the token axis
+    (T action tokens or 1 + n_obs cond tokens per sample) with bias / GELU /
+    Mish / residual in the epilogue; LayerNorm (vit.cu), the masked attentions,
+    staging and the scheduler update are dpt.cu kernels.  One call = one
+    denoise iteration of the whole batch."""
+
+    def __init__(self, model: DeviceModel, s_max: int):
+        torch = model.torch
+        cfg = model.cfg
+        if model.dt != _lib.DT_BF16:
+            raise ConfigInvalid("the DP-T denoiser runs in bf16 only")
+        self.m, self.s_max = model, s_max
+        dev, td = model.dev, model.tdtype
+        E, H, T = cfg.dpt_emb, cfg.dpt_heads, cfg.horizon
+        self.E, self.H, self.T = E, H, T
+        self.n_obs = cfg.n_obs_steps
+        self.tc = 1 + self.n_obs
+        self.tok_w = cfg.feat_dim + cfg.agent_pos_dim
+        self.gpad = _round(self.tok_w, 64)
+        w = model.w
+
+        def z(*shape, dtype=td):
+            return torch.zeros(*shape, dtype=dtype, device=dev)
+
+        self.xin = z(s_max, T, 64)
+        self.gcbuf = z(s_max, self.n_obs, self.gpad)
+        self.c = z(s_max, self.tc, E)
+        self.cobs = z(s_max, self.n_obs, E)
+        self.e1 = z(s_max, self.tc, 4 * E)
+        self.mem = z(s_max, self.tc, E)
+        self.ha, self.hb = z(s_max, T, E), z(s_max, T, E)
+        self.ln = z(s_max, T, E)
+        self.qkv = z(s_max, T, 3 * E)
+        self.att = z(s_max, T, E)
+        self.q2 = z(s_max, T, E)
+        self.kv2 = z(s_max, self.tc, 2 * E)
+        self.ff = z(s_max, T, 4 * E)
+        self.eps_bf = z(s_max, T, cfg.action_dim)
+        self.eps = z(s_max, T, cfg.action_dim, dtype=torch.float32)
+        self.pos_rep = w["dpt.pos"].to(dev, td)[None].repeat(s_max, 1, 1).contiguous()
+        self.cond_pos = model.f32(w["dpt.cond_pos"])
+        tab = scheduler_tables(cfg)["timestep"]
+        half = E // 2
+        freqs = torch.exp(torch.arange(half, dtype=torch.float32) * -(math.log(10000) / (half - 1)))
+        arg = torch.tensor(tab, dtype=torch.float32)[:, None] * freqs[None]
+        self.temb = model.f32(torch.cat([arg.sin(), arg.cos()], dim=1))
+        self.prog = []
+        self.max_scratch = 0
+
+        def lw(name, rows=None):
+            t = w[name + ".w"] if rows is None else w[name + ".w"][rows[0]:rows[1]]
+            return t.reshape(*t.shape, 1, 1)
+
+        def lb(name, rows=None):
+            t = w[name + ".b"] if rows is None else w[name + ".b"][rows[0]:rows[1]]
+            return model.f32(t)
+
+        def ln(src, g):
+            self.prog.append(("ln", src, model.f32(w[g + ".g"]), model.f32(w[g + ".b"])))
+
+        self._lin(model.conv_weight(lw("dpt.cond_obs"), cin_pad=self.gpad), lb("dpt.cond_obs"), self.gcbuf, self.gpad,
+                  self.cobs, E, self.n_obs)
+        self.prog.append(("cond",))
+        self._lin(model.conv_weight(lw("dpt.enc1")), lb("dpt.enc1"), self.c, E, self.e1, 4 * E, self.tc,
+                  act=_lib.ACT_MISH)
+        self._lin(model.conv_weight(lw("dpt.enc2")), lb("dpt.enc2"), self.e1, 4 * E, self.mem, E, self.tc)
+        self._lin(model.conv_weight(lw("dpt.input"), cin_pad=64), lb("dpt.input"), self.xin, 64, self.ha, E, T,
+                  res=self.pos_rep)
+        cur, nxt = self.ha, self.hb
+        for l in range(cfg.dpt_layers):
+            p = f"dpt.l{l}"
+            ln(cur, p + ".ln1")
+            self._lin(model.conv_weight(lw(p + ".sa_in")), lb(p + ".sa_in"), self.ln, E, self.qkv, 3 * E, T)
+            self.prog.append(("attn", self.qkv, 0, 3 * E, self.qkv, E, 3 * E, self.qkv, 2 * E, 3 * E, T, 0))
+            self._lin(model.conv_weight(lw(p + ".sa_out")), lb(p + ".sa_out"), self.att, E, nxt, E, T, res=cur)
+            cur, nxt = nxt, cur
+            ln(cur, p + ".ln2")
+            self._lin(model.conv_weight(lw(p + ".ca_in", (0, E))), lb(p + ".ca_in", (0, E)), self.ln, E, self.q2, E, T)
+            self._lin(model.conv_weight(lw(p + ".ca_in", (E, 3 * E))), lb(p + ".ca_in", (E, 3 * E)), self.mem, E,
+                      self.kv2, 2 * E, self.tc)
+            self.prog.append(("attn", self.q2, 0, E, self.kv2, 0, 2 * E, self.kv2, E, 2 * E, self.tc, 1))
+            self._lin(model.conv_weight(lw(p + ".ca_out")), lb(p + ".ca_out"), self.att, E, nxt, E, T, res=cur)
+            cur, nxt = nxt, cur
+            ln(cur, p + ".ln3")
+            self._lin(model.conv_weight(lw(p + ".ff1")), lb(p + ".ff1"), self.ln, E, self.ff, 4 * E, T,
+                      act=_lib.ACT_GELU)
+            self._lin(model.conv_weight(lw(p + ".ff2")), lb(p + ".ff2"), self.ff, 4 * E, nxt, E, T, res=cur)
+            cur, nxt = nxt, cur
+        ln(cur, "dpt.lnf")
+        self._lin(model.conv_weight(lw("dpt.head")), lb("dpt.head"), self.ln, E, self.eps_bf, cfg.action_dim, T,
+                  out_f32=self.eps)
+        self.scratch = torch.zeros(max(1, self.max_scratch), dtype=torch.float32, device=dev)
+
+    def _lin(self, wconv, bias, inp, in_pitch, out, out_pitch, rows, act=0, res=None, out_f32=None):
+        wm, cp, _, _, kp = wconv
+        M = wm.shape[0]
+        op = _op(w=wm.data_ptr(), bias=bias.data_ptr(), inp=inp.data_ptr(), out=out.data_ptr(), M=M, Cin=cp, Kp=kp,
+                 H=1, W=rows, in_pitch=in_pitch, in_coff=0, kh=1, kw=1, stride=1, pad_h=0, pad_w=0, Ho=1, Wo=rows,
+                 out_pitch=out_pitch, out_coff=0, act=act, res_before_act=0, splits=_splits(M, self.s_max * rows, kp),
+                 cta_target=0 if out_f32 is not None else 148)
+        if res is not None:
+            op.res, op.res_pitch, op.res_coff = res.data_ptr(), out_pitch, 0
+        if out_f32 is not None:
+            op.out_f32 = out_f32.data_ptr()
+        need = _lib.load().auras_conv_scratch_floats(_lib.C.byref(op), self.m.dt, self.s_max)
+        self.max_scratch = max(self.max_scratch, int(need))
+        self.prog.append(("conv", op))
+
+    def iterate(self, S, agents, lanes, steps, x_lanes, lanes_per_agent, ring, ring_agent_stride, slot_floats,
+                fetched, noise_lanes, sched, stream):
+        """One denoise iteration for samples (agents[s], lanes[s], steps[s]),
+        s < S (int32 device arrays); x lanes updated in place."""
+        lib = _lib.load()
+        cfg = self.m.cfg
+        st = stream.cuda_stream
+        E = self.E
+        _lib.check(lib.auras_dpt_prep(agents, lanes, steps, S, x_lanes, lanes_per_agent, cfg.horizon, cfg.action_dim,
+                                      self.xin.data_ptr(), ring, ring_agent_stride, slot_floats, fetched, self.tok_w,
+                                      self.n_obs, self.gcbuf.data_ptr(), self.gpad, self.temb.data_ptr(), E,
+                                      self.c.data_ptr(), self.cond_pos.data_ptr(), st), "dpt_prep")
+        for item in self.prog:
+            kind = item[0]
+            if kind == "conv":
+                _lib.check(lib.auras_conv(_lib.C.byref(item[1]), self.m.dt, S, None, 0, self.scratch.data_ptr(),
+                                          self.scratch.numel(), st), "dpt conv")
+            elif kind == "ln":
+                _, src, g, b = item
+                _lib.check(lib.auras_layernorm(src.data_ptr(), E, self.ln.data_ptr(), E, 0, g.data_ptr(), b.data_ptr(),
+                                               S * self.T, E, 1e-5, st), "layernorm")
+            elif kind == "cond":
+                _lib.check(lib.auras_dpt_cond(self.cobs.data_ptr(), self.c.data_ptr(), self.cond_pos.data_ptr(), S,
+                                              self.n_obs, E, st), "dpt_cond")
+            else:
+                _, qb, qo, ldq, kb, ko, ldk, vb, vo, ldv, nk, moff = item
+                _lib.check(lib.auras_attention(qb.data_ptr() + 2 * qo, ldq, kb.data_ptr() + 2 * ko, ldk,
+                                               vb.data_ptr() + 2 * vo, ldv, self.att.data_ptr(), E, S, self.T, nk,
+                                               self.H, E // self.H, moff, st), "attention")
+        _lib.check(lib.auras_dpt_update(self.eps.data_ptr(), cfg.action_dim, agents, lanes, steps, S, x_lanes,
+                                        noise_lanes, lanes_per_agent, cfg.horizon, cfg.action_dim, _lib.C.byref(sched),
+                                        st), "dpt_update")
+
+
 class Denoiser:
     """ConditionalUnet1D program over S_max samples (K3-K6 of SURVEY.md §2.4)."""
 

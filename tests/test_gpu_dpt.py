@@ -1,0 +1,69 @@
+"""DP-T transformer denoiser (BASELINE configs[3]) on the B200 vs the CPU
+restatement (oracle/dp_model.py dpt_eps, pinned against torch's
+TransformerDecoderLayer).  A batch of samples at different inference steps,
+each reading its agent's ring slot: eps within 3e-2 normwise relative (bf16
+weights and activations, fp32 accumulation), and the scheduler update of the
+request lanes within the same tolerance of the oracle's step."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import dp_model
+from paper_2509_09560_b200 import _lib
+from paper_2509_09560_b200 import diffusion as D
+
+pytestmark = pytest.mark.gpu
+
+
+def test_dpt_iteration_matches_oracle():
+    cfg = D.DPConfig(name="dpt_gpu_test", encoder="vit_b16", image_hw=224, feat_dim=768, action_dim=7,
+                     denoiser="transformer")
+    w = D.init_weights(cfg, 4, device="cpu")
+    model = D.DeviceModel(cfg, w, "bf16")
+    S = 5
+    den = D.DPTDenoiser(model, 8)
+    rng = np.random.default_rng(1)
+    T, A = cfg.horizon, cfg.action_dim
+    steps = np.array([0, 13, 50, 98, 99], dtype=np.int32)
+    agents = np.arange(S, dtype=np.int32)
+    lanes = np.zeros(S, dtype=np.int32)
+    x0 = rng.standard_normal((S, 1, T * A)).astype(np.float32)
+    noise = rng.standard_normal((S, 1, cfg.num_inference_steps, T * A)).astype(np.float32)
+    slot_floats = _lib_round(cfg.gc_dim, 8) + 16
+    ring = np.zeros((S, 2, slot_floats), dtype=np.float32)
+    gcs = rng.standard_normal((S, cfg.gc_dim)).astype(np.float32)
+    ring[:, 1, :cfg.gc_dim] = gcs                      # the frame fetched slot 1
+    dev = torch.device("cuda")
+    t = {k: torch.from_numpy(v).to(dev) for k, v in dict(agents=agents, lanes=lanes, steps=steps, x=x0, noise=noise,
+                                                         ring=ring).items()}
+    fetched = torch.tensor([1, 7, 3], dtype=torch.int64, device=dev)
+    sched = D.scheduler_tables(cfg)
+    st_t = {k: torch.tensor(v, dtype=torch.int32 if k == "timestep" else torch.float32, device=dev)
+            for k, v in sched.items()}
+    sc = _lib.Sched()
+    for k in ("timestep", "sqrt_ab", "sqrt_1mab", "c_x0", "c_xt", "c_eps", "sigma"):
+        setattr(sc, k, st_t[k].data_ptr())
+    sc.n_steps, sc.clip_sample, sc.ddpm = cfg.num_inference_steps, int(cfg.clip_sample), 1
+    stream = torch.cuda.current_stream()
+    den.iterate(S, t["agents"].data_ptr(), t["lanes"].data_ptr(), t["steps"].data_ptr(), t["x"].data_ptr(), 1,
+                t["ring"].data_ptr(), 2 * slot_floats, slot_floats, fetched.data_ptr(), t["noise"].data_ptr(), sc,
+                stream)
+    torch.cuda.synchronize()
+    eps = den.eps[:S].cpu().numpy()
+    xs = t["x"].cpu().numpy()
+    osch = dp_model.Scheduler(cfg)
+    for s in range(S):
+        xin = torch.from_numpy(x0[s, 0].reshape(T, A))
+        with torch.no_grad():
+            want = dp_model.dpt_eps(w, cfg, xin, int(sched["timestep"][steps[s]]), torch.from_numpy(gcs[s])).numpy()
+            wx = osch.step(int(steps[s]), xin, torch.from_numpy(want),
+                           torch.from_numpy(noise[s, 0, steps[s]].reshape(T, A))).numpy()
+        err = np.linalg.norm(eps[s] - want) / np.linalg.norm(want)
+        assert err <= 3e-2, (s, err)
+        xerr = np.linalg.norm(xs[s, 0].reshape(T, A) - wx) / np.linalg.norm(wx)
+        assert xerr <= 3e-2, (s, xerr)
+
+
+def _lib_round(x, m):
+    return (x + m - 1) // m * m
