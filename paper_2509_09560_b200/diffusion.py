@@ -96,9 +96,11 @@ PRESETS = {
     "pusht": DPConfig(name="pusht"),
     # DP default UNet widths (256, 512, 1024)
     "dp_default": DPConfig(name="dp_default", down_dims=(256, 512, 1024), dsed=256),
-    # BASELINE configs[3], perception half: ViT-B/16 at 224x224, 7-DoF actions, bf16;
-    # the denoiser is the DP-default ConditionalUnet1D (the DP-T transformer
-    # denoiser of that config is not built yet)
+    # BASELINE configs[3]: transformer diffusion policy -- ViT-B/16 at 224x224,
+    # DP-T denoiser (8 layers, 256 wide, 4 heads), 7-DoF actions, bf16
+    "vit_dpt": DPConfig(name="vit_dpt", encoder="vit_b16", image_hw=224, feat_dim=768, action_dim=7,
+                        denoiser="transformer"),
+    # ViT-B/16 perception with the DP-default ConditionalUnet1D denoiser
     "vit": DPConfig(name="vit", encoder="vit_b16", image_hw=224, feat_dim=768, action_dim=7,
                     down_dims=(256, 512, 1024), dsed=256),
 }
@@ -358,6 +360,14 @@ def encoder_flops(cfg: DPConfig):
         groups.append(f)
         hw, cin = ho, c
     return groups
+
+
+def dpt_flops_per_sample(cfg: DPConfig) -> float:
+    """2 x MACs of one DP-T denoise step for one sample."""
+    E, T, tc, L = cfg.dpt_emb, cfg.horizon, 1 + cfg.n_obs_steps, cfg.dpt_layers
+    per_layer = T * (3 * E * E + E * E + E * E + E * E + 8 * E * E) + tc * 2 * E * E + 2 * T * T * E + 2 * T * tc * E
+    cond = cfg.n_obs_steps * (cfg.feat_dim + cfg.agent_pos_dim) * E + tc * 8 * E * E
+    return 2.0 * (L * per_layer + cond + T * cfg.action_dim * E * 2)
 
 
 def unet_flops_per_sample(cfg: DPConfig) -> float:
@@ -1121,7 +1131,8 @@ class DPSession:
         self.model = _device_model(gen, gd)
         self.pmodel = _device_model(gen, self.pd) if self.pd != gd else self.model
         self.gc_pad = _round(cfg.gc_dim, 8)
-        _, F = film_layout(cfg)
+        self.dpt = cfg.denoiser == "transformer"
+        F = 0 if self.dpt else film_layout(cfg)[1]
         self.slot_floats = self.gc_pad + F
         self.store = ContextStore(capacity, slot_elems=self.slot_floats, agents=agents,
                                   dtype=torch.float32, device=dev)
@@ -1129,7 +1140,6 @@ class DPSession:
             self.encoder = (ViTEncoder if cfg.encoder == "vit_b16" else Encoder)(self.pmodel, agents)
         s_max = agents * max(1, lanes)
         s_max = min(s_max, 64)
-        self.denoiser = Denoiser(self.model, s_max, self.store, self.gc_pad, gen.use_graph)
         sched = scheduler_tables(cfg)
         self.sched_t = {k: torch.tensor(v, dtype=torch.int32 if k == "timestep" else torch.float32,
                                         device=dev) for k, v in sched.items()}
@@ -1138,16 +1148,25 @@ class DPSession:
             setattr(sc, k, self.sched_t[k].data_ptr())
         sc.n_steps, sc.clip_sample = cfg.num_inference_steps, int(cfg.clip_sample)
         sc.ddpm = int(cfg.scheduler == "ddpm")
-        ops = (_lib.ConvOp * len(self.denoiser.ops))(*self.denoiser.ops)
-        payload = self.store.payload
-        self.plan = self.lib.auras_unet_plan_create(
-            ops, len(self.denoiser.ops), self.model.dt, s_max, cfg.horizon, cfg.action_dim,
-            self.denoiser.film_tau_ptr, payload.data_ptr() + 4 * self.gc_pad, self.denoiser.F,
-            self.slot_floats, capacity * self.slot_floats, self.denoiser.final_w.data_ptr(),
-            self.denoiser.final_b.data_ptr(), cfg.down_dims[0], _lib.C.byref(sc),
-            self.denoiser.xin.data_ptr(), 64)
-        if not self.plan:
-            _lib.check(-2, "unet_plan_create")
+        self.sc = sc
+        self.plan = None
+        if self.dpt:
+            # DP-T denoiser: a Python-driven program of conv-path GEMMs and dpt.cu kernels,
+            # one batched launch sequence per denoise iteration
+            self.denoiser = DPTDenoiser(self.model, s_max)
+            self.sample_idx = torch.zeros(cfg.num_inference_steps, 3, s_max, dtype=torch.int32, device=dev)
+        else:
+            self.denoiser = Denoiser(self.model, s_max, self.store, self.gc_pad, gen.use_graph)
+            ops = (_lib.ConvOp * len(self.denoiser.ops))(*self.denoiser.ops)
+            payload = self.store.payload
+            self.plan = self.lib.auras_unet_plan_create(
+                ops, len(self.denoiser.ops), self.model.dt, s_max, cfg.horizon, cfg.action_dim,
+                self.denoiser.film_tau_ptr, payload.data_ptr() + 4 * self.gc_pad, self.denoiser.F,
+                self.slot_floats, capacity * self.slot_floats, self.denoiser.final_w.data_ptr(),
+                self.denoiser.final_b.data_ptr(), cfg.down_dims[0], _lib.C.byref(sc),
+                self.denoiser.xin.data_ptr(), 64)
+            if not self.plan:
+                _lib.check(-2, "unet_plan_create")
         self.s_max = s_max
         hr = cfg.horizon * cfg.action_dim
         self.row = hr
@@ -1162,13 +1181,16 @@ class DPSession:
         self.out = torch.zeros(max(1, max_outputs), agents, hr, dtype=torch.float32, device=dev)
         self.fetched = torch.zeros(3, dtype=torch.int64, device=dev)
         self.version_log = torch.zeros(max(1, max_frames), dtype=torch.int64, device=dev)
-        self.film_o = self.denoiser.film_o
         self.stage = None
+        self.film_op = None
         if self.disagg:
-            self.film_o = self.film_o.to(pdev)
             self.stage = torch.zeros(agents, self.slot_floats, dtype=torch.float32, device=pdev)
-        self.film_op = _lib.LinearOp(w=self.film_o.data_ptr(), bias=0, M=self.denoiser.F,
-                                     K=cfg.gc_dim, mish_in=1, ldw=self.gc_pad)
+        if not self.dpt:
+            self.film_o = self.denoiser.film_o
+            if self.disagg:
+                self.film_o = self.film_o.to(pdev)
+            self.film_op = _lib.LinearOp(w=self.film_o.data_ptr(), bias=0, M=self.denoiser.F,
+                                         K=cfg.gc_dim, mish_in=1, ldw=self.gc_pad)
         self.resident = None
         if getattr(policy, "resident_frames", 0):
             self._stage_resident(policy.resident_frames)
@@ -1263,9 +1285,10 @@ class DPSession:
                 stride, self.p.cuda_stream), "assemble_cond")
             self.first = False
             # FiLM projection of the new context, once per publish, into the slot
-            _lib.check(self.lib.auras_linear(_lib.C.byref(self.film_op), self.pmodel.dt, self.A, base,
-                                             stride, base + 4 * self.gc_pad, stride,
-                                             self.p.cuda_stream), "film projection")
+            if self.film_op is not None:
+                _lib.check(self.lib.auras_linear(_lib.C.byref(self.film_op), self.pmodel.dt, self.A, base,
+                                                 stride, base + 4 * self.gc_pad, stride,
+                                                 self.p.cuda_stream), "film projection")
             if self.disagg:
                 # one pitched P2P copy: A staged slots -> slot `slot` of each agent's ring
                 _lib.check(self.lib.auras_peer_copy(ring, 4 * ring_stride, base, 4 * stride,
@@ -1292,14 +1315,42 @@ class DPSession:
         if self.instrument:
             e0 = self.torch.cuda.Event(enable_timing=True)
             e0.record(self.g)
-        _lib.check(self.lib.auras_unet_generate(
-            self.plan, S, ia(lanes), ia(agents), ia(start), ia(count), iters, self.R,
-            self.x.data_ptr(), _lib.ptr(self.noise), self.fetched.data_ptr(),
-            int(self.gen.use_graph), self.g.cuda_stream), "unet_generate")
+        if self.dpt:
+            self._generate_dpt(agents, lanes, start, count, iters)
+        else:
+            _lib.check(self.lib.auras_unet_generate(
+                self.plan, S, ia(lanes), ia(agents), ia(start), ia(count), iters, self.R,
+                self.x.data_ptr(), _lib.ptr(self.noise), self.fetched.data_ptr(),
+                int(self.gen.use_graph), self.g.cuda_stream), "unet_generate")
         if self.instrument:
             e1 = self.torch.cuda.Event(enable_timing=True)
             e1.record(self.g)
             self.gen_events.append((e0, e1, iters, S))
+
+    def _generate_dpt(self, agents, lanes, start, count, iters):
+        """Iteration r runs every sample with count > r at inference step
+        start + r; the per-iteration (agent, lane, step) lists go to the device
+        in one copy."""
+        torch = self.torch
+        idx = np.zeros((iters, 3, self.s_max), dtype=np.int32)
+        active = []
+        for r in range(iters):
+            sel = [j for j in range(len(agents)) if count[j] > r]
+            active.append(len(sel))
+            idx[r, 0, :len(sel)] = [agents[j] for j in sel]
+            idx[r, 1, :len(sel)] = [lanes[j] for j in sel]
+            idx[r, 2, :len(sel)] = [start[j] + r for j in sel]
+        dst = self.sample_idx[:iters]
+        with torch.cuda.stream(self.g):
+            dst.copy_(torch.from_numpy(idx).pin_memory(), non_blocking=True)
+        base = dst.data_ptr()
+        row = 4 * self.s_max
+        cap = self.store.capacity
+        for r in range(iters):
+            b = base + r * 3 * row
+            self.denoiser.iterate(active[r], b, b + row, b + 2 * row, self.x.data_ptr(), self.R,
+                                  self.store.payload.data_ptr(), cap * self.slot_floats, self.slot_floats,
+                                  self.fetched.data_ptr(), _lib.ptr(self.noise), self.sc, self.g)
 
     def finish(self, lane, out_index):
         A = self.A
@@ -1346,7 +1397,7 @@ def make_diffusion_policy(config="pusht", dtype: str = "bf16", seed: int = 0, we
         import torch
         weights = init_weights(cfg, seed, device="cuda" if torch.cuda.is_available() else "cpu")
     gflop = [f / 1e9 for f in encoder_flops(cfg)]
-    step_gflop = unet_flops_per_sample(cfg) / 1e9
+    step_gflop = (dpt_flops_per_sample(cfg) if cfg.denoiser == "transformer" else unet_flops_per_sample(cfg)) / 1e9
     perception = DPPerception(layer_costs=tuple(gflop), obs_width=cfg.agent_pos_dim)
     generation = DPGeneration(cfg=cfg, dtype=dtype, seed=seed, weights=weights, step_cost=step_gflop,
                               use_graph=use_graph, perception_device=perception_device)

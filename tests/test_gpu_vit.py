@@ -125,3 +125,22 @@ def test_vit_policy_pipelined_matches_oracle():
     assert g.shape == r.shape and g.shape[1] == 16 * 7
     assert float(np.abs(g - r).max() / np.abs(r).max()) <= 6e-2
     assert [q.context_versions for q in res.requests] == [q.context_versions for q in ref.requests]
+
+
+def test_vit_dpt_policy_pipelined_matches_oracle():
+    """BASELINE configs[3] end to end: ViT-B/16 perception + DP-T transformer
+    denoiser, 7-DoF actions, through run_pipelined at depth 2, against the
+    oracle pipeline (bf16 action tolerance 6e-2 normwise, exact versions)."""
+    w = D.init_weights(D.PRESETS["vit_dpt"], 0, device="cpu")
+    pol = D.make_diffusion_policy("vit_dpt", dtype="bf16", weights=w)
+    gen = pol.generation
+    for cfg in (dict(pp_perception=1, pp_generation=2, fetch_offset=0),
+                dict(pp_perception=1, pp_generation=4, fetch_offset=-1)):
+        res = run_pipelined(PipelineConfig(**cfg), pol, None, 5)
+        orc = dp_model.OracleDP(gen.weights, gen.cfg, gen.seed, 0, pol.perception.layer_costs, gen.step_cost)
+        ref = osched.run_pipelined(cfg, orc, None, 5)
+        g = np.array([a.values for a in res.actions])
+        r = np.array([a.values for a in ref.actions])
+        assert g.shape == r.shape and g.shape[1] == 16 * 7
+        assert float(np.abs(g - r).max() / np.abs(r).max()) <= 6e-2
+        assert [q.context_versions for q in res.requests] == [q.context_versions for q in ref.requests]
