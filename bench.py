@@ -431,8 +431,13 @@ def main():
     # roofline of the denoise chain (all UNet GEMM + epilogue launches of a frame),
     # timed with CUDA events on the generation stream around each frame's chain
     gen_ms, gen_steps, gen_S = 0.0, 0, []
-    bytes_step = D.unet_stream_bytes(cfg)
-    flops_sample = D.unet_flops_per_sample(cfg)
+    dpt = cfg.denoiser == "transformer"
+    if dpt:
+        bytes_step = 2 * sum(v.numel() for k, v in weights.items() if k.startswith("dpt."))
+        flops_sample = D.dpt_flops_per_sample(cfg)
+    else:
+        bytes_step = D.unet_stream_bytes(cfg)
+        flops_sample = D.unet_flops_per_sample(cfg)
     ev = LAST_EVENTS.get("events", [])
     for e0, e1, iters, S in ev:
         gen_ms += e0.elapsed_time(e1)
@@ -440,7 +445,7 @@ def main():
         gen_S.append(S)
     S_med = int(np.median(gen_S)) if gen_S else A * args.depth
     step_ms = gen_ms / max(1, gen_steps)
-    act_bytes = S_med * (cfg.horizon * cfg.action_dim * 8 + 2 * D.film_layout(cfg)[1] * 4)
+    act_bytes = S_med * (cfg.horizon * cfg.action_dim * 8 + (0 if dpt else 2 * D.film_layout(cfg)[1] * 4))
     achieved = (bytes_step + act_bytes) / (step_ms / 1e3) / 1e9 if step_ms > 0 else 0.0
     peaks = {}
     try:
@@ -481,10 +486,10 @@ def main():
     out = {"metric": METRIC, "value": value, "unit": "actions/s", "n_gpus": dist.world,
            "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-           "config": {"workload": f"{'configs[3] (perception half)' if cfg.encoder == 'vit_b16' else 'configs[1]'}: "
+           "config": {"workload": f"{('configs[3]' if cfg.denoiser == 'transformer' else 'configs[3] perception + UNet') if cfg.encoder == 'vit_b16' else 'configs[1]'}: "
                                   f"Diffusion Policy ({cfg.name}: "
                                   f"{'ViT-B/16' if cfg.encoder == 'vit_b16' else 'ResNet-18-GN'} "
-                                  f"encoder, UNet {list(cfg.down_dims)}, {cfg.num_inference_steps}-step "
+                                  f"encoder, {'DP-T transformer denoiser' if cfg.denoiser == 'transformer' else 'UNet ' + str(list(cfg.down_dims))}, {cfg.num_inference_steps}-step "
                                   f"{cfg.scheduler.upper()}, horizon {cfg.horizon}, action dim "
                                   f"{cfg.action_dim}, {cfg.image_hw}x{cfg.image_hw} frames) on 1 B200 per rank",
                       "model": f"dp-cnn-{cfg.name}", "depth": args.depth,
@@ -500,7 +505,7 @@ def main():
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                         "frac": achieved / hbm_peak, "traffic": traffic,
                         "traffic_source": "ncu dram__bytes_read+write per launch, profiles/r1_ncu_unet_cluster.json",
-                        "kernel": "denoise chain (UNet conv GEMMs + fused epilogues), per step",
+                        "kernel": "denoise chain (" + ("DP-T GEMMs + attention + update" if dpt else "UNet conv GEMMs + fused epilogues") + "), per step",
                         "step_ms": step_ms, "algorithmic_bytes_per_step": bytes_step + act_bytes,
                         "tensor_tflops": tflops, "tensor_frac": tflops / tc_peak,
                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
@@ -569,12 +574,17 @@ def _install_capture():
     def close(self):
         if self.gen_events:
             LAST_EVENTS["events"] = list(self.gen_events)
-        LAST_EVENTS["denoiser_ops"] = list(self.denoiser.ops)
-        LAST_EVENTS["launches_per_iter"] = int(self.lib.auras_unet_launches_per_iter(self.plan))
         S_seen = sorted({ev[3] for ev in self.gen_events})
-        names = {0: "layer-by-layer", 1: "megakernel (split-K via L2)", 2: "cluster megakernel (DSMEM)"}
-        LAST_EVENTS["denoise_kernel"] = {int(S): names.get(int(self.lib.auras_unet_kernel_for(self.plan, S)), "?")
-                                         for S in S_seen}
+        if self.dpt:
+            # prep + program (a conv op is GEMM + epilogue) + update
+            LAST_EVENTS["launches_per_iter"] = 2 + sum(2 if it[0] == "conv" else 1 for it in self.denoiser.prog)
+            LAST_EVENTS["denoise_kernel"] = {int(S): "dp-t program (conv-path GEMMs + dpt.cu)" for S in S_seen}
+        else:
+            LAST_EVENTS["denoiser_ops"] = list(self.denoiser.ops)
+            LAST_EVENTS["launches_per_iter"] = int(self.lib.auras_unet_launches_per_iter(self.plan))
+            names = {0: "layer-by-layer", 1: "megakernel (split-K via L2)", 2: "cluster megakernel (DSMEM)"}
+            LAST_EVENTS["denoise_kernel"] = {int(S): names.get(int(self.lib.auras_unet_kernel_for(self.plan, S)), "?")
+                                             for S in S_seen}
         LAST_EVENTS["encoder_launches"] = 1 + sum(
             (2 if item[0] == "conv" else 1) for g in self.encoder.groups.values() for item in g)
         orig_close(self)

@@ -1154,6 +1154,7 @@ class DPSession:
             # DP-T denoiser: a Python-driven program of conv-path GEMMs and dpt.cu kernels,
             # one batched launch sequence per denoise iteration
             self.denoiser = DPTDenoiser(self.model, s_max)
+            self.dpt_graphs = {}
             self.sample_idx = torch.zeros(cfg.num_inference_steps, 3, s_max, dtype=torch.int32, device=dev)
         else:
             self.denoiser = Denoiser(self.model, s_max, self.store, self.gc_pad, gen.use_graph)
@@ -1348,9 +1349,25 @@ class DPSession:
         cap = self.store.capacity
         for r in range(iters):
             b = base + r * 3 * row
-            self.denoiser.iterate(active[r], b, b + row, b + 2 * row, self.x.data_ptr(), self.R,
-                                  self.store.payload.data_ptr(), cap * self.slot_floats, self.slot_floats,
-                                  self.fetched.data_ptr(), _lib.ptr(self.noise), self.sc, self.g)
+
+            def run(S=active[r], b=b):
+                self.denoiser.iterate(S, b, b + row, b + 2 * row, self.x.data_ptr(), self.R,
+                                      self.store.payload.data_ptr(), cap * self.slot_floats, self.slot_floats,
+                                      self.fetched.data_ptr(), _lib.ptr(self.noise), self.sc, self.g)
+            if not self.gen.use_graph or os.environ.get("AURAS_DPT_GRAPH") == "0":
+                run()
+                continue
+            # one CUDA graph per (batch size, iteration slot): every pointer the
+            # program reads is fixed, the per-frame sample lists arrive by the copy above
+            key = (active[r], r)
+            graph = self.dpt_graphs.get(key)
+            if graph is None:
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, stream=self.g):
+                    run()
+                self.dpt_graphs[key] = graph
+            with torch.cuda.stream(self.g):
+                graph.replay()
 
     def finish(self, lane, out_index):
         A = self.A
