@@ -29,6 +29,10 @@ Contents
   arithmetic is "parity unpinned" by the reference: the reference pins only
   the schedule that decides which context version each denoise step reads.
   The restatement follows SURVEY.md Appendix B and states every choice.
+  BASELINE configs[3]'s networks are restated here too: ViT-B/16
+  (`encode_vit`) and Diffusion Policy's TransformerForDiffusion (`dpt_eps`),
+  each pinned against torch's own TransformerEncoderLayer /
+  TransformerDecoderLayer loaded with the same weights (tests/test_dp_host.py).
 * `transformer` -- the reference's float64 causal transformer
   (fp/transformer.py:58-211) restated in numpy, the checker for the device
   merged prefill.  PINNED against hidden states, KV rows, logits and greedy
