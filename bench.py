@@ -486,7 +486,7 @@ def main():
     out = {"metric": METRIC, "value": value, "unit": "actions/s", "n_gpus": dist.world,
            "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-           "config": {"workload": f"{('configs[3]' if cfg.denoiser == 'transformer' else 'configs[3] perception + UNet') if cfg.encoder == 'vit_b16' else 'configs[1]'}: "
+           "config": {"workload": f"{('configs[3]' if cfg.denoiser == 'transformer' else 'configs[3] perception + UNet') if cfg.encoder == 'vit_b16' else ('configs[0]' if cfg.name == 'tiny' else 'configs[1]')}: "
                                   f"Diffusion Policy ({cfg.name}: "
                                   f"{'ViT-B/16' if cfg.encoder == 'vit_b16' else 'ResNet-18-GN'} "
                                   f"encoder, {'DP-T transformer denoiser' if cfg.denoiser == 'transformer' else 'UNet ' + str(list(cfg.down_dims))}, {cfg.num_inference_steps}-step "
