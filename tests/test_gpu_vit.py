@@ -144,3 +144,28 @@ def test_vit_dpt_policy_pipelined_matches_oracle():
         assert g.shape == r.shape and g.shape[1] == 16 * 7
         assert float(np.abs(g - r).max() / np.abs(r).max()) <= 6e-2
         assert [q.context_versions for q in res.requests] == [q.context_versions for q in ref.requests]
+
+
+def test_vit_dpt_two_agents_and_sequential_match_oracle():
+    """configs[3] with two agents batched into the same kernels (each against
+    its own oracle run), and the depth-1 sequential baseline."""
+    w = D.init_weights(D.PRESETS["vit_dpt"], 0, device="cpu")
+    pol = D.make_diffusion_policy("vit_dpt", dtype="bf16", weights=w, agents=2)
+    gen = pol.generation
+    cfg = dict(pp_perception=1, pp_generation=3, fetch_offset=0)
+    res = run_pipelined(PipelineConfig(**cfg), pol, None, 5, agents=2)
+    for a in range(2):
+        orc = dp_model.OracleDP(gen.weights, gen.cfg, gen.seed, a, pol.perception.layer_costs, gen.step_cost)
+        ref = osched.run_pipelined(cfg, orc, None, 5)
+        g = np.array([x.values for x in res.agent_actions[a]])
+        r = np.array([x.values for x in ref.actions])
+        assert g.shape == r.shape
+        assert float(np.abs(g - r).max() / np.abs(r).max()) <= 6e-2, a
+    from paper_2509_09560_b200 import run_sequential
+    pol1 = D.make_diffusion_policy("vit_dpt", dtype="bf16", weights=w)
+    res = run_sequential(pol1, None, 2)
+    orc = dp_model.OracleDP(gen.weights, gen.cfg, gen.seed, 0, pol1.perception.layer_costs, gen.step_cost)
+    ref = osched.run_sequential(orc, None, 2)
+    g = np.array([x.values for x in res.actions])
+    r = np.array([x.values for x in ref.actions])
+    assert g.shape == r.shape and float(np.abs(g - r).max() / np.abs(r).max()) <= 6e-2
