@@ -492,11 +492,14 @@ def main():
                                   f"encoder, {'DP-T transformer denoiser' if cfg.denoiser == 'transformer' else 'UNet ' + str(list(cfg.down_dims))}, {cfg.num_inference_steps}-step "
                                   f"{cfg.scheduler.upper()}, horizon {cfg.horizon}, action dim "
                                   f"{cfg.action_dim}, {cfg.image_hw}x{cfg.image_hw} frames) on 1 B200 per rank",
-                      "model": f"dp-cnn-{cfg.name}", "depth": args.depth,
+                      "model": f"{'dp-transformer' if cfg.denoiser == 'transformer' else 'dp-cnn'}-{cfg.name}", "depth": args.depth,
                       "pp": [1, args.depth], "fetch_offset": args.offset, "alpha": 0.0,
                       "agents_per_gpu": A, "global_batch": A * dist.world,
                       "samples_per_denoise_step": S_med, "parallelism": f"replicas x{dist.world}",
-                      "l2": "inputs larger than L2: 488 MB of UNet weights streamed per denoise step",
+                      "l2": (f"inputs larger than L2: {bytes_step / 1e6:.0f} MB of denoiser weights streamed per step"
+                             if bytes_step > 126e6 else
+                             f"no L2 flush: the {bytes_step / 1e6:.0f} MB of denoiser weights fit in the 126 MB L2 and "
+                             f"stay resident across steps, as in steady-state serving"),
                       "inputs": f"{n_res} synthetic frames + request noise pre-staged in HBM",
                       "perception_device": args.perception_device},
            "p99_action_latency_ms": p99, "mean_action_latency_ms": jmean,
