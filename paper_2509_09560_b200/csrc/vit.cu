@@ -89,7 +89,7 @@ __global__ void layernorm_kernel(const __nv_bfloat16 *__restrict__ in, int64_t l
 }
 
 constexpr int ATT_THREADS = 256;
-constexpr int ATT_QB = 8;           // queries per CTA: one per warp, many CTAs
+constexpr int ATT_QB = 16;          // queries per CTA (two per warp): measured best with the 16-byte K/V staging
 
 // grid (S * heads, ceil(N / ATT_QB)); dh <= 64 (two head columns per lane).
 __global__ void __launch_bounds__(ATT_THREADS) vit_attention_kernel(const __nv_bfloat16 *__restrict__ qkv,
