@@ -21,6 +21,29 @@ int cuda_check(cudaError_t e, const char *what);
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute is per device, so a process-wide flag would miss the second
+// GPU of the disaggregated variant.
+template <typename F>
+inline int ensure_smem_attr(F *func, int bytes) {
+  struct Entry {
+    const void *f;
+    int dev, bytes;
+  };
+  static thread_local Entry cache[64];
+  static thread_local int n = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = -1;
+  for (int i = 0; i < n; ++i)
+    if (cache[i].f == reinterpret_cast<const void *>(func) && cache[i].dev == dev && cache[i].bytes >= bytes)
+      return AURAS_OK;
+  const int rc = cuda_check(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                            "cudaFuncSetAttribute");
+  if (rc) return rc;
+  if (n < 64) cache[n++] = Entry{reinterpret_cast<const void *>(func), dev, bytes};
+  return AURAS_OK;
+}
+
 // ---------------------------------------------------------------- numerics
 template <typename T> struct Elem;
 template <> struct Elem<float> {

@@ -227,8 +227,7 @@ int launch_linear(LinArgs a, cudaStream_t st) {
     const size_t smem = sizeof(float) * b.N * a.ldw;
     if (smem > 200 * 1024) { set_error("linear: K too large"); return AURAS_E_ARG; }
     if (smem > 48 * 1024)
-      AURAS_CUDA(cudaFuncSetAttribute(linear_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
+      if (int rc = ensure_smem_attr(linear_kernel<T>, (int)smem)) return rc;
     int blocks = (a.M + 7) / 8;
     blocks = std::min(blocks, 148 * 8);
     linear_kernel<T><<<blocks, 256, smem, st>>>(b);

@@ -194,11 +194,7 @@ int launch_gemm_gather(const ConvGemmArgs &g, cudaStream_t st) {
   CUtensorMap tmA;
   int rc = make_weight_map(&tmA, g.w, g.M, g.Kp);
   if (rc) return rc;
-  static bool attr = false;
-  if (!attr) {
-    AURAS_CUDA(cudaFuncSetAttribute(conv_gemm_tc_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GG_SMEM));
-    attr = true;
-  }
+  if (int rc2 = ensure_smem_attr(conv_gemm_tc_gather, (int)GG_SMEM)) return rc2;
   GatherArgs a;
   a.in = static_cast<const __nv_bfloat16 *>(g.in);
   a.partial = g.partial;

@@ -187,11 +187,7 @@ int launch_gemm_sm100(const ConvGemmArgs &g, cudaStream_t st) {
   if (rc) return rc;
   rc = make_act_map(&tmB, g.in, g.in_coff, g.Cin, g.in_pitch, g.W, g.stride, g.N / g.Wo, g.Wo, p.s_box);
   if (rc) return rc;
-  static size_t configured = 0;
-  if (p.smem > configured) {
-    AURAS_CUDA(cudaFuncSetAttribute(conv_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    configured = 227 * 1024;
-  }
+  if (int rc2 = ensure_smem_attr(conv_gemm_tc, 227 * 1024)) return rc2;
   TcArgs a;
   a.partial = g.partial;
   a.M = g.M; a.N = g.N; a.Cin = g.Cin; a.Wo = g.Wo; a.stride = g.stride; a.pad = g.pad_w;

@@ -494,11 +494,8 @@ extern "C" int auras_tf_forward(const double *params, int d_model, int n_heads, 
               m.max_len);
     return AURAS_E_ARG;
   }
-  static thread_local size_t configured = 0;
-  if (smem_blk > 48 * 1024 && smem_blk > configured) {
-    AURAS_CUDA(cudaFuncSetAttribute(tf_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_blk));
-    configured = smem_blk;
-  }
+  if (smem_blk > 48 * 1024)
+    if (int rc = ensure_smem_attr(tf_block, (int)smem_blk)) return rc;
   if (smem_qkv > 48 * 1024) {
     set_error("transformer forward: d=%d too wide", m.d);
     return AURAS_E_ARG;

@@ -228,11 +228,8 @@ extern "C" int auras_vit_attention(const void *qkv, void *out, int S, int N, int
     set_error("vit_attention: %d tokens need %zu B of shared memory", N, smem);
     return AURAS_E_ARG;
   }
-  static thread_local size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    AURAS_CUDA(cudaFuncSetAttribute(vit_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = smem;
-  }
+  if (smem > 48 * 1024)
+    if (int rc = ensure_smem_attr(vit_attention_kernel, (int)smem)) return rc;
   dim3 grid(S * heads, (n_valid + ATT_QB - 1) / ATT_QB);
   vit_attention_kernel<<<grid, ATT_THREADS, smem, as_stream(stream)>>>(
       static_cast<const __nv_bfloat16 *>(qkv), static_cast<__nv_bfloat16 *>(out), N, n_valid, heads, dh,
