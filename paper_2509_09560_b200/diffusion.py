@@ -736,7 +736,8 @@ class DPTDenoiser:
         self.qkv = z(s_max, T, 3 * E)
         self.att = z(s_max, T, E)
         self.q2 = z(s_max, T, E)
-        self.kv2 = z(s_max, self.tc, 2 * E)
+        L = cfg.dpt_layers
+        self.kv2 = z(s_max, self.tc, L * 2 * E)       # cross-attention K|V of every layer
         self.ff = z(s_max, T, 4 * E)
         self.eps_bf = z(s_max, T, cfg.action_dim)
         self.eps = z(s_max, T, cfg.action_dim, dtype=torch.float32)
@@ -769,6 +770,12 @@ class DPTDenoiser:
         self._lin(model.conv_weight(lw("dpt.enc2")), lb("dpt.enc2"), self.e1, 4 * E, self.mem, E, self.tc)
         self._lin(model.conv_weight(lw("dpt.input"), cin_pad=64), lb("dpt.input"), self.xin, 64, self.ha, E, T,
                   res=self.pos_rep)
+        # the memory does not change across the decoder layers: one GEMM projects
+        # the cross-attention K|V of all layers (rows E..3E of each ca_in)
+        kvw = torch.cat([w[f"dpt.l{l}.ca_in.w"][E:3 * E] for l in range(L)])
+        kvb = torch.cat([w[f"dpt.l{l}.ca_in.b"][E:3 * E] for l in range(L)])
+        self._lin(model.conv_weight(kvw.reshape(*kvw.shape, 1, 1)), model.f32(kvb), self.mem, E, self.kv2,
+                  L * 2 * E, self.tc)
         cur, nxt = self.ha, self.hb
         for l in range(cfg.dpt_layers):
             p = f"dpt.l{l}"
@@ -779,9 +786,8 @@ class DPTDenoiser:
             cur, nxt = nxt, cur
             ln(cur, p + ".ln2")
             self._lin(model.conv_weight(lw(p + ".ca_in", (0, E))), lb(p + ".ca_in", (0, E)), self.ln, E, self.q2, E, T)
-            self._lin(model.conv_weight(lw(p + ".ca_in", (E, 3 * E))), lb(p + ".ca_in", (E, 3 * E)), self.mem, E,
-                      self.kv2, 2 * E, self.tc)
-            self.prog.append(("attn", self.q2, 0, E, self.kv2, 0, 2 * E, self.kv2, E, 2 * E, self.tc, 1))
+            self.prog.append(("attn", self.q2, 0, E, self.kv2, l * 2 * E, L * 2 * E, self.kv2, l * 2 * E + E,
+                              L * 2 * E, self.tc, 1))
             self._lin(model.conv_weight(lw(p + ".ca_out")), lb(p + ".ca_out"), self.att, E, nxt, E, T, res=cur)
             cur, nxt = nxt, cur
             ln(cur, p + ".ln3")
