@@ -580,7 +580,7 @@ def _install_capture():
         S_seen = sorted({ev[3] for ev in self.gen_events})
         if self.dpt:
             # prep + program (a conv op is GEMM + epilogue) + update
-            LAST_EVENTS["launches_per_iter"] = 2 + sum(2 if it[0] == "conv" else 1 for it in self.denoiser.prog)
+            LAST_EVENTS["launches_per_iter"] = 2 + sum(2 if it[0] in ("conv", "conv_ln") else 1 for it in self.denoiser.prog)
             LAST_EVENTS["denoise_kernel"] = {int(S): "dp-t program (conv-path GEMMs + dpt.cu)" for S in S_seen}
         else:
             LAST_EVENTS["denoiser_ops"] = list(self.denoiser.ops)

@@ -256,6 +256,12 @@ int auras_unet_mega_trace(auras_unet_plan *plan, int S, long long *trace, int *t
 int auras_conv(const auras_conv_op *op, int dtype, int S, const float *film_rows,
                int film_stride, float *scratch, int64_t scratch_floats, void *stream);
 
+/* auras_conv for a plain token-wise linear layer followed by LayerNorm
+ * (out = act(W x + b) + res, ln_out = LayerNorm(out) with eps): the DP-T
+ * decoder's residual adds fused with the next layer norm.  bf16, M <= 1024. */
+int auras_conv_ln(const auras_conv_op *op, int dtype, int S, const float *ln_gamma, const float *ln_beta,
+                  void *ln_out, int ln_pitch, float eps, float *scratch, int64_t scratch_floats, void *stream);
+
 /* fp32 scratch floats auras_conv needs for this op at batch S (the engine
  * picks its own split-K factor). */
 int64_t auras_conv_scratch_floats(const auras_conv_op *op, int dtype, int S);

@@ -66,6 +66,7 @@ _SIGNATURES = {
     "auras_ar_generate": (C.c_int, [vp, C.c_int, ip, ip, ip, C.c_int, vp, vp, f64, vp]),
     "auras_ar_finish": (C.c_int, [vp, C.c_int, C.c_int, vp, vp]),
     "auras_ring_copy_slot": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp]),
+    "auras_conv_ln": (C.c_int, [C.POINTER(ConvOp), C.c_int, C.c_int, vp, vp, vp, C.c_int, C.c_float, vp, i64, vp]),
     "auras_conv_scratch_floats": (i64, [C.POINTER(ConvOp), C.c_int, C.c_int]),
     "auras_dpt_prep": (C.c_int, [vp, vp, vp, C.c_int, vp, C.c_int, C.c_int, C.c_int, vp, vp, i64, C.c_int, vp,
                                  C.c_int, C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, vp]),

@@ -156,6 +156,74 @@ __global__ void __launch_bounds__(256) tok_epilogue(EpiArgs a) {
   }
 }
 
+// Token epilogue fused with the LayerNorm that follows a residual add (the
+// DP-T decoder, M <= 1024): one CTA per token (measured faster than 8 per
+// CTA: more CTAs in flight), one thread per channel;
+// out[n] = partials + bias + residual (bf16, stored), ln[n] = LayerNorm(out[n])
+// with fp32 statistics of the stored (rounded) values, as a separate
+// layernorm launch would compute them.
+constexpr int TLN_TOK = 1;
+__global__ void __launch_bounds__(1024) tok_epilogue_ln(EpiArgs a, const float *__restrict__ g,
+                                                         const float *__restrict__ b, __nv_bfloat16 *__restrict__ ln,
+                                                         int ln_pitch, float eps) {
+  __shared__ float red[2][TLN_TOK][32];
+  const int m = threadIdx.x, n0 = blockIdx.x * TLN_TOK;
+  const int warp = m >> 5, lane = m & 31, nw = blockDim.x >> 5;
+  const int64_t NM = (int64_t)a.N * a.M;
+  const auto *res = static_cast<const __nv_bfloat16 *>(a.res);
+  auto *out = static_cast<__nv_bfloat16 *>(a.out);
+  float y[TLN_TOK];
+#pragma unroll
+  for (int t = 0; t < TLN_TOK; ++t) {
+    const int n = n0 + t;
+    float v = 0.f;
+    if (n < a.N && m < a.M) {
+      v = a.bias ? a.bias[m] : 0.f;
+      for (int z = 0; z < a.splits; ++z) v += a.partial[z * NM + (int64_t)m * a.N + n];
+      v = activate(v, a.act);
+      if (res) v += __bfloat162float(res[(int64_t)n * a.res_pitch + a.res_coff + m]);
+      const __nv_bfloat16 hv = __float2bfloat16_rn(v);
+      out[(int64_t)n * a.out_pitch + a.out_coff + m] = hv;
+      v = __bfloat162float(hv);
+    }
+    y[t] = v;
+  }
+  // mean, then biased variance, per token (block reductions over the channels)
+  float part[TLN_TOK];
+#pragma unroll
+  for (int t = 0; t < TLN_TOK; ++t) {
+    float v = y[t];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    part[t] = v;
+  }
+  if (lane == 0)
+    for (int t = 0; t < TLN_TOK; ++t) red[0][t][warp] = part[t];
+  __syncthreads();
+  float mu[TLN_TOK];
+#pragma unroll
+  for (int t = 0; t < TLN_TOK; ++t) {
+    float sum = 0.f;
+    for (int w = 0; w < nw; ++w) sum += red[0][t][w];
+    mu[t] = sum / a.M;
+    float d = m < a.M ? y[t] - mu[t] : 0.f;
+    d *= d;
+    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    part[t] = d;
+  }
+  if (lane == 0)
+    for (int t = 0; t < TLN_TOK; ++t) red[1][t][warp] = part[t];
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < TLN_TOK; ++t) {
+    const int n = n0 + t;
+    float q = 0.f;
+    for (int w = 0; w < nw; ++w) q += red[1][t][w];
+    const float rstd = rsqrtf(q / a.M + eps);
+    if (n < a.N && m < a.M)
+      ln[(int64_t)n * ln_pitch + m] = __float2bfloat16_rn((y[t] - mu[t]) * rstd * g[m] + b[m]);
+  }
+}
+
 // ------------------------------------------------------------------ linear / GEMV
 // y[n][m] = sum_k W[m][k] * f(x[n][k]) + b[m]; one warp per output row m,
 // x staged in shared memory; weights streamed once with 16-byte loads.
@@ -393,6 +461,27 @@ extern "C" int64_t auras_conv_scratch_floats(const auras_conv_op *op, int dtype,
 }
 
 extern "C" {
+
+int auras_conv_ln(const auras_conv_op *op, int dtype, int S, const float *ln_gamma, const float *ln_beta,
+                  void *ln_out, int ln_pitch, float eps, float *scratch, int64_t scratch_floats, void *stream) {
+  if (!op || !scratch || !ln_out || dtype != AURAS_DT_BF16) { set_error("conv_ln: bad args"); return AURAS_E_ARG; }
+  if (op->gn_gamma || op->pool_out || op->film_off >= 0 || op->out_stuff || op->out_f32 || op->res_f32 ||
+      op->Ho != 1 || op->M > 1024 || op->M % 32) {
+    set_error("conv_ln: only plain 1-row token convolutions with M <= 1024, M %% 32 == 0");
+    return AURAS_E_ARG;
+  }
+  if (conv_scratch_floats(*op, S, dtype) > scratch_floats) { set_error("conv_ln: scratch too small"); return AURAS_E_ARG; }
+  ConvGemmArgs g;
+  EpiArgs e;
+  int rc = conv_op_to_args(*op, S, dtype, scratch, g, e);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  if ((rc = run_gemm(g, dtype, st))) return rc;
+  tok_epilogue_ln<<<(e.N + TLN_TOK - 1) / TLN_TOK, e.M, 0, st>>>(e, ln_gamma, ln_beta,
+                                                                static_cast<__nv_bfloat16 *>(ln_out), ln_pitch, eps);
+  AURAS_LAUNCHED("tok_epilogue_ln");
+  return AURAS_OK;
+}
 
 int auras_conv(const auras_conv_op *op, int dtype, int S, const float *film_rows, int film_stride,
                float *scratch, int64_t scratch_floats, void *stream) {

@@ -768,39 +768,48 @@ class DPTDenoiser:
         self._lin(model.conv_weight(lw("dpt.enc1")), lb("dpt.enc1"), self.c, E, self.e1, 4 * E, self.tc,
                   act=_lib.ACT_MISH)
         self._lin(model.conv_weight(lw("dpt.enc2")), lb("dpt.enc2"), self.e1, 4 * E, self.mem, E, self.tc)
-        self._lin(model.conv_weight(lw("dpt.input"), cin_pad=64), lb("dpt.input"), self.xin, 64, self.ha, E, T,
-                  res=self.pos_rep)
         # the memory does not change across the decoder layers: one GEMM projects
         # the cross-attention K|V of all layers (rows E..3E of each ca_in)
         kvw = torch.cat([w[f"dpt.l{l}.ca_in.w"][E:3 * E] for l in range(L)])
         kvb = torch.cat([w[f"dpt.l{l}.ca_in.b"][E:3 * E] for l in range(L)])
         self._lin(model.conv_weight(kvw.reshape(*kvw.shape, 1, 1)), model.f32(kvb), self.mem, E, self.kv2,
                   L * 2 * E, self.tc)
+        fuse = os.environ.get("AURAS_DPT_FUSE_LN", "1") == "1"
+
+        def lnp(g):
+            return (model.f32(w[g + ".g"]), model.f32(w[g + ".b"]))
+
+        def res_ln(wconv, bias, inp, in_pitch, out, res, g):
+            """residual GEMM followed by LayerNorm g into self.ln: one fused
+            epilogue (auras_conv_ln) or GEMM + layernorm launches"""
+            self._lin(wconv, bias, inp, in_pitch, out, E, T, res=res, ln=lnp(g) if fuse else None)
+            if not fuse:
+                ln(out, g)
+
         cur, nxt = self.ha, self.hb
+        res_ln(model.conv_weight(lw("dpt.input"), cin_pad=64), lb("dpt.input"), self.xin, 64, cur, self.pos_rep,
+               "dpt.l0.ln1")
         for l in range(cfg.dpt_layers):
             p = f"dpt.l{l}"
-            ln(cur, p + ".ln1")
             self._lin(model.conv_weight(lw(p + ".sa_in")), lb(p + ".sa_in"), self.ln, E, self.qkv, 3 * E, T)
             self.prog.append(("attn", self.qkv, 0, 3 * E, self.qkv, E, 3 * E, self.qkv, 2 * E, 3 * E, T, 0))
-            self._lin(model.conv_weight(lw(p + ".sa_out")), lb(p + ".sa_out"), self.att, E, nxt, E, T, res=cur)
+            res_ln(model.conv_weight(lw(p + ".sa_out")), lb(p + ".sa_out"), self.att, E, nxt, cur, p + ".ln2")
             cur, nxt = nxt, cur
-            ln(cur, p + ".ln2")
             self._lin(model.conv_weight(lw(p + ".ca_in", (0, E))), lb(p + ".ca_in", (0, E)), self.ln, E, self.q2, E, T)
             self.prog.append(("attn", self.q2, 0, E, self.kv2, l * 2 * E, L * 2 * E, self.kv2, l * 2 * E + E,
                               L * 2 * E, self.tc, 1))
-            self._lin(model.conv_weight(lw(p + ".ca_out")), lb(p + ".ca_out"), self.att, E, nxt, E, T, res=cur)
+            res_ln(model.conv_weight(lw(p + ".ca_out")), lb(p + ".ca_out"), self.att, E, nxt, cur, p + ".ln3")
             cur, nxt = nxt, cur
-            ln(cur, p + ".ln3")
             self._lin(model.conv_weight(lw(p + ".ff1")), lb(p + ".ff1"), self.ln, E, self.ff, 4 * E, T,
                       act=_lib.ACT_GELU)
-            self._lin(model.conv_weight(lw(p + ".ff2")), lb(p + ".ff2"), self.ff, 4 * E, nxt, E, T, res=cur)
+            nxt_ln = f"dpt.l{l + 1}.ln1" if l + 1 < cfg.dpt_layers else "dpt.lnf"
+            res_ln(model.conv_weight(lw(p + ".ff2")), lb(p + ".ff2"), self.ff, 4 * E, nxt, cur, nxt_ln)
             cur, nxt = nxt, cur
-        ln(cur, "dpt.lnf")
         self._lin(model.conv_weight(lw("dpt.head")), lb("dpt.head"), self.ln, E, self.eps_bf, cfg.action_dim, T,
                   out_f32=self.eps)
         self.scratch = torch.zeros(max(1, self.max_scratch), dtype=torch.float32, device=dev)
 
-    def _lin(self, wconv, bias, inp, in_pitch, out, out_pitch, rows, act=0, res=None, out_f32=None):
+    def _lin(self, wconv, bias, inp, in_pitch, out, out_pitch, rows, act=0, res=None, out_f32=None, ln=None):
         wm, cp, _, _, kp = wconv
         M = wm.shape[0]
         op = _op(w=wm.data_ptr(), bias=bias.data_ptr(), inp=inp.data_ptr(), out=out.data_ptr(), M=M, Cin=cp, Kp=kp,
@@ -813,7 +822,7 @@ class DPTDenoiser:
             op.out_f32 = out_f32.data_ptr()
         need = _lib.load().auras_conv_scratch_floats(_lib.C.byref(op), self.m.dt, self.s_max)
         self.max_scratch = max(self.max_scratch, int(need))
-        self.prog.append(("conv", op))
+        self.prog.append(("conv", op) if ln is None else ("conv_ln", op, ln[0], ln[1]))
 
     def iterate(self, S, agents, lanes, steps, x_lanes, lanes_per_agent, ring, ring_agent_stride, slot_floats,
                 fetched, noise_lanes, sched, stream):
@@ -832,6 +841,11 @@ class DPTDenoiser:
             if kind == "conv":
                 _lib.check(lib.auras_conv(_lib.C.byref(item[1]), self.m.dt, S, None, 0, self.scratch.data_ptr(),
                                           self.scratch.numel(), st), "dpt conv")
+            elif kind == "conv_ln":
+                _, op, g, b = item
+                _lib.check(lib.auras_conv_ln(_lib.C.byref(op), self.m.dt, S, g.data_ptr(), b.data_ptr(),
+                                             self.ln.data_ptr(), E, 1e-5, self.scratch.data_ptr(),
+                                             self.scratch.numel(), st), "dpt conv_ln")
             elif kind == "ln":
                 _, src, g, b = item
                 _lib.check(lib.auras_layernorm(src.data_ptr(), E, self.ln.data_ptr(), E, 0, g.data_ptr(), b.data_ptr(),
