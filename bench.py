@@ -589,7 +589,7 @@ def _install_capture():
             LAST_EVENTS["denoise_kernel"] = {int(S): names.get(int(self.lib.auras_unet_kernel_for(self.plan, S)), "?")
                                              for S in S_seen}
         LAST_EVENTS["encoder_launches"] = 1 + sum(
-            (2 if item[0] == "conv" else 1) for g in self.encoder.groups.values() for item in g)
+            (2 if item[0] in ("conv", "conv_ln") else 1) for g in self.encoder.groups.values() for item in g)
         orig_close(self)
     D.DPSession.close = close
 

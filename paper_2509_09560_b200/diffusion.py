@@ -617,29 +617,42 @@ class ViTEncoder:
                    self.patches, D, g, g)
         self.groups["embed"].append(("tokens",))
         per = cfg.vit_depth // 4
+        # residual adds fused with the LayerNorm that follows them (auras_conv_ln):
+        # proj -> ln2, fc2 -> the next block's ln1.  Off by default here: at 768
+        # channels x 200 tokens the transposing token epilogue + a layernorm
+        # launch measured faster (1.55 vs 1.71 ms per frame); on for the DP-T
+        # (256 channels x 16 tokens per sample), where it wins 13 %
+        fuse = os.environ.get("AURAS_VIT_FUSE_LN", "0") == "1"
+
+        def lnp(name):
+            return (model.f32(w[name + ".g"]), model.f32(w[name + ".b"]))
+
         for i in range(cfg.vit_depth):
             gname = f"blocks{min(i // per, 3)}"
             p = f"vit.b{i}"
             lin = lambda name: model.conv_weight(w[name + ".w"].reshape(*w[name + ".w"].shape, 1, 1))  # noqa: E731
-            self.groups[gname].append(("ln", self.xa, self.ln, model.f32(w[p + ".ln1.g"]),
-                                       model.f32(w[p + ".ln1.b"])))
+            if i == 0 or not fuse:
+                self.groups[gname].append(("ln", self.xa, self.ln) + lnp(p + ".ln1"))
             wm, cp, _, _, _ = lin(p + ".qkv")
             self._tok(gname, wm, model.f32(w[p + ".qkv.b"]), self.ln, D, cp, self.qkv, 3 * D)
             self.groups[gname].append(("attn",))
             wm, cp, _, _, _ = lin(p + ".proj")
-            self._tok(gname, wm, model.f32(w[p + ".proj.b"]), self.att, D, cp, self.xb, D, res=self.xa)
-            self.groups[gname].append(("ln", self.xb, self.ln, model.f32(w[p + ".ln2.g"]),
-                                       model.f32(w[p + ".ln2.b"])))
+            self._tok(gname, wm, model.f32(w[p + ".proj.b"]), self.att, D, cp, self.xb, D, res=self.xa,
+                      ln=lnp(p + ".ln2") if fuse else None)
+            if not fuse:
+                self.groups[gname].append(("ln", self.xb, self.ln) + lnp(p + ".ln2"))
             wm, cp, _, _, _ = lin(p + ".fc1")
             self._tok(gname, wm, model.f32(w[p + ".fc1.b"]), self.ln, D, cp, self.hid, cfg.vit_mlp,
                       act=_lib.ACT_GELU)
             wm, cp, _, _, _ = lin(p + ".fc2")
-            self._tok(gname, wm, model.f32(w[p + ".fc2.b"]), self.hid, cfg.vit_mlp, cp, self.xa, D, res=self.xb)
+            nxt = lnp(f"vit.b{i + 1}.ln1") if (fuse and i + 1 < cfg.vit_depth) else None
+            self._tok(gname, wm, model.f32(w[p + ".fc2.b"]), self.hid, cfg.vit_mlp, cp, self.xa, D, res=self.xb,
+                      ln=nxt)
         self.norm = (model.f32(w["vit.norm.g"]), model.f32(w["vit.norm.b"]))
         self.groups["blocks3"].append(("final",))
         self.scratch = torch.zeros(max(1, self.max_scratch), dtype=torch.float32, device=dev)
 
-    def _tok(self, group, wm, bias, inp, in_pitch, cin, out, out_pitch, act=0, res=None):
+    def _tok(self, group, wm, bias, inp, in_pitch, cin, out, out_pitch, act=0, res=None, ln=None):
         """A token-wise linear layer as a 1-row convolution over the (padded)
         token axis: with N a multiple of 8 it takes the TMA 1-D tcgen05 path;
         the epilogue is the token-wise transposing one (cta_target > 0), which
@@ -647,10 +660,10 @@ class ViTEncoder:
         (perception runs alone while the denoise kernel is not resident)."""
         N = self.n_tok
         self._conv(group, wm, bias, inp, in_pitch, 1, N, cin, 1, 1, 1, out, out_pitch, 1, N, act=act, res=res,
-                   cta_target=148)
+                   cta_target=148, ln=ln)
 
     def _conv(self, group, wm, bias, inp, in_pitch, H, W, cin, kh, kw, stride, out, out_pitch, Ho, Wo,
-              act=0, res=None, S=None, cta_target=0):
+              act=0, res=None, S=None, cta_target=0, ln=None):
         M, kp = wm.shape
         S = self.A if S is None else S
         N = S * Ho * Wo
@@ -662,7 +675,7 @@ class ViTEncoder:
             op.res, op.res_pitch, op.res_coff = res.data_ptr(), out_pitch, 0
         need = _lib.load().auras_conv_scratch_floats(_lib.C.byref(op), self.m.dt, S)
         self.max_scratch = max(self.max_scratch, int(need))
-        self.groups[group].append(("conv", op, S))
+        self.groups[group].append(("conv", op, S) if ln is None else ("conv_ln", op, S, ln[0], ln[1]))
 
     def run(self, lo, hi, stream):
         lib = _lib.load()
@@ -680,6 +693,11 @@ class ViTEncoder:
                 if kind == "conv":
                     _lib.check(lib.auras_conv(_lib.C.byref(item[1]), self.m.dt, item[2], None, 0,
                                               self.scratch.data_ptr(), self.scratch.numel(), st), "vit conv")
+                elif kind == "conv_ln":
+                    _, op, S_, g, b = item
+                    _lib.check(lib.auras_conv_ln(_lib.C.byref(op), self.m.dt, S_, g.data_ptr(), b.data_ptr(),
+                                                 self.ln.data_ptr(), D, 1e-6, self.scratch.data_ptr(),
+                                                 self.scratch.numel(), st), "vit conv_ln")
                 elif kind == "tokens":
                     _lib.check(lib.auras_vit_tokens(self.patches.data_ptr(), self.cls.data_ptr(),
                                                     self.pos.data_ptr(), self.xa.data_ptr(), self.A, N,

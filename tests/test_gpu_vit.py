@@ -169,3 +169,21 @@ def test_vit_dpt_two_agents_and_sequential_match_oracle():
     g = np.array([x.values for x in res.actions])
     r = np.array([x.values for x in ref.actions])
     assert g.shape == r.shape and float(np.abs(g - r).max() / np.abs(r).max()) <= 6e-2
+
+
+def test_vit_encoder_fused_layernorm_path(monkeypatch):
+    """The residual + LayerNorm fused epilogue (auras_conv_ln) on the ViT
+    program gives the same feature as the default path within bf16 noise."""
+    cfg = D.PRESETS["vit"]
+    w = vit_weights()
+    model = D.DeviceModel(cfg, w, "bf16")
+    imgs = np.random.default_rng(5).integers(0, 256, (1, 3, 224, 224), dtype=np.uint8)
+    feats = []
+    for fuse in ("0", "1"):
+        monkeypatch.setenv("AURAS_VIT_FUSE_LN", fuse)
+        enc = D.ViTEncoder(model, 1)
+        enc.img.copy_(torch.from_numpy(imgs))
+        enc.run(0, len(enc.GROUPS), torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        feats.append(enc.feat.cpu().numpy()[0])
+    assert np.linalg.norm(feats[0] - feats[1]) / np.linalg.norm(feats[0]) <= 2e-2
