@@ -27,14 +27,14 @@ in `diffusion.py`.
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Optional
 
 import numpy as np
 
 from . import _lib
 from .context import ContextKind, ContextStore
-from .errors import IncompleteGeneration, ShapeMismatch
+from .errors import ShapeMismatch
 
 
 @dataclass(frozen=True)
