@@ -498,8 +498,9 @@ int auras_conv(const auras_conv_op *op, int dtype, int S, const float *film_rows
   }
   cudaStream_t st = as_stream(stream);
   if ((rc = run_gemm(g, dtype, st))) return rc;
+  // (any Ho: NHWC rows ((s * Ho + y) * Wo + x) are the GEMM's n in order)
   if (op->cta_target > 0 && !e.gn_gamma && !e.pool_out && e.film_off < 0 && !e.out_stuff && !e.out_f32 &&
-      !e.res_f32 && op->Ho == 1 && e.out) {
+      !e.res_f32 && e.out) {
     dim3 grid((e.M + 31) / 32, (e.N + 31) / 32);
     if (dtype == AURAS_DT_BF16) tok_epilogue<__nv_bfloat16><<<grid, 256, 0, st>>>(e);
     else tok_epilogue<float><<<grid, 256, 0, st>>>(e);

@@ -614,7 +614,7 @@ class ViTEncoder:
         self.pos = model.f32(w["vit.pos"])
         wm, cp, kh, kw, kp = model.conv_weight(w["vit.patch.w"], cin_pad=8)
         self._conv("embed", wm, model.f32(w["vit.patch.b"]), self.x0, 8, H, H, cp, kh, kw, P,
-                   self.patches, D, g, g)
+                   self.patches, D, g, g, cta_target=148)
         self.groups["embed"].append(("tokens",))
         per = cfg.vit_depth // 4
         # residual adds fused with the LayerNorm that follows them (auras_conv_ln):
