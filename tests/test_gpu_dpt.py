@@ -67,3 +67,24 @@ def test_dpt_iteration_matches_oracle():
 
 def _lib_round(x, m):
     return (x + m - 1) // m * m
+
+
+def test_small_vit_dpt_ddim_pipeline_matches_oracle():
+    """The DP-T path with a DDIM scheduler (16 steps), a 2-block ViT at 64x64
+    and a 2-layer denoiser: pipelined at depth 4 vs the oracle pipeline."""
+    from oracle import schedule as osched
+    from paper_2509_09560_b200 import PipelineConfig, run_pipelined
+    cfg = D.DPConfig(name="dpt_ddim_test", encoder="vit_b16", image_hw=64, feat_dim=768, action_dim=7,
+                     denoiser="transformer", scheduler="ddim", num_inference_steps=16, vit_depth=4, dpt_layers=2)
+    w = D.init_weights(cfg, 3, device="cpu")
+    pol = D.make_diffusion_policy(cfg, dtype="bf16", weights=w)
+    gen = pol.generation
+    pcfg = dict(pp_perception=1, pp_generation=4, fetch_offset=-1)
+    res = run_pipelined(PipelineConfig(**pcfg), pol, None, 8)
+    orc = dp_model.OracleDP(gen.weights, gen.cfg, gen.seed, 0, pol.perception.layer_costs, gen.step_cost)
+    ref = osched.run_pipelined(pcfg, orc, None, 8)
+    g = np.array([a.values for a in res.actions])
+    r = np.array([a.values for a in ref.actions])
+    assert g.shape == r.shape and len(g) > 0
+    assert float(np.abs(g - r).max() / np.abs(r).max()) <= 6e-2
+    assert [q.context_versions for q in res.requests] == [q.context_versions for q in ref.requests]
