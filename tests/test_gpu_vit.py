@@ -187,3 +187,21 @@ def test_vit_encoder_fused_layernorm_path(monkeypatch):
         torch.cuda.synchronize()
         feats.append(enc.feat.cpu().numpy()[0])
     assert np.linalg.norm(feats[0] - feats[1]) / np.linalg.norm(feats[0]) <= 2e-2
+
+
+def test_vit_and_dpt_refuse_fp32():
+    """configs[3] is a bf16 configuration: the ViT encoder and the DP-T
+    denoiser refuse the fp32 path loudly instead of falling back."""
+    from paper_2509_09560_b200 import ConfigInvalid
+    cfg = D.PRESETS["vit_dpt"]
+    model = D.DeviceModel(cfg, vit_dpt_weights(), "fp32")
+    with pytest.raises(ConfigInvalid):
+        D.ViTEncoder(model, 1)
+    with pytest.raises(ConfigInvalid):
+        D.DPTDenoiser(model, 4)
+
+
+def vit_dpt_weights():
+    if "vit_dpt" not in _W:
+        _W["vit_dpt"] = D.init_weights(D.PRESETS["vit_dpt"], 0, device="cpu")
+    return _W["vit_dpt"]
