@@ -299,6 +299,11 @@ int auras_dpt_prep(const int *agents, const int *lanes, const int *steps, int S,
                    int64_t ring_agent_stride, int slot_floats, const int64_t *fetched, int tok_w, int n_obs,
                    void *gcbuf, int gpad, const float *temb, int E, void *c, const float *cond_pos, void *stream);
 int auras_dpt_cond(const void *cobs, void *c, const float *cond_pos, int S, int n_obs, int E, void *stream);
+/* kv2[s] = [kvt[steps[s]]; kvo[agents[s]][0..tc-2]]: rows of lw bf16 (the
+ * cross-attention K|V of every layer), time row by inference step, observation
+ * rows computed once per frame. */
+int auras_dpt_kv_gather(void *kv2, const void *kvt, const void *kvo, const int *agents, const int *steps, int S,
+                        int tc, int lw, void *stream);
 /* softmax(q k^T / sqrt(dh) + mask) v, key j visible to query n iff
  * j <= n + mask_off; rows (s * Nq + n) * ld + head * dh; Nk <= 32. */
 int auras_attention(const void *q, int ldq, const void *k, int ldk, const void *v, int ldv, void *out, int ldo,

@@ -71,6 +71,7 @@ _SIGNATURES = {
     "auras_dpt_prep": (C.c_int, [vp, vp, vp, C.c_int, vp, C.c_int, C.c_int, C.c_int, vp, vp, i64, C.c_int, vp,
                                  C.c_int, C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, vp]),
     "auras_dpt_cond": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, vp]),
+    "auras_dpt_kv_gather": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, vp]),
     "auras_attention": (C.c_int, [vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, C.c_int, C.c_int, C.c_int, C.c_int,
                                   C.c_int, C.c_int, C.c_int, vp]),
     "auras_dpt_update": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_int, vp, vp, C.c_int, C.c_int, C.c_int,

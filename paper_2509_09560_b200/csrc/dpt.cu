@@ -47,6 +47,19 @@ __global__ void dpt_prep_kernel(const int *__restrict__ agents, const int *__res
     c[(int64_t)s * (1 + n_obs) * E + e] = __float2bfloat16_rn(temb[(int64_t)i * E + e] + cond_pos[e]);
 }
 
+// Per iteration: the cross-attention K|V rows of every sample from the time
+// table (by inference step) and the frame's observation rows (by agent).
+__global__ void dpt_kv_gather_kernel(__nv_bfloat16 *__restrict__ kv2, const __nv_bfloat16 *__restrict__ kvt,
+                                     const __nv_bfloat16 *__restrict__ kvo, const int *__restrict__ agents,
+                                     const int *__restrict__ steps, int tc, int lw) {
+  const int s = blockIdx.x / tc, r = blockIdx.x % tc;
+  const __nv_bfloat16 *src = r == 0 ? kvt + (int64_t)steps[s] * lw : kvo + ((int64_t)agents[s] * (tc - 1) + r - 1) * lw;
+  __nv_bfloat16 *dst = kv2 + ((int64_t)s * tc + r) * lw;
+  const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+  uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+  for (int i = threadIdx.x; i < lw / 8; i += blockDim.x) d4[i] = s4[i];
+}
+
 __global__ void dpt_cond_kernel(const __nv_bfloat16 *__restrict__ cobs, __nv_bfloat16 *__restrict__ c,
                                 const float *__restrict__ cond_pos, int S, int n_obs, int E) {
   const int64_t total = (int64_t)S * n_obs * E;
@@ -199,5 +212,19 @@ extern "C" int auras_dpt_update(const float *eps, int eps_pitch, const int *agen
   dpt_update_kernel<<<S, 128, 0, as_stream(stream)>>>(eps, eps_pitch, agents, lanes, steps, x_lanes, noise_lanes,
                                                       lanes_per_agent, horizon, adim, *sched);
   AURAS_LAUNCHED("dpt_update");
+  return AURAS_OK;
+}
+
+extern "C" int auras_dpt_kv_gather(void *kv2, const void *kvt, const void *kvo, const int *agents, const int *steps,
+                                   int S, int tc, int lw, void *stream) {
+  if (S < 1 || tc < 1 || lw % 8) {
+    set_error("dpt_kv_gather: bad sizes S=%d tc=%d lw=%d", S, tc, lw);
+    return AURAS_E_ARG;
+  }
+  dpt_kv_gather_kernel<<<S * tc, 256, 0, as_stream(stream)>>>(static_cast<__nv_bfloat16 *>(kv2),
+                                                              static_cast<const __nv_bfloat16 *>(kvt),
+                                                              static_cast<const __nv_bfloat16 *>(kvo), agents, steps,
+                                                              tc, lw);
+  AURAS_LAUNCHED("dpt_kv_gather");
   return AURAS_OK;
 }

@@ -780,6 +780,12 @@ class DPTDenoiser:
         def ln(src, g):
             self.prog.append(("ln", src, model.f32(w[g + ".g"]), model.f32(w[g + ".b"])))
 
+        # cond tokens -> memory -> cross-attention K|V of every layer.  The time row
+        # depends only on the inference step (a table, below) and the observation
+        # rows only on the fetched context, so this program runs once per frame
+        # (frame_cond) and every iteration gathers its rows (dpt_kv_gather).
+        self.hoist = os.environ.get("AURAS_DPT_HOIST", "1") == "1"
+        self.cond_prog, self.prog = self.prog, []
         self._lin(model.conv_weight(lw("dpt.cond_obs"), cin_pad=self.gpad), lb("dpt.cond_obs"), self.gcbuf, self.gpad,
                   self.cobs, E, self.n_obs)
         self.prog.append(("cond",))
@@ -792,6 +798,22 @@ class DPTDenoiser:
         kvb = torch.cat([w[f"dpt.l{l}.ca_in.b"][E:3 * E] for l in range(L)])
         self._lin(model.conv_weight(kvw.reshape(*kvw.shape, 1, 1)), model.f32(kvb), self.mem, E, self.kv2,
                   L * 2 * E, self.tc)
+        self.cond_prog, self.prog = self.prog, self.cond_prog
+        if self.hoist:
+            # time-row table with the per-iteration program's arithmetic: bf16
+            # operands and activations, fp32 accumulation
+            W = model.w
+
+            def r16(t):
+                return t.to(td).float()
+
+            c0 = r16(self.temb + W["dpt.cond_pos"][0])
+            h = r16(torch.nn.functional.mish(c0 @ r16(W["dpt.enc1.w"]).T + W["dpt.enc1.b"]))
+            m0 = r16(h @ r16(W["dpt.enc2.w"]).T + W["dpt.enc2.b"])
+            self.kvt = (m0 @ r16(kvw.to(dev)).T + kvb.to(dev)).to(td).contiguous()      # [n_steps][L * 2E]
+            self.kvo = z(s_max, self.n_obs, L * 2 * E)
+            self.ar = torch.arange(s_max, dtype=torch.int32, device=dev)
+            self.zr = torch.zeros(s_max, dtype=torch.int32, device=dev)
         fuse = os.environ.get("AURAS_DPT_FUSE_LN", "1") == "1"
 
         def lnp(g):
@@ -854,7 +876,35 @@ class DPTDenoiser:
                                       self.xin.data_ptr(), ring, ring_agent_stride, slot_floats, fetched, self.tok_w,
                                       self.n_obs, self.gcbuf.data_ptr(), self.gpad, self.temb.data_ptr(), E,
                                       self.c.data_ptr(), self.cond_pos.data_ptr(), st), "dpt_prep")
-        for item in self.prog:
+        if self.hoist:
+            _lib.check(lib.auras_dpt_kv_gather(self.kv2.data_ptr(), self.kvt.data_ptr(), self.kvo.data_ptr(), agents,
+                                               steps, S, self.tc, self.kv2.shape[-1], st), "dpt_kv_gather")
+        self._run(self.prog if self.hoist else self.cond_prog + self.prog, S, st)
+        _lib.check(lib.auras_dpt_update(self.eps.data_ptr(), cfg.action_dim, agents, lanes, steps, S, x_lanes,
+                                        noise_lanes, lanes_per_agent, cfg.horizon, cfg.action_dim, _lib.C.byref(sched),
+                                        st), "dpt_update")
+
+    def frame_cond(self, A, x_lanes, lanes_per_agent, ring, ring_agent_stride, slot_floats, fetched, stream):
+        """Once per frame (hoisted mode): the observation rows' cross-attention
+        K|V of the A agents from the fetched context, into kvo."""
+        if not self.hoist:
+            return
+        lib = _lib.load()
+        cfg = self.m.cfg
+        st = stream.cuda_stream
+        _lib.check(lib.auras_dpt_prep(self.ar.data_ptr(), self.zr.data_ptr(), self.zr.data_ptr(), A, x_lanes,
+                                      lanes_per_agent, cfg.horizon, cfg.action_dim, self.xin.data_ptr(), ring,
+                                      ring_agent_stride, slot_floats, fetched, self.tok_w, self.n_obs,
+                                      self.gcbuf.data_ptr(), self.gpad, self.temb.data_ptr(), self.E,
+                                      self.c.data_ptr(), self.cond_pos.data_ptr(), st), "dpt_prep")
+        self._run(self.cond_prog, A, st)
+        with self.m.torch.cuda.stream(stream):
+            self.kvo[:A].copy_(self.kv2[:A, 1:])
+
+    def _run(self, prog, S, st):
+        lib = _lib.load()
+        E = self.E
+        for item in prog:
             kind = item[0]
             if kind == "conv":
                 _lib.check(lib.auras_conv(_lib.C.byref(item[1]), self.m.dt, S, None, 0, self.scratch.data_ptr(),
@@ -882,9 +932,6 @@ class DPTDenoiser:
                 _lib.check(lib.auras_attention(qb.data_ptr() + 2 * qo, ldq, kb.data_ptr() + 2 * ko, ldk,
                                                vb.data_ptr() + 2 * vo, ldv, self.att.data_ptr(), E, S, self.T, nk,
                                                self.H, E // self.H, moff, st), "attention")
-        _lib.check(lib.auras_dpt_update(self.eps.data_ptr(), cfg.action_dim, agents, lanes, steps, S, x_lanes,
-                                        noise_lanes, lanes_per_agent, cfg.horizon, cfg.action_dim, _lib.C.byref(sched),
-                                        st), "dpt_update")
 
 
 class Denoiser:
@@ -1391,6 +1438,9 @@ class DPSession:
         base = dst.data_ptr()
         row = 4 * self.s_max
         cap = self.store.capacity
+        # observation rows of the cross-attention memory: once per frame
+        self.denoiser.frame_cond(self.A, self.x.data_ptr(), self.R, self.store.payload.data_ptr(),
+                                 cap * self.slot_floats, self.slot_floats, self.fetched.data_ptr(), self.g)
         for r in range(iters):
             b = base + r * 3 * row
 
