@@ -45,6 +45,36 @@ def _mish(x):
     return x * torch.tanh(F.softplus(x))
 
 
+def _id(x):
+    return x
+
+
+def _bf16(x):
+    """Round to bf16 (round-to-nearest-even) and back: a tensor stored in bf16."""
+    return x.to(torch.bfloat16).to(torch.float32)
+
+
+# Weights the B200 bf16 path holds in bf16 (the tensor-core operands and the
+# FiLM / time-MLP GEMV weights); everything else (biases, GroupNorm affine,
+# the final 1x1 output conv, the ViT / DP-T transformers) stays fp32.
+_BF16_WEIGHT_SUFFIXES = (".w",)
+_FP32_WEIGHTS = ("unet.final.out.w",)
+
+
+def bf16_weights(w):
+    """The bf16-faithful oracle's weight dict: every conv / FiLM / time-MLP
+    weight of the CNN policy rounded to bf16 exactly as
+    DeviceModel.conv_weight / Denoiser._build_tables store them."""
+    out = {}
+    for k, v in w.items():
+        cnn = k.startswith("enc.") or k.startswith("unet.")
+        if cnn and k.endswith(_BF16_WEIGHT_SUFFIXES) and k not in _FP32_WEIGHTS:
+            out[k] = _bf16(v)
+        else:
+            out[k] = v
+    return out
+
+
 def _gn(x, w, name, groups):
     return F.group_norm(x, groups, w[name + ".g"], w[name + ".b"], eps=1e-5)
 
@@ -80,24 +110,30 @@ def encode_vit(w, img_u8: np.ndarray, pos) -> torch.Tensor:
     return torch.cat([x[0, 0], torch.as_tensor(np.asarray(pos, dtype=np.float32))])
 
 
-def encode(w, img_u8: np.ndarray, pos) -> torch.Tensor:
+def encode(w, img_u8: np.ndarray, pos, store=_id) -> torch.Tensor:
     """ResNet-18 with GroupNorm(C/16) and no fc -> [512 feature, agent_pos]
-    (the ViT-B/16 encoder when the weights hold one)."""
+    (the ViT-B/16 encoder when the weights hold one).  `store` is applied
+    wherever the device stores an activation tensor (identity: fp32 oracle;
+    _bf16: the bf16-faithful oracle -- the image, every block output; the
+    pooled feature is averaged from the unrounded fp32 epilogue values)."""
     if "vit.patch.w" in w:
         return encode_vit(w, img_u8, pos)
-    x = torch.from_numpy(np.asarray(img_u8)).float()[None] * (2.0 / 255.0) - 1.0
-    x = F.relu(_gn(F.conv2d(x, w["enc.conv1.w"], stride=2, padding=3), w, "enc.gn1", 4))
+    x = store(torch.from_numpy(np.asarray(img_u8)).float()[None] * (2.0 / 255.0) - 1.0)
+    x = store(F.relu(_gn(F.conv2d(x, w["enc.conv1.w"], stride=2, padding=3), w, "enc.gn1", 4)))
     x = F.max_pool2d(x, 3, 2, 1)
+    n_blocks = 2 * len(RESNET)
     for li, (c, stride) in enumerate(RESNET, start=1):
         for bi in range(2):
             p = f"enc.layer{li}.{bi}"
             s = stride if bi == 0 else 1
-            y = F.relu(_gn(F.conv2d(x, w[p + ".conv1.w"], stride=s, padding=1), w, p + ".gn1", c // 16))
+            y = store(F.relu(_gn(F.conv2d(x, w[p + ".conv1.w"], stride=s, padding=1), w, p + ".gn1", c // 16)))
             y = _gn(F.conv2d(y, w[p + ".conv2.w"], padding=1), w, p + ".gn2", c // 16)
             idt = x
             if p + ".ds.w" in w:
-                idt = _gn(F.conv2d(x, w[p + ".ds.w"], stride=s), w, p + ".dsgn", c // 16)
+                idt = store(_gn(F.conv2d(x, w[p + ".ds.w"], stride=s), w, p + ".dsgn", c // 16))
             x = F.relu(y + idt)
+            if 2 * (li - 1) + bi + 1 < n_blocks:
+                x = store(x)
     feat = x.mean(dim=(2, 3))[0]
     return torch.cat([feat, torch.as_tensor(np.asarray(pos, dtype=np.float32))])
 
@@ -112,41 +148,49 @@ def _sinusoidal(t: int, dim: int) -> torch.Tensor:
     return torch.cat([arg.sin(), arg.cos()])[None]
 
 
-def _block(w, name, x, cond, k, groups):
+def _block(w, name, x, cond, k, groups, store=_id):
     p = "unet." + name
     h = _mish(_gn(F.conv1d(x, w[p + ".c1.w"], w[p + ".c1.b"], padding=k // 2), w, p + ".g1", groups))
     e = F.linear(_mish(cond), w[p + ".film.w"], w[p + ".film.b"])
     co = h.shape[1]
-    h = e[:, :co, None] * h + e[:, co:, None]
+    h = store(e[:, :co, None] * h + e[:, co:, None])
     h = _mish(_gn(F.conv1d(h, w[p + ".c2.w"], w[p + ".c2.b"], padding=k // 2), w, p + ".g2", groups))
     res = F.conv1d(x, w[p + ".res.w"], w[p + ".res.b"]) if p + ".res.w" in w else x
-    return h + res
+    return store(h + res)
 
 
-def unet_eps(w, cfg, x: torch.Tensor, timestep: int, gc: torch.Tensor) -> torch.Tensor:
-    """ConditionalUnet1D forward: x (horizon, action_dim) -> eps (horizon, action_dim)."""
+def unet_eps(w, cfg, x: torch.Tensor, timestep: int, gc: torch.Tensor, store=_id) -> torch.Tensor:
+    """ConditionalUnet1D forward: x (horizon, action_dim) -> eps (horizon, action_dim).
+
+    `store` is applied wherever the device stores an activation tensor:
+    identity for the fp32 oracle; _bf16 for the bf16-faithful oracle, which
+    with bf16_weights() reproduces the tensor-core path's rounding points --
+    the conv input x_t, each block's conv1 (GN, Mish, FiLM) and conv2 (GN,
+    Mish, + residual) outputs, down/up-sampling outputs and the final block's
+    output; the 1x1 residual conv output, FiLM rows, GroupNorm statistics,
+    accumulation, eps and the scheduler update stay fp32."""
     k, g = cfg.kernel_size, cfg.n_groups
     temb = F.linear(_mish(F.linear(_sinusoidal(timestep, cfg.dsed), w["unet.temb.l1.w"],
                                    w["unet.temb.l1.b"])), w["unet.temb.l2.w"], w["unet.temb.l2.b"])
     cond = torch.cat([temb, gc[None]], dim=-1)
-    h = x.T[None]
+    h = store(x.T[None])
     L = len(cfg.down_dims)
     skips = []
     for i in range(L):
-        h = _block(w, f"down{i}.0", h, cond, k, g)
-        h = _block(w, f"down{i}.1", h, cond, k, g)
+        h = _block(w, f"down{i}.0", h, cond, k, g, store)
+        h = _block(w, f"down{i}.1", h, cond, k, g, store)
         skips.append(h)
         if i < L - 1:
-            h = F.conv1d(h, w[f"unet.down{i}.ds.w"], w[f"unet.down{i}.ds.b"], stride=2, padding=1)
-    h = _block(w, "mid.0", h, cond, k, g)
-    h = _block(w, "mid.1", h, cond, k, g)
+            h = store(F.conv1d(h, w[f"unet.down{i}.ds.w"], w[f"unet.down{i}.ds.b"], stride=2, padding=1))
+    h = _block(w, "mid.0", h, cond, k, g, store)
+    h = _block(w, "mid.1", h, cond, k, g, store)
     for i in range(L - 1):
         h = torch.cat([h, skips.pop()], dim=1)
-        h = _block(w, f"up{i}.0", h, cond, k, g)
-        h = _block(w, f"up{i}.1", h, cond, k, g)
-        h = F.conv_transpose1d(h, w[f"unet.up{i}.us.w"], w[f"unet.up{i}.us.b"], stride=2, padding=1)
-    h = _mish(_gn(F.conv1d(h, w["unet.final.c.w"], w["unet.final.c.b"], padding=k // 2), w,
-                  "unet.final.g", g))
+        h = _block(w, f"up{i}.0", h, cond, k, g, store)
+        h = _block(w, f"up{i}.1", h, cond, k, g, store)
+        h = store(F.conv_transpose1d(h, w[f"unet.up{i}.us.w"], w[f"unet.up{i}.us.b"], stride=2, padding=1))
+    h = store(_mish(_gn(F.conv1d(h, w["unet.final.c.w"], w["unet.final.c.b"], padding=k // 2), w,
+                        "unet.final.g", g)))
     h = F.conv1d(h, w["unet.final.out.w"], w["unet.final.out.b"])
     return h[0].T
 
@@ -278,8 +322,8 @@ def synthetic_frame(cfg, seed, agent, frame):
 
 
 class OraclePerception:
-    def __init__(self, w, cfg, layer_costs):
-        self.w, self.cfg = w, cfg
+    def __init__(self, w, cfg, layer_costs, store=_id):
+        self.w, self.cfg, self.store = w, cfg, store
         self.layer_costs = tuple(layer_costs)
         self.layers = self.layer_costs
         self.prev = None
@@ -296,7 +340,7 @@ class OraclePerception:
 
     def finalize(self, latent, obs):
         with torch.no_grad():
-            h = encode(self.w, obs.image, obs.vector)
+            h = encode(self.w, obs.image, obs.vector, self.store)
         if self.cfg.n_obs_steps == 2:
             old = h if self.prev is None else self.prev
             gc = torch.cat([old, h])
@@ -310,8 +354,9 @@ class OraclePerception:
 
 
 class OracleGeneration:
-    def __init__(self, w, cfg, seed, agent, step_cost):
+    def __init__(self, w, cfg, seed, agent, step_cost, store=_id):
         self.w, self.cfg, self.seed, self.agent = w, cfg, seed, agent
+        self.store = store
         self.sched = Scheduler(cfg)
         self.n_iterations = cfg.num_inference_steps
         self.step_cost = step_cost
@@ -333,8 +378,10 @@ class OracleGeneration:
     def step(self, state, ctx):
         i = state.steps
         with torch.no_grad():
-            fn = dpt_eps if "dpt.input.w" in self.w else unet_eps
-            eps = fn(self.w, self.cfg, state.x, self.sched.timesteps[i], ctx.payload)
+            if "dpt.input.w" in self.w:
+                eps = dpt_eps(self.w, self.cfg, state.x, self.sched.timesteps[i], ctx.payload)
+            else:
+                eps = unet_eps(self.w, self.cfg, state.x, self.sched.timesteps[i], ctx.payload, self.store)
             x = self.sched.step(i, state.x, eps, None if state.z is None else state.z[i])
         return State(x, state.z, i + 1)
 
@@ -353,11 +400,19 @@ class OracleDP:
 
     kind = "conditioning"          # compares unequal to ContextKind.AUTOREGRESSIVE
 
-    def __init__(self, weights, cfg, seed, agent, layer_costs, step_cost):
+    def __init__(self, weights, cfg, seed, agent, layer_costs, step_cost, numerics="fp32"):
+        """numerics "fp32": the reference-precision oracle; "bf16": the
+        bf16-faithful oracle of the tensor-core path (bf16_weights + a bf16
+        store at every point the device stores an activation; CNN policy)."""
         w = {k: v.detach().to("cpu", torch.float32) for k, v in weights.items()}
-        self.cfg, self.seed, self.agent = cfg, seed, agent
-        self.perception = OraclePerception(w, cfg, layer_costs)
-        self.generation = OracleGeneration(w, cfg, seed, agent, step_cost)
+        store = _id
+        if numerics == "bf16":
+            w, store = bf16_weights(w), _bf16
+        elif numerics != "fp32":
+            raise ValueError(f"numerics must be fp32 or bf16, not {numerics!r}")
+        self.cfg, self.seed, self.agent, self.numerics = cfg, seed, agent, numerics
+        self.perception = OraclePerception(w, cfg, layer_costs, store)
+        self.generation = OracleGeneration(w, cfg, seed, agent, step_cost, store)
 
     @property
     def sequential_cost(self):

@@ -207,6 +207,7 @@ class _Device:
         self.ingest_event = {}       # request -> event after ingest (P)
         self.slot_read = {}          # slot -> last G event that read it
         self.lane_free = {}          # lane -> G event after the previous occupant's finish
+        self.out_ready = {}          # out_index -> G event after the finish that wrote it
         self.t_start, self.t_end = {}, {}
         self.origin = None
         self.throttle = []
@@ -272,7 +273,16 @@ class _Device:
 
     def finish(self, lane, out_index):
         self.session.finish(lane, out_index)
-        self.lane_free[lane] = self.event(self.G)
+        ev = self.event(self.G)
+        self.lane_free[lane] = ev
+        # the action row is written on G (a non-blocking stream): a mid-run
+        # host read must wait for this event, not just issue a D2H
+        self.out_ready[out_index] = ev
+
+    def wait_output(self, out_index):
+        ev = self.out_ready.pop(out_index, None)
+        if ev is not None:
+            ev.synchronize()
 
     def republish(self, src_slot, slot, frame, version):
         """Token-prefix update of the shared context (autoregressive policies)."""
@@ -288,6 +298,7 @@ class _Device:
     def synchronize(self):
         self.P.synchronize()
         self.G.synchronize()
+        self.out_ready.clear()
 
 
 class _Emissions:
@@ -314,7 +325,9 @@ class _Emissions:
 
     def materialize(self, k, agent):
         if k not in self.cache:
-            self.cache[k] = self._make(k, self.device.session.read_action(self.items[k][0]))
+            out_index = self.items[k][0]
+            self.device.wait_output(out_index)      # the finish kernel on G has written the row
+            self.cache[k] = self._make(k, self.device.session.read_action(out_index))
         return self.cache[k][agent]
 
     def all(self):
@@ -659,12 +672,15 @@ def run_sequential(policy, env, duration: int, frame_interval: Optional[float] =
 
 def _ingest_keyed(dev, key, seed, lane, observations):
     """dev.ingest with the request state seeded by `seed` but the ingest event
-    filed under `key` (PAR jobs share dispatch frames; DEC seeds by time)."""
+    filed under `key` (PAR jobs share dispatch frames; DEC seeds by time).
+    key None: nothing consumes the event (DEC's perception lane: its publish
+    is ordered by the publish event), so none is kept."""
     ev = dev.lane_free.pop(lane, None)
     if ev is not None:
         dev.P.wait_event(ev)
     dev.session.ingest(seed, lane, observations)
-    dev.ingest_event[key] = dev.event(dev.P)
+    if key is not None:
+        dev.ingest_event[key] = dev.event(dev.P)
 
 
 def run_parallel(policy, env, workers: int, duration: int, frame_interval: Optional[float] = None,
@@ -858,7 +874,7 @@ def run_decoupled(policy, env, duration: int, frame_interval: Optional[float] = 
             what, when = min(cands, key=lambda c: (c[1], order[c[0]]))
             if what == "publish":
                 keys += 1
-                _ingest_keyed(dev, ("p", keys), t, P_LANE, p_obs)
+                _ingest_keyed(dev, None, t, P_LANE, p_obs)
                 dev.session.perceive(P_LANE, 0, n_layers)
                 slot, version = store.reserve(t, p_obs[0].id)
                 dev.publish(P_LANE, t, slot, version)
