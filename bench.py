@@ -43,6 +43,13 @@ def parse():
     ap.add_argument("--depth", type=int, default=8)
     ap.add_argument("--offset", type=int, default=0)
     ap.add_argument("--agents", type=int, default=1, help="agents per GPU")
+    ap.add_argument("--total-agents", type=int, default=None,
+                    help="BASELINE configs[4]: this many agents over all GPUs (agents per GPU = "
+                         "total / N; overrides --agents)")
+    ap.add_argument("--disaggregated", action="store_true",
+                    help="also time the disaggregated variant on rank 0 after the replicas run: "
+                         "perception on GPU local_rank+1 (when the node has it), context slots "
+                         "shipped to the generation GPU over NVLink P2P")
     ap.add_argument("--config", default="pusht")
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--no-e2e", action="store_true")
@@ -61,6 +68,29 @@ def parse():
 
 
 # ---------------------------------------------------------------- distributed plumbing
+
+def spawn_command(argv, n, port):
+    """`python bench.py --gpus N ...` run outside a launcher re-executes itself
+    as N ranks (one process per GPU) under torch.distributed.run, the same
+    launch the driver uses for its scaling runs."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port),
+            os.path.abspath(__file__)] + list(argv)
+
+
+def maybe_spawn(args):
+    """Returns None when this process is a rank (WORLD_SIZE set, or N = 1);
+    otherwise runs the N-rank job and returns its exit code."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    import subprocess
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "WARN")
+    return subprocess.call(spawn_command(sys.argv[1:], args.gpus, port), env=env)
 
 class Dist:
     def __init__(self):
@@ -381,6 +411,35 @@ def merged_prefill_bench(pp_g=4, reps=50, vision_len=96, language_len=32, l_a=7)
             "note": "device time, CUDA events over %d reps; CPU = oracle/transformer.py numpy" % reps}
 
 
+def disaggregated_leg(args, cfg, weights, A, W, K, dist):
+    """SURVEY.md §8(e) disaggregated variant, timed on rank 0 while the other
+    ranks wait: generation on this rank's GPU, perception (encoder, cond
+    assembly, FiLM projection) on the next GPU of the node, each publish
+    shipped into the generation GPU's ring by one P2P copy and released at
+    system scope.  With a single visible GPU both roles share it (same code
+    path, no NVLink hop)."""
+    import torch
+    from paper_2509_09560_b200 import diffusion as D
+    dist.barrier()
+    out = None
+    if dist.rank == 0:
+        gd = torch.cuda.current_device()
+        pd = gd + 1 if torch.cuda.device_count() > gd + 1 else gd
+        pol = D.make_diffusion_policy(cfg, dtype=args.dtype, weights=weights, agents=A,
+                                      resident_frames=64, perception_device=pd)
+        solo = Dist()
+        solo.world = 1
+        win, res, fill = run_window(pol, args.depth, args.offset, A, W, K, solo, gd)
+        t0 = fill + W
+        p99, _ = steady_jct_ms(res, t0, K)
+        out = {"value": K * A / (win.ms / 1e3), "unit": "actions/s", "generation_gpu": gd,
+               "perception_gpu": pd, "p99_action_latency_ms": p99,
+               "link": "NVLink P2P (cudaMemcpy2DAsync peer copy + st.release.sys)" if pd != gd
+               else "same GPU (no second GPU visible): staged copy + system-scope release only"}
+    dist.barrier()
+    return out
+
+
 def reference_arm(args, dist):
     if dist.rank != 0:
         return
@@ -402,7 +461,14 @@ def reference_arm(args, dist):
 
 def main():
     args = parse()
+    rc = maybe_spawn(args)
+    if rc is not None:
+        sys.exit(rc)
     dist = Dist()
+    if dist.world > 1 and args.gpus != dist.world:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE {dist.world}; using the launcher's world",
+              file=sys.stderr)
+    args.gpus = dist.world
     if args.impl == "reference":
         dist.init("gloo")
         reference_arm(args, dist)
@@ -414,6 +480,10 @@ def main():
 
     cfg = D.PRESETS[args.config]
     A = args.agents
+    if args.total_agents is not None:
+        if args.total_agents % dist.world:
+            raise SystemExit(f"--total-agents {args.total_agents} does not split over {dist.world} GPUs")
+        A = args.total_agents // dist.world
     W, K = max(3, args.warmup), max(1, args.steps)
     weights = D.init_weights(cfg, seed=0, device="cuda")
     n_res = 64
@@ -495,6 +565,7 @@ def main():
                       "model": f"{'dp-transformer' if cfg.denoiser == 'transformer' else 'dp-cnn'}-{cfg.name}", "depth": args.depth,
                       "pp": [1, args.depth], "fetch_offset": args.offset, "alpha": 0.0,
                       "agents_per_gpu": A, "global_batch": A * dist.world,
+                      "total_agents": A * dist.world,
                       "samples_per_denoise_step": S_med, "parallelism": f"replicas x{dist.world}",
                       "l2": (f"inputs larger than L2: {bytes_step / 1e6:.0f} MB of denoiser weights streamed per step"
                              if bytes_step > 126e6 else
@@ -514,6 +585,10 @@ def main():
                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
                         "denoise_kernel_by_S": LAST_EVENTS.get("denoise_kernel")},
            "gpu_launches": launches, "clocks": win.clock_info}
+    if args.total_agents is not None:
+        out["config"]["workload"] = (f"configs[4]: {args.total_agents} independent agents over "
+                                     f"{dist.world} B200 ({A} per GPU, batched into one denoise launch "
+                                     f"per frame); model: " + out["config"]["workload"])
 
     # --- depth-1 baseline (the same engine, run_sequential)
     if not args.no_depth1:
@@ -558,6 +633,9 @@ def main():
                                                               if cfg.scheduler == "ddpm" else 0)))
         out["e2e"] = {"value": e2e, "unit": "actions/s", "h2d_bytes_per_step": h2d,
                       "d2h_bytes_per_step": A * 4 * cfg.horizon * cfg.action_dim}
+
+    if args.disaggregated:
+        out["disaggregated"] = disaggregated_leg(args, cfg, weights, A, W, K, dist)
 
     if dist.rank == 0 and not args.no_cpu:
         out["cpu_baseline"] = cpu_oracle_sample(args.config, args.cpu_seconds)
