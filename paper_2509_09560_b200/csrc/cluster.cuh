@@ -111,7 +111,8 @@ struct ClParams {
   int *flags;
   float2 *gstats;           // per tile of a 256-channel GroupNorm: (mean, M2) per sample
   int n_ops, S, nc, n_tasks;
-  int l2_prefetch;          // bulk-prefetch the next task's weights into L2
+  int l2_prefetch;          // L2 prefetch mode for the ring overflow of a task's weights
+  int hack;                 // timing experiments (AURAS_CL_HACK); 0 in production
   UnetDev *dev;
   auras_sched sched;
   int horizon, adim;

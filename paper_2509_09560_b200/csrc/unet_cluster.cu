@@ -106,6 +106,7 @@ struct alignas(64) ClOp {
   int rsh;                    // receive-buffer row stride (halves)
   // activation addressing: element (s, t, c) at base + (c >> 6) * plane + (s * T + t) * row + (c & 63)
   // (channel-blocked [C/64][S][T][64] buffers owned by this kernel, or the plan's [S][T][pitch] layout)
+  const uint8_t *wt;          // tiled weights (L2 prefetch addresses)
   __nv_bfloat16 *out_base;
   const __nv_bfloat16 *res_base;
   int64_t out_plane, res_plane;
@@ -119,6 +120,9 @@ __device__ __forceinline__ long long ck_time() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+
+// Per-task, per-rank globaltimer stamps (diagnostics): trace[(t * CL + rank) * 16 + k]
+#define CK_TR(k) (P.trace[((int64_t)t * CL + rank) * 16 + (k)] = ck_time())
 
 __device__ __forceinline__ void ck_spin(const int *ctr, int target) {
   while (ld_acquire_i32(ctr) < target) {
@@ -202,42 +206,45 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
   const uint32_t tmem = *tmem_slot;
   // the frame's denoise iterations all run in this launch (control word set per frame)
   const int iters = max(1, P.dev->ctrl.iters), r0 = P.dev->r;
-  if (P.trace && threadIdx.x == 0)
-    P.trace[16 * (int64_t)P.n_tasks + ((int64_t)blockIdx.x * 1024 + 1023) * 3] = ck_time();
+  if (P.trace && threadIdx.x == 0) P.trace[16 * CL * (int64_t)P.n_tasks + 2 * blockIdx.x] = ck_time();
 
   if (warp < CK_NWW) {
     // ------------------------------------------------ weights: this CTA's K share of every task
-    // Optional L2 prefetch of the next task's share (off by default: measured
-    // +333 MB DRAM reads per step from lines evicted before use).
-    auto l2_prefetch = [&](int t) {
-      const int4 tk = P.tasks[t];
-      const ClOp *op = &P.ops[tk.x >> 8];
-      const int kps = op->kps, kbt = op->kb_total, nmt = op->nmt;
-      const int kb0 = rank * kps, kb1 = min(kbt, kb0 + kps);
-      const int step = 3 - nmt, row0 = tk.y * nmt * kbt * 128;
-      for (int kb = kb0 + step * lane; kb < kb1; kb += 32 * step)
-        asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(&op->tmA), "r"(0),
-                     "r"(row0 + kb * 128 * nmt)
-                     : "memory");
-    };
-    auto next_gemm = [&](int t) {
-      for (++t; t < t1; ++t)
-        if ((P.tasks[t].x & 0xff) == K_GEMM) return t;
-      return -1;
-    };
-    const bool pf = P.l2_prefetch && warp == 0;
+    // L2 prefetch of the part of a task's K share that does not fit in the
+    // ring (P.l2_prefetch: 1 = per-line prefetch.global.L2 from the LSU path,
+    // 2 = one bulk prefetch per warp through the copy engine).  Issued when the
+    // producers enter the task, i.e. while the previous task drains and the
+    // layer's dependency is still unresolved, so the HBM stream keeps flowing
+    // through the epilogue chain and the ring refills from L2.
+    const int pf = P.l2_prefetch;
     int ia = 0;
-    if (pf) {
-      const int f = next_gemm(t0 - 1);
-      if (f >= 0) l2_prefetch(f);
-    }
     for (int it = 0; it < iters; ++it)
     for (int t = t0; t < t1; ++t) {
       const int4 tk = P.tasks[t];
       if ((tk.x & 0xff) != K_GEMM) continue;
       if (pf) {
-        const int nx = next_gemm(t);
-        if (nx >= 0) l2_prefetch(nx);
+        const ClOp *op = &P.ops[tk.x >> 8];
+        const int kps = op->kps, kbt = op->kb_total, nmt = op->nmt;
+        const int kb0 = rank * kps, kb1 = min(kbt, kb0 + kps);
+        const int64_t row0 = (int64_t)tk.y * nmt * kbt * 128;
+        const int64_t lo = (row0 + (int64_t)kb0 * 128 * nmt) * 128 + (int64_t)CK_NA * CK_A_STAGE;
+        const int64_t hi = (row0 + (int64_t)kb1 * 128 * nmt) * 128;
+        if (hi > lo) {
+          const uint8_t *base = op->wt;
+          if (pf == 1) {
+            for (int64_t b = lo + (int64_t)(warp * 32 + lane) * 128; b < hi; b += CK_NWW * 32 * 128)
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(base + b));
+          } else if (pf == 3) {
+            for (int64_t b = lo + (int64_t)(warp * 32 + lane) * 128; b < hi; b += CK_NWW * 32 * 128)
+              asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(base + b));
+          } else if (lane == 0) {
+            const int64_t chunk = ((hi - lo + CK_NWW - 1) / CK_NWW + 15) & ~15ll;
+            const int64_t a = lo + warp * chunk, e = min(hi, a + chunk);
+            if (e > a)
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + a), "r"((uint32_t)(e - a))
+                           : "memory");
+          }
+        }
       }
       const ClOp *op = &P.ops[tk.x >> 8];
       const int kps = op->kps, kbt = op->kb_total;
@@ -252,6 +259,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           if (st % CK_NWW != warp) continue;         // a stage always has the same issuing warp
           const bool two = kb + 1 < kb1;
           mbar_wait(&emptyA[st], ((ia / CK_NA) & 1) ^ 1);
+          if (P.hack & 2) { if (lane == 0) mbar_arrive(&fullA[st]); __syncwarp(); continue; }
           tma_load_2d_warp(sA + st * CK_A_STAGE, two ? &op->tmA : &op->tmA1, &fullA[st],
                            two ? CK_A_STAGE : CK_A_BYTES, 0, row0 + kb * 128);
         }
@@ -260,6 +268,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           const int st = ia % CK_NA;
           if (st % CK_NWW != warp) continue;         // a stage always has the same issuing warp
           mbar_wait(&emptyA[st], ((ia / CK_NA) & 1) ^ 1);
+          if (P.hack & 2) { if (lane == 0) mbar_arrive(&fullA[st]); __syncwarp(); continue; }
           tma_load_2d_warp(sA + st * CK_A_STAGE, &op->tmA, &fullA[st], CK_A_STAGE, 0, row0 + kb * 256);
         }
       }
@@ -280,9 +289,10 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
       const uint32_t bbytes = op->rows * 128;
       const CUtensorMap *tmB = &op->tmB;
       if (lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(tmB) : "memory");   // descriptor fetch off the critical path
         for (int d = 0; d < 3; ++d) ck_wait_dep(P, prep_done, op->gemm_dep[d], op->gemm_tgt[d], it);
         fence_proxy_async();
-        if (P.trace && rank == 0) P.trace[8 * t + 0] = ck_time();
+        if (P.trace && bw == 0) CK_TR(0);
       }
       __syncwarp();
       const int kb0 = rank * kps, kb1 = min(kbt, kb0 + kps);
@@ -296,6 +306,19 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         const int off = tap - pad;
         const int q = off >= 0 ? off / stride : -((-off + stride - 1) / stride);
         const int h = off - q * stride;
+        if ((P.hack & 1) && j > 0) { if (lane == 0) mbar_arrive(&fullB[sb]); __syncwarp(); continue; }
+        if (P.hack & 8) {
+          if (lane == ((j / CK_NBW) & 31)) {
+            mbar_expect_tx(&fullB[sb], bbytes);
+            asm volatile(
+                "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+                "%6, %7}], [%2];" ::"r"(smem_u32(sB + sb * bstage)),
+                "l"(tmB), "r"(smem_u32(&fullB[sb])), "r"(0), "r"(h), "r"(q), "r"(tk.z * sbox), "r"(c0 >> 6)
+                : "memory");
+          }
+          __syncwarp();
+          continue;
+        }
         tma_load_5d_warp(sB + sb * bstage, tmB, &fullB[sb], bbytes, 0, h, q, tk.z * sbox, c0 >> 6);
       }
     }
@@ -325,6 +348,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&fullA[sa], (pa_bits >> sa) & 1);
           mbar_wait(&fullB[sb], (par >> sb) & 1);
+          if (P.trace && lane == 0 && kb == kb0) CK_TR(1);
           par ^= 1u << sb;
           pa_bits ^= 1u << sa;
           umma_kblock2_warp(dt, dt + CK_BN, umma_desc(sA0 + sa * CK_A_STAGE), umma_desc(sB0 + sb * bstage), idesc,
@@ -343,6 +367,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           const int nk = min(2, kb1 - kb);
           for (int i = 0; i < nk; ++i) {
             mbar_wait(&fullB[sb], (par >> sb) & 1);
+            if (P.trace && lane == 0 && kb == kb0 && i == 0) CK_TR(1);
             par ^= 1u << sb;
             umma_kblock_warp(dt, umma_desc(a0 + i * CK_A_BYTES), umma_desc(sB0 + sb * bstage), idesc,
                              (kb > kb0 || i > 0) ? 1u : 0u);
@@ -354,6 +379,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           ++ia;
         }
       }
+      if (P.trace && lane == 0) CK_TR(2);
       if (kb1 > kb0) umma_commit_warp(&tfull[buf]);
       else if (lane == 0) mbar_arrive(&tfull[buf]);      // empty K share: the drain pushes zeros
       __syncwarp();
@@ -395,6 +421,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           if (gn) mbar_expect_tx(&rbar[2 + (gn_i & 1)], (uint32_t)(CL * 2 * nmt * sbox * 8));
           if (film) ck_spin(prep_done, S * (it + 1));
           for (int d = 0; d < 2; ++d) ck_wait_dep(P, prep_done, op->epi_dep[d], op->epi_tgt[d], it);
+          if (P.trace) CK_TR(12);
         }
         esync();
         // ---- element ownership.  Thread et belongs to (atom pa, sample pj) pair pi = et / L
@@ -455,7 +482,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         {
           mbar_wait(&tfull[buf], (gi >> 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 1] = ck_time();
+          if (P.trace && et == 0) CK_TR(3);
           const int quad = ew & 3, half = ew >> 2;
           const int m = quad * 32 + lane;
           const int cpu = bn >> 4, nch = nmt * cpu;
@@ -486,10 +513,10 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[buf]);
-          if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 5] = ck_time();
+          if (P.trace && et == 0) CK_TR(4);
         }
         mbar_wait_cluster(&rbar[buf], (gi >> 1) & 1);            // all 8 CTAs' partials have landed
-        if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 2] = ck_time();
+        if (P.trace && et == 0) CK_TR(5);
         // ---- fixed-order sum of the 8 K slices + bias (fp32)
 #pragma unroll
         for (int k = 0; k < VMAX; ++k) {
@@ -529,9 +556,9 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
             if (et == 0) red_release_add(&P.flags[fi], 1);
           }
         }
-        if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 6] = ck_time();
+        if (P.trace && et == 0) CK_TR(6);
         if (gn) mbar_wait_cluster(&rbar[2 + (gn_i & 1)], (gn_i >> 1) & 1);   // every peer's statistics
-        if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 3] = ck_time();
+        if (P.trace && et == 0) CK_TR(7);
         if (gn) {
           // ---- merge the atoms of each group (butterfly, fixed lane order); task atoms are
           //      numbered in channel order q = tile * 16 + within-tile atom; 256-channel groups
@@ -585,7 +612,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           mean_g = gs.x;
           rstd_g = rsqrtf(gs.y / ncount + 1e-5f);
         }
-        if (P.trace && rank == 0 && et == 0) P.trace[8 * t + 7] = ck_time();
+        if (P.trace && et == 0) CK_TR(8);
         // ---- normalise, activate, FiLM, residual (registers) and store 4 channels per half
         if (mine) {
           const float rba = e.res_before_act ? 1.f : 0.f;
@@ -624,17 +651,19 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
                   make_float4(y[4 * h], y[4 * h + 1], y[4 * h + 2], y[4 * h + 3]);
           }
         }
+        if (P.trace && et == 0) CK_TR(9);
         fence_proxy_async();
         esync();
         if (et == 0) {
+          if (P.trace) CK_TR(10);
           red_release_add(&done[opi], 1);
-          if (P.trace && rank == 0) P.trace[8 * t + 4] = ck_time();
+          if (P.trace) CK_TR(11);
         }
         ++gi;
         gn_i += gn;
       } else if (type == K_PREP) {
         if (tk.w != rank || it > 0) continue;            // later iterations: prepared by the final task
-        if (P.trace && et == 0) P.trace[8 * t + 0] = ck_time();
+        if (P.trace && et == 0) CK_TR(0);
         prep_body<__nv_bfloat16>(P.dev, tk.y, et, CK_EPI, P.sched, P.horizon, P.adim, P.xin, P.x_pitch,
                                  P.ring_slot_stride, P.ring_agent_stride, r0);
         fence_proxy_async();
@@ -642,12 +671,12 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         if (et == 0) {
           __threadfence();
           atomicAdd(prep_done, 1);
-          if (P.trace) P.trace[8 * t + 4] = ck_time();
+          if (P.trace) CK_TR(11);
         }
       } else if (type == K_FINAL) {
         if (tk.w != rank) continue;
         if (et == 0) ck_spin(&done[P.n_ops - 1], P.ops[P.n_ops - 1].tiles * CL * (it + 1));
-        if (P.trace && et == 0) P.trace[8 * t + 0] = ck_time();
+        if (P.trace && et == 0) CK_TR(0);
         esync();
         final_body<__nv_bfloat16>(P.dev, tk.y, et, CK_EPI, P.sched, P.horizon, P.adim, P.y_final, P.y_pitch,
                                   P.final_cin, P.wf, P.bf, eps, esync, r0 + it);
@@ -664,15 +693,14 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
             atomicAdd(prep_done, 1);
           }
         }
-        if (P.trace && et == 0) P.trace[8 * t + 4] = ck_time();
+        if (P.trace && et == 0) CK_TR(11);
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   cluster_sync_all();                       // no CTA leaves while peers may still touch its smem
-  if (P.trace && threadIdx.x == 0)
-    P.trace[16 * (int64_t)P.n_tasks + ((int64_t)blockIdx.x * 1024 + 1023) * 3 + 1] = ck_time();
+  if (P.trace && threadIdx.x == 0) P.trace[16 * CL * (int64_t)P.n_tasks + 2 * blockIdx.x + 1] = ck_time();
   if (warp == CK_MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CK_TMEM_COLS));
 }
 
@@ -832,6 +860,7 @@ int clus_build(ClConfig &cc, const std::vector<auras_conv_op> &ops, int S, const
     }
     void *wt = nullptr;
     if ((rc = tiled_weights(cache, o, &wt, m.nmt))) return rc;
+    m.wt = static_cast<const uint8_t *>(wt);
     if ((rc = make_tiled_weight_map(&m.tmA, wt, m.m_tiles * m.kb_total * 128, 256))) return rc;
     if ((rc = make_tiled_weight_map(&m.tmA1, wt, m.m_tiles * m.kb_total * 128, 128))) return rc;
     // ---- activation buffers: every tensor a later op reads through TMA is re-laid
@@ -984,6 +1013,8 @@ int clus_build(ClConfig &cc, const std::vector<auras_conv_op> &ops, int S, const
   {
     const char *e = getenv("AURAS_CL_L2PF");
     cc.params.l2_prefetch = e ? atoi(e) : 0;
+    e = getenv("AURAS_CL_HACK");        // timing experiments only: 1 = skip activation boxes, 2 = skip weights
+    cc.params.hack = e ? atoi(e) : 0;
   }
   return AURAS_OK;
 }

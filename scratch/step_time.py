@@ -24,7 +24,7 @@ n = 0
 if trace_on:
     n = lib.auras_unet_mega_trace(sess.plan, S, None, None, 0)
     tasks = np.zeros((n, 4), dtype=np.int32)
-    trace = torch.zeros(n * 16 + 148 * 1024 * 3, dtype=torch.int64, device="cuda")
+    trace = torch.zeros(n * 128 + 4096, dtype=torch.int64, device="cuda")
     assert lib.auras_unet_mega_trace(sess.plan, S, trace.data_ptr(), tasks.ctypes.data, n) == n
 ts = []
 for it in range(8):
@@ -43,8 +43,5 @@ print("S", S, "step ms", " ".join(f"{t:.3f}" for t in ts), "min", min(ts[2:]))
 x = sess.x[0, :S].cpu().numpy()
 print("x finite", np.isfinite(x).all(), "x[0,:4]", x[0, :4])
 if trace_on:
-    full = trace.cpu().numpy()[:n * 8].reshape(n, 8)
-    full2 = trace.cpu().numpy()[n * 8:n * 16].reshape(n, 8)
-    kb = trace.cpu().numpy()[n * 16:].reshape(148, 1024, 3)
-    np.save(f"gpurun_out/kbtrace_{S}.npy", kb)
-    json.dump({"tasks": tasks.tolist(), "trace": full.tolist(), "trace2": full2.tolist()}, open(f"gpurun_out/ctrace_{S}.json", "w"))
+    tr = trace.cpu().numpy()
+    np.savez(f"gpurun_out/ctrace_{S}.npz", tasks=tasks, trace=tr[:n * 128].reshape(n, 8, 16), cta=tr[n * 128:n * 128 + 296].reshape(148, 2))

@@ -31,7 +31,9 @@ __global__ void __launch_bounds__(128, 1) bench(int nkb, int bn, int mode, long 
       while (*stop == 0) { int v; asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory"); }
     }
   }
-  if (warp == 1) {
+  const int nissue = mode == 50 ? 2 : mode == 51 ? 3 : 1;
+  if (warp >= 1 && warp <= nissue) {
+    const int iw = warp - 1;
     const uint32_t idesc = umma_idesc(bn);
     long long t0 = clock64();
     for (int kb = 0; kb < nkb; ++kb) {
@@ -48,6 +50,42 @@ __global__ void __launch_bounds__(128, 1) bench(int nkb, int bn, int mode, long 
       if (mode == 7 || mode == 13) {                  // + wait on an already-completed barrier (+ the stage commit path)
         mbar_wait(&bars[20], 0);
         umma_kblock2_warp(tmem, tmem + 64, umma_desc(a0), umma_desc(b0), idesc, kb > 0);
+        umma_commit_warp(&bars[sa % 8]); umma_commit_warp(&bars[8 + sb]);
+        __syncwarp();
+        continue;
+      }
+      if (mode == 50 || mode == 51) {
+        umma_kblock_warp(tmem + iw * 64, umma_desc(a0), umma_desc(b0), idesc, kb > 0);
+        umma_commit_warp(&bars[sa % 8]); umma_commit_warp(&bars[8 + sb]);
+        __syncwarp();
+        continue;
+      }
+      if (mode >= 40 && mode < 50) {                  // operand-major / M variants of the K=64 block
+        uint32_t id = idesc;
+        uint64_t ad = umma_desc(a0), bd = umma_desc(b0);
+        if (mode == 40 || mode == 43) { id |= 1u << 15; ad = (ad & ~(0x3FFFull << 16)) | ((uint64_t)(8192 >> 4) << 16); }
+        if (mode == 41) id = (id & ~(0x1Fu << 24)) | ((uint32_t)(64 >> 4) << 24);
+        if (mode == 42 || mode == 43) { id |= 1u << 16; bd = (bd & ~(0x3FFFull << 16)) | ((uint64_t)(8192 >> 4) << 16); }
+        if (mode == 44) id = (id & ~(0x1Fu << 24)) | ((uint32_t)(256 >> 4) << 24);
+        umma_kblock_warp(tmem, ad, bd, id, kb > 0);
+        umma_commit_warp(&bars[sa % 8]); umma_commit_warp(&bars[8 + sb]);
+        __syncwarp();
+        continue;
+      }
+      if (mode >= 20 && mode < 30) {                  // 4 K=16 steps into `nacc` accumulators (round robin)
+        const int nacc = mode - 20;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16_warp(tmem + (kk % nacc) * 64, umma_desc(a0 + kk * 32), umma_desc(b0 + kk * 32), idesc, (kb > 0) ? 1u : 0u);
+        umma_commit_warp(&bars[sa % 8]); umma_commit_warp(&bars[8 + sb]);
+        __syncwarp();
+        continue;
+      }
+      if (mode >= 30 && mode < 40) {                  // 8 K=16 steps (two k-blocks) into `nacc` accumulators
+        const int nacc = mode - 30;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_bf16_warp(tmem + (kk % nacc) * 32, umma_desc(a0 + (kk & 3) * 32 + (kk >> 2) * 16384), umma_desc(b0 + (kk & 3) * 32), idesc, (kb > 0) ? 1u : 0u);
         umma_commit_warp(&bars[sa % 8]); umma_commit_warp(&bars[8 + sb]);
         __syncwarp();
         continue;
@@ -69,10 +107,10 @@ __global__ void __launch_bounds__(128, 1) bench(int nkb, int bn, int mode, long 
       if (mode >= 2) { umma_commit_warp(&bars[sa % 8]); umma_commit_warp(&bars[8 + sb]); }
       __syncwarp();
     }
-    umma_commit_warp(&bars[15]);
-    mbar_wait(&bars[15], 0);
+    umma_commit_warp(&bars[24 + iw]);
+    mbar_wait(&bars[24 + iw], 0);
     long long t1 = clock64();
-    if (lane == 0) { out[0] = t1 - t0; *(volatile int *)(flag + 1) = 1; }
+    if (lane == 0 && iw == 0) { out[0] = t1 - t0; *(volatile int *)(flag + 1) = 1; }
   }
   asm volatile("tcgen05.fence::before_thread_sync;"); __syncthreads();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
@@ -88,7 +126,7 @@ int main() {
     enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE); }
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 232000);
-  for (int bn : {32}) for (int grid : {1, 112}) for (int mode : {3, 5, 13}) for (int nkb : {2000}) {
+  for (int bn : {32, 64}) for (int grid : {1}) for (int mode : {4, 50, 51}) for (int nkb : {2000}) {
     cudaMemset(flag, 0, 64);
     bench<<<grid, 128, 232000>>>(nkb, bn, mode, d, tm, flag);
     long long h = 0; cudaError_t e = cudaDeviceSynchronize(); cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
