@@ -242,6 +242,11 @@ int auras_unet_generate(auras_unet_plan *plan, int S, const int *lanes, const in
  * 1 persistent megakernel with split-K through L2, 2 cluster megakernel
  * (DSMEM split-K + GroupNorm), -1 not chosen yet (picked by a timed dry run
  * of both persistent kernels on the first generate of that S). */
+/* Health of the persistent denoise kernels (no reference counterpart: the
+ * reference's deadlock guard is executor.py:311-313 on the host).  0 = fine,
+ * 1 = a device-side dependency wait timed out (surfaced as DeadlockDetected),
+ * < 0 = error.  Synchronous; reads and clears the error word. */
+int auras_unet_check(auras_unet_plan *plan);
 int auras_unet_kernel_for(const auras_unet_plan *plan, int S);
 
 int auras_unet_launches_per_iter(const auras_unet_plan *plan);

@@ -51,6 +51,11 @@ __device__ __forceinline__ void st_async_v4_b32(uint32_t addr, uint32_t a, uint3
                : "memory");
 }
 
+__device__ __forceinline__ void st_async_b32(uint32_t addr, uint32_t a, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(addr), "r"(a), "r"(bar)
+               : "memory");
+}
+
 __device__ __forceinline__ void st_async_v2_f32(uint32_t addr, float a, float b, uint32_t bar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(addr), "f"(a),
                "f"(b), "r"(bar)
@@ -110,6 +115,7 @@ struct ClParams {
   int *ctr;                 // [n_ops] tile completions x 8, [1] prep, then pair flags
   int *flags;
   float2 *gstats;           // per tile of a 256-channel GroupNorm: (mean, M2) per sample
+  int *err;                 // sticky error word: 1 = a dependency wait timed out
   int n_ops, S, nc, n_tasks;
   int l2_prefetch;          // L2 prefetch mode for the ring overflow of a task's weights
   int hack;                 // timing experiments (AURAS_CL_HACK); 0 in production
@@ -148,6 +154,7 @@ int clus_build(ClConfig &cc, const std::vector<auras_conv_op> &ops, int S, const
                const ClParams &base, const float *film_tau, int film_width, const float *ring_film,
                TiledCache &cache);
 int clus_launch(const ClConfig &cc, cudaStream_t st);
+int clus_error(const ClConfig &cc);
 int clus_set_trace(ClConfig &cc, long long *trace);
 void clus_free(ClConfig &cc);
 

@@ -522,12 +522,7 @@ int mega_build(MegaConfig &mc, const std::vector<auras_conv_op> &ops, int S, con
   const char *ad = getenv("AURAS_MEGA_A_DEPTH");
   mc.params.na = na;
   mc.params.a_depth = ad ? std::max(1, std::min(na, atoi(ad))) : na;
-  static bool attr = false;
-  if (!attr) {
-    AURAS_CUDA(cudaFuncSetAttribute(unet_mega, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MK_SMEM));
-    attr = true;
-  }
-  return AURAS_OK;
+  return ensure_smem_attr(unet_mega, (int)MK_SMEM);
 }
 
 int mega_launch(const MegaConfig &mc, cudaStream_t st) {

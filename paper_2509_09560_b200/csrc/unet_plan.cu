@@ -443,6 +443,21 @@ int auras_unet_kernel_for(const auras_unet_plan *p, int S) {
   return it == p->use_clus_for.end() ? -1 : 1 + it->second;
 }
 
+// Health of the persistent kernels: 0, or 1 when a dependency wait in a
+// cluster-kernel launch gave up after its timeout (the pipeline stalled; the
+// launch's outputs are garbage).  Reads and clears the sticky error words;
+// synchronous (call where the host already waits on the generation stream).
+int auras_unet_check(auras_unet_plan *p) {
+  if (!p) return AURAS_E_ARG;
+  int bad = 0;
+  for (auto &kv : p->clus) {
+    const int v = clus_error(kv.second);
+    if (v < 0) { set_error("reading the cluster kernel's error word failed"); return AURAS_E_CUDA; }
+    bad |= v;
+  }
+  return bad;
+}
+
 int auras_unet_launches_per_iter(const auras_unet_plan *p) {
   if (!p) return AURAS_E_ARG;
   return p->use_mega ? 2 : 3 + 2 * (int)p->ops.size();

@@ -44,7 +44,7 @@ import numpy as np
 
 from . import _lib
 from .context import ContextKind, ContextStore
-from .errors import ConfigInvalid, ShapeMismatch
+from .errors import ConfigInvalid, DeadlockDetected, ShapeMismatch
 from .policy import ActionOutput, Observation, Policy
 
 
@@ -1470,11 +1470,26 @@ class DPSession:
                                             self.out[out_index].data_ptr(), self.g.cuda_stream),
                    "dp_finish")
 
+    def _check_device(self):
+        # a dependency wait inside the persistent denoise kernel that timed out
+        # (csrc/unet_cluster.cu ck_spin) means the launch's outputs are garbage:
+        # fail loudly instead of returning them (fp/executor.py:311-313 raises the
+        # host-side analogue)
+        if self.plan:
+            rc = self.lib.auras_unet_check(self.plan)
+            if rc == 1:
+                raise DeadlockDetected("denoise kernel: a device-side dependency wait timed out")
+            _lib.check(rc, "unet_check")
+
     def read_actions(self, n):
-        return self.out[:n].cpu().numpy()
+        a = self.out[:n].cpu().numpy()
+        self._check_device()
+        return a
 
     def read_action(self, i):
-        return self.out[i].cpu().numpy()
+        a = self.out[i].cpu().numpy()
+        self._check_device()
+        return a
 
     def read_version_log(self, n):
         return self.version_log[:n].cpu().numpy()

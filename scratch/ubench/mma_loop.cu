@@ -126,7 +126,7 @@ int main() {
     enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE); }
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 232000);
-  for (int bn : {32, 64}) for (int grid : {1}) for (int mode : {4, 50, 51}) for (int nkb : {2000}) {
+  for (int bn : {16, 32, 64, 128, 256}) for (int grid : {1, 148}) for (int mode : {0, 4, 8, 12}) for (int nkb : {2000}) {
     cudaMemset(flag, 0, 64);
     bench<<<grid, 128, 232000>>>(nkb, bn, mode, d, tm, flag);
     long long h = 0; cudaError_t e = cudaDeviceSynchronize(); cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);

@@ -26,12 +26,13 @@ def _plan(S, n_steps, rng):
     return [(int(s), int(c)) for s, c in zip(starts, counts)]
 
 
-def run_denoise_launch(cfg_name, S, agents=1, seed=0):
+def run_denoise_launch(cfg_name, S, agents=1, seed=0, w=None):
     """One DPSession.generate call (one denoise launch per iteration chain of
     the frame) over S samples on the device, and the same samples through the
-    bf16-faithful oracle.  Returns (device x, oracle x, x_in)."""
+    bf16-faithful oracle.  Returns (device x, oracle x, x_in, kernel id).
+    `w`: weights to use instead of the seeded preset weights."""
     cfg = D.PRESETS[cfg_name]
-    w = weights(cfg_name)
+    w = weights(cfg_name) if w is None else w
     pol = D.make_diffusion_policy(cfg_name, dtype="bf16", weights=w, agents=agents)
     lanes = -(-S // agents)
     P, G = torch.cuda.Stream(), torch.cuda.Stream()
