@@ -780,9 +780,9 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
 
 // ---------------------------------------------------------------- host side
 
-static int pow2_floor(int x) {
+static int pow2_ceil(int x) {
   int p = 1;
-  while (p * 2 <= x) p *= 2;
+  while (p < x) p *= 2;
   return p;
 }
 
@@ -896,7 +896,14 @@ int clus_build(ClConfig &cc, const std::vector<auras_conv_op> &ops, int S, const
     m.nmt = (dual && m.m_tiles % 2 == 0 && (m.m_tiles > nc || m.cg == 256)) ? 2 : 1;
     m.pair = m.gn && m.cg == 256 && m.nmt == 1;
     const int cap = m.nmt == 2 ? bn_cap / 2 : bn_cap;
-    m.s_box = std::min(CK_SMAX, pow2_floor(std::max(1, std::min(S, cap / o.Wo))));
+    {
+      // samples per column tile: as few tiles as the width allows, each padded up to a
+      // power of two (the TMA box zero-fills samples past S; the epilogue skips them),
+      // so e.g. S = 5..7 stream each layer's weights once, like S = 8
+      const int smax = std::min(CK_SMAX, std::max(1, cap / o.Wo));
+      const int ntl = (S + smax - 1) / smax;
+      m.s_box = std::min(smax, pow2_ceil((S + ntl - 1) / ntl));
+    }
     m.rows = m.s_box * o.Wo;
     m.bn = std::max(16, m.rows);
     if (m.nmt == 2 && (m.bn > bn_var / 2 || 4 * m.s_box > 64)) {
