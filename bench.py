@@ -219,7 +219,7 @@ class Window:
 
 
 def run_window(policy, depth, offset, agents, W, K, dist, device, sequential=False, on_frame=None,
-               frame_source=None):
+               frame_source=None, alpha=0.0):
     from paper_2509_09560_b200 import PipelineConfig, run_pipelined, run_sequential
     if sequential:
         fill = 0
@@ -228,7 +228,7 @@ def run_window(policy, depth, offset, agents, W, K, dist, device, sequential=Fal
         res = run_sequential(policy, None, duration, clock="device", agents=agents, frame_hook=win,
                              frame_source=frame_source)
     else:
-        cfg = PipelineConfig(pp_perception=1, pp_generation=depth, fetch_offset=offset)
+        cfg = PipelineConfig(pp_perception=1, pp_generation=depth, fetch_offset=offset, alpha=alpha)
         fill = depth - 1 - offset
         duration = fill + W + K + 1
         win = Window(dist, fill + W, K, device, on_frame)
@@ -597,11 +597,18 @@ def main():
         out["depth1"] = {"value": v1, "unit": "actions/s", "speedup_at_depth": value / v1}
 
     if args.sweep:
-        sweep = {}
-        for k in range(1, 9):
-            wk, rk, fk = run_window(pol, k, 0, A, 3, 12, dist, dist.local)
-            sweep[k] = 12 * A * dist.world / (dist.max(wk.ms) / 1e3)
-        out["depth_sweep_offset0"] = sweep
+        # BASELINE configs[2]: depth k = 1..8 at offsets 0 and -1 (fp/executor.py:62-65,
+        # 220-221), plus the skewed split alpha = 1 at k = 5 (fp/partition.py:111-123)
+        for off in (0, -1):
+            sweep = {}
+            for k in range(1, 9):
+                if k - 1 - off < 0:
+                    continue
+                wk, rk, fk = run_window(pol, k, off, A, 3, 12, dist, dist.local)
+                sweep[k] = 12 * A * dist.world / (dist.max(wk.ms) / 1e3)
+            out[f"depth_sweep_offset{off}"] = sweep
+        wk, rk, fk = run_window(pol, 5, 0, A, 3, 12, dist, dist.local, alpha=1.0)
+        out["alpha1_k5"] = 12 * A * dist.world / (dist.max(wk.ms) / 1e3)
 
     if args.baselines:
         out["baselines"] = baseline_modes(pol, args.depth, A, dist)

@@ -57,6 +57,14 @@ int auras_ring_fetch(const int64_t *meta, const int64_t *state, int capacity, in
 /* Disaggregated variant (perception GPU != generation GPU): the same commit
  * with a system-scope release so a consumer on another GPU (or a peer-mapped
  * reader) observes the payload before the version. */
+/* Stress test of the ring's publish/fetch ordering (test support; replaces the
+ * threaded torn-read test of t/test_context_store.py:148-183 / fp/verify.py:83-123
+ * on the device).  One writer block publishes n_versions into a `capacity`-slot
+ * ring of `words` fp64 words with commit_slot's order while `readers` blocks
+ * fetch the newest entry seqlock-style.  Synchronous.  counts_host receives
+ * [readers][4] = {consistent reads, retries, torn reads, version regressions}. */
+int auras_ring_stress(int capacity, int words, int n_versions, int readers, unsigned long long *counts_host);
+
 int auras_ring_commit_sys(int64_t *meta, int64_t *state, int capacity, int64_t frame,
                           int64_t expected_version, void *stream);
 

@@ -92,6 +92,7 @@ _SIGNATURES = {
     "auras_unet_mega_trace": (C.c_int, [vp, C.c_int, vp, vp, C.c_int]),
     "auras_unet_kernel_for": (C.c_int, [vp, C.c_int]),
     "auras_unet_check": (C.c_int, [vp]),
+    "auras_ring_stress": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, vp]),
     "auras_unet_launches_per_iter": (C.c_int, [vp]),
     "auras_conv": (C.c_int, [C.POINTER(ConvOp), C.c_int, C.c_int, vp, C.c_int, vp, i64, vp]),
     "auras_linear": (C.c_int, [C.POINTER(LinearOp), C.c_int, C.c_int, vp, C.c_int, vp, C.c_int, vp]),

@@ -119,6 +119,9 @@ struct ClParams {
   int n_ops, S, nc, n_tasks;
   int l2_prefetch;          // L2 prefetch mode for the ring overflow of a task's weights
   int hack;                 // timing experiments (AURAS_CL_HACK); 0 in production
+  int fault;                // stall injection for the watchdog test (AURAS_FAULT_STALL); 0 in production
+  long long spin_timeout_ns;
+  int spin_mode;
   UnetDev *dev;
   auras_sched sched;
   int horizon, adim;

@@ -81,6 +81,92 @@ __global__ void ring_fetch_kernel(const int64_t *meta, const int64_t *state, int
   if (log) log[log_index] = v;
 }
 
+// ---------------------------------------------------------------- ring stress (test)
+// t/test_context_store.py:148-183 on the device: block 0 publishes versions
+// 1..n into a `capacity`-slot ring with the product's order (version word
+// invalidated with a release store, payload written by the whole block, then
+// commit_slot: frame, fence, version with release); blocks 1..readers fetch the
+// newest entry concurrently, seqlock style: acquire the version, read the
+// payload, fence, re-read the version.  A read whose two versions agree must
+// carry the writer's words for that version (fp/context.py:28-36 checks a
+// checksum; here every word is checked) and versions must never go backwards.
+// counts[r] = {consistent reads, retries, torn reads, version regressions}.
+__device__ __forceinline__ double stress_word(int64_t v, int j) { return (double)v * 4096.0 + (double)j; }
+
+__global__ void ring_stress_kernel(int64_t *meta, int64_t *state, double *payload, int capacity, int words,
+                                   int n, int *done, unsigned long long *counts) {
+  if (blockIdx.x == 0) {
+    for (int64_t v = 1; v <= n; ++v) {
+      const int64_t frame = v - 1;
+      const int slot = ring_slot(frame, capacity);
+      if (threadIdx.x == 0) st_release_gpu(&meta[2 * slot + 1], -1);
+      __syncthreads();
+      for (int j = threadIdx.x; j < words; j += blockDim.x) payload[(int64_t)slot * words + j] = stress_word(v, j);
+      __syncthreads();
+      if (threadIdx.x == 0) commit_slot(meta, state, capacity, frame, v);
+      __syncthreads();
+      __nanosleep(1000);                            // give readers a window between publishes
+    }
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicExch(done, 1);
+    }
+    return;
+  }
+  __shared__ int64_t s_v;
+  __shared__ int s_bad, s_stop;
+  unsigned long long ok = 0, retry = 0, torn = 0, regress = 0;
+  int64_t last = 0;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      s_stop = atomicAdd(done, 0);
+      int64_t vc;
+      asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(vc) : "l"(&state[0]) : "memory");
+      int64_t v1 = -1;
+      if (vc > 0) v1 = ld_acquire_gpu(&meta[2 * ring_slot(vc - 1, capacity) + 1]);
+      s_v = (vc > 0 && v1 == vc) ? vc : 0;
+      s_bad = 0;
+    }
+    __syncthreads();
+    const int64_t v = s_v;
+    const int stop = s_stop;
+    if (v > 0) {
+      const int slot = ring_slot(v - 1, capacity);
+      int bad = 0;
+      for (int j = threadIdx.x; j < words; j += blockDim.x) {
+        double x;
+        asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(x) : "l"(&payload[(int64_t)slot * words + j]) : "memory");
+        bad |= x != stress_word(v, j);
+      }
+      __threadfence();                              // payload reads before the re-check
+      if (bad) atomicOr(&s_bad, 1);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int64_t v2;
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v2) : "l"(&meta[2 * slot + 1]) : "memory");
+        if (v2 != v) ++retry;                       // overwritten while reading: discard
+        else if (s_bad) ++torn;
+        else {
+          ++ok;
+          if (v < last) ++regress;
+          last = v;
+        }
+      }
+    } else if (threadIdx.x == 0) {
+      ++retry;
+    }
+    __syncthreads();
+    if (stop) break;
+  }
+  if (threadIdx.x == 0) {
+    unsigned long long *c = counts + 4 * (blockIdx.x - 1);
+    c[0] = ok;
+    c[1] = retry;
+    c[2] = torn;
+    c[3] = regress;
+  }
+}
+
 // ---------------------------------------------------------------- toy policy
 
 __global__ void toy_ingest_kernel(double *latent, int lane, double o0, double o1, double o2,
@@ -170,6 +256,43 @@ int auras_ring_commit(int64_t *meta, int64_t *state, int capacity, int64_t frame
   ring_commit_kernel<<<1, 1, 0, as_stream(stream)>>>(meta, state, capacity, frame, expected_version);
   AURAS_LAUNCHED("ring_commit_kernel");
   return AURAS_OK;
+}
+
+int auras_ring_stress(int capacity, int words, int n_versions, int readers, unsigned long long *counts_host) {
+  if (capacity < 2 || words < 1 || n_versions < 1 || readers < 1 || readers > 64 || !counts_host) {
+    set_error("ring_stress: bad args");
+    return AURAS_E_ARG;
+  }
+  int64_t *meta = nullptr, *state = nullptr;
+  double *payload = nullptr;
+  int *done = nullptr;
+  unsigned long long *counts = nullptr;
+  int rc = AURAS_OK;
+  if ((rc = cuda_check(cudaMalloc(&meta, sizeof(int64_t) * 2 * capacity), "malloc")) ||
+      (rc = cuda_check(cudaMalloc(&state, sizeof(int64_t) * 4), "malloc")) ||
+      (rc = cuda_check(cudaMalloc(&payload, sizeof(double) * (size_t)capacity * words), "malloc")) ||
+      (rc = cuda_check(cudaMalloc(&done, sizeof(int)), "malloc")) ||
+      (rc = cuda_check(cudaMalloc(&counts, sizeof(unsigned long long) * 4 * readers), "malloc")))
+    goto out;
+  cudaMemset(meta, 0, sizeof(int64_t) * 2 * capacity);
+  cudaMemset(payload, 0, sizeof(double) * (size_t)capacity * words);
+  cudaMemset(done, 0, sizeof(int));
+  {
+    const int64_t st0[4] = {0, -1, 0, 0};
+    cudaMemcpy(state, st0, sizeof(st0), cudaMemcpyHostToDevice);
+  }
+  ring_stress_kernel<<<1 + readers, 256>>>(meta, state, payload, capacity, words, n_versions, done, counts);
+  if ((rc = cuda_check(cudaGetLastError(), "ring_stress_kernel"))) goto out;
+  if ((rc = cuda_check(cudaDeviceSynchronize(), "ring_stress_kernel"))) goto out;
+  rc = cuda_check(cudaMemcpy(counts_host, counts, sizeof(unsigned long long) * 4 * readers,
+                             cudaMemcpyDeviceToHost), "copy counts");
+out:
+  cudaFree(meta);
+  cudaFree(state);
+  cudaFree(payload);
+  cudaFree(done);
+  cudaFree(counts);
+  return rc;
 }
 
 int auras_ring_commit_sys(int64_t *meta, int64_t *state, int capacity, int64_t frame,

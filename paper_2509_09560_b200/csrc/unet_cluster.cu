@@ -131,35 +131,48 @@ __device__ __forceinline__ long long ck_time() {
 
 // Dependency wait.  Polls with relaxed loads (an ld.acquire.gpu in the loop
 // emits an L1 invalidation per probe), then one acquire load.  A wait longer
-// than kSpinTimeoutNs flags P.err (surfaced by the host as DeadlockDetected,
-// auras_unet_check) and gives up instead of hanging the GPU.
-constexpr long long kSpinTimeoutNs = 2000000000ll;
-
+// than P.spin_timeout_ns (2 s; AURAS_SPIN_TIMEOUT_MS) flags P.err -- surfaced by
+// the host as DeadlockDetected (auras_unet_check) -- and gives up instead of
+// hanging the GPU.
 __device__ __forceinline__ int ld_relaxed_i32(const int *p) {
   int v;
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
-__device__ __noinline__ void ck_spin_slow(int *err, const int *ctr, int target) {
+__device__ __noinline__ void ck_spin_slow(int *err, long long timeout_ns, const int *ctr, int target) {
   const long long t0 = ck_time();
   for (int n = 1; ld_relaxed_i32(ctr) < target; ++n)
-    if ((n & 1023) == 0 && ck_time() - t0 > kSpinTimeoutNs) {
+    if ((n & 1023) == 0 && ck_time() - t0 > timeout_ns) {
       atomicExch(err, 1);
       return;
     }
 }
 
-__device__ __forceinline__ void ck_spin(int *err, const int *ctr, int target) {
-  if (ld_relaxed_i32(ctr) < target) ck_spin_slow(err, ctr, target);
-  (void)ld_acquire_i32(ctr);
+__device__ __noinline__ void ck_spin_slow_acq(int *err, long long timeout_ns, const int *ctr, int target) {
+  const long long t0 = ck_time();
+  for (int n = 1; ld_acquire_i32(ctr) < target; ++n)
+    if ((n & 1023) == 0 && ck_time() - t0 > timeout_ns) {
+      atomicExch(err, 1);
+      return;
+    }
+}
+
+__device__ __forceinline__ void ck_spin(const ClParams &P, const int *ctr, int target) {
+  if (P.spin_mode == 2) {
+    if (ld_acquire_i32(ctr) < target) ck_spin_slow_acq(P.err, P.spin_timeout_ns, ctr, target);
+    return;
+  }
+  if (ld_relaxed_i32(ctr) < target) ck_spin_slow(P.err, P.spin_timeout_ns, ctr, target);
+  if (P.spin_mode == 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  else (void)ld_acquire_i32(ctr);
 }
 
 // Counters accumulate over the frame's iterations: iteration `it` needs
 // (it + 1) x the per-iteration count.
 __device__ __forceinline__ void ck_wait_dep(const ClParams &P, const int *prep_done, int d, int tgt, int it) {
-  if (d == -2) ck_spin(P.err, prep_done, P.S * (it + 1));
-  else if (d >= 0) ck_spin(P.err, &P.ctr[d], tgt * (it + 1));
+  if (d == -2) ck_spin(P, prep_done, P.S * (it + 1));
+  else if (d >= 0) ck_spin(P, &P.ctr[d], P.fault ? 0x7fffffff : tgt * (it + 1));   // fault: stall injection (tests)
 }
 
 // Equal-count merge of k (mean, M2) pairs of n0 values each (fixed order).
@@ -459,7 +472,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           // CTAs; with GroupNorm, (mean, M2) of 2 * nmt atoms x s_box samples from each
           mbar_expect_tx(&rbar[buf], (uint32_t)(CL * 16 * nmt * bn * 2));
           if (gn) mbar_expect_tx(&rbar[2 + (gn_i & 1)], (uint32_t)(CL * 2 * nmt * sbox * 8));
-          if (film) ck_spin(P.err, prep_done, S * (it + 1));
+          if (film) ck_spin(P, prep_done, S * (it + 1));
           for (int d = 0; d < 2; ++d) ck_wait_dep(P, prep_done, op->epi_dep[d], op->epi_tgt[d], it);
           if (P.trace) CK_TR(12);
         }
@@ -546,10 +559,15 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
               // otherwise e = 0 and nothing extra is sent.
               // (columns past the tile's `rows` hold products of stale operand rows: excluded)
               float mx = 0.f;
+              if (c + 16 <= rows) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) mx = fmaxf(mx, c + i < rows ? fabsf(x[i]) : 0.f);
+                for (int i = 0; i < 16; ++i) mx = fmaxf(mx, fabsf(x[i]));
+              } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) mx = fmaxf(mx, c + i < rows ? fabsf(x[i]) : 0.f);
+              }
               const int ex = min(126, max(0, ((__float_as_int(mx) >> 23) & 0xff) - 127 - 14));
-              if (__any_sync(0xffffffffu, ex > 0)) {
+              if (!(P.hack & 128) && __any_sync(0xffffffffu, ex > 0)) {
                 if (ex > 0) {
                   const float down = __int_as_float((127 - ex) << 23);
 #pragma unroll
@@ -636,7 +654,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           float2 gs = make_float2(0.f, 0.f);
           float ncount = 1.f;
           if (pair) {                                     // partner tile's 8 CTAs have published
-            if (et == 0) ck_spin(P.err, &P.flags[fi ^ 1], CL);
+            if (et == 0) ck_spin(P, &P.flags[fi ^ 1], CL);
             esync();
           }
           if (in_pair) {
@@ -749,7 +767,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         }
       } else if (type == K_FINAL) {
         if (tk.w != rank) continue;
-        if (et == 0) ck_spin(P.err, &done[P.n_ops - 1], P.ops[P.n_ops - 1].tiles * CL * (it + 1));
+        if (et == 0) ck_spin(P, &done[P.n_ops - 1], P.ops[P.n_ops - 1].tiles * CL * (it + 1));
         if (P.trace && et == 0) CK_TR(0);
         esync();
         final_body<__nv_bfloat16>(P.dev, tk.y, et, CK_EPI, P.sched, P.horizon, P.adim, P.y_final, P.y_pitch,
@@ -1102,6 +1120,12 @@ int clus_build(ClConfig &cc, const std::vector<auras_conv_op> &ops, int S, const
     cc.params.l2_prefetch = e ? atoi(e) : 0;
     e = getenv("AURAS_CL_HACK");        // timing experiments only: 1 = skip activation boxes, 2 = skip weights
     cc.params.hack = e ? atoi(e) : 0;
+    e = getenv("AURAS_SPIN_TIMEOUT_MS");
+    cc.params.spin_timeout_ns = (long long)((e ? atof(e) : 2000.0) * 1e6);
+    e = getenv("AURAS_SPIN_MODE");
+    cc.params.spin_mode = e ? atoi(e) : 0;
+    e = getenv("AURAS_FAULT_STALL");    // tests: every layer dependency becomes unreachable
+    cc.params.fault = e ? atoi(e) : 0;
   }
   return AURAS_OK;
 }
