@@ -71,15 +71,10 @@ def _lib_round(x, m):
     return (x + m - 1) // m * m
 
 
-def test_small_vit_dpt_ddim_pipeline_matches_oracle():
-    """The DP-T path with a DDIM scheduler (16 steps), a 4-block ViT at 64x64
-    and a 2-layer denoiser: pipelined at depth 4 vs the oracle pipeline.
-    Tolerance 1e-1: DDIM (eta = 0) is a deterministic chain whose
-    coefficients amplify the ~0.5 % per-step bf16 eps error of these random
-    weights to 5-7 % on the action (measured); the per-step bar (3e-2, test
-    above) and the DDPM pipelines (6e-2) carry the precision claim."""
+def _ddim_pipeline_err(hoist, monkeypatch):
     from oracle import schedule as osched
     from paper_2509_09560_b200 import PipelineConfig, run_pipelined
+    monkeypatch.setenv("AURAS_DPT_HOIST", "1" if hoist else "0")
     cfg = D.DPConfig(name="dpt_ddim_test", encoder="vit_b16", image_hw=64, feat_dim=768, action_dim=7,
                      denoiser="transformer", scheduler="ddim", num_inference_steps=16, vit_depth=4, dpt_layers=2)
     w = D.init_weights(cfg, 3, device="cpu")
@@ -92,5 +87,25 @@ def test_small_vit_dpt_ddim_pipeline_matches_oracle():
     g = np.array([a.values for a in res.actions])
     r = np.array([a.values for a in ref.actions])
     assert g.shape == r.shape and len(g) > 0
-    assert float(np.abs(g - r).max() / np.abs(r).max()) <= 1e-1
     assert [q.context_versions for q in res.requests] == [q.context_versions for q in ref.requests]
+    return float(np.abs(g - r).max() / np.abs(r).max())
+
+
+def test_small_vit_dpt_ddim_pipeline_matches_oracle(monkeypatch):
+    """The DP-T path with a DDIM scheduler (16 steps), a 4-block ViT at 64x64
+    and a 2-layer denoiser: pipelined at depth 4 vs the fp32 oracle pipeline.
+
+    DDIM (eta = 0) is a deterministic chain whose coefficients amplify the
+    ~0.5 % per-step bf16 eps error of these random weights (per-step bar 3e-2,
+    test above) to several % on the action, so the absolute bar is 1e-1.  The
+    hoisted cross-attention memory (time rows tabled per inference step,
+    observation K|V once per frame) must not be the source of that error: the
+    hoisted path's error may not exceed the per-iteration path's
+    (AURAS_DPT_HOIST=0, every GEMM of the cross-attention on the device each
+    iteration) by more than 10 % + 1e-3."""
+    e_hoist = _ddim_pipeline_err(True, monkeypatch)
+    e_plain = _ddim_pipeline_err(False, monkeypatch)
+    print(f"DDIM DP-T pipeline vs fp32 oracle: hoisted {e_hoist:.3e}, per-iteration {e_plain:.3e}")
+    assert e_plain <= 1e-1, e_plain
+    assert e_hoist <= 1e-1, e_hoist
+    assert e_hoist <= 1.1 * e_plain + 1e-3, (e_hoist, e_plain)
