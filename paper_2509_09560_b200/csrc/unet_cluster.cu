@@ -158,41 +158,6 @@ __device__ __noinline__ void ck_spin_slow_acq(int *err, long long timeout_ns, co
     }
 }
 
-// mbarrier wait (acquire, cluster scope) with the same watchdog: a task's
-// partials come from the 7 peers; if one of them stalled, give up after the
-// timeout and flag P.err rather than hang the GPU.  (Every wait keeps its own
-// timeout -- no early exit once P.err is set: the DSMEM exchanges of the
-// remaining tasks must stay matched, or CTAs would run ahead of their peers'
-// stores into their shared memory.)
-__device__ __noinline__ void ck_wait_cluster_slow(int *err, long long timeout_ns, uint64_t *bar, uint32_t parity) {
-  const long long t0 = ck_time();
-  for (int n = 1;; ++n) {
-    uint32_t ok;
-    asm volatile(
-        "{\n.reg .pred p;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (ok) return;
-    if ((n & 63) == 0 && ck_time() - t0 > timeout_ns) {
-      atomicExch(err, 1);
-      return;
-    }
-  }
-}
-
-__device__ __forceinline__ void ck_wait_cluster(const ClParams &P, uint64_t *bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n.reg .pred p;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  // (at least 2 s whatever AURAS_SPIN_TIMEOUT_MS says: a peer may legitimately be a few
-  // dependency timeouts behind, and giving up on its partials would unmatch the exchange)
-  if (!ok) ck_wait_cluster_slow(P.err, max(P.spin_timeout_ns, 2000000000ll), bar, parity);
-}
-
 __device__ __forceinline__ void ck_spin(const ClParams &P, const int *ctr, int target) {
   if (P.spin_mode == 2) {
     if (ld_acquire_i32(ctr) < target) ck_spin_slow_acq(P.err, P.spin_timeout_ns, ctr, target);
@@ -378,7 +343,8 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
       const CUtensorMap *tmB = &op->tmB;
       if (lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(tmB) : "memory");   // descriptor fetch off the critical path
-        for (int d = 0; d < 3; ++d) ck_wait_dep(P, prep_done, op->gemm_dep[d], op->gemm_tgt[d], it);
+        if (!(P.hack & 32768))
+          for (int d = 0; d < 3; ++d) ck_wait_dep(P, prep_done, op->gemm_dep[d], op->gemm_tgt[d], it);
         fence_proxy_async();
         if (P.trace && bw == 0) CK_TR(0);
       }
@@ -394,7 +360,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         const int off = tap - pad;
         const int q = off >= 0 ? off / stride : -((-off + stride - 1) / stride);
         const int h = off - q * stride;
-        if ((P.hack & 1) && j > 0) { if (lane == 0) mbar_arrive(&fullB[sb]); __syncwarp(); continue; }
+        if ((P.hack & 1) && (j > 0 || (P.hack & 16384))) { if (lane == 0) mbar_arrive(&fullB[sb]); __syncwarp(); continue; }
         if (P.hack & 8) {
           if (lane == ((j / CK_NBW) & 31)) {
             mbar_expect_tx(&fullB[sb], bbytes);
@@ -439,8 +405,9 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           if (P.trace && lane == 0 && kb == kb0) CK_TR(1);
           par ^= 1u << sb;
           pa_bits ^= 1u << sa;
-          umma_kblock2_warp(dt, dt + CK_BN, umma_desc(sA0 + sa * CK_A_STAGE), umma_desc(sB0 + sb * bstage), idesc,
-                            kb > kb0 ? 1u : 0u);
+          if (!(P.hack & 1024))
+            umma_kblock2_warp(dt, dt + CK_BN, umma_desc(sA0 + sa * CK_A_STAGE), umma_desc(sB0 + sb * bstage), idesc,
+                              kb > kb0 ? 1u : 0u);
           umma_commit_warp(&emptyB[sb]);
           umma_commit_warp(&emptyA[sa]);
           sb = sb + 1 == nbst ? 0 : sb + 1;
@@ -457,8 +424,9 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
             mbar_wait(&fullB[sb], (par >> sb) & 1);
             if (P.trace && lane == 0 && kb == kb0 && i == 0) CK_TR(1);
             par ^= 1u << sb;
-            umma_kblock_warp(dt, umma_desc(a0 + i * CK_A_BYTES), umma_desc(sB0 + sb * bstage), idesc,
-                             (kb > kb0 || i > 0) ? 1u : 0u);
+            if (!(P.hack & 1024))
+              umma_kblock_warp(dt, umma_desc(a0 + i * CK_A_BYTES), umma_desc(sB0 + sb * bstage), idesc,
+                               (kb > kb0 || i > 0) ? 1u : 0u);
             umma_commit_warp(&emptyB[sb]);
             sb = sb + 1 == nbst ? 0 : sb + 1;
           }
@@ -488,6 +456,10 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         const EpiArgs e = op->epi;
         const int M = op->M, Wo = op->Wo, sbox = op->s_box, rows = op->rows, bn = op->bn;
         const int kps = op->kps, kbt = op->kb_total, gn = op->gn, cg = op->cg, pair = op->pair;
+        // timing ablations (AURAS_CL_HACK, scratch/r2_ab.sh; 0 in production): 256 no statistics
+        // exchange, 512 no partials exchange, 1024 no UMMA, 2048 no apply / store, 16384 (with 1)
+        // no activation boxes, 32768 no dependency waits
+        const int gnx = gn && !(P.hack & 256);
         const int nmt = op->nmt, mt0 = tk.y * nmt, nt = tk.z, S = P.S;
         const int lwo = op->lwo, lsb = op->lsb, lcg = op->lcg;
         const int RPC = 16 * nmt;                        // rows (channels) owned by this CTA
@@ -505,10 +477,11 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         if (et == 0) {
           // bytes this CTA will receive: 16 * nmt rows x bn fp16 partials from each of the 8
           // CTAs; with GroupNorm, (mean, M2) of 2 * nmt atoms x s_box samples from each
-          mbar_expect_tx(&rbar[buf], (uint32_t)(CL * 16 * nmt * bn * 2));
-          if (gn) mbar_expect_tx(&rbar[2 + (gn_i & 1)], (uint32_t)(CL * 2 * nmt * sbox * 8));
+          if (!(P.hack & 512)) mbar_expect_tx(&rbar[buf], (uint32_t)(CL * 16 * nmt * bn * 2));
+          if (gnx) mbar_expect_tx(&rbar[2 + (gn_i & 1)], (uint32_t)(CL * 2 * nmt * sbox * 8));
           if (film) ck_spin(P, prep_done, S * (it + 1));
-          for (int d = 0; d < 2; ++d) ck_wait_dep(P, prep_done, op->epi_dep[d], op->epi_tgt[d], it);
+          if (!(P.hack & 32768))
+            for (int d = 0; d < 2; ++d) ck_wait_dep(P, prep_done, op->epi_dep[d], op->epi_tgt[d], it);
           if (P.trace) CK_TR(12);
         }
         esync();
@@ -601,8 +574,9 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
 #pragma unroll
                 for (int i = 0; i < 16; ++i) mx = fmaxf(mx, c + i < rows ? fabsf(x[i]) : 0.f);
               }
-              const int ex = min(126, max(0, ((__float_as_int(mx) >> 23) & 0xff) - 127 - 14));
-              if (!(P.hack & 128) && __any_sync(0xffffffffu, ex > 0)) {
+#ifndef CK_NO_RANGE
+              if (__any_sync(0xffffffffu, mx >= 32768.f) && !(P.hack & 128)) {
+                const int ex = min(126, max(0, ((__float_as_int(mx) >> 23) & 0xff) - 127 - 14));
                 if (ex > 0) {
                   const float down = __int_as_float((127 - ex) << 23);
 #pragma unroll
@@ -616,14 +590,17 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
                 }
                 asm volatile("fence.acq_rel.cluster;" ::: "memory");
               }
+#endif
               uint32_t hw[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
                 const __half2 h2 = __floats2half2_rn(x[2 * i], x[2 * i + 1]);
                 hw[i] = *reinterpret_cast<const uint32_t *>(&h2);
               }
-              st_async_v4_b32(dst + c * 2, hw[0], hw[1], hw[2], hw[3], rbar_dst);
-              st_async_v4_b32(dst + c * 2 + 16, hw[4], hw[5], hw[6], hw[7], rbar_dst);
+              if (!(P.hack & 512)) {
+                st_async_v4_b32(dst + c * 2, hw[0], hw[1], hw[2], hw[3], rbar_dst);
+                st_async_v4_b32(dst + c * 2 + 16, hw[4], hw[5], hw[6], hw[7], rbar_dst);
+              }
             }
           }
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -631,29 +608,40 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           if (lane == 0) mbar_arrive(&tempty[buf]);
           if (P.trace && et == 0) CK_TR(4);
         }
-        ck_wait_cluster(P, &rbar[buf], (gi >> 1) & 1);           // all 8 CTAs' partials have landed
+        if (!(P.hack & 512)) mbar_wait_cluster(&rbar[buf], (gi >> 1) & 1);   // all 8 CTAs' partials have landed
         if (P.trace && et == 0) CK_TR(5);
         // ---- fixed-order sum of the 8 K slices + bias (fp32); slices a source scaled
-        //      (exponent bytes, flagged per buffer) are scaled back
+        //      (exponent bytes, flagged per buffer: rare) are scaled back out of line
+#ifndef CK_NO_RANGE
         const uint32_t scaled = expf[buf];
+#else
+        const uint32_t scaled = 0;
+#endif
+        if (!scaled) {
 #pragma unroll
-        for (int k = 0; k < VMAX; ++k) {
-          float acc = bias[k];
-          if (mine && k < 4 * NH) {
-            const __half *rp = recvb + (row0 + k) * RSH + col;
-            if (!scaled) {
+          for (int k = 0; k < VMAX; ++k) {
+            float acc = bias[k];
+            if (mine && k < 4 * NH) {
+              const __half *rp = recvb + (row0 + k) * RSH + col;
 #pragma unroll
               for (int src = 0; src < CL; ++src) acc += __half2float(rp[src * RPC * RSH]);
-            } else {
-              acc += ck_sum_scaled(rp, RPC * RSH, exps + buf * Lay::EXP_BYTES + (row0 + k) * 8 + (col >> 4));
             }
+            v[k] = acc;
           }
-          v[k] = acc;
+        } else {
+#pragma unroll
+          for (int k = 0; k < VMAX; ++k) {
+            float acc = bias[k];
+            if (mine && k < 4 * NH)
+              acc += ck_sum_scaled(recvb + (row0 + k) * RSH + col, RPC * RSH,
+                                   exps + buf * Lay::EXP_BYTES + (row0 + k) * 8 + (col >> 4));
+            v[k] = acc;
+          }
         }
         const float n0 = 8.f * Wo;
         const int fi = pair ? op->flag_base + nt * op->m_tiles + mt0 : 0;
         float mean_g = 0.f, rstd_g = 1.f;
-        if (gn) {
+        if (gnx) {
           // ---- atom statistics: 8 rows x Wo columns of (pa, pj), butterfly over the pair's L lanes
           if (in_pair) {
             float sum = 0.f, sq = 0.f;
@@ -679,9 +667,9 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           }
         }
         if (P.trace && et == 0) CK_TR(6);
-        if (gn) ck_wait_cluster(P, &rbar[2 + (gn_i & 1)], (gn_i >> 1) & 1);   // every peer's statistics
+        if (gnx) mbar_wait_cluster(&rbar[2 + (gn_i & 1)], (gn_i >> 1) & 1);   // every peer's statistics
         if (P.trace && et == 0) CK_TR(7);
-        if (gn) {
+        if (gnx) {
           // ---- merge the atoms of each group (butterfly, fixed lane order); task atoms are
           //      numbered in channel order q = tile * 16 + within-tile atom; 256-channel groups
           //      split over two tasks also merge the partner tile's statistics from L2.  Every
@@ -736,7 +724,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
         }
         if (P.trace && et == 0) CK_TR(8);
         // ---- normalise, activate, FiLM, residual (registers) and store 4 channels per half
-        if (mine) {
+        if (mine && !(P.hack & 2048)) {
           const float rba = e.res_before_act ? 1.f : 0.f;
           const float is_mish = e.act == AURAS_ACT_MISH ? 1.f : 0.f;
           const float is_relu = e.act == AURAS_ACT_RELU ? 1.f : 0.f;
@@ -787,7 +775,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
           if (P.trace) CK_TR(11);
         }
         ++gi;
-        gn_i += gn;
+        gn_i += gnx;
       } else if (type == K_PREP) {
         if (tk.w != rank || it > 0) continue;            // later iterations: prepared by the final task
         if (P.trace && et == 0) CK_TR(0);
