@@ -525,10 +525,10 @@ def main():
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     tflops = S_med * flops_sample / (step_ms / 1e3) / 1e12 if step_ms > 0 else 0.0
     # DRAM bytes per launch of the denoise kernel from the committed ncu --set full
-    # capture (profiles/r1_ncu_unet_cluster.json), for the same S, when it was captured
+    # capture (profiles/r2_ncu_unet_cluster.json), for the same S, when it was captured
     traffic = None
     try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "r1_ncu_unet_cluster.json")))
+        prof = json.load(open(os.path.join(ROOT, "profiles", "r2_ncu_unet_cluster.json")))
         dk = LAST_EVENTS.get("denoise_kernel") or {}
         kern = dk.get(S_med) or dk.get(str(S_med)) or ""
         if f"S{S_med}" in prof and "cluster" in kern and args.config == prof.get("config", "pusht"):
@@ -578,7 +578,7 @@ def main():
            "mean_staleness_final_frames": float(np.mean(ages)) if ages else None,
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                         "frac": achieved / hbm_peak, "traffic": traffic,
-                        "traffic_source": "ncu dram__bytes_read+write per launch, profiles/r1_ncu_unet_cluster.json",
+                        "traffic_source": "ncu dram__bytes_read+write per launch, profiles/r2_ncu_unet_cluster.json",
                         "kernel": "denoise chain (" + ("DP-T GEMMs + attention + update" if dpt else "UNet conv GEMMs + fused epilogues") + "), per step",
                         "step_ms": step_ms, "algorithmic_bytes_per_step": bytes_step + act_bytes,
                         "tensor_tflops": tflops, "tensor_frac": tflops / tc_peak,
