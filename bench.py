@@ -189,14 +189,20 @@ class Window:
     """frame_hook: drain + barrier + start event at frame `t0`; end event on the
     generation stream after frame t0+K-1; clocks sampled in between."""
 
-    def __init__(self, dist, t0, K, device, on_frame=None):
+    def __init__(self, dist, t0, K, device, on_frame=None, on_mid=None):
         import torch
         self.torch, self.dist, self.t0, self.K = torch, dist, t0, K
         self.start = torch.cuda.Event(enable_timing=True)
         self.end = torch.cuda.Event(enable_timing=True)
         self.clocks = ClockSampler(device)
         self.on_frame = on_frame
+        self.on_mid = on_mid
         self.result = None
+
+    def mid(self, t, dev, emis):
+        # after the frame's perception is queued, before its generation (executor hook)
+        if self.on_mid is not None and self.t0 <= t < self.t0 + self.K:
+            self.on_mid(t, dev, emis)
 
     def __call__(self, t, dev, emis):
         if t == self.t0:
@@ -219,7 +225,7 @@ class Window:
 
 
 def run_window(policy, depth, offset, agents, W, K, dist, device, sequential=False, on_frame=None,
-               frame_source=None, alpha=0.0):
+               frame_source=None, alpha=0.0, on_mid=None):
     from paper_2509_09560_b200 import PipelineConfig, run_pipelined, run_sequential
     if sequential:
         fill = 0
@@ -231,7 +237,7 @@ def run_window(policy, depth, offset, agents, W, K, dist, device, sequential=Fal
         cfg = PipelineConfig(pp_perception=1, pp_generation=depth, fetch_offset=offset, alpha=alpha)
         fill = depth - 1 - offset
         duration = fill + W + K + 1
-        win = Window(dist, fill + W, K, device, on_frame)
+        win = Window(dist, fill + W, K, device, on_frame, on_mid)
         res = run_pipelined(cfg, policy, None, duration, clock="device", agents=agents,
                             frame_hook=win, frame_source=frame_source)
     return win, res, fill
@@ -628,18 +634,32 @@ def main():
             o = frames[(agent, frame % 64)]
             return type(o)(frame=frame, vector=o.vector, image=o.image)
 
+        # Every frame the host blocks on the device->host read of the newest emitted
+        # action.  Headline: the read sits where a serving loop puts it -- frame t's
+        # observation is uploaded and its perception queued, then the host waits
+        # for action t-1 and only then queues frame t's generation (executor mid-
+        # frame hook).  Strict ("e2e_lag0"): the host waits for action t-1 before
+        # it touches frame t at all, which also serialises frame t's perception
+        # behind frame t-1's generation.
         def readback(t, dev, emis):
             if emis.items:
-                emis.materialize(len(emis.items) - 1, 0)     # D2H of the newest action
+                emis.materialize(len(emis.items) - 1, 0)     # D2H of the newest action + host sync
 
         we, re_, fe = run_window(host_pol, args.depth, args.offset, A, W, K, dist, dist.local,
-                                 on_frame=readback, frame_source=source)
+                                 on_mid=readback, frame_source=source)
         e2e = K * A * dist.world / (dist.max(we.ms) / 1e3)
+        w0, _, _ = run_window(host_pol, args.depth, args.offset, A, W, K, dist, dist.local,
+                              on_frame=readback, frame_source=source)
+        e2e_lag0 = K * A * dist.world / (dist.max(w0.ms) / 1e3)
         h2d = A * (cfg.image_channels * cfg.image_hw ** 2 + 4 * cfg.agent_pos_dim
                    + 4 * cfg.horizon * cfg.action_dim * (1 + (cfg.num_inference_steps
                                                               if cfg.scheduler == "ddpm" else 0)))
         out["e2e"] = {"value": e2e, "unit": "actions/s", "h2d_bytes_per_step": h2d,
-                      "d2h_bytes_per_step": A * 4 * cfg.horizon * cfg.action_dim}
+                      "d2h_bytes_per_step": A * 4 * cfg.horizon * cfg.action_dim,
+                      "readback": "every frame: upload the frame, queue its perception, block on the D2H read "
+                                  "of the newest action, then queue the frame's generation"}
+        out["e2e_lag0"] = {"value": e2e_lag0, "unit": "actions/s",
+                           "readback": "every frame the host blocks on the newest action before enqueueing the frame"}
 
     if args.disaggregated:
         out["disaggregated"] = disaggregated_leg(args, cfg, weights, A, W, K, dist)

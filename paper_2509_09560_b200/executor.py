@@ -446,6 +446,12 @@ def run_pipelined(cfg: PipelineConfig, policy, env, duration: int, *, clock: str
                 side.append(p_cost[s - 1])
             rec["perception"].append(entry)
 
+        # optional mid-frame hook: the frame's observation and perception are queued,
+        # its generation not yet (a serving loop blocks on the previous action here)
+        mid = getattr(frame_hook, "mid", None)
+        if mid is not None:
+            mid(t, dev, emis)
+
         active = []
         for j in range(1, pp_g + 1):
             b = t - shift - (j - 1)
