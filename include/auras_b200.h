@@ -325,6 +325,48 @@ int auras_dpt_update(const float *eps, int eps_pitch, const int *agents, const i
                      float *x_lanes, const float *noise_lanes, int lanes_per_agent, int horizon, int adim,
                      const auras_sched *sched, void *stream);
 
+/* Persistent DP-T iteration (csrc/dpt_persist.cu): one launch of one 8-CTA
+ * cluster runs a whole denoise iteration of up to 128 action tokens (8 samples
+ * x horizon 16) as a program of phases -- GEMM (tcgen05, CTA r owns columns
+ * [r N/8, (r+1) N/8)), LayerNorm, attention, scheduler update -- separated by
+ * cluster barriers.  Replaces the ~110 launches per iteration of the program
+ * built from auras_conv / auras_layernorm / auras_attention / auras_dpt_update
+ * (GenerationModel.step of the transformer policy, fp/policy.py:217-228).
+ * Every pointer is device memory. */
+typedef struct auras_dpt_gemm {
+  const void *act;          /* A: [act_rows = 128][K] bf16 (tokens x channels) */
+  int act_rows, K;          /* K % 64 == 0 */
+  const void *w;            /* W: [N][K] bf16 */
+  int N;                    /* N % 128 == 0 (8 CTAs x 16k columns) or N <= 16 (one CTA) */
+  const float *bias;        /* [N] */
+  const void *res;          /* optional bf16 residual [rows][ldr] (may alias out) */
+  int ldr;
+  void *out;                /* optional bf16 output [rows][ldo] */
+  int ldo;
+  float *out_f32;           /* optional fp32 output [rows][ldf] */
+  int ldf;
+  int act_fn;               /* AURAS_ACT_* applied before the residual */
+  const void *ln_src;       /* optional: A = LayerNorm(ln_src [128][256] bf16; ln_g, ln_b), computed in the
+                               GEMM phase itself (act is then ignored; K = 256) */
+  const float *ln_g, *ln_b;
+} auras_dpt_gemm;
+typedef struct auras_dpt_op {
+  int type;                 /* 0 GEMM, 1 LayerNorm (E = 256), 2 attention, 3 scheduler update */
+  int gemm;                 /* GEMM: index into the gemm table */
+  const void *in;           /* LN input rows / attention q */
+  void *out;                /* LN output rows / attention output */
+  const float *g, *b;       /* LN affine */
+  const void *k, *v;        /* attention keys / values: rows (s * nk + j) */
+  int ldi, ldo, ldk, ldv, nk, mask_off, heads, dh;
+} auras_dpt_op;
+int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const auras_dpt_op *ops, int n_ops, int T,
+                            void **plan);
+int auras_dpt_persist_run(void *plan, int S, const float *eps, int eps_pitch, const int *agents, const int *lanes,
+                          const int *steps, float *x_lanes, const float *noise_lanes, int lanes_per_agent,
+                          int horizon, int adim, const auras_sched *sched, void *stream);
+int auras_dpt_persist_trace(void *plan, long long *out, int n);   /* diagnostics (AURAS_DPT_TRACE) */
+void auras_dpt_persist_free(void *plan);
+
 /* Assemble global_cond rows (the ContextStore.publish payload of the DP
  * plugin): for agent a, row = [feat_prev, pos_prev, feat, pos] (n_obs_steps
  * = 2) or [feat, pos] (1); feat_prev/pos_prev are the agent's previous

@@ -43,6 +43,18 @@ class LinearOp(C.Structure):
     _fields_ = [("w", vp), ("bias", vp), ("M", i32), ("K", i32), ("mish_in", i32), ("ldw", i32)]
 
 
+class DptGemm(C.Structure):
+    _fields_ = [("act", vp), ("act_rows", i32), ("K", i32), ("w", vp), ("N", i32), ("bias", vp), ("res", vp),
+                ("ldr", i32), ("out", vp), ("ldo", i32), ("out_f32", vp), ("ldf", i32), ("act_fn", i32),
+                ("ln_src", vp), ("ln_g", vp), ("ln_b", vp)]
+
+
+class DptOp(C.Structure):
+    _fields_ = [("type", i32), ("gemm", i32), ("inp", vp), ("out", vp), ("g", vp), ("b", vp), ("k", vp), ("v", vp),
+                ("ldi", i32), ("ldo", i32), ("ldk", i32), ("ldv", i32), ("nk", i32), ("mask_off", i32),
+                ("heads", i32), ("dh", i32)]
+
+
 class Sched(C.Structure):
     _fields_ = [("timestep", vp), ("sqrt_ab", vp), ("sqrt_1mab", vp), ("c_x0", vp), ("c_xt", vp),
                 ("c_eps", vp), ("sigma", vp), ("n_steps", i32), ("clip_sample", i32), ("ddpm", i32),
@@ -93,6 +105,12 @@ _SIGNATURES = {
     "auras_unet_kernel_for": (C.c_int, [vp, C.c_int]),
     "auras_unet_check": (C.c_int, [vp]),
     "auras_ring_stress": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, vp]),
+    "auras_dpt_persist_build": (C.c_int, [C.POINTER(DptGemm), C.c_int, C.POINTER(DptOp), C.c_int, C.c_int,
+                                          C.POINTER(vp)]),
+    "auras_dpt_persist_run": (C.c_int, [vp, C.c_int, vp, C.c_int, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int,
+                                        C.POINTER(Sched), vp]),
+    "auras_dpt_persist_free": (None, [vp]),
+    "auras_dpt_persist_trace": (C.c_int, [vp, vp, C.c_int]),
     "auras_unet_launches_per_iter": (C.c_int, [vp]),
     "auras_conv": (C.c_int, [C.POINTER(ConvOp), C.c_int, C.c_int, vp, C.c_int, vp, i64, vp]),
     "auras_linear": (C.c_int, [C.POINTER(LinearOp), C.c_int, C.c_int, vp, C.c_int, vp, C.c_int, vp]),

@@ -743,7 +743,10 @@ class DPTDenoiser:
         def z(*shape, dtype=td):
             return torch.zeros(*shape, dtype=dtype, device=dev)
 
-        self.xin = z(s_max, T, 64)
+        # activation rows are allocated for at least 8 samples (128 tokens): the
+        # persistent iteration's TMA maps read 128-row boxes
+        s_alloc = max(s_max, 8)
+        self.xin = z(s_alloc, T, 64)
         self.gcbuf = z(s_max, self.n_obs, self.gpad)
         self.c = z(s_max, self.tc, E)
         self.cobs = z(s_max, self.n_obs, E)
@@ -758,8 +761,9 @@ class DPTDenoiser:
         self.kv2 = z(s_max, self.tc, L * 2 * E)       # cross-attention K|V of every layer
         self.ff = z(s_max, T, 4 * E)
         self.eps_bf = z(s_max, T, cfg.action_dim)
-        self.eps = z(s_max, T, cfg.action_dim, dtype=torch.float32)
-        self.pos_rep = w["dpt.pos"].to(dev, td)[None].repeat(s_max, 1, 1).contiguous()
+        self.eps_prog = z(s_max, T, cfg.action_dim, dtype=torch.float32)
+        self._last_persist = False
+        self.pos_rep = w["dpt.pos"].to(dev, td)[None].repeat(s_alloc, 1, 1).contiguous()
         self.cond_pos = model.f32(w["dpt.cond_pos"])
         tab = scheduler_tables(cfg)["timestep"]
         half = E // 2
@@ -846,8 +850,81 @@ class DPTDenoiser:
             res_ln(model.conv_weight(lw(p + ".ff2")), lb(p + ".ff2"), self.ff, 4 * E, nxt, cur, nxt_ln)
             cur, nxt = nxt, cur
         self._lin(model.conv_weight(lw("dpt.head")), lb("dpt.head"), self.ln, E, self.eps_bf, cfg.action_dim, T,
-                  out_f32=self.eps)
+                  out_f32=self.eps_prog)
         self.scratch = torch.zeros(max(1, self.max_scratch), dtype=torch.float32, device=dev)
+        # the persistent iteration (csrc/dpt_persist.cu): one cluster launch per
+        # iteration for up to 8 samples, the same program as above (AURAS_DPT_PERSIST=0
+        # keeps the launch-per-layer program)
+        self.pplan = None
+        if self.hoist and os.environ.get("AURAS_DPT_PERSIST", "1") != "0" and E == 256 and T * 8 <= 128:
+            self._build_persist(lw, lb, lnp)
+
+    @property
+    def eps(self):
+        """[S][T][action_dim] fp32 eps of the last iteration (either program)."""
+        if self._last_persist:
+            return self.p_eps.view(-1, self.T, self.m.cfg.action_dim)
+        return self.eps_prog
+
+    def _build_persist(self, lw, lb, lnp):
+        torch, model, cfg = self.m.torch, self.m, self.m.cfg
+        E, T, L = self.E, self.T, cfg.dpt_layers
+        dev, td = model.dev, model.tdtype
+        R = 128
+
+        def z(width, dtype=td):
+            return torch.zeros(R, width, dtype=dtype, device=dev)
+
+        self.p_h, self.p_ln, self.p_qkv = z(E), z(E), z(3 * E)
+        self.p_att, self.p_q2, self.p_ff = z(E), z(E), z(4 * E)
+        self.p_eps = z(cfg.action_dim, torch.float32)
+        keep = self.p_keep = []
+        gemms, ops = [], []
+
+        def gemm(act, K, wname, rows=None, res=None, out=None, ldo=0, out_f32=None, act_fn=0, cin_pad=None,
+                 ln=None):
+            """one GEMM phase; ln = LayerNorm name: A = LN(residual stream), computed in the phase"""
+            wm = model.conv_weight(lw(wname, rows), cin_pad=cin_pad)[0]
+            bias = lb(wname, rows)
+            keep.extend([wm, bias])
+            g = _lib.DptGemm(act=act.data_ptr() if act is not None else 0, act_rows=R, K=K, w=wm.data_ptr(),
+                             N=wm.shape[0], bias=bias.data_ptr(), res=_lib.ptr(res),
+                             ldr=E if res is not None else 0, out=_lib.ptr(out), ldo=ldo, out_f32=_lib.ptr(out_f32),
+                             ldf=cfg.action_dim if out_f32 is not None else 0, act_fn=act_fn)
+            if ln is not None:
+                lg, lbb = lnp(ln)
+                keep.extend([lg, lbb])
+                g.ln_src, g.ln_g, g.ln_b = self.p_h.data_ptr(), lg.data_ptr(), lbb.data_ptr()
+            gemms.append(g)
+            ops.append(_lib.DptOp(type=0, gemm=len(gemms) - 1))
+
+        def attn(q, ldq, k, v, ldk, nk, mask_off):
+            ops.append(_lib.DptOp(type=2, inp=q, out=self.p_att.data_ptr(), k=k, v=v, ldi=ldq, ldo=E, ldk=ldk,
+                                  ldv=ldk, nk=nk, mask_off=mask_off, heads=self.H, dh=E // self.H))
+
+        # h = input(x) + pos; every LayerNorm runs inside the GEMM phase that consumes it
+        gemm(self.xin, 64, "dpt.input", res=self.pos_rep, out=self.p_h, ldo=E, cin_pad=64)
+        kv, lkv = self.kv2.data_ptr(), L * 2 * E
+        for l in range(L):
+            p = f"dpt.l{l}"
+            gemm(None, E, p + ".sa_in", out=self.p_qkv, ldo=3 * E, ln=p + ".ln1")
+            q0 = self.p_qkv.data_ptr()
+            attn(q0, 3 * E, q0 + 2 * E, q0 + 2 * 2 * E, 3 * E, T, 0)
+            gemm(self.p_att, E, p + ".sa_out", res=self.p_h, out=self.p_h, ldo=E)
+            gemm(None, E, p + ".ca_in", rows=(0, E), out=self.p_q2, ldo=E, ln=p + ".ln2")
+            attn(self.p_q2.data_ptr(), E, kv + 2 * l * 2 * E, kv + 2 * (l * 2 * E + E), lkv, self.tc, 1)
+            gemm(self.p_att, E, p + ".ca_out", res=self.p_h, out=self.p_h, ldo=E)
+            gemm(None, E, p + ".ff1", out=self.p_ff, ldo=4 * E, act_fn=_lib.ACT_GELU, ln=p + ".ln3")
+            gemm(self.p_ff, 4 * E, p + ".ff2", res=self.p_h, out=self.p_h, ldo=E)
+        gemm(None, E, "dpt.head", out_f32=self.p_eps, ln="dpt.lnf")
+        ops.append(_lib.DptOp(type=3))
+        lib = _lib.load()
+        ga = (_lib.DptGemm * len(gemms))(*gemms)
+        oa = (_lib.DptOp * len(ops))(*ops)
+        plan = _lib.vp()
+        _lib.check(lib.auras_dpt_persist_build(ga, len(gemms), oa, len(ops), T, _lib.C.byref(plan)),
+                   "dpt_persist_build")
+        self.pplan = plan.value
 
     def _lin(self, wconv, bias, inp, in_pitch, out, out_pitch, rows, act=0, res=None, out_f32=None, ln=None):
         wm, cp, _, _, kp = wconv
@@ -879,8 +956,15 @@ class DPTDenoiser:
         if self.hoist:
             _lib.check(lib.auras_dpt_kv_gather(self.kv2.data_ptr(), self.kvt.data_ptr(), self.kvo.data_ptr(), agents,
                                                steps, S, self.tc, self.kv2.shape[-1], st), "dpt_kv_gather")
+        if self.pplan and S * self.T <= 128:
+            _lib.check(lib.auras_dpt_persist_run(self.pplan, S, self.p_eps.data_ptr(), cfg.action_dim, agents, lanes,
+                                                 steps, x_lanes, noise_lanes, lanes_per_agent, cfg.horizon,
+                                                 cfg.action_dim, _lib.C.byref(sched), st), "dpt_persist_run")
+            self._last_persist = True
+            return
         self._run(self.prog if self.hoist else self.cond_prog + self.prog, S, st)
-        _lib.check(lib.auras_dpt_update(self.eps.data_ptr(), cfg.action_dim, agents, lanes, steps, S, x_lanes,
+        self._last_persist = False
+        _lib.check(lib.auras_dpt_update(self.eps_prog.data_ptr(), cfg.action_dim, agents, lanes, steps, S, x_lanes,
                                         noise_lanes, lanes_per_agent, cfg.horizon, cfg.action_dim, _lib.C.byref(sched),
                                         st), "dpt_update")
 
