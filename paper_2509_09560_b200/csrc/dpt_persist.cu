@@ -123,34 +123,28 @@ __device__ __forceinline__ void dp_ln_row(const __nv_bfloat16 *xr, __nv_bfloat16
 }
 
 // Attention queries [q0, q1) of the flattened (sample, head, query) space by
-// one warp (dh = 64, nk <= 32 keys; key j visible to query n iff
-// j <= n + mask_off).  Every load is issued up front (a phase runs on 8 SMs, so
+// one warp (dh = 64, nk <= 16 keys; key j visible to query n iff
+// j <= n + mask_off), four queries at a time with their reductions
+// interleaved.  Every load is issued up front (a phase runs on 16 SMs, so
 // latency must not serialise): lane j holds key row j (scores), lane l holds
 // value columns 2l, 2l+1 of every key (output); K / V are reloaded only when
 // the (sample, head) unit changes.
+constexpr int DP_QB = 4;
+
 __device__ __forceinline__ void dp_attn_block(const DpOpDev &o, int q0, int q1, int T, int lane) {
   const int nk = o.nk, dh = 64;
   const float scale = rsqrtf((float)dh);
   int unit = -1;
   uint4 kr[8];
   float2 vc[DP_MAXK];
-  // query row qi (64 bf16): lane takes columns 2 lane, 2 lane + 1 (all lanes see it via shuffles);
-  // the rows of a block of 8 queries are loaded together (one L2 latency per block)
-  auto qload = [&](int qi) {
-    const int n = qi % T, u = qi / T, h = u % o.heads, s = u / o.heads;
-    return *reinterpret_cast<const uint32_t *>(o.in + ((int64_t)s * T + n) * o.ldi + h * dh + 2 * lane);
-  };
-  uint32_t qblk[8];
-  for (int qi = q0; qi < q1; ++qi) {
-    const int n = qi % T, u = qi / T, h = u % o.heads, s = u / o.heads;
-    if (((qi - q0) & 7) == 0) {
+  for (int qi = q0; qi < q1;) {
+    const int n0 = qi % T, u = qi / T, h = u % o.heads, s = u / o.heads;
+    const int nq = min(min(DP_QB, q1 - qi), T - n0);    // queries of this unit in the batch
+    uint32_t qw[DP_QB];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) qblk[i] = qi + i < q1 ? qload(qi + i) : 0u;
-    }
-    uint32_t qw = qblk[0];
-#pragma unroll
-    for (int i = 1; i < 8; ++i)
-      if (((qi - q0) & 7) == i) qw = qblk[i];
+    for (int b = 0; b < DP_QB; ++b)
+      qw[b] = b < nq ? *reinterpret_cast<const uint32_t *>(o.in + ((int64_t)s * T + n0 + b) * o.ldi + h * dh + 2 * lane)
+                     : 0u;
     if (u != unit) {
       unit = u;
       if (lane < nk) {
@@ -167,40 +161,65 @@ __device__ __forceinline__ void dp_attn_block(const DpOpDev &o, int q0, int q1, 
                              o.v + ((int64_t)s * nk + j) * o.ldv + h * dh + 2 * lane))
                        : make_float2(0.f, 0.f);
     }
-    // score of key `lane`: q . k over 64 columns, 4 independent chains
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    // scores of key `lane` for the batch's queries
+    float sc[DP_QB];
+#pragma unroll
+    for (int b = 0; b < DP_QB; ++b) sc[b] = 0.f;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t kw[4] = {kr[i].x, kr[i].y, kr[i].z, kr[i].w};
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const uint32_t qq = __shfl_sync(0xffffffffu, qw, 4 * i + c);    // columns 8 i + 2 c, +1
-        const float2 qf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&qq));
         const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&kw[c]));
-        acc[c] = fmaf(qf.x, kf.x, acc[c]);
-        acc[c] = fmaf(qf.y, kf.y, acc[c]);
+#pragma unroll
+        for (int b = 0; b < DP_QB; ++b) {
+          const uint32_t qq = __shfl_sync(0xffffffffu, qw[b], 4 * i + c);   // columns 8 i + 2 c, +1
+          const float2 qf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&qq));
+          sc[b] = fmaf(qf.x, kf.x, sc[b]);
+          sc[b] = fmaf(qf.y, kf.y, sc[b]);
+        }
       }
     }
-    const float a = ((acc[0] + acc[1]) + (acc[2] + acc[3])) * scale;
-    const int vis = min(nk, n + o.mask_off + 1);
-    const bool on = lane < vis;
-    float mx = on ? a : -INFINITY;
+    float mx[DP_QB], pe[DP_QB], sm[DP_QB];
 #pragma unroll
-    for (int off = 16; off; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    const float pexp = on ? __expf(a - mx) : 0.f;
-    const float inv = 1.f / dp_wsum(pexp);
-    float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
-#pragma unroll
-    for (int j = 0; j < DP_MAXK; j += 2) {
-      if (j >= nk) break;
-      const float p0 = __shfl_sync(0xffffffffu, pexp, j), p1 = __shfl_sync(0xffffffffu, pexp, j + 1);
-      o0 = fmaf(p0, vc[j].x, o0);
-      o1 = fmaf(p0, vc[j].y, o1);
-      o2 = fmaf(p1, vc[j + 1].x, o2);
-      o3 = fmaf(p1, vc[j + 1].y, o3);
+    for (int b = 0; b < DP_QB; ++b) {
+      sc[b] *= scale;
+      mx[b] = lane < min(nk, n0 + b + o.mask_off + 1) ? sc[b] : -INFINITY;
     }
-    *reinterpret_cast<__nv_bfloat162 *>(o.out + ((int64_t)s * T + n) * o.ldo + h * dh + 2 * lane) =
-        __floats2bfloat162_rn((o0 + o2) * inv, (o1 + o3) * inv);
+#pragma unroll
+    for (int off = 16; off; off >>= 1)
+#pragma unroll
+      for (int b = 0; b < DP_QB; ++b) mx[b] = fmaxf(mx[b], __shfl_xor_sync(0xffffffffu, mx[b], off));
+#pragma unroll
+    for (int b = 0; b < DP_QB; ++b) {
+      pe[b] = lane < min(nk, n0 + b + o.mask_off + 1) ? __expf(sc[b] - mx[b]) : 0.f;
+      sm[b] = pe[b];
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1)
+#pragma unroll
+      for (int b = 0; b < DP_QB; ++b) sm[b] += __shfl_xor_sync(0xffffffffu, sm[b], off);
+    float ox[DP_QB], oy[DP_QB];
+#pragma unroll
+    for (int b = 0; b < DP_QB; ++b) { ox[b] = 0.f; oy[b] = 0.f; }
+#pragma unroll
+    for (int j = 0; j < DP_MAXK; ++j) {
+      if (j >= nk) break;
+#pragma unroll
+      for (int b = 0; b < DP_QB; ++b) {
+        const float pj = __shfl_sync(0xffffffffu, pe[b], j);
+        ox[b] = fmaf(pj, vc[j].x, ox[b]);
+        oy[b] = fmaf(pj, vc[j].y, oy[b]);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < DP_QB; ++b) {
+      if (b >= nq) break;
+      const float inv = 1.f / sm[b];
+      *reinterpret_cast<__nv_bfloat162 *>(o.out + ((int64_t)s * T + n0 + b) * o.ldo + h * dh + 2 * lane) =
+          __floats2bfloat162_rn(ox[b] * inv, oy[b] * inv);
+    }
+    qi += nq;
   }
 }
 
