@@ -53,7 +53,7 @@ constexpr size_t DP_SMEM = 1024 + (size_t)DP_STAGES * DP_STAGE + 4 * DP_A_BYTES 
 constexpr int DP_MAXK = 16;                   // keys per query (horizon <= 16; 3 cond tokens)
 constexpr int DP_E = 256;                     // embedding width (LayerNorm row)
 
-enum { DP_GEMM = 0, DP_LN = 1, DP_ATTN = 2, DP_UPDATE = 3 };
+enum { DP_GEMM = 0, DP_LN = 1, DP_ATTN = 2, DP_UPDATE = 3, DP_NOP = 4 };
 
 struct alignas(64) DpGemmDev {
   CUtensorMap tmA;           // activation [128][K] bf16, box {64, 128} (unless ln_g: A = LN(ln_src))
@@ -459,6 +459,8 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
       const int items = P.S * o.heads * P.T, per = (items + DP_CL * 8 - 1) / (DP_CL * 8);
       const int gw = rank * 8 + warp;
       dp_attn_block(o, min(items, gw * per), min(items, (gw + 1) * per), P.T, lane);
+    } else if (o.type == DP_NOP) {
+      // timing probe: a phase with no work (the cost of the phase boundary alone)
     } else {
       // ---- DDPM / DDIM update of sample s (dpt.cu dpt_update_kernel arithmetic)
       const auras_sched &sch = P.sched;
@@ -572,7 +574,7 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
     d.ldi = s.ldi; d.ldo = s.ldo; d.ldk = s.ldk; d.ldv = s.ldv;
     d.nk = s.nk; d.mask_off = s.mask_off; d.heads = s.heads; d.dh = s.dh;
     if ((s.type == DP_GEMM && (s.gemm < 0 || s.gemm >= n_gemms)) || (s.type == DP_ATTN && (s.nk > DP_MAXK || s.dh != 64)) ||
-        s.type < 0 || s.type > DP_UPDATE) {
+        s.type < 0 || s.type > DP_NOP) {
       set_error("dpt_persist_build: op %d", i);
       return AURAS_E_ARG;
     }

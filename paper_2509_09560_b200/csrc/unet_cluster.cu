@@ -680,7 +680,7 @@ __global__ void __launch_bounds__(CK_THREADS, 1) unet_cluster(const __grid_const
             if (et == 0) ck_spin(P, &P.flags[fi ^ 1], CL);
             esync();
           }
-          if (in_pair) {
+          if (in_pair && !(P.hack & 4096)) {           // (4096: timing probe -- skip the merge arithmetic)
             const int cha = chan(8 * pa);
             const int gf = (cha >> lcg) << lcg;
             const int tlo = mt0 * 128, thi = min((mt0 + nmt) * 128, M);

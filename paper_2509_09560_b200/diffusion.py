@@ -918,6 +918,7 @@ class DPTDenoiser:
             gemm(self.p_ff, 4 * E, p + ".ff2", res=self.p_h, out=self.p_h, ldo=E)
         gemm(None, E, "dpt.head", out_f32=self.p_eps, ln="dpt.lnf")
         ops.append(_lib.DptOp(type=3))
+        ops.extend(_lib.DptOp(type=4) for _ in range(int(os.environ.get("AURAS_DPT_NOPS", "0"))))   # timing probe
         lib = _lib.load()
         ga = (_lib.DptGemm * len(gemms))(*gemms)
         oa = (_lib.DptOp * len(ops))(*ops)
