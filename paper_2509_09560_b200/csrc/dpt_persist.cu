@@ -43,13 +43,28 @@ namespace auras {
 #define DP_CLUSTER 16
 #endif
 constexpr int DP_CL = DP_CLUSTER;             // CTAs in the cluster (16: non-portable cluster size)
-constexpr int DP_THREADS = 256;               // warps 0 TMA, 1 MMA, 4-7 epilogue; all 8 in SIMT phases
-constexpr int DP_STAGES = 4;
+constexpr int DP_CT = 256;                    // compute warps 0-7: LN / epilogue / SIMT phases; warp 1 issues the MMAs
+constexpr int DP_THREADS = DP_CT + 32;        // + warp 8: the TMA producer (never writes generic memory, so it
+                                              //   never executes a proxy fence behind its own bulk loads)
+constexpr int DP_STAGES = 8;                  // ring depth: the K = 1024 GEMM streams 16 k-blocks
 constexpr int DP_A_BYTES = 128 * 64 * 2;      // one 128-token x 64-channel activation k-block
-constexpr int DP_B_MAX = 128 * 64 * 2;        // weight slice k-block, <= 128 rows
-constexpr int DP_STAGE = DP_A_BYTES + DP_B_MAX;
+constexpr int DP_B_BYTES = 64 * 64 * 2;       // weight slice k-block, <= 64 rows (N <= 64 x 16)
+constexpr int DP_R_BYTES = 128 * 16 * 2;      // residual slice (TMA'd when the slice is 16 columns)
+// shared memory: A ring [8][16 KB] | B ring [8][8 KB] | residual slice | barriers | metadata.  The
+// LayerNorm'd A tile (4 k-blocks) aliases A-ring stages 0-3: a LayerNorm GEMM loads no A blocks, and
+// the previous GEMM's MMAs completed before the phase barrier.
+constexpr size_t DP_B_OFF = (size_t)DP_STAGES * DP_A_BYTES;
+constexpr size_t DP_R_OFF = DP_B_OFF + (size_t)DP_STAGES * DP_B_BYTES;
+constexpr size_t DP_BAR_OFF = DP_R_OFF + DP_R_BYTES;
 constexpr int DP_TMEM_COLS = 128;
-constexpr size_t DP_SMEM = 1024 + (size_t)DP_STAGES * DP_STAGE + 4 * DP_A_BYTES + 256;   // ring + LayerNorm'd A
+// Program metadata and this CTA's bias slices are staged in shared memory at launch: every
+// phase barrier (barrier.cluster acquire) invalidates L1, so a per-phase read of the op
+// table from global memory would be an L2 round trip (~1 us) on the critical path of
+// every one of the ~67 phases.
+constexpr int DP_MAX_OPS = 96, DP_MAX_GEMMS = 56, DP_BIAS_SLAB = 3072;
+constexpr size_t DP_META_OFF = DP_BAR_OFF + 256;
+constexpr size_t DP_META_BYTES = (size_t)DP_MAX_OPS * 104 + DP_MAX_GEMMS * 96 + DP_BIAS_SLAB * 4;
+constexpr size_t DP_SMEM = 1024 + DP_META_OFF + DP_META_BYTES;   // ring + LayerNorm'd A + barriers + metadata
 constexpr int DP_MAXK = 16;                   // keys per query (horizon <= 16; 3 cond tokens)
 constexpr int DP_E = 256;                     // embedding width (LayerNorm row)
 
@@ -58,6 +73,7 @@ enum { DP_GEMM = 0, DP_LN = 1, DP_ATTN = 2, DP_UPDATE = 3, DP_NOP = 4 };
 struct alignas(64) DpGemmDev {
   CUtensorMap tmA;           // activation [128][K] bf16, box {64, 128} (unless ln_g: A = LN(ln_src))
   CUtensorMap tmB;           // weight [N][K] bf16, box {64, ncta}
+  CUtensorMap tmR;           // residual [128][N] bf16 (pitch ldr), box {ncta, 128}, unswizzled (when rtma)
   const float *bias;
   const __nv_bfloat16 *res;  // residual (may alias out: each element is read, then written, by one thread)
   __nv_bfloat16 *out;
@@ -65,7 +81,20 @@ struct alignas(64) DpGemmDev {
   int K, N, ncta, ldo, ldr, ldf, act, ctas;
   const __nv_bfloat16 *ln_src;   // optional: A = LayerNorm(ln_src [128][256]) (K = 256), computed in the phase
   const float *ln_g, *ln_b;
+  int boff;                  // this GEMM's bias slice in the shared-memory slab
+  int rtma;                  // the residual slice is TMA'd into shared memory (16-column slices)
 };
+
+// The GEMM fields the phases read (no tensor maps: those stay in global memory for the TMA unit).
+struct DpGemmMeta {
+  const __nv_bfloat16 *res;
+  __nv_bfloat16 *out;
+  float *out_f32;
+  const __nv_bfloat16 *ln_src;
+  const float *ln_g, *ln_b;
+  int K, N, ncta, ldo, ldr, ldf, act, ctas, boff, rtma;
+};
+static_assert(sizeof(DpGemmMeta) <= 96, "DpGemmMeta");
 
 struct DpOpDev {
   int type, gemm;
@@ -74,13 +103,20 @@ struct DpOpDev {
   const float *g, *b;        // LN affine
   const __nv_bfloat16 *k, *v;
   int ldi, ldo, ldk, ldv, nk, mask_off, heads, dh;
+  // GEMM ops: parities of this op's lnbar (bit 0) / resbar (bit 1) / done (bit 2) phase and its
+  // first ring job, [0] for CTAs 1.., [1] for CTA 0 (which also runs the single-CTA GEMMs);
+  // host-computed so that no counter lives across phases (168 registers: it would be spilled)
+  int par[2], job[2];
 };
+static_assert(sizeof(DpOpDev) == 104, "DpOpDev");
 
 struct DpParams {
   long long *trace;          // optional: globaltimer after every phase barrier (CTA 0, thread 0)
   const DpOpDev *ops;
   const DpGemmDev *gemms;
-  int n_ops, S, T;
+  int n_ops, n_gemms, S, T;
+  int dbg;                   // AURAS_DPT_DBG timing variants (0 in production)
+  int pf;                    // weight prefetch across phase barriers (0: only in the GEMM's own phase)
   // update
   const float *eps;
   int eps_pitch;
@@ -131,12 +167,13 @@ __device__ __forceinline__ void dp_ln_row(const __nv_bfloat16 *xr, __nv_bfloat16
 // the (sample, head) unit changes.
 constexpr int DP_QB = 4;
 
-__device__ __forceinline__ void dp_attn_block(const DpOpDev &o, int q0, int q1, int T, int lane) {
+// (noinline: its ~130 live registers must not push the persistent loop's state into local memory)
+__device__ __noinline__ void dp_attn_block(const DpOpDev &o, int q0, int q1, int T, int lane) {
   const int nk = o.nk, dh = 64;
   const float scale = rsqrtf((float)dh);
   int unit = -1;
   uint4 kr[8];
-  float2 vc[DP_MAXK];
+  __nv_bfloat162 vc[DP_MAXK];    // value columns 2 lane, 2 lane + 1 of every key (bf16 pairs: half the registers)
   for (int qi = q0; qi < q1;) {
     const int n0 = qi % T, u = qi / T, h = u % o.heads, s = u / o.heads;
     const int nq = min(min(DP_QB, q1 - qi), T - n0);    // queries of this unit in the batch
@@ -157,9 +194,8 @@ __device__ __forceinline__ void dp_attn_block(const DpOpDev &o, int q0, int q1, 
       }
 #pragma unroll
       for (int j = 0; j < DP_MAXK; ++j)
-        vc[j] = j < nk ? __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(
-                             o.v + ((int64_t)s * nk + j) * o.ldv + h * dh + 2 * lane))
-                       : make_float2(0.f, 0.f);
+        vc[j] = j < nk ? *reinterpret_cast<const __nv_bfloat162 *>(o.v + ((int64_t)s * nk + j) * o.ldv + h * dh + 2 * lane)
+                       : __floats2bfloat162_rn(0.f, 0.f);
     }
     // scores of key `lane` for the batch's queries
     float sc[DP_QB];
@@ -205,17 +241,18 @@ __device__ __forceinline__ void dp_attn_block(const DpOpDev &o, int q0, int q1, 
 #pragma unroll
     for (int j = 0; j < DP_MAXK; ++j) {
       if (j >= nk) break;
+      const float2 vf = __bfloat1622float2(vc[j]);
 #pragma unroll
       for (int b = 0; b < DP_QB; ++b) {
         const float pj = __shfl_sync(0xffffffffu, pe[b], j);
-        ox[b] = fmaf(pj, vc[j].x, ox[b]);
-        oy[b] = fmaf(pj, vc[j].y, oy[b]);
+        ox[b] = fmaf(pj, vf.x, ox[b]);
+        oy[b] = fmaf(pj, vf.y, oy[b]);
       }
     }
 #pragma unroll
     for (int b = 0; b < DP_QB; ++b) {
       if (b >= nq) break;
-      const float inv = 1.f / sm[b];
+      const float inv = __fdividef(1.f, sm[b]);     // sm >= 1 (the row max contributes exp(0))
       *reinterpret_cast<__nv_bfloat162 *>(o.out + ((int64_t)s * T + n0 + b) * o.ldo + h * dh + 2 * lane) =
           __floats2bfloat162_rn(ox[b] * inv, oy[b] * inv);
     }
@@ -223,16 +260,223 @@ __device__ __forceinline__ void dp_attn_block(const DpOpDev &o, int q0, int q1, 
   }
 }
 
+// Every CTA of the cluster needs the same activation block: each loads 128 / DP_CL of its rows and
+// multicasts them to all (16 SMs reading the same L2 lines at once serialise on those lines: a
+// per-CTA 16 KB block took ~850 cycles, 19 B/cycle).
+constexpr int DP_MROWS = 128 / DP_CL;
+constexpr uint16_t DP_MASK = (uint16_t)((1u << DP_CL) - 1);
+static_assert(128 % DP_CL == 0, "multicast slices");
+
+__device__ __forceinline__ void dp_tma_mc(void *dst, const CUtensorMap *tm, uint64_t *bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(DP_MASK)
+      : "memory");
+}
+
+// MMA completion arrives on the same barrier in every CTA (a ring stage is free only when all the
+// CTAs its multicast fills have consumed it).
+__device__ __forceinline__ void dp_commit_all(uint64_t *bar) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 rx;\n"
+      ".reg .pred px;\n"
+      "elect.sync rx|px, 0xffffffff;\n"
+      "@px tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+      "}\n" ::"r"(smem_u32(bar)), "h"(DP_MASK)
+      : "memory");
+}
+
+__device__ __forceinline__ bool dp_stage_free(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Weight-slice cursor of the TMA producer.  Weights are constant for the whole
+// launch, so the k-blocks of upcoming GEMMs are issued as soon as a ring stage
+// frees up -- at the end of the previous GEMM phase, i.e. during the phase
+// barrier and any SIMT phases in between -- and their L2 latency leaves the
+// critical path.  Ring job j (in program order over the GEMMs this CTA takes
+// part in) uses stage j % DP_STAGES; its full barrier expects two arrivals:
+// the weight block (issued here, early) and the activation block (issued in
+// the GEMM's own phase, or a plain arrive when A is the LayerNorm tile).
+struct DpBCursor {
+  int op = 0, kb = 0, job = 0;
+};
+
+// Issue the next weight k-block; false when the program has none left or
+// (non-blocking) its stage is still held by the MMAs.
+__device__ __forceinline__ bool dp_issue_b(const DpParams &P, const DpOpDev *ops, const DpGemmMeta *gm, DpBCursor &c,
+                                           int rank, uint8_t *smem, uint64_t *full, uint64_t *empty, bool block) {
+  while (c.op < P.n_ops) {
+    const DpOpDev &o = ops[c.op];
+    if (o.type != DP_GEMM || c.kb == gm[o.gemm].K / 64) {
+      ++c.op;
+      c.kb = 0;
+      continue;
+    }
+    const DpGemmMeta &g = gm[o.gemm];
+    const int st = c.job % DP_STAGES;
+    const uint32_t par = ((c.job / DP_STAGES) & 1) ^ 1;
+    if (block) {
+      if (P.dbg & 2) { while (!dp_stage_free(&empty[st], par)) {} }
+      else mbar_wait(&empty[st], par);
+    }
+    else if (!dp_stage_free(&empty[st], par)) return false;
+    mbar_expect_tx(&full[st], g.ncta * 128);
+    tma_load_2d(smem + DP_B_OFF + st * DP_B_BYTES, &P.gemms[o.gemm].tmB, &full[st], c.kb * 64, rank * g.ncta);
+    ++c.kb;
+    ++c.job;
+    return true;
+  }
+  return false;
+}
+
+// GELU with erf from Abramowitz & Stegun 7.1.26 (|error| <= 1.5e-7, far below the bf16 rounding of
+// the stored activation): branch-free, so the 16 columns of a chunk evaluate with full ILP (erff
+// branches per element and serialises).
+__device__ __forceinline__ float dp_gelu(float x) {
+  const float z = fabsf(x) * 0.70710678118654752f;
+  const float t = __fdividef(1.f, fmaf(0.3275911f, z, 1.f));
+  float p = fmaf(1.061405429f, t, -1.453152027f);
+  p = fmaf(p, t, 1.421413741f);
+  p = fmaf(p, t, -0.284496736f);
+  p = fmaf(p, t, 0.254829592f);
+  const float e = 1.f - p * t * __expf(-z * z);          // erf(|x| / sqrt 2)
+  return 0.5f * x * (1.f + copysignf(e, x));
+}
+
+// Sub-phase stamps (SM clock, CTA 0) after the per-phase globaltimer stamps: diagnostics only.
+#define DP_STAMP(k, cond)                                                                              \
+  do {                                                                                                 \
+    if (P.trace && rank == 0 && (cond)) P.trace[P.n_ops + 1 + 8 * oi + (k)] = clock64();              \
+  } while (0)
+#define DP_KSTAMP(k, cond)                                                                             \
+  do {                                                                                                 \
+    if (P.trace && rank == 0 && (cond) && (k) < 64) P.trace[9 * P.n_ops + 1 + 64 * oi + (k)] = clock64(); \
+  } while (0)
+
+// LayerNorm of the 128 x 256 tile in sAln, in place (UMMA layout: K-major, 128B swizzle, 16-byte
+// chunk j of row r at chunk j ^ (r & 7)); warp w normalises rows w, w + 8, ..., 8 at a time with
+// their reductions interleaved; lane l owns columns 8 l .. 8 l + 7 (k-block l / 8, chunk l % 8).
+// Rows >= S T hold stale finite activations: normalised too, never stored (a row of D depends
+// only on its own row of A).  noinline for the same reason as dp_attn_block.
+__device__ __noinline__ void dp_ln_tile(uint8_t *sAln, const float *ln_g, const float *ln_b, int warp, int lane) {
+  const float4 g0 = *reinterpret_cast<const float4 *>(ln_g + 8 * lane);
+  const float4 g1 = *reinterpret_cast<const float4 *>(ln_g + 8 * lane + 4);
+  const float4 b0 = *reinterpret_cast<const float4 *>(ln_b + 8 * lane);
+  const float4 b1 = *reinterpret_cast<const float4 *>(ln_b + 8 * lane + 4);
+  const float ga[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+  const float ba[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+  const int kbl = lane >> 3, ch = lane & 7;
+  for (int hb = 0; hb < 2; ++hb) {
+    uint4 *px[8];
+    uint4 xin4[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = warp + 8 * (8 * hb + i);
+      px[i] = reinterpret_cast<uint4 *>(sAln + kbl * DP_A_BYTES + r * 128 + ((ch ^ (r & 7)) << 4));
+      xin4[i] = *px[i];
+    }
+    float mu[8], rs[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t xw[4] = {xin4[i].x, xin4[i].y, xin4[i].z, xin4[i].w};
+      float sm = 0.f;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&xw[k]));
+        sm += f.x + f.y;
+      }
+      mu[i] = sm;
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mu[i] += __shfl_xor_sync(0xffffffffu, mu[i], off);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      mu[i] *= 1.f / DP_E;
+      const uint32_t xw[4] = {xin4[i].x, xin4[i].y, xin4[i].z, xin4[i].w};
+      float q = 0.f;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&xw[k]));
+        q += (f.x - mu[i]) * (f.x - mu[i]) + (f.y - mu[i]) * (f.y - mu[i]);
+      }
+      rs[i] = q;
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rs[i] += __shfl_xor_sync(0xffffffffu, rs[i], off);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      // (rows >= S T hold stale finite activations: normalised too, never stored --
+      //  a row of D depends only on its own row of A)
+      const float rstd = rsqrtf(rs[i] * (1.f / DP_E) + 1e-5f);
+      const uint32_t xw[4] = {xin4[i].x, xin4[i].y, xin4[i].z, xin4[i].w};
+      uint32_t yw[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&xw[k]));
+        const __nv_bfloat162 h2 = __floats2bfloat162_rn((f.x - mu[i]) * rstd * ga[2 * k] + ba[2 * k],
+                                                        (f.y - mu[i]) * rstd * ga[2 * k + 1] + ba[2 * k + 1]);
+        yw[k] = *reinterpret_cast<const uint32_t *>(&h2);
+      }
+      *px[i] = make_uint4(yw[0], yw[1], yw[2], yw[3]);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_constant__ DpParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + DP_STAGES * DP_STAGE + 4 * DP_A_BYTES);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + DP_BAR_OFF);
   uint64_t *empty = full + DP_STAGES;
   uint64_t *done = empty + DP_STAGES;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+  uint64_t *lnbar = done + 1;     // the LayerNorm source tile landed in sAln
+  uint64_t *resbar = lnbar + 1;   // the residual slice landed in sAln
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(resbar + 1);
+  DpOpDev *sops = reinterpret_cast<DpOpDev *>(smem + DP_META_OFF);
+  DpGemmMeta *sgm = reinterpret_cast<DpGemmMeta *>(smem + DP_META_OFF + DP_MAX_OPS * 104);
+  float *sbias = reinterpret_cast<float *>(smem + DP_META_OFF + DP_MAX_OPS * 104 + DP_MAX_GEMMS * 96);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = (int)cluster_ctarank();
-  const int rows = P.S * P.T;
+#define rows (P.S * P.T)      // (from the constant bank: not a register across the phase loop)
+  {
+    // ---- stage the program and this CTA's bias slices
+    const uint64_t *src = reinterpret_cast<const uint64_t *>(P.ops);
+    uint64_t *dst = reinterpret_cast<uint64_t *>(sops);
+    for (int i = threadIdx.x; i < P.n_ops * 13; i += DP_THREADS) dst[i] = src[i];
+    for (int i = threadIdx.x; i < P.n_gemms; i += DP_THREADS) {
+      const DpGemmDev &g = P.gemms[i];
+      DpGemmMeta m;
+      m.res = g.res; m.out = g.out; m.out_f32 = g.out_f32;
+      m.ln_src = g.ln_src; m.ln_g = g.ln_g; m.ln_b = g.ln_b;
+      m.K = g.K; m.N = g.N; m.ncta = g.ncta; m.ldo = g.ldo; m.ldr = g.ldr; m.ldf = g.ldf;
+      m.act = g.act; m.ctas = g.ctas; m.boff = g.boff; m.rtma = g.rtma;
+      sgm[i] = m;
+    }
+    for (int i = warp; i < P.n_gemms; i += DP_THREADS / 32) {
+      const DpGemmDev &g = P.gemms[i];
+      if (rank >= g.ctas) continue;
+      for (int c = lane; c < g.ncta; c += 32) {
+        const int n = rank * g.ncta + c;
+        sbias[g.boff + c] = n < g.N ? g.bias[n] : 0.f;
+      }
+    }
+  }
   if (P.trace && rank == 0 && threadIdx.x == 0) {
     long long tn;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
@@ -241,10 +485,12 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < DP_STAGES; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&full[i], 2);      // weight block + activation block (see DpBCursor)
+      mbar_init(&empty[i], DP_CL);   // one multicast commit from every CTA
     }
     mbar_init(done, 1);
+    mbar_init(lnbar, 1);
+    mbar_init(resbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -257,159 +503,162 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  int ip = 0, ic = 0, ng = 0;     // producer / consumer ring positions, GEMMs done by this CTA
+  if (warp == DP_CT / 32) {
+    // ---- TMA producer warp (lane 0).  Per phase: the activation k-blocks of this phase's
+    //      GEMM (they depend on the previous phase, so only after its barrier), then -- having
+    //      arrived on the phase barrier already -- the weight blocks of the next GEMMs into the
+    //      stages the ring frees up (DpBCursor), then the barrier wait.
+    DpBCursor bc;
+    int ip = 0;
+    for (int oi = 0; oi < P.n_ops; ++oi) {
+      const DpOpDev &o = sops[oi];
+      if (lane == 0 && o.type == DP_GEMM) {     // (every CTA streams every GEMM: the multicast ring runs in lockstep)
+        const DpGemmMeta &g = sgm[o.gemm];
+        const int nkb = g.K / 64;
+        const bool lnA = g.ln_g != nullptr;
+        if (lnA) {
+          // the residual-stream rows to normalise, straight into the A tile (normalised in place)
+          mbar_expect_tx(lnbar, 4 * DP_A_BYTES);
+#pragma unroll
+          for (int kb = 0; kb < 4; ++kb)
+            dp_tma_mc(smem + kb * DP_A_BYTES + rank * DP_MROWS * 128, &P.gemms[o.gemm].tmA, lnbar, kb * 64,
+                      rank * DP_MROWS);
+        }
+        for (int kb = 0; kb < nkb; ++kb, ++ip) {
+          while (bc.job <= ip) dp_issue_b(P, sops, sgm, bc, rank, smem, full, empty, true);
+          DP_KSTAMP(kb, kb < 16);
+          const int st = ip % DP_STAGES;
+          if (lnA) {
+            mbar_arrive(&full[st]);                   // A comes from the LayerNorm warps
+          } else {
+            mbar_expect_tx(&full[st], DP_A_BYTES);     // (all DP_CL slices, from every CTA)
+            dp_tma_mc(smem + st * DP_A_BYTES + rank * DP_MROWS * 128, &P.gemms[o.gemm].tmA, &full[st], kb * 64,
+                      rank * DP_MROWS);
+          }
+          DP_KSTAMP(16 + kb, kb < 16);
+        }
+        if (g.rtma && rank < g.ctas) {
+          mbar_expect_tx(resbar, 128 * g.ncta * 2);
+          tma_load_2d(smem + DP_R_OFF, &P.gemms[o.gemm].tmR, resbar, rank * g.ncta, 0);
+        }
+        DP_STAMP(1, true);
+      }
+      __syncwarp();
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+      if (lane == 0 && P.pf) {
+        // weight blocks ahead: jobs < ip + DP_STAGES only wait for MMAs of this phase or
+        // earlier ones, which complete without the producer
+        while (bc.job < ip + DP_STAGES && dp_issue_b(P, sops, sgm, bc, rank, smem, full, empty, true)) {}
+      }
+      __syncwarp();
+      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
+  } else {
   for (int oi = 0; oi < P.n_ops; ++oi) {
-    const DpOpDev &o = P.ops[oi];
+    const DpOpDev &o = sops[oi];
+    DP_STAMP(0, threadIdx.x == 0);
     if (o.type == DP_GEMM) {
-      const DpGemmDev &g = P.gemms[o.gemm];
-      if (rank < g.ctas) {
+      const DpGemmMeta &g = sgm[o.gemm];
+      {
         const int nkb = g.K / 64, ncta = g.ncta;
         const bool lnA = g.ln_g != nullptr;                // A = LayerNorm(src) computed here, not loaded
-        uint8_t *sAln = smem + DP_STAGES * DP_STAGE;       // 128 x 256 bf16, four 128B-swizzled k-blocks
-        if (warp == 0 && lane == 0) {
-          // ---- TMA producer: weight slice k-block (+ activation k-block) per stage
-          if (!lnA) asm volatile("prefetch.tensormap [%0];" ::"l"(&g.tmA) : "memory");
-          asm volatile("prefetch.tensormap [%0];" ::"l"(&g.tmB) : "memory");
-          for (int kb = 0; kb < nkb; ++kb, ++ip) {
-            const int st = ip % DP_STAGES;
-            mbar_wait(&empty[st], ((ip / DP_STAGES) & 1) ^ 1);
-            uint8_t *sa = smem + st * DP_STAGE;
-            mbar_expect_tx(&full[st], (lnA ? 0 : DP_A_BYTES) + ncta * 128);
-            if (!lnA) tma_load_2d(sa, &g.tmA, &full[st], kb * 64, 0);
-            tma_load_2d(sa + DP_A_BYTES, &g.tmB, &full[st], kb * 64, rank * ncta);
-          }
-        }
-        __syncwarp();
+        uint8_t *sAln = smem;                              // 128 x 256 bf16, four 128B-swizzled k-blocks
         if (lnA) {
-          // ---- the A operand: LayerNorm of every token row of the residual stream, written
-          //      straight into the UMMA layout (K-major, 128B swizzle: 16-byte chunk j of row r
-          //      at chunk j ^ (r & 7)); lane l owns columns 8 l .. 8 l + 7
-          // this warp's 16 rows in two batches of 8: a batch's loads are issued together and its
-          // warp reductions interleaved (independent chains)
-          const float4 g0 = *reinterpret_cast<const float4 *>(g.ln_g + 8 * lane);
-          const float4 g1 = *reinterpret_cast<const float4 *>(g.ln_g + 8 * lane + 4);
-          const float4 b0 = *reinterpret_cast<const float4 *>(g.ln_b + 8 * lane);
-          const float4 b1 = *reinterpret_cast<const float4 *>(g.ln_b + 8 * lane + 4);
-          const float ga[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-          const float ba[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-          for (int hb = 0; hb < 2; ++hb) {
-          uint4 xin4[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int r = warp + 8 * (8 * hb + i);
-            xin4[i] = r < rows ? *reinterpret_cast<const uint4 *>(g.ln_src + (int64_t)r * DP_E + 8 * lane)
-                               : make_uint4(0, 0, 0, 0);
-          }
-          // statistics of the 16 rows with their warp reductions interleaved (independent chains)
-          float mu[8], rs[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const uint32_t xw[4] = {xin4[i].x, xin4[i].y, xin4[i].z, xin4[i].w};
-            float sm = 0.f;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&xw[k]));
-              sm += f.x + f.y;
-            }
-            mu[i] = sm;
-          }
-#pragma unroll
-          for (int off = 16; off; off >>= 1)
-#pragma unroll
-            for (int i = 0; i < 8; ++i) mu[i] += __shfl_xor_sync(0xffffffffu, mu[i], off);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            mu[i] *= 1.f / DP_E;
-            const uint32_t xw[4] = {xin4[i].x, xin4[i].y, xin4[i].z, xin4[i].w};
-            float q = 0.f;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&xw[k]));
-              q += (f.x - mu[i]) * (f.x - mu[i]) + (f.y - mu[i]) * (f.y - mu[i]);
-            }
-            rs[i] = q;
-          }
-#pragma unroll
-          for (int off = 16; off; off >>= 1)
-#pragma unroll
-            for (int i = 0; i < 8; ++i) rs[i] += __shfl_xor_sync(0xffffffffu, rs[i], off);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int r = warp + 8 * (8 * hb + i);
-            if (r >= rows) break;
-            const float rstd = rsqrtf(rs[i] * (1.f / DP_E) + 1e-5f);
-            const uint32_t xw[4] = {xin4[i].x, xin4[i].y, xin4[i].z, xin4[i].w};
-            uint32_t yw[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&xw[k]));
-              const __nv_bfloat162 h2 = __floats2bfloat162_rn((f.x - mu[i]) * rstd * ga[2 * k] + ba[2 * k],
-                                                              (f.y - mu[i]) * rstd * ga[2 * k + 1] + ba[2 * k + 1]);
-              yw[k] = *reinterpret_cast<const uint32_t *>(&h2);
-            }
-            const int kb = lane >> 3, ch = lane & 7;          // k-block of these 8 columns, chunk within the row
-            *reinterpret_cast<uint4 *>(sAln + kb * DP_A_BYTES + r * 128 + ((ch ^ (r & 7)) << 4)) =
-                make_uint4(yw[0], yw[1], yw[2], yw[3]);
-          }
-          }
+          // ---- the A operand: LayerNorm of every token row of the residual stream.  The
+          //      producer TMA'd the rows into sAln in the UMMA layout (K-major, 128B swizzle:
+          //      16-byte chunk j of row r at chunk j ^ (r & 7)); each warp normalises its 16 rows
+          //      in place, 8 at a time with their reductions interleaved; lane l owns columns
+          //      8 l .. 8 l + 7 (k-block l / 8, chunk l % 8)
+          mbar_wait(lnbar, o.par[rank == 0] & 1);
+          dp_ln_tile(sAln, g.ln_g, g.ln_b, warp, lane);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncthreads();
+          named_sync(1, DP_CT);
+          DP_STAMP(2, threadIdx.x == 0);
         }
         if (warp == 1) {
           // ---- MMA issuer
+          // Each barrier probe is a round trip to the synchronisation unit (~200 cycles), more
+          // than the four UMMAs of a k-block: after the blocking wait for stage kb, the next
+          // stages are probed together (independent test_waits in flight at once) and every
+          // k-block already landed is issued back to back.
           const uint32_t idesc = umma_idesc(ncta);
-          for (int kb = 0; kb < nkb; ++kb, ++ic) {
-            const int st = ic % DP_STAGES;
-            mbar_wait(&full[st], (ic / DP_STAGES) & 1);
+          const int j0 = o.job[rank == 0];
+          for (int kb = 0; kb < nkb;) {
+            const int ic = j0 + kb;
+            mbar_wait(&full[ic % DP_STAGES], (ic / DP_STAGES) & 1);
+            constexpr int PROBE = 4;
+            bool t[PROBE - 1];
+#pragma unroll
+            for (int r = 1; r < PROBE; ++r)
+              t[r - 1] = kb + r < nkb && dp_stage_free(&full[(ic + r) % DP_STAGES], ((ic + r) / DP_STAGES) & 1);
+            int ready = 1;
+#pragma unroll
+            for (int r = 0; r < PROBE - 1; ++r) ready += (ready == r + 1 && t[r]) ? 1 : 0;
+            if (kb == 0) DP_STAMP(3, lane == 0);
+            DP_KSTAMP(32 + kb, lane == 0 && kb < 16);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t sa = lnA ? smem_u32(sAln + kb * DP_A_BYTES) : smem_u32(smem + st * DP_STAGE);
-            const uint32_t sb = smem_u32(smem + st * DP_STAGE) + DP_A_BYTES;
-            umma_kblock_warp(tmem, umma_desc(sa), umma_desc(sb), idesc, kb > 0 ? 1u : 0u);
-            umma_commit_warp(&empty[st]);
-            if (kb == nkb - 1) umma_commit_warp(done);
+            for (int r = 0; r < ready; ++r, ++kb) {
+              const int st = (j0 + kb) % DP_STAGES;
+              const uint32_t sa = smem_u32(lnA ? sAln + kb * DP_A_BYTES : smem + st * DP_A_BYTES);
+              const uint32_t sb = smem_u32(smem + DP_B_OFF + st * DP_B_BYTES);
+              if (!(P.dbg & 8)) umma_kblock_warp(tmem, umma_desc(sa), umma_desc(sb), idesc, kb > 0 ? 1u : 0u);
+              dp_commit_all(&empty[st]);
+            }
+            if (kb == nkb) DP_STAMP(4, lane == 0);
             __syncwarp();
           }
+          umma_commit_warp(done);
+          __syncwarp();
         }
         {
           // ---- epilogue, all 8 warps: token row = TMEM lane (warp % 4 quadrant), warps
           //      0-3 / 4-7 take alternate 16-column chunks
           const int row = (warp & 3) * 32 + lane, grp = warp >> 2;
           const int n0 = rank * ncta;
-          // residual of this warp's first two chunks while the MMAs run
-          uint4 rpre[4];
-          const bool pre = g.res && row < rows && n0 + ncta <= g.N;
-          if (pre) {
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              const int c = 16 * (grp + 2 * k);
-              const uint4 *rp = reinterpret_cast<const uint4 *>(g.res + (int64_t)row * g.ldr + n0 + c);
-              rpre[2 * k] = c < ncta ? rp[0] : make_uint4(0, 0, 0, 0);
-              rpre[2 * k + 1] = c < ncta ? rp[1] : make_uint4(0, 0, 0, 0);
-            }
+          const uint8_t *sres = smem + DP_R_OFF + row * ncta * 2;     // this row of the TMA'd residual slice
+          // the GEMM's fields in registers: g lives in shared memory behind a generic pointer, so
+          // every global store below would otherwise force it to be re-read
+          const float *bias_s = sbias + g.boff;
+          const __nv_bfloat16 *res = g.res;
+          __nv_bfloat16 *out = g.out;
+          float *outf = g.out_f32;
+          const int ldo = g.ldo, ldr = g.ldr, ldf = g.ldf, act = g.act, N = g.N;
+          const bool rtma = g.rtma != 0 && rank < g.ctas;
+          const int ncols = rank < g.ctas ? ncta : 0;    // (the single-CTA head: only CTA 0 stores)
+          if (P.dbg & 1) mbar_wait_sleep(done, (o.par[rank == 0] >> 2) & 1, 256);
+          else mbar_wait(done, (o.par[rank == 0] >> 2) & 1);
+          if (rtma) {
+            mbar_wait(resbar, (o.par[rank == 0] >> 1) & 1);
           }
-          mbar_wait(done, ng & 1);
+          DP_STAMP(5, threadIdx.x == 0);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          for (int c = 16 * grp, k = 0; c < ncta; c += 32, ++k) {
+          for (int c = 16 * grp; c < ncols; c += 32) {
             float v[16];
             tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + c, v);
+            DP_KSTAMP(48 + 3 * (c >> 5), threadIdx.x == 0 && c < 96);
             if (row >= rows) continue;
             const int nb = n0 + c;
-            if (nb + 16 <= g.N) {
+            if (nb + 16 <= N) {
 #pragma unroll
               for (int i = 0; i < 16; i += 4) {
-                const float4 bb = *reinterpret_cast<const float4 *>(g.bias + nb + i);
+                const float4 bb = *reinterpret_cast<const float4 *>(bias_s + c + i);
                 v[i] += bb.x; v[i + 1] += bb.y; v[i + 2] += bb.z; v[i + 3] += bb.w;
               }
-              if (g.act)
+              if (act == AURAS_ACT_GELU) {
 #pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = activate(v[i], g.act);
-              if (g.res) {
+                for (int i = 0; i < 16; ++i) v[i] = dp_gelu(v[i]);
+              } else if (act) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = activate(v[i], act);
+              }
+              DP_KSTAMP(49 + 3 * (c >> 5), threadIdx.x == 0 && c < 96);
+              if (res) {
                 uint4 r0, r1;
-                if (pre && k < 2) {
-                  r0 = k == 0 ? rpre[0] : rpre[2];
-                  r1 = k == 0 ? rpre[1] : rpre[3];
+                if (rtma) {
+                  r0 = reinterpret_cast<const uint4 *>(sres + c * 2)[0];
+                  r1 = reinterpret_cast<const uint4 *>(sres + c * 2)[1];
                 } else {
-                  const uint4 *rp = reinterpret_cast<const uint4 *>(g.res + (int64_t)row * g.ldr + nb);
+                  const uint4 *rp = reinterpret_cast<const uint4 *>(res + (int64_t)row * ldr + nb);
                   r0 = rp[0];
                   r1 = rp[1];
                 }
@@ -421,35 +670,40 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
                   v[2 * i + 1] += f.y;
                 }
               }
-              if (g.out) {
+              if (out) {
                 uint32_t ow[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                   const __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
                   ow[i] = *reinterpret_cast<const uint32_t *>(&h2);
                 }
-                uint4 *op = reinterpret_cast<uint4 *>(g.out + (int64_t)row * g.ldo + nb);
+                uint4 *op = reinterpret_cast<uint4 *>(out + (int64_t)row * ldo + nb);
                 op[0] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
                 op[1] = make_uint4(ow[4], ow[5], ow[6], ow[7]);
               }
-              if (g.out_f32)
+              if (outf) {
+                float4 *fp = reinterpret_cast<float4 *>(outf + (int64_t)row * ldf + nb);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) g.out_f32[(int64_t)row * g.ldf + nb + i] = v[i];
+                for (int i = 0; i < 4; ++i) fp[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+              }
+              DP_KSTAMP(50 + 3 * (c >> 5), threadIdx.x == 0 && c < 96);
             } else {
-              // ragged tail (the 7-wide action head): scalar, columns < N only
+              // ragged tail (the 7-wide action head): columns < N only
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
-                const int n = nb + i;
-                if (n >= g.N) continue;
-                float x = activate(v[i] + g.bias[n], g.act);
-                if (g.res) x += __bfloat162float(g.res[(int64_t)row * g.ldr + n]);
-                if (g.out) g.out[(int64_t)row * g.ldo + n] = __float2bfloat16_rn(x);
-                if (g.out_f32) g.out_f32[(int64_t)row * g.ldf + n] = x;
+                v[i] = activate(v[i] + bias_s[c + i], act);
+                if (res && nb + i < N) v[i] += __bfloat162float(res[(int64_t)row * ldr + nb + i]);
               }
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                if (nb + i >= N) break;
+                if (out) out[(int64_t)row * ldo + nb + i] = __float2bfloat16_rn(v[i]);
+                if (outf) outf[(int64_t)row * ldf + nb + i] = v[i];
+              }
+              DP_KSTAMP(50, threadIdx.x == 0);
             }
           }
         }
-        ++ng;
       }
     } else if (o.type == DP_LN) {
       for (int r = rank * 8 + warp; r < rows; r += DP_CL * 8)
@@ -472,7 +726,7 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
                                        : nullptr;
         const float sab = sch.sqrt_ab[i], s1m = sch.sqrt_1mab[i];
         const float cx0 = sch.c_x0[i], cxt = sch.c_xt[i], ceps = sch.c_eps[i], sig = sch.sigma[i];
-        for (int e = threadIdx.x; e < P.horizon * P.adim; e += DP_THREADS) {
+        for (int e = threadIdx.x; e < P.horizon * P.adim; e += DP_CT) {
           const int t = e / P.adim, a = e % P.adim;
           const float xt = x[e], ep = P.eps[((int64_t)s * P.horizon + t) * P.eps_pitch + a];
           float x0 = (xt - s1m * ep) / sab;
@@ -483,8 +737,13 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
         }
       }
     }
-    // phase boundary: generic stores visible to the next phase's TMA reads, TMEM drained
+    // weight blocks of the next GEMMs into the stages this phase released
+    DP_STAMP(6, threadIdx.x == 0);
+    // phase boundary: generic global stores visible to the next phase's TMA reads, TMEM drained
+    // (the residual reads of sAln completed into registers before this point; LayerNorm's
+    // generic writes of sAln were proxy-fenced in their phase)
     fence_proxy_async();
+    DP_STAMP(7, threadIdx.x == 0);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     cluster_sync_all();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -494,8 +753,10 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
       P.trace[oi + 1] = tn;
     }
   }
+  }
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(DP_TMEM_COLS));
 }
+#undef rows
 
 struct DpPlan {
   DpOpDev *ops = nullptr;
@@ -503,6 +764,22 @@ struct DpPlan {
   long long *trace = nullptr;          // AURAS_DPT_TRACE: per-phase timestamps of the last run
   int n_ops = 0, n_gemms = 0, T = 16;
 };
+
+// Residual slice map: [rows][N] bf16 with row pitch ld, box {ncta, 128}, no swizzle (row-major
+// [128][ncta] in shared memory).
+static int dp_map_res(CUtensorMap *tm, const void *base, int N, int ld, int rows, int ncta) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return AURAS_E_CUDA; }
+  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)ncta, 128};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("dpt_persist residual map: CUresult %d", (int)r); return AURAS_E_CUDA; }
+  return AURAS_OK;
+}
 
 static int dp_map(CUtensorMap *tm, const void *base, int K, int rows, int box_rows) {
   EncodeTiledFn enc = encode_fn();
@@ -531,15 +808,21 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
     set_error("dpt_persist_build: bad arguments");
     return AURAS_E_ARG;
   }
+  if (n_ops > DP_MAX_OPS || n_gemms > DP_MAX_GEMMS) {
+    set_error("dpt_persist_build: %d ops / %d GEMMs (max %d / %d)", n_ops, n_gemms, DP_MAX_OPS, DP_MAX_GEMMS);
+    return AURAS_E_ARG;
+  }
   std::vector<DpGemmDev> hg(n_gemms);
+  int boff = 0;
   for (int i = 0; i < n_gemms; ++i) {
     const auras_dpt_gemm &s = gemms[i];
     DpGemmDev &d = hg[i];
     memset(&d, 0, sizeof(d));
     const int ctas = s.N <= 16 ? 1 : DP_CL;
     const int ncta = ctas == 1 ? 16 : s.N / DP_CL;
-    if (s.K % 64 || s.act_rows != 128 || (ctas > 1 && (s.N % DP_CL || ncta % 16 || ncta > 128)) ||
-        (s.out && s.ldo % 8) || (s.res && s.ldr % 8)) {
+    if (s.K % 64 || s.act_rows != 128 || (ctas > 1 && (s.N % DP_CL || ncta % 16 || ncta * 128 > DP_B_BYTES)) ||
+        (s.out && s.ldo % 8) || (s.res && s.ldr % 8) ||
+        (ctas > 1 && s.out_f32 && (s.ldf % 4 || (reinterpret_cast<uintptr_t>(s.out_f32) & 15)))) {
       set_error("dpt_persist_build: gemm %d shape K=%d N=%d rows=%d", i, s.K, s.N, s.act_rows);
       return AURAS_E_ARG;
     }
@@ -547,20 +830,30 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
       set_error("dpt_persist_build: gemm %d LayerNorm'd A needs K = 256", i);
       return AURAS_E_ARG;
     }
-    if (!s.ln_g)
-      if (int rc = dp_map(&d.tmA, s.act, s.K, s.act_rows, 128)) return rc;
+    // A operand, or (LayerNorm'd A) the residual-stream rows the phase normalises in place
+    if (int rc = dp_map(&d.tmA, s.ln_g ? s.ln_src : s.act, s.K, s.act_rows, DP_MROWS)) return rc;
     d.ln_src = static_cast<const __nv_bfloat16 *>(s.ln_src);
     d.ln_g = s.ln_g;
     d.ln_b = s.ln_b;
     if (int rc = dp_map(&d.tmB, s.w, s.K, s.N, ncta)) return rc;
     d.bias = s.bias;
     d.res = static_cast<const __nv_bfloat16 *>(s.res);
+    d.rtma = s.res && ctas > 1 && ncta * 128 * 2 <= DP_R_BYTES && (reinterpret_cast<uintptr_t>(s.res) & 15) == 0 ? 1 : 0;
+    if (d.rtma)
+      if (int rc = dp_map_res(&d.tmR, s.res, s.N, s.ldr, s.act_rows, ncta)) return rc;
     d.out = static_cast<__nv_bfloat16 *>(s.out);
     d.out_f32 = s.out_f32;
     d.K = s.K; d.N = s.N; d.ncta = ncta; d.ctas = ctas;
+    d.boff = boff;
+    boff += (ncta + 3) & ~3;           // float4-aligned slices
+    if (boff > DP_BIAS_SLAB) {
+      set_error("dpt_persist_build: bias slices exceed %d floats", DP_BIAS_SLAB);
+      return AURAS_E_ARG;
+    }
     d.ldo = s.ldo; d.ldr = s.ldr; d.ldf = s.ldf; d.act = s.act_fn;
   }
   std::vector<DpOpDev> ho(n_ops);
+  int nln[2] = {0, 0}, nres[2] = {0, 0}, ng[2] = {0, 0}, nj[2] = {0, 0};   // [CTAs 1..] / [CTA 0]
   for (int i = 0; i < n_ops; ++i) {
     const auras_dpt_op &s = ops[i];
     DpOpDev &d = ho[i];
@@ -573,6 +866,19 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
     d.v = static_cast<const __nv_bfloat16 *>(s.v);
     d.ldi = s.ldi; d.ldo = s.ldo; d.ldk = s.ldk; d.ldv = s.ldv;
     d.nk = s.nk; d.mask_off = s.mask_off; d.heads = s.heads; d.dh = s.dh;
+    if (s.type == DP_GEMM && s.gemm >= 0 && s.gemm < n_gemms) {
+      const DpGemmDev &gg = hg[s.gemm];
+      for (int c = 0; c < 2; ++c) {
+        const bool runs = true;        // every CTA streams every GEMM (multicast ring)
+        d.par[c] = (nln[c] & 1) | ((nres[c] & 1) << 1) | ((ng[c] & 1) << 2);
+        d.job[c] = nj[c];
+        if (!runs) continue;
+        if (gg.ln_g) ++nln[c];
+        if (gg.rtma) ++nres[c];
+        ++ng[c];
+        nj[c] += gg.K / 64;
+      }
+    }
     if ((s.type == DP_GEMM && (s.gemm < 0 || s.gemm >= n_gemms)) || (s.type == DP_ATTN && (s.nk > DP_MAXK || s.dh != 64)) ||
         s.type < 0 || s.type > DP_NOP) {
       set_error("dpt_persist_build: op %d", i);
@@ -591,7 +897,10 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
   }
   cudaMemcpy(p->ops, ho.data(), sizeof(DpOpDev) * n_ops, cudaMemcpyHostToDevice);
   cudaMemcpy(p->gemms, hg.data(), sizeof(DpGemmDev) * n_gemms, cudaMemcpyHostToDevice);
-  if (getenv("AURAS_DPT_TRACE")) cudaMalloc(&p->trace, sizeof(long long) * (n_ops + 1));
+  if (getenv("AURAS_DPT_TRACE")) {
+    cudaMalloc(&p->trace, sizeof(long long) * (73 * n_ops + 1));
+    cudaMemset(p->trace, 0, sizeof(long long) * (73 * n_ops + 1));
+  }
   *plan_out = p;
   return cuda_check(cudaGetLastError(), "dpt_persist_build");
 }
@@ -615,12 +924,20 @@ int auras_dpt_persist_run(void *plan, int S, const float *eps, int eps_pitch, co
   DpParams P;
   memset(&P, 0, sizeof(P));
   P.trace = p->trace;
-  P.ops = p->ops; P.gemms = p->gemms; P.n_ops = p->n_ops; P.S = S; P.T = p->T;
+  P.ops = p->ops; P.gemms = p->gemms; P.n_ops = p->n_ops; P.n_gemms = p->n_gemms; P.S = S; P.T = p->T;
   P.eps = eps; P.eps_pitch = eps_pitch;
   P.agents = agents; P.lanes = lanes; P.steps = steps;
   P.x_lanes = x_lanes; P.noise_lanes = noise_lanes;
   P.lanes_per_agent = lanes_per_agent; P.horizon = horizon; P.adim = adim;
   P.sched = *sched;
+  {
+    static int pf = -1;
+    if (pf < 0) pf = getenv("AURAS_DPT_PF") ? atoi(getenv("AURAS_DPT_PF")) : 1;
+    P.pf = pf;
+    static int dbg = -1;
+    if (dbg < 0) dbg = getenv("AURAS_DPT_DBG") ? atoi(getenv("AURAS_DPT_DBG")) : 0;
+    P.dbg = dbg;
+  }
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3(DP_CL);
@@ -643,7 +960,7 @@ int auras_dpt_persist_run(void *plan, int S, const float *eps, int eps_pitch, co
 int auras_dpt_persist_trace(void *plan, long long *out, int n) {
   DpPlan *p = static_cast<DpPlan *>(plan);
   if (!p || !p->trace || !out) return 0;
-  const int m = std::min(n, p->n_ops + 1);
+  const int m = std::min(n, 73 * p->n_ops + 1);   // per-phase stamps, then 8 sub-phase clocks per op
   cudaMemcpy(out, p->trace, sizeof(long long) * m, cudaMemcpyDeviceToHost);
   return m;
 }

@@ -38,11 +38,26 @@ if os.environ.get("AURAS_DPT_TRACE"):
     import ctypes
     from paper_2509_09560_b200 import _lib
     den = sess.denoiser
-    n = 200
+    n = 20000
     buf = (ctypes.c_longlong * n)()
-    m = _lib.load().auras_dpt_persist_trace(den.pplan, buf, n)
+    mm = _lib.load().auras_dpt_persist_trace(den.pplan, buf, n)
+    n_ops = (mm - 1) // 73
+    m = n_ops + 1
     t = np.array(buf[:m], dtype=np.int64)
+    sub = np.array(buf[m:9 * n_ops + 1], dtype=np.int64).reshape(n_ops, 8)
+    ks = np.array(buf[9 * n_ops + 1:mm], dtype=np.int64).reshape(n_ops, 64)
     d = np.diff(t) / 1e3
     kinds = []
     print("phases", m - 1, "total us", (t[-1] - t[0]) / 1e3)
     print("per phase us:", " ".join(f"{x:.1f}" for x in d))
+    names = ["start", "prod", "ln", "mma0", "mmaN", "done", "epi", "fence"]
+    print("sub-phase clocks (cycles after phase start; layer 2 ops + head/update):")
+    for oi in list(range(9, 17)) + [n_ops - 2, n_ops - 1]:
+        r = sub[oi]
+        print(f"  op {oi:3d}: " + " ".join(f"{names[k]}={(r[k] - r[0]) if r[k] else -1}" for k in range(1, 8)))
+    for oi in (9, 15, 16, n_ops - 2):
+        r0 = sub[oi][0]
+        print(f"  op {oi} epilogue : " + " ".join(str(ks[oi][48 + j] - r0) if ks[oi][48 + j] else "-" for j in range(6)))
+        k = ks[oi]
+        for name, off in (("B ready", 0), ("A issued", 16), ("MMA full", 32)):
+            print(f"  op {oi} {name:9s}: " + " ".join(str(k[off + j] - r0) if k[off + j] else "-" for j in range(16)))
