@@ -62,7 +62,8 @@ constexpr int DP_TMEM_COLS = 128;
 // table from global memory would be an L2 round trip (~1 us) on the critical path of
 // every one of the ~67 phases.
 constexpr int DP_MAX_OPS = 96, DP_MAX_GEMMS = 56, DP_BIAS_SLAB = 3072;
-constexpr size_t DP_META_OFF = DP_BAR_OFF + 256;
+constexpr size_t DP_STAT_OFF = DP_BAR_OFF + 256;  // per-row (mean, rstd) of the tile a LayerNorm phase applies
+constexpr size_t DP_META_OFF = DP_STAT_OFF + 128 * 8;
 constexpr size_t DP_META_BYTES = (size_t)DP_MAX_OPS * 104 + DP_MAX_GEMMS * 96 + DP_BIAS_SLAB * 4;
 constexpr size_t DP_SMEM = 1024 + DP_META_OFF + DP_META_BYTES;   // ring + LayerNorm'd A + barriers + metadata
 constexpr int DP_MAXK = 16;                   // keys per query (horizon <= 16; 3 cond tokens)
@@ -83,6 +84,8 @@ struct alignas(64) DpGemmDev {
   const float *ln_g, *ln_b;
   int boff;                  // this GEMM's bias slice in the shared-memory slab
   int rtma;                  // the residual slice is TMA'd into shared memory (16-column slices)
+  int stats_out;             // epilogue writes per-row (mean, M2) of its 16 stored columns to P.stats
+  int stats_in;              // the LayerNorm'd A uses the row statistics the previous writer left in P.stats
 };
 
 // The GEMM fields the phases read (no tensor maps: those stay in global memory for the TMA unit).
@@ -92,7 +95,7 @@ struct DpGemmMeta {
   float *out_f32;
   const __nv_bfloat16 *ln_src;
   const float *ln_g, *ln_b;
-  int K, N, ncta, ldo, ldr, ldf, act, ctas, boff, rtma;
+  int K, N, ncta, ldo, ldr, ldf, act, ctas, boff, rtma, stats_out, stats_in;
 };
 static_assert(sizeof(DpGemmMeta) <= 96, "DpGemmMeta");
 
@@ -117,6 +120,7 @@ struct DpParams {
   int n_ops, n_gemms, S, T;
   int dbg;                   // AURAS_DPT_DBG timing variants (0 in production)
   int pf;                    // weight prefetch across phase barriers (0: only in the GEMM's own phase)
+  float2 *stats;             // [128 rows][DP_CL slices] (mean, M2) of the residual stream's last writer
   // update
   const float *eps;
   int eps_pitch;
@@ -168,7 +172,7 @@ __device__ __forceinline__ void dp_ln_row(const __nv_bfloat16 *xr, __nv_bfloat16
 constexpr int DP_QB = 4;
 
 // (noinline: its ~130 live registers must not push the persistent loop's state into local memory)
-__device__ __noinline__ void dp_attn_block(const DpOpDev &o, int q0, int q1, int T, int lane) {
+__device__ __noinline__ void dp_attn_block(const DpOpDev &o, int q0, int q1, int T, int lane, long long *stamp) {
   const int nk = o.nk, dh = 64;
   const float scale = rsqrtf((float)dh);
   int unit = -1;
@@ -216,6 +220,7 @@ __device__ __noinline__ void dp_attn_block(const DpOpDev &o, int q0, int q1, int
         }
       }
     }
+    if (stamp && qi == q0) stamp[0] = clock64();
     float mx[DP_QB], pe[DP_QB], sm[DP_QB];
 #pragma unroll
     for (int b = 0; b < DP_QB; ++b) {
@@ -439,6 +444,30 @@ __device__ __noinline__ void dp_ln_tile(uint8_t *sAln, const float *ln_g, const 
   }
 }
 
+// LayerNorm of the tile with the row statistics given (mean, rstd per row in shared memory): the
+// normalisation pass only, no reductions.
+__device__ __forceinline__ void dp_ln_apply(uint8_t *sAln, const float (&ga)[8], const float (&ba)[8],
+                                            const float2 *srs, int warp, int lane) {
+  const int kbl = lane >> 3, ch = lane & 7;
+#pragma unroll 4
+  for (int i = 0; i < 128 / 8; ++i) {
+    const int r = warp + 8 * i;
+    uint4 *px = reinterpret_cast<uint4 *>(sAln + kbl * DP_A_BYTES + r * 128 + ((ch ^ (r & 7)) << 4));
+    const uint4 xv = *px;
+    const float2 st = srs[r];
+    const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+    uint32_t yw[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&xw[k]));
+      const __nv_bfloat162 h2 = __floats2bfloat162_rn((f.x - st.x) * st.y * ga[2 * k] + ba[2 * k],
+                                                      (f.y - st.x) * st.y * ga[2 * k + 1] + ba[2 * k + 1]);
+      yw[k] = *reinterpret_cast<const uint32_t *>(&h2);
+    }
+    *px = make_uint4(yw[0], yw[1], yw[2], yw[3]);
+  }
+}
+
 __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_constant__ DpParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -466,6 +495,7 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
       m.ln_src = g.ln_src; m.ln_g = g.ln_g; m.ln_b = g.ln_b;
       m.K = g.K; m.N = g.N; m.ncta = g.ncta; m.ldo = g.ldo; m.ldr = g.ldr; m.ldf = g.ldf;
       m.act = g.act; m.ctas = g.ctas; m.boff = g.boff; m.rtma = g.rtma;
+      m.stats_out = g.stats_out; m.stats_in = g.stats_in;
       sgm[i] = m;
     }
     for (int i = warp; i < P.n_gemms; i += DP_THREADS / 32) {
@@ -569,8 +599,49 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
           //      16-byte chunk j of row r at chunk j ^ (r & 7)); each warp normalises its 16 rows
           //      in place, 8 at a time with their reductions interleaved; lane l owns columns
           //      8 l .. 8 l + 7 (k-block l / 8, chunk l % 8)
-          mbar_wait(lnbar, o.par[rank == 0] & 1);
-          dp_ln_tile(sAln, g.ln_g, g.ln_b, warp, lane);
+          if (g.stats_in) {
+            // row statistics from the 16 column-slice partials the residual GEMM's epilogue
+            // left (equal-count Chan combination, a 4-level tree), one row per thread; the
+            // loads overlap the tile's TMA
+            float2 *srs = reinterpret_cast<float2 *>(smem + DP_STAT_OFF);
+            // this lane's LayerNorm affine (columns 8 lane .. 8 lane + 7) first: an L2 round trip
+            // that would otherwise stall the first normalised row
+            const float4 g0 = *reinterpret_cast<const float4 *>(g.ln_g + 8 * lane);
+            const float4 g1 = *reinterpret_cast<const float4 *>(g.ln_g + 8 * lane + 4);
+            const float4 b0 = *reinterpret_cast<const float4 *>(g.ln_b + 8 * lane);
+            const float4 b1 = *reinterpret_cast<const float4 *>(g.ln_b + 8 * lane + 4);
+            if (threadIdx.x < 128) {
+              const float4 *sp = reinterpret_cast<const float4 *>(P.stats + threadIdx.x * DP_CL);
+              float mu[DP_CL], m2[DP_CL];
+#pragma unroll
+              for (int i = 0; i < DP_CL / 2; ++i) {
+                const float4 q = sp[i];
+                mu[2 * i] = q.x; m2[2 * i] = q.y; mu[2 * i + 1] = q.z; m2[2 * i + 1] = q.w;
+              }
+              float n = (float)(DP_E / DP_CL);
+#pragma unroll
+              for (int w = 1; w < DP_CL; w *= 2) {
+#pragma unroll
+                for (int i = 0; i < DP_CL; i += 2 * w) {
+                  const float d = mu[i + w] - mu[i];
+                  m2[i] = m2[i] + m2[i + w] + d * d * (0.5f * n);
+                  mu[i] = 0.5f * (mu[i] + mu[i + w]);
+                }
+                n *= 2.f;
+              }
+              srs[threadIdx.x] = make_float2(mu[0], rsqrtf(m2[0] * (1.f / DP_E) + 1e-5f));
+            }
+            named_sync(1, DP_CT);
+            mbar_wait(lnbar, o.par[rank == 0] & 1);
+            DP_KSTAMP(57, threadIdx.x == 0);
+            const float ga[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+            const float ba[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+            dp_ln_apply(sAln, ga, ba, srs, warp, lane);
+          } else {
+            mbar_wait(lnbar, o.par[rank == 0] & 1);
+            DP_KSTAMP(57, threadIdx.x == 0);
+            dp_ln_tile(sAln, g.ln_g, g.ln_b, warp, lane);
+          }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           named_sync(1, DP_CT);
           DP_STAMP(2, threadIdx.x == 0);
@@ -624,6 +695,7 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
           float *outf = g.out_f32;
           const int ldo = g.ldo, ldr = g.ldr, ldf = g.ldf, act = g.act, N = g.N;
           const bool rtma = g.rtma != 0 && rank < g.ctas;
+          const bool stats_out = g.stats_out != 0;
           const int ncols = rank < g.ctas ? ncta : 0;    // (the single-CTA head: only CTA 0 stores)
           if (P.dbg & 1) mbar_wait_sleep(done, (o.par[rank == 0] >> 2) & 1, 256);
           else mbar_wait(done, (o.par[rank == 0] >> 2) & 1);
@@ -680,6 +752,22 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
                 uint4 *op = reinterpret_cast<uint4 *>(out + (int64_t)row * ldo + nb);
                 op[0] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
                 op[1] = make_uint4(ow[4], ow[5], ow[6], ow[7]);
+                if (stats_out) {
+                  // (mean, M2) of the 16 stored (bf16-rounded) values: the next LayerNorm's input
+                  float x[16], sm = 0.f;
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) {
+                    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&ow[i]));
+                    x[2 * i] = f.x;
+                    x[2 * i + 1] = f.y;
+                    sm += f.x + f.y;
+                  }
+                  const float mu = sm * (1.f / 16.f);
+                  float m2 = 0.f;
+#pragma unroll
+                  for (int i = 0; i < 16; ++i) m2 = fmaf(x[i] - mu, x[i] - mu, m2);
+                  P.stats[row * DP_CL + rank] = make_float2(mu, m2);
+                }
               }
               if (outf) {
                 float4 *fp = reinterpret_cast<float4 *>(outf + (int64_t)row * ldf + nb);
@@ -690,10 +778,14 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
             } else {
               // ragged tail (the 7-wide action head): columns < N only
 #pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                v[i] = activate(v[i] + bias_s[c + i], act);
-                if (res && nb + i < N) v[i] += __bfloat162float(res[(int64_t)row * ldr + nb + i]);
-              }
+              for (int i = 0; i < 16; ++i) v[i] += bias_s[c + i];
+              if (act)
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = activate(v[i], act);
+              if (res)
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                  if (nb + i < N) v[i] += __bfloat162float(res[(int64_t)row * ldr + nb + i]);
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
                 if (nb + i >= N) break;
@@ -712,7 +804,8 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
       // contiguous query ranges over the 64 warps of the cluster
       const int items = P.S * o.heads * P.T, per = (items + DP_CL * 8 - 1) / (DP_CL * 8);
       const int gw = rank * 8 + warp;
-      dp_attn_block(o, min(items, gw * per), min(items, (gw + 1) * per), P.T, lane);
+      long long *stamp = P.trace && rank == 0 && threadIdx.x == 0 ? P.trace + 9 * P.n_ops + 1 + 64 * oi + 56 : nullptr;
+      dp_attn_block(o, min(items, gw * per), min(items, (gw + 1) * per), P.T, lane, stamp);
     } else if (o.type == DP_NOP) {
       // timing probe: a phase with no work (the cost of the phase boundary alone)
     } else {
@@ -759,6 +852,7 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
 #undef rows
 
 struct DpPlan {
+  float2 *stats = nullptr;             // [128][DP_CL] row-statistics partials
   DpOpDev *ops = nullptr;
   DpGemmDev *gemms = nullptr;
   long long *trace = nullptr;          // AURAS_DPT_TRACE: per-phase timestamps of the last run
@@ -885,16 +979,40 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
       return AURAS_E_ARG;
     }
   }
+  {
+    // Row-statistics handoff: a GEMM whose epilogue writes 16-column slices of a 256-wide
+    // activation (N = DP_E over the cluster) records per-slice (mean, M2); a later LayerNorm'd
+    // GEMM reading that same activation, with no other writer in between, uses them.
+    // (one statistics buffer: only writers of a LayerNorm source take part)
+    std::vector<const void *> lsrc;
+    for (int i = 0; i < n_gemms; ++i)
+      if (hg[i].ln_g) lsrc.push_back(hg[i].ln_src);
+    auto is_lsrc = [&](const void *q) { return std::find(lsrc.begin(), lsrc.end(), q) != lsrc.end(); };
+    const void *valid = nullptr;
+    for (int i = 0; i < n_ops; ++i) {
+      if (ops[i].type != DP_GEMM) continue;
+      DpGemmDev &d = hg[ops[i].gemm];
+      if (d.ln_g) d.stats_in = valid && d.ln_src == valid;
+      if (d.out && is_lsrc(d.out)) {
+        const bool ok = d.N == DP_E && d.ncta == 16 && d.ctas == DP_CL;
+        d.stats_out = ok;
+        valid = ok ? d.out : nullptr;
+      }
+    }
+  }
   DpPlan *p = new DpPlan;
   p->n_ops = n_ops;
   p->n_gemms = n_gemms;
   p->T = T;
   if (cudaMalloc(&p->ops, sizeof(DpOpDev) * n_ops) != cudaSuccess ||
-      cudaMalloc(&p->gemms, sizeof(DpGemmDev) * n_gemms) != cudaSuccess) {
+      cudaMalloc(&p->gemms, sizeof(DpGemmDev) * n_gemms) != cudaSuccess ||
+      cudaMalloc(&p->stats, sizeof(float2) * 128 * DP_CL) != cudaSuccess) {
     cudaFree(p->ops);
+    cudaFree(p->gemms);
     delete p;
     return cuda_check(cudaGetLastError(), "dpt_persist alloc");
   }
+  cudaMemset(p->stats, 0, sizeof(float2) * 128 * DP_CL);
   cudaMemcpy(p->ops, ho.data(), sizeof(DpOpDev) * n_ops, cudaMemcpyHostToDevice);
   cudaMemcpy(p->gemms, hg.data(), sizeof(DpGemmDev) * n_gemms, cudaMemcpyHostToDevice);
   if (getenv("AURAS_DPT_TRACE")) {
@@ -924,6 +1042,7 @@ int auras_dpt_persist_run(void *plan, int S, const float *eps, int eps_pitch, co
   DpParams P;
   memset(&P, 0, sizeof(P));
   P.trace = p->trace;
+  P.stats = p->stats;
   P.ops = p->ops; P.gemms = p->gemms; P.n_ops = p->n_ops; P.n_gemms = p->n_gemms; P.S = S; P.T = p->T;
   P.eps = eps; P.eps_pitch = eps_pitch;
   P.agents = agents; P.lanes = lanes; P.steps = steps;
@@ -971,6 +1090,7 @@ void auras_dpt_persist_free(void *plan) {
   cudaFree(p->trace);
   cudaFree(p->ops);
   cudaFree(p->gemms);
+  cudaFree(p->stats);
   delete p;
 }
 
