@@ -358,6 +358,7 @@ typedef struct auras_dpt_op {
   const float *g, *b;       /* LN affine */
   const void *k, *v;        /* attention keys / values: rows (s * nk + j) */
   int ldi, ldo, ldk, ldv, nk, mask_off, heads, dh;
+  int qrows, krows;         /* attention: rows of the q buffer / of the k, v buffers (TMA bounds) */
 } auras_dpt_op;
 int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const auras_dpt_op *ops, int n_ops, int T,
                             void **plan);

@@ -113,10 +113,19 @@ struct DpOpDev {
 };
 static_assert(sizeof(DpOpDev) == 104, "DpOpDev");
 
+// Attention operand maps (128B-swizzled boxes {64, rows}: q {dh, T}, k / v {dh, nk}).
+struct alignas(64) DpAttnDev {
+  CUtensorMap tq, tk, tv;
+};
+constexpr int DP_ATT_UNIT = 3 * 2048;         // q, k, v tiles of one (sample, head) unit, <= 16 rows each
+constexpr int DP_ATT_SLOTS = 4;               // units per CTA (S * heads <= 4 * DP_CL)
+constexpr size_t DP_ATT_OFF = 4 * (size_t)DP_A_BYTES;   // A-ring stages 4-5: idle outside GEMM phases
+
 struct DpParams {
   long long *trace;          // optional: globaltimer after every phase barrier (CTA 0, thread 0)
   const DpOpDev *ops;
   const DpGemmDev *gemms;
+  const DpAttnDev *attns;    // per attention op (DpOpDev::gemm indexes it)
   int n_ops, n_gemms, S, T;
   int dbg;                   // AURAS_DPT_DBG timing variants (0 in production)
   int pf;                    // weight prefetch across phase barriers (0: only in the GEMM's own phase)
@@ -263,6 +272,7 @@ __device__ __noinline__ void dp_attn_block(const DpOpDev &o, int q0, int q1, int
     }
     qi += nq;
   }
+  if (stamp) stamp[1] = clock64();
 }
 
 // Every CTA of the cluster needs the same activation block: each loads 128 / DP_CL of its rows and
@@ -371,6 +381,128 @@ __device__ __forceinline__ float dp_gelu(float x) {
     if (P.trace && rank == 0 && (cond) && (k) < 64) P.trace[9 * P.n_ops + 1 + 64 * oi + (k)] = clock64(); \
   } while (0)
 
+// Attention of queries [n0, n0 + DP_QB) of unit (s, h) from its TMA'd tiles (128B-swizzled rows of
+// 64 bf16: 16-byte chunk c of row r at chunk c ^ (r & 7)).  Lane j scores key j (its K row chunks
+// against the broadcast q chunks), softmax over the lanes, lane l accumulates output dims 2l, 2l+1.
+__device__ __forceinline__ const uint8_t *dp_sw(const uint8_t *t, int r, int chunk) {
+  return t + r * 128 + ((chunk ^ (r & 7)) << 4);
+}
+
+__device__ __forceinline__ void dp_ldsm4(uint32_t (&r)[4], const void *p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void dp_ldsm4t(uint32_t (&r)[4], const void *p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+// D += A B, m16n8k16, bf16 in, fp32 accumulate
+__device__ __forceinline__ void dp_mma(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+               "{%0, %1, %2, %3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t dp_pack(float lo, float hi) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t *>(&h);
+}
+
+// One (sample, head) unit by one warp on the tensor cores (the tiles are 16 x 64: far too small
+// for tcgen05, one mma.sync m16n8k16 sequence is ~30 instructions): S = Q K^T (16 queries x 16
+// key slots), masked softmax on the accumulator fragments, O = P V with P split into bf16 hi + lo
+// parts (P V to ~2^-16, as the fp32 softmax of the launch-per-layer program).  Key slots >= nk
+// hold finite neighbouring rows (or TMA zero fill) and are masked.
+__device__ __noinline__ void dp_attn_tile(const DpOpDev &o, const uint8_t *t, int s, int h, int T, int lane) {
+  const uint8_t *tq = t, *tk = t + 2048, *tv = t + 4096;
+  const int g = lane >> 2, tq4 = lane & 3;
+  const int lr = lane & 15, lc = lane >> 4;          // ldmatrix row / chunk-half of this lane
+  float sc[2][4];                                    // [key n-tile][c0..c3]
+#pragma unroll
+  for (int n = 0; n < 2; ++n)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) sc[n][i] = 0.f;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {                   // head dims 16 ks .. 16 ks + 15
+    uint32_t a[4], b[4];
+    dp_ldsm4(a, dp_sw(tq, lr, 2 * ks + lc));
+    // K: lanes 0-7 keys 0-7 dims +0, 8-15 keys 0-7 dims +8, 16-23 keys 8-15 +0, 24-31 keys 8-15 +8
+    dp_ldsm4(b, dp_sw(tk, (lane & 7) + 8 * (lane >> 4), 2 * ks + ((lane >> 3) & 1)));
+    dp_mma(sc[0], a, b[0], b[1]);
+    dp_mma(sc[1], a, b[2], b[3]);
+  }
+  // masked softmax: this lane holds rows g (c0, c1) and g + 8 (c2, c3), key slots 8 n + 2 tq4 + {0, 1}
+  const float scale = 0.125f;                         // 1 / sqrt(64)
+  float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+  for (int n = 0; n < 2; ++n)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = g + 8 * (i >> 1), key = 8 * n + 2 * tq4 + (i & 1);
+      const bool ok = key < o.nk && key <= row + o.mask_off;
+      sc[n][i] = ok ? sc[n][i] * scale : -INFINITY;
+      mx[i >> 1] = fmaxf(mx[i >> 1], sc[n][i]);
+    }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+    mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+  }
+  float sm[2] = {0.f, 0.f};
+#pragma unroll
+  for (int n = 0; n < 2; ++n)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      sc[n][i] = sc[n][i] == -INFINITY ? 0.f : __expf(sc[n][i] - mx[i >> 1]);
+      sm[i >> 1] += sc[n][i];
+    }
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    sm[r] += __shfl_xor_sync(0xffffffffu, sm[r], 1);
+    sm[r] += __shfl_xor_sync(0xffffffffu, sm[r], 2);
+  }
+  // P as the A operand (the m16n8 accumulator layout is the m16n8k16 A layout), hi + lo bf16
+  uint32_t ph[4], pl[4];
+  {
+    const float p[8] = {sc[0][0], sc[0][1], sc[0][2], sc[0][3], sc[1][0], sc[1][1], sc[1][2], sc[1][3]};
+    const int ord[4][2] = {{0, 1}, {2, 3}, {4, 5}, {6, 7}};   // a0 (g, k 0-7) a1 (g+8, k 0-7) a2 (g, 8-15) a3
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float x0 = p[ord[i][0]], x1 = p[ord[i][1]];
+      ph[i] = dp_pack(x0, x1);
+      const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&ph[i]));
+      pl[i] = dp_pack(x0 - hf.x, x1 - hf.y);
+    }
+  }
+  const float inv[2] = {__fdividef(1.f, sm[0]), __fdividef(1.f, sm[1])};
+#pragma unroll
+  for (int dn = 0; dn < 4; ++dn) {                   // head dims 16 dn .. 16 dn + 15: two n-tiles
+    uint32_t b[4];
+    // V^T fragments: lanes 0-7 keys 0-7 / 8-15 keys 8-15 at dims +0, 16-23 / 24-31 at dims +8
+    dp_ldsm4t(b, dp_sw(tv, (lane & 7) + 8 * ((lane >> 3) & 1), 2 * dn + (lane >> 4)));
+    float acc[2][4];
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[n][i] = 0.f;
+    dp_mma(acc[0], ph, b[0], b[1]);
+    dp_mma(acc[0], pl, b[0], b[1]);
+    dp_mma(acc[1], ph, b[2], b[3]);
+    dp_mma(acc[1], pl, b[2], b[3]);
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int row = g + 8 * r;
+        if (row < T)
+          *reinterpret_cast<uint32_t *>(o.out + ((int64_t)s * T + row) * o.ldo + h * 64 + 16 * dn + 8 * n + 2 * tq4) =
+              dp_pack(acc[n][2 * r] * inv[r], acc[n][2 * r + 1] * inv[r]);
+      }
+  }
+}
+
 // LayerNorm of the 128 x 256 tile in sAln, in place (UMMA layout: K-major, 128B swizzle, 16-byte
 // chunk j of row r at chunk j ^ (r & 7)); warp w normalises rows w, w + 8, ..., 8 at a time with
 // their reductions interleaved; lane l owns columns 8 l .. 8 l + 7 (k-block l / 8, chunk l % 8).
@@ -475,8 +607,9 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
   uint64_t *empty = full + DP_STAGES;
   uint64_t *done = empty + DP_STAGES;
   uint64_t *lnbar = done + 1;     // the LayerNorm source tile landed in sAln
-  uint64_t *resbar = lnbar + 1;   // the residual slice landed in sAln
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(resbar + 1);
+  uint64_t *resbar = lnbar + 1;   // the residual slice landed
+  uint64_t *attbar = resbar + 1;  // the attention tiles landed
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(attbar + 1);
   DpOpDev *sops = reinterpret_cast<DpOpDev *>(smem + DP_META_OFF);
   DpGemmMeta *sgm = reinterpret_cast<DpGemmMeta *>(smem + DP_META_OFF + DP_MAX_OPS * 104);
   float *sbias = reinterpret_cast<float *>(smem + DP_META_OFF + DP_MAX_OPS * 104 + DP_MAX_GEMMS * 96);
@@ -521,6 +654,7 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
     mbar_init(done, 1);
     mbar_init(lnbar, 1);
     mbar_init(resbar, 1);
+    mbar_init(attbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -572,6 +706,20 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
           tma_load_2d(smem + DP_R_OFF, &P.gemms[o.gemm].tmR, resbar, rank * g.ncta, 0);
         }
         DP_STAMP(1, true);
+      } else if (lane == 0 && o.type == DP_ATTN) {
+        // this CTA's (sample, head) units u = rank + DP_CL k: q / k / v tiles in one transaction
+        const DpAttnDev &a = P.attns[o.gemm];
+        const int units = P.S * o.heads;
+        int bytes = 0;
+        for (int u = rank; u < units; u += DP_CL) bytes += (P.T + 2 * 16) * 128;
+        mbar_expect_tx(attbar, bytes);                     // (0 bytes: a plain arrive)
+        for (int u = rank, k = 0; u < units; u += DP_CL, ++k) {
+          const int sidx = u / o.heads, h = u % o.heads;
+          uint8_t *t = smem + DP_ATT_OFF + k * DP_ATT_UNIT;
+          tma_load_2d(t, &a.tq, attbar, h * 64, sidx * P.T);
+          tma_load_2d(t + 2048, &a.tk, attbar, h * 64, sidx * o.nk);
+          tma_load_2d(t + 4096, &a.tv, attbar, h * 64, sidx * o.nk);
+        }
       }
       __syncwarp();
       asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
@@ -801,11 +949,14 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
       for (int r = rank * 8 + warp; r < rows; r += DP_CL * 8)
         dp_ln_row(o.in + (int64_t)r * o.ldi, o.out + (int64_t)r * o.ldo, o.g, o.b, lane);
     } else if (o.type == DP_ATTN) {
-      // contiguous query ranges over the 64 warps of the cluster
-      const int items = P.S * o.heads * P.T, per = (items + DP_CL * 8 - 1) / (DP_CL * 8);
-      const int gw = rank * 8 + warp;
       long long *stamp = P.trace && rank == 0 && threadIdx.x == 0 ? P.trace + 9 * P.n_ops + 1 + 64 * oi + 56 : nullptr;
-      dp_attn_block(o, min(items, gw * per), min(items, (gw + 1) * per), P.T, lane, stamp);
+      mbar_wait(attbar, (o.par[0] >> 3) & 1);
+      if (stamp) stamp[0] = clock64();
+      // unit slot k (u = rank + DP_CL k) on warp k
+      const int u = rank + DP_CL * warp;
+      if (warp < DP_ATT_SLOTS && u < P.S * o.heads)
+        dp_attn_tile(o, smem + DP_ATT_OFF + warp * DP_ATT_UNIT, u / o.heads, u % o.heads, P.T, lane);
+      if (stamp) stamp[1] = clock64();
     } else if (o.type == DP_NOP) {
       // timing probe: a phase with no work (the cost of the phase boundary alone)
     } else {
@@ -853,10 +1004,11 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
 
 struct DpPlan {
   float2 *stats = nullptr;             // [128][DP_CL] row-statistics partials
+  DpAttnDev *attns = nullptr;          // attention operand maps, per attention op
   DpOpDev *ops = nullptr;
   DpGemmDev *gemms = nullptr;
   long long *trace = nullptr;          // AURAS_DPT_TRACE: per-phase timestamps of the last run
-  int n_ops = 0, n_gemms = 0, T = 16;
+  int n_ops = 0, n_gemms = 0, T = 16, heads = 0;   // (heads: the most of any attention op)
 };
 
 // Residual slice map: [rows][N] bf16 with row pitch ld, box {ncta, 128}, no swizzle (row-major
@@ -872,6 +1024,25 @@ static int dp_map_res(CUtensorMap *tm, const void *base, int N, int ld, int rows
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) { set_error("dpt_persist residual map: CUresult %d", (int)r); return AURAS_E_CUDA; }
+  return AURAS_OK;
+}
+
+// [rows][cols] bf16 with row pitch ld (elements), box {64, box_rows}, 128B swizzle.
+static int dp_map_pitch(CUtensorMap *tm, const void *base, int cols, int ld, int rows, int box_rows) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return AURAS_E_CUDA; }
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * 2) % 16) {
+    set_error("dpt_persist map: unaligned operand");
+    return AURAS_E_ARG;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("dpt_persist map: CUresult %d", (int)r); return AURAS_E_CUDA; }
   return AURAS_OK;
 }
 
@@ -948,6 +1119,7 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
   }
   std::vector<DpOpDev> ho(n_ops);
   int nln[2] = {0, 0}, nres[2] = {0, 0}, ng[2] = {0, 0}, nj[2] = {0, 0};   // [CTAs 1..] / [CTA 0]
+  int natt = 0;
   for (int i = 0; i < n_ops; ++i) {
     const auras_dpt_op &s = ops[i];
     DpOpDev &d = ho[i];
@@ -960,6 +1132,10 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
     d.v = static_cast<const __nv_bfloat16 *>(s.v);
     d.ldi = s.ldi; d.ldo = s.ldo; d.ldk = s.ldk; d.ldv = s.ldv;
     d.nk = s.nk; d.mask_off = s.mask_off; d.heads = s.heads; d.dh = s.dh;
+    if (s.type == DP_ATTN) {
+      d.par[0] = d.par[1] = (natt & 1) << 3;
+      ++natt;
+    }
     if (s.type == DP_GEMM && s.gemm >= 0 && s.gemm < n_gemms) {
       const DpGemmDev &gg = hg[s.gemm];
       for (int c = 0; c < 2; ++c) {
@@ -978,6 +1154,26 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
       set_error("dpt_persist_build: op %d", i);
       return AURAS_E_ARG;
     }
+  }
+  std::vector<DpAttnDev> ha;
+  int max_heads = 0;
+  for (int i = 0; i < n_ops; ++i) {
+    if (ops[i].type != DP_ATTN) continue;
+    const auras_dpt_op &s = ops[i];
+    if (s.qrows < 1 || s.krows < 1 || s.heads * 64 > s.ldi || s.heads * 64 > s.ldk || s.ldk != s.ldv ||
+        s.nk < 1 || s.nk > 16) {
+      set_error("dpt_persist_build: attention op %d (qrows %d krows %d)", i, s.qrows, s.krows);
+      return AURAS_E_ARG;
+    }
+    DpAttnDev a;
+    memset(&a, 0, sizeof(a));
+    if (int rc = dp_map_pitch(&a.tq, s.in, s.heads * 64, s.ldi, s.qrows, T)) return rc;
+    // (k / v boxes of 16 rows: slots >= nk hold neighbouring rows or zero fill, masked in the kernel)
+    if (int rc = dp_map_pitch(&a.tk, s.k, s.heads * 64, s.ldk, s.krows, 16)) return rc;
+    if (int rc = dp_map_pitch(&a.tv, s.v, s.heads * 64, s.ldv, s.krows, 16)) return rc;
+    ho[i].gemm = (int)ha.size();
+    max_heads = std::max(max_heads, s.heads);
+    ha.push_back(a);
   }
   {
     // Row-statistics handoff: a GEMM whose epilogue writes 16-column slices of a 256-wide
@@ -1004,15 +1200,18 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
   p->n_ops = n_ops;
   p->n_gemms = n_gemms;
   p->T = T;
+  p->heads = max_heads;
   if (cudaMalloc(&p->ops, sizeof(DpOpDev) * n_ops) != cudaSuccess ||
       cudaMalloc(&p->gemms, sizeof(DpGemmDev) * n_gemms) != cudaSuccess ||
-      cudaMalloc(&p->stats, sizeof(float2) * 128 * DP_CL) != cudaSuccess) {
+      cudaMalloc(&p->stats, sizeof(float2) * 128 * DP_CL) != cudaSuccess ||
+      cudaMalloc(&p->attns, sizeof(DpAttnDev) * std::max<size_t>(1, ha.size())) != cudaSuccess) {
     cudaFree(p->ops);
     cudaFree(p->gemms);
     delete p;
     return cuda_check(cudaGetLastError(), "dpt_persist alloc");
   }
   cudaMemset(p->stats, 0, sizeof(float2) * 128 * DP_CL);
+  if (!ha.empty()) cudaMemcpy(p->attns, ha.data(), sizeof(DpAttnDev) * ha.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(p->ops, ho.data(), sizeof(DpOpDev) * n_ops, cudaMemcpyHostToDevice);
   cudaMemcpy(p->gemms, hg.data(), sizeof(DpGemmDev) * n_gemms, cudaMemcpyHostToDevice);
   if (getenv("AURAS_DPT_TRACE")) {
@@ -1027,7 +1226,7 @@ int auras_dpt_persist_run(void *plan, int S, const float *eps, int eps_pitch, co
                           const int *steps, float *x_lanes, const float *noise_lanes, int lanes_per_agent,
                           int horizon, int adim, const auras_sched *sched, void *stream) {
   DpPlan *p = static_cast<DpPlan *>(plan);
-  if (!p || !sched || S < 1 || S * p->T > 128 || horizon != p->T) {
+  if (!p || !sched || S < 1 || S * p->T > 128 || horizon != p->T || S * p->heads > DP_ATT_SLOTS * DP_CL) {
     set_error("dpt_persist_run: bad arguments (S=%d)", S);
     return AURAS_E_ARG;
   }
@@ -1043,6 +1242,7 @@ int auras_dpt_persist_run(void *plan, int S, const float *eps, int eps_pitch, co
   memset(&P, 0, sizeof(P));
   P.trace = p->trace;
   P.stats = p->stats;
+  P.attns = p->attns;
   P.ops = p->ops; P.gemms = p->gemms; P.n_ops = p->n_ops; P.n_gemms = p->n_gemms; P.S = S; P.T = p->T;
   P.eps = eps; P.eps_pitch = eps_pitch;
   P.agents = agents; P.lanes = lanes; P.steps = steps;
@@ -1091,6 +1291,7 @@ void auras_dpt_persist_free(void *plan) {
   cudaFree(p->ops);
   cudaFree(p->gemms);
   cudaFree(p->stats);
+  cudaFree(p->attns);
   delete p;
 }
 

@@ -898,9 +898,10 @@ class DPTDenoiser:
             gemms.append(g)
             ops.append(_lib.DptOp(type=0, gemm=len(gemms) - 1))
 
-        def attn(q, ldq, k, v, ldk, nk, mask_off):
+        def attn(q, ldq, k, v, ldk, nk, mask_off, krows):
             ops.append(_lib.DptOp(type=2, inp=q, out=self.p_att.data_ptr(), k=k, v=v, ldi=ldq, ldo=E, ldk=ldk,
-                                  ldv=ldk, nk=nk, mask_off=mask_off, heads=self.H, dh=E // self.H))
+                                  ldv=ldk, nk=nk, mask_off=mask_off, heads=self.H, dh=E // self.H, qrows=R,
+                                  krows=krows))
 
         # h = input(x) + pos; every LayerNorm runs inside the GEMM phase that consumes it
         gemm(self.xin, 64, "dpt.input", res=self.pos_rep, out=self.p_h, ldo=E, cin_pad=64)
@@ -909,10 +910,11 @@ class DPTDenoiser:
             p = f"dpt.l{l}"
             gemm(None, E, p + ".sa_in", out=self.p_qkv, ldo=3 * E, ln=p + ".ln1")
             q0 = self.p_qkv.data_ptr()
-            attn(q0, 3 * E, q0 + 2 * E, q0 + 2 * 2 * E, 3 * E, T, 0)
+            attn(q0, 3 * E, q0 + 2 * E, q0 + 2 * 2 * E, 3 * E, T, 0, R)
             gemm(self.p_att, E, p + ".sa_out", res=self.p_h, out=self.p_h, ldo=E)
             gemm(None, E, p + ".ca_in", rows=(0, E), out=self.p_q2, ldo=E, ln=p + ".ln2")
-            attn(self.p_q2.data_ptr(), E, kv + 2 * l * 2 * E, kv + 2 * (l * 2 * E + E), lkv, self.tc, 1)
+            attn(self.p_q2.data_ptr(), E, kv + 2 * l * 2 * E, kv + 2 * (l * 2 * E + E), lkv, self.tc, 1,
+                 self.kv2.shape[0] * self.kv2.shape[1])
             gemm(self.p_att, E, p + ".ca_out", res=self.p_h, out=self.p_h, ldo=E)
             gemm(None, E, p + ".ff1", out=self.p_ff, ldo=4 * E, act_fn=_lib.ACT_GELU, ln=p + ".ln3")
             gemm(self.p_ff, 4 * E, p + ".ff2", res=self.p_h, out=self.p_h, ldo=E)

@@ -63,4 +63,4 @@ if os.environ.get("AURAS_DPT_TRACE"):
             print(f"  op {oi} {name:9s}: " + " ".join(str(k[off + j] - r0) if k[off + j] else "-" for j in range(16)))
     for oi in (9, 10, 12, 13, 15):
         r0 = sub[oi][0]
-        print(f"  op {oi} attn-scores/ln-landed: {ks[oi][56] - r0 if ks[oi][56] else '-'} {ks[oi][57] - r0 if ks[oi][57] else '-'}")
+        print(f"  op {oi} attn-scores/attn-end/ln-landed: {ks[oi][56] - r0 if ks[oi][56] else '-'} {ks[oi][57] - r0 if ks[oi][57] else '-'}")
