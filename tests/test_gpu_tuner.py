@@ -60,7 +60,10 @@ def test_tuner_on_measured_device_throughput():
                         clock="device")
     thr = sorted(p.throughput for p in probe.evaluated)
     assert thr[0] > 0
-    req = _req(g["request"], throughput_requirement=float(np.median(thr)))
+    # the second search re-measures every point: a requirement between the slowest and the
+    # fastest with a margin both ways (the fastest points stay feasible under timing noise)
+    assert thr[-1] > 1.3 * thr[0], thr
+    req = _req(g["request"], throughput_requirement=float(np.sqrt(thr[0] * thr[-1])))
     res = grid_search(pol, _factory(g["env_frames"]), req, clock="device")
     assert 0 < len(res.ranked) <= len(res.evaluated)
     assert all(p.throughput >= req.throughput_requirement for p in res.ranked)
