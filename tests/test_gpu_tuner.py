@@ -52,20 +52,23 @@ def test_tuner_matches_reference_exactly():
 
 def test_tuner_on_measured_device_throughput():
     """clock="device": each grid point's throughput is actions/s of the real
-    kernels; a requirement between the slowest and fastest measured points
-    leaves a strict, non-empty feasible subset, ranked by tracking error."""
+    kernels.  The grid points of the toy policy run within ~10% of each other,
+    so the requirement is set clear of timing noise on both sides: below every
+    measured point (all feasible, ranked by tracking error) and above every
+    point (NoFeasibleConfig carrying the measured result)."""
     g = load("tuner")
     pol = make_conditioning_policy(**g["policy"])
     probe = grid_search(pol, _factory(g["env_frames"]), _req(g["request"], throughput_requirement=1e-9),
                         clock="device")
     thr = sorted(p.throughput for p in probe.evaluated)
     assert thr[0] > 0
-    # the second search re-measures every point: a requirement between the slowest and the
-    # fastest with a margin both ways (the fastest points stay feasible under timing noise)
-    assert thr[-1] > 1.3 * thr[0], thr
-    req = _req(g["request"], throughput_requirement=float(np.sqrt(thr[0] * thr[-1])))
+    req = _req(g["request"], throughput_requirement=0.5 * thr[0])
     res = grid_search(pol, _factory(g["env_frames"]), req, clock="device")
     assert 0 < len(res.ranked) <= len(res.evaluated)
     assert all(p.throughput >= req.throughput_requirement for p in res.ranked)
     errs = [p.mean_error for p in res.ranked]
     assert errs == sorted(errs)
+    with pytest.raises(NoFeasibleConfig) as exc:
+        grid_search(pol, _factory(g["env_frames"]), _req(g["request"], throughput_requirement=3.0 * thr[-1]),
+                    clock="device")
+    assert len(exc.value.result.evaluated) == len(probe.evaluated)
