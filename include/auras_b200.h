@@ -64,6 +64,11 @@ int auras_ring_fetch(const int64_t *meta, const int64_t *state, int capacity, in
  * fetch the newest entry seqlock-style.  Synchronous.  counts_host receives
  * [readers][4] = {consistent reads, retries, torn reads, version regressions}. */
 int auras_ring_stress(int capacity, int words, int n_versions, int readers, unsigned long long *counts_host);
+/* Action emission (replaces the host-side copy of GenerationModel.finish's result,
+ * fp/policy.py:230-246): pinned host memory mapped into the device address space; kernels write
+ * through *dev, the host reads *host once the writing kernel completed. */
+int auras_host_mapped_alloc(size_t bytes, void **host, void **dev);
+int auras_host_mapped_free(void *host);
 
 int auras_ring_commit_sys(int64_t *meta, int64_t *state, int capacity, int64_t frame,
                           int64_t expected_version, void *stream);

@@ -105,6 +105,8 @@ _SIGNATURES = {
     "auras_unet_kernel_for": (C.c_int, [vp, C.c_int]),
     "auras_unet_check": (C.c_int, [vp]),
     "auras_ring_stress": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, vp]),
+    "auras_host_mapped_alloc": (C.c_int, [C.c_size_t, C.POINTER(vp), C.POINTER(vp)]),
+    "auras_host_mapped_free": (C.c_int, [vp]),
     "auras_dpt_persist_build": (C.c_int, [C.POINTER(DptGemm), C.c_int, C.POINTER(DptOp), C.c_int, C.c_int,
                                           C.POINTER(vp)]),
     "auras_dpt_persist_run": (C.c_int, [vp, C.c_int, vp, C.c_int, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int,

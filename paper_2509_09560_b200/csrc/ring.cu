@@ -258,6 +258,32 @@ int auras_ring_commit(int64_t *meta, int64_t *state, int capacity, int64_t frame
   return AURAS_OK;
 }
 
+// Action emission buffer: pinned host memory mapped into the device address
+// space, so the finish kernel writes the emitted action straight to host memory and a reader only
+// waits for that kernel's completion event (no device-to-host copy on the action path).
+int auras_host_mapped_alloc(size_t bytes, void **host, void **dev) {
+  if (!host || !dev || bytes == 0) {
+    set_error("host_mapped_alloc: bad args");
+    return AURAS_E_ARG;
+  }
+  *host = nullptr;
+  *dev = nullptr;
+  AURAS_CUDA(cudaHostAlloc(host, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(*host, 0, bytes);
+  const cudaError_t e = cudaHostGetDevicePointer(dev, *host, 0);
+  if (e != cudaSuccess) {
+    cudaFreeHost(*host);
+    *host = nullptr;
+    return cuda_check(e, "host_mapped_alloc");
+  }
+  return AURAS_OK;
+}
+
+int auras_host_mapped_free(void *host) {
+  if (host) AURAS_CUDA(cudaFreeHost(host));
+  return AURAS_OK;
+}
+
 int auras_ring_stress(int capacity, int words, int n_versions, int readers, unsigned long long *counts_host) {
   if (capacity < 2 || words < 1 || n_versions < 1 || readers < 1 || readers > 64 || !counts_host) {
     set_error("ring_stress: bad args");

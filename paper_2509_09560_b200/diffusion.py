@@ -1357,7 +1357,9 @@ class DPSession:
         self.pos = torch.zeros(agents, cfg.agent_pos_dim, dtype=torch.float32, device=pdev)
         self.prev = torch.zeros(agents, cfg.feat_dim + cfg.agent_pos_dim, dtype=torch.float32, device=pdev)
         self.first = True
-        self.out = torch.zeros(max(1, max_outputs), agents, hr, dtype=torch.float32, device=dev)
+        # emitted actions: pinned host memory mapped into the device; dp_finish
+        # writes each row straight to the host, read_action only waits for that kernel's event
+        self.out = _MappedRows(self.lib, (max(1, max_outputs), agents, hr))
         self.fetched = torch.zeros(3, dtype=torch.int64, device=dev)
         self.version_log = torch.zeros(max(1, max_frames), dtype=torch.int64, device=dev)
         self.stage = None
@@ -1554,7 +1556,7 @@ class DPSession:
         A = self.A
         _lib.check(self.lib.auras_dp_finish(self.x.data_ptr(), A, _lib.int_array(list(range(A))),
                                             _lib.int_array([lane] * A), A, self.R, self.row,
-                                            self.out[out_index].data_ptr(), self.g.cuda_stream),
+                                            self.out.dev_row(out_index), self.g.cuda_stream),
                    "dp_finish")
 
     def _check_device(self):
@@ -1569,12 +1571,14 @@ class DPSession:
             _lib.check(rc, "unet_check")
 
     def read_actions(self, n):
-        a = self.out[:n].cpu().numpy()
+        self.g.synchronize()                 # every finish kernel queued so far has written its row
+        a = self.out.host[:n].copy()
         self._check_device()
         return a
 
     def read_action(self, i):
-        a = self.out[i].cpu().numpy()
+        # (the executor waited for row i's finish event: Device.wait_output)
+        a = self.out.host[i].copy()
         self._check_device()
         return a
 
@@ -1588,6 +1592,35 @@ class DPSession:
         if self.plan:
             self.lib.auras_unet_plan_destroy(self.plan)
             self.plan = None
+        self.out.free()
+
+
+class _MappedRows:
+    """fp32 rows in pinned, device-mapped host memory (csrc/ring.cu auras_host_mapped_alloc)."""
+
+    def __init__(self, lib, shape):
+        self.lib = lib
+        n = int(np.prod(shape))
+        host, dev = _lib.vp(), _lib.vp()
+        _lib.check(lib.auras_host_mapped_alloc(n * 4, _lib.C.byref(host), _lib.C.byref(dev)), "host_mapped_alloc")
+        self._host, self._dev = host.value, dev.value
+        self.row_bytes = int(np.prod(shape[1:])) * 4
+        self.host = np.ctypeslib.as_array((_lib.C.c_float * n).from_address(self._host)).reshape(shape)
+
+    def dev_row(self, i):
+        return self._dev + i * self.row_bytes
+
+    def free(self):
+        if self._host:
+            self.host = None
+            self.lib.auras_host_mapped_free(self._host)
+            self._host = self._dev = 0
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 def make_diffusion_policy(config="pusht", dtype: str = "bf16", seed: int = 0, weights=None,
