@@ -356,9 +356,17 @@ def _agents_and_envs(policy, env, agents):
 
 
 def _require_plugin(policy):
-    if not hasattr(policy, "open_session"):
-        raise ConfigInvalid("the B200 engine needs a B200 policy plugin (make_conditioning_policy "
-                            "or make_diffusion_policy from paper_2509_09560_b200)")
+    """The device plugins (open_session), or a reference-style duck-typed policy
+    (fp/policy.py:46-272 protocol) wrapped to run its callbacks on the host."""
+    if hasattr(policy, "open_session"):
+        return policy
+    from .policy import HostPolicy, is_reference_plugin
+    if is_reference_plugin(policy):
+        return HostPolicy(policy)
+    raise ConfigInvalid("the B200 engine needs a policy plugin: make_conditioning_policy / "
+                        "make_diffusion_policy / make_autoregressive_policy from paper_2509_09560_b200, "
+                        "or an object with the reference's perception (start / apply_layers / finalize) "
+                        "and generation (initial_state / step / finish) protocol")
 
 
 # ---------------------------------------------------------------- pipelined mode
@@ -368,7 +376,7 @@ def run_pipelined(cfg: PipelineConfig, policy, env, duration: int, *, clock: str
     """fp/executor.py:200-399 on the B200.  `env` may be one environment, a list
     (one per agent, batched into the same kernels), or None (synthetic
     observations from `frame_source(agent, frame)` when given)."""
-    _require_plugin(policy)
+    policy = _require_plugin(policy)
     cfg.validate(policy)
     if clock not in ("virtual", "device"):
         raise ConfigInvalid(f"unknown clock {clock!r}")
@@ -593,7 +601,7 @@ def run_sequential(policy, env, duration: int, frame_interval: Optional[float] =
                    frame_source=None, frame_hook=None) -> RunResult:
     """fp/executor.py:406-461 on the B200: one request at a time (depth 1);
     observations arriving while a request is in flight are dropped."""
-    _require_plugin(policy)
+    policy = _require_plugin(policy)
     if clock not in ("virtual", "device"):
         raise ConfigInvalid(f"unknown clock {clock!r}")
     _lib.load()
@@ -700,7 +708,7 @@ def run_parallel(policy, env, workers: int, duration: int, frame_interval: Optio
     dispatched (its context in its own ring slot), so its action is ready by
     the frame it lands.  With capacity 1 the jobs' device work is sequential
     -- the processor-sharing model's total throughput."""
-    _require_plugin(policy)
+    policy = _require_plugin(policy)
     if workers < 1:
         raise ConfigInvalid("need at least one worker")
     if clock not in ("virtual", "device"):
@@ -823,7 +831,7 @@ def run_decoupled(policy, env, duration: int, frame_interval: Optional[float] = 
     runs all n denoise iterations on G once a context derived from an unused
     observation exists.  The event order is the reference's (publish < start
     < finish at equal times)."""
-    _require_plugin(policy)
+    policy = _require_plugin(policy)
     if clock not in ("virtual", "device"):
         raise ConfigInvalid(f"unknown clock {clock!r}")
     _lib.load()

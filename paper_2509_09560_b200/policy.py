@@ -336,3 +336,128 @@ def make_autoregressive_policy(layer_costs=(14.0, 14.0), l_a: int = ACTION_TOKEN
                   generation=TokenGeneration(n_iterations=l_a, step_cost=decode_cost,
                                              prefill_cost=prefill_cost, decode_cost=decode_cost,
                                              max_action=max_action))
+
+
+# ---------------------------------------------------------------- reference-style plugins
+
+def is_reference_plugin(policy) -> bool:
+    """The reference's duck-typed plugin protocol (fp/policy.py:46-272): a
+    perception model with start / apply_layers / finalize and a generation
+    model with initial_state / step / finish."""
+    p, g = getattr(policy, "perception", None), getattr(policy, "generation", None)
+    return (p is not None and g is not None
+            and all(callable(getattr(p, m, None)) for m in ("start", "apply_layers", "finalize"))
+            and all(callable(getattr(g, m, None)) for m in ("initial_state", "step", "finish")))
+
+
+class HostPolicy:
+    """A reference-style policy object under the B200 engine.  The engine's
+    schedule, context ring bookkeeping, versions, streams and events are the
+    same as for the device plugins; the policy's own callbacks run on the host
+    in stream order (they are arbitrary Python: nothing here can move them onto
+    the GPU).  Use make_conditioning_policy / make_diffusion_policy /
+    make_autoregressive_policy for the device kernels."""
+
+    def __init__(self, policy):
+        self.ref = policy
+        self.perception = policy.perception
+        self.generation = policy.generation
+        kind = getattr(policy, "kind", ContextKind.CONDITIONING)
+        self.kind = ContextKind(getattr(kind, "value", kind))
+        # (no synthetic_observation: without an environment the executor makes the
+        #  reference's zero observation, fp/executor.py:142-143)
+
+    @property
+    def sequential_cost(self) -> float:
+        sc = getattr(self.ref, "sequential_cost", None)
+        if sc is not None:
+            return float(sc)
+        return float(self.perception.total_cost) + float(self.generation.total_cost)
+
+    def open_session(self, **kw):
+        return HostPluginSession(self, **kw)
+
+
+class HostPluginSession:
+    """The session protocol of the device plugins (ingest / perceive / publish /
+    fetch / generate / finish, fp/executor.py:256-380) over a reference-style
+    policy's callbacks.  Each call runs once the stream it is ordered on has
+    drained, so the host work observes the same ordering the device work
+    would.  Contexts live in a host ring indexed like the device ring."""
+
+    def __init__(self, policy, *, capacity, lanes, agents, max_outputs, max_frames,
+                 p_stream, g_stream, pp_perception=1):
+        import torch
+        if agents != 1:
+            raise ValueError("a reference-style policy runs one agent per session")
+        self.pol = policy
+        self.per, self.gen = policy.perception, policy.generation
+        self.p, self.g = p_stream, g_stream
+        dev = torch.device("cuda", torch.cuda.current_device())
+        # the executor's host mirror (reserve / resolve) of the ring; the payload stays unused
+        self.store = ContextStore(capacity, slot_elems=1, agents=1, dtype=torch.float64, device=dev)
+        self.obs = [None] * lanes
+        self.latent = [None] * lanes
+        self.state = [None] * lanes
+        self.slots = [None] * capacity           # (frame, version, context)
+        self.ctx = None
+        self.out = [None] * max(1, max_outputs)
+        self.version_log = np.zeros(max(1, max_frames), dtype=np.int64)
+
+    def ingest(self, t, lane, observations):
+        self.p.synchronize()
+        obs = observations[0]
+        self.obs[lane] = obs
+        self.latent[lane] = self.per.start(obs)
+        self.state[lane] = self.gen.initial_state(seed=t)
+
+    def perceive(self, lane, lo, hi):
+        self.p.synchronize()
+        self.latent[lane] = self.per.apply_layers(self.latent[lane], lo, hi)
+
+    def publish(self, lane, frame, slot, version):
+        self.p.synchronize()
+        ctx = self.per.finalize(self.latent[lane], self.obs[lane])
+        # fp/context.py:129-143 stamps the produced frame
+        if getattr(ctx, "produced_frame", frame) != frame and hasattr(ctx, "with_produced_frame"):
+            ctx = ctx.with_produced_frame(frame)
+        self.slots[slot] = (frame, version, ctx)
+
+    def republish(self, src_slot, slot, frame, version):
+        self.p.synchronize()
+        _, _, ctx = self.slots[src_slot]
+        self.slots[slot] = (frame, version, ctx)
+
+    def fetch(self, target, log_index):
+        self.g.synchronize()
+        entry = self.slots[target % len(self.slots)]
+        if entry is None or entry[0] != target:
+            from .errors import NotYetPublished
+            raise NotYetPublished(f"no context published for frame {target}")
+        self.version_log[log_index] = entry[1]
+        self.ctx = entry[2]
+
+    def generate(self, batch):
+        self.g.synchronize()
+        for lane, _start, iters in batch:
+            for _ in range(iters):
+                self.state[lane] = self.gen.step(self.state[lane], self.ctx)
+
+    def finish(self, lane, out_index):
+        self.g.synchronize()
+        self.out[out_index] = tuple(self.gen.finish(self.state[lane]).values)
+
+    def read_actions(self, n):
+        return [[self.out[i]] for i in range(n)]
+
+    def read_action(self, i):
+        return [self.out[i]]
+
+    def read_version_log(self, n):
+        return self.version_log[:n].copy()
+
+    def action_values(self, row):
+        return tuple(row)
+
+    def close(self):
+        pass
