@@ -1283,9 +1283,8 @@ class DPSession:
     def __init__(self, policy, *, capacity, lanes, agents, max_outputs, max_frames,
                  p_stream, g_stream, pp_perception=1):
         import torch
-        if pp_perception != 1:
-            raise ConfigInvalid("the DP plugin runs its encoder as one perception stage "
-                                "(pp_perception = 1, the paper's depth sweep)")
+        if pp_perception < 1:
+            raise ConfigInvalid("pp_perception must be positive")
         self.torch = torch
         self.lib = _lib.load()
         gen: DPGeneration = policy.generation
@@ -1314,8 +1313,14 @@ class DPSession:
         self.slot_floats = self.gc_pad + F
         self.store = ContextStore(capacity, slot_elems=self.slot_floats, agents=agents,
                                   dtype=torch.float32, device=dev)
+        # staged perception (fp/executor.py:273-291): up to pp_perception requests are in
+        # flight in the encoder at once, each mid-way through its layer groups, so each
+        # gets its own activation set (round-robin at ingest; weights are shared)
         with torch.cuda.device(self.pd):
-            self.encoder = (ViTEncoder if cfg.encoder == "vit_b16" else Encoder)(self.pmodel, agents)
+            enc_cls = ViTEncoder if cfg.encoder == "vit_b16" else Encoder
+            self.encoders = [enc_cls(self.pmodel, agents) for _ in range(pp_perception)]
+        self.encoder = self.encoders[0]
+        self._enc_of, self._n_ingest = {}, 0
         s_max = agents * max(1, lanes)
         s_max = min(s_max, 64)
         sched = scheduler_tables(cfg)
@@ -1354,7 +1359,9 @@ class DPSession:
         if cfg.scheduler == "ddpm":
             self.noise = torch.zeros(agents, lanes, cfg.num_inference_steps, hr, dtype=torch.float32,
                                      device=dev)
-        self.pos = torch.zeros(agents, cfg.agent_pos_dim, dtype=torch.float32, device=pdev)
+        self.pos_k = [torch.zeros(agents, cfg.agent_pos_dim, dtype=torch.float32, device=pdev)
+                      for _ in range(len(self.encoders))]
+        self.pos = self.pos_k[0]
         self.prev = torch.zeros(agents, cfg.feat_dim + cfg.agent_pos_dim, dtype=torch.float32, device=pdev)
         self.first = True
         # emitted actions: pinned host memory mapped into the device; dp_finish
@@ -1415,13 +1422,17 @@ class DPSession:
         if len(observations) != self.A:
             raise ShapeMismatch(f"{len(observations)} observations for {self.A} agents")
         lane_stream = self.g if self.disagg else self.p
+        k = self._n_ingest % len(self.encoders)
+        self._n_ingest += 1
+        self._enc_of[lane] = k
+        enc, pos_buf = self.encoders[k], self.pos_k[k]
         if observations[0].image is None:
             if self.resident is None:
                 raise ShapeMismatch("observation without an image and no resident inputs")
             r, i = self.resident, t % self.resident["n"]
             with torch.cuda.stream(self.p):
-                self.encoder.img.copy_(r["img"][i], non_blocking=True)
-                self.pos.copy_(r["pos"][i], non_blocking=True)
+                enc.img.copy_(r["img"][i], non_blocking=True)
+                pos_buf.copy_(r["pos"][i], non_blocking=True)
             with torch.cuda.stream(lane_stream):
                 self.x[:, lane].copy_(r["x"][i], non_blocking=True)
                 if self.noise is not None:
@@ -1434,8 +1445,8 @@ class DPSession:
         if pos.shape[1] != cfg.agent_pos_dim:
             raise ShapeMismatch(f"agent_pos width {pos.shape[1]} != {cfg.agent_pos_dim}")
         with torch.cuda.stream(self.p):
-            self.encoder.img.copy_(torch.from_numpy(imgs).pin_memory(), non_blocking=True)
-            self.pos.copy_(torch.from_numpy(pos).pin_memory(), non_blocking=True)
+            enc.img.copy_(torch.from_numpy(imgs).pin_memory(), non_blocking=True)
+            pos_buf.copy_(torch.from_numpy(pos).pin_memory(), non_blocking=True)
         xs, zs = [], []
         for a in range(self.A):
             xT, z = request_noise(cfg, self.gen.seed, a, t)
@@ -1449,7 +1460,7 @@ class DPSession:
 
     def perceive(self, lane, lo, hi):
         with self.torch.cuda.device(self.pd):
-            self.encoder.run(lo, hi, self.p)
+            self.encoders[self._enc_of.get(lane, 0)].run(lo, hi, self.p)
 
     def publish(self, lane, frame, slot, version):
         st = self.store
@@ -1460,8 +1471,9 @@ class DPSession:
                 base, stride = self.stage.data_ptr(), self.slot_floats
             else:
                 base, stride = ring, ring_stride
+            k = self._enc_of.get(lane, 0)
             _lib.check(self.lib.auras_dp_assemble_cond(
-                self.encoder.feat.data_ptr(), self.pos.data_ptr(), self.prev.data_ptr(), self.A,
+                self.encoders[k].feat.data_ptr(), self.pos_k[k].data_ptr(), self.prev.data_ptr(), self.A,
                 self.cfg.feat_dim, self.cfg.agent_pos_dim, self.cfg.n_obs_steps, int(self.first), base,
                 stride, self.p.cuda_stream), "assemble_cond")
             self.first = False

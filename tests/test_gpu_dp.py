@@ -50,7 +50,7 @@ def rel_err(got, want):
 
 
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
-@pytest.mark.parametrize("pp,off", [((1, 2), 0), ((1, 2), -1), ((1, 4), 0)])
+@pytest.mark.parametrize("pp,off", [((1, 2), 0), ((1, 2), -1), ((1, 4), 0), ((2, 2), 0), ((3, 2), -1)])
 def test_tiny_pipelined_matches_oracle(dtype, pp, off):
     pol = D.make_diffusion_policy("tiny", dtype=dtype, weights=weights("tiny"))
     cfg = dict(pp_perception=pp[0], pp_generation=pp[1], fetch_offset=off)

@@ -135,7 +135,8 @@ def test_vit_dpt_policy_pipelined_matches_oracle():
     pol = D.make_diffusion_policy("vit_dpt", dtype="bf16", weights=w)
     gen = pol.generation
     for cfg in (dict(pp_perception=1, pp_generation=2, fetch_offset=0),
-                dict(pp_perception=1, pp_generation=4, fetch_offset=-1)):
+                dict(pp_perception=1, pp_generation=4, fetch_offset=-1),
+                dict(pp_perception=2, pp_generation=2, fetch_offset=0)):      # staged ViT perception
         res = run_pipelined(PipelineConfig(**cfg), pol, None, 5)
         orc = dp_model.OracleDP(gen.weights, gen.cfg, gen.seed, 0, pol.perception.layer_costs, gen.step_cost)
         ref = osched.run_pipelined(cfg, orc, None, 5)
