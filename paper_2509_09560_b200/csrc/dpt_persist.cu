@@ -129,6 +129,7 @@ struct DpParams {
   int n_ops, n_gemms, S, T;
   int dbg;                   // AURAS_DPT_DBG timing variants (0 in production)
   int pf;                    // weight prefetch across phase barriers (0: only in the GEMM's own phase)
+  int mslices;               // CTAs that load (and multicast) a slice of each activation block
   float2 *stats;             // [128 rows][DP_CL slices] (mean, M2) of the residual stream's last writer
   // update
   const float *eps;
@@ -687,8 +688,9 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
           mbar_expect_tx(lnbar, 4 * DP_A_BYTES);
 #pragma unroll
           for (int kb = 0; kb < 4; ++kb)
-            dp_tma_mc(smem + kb * DP_A_BYTES + rank * DP_MROWS * 128, &P.gemms[o.gemm].tmA, lnbar, kb * 64,
-                      rank * DP_MROWS);
+            if (rank < P.mslices)
+              dp_tma_mc(smem + kb * DP_A_BYTES + rank * (128 / P.mslices) * 128, &P.gemms[o.gemm].tmA, lnbar,
+                        kb * 64, rank * (128 / P.mslices));
         }
         for (int kb = 0; kb < nkb; ++kb, ++ip) {
           while (bc.job <= ip) dp_issue_b(P, sops, sgm, bc, rank, smem, full, empty, true);
@@ -698,8 +700,9 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
             mbar_arrive(&full[st]);                   // A comes from the LayerNorm warps
           } else {
             mbar_expect_tx(&full[st], DP_A_BYTES);     // (all DP_CL slices, from every CTA)
-            dp_tma_mc(smem + st * DP_A_BYTES + rank * DP_MROWS * 128, &P.gemms[o.gemm].tmA, &full[st], kb * 64,
-                      rank * DP_MROWS);
+            if (rank < P.mslices)
+              dp_tma_mc(smem + st * DP_A_BYTES + rank * (128 / P.mslices) * 128, &P.gemms[o.gemm].tmA, &full[st],
+                        kb * 64, rank * (128 / P.mslices));
           }
           DP_KSTAMP(16 + kb, kb < 16);
         }
@@ -1005,6 +1008,17 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
 }
 #undef rows
 
+// CTAs loading a multicast slice of each activation block (AURAS_DPT_MSLICES: 1, 2, 4, 8 or 16)
+static int dp_mslices() {
+  static int m = -1;
+  if (m < 0) {
+    const char *e = getenv("AURAS_DPT_MSLICES");
+    m = e ? atoi(e) : DP_CL;
+    if (m < 1 || m > DP_CL || (DP_CL % m) || (128 % m)) m = DP_CL;
+  }
+  return m;
+}
+
 struct DpPlan {
   float2 *stats = nullptr;             // [128][DP_CL] row-statistics partials
   DpAttnDev *attns = nullptr;          // attention operand maps, per attention op
@@ -1099,7 +1113,7 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
       return AURAS_E_ARG;
     }
     // A operand, or (LayerNorm'd A) the residual-stream rows the phase normalises in place
-    if (int rc = dp_map(&d.tmA, s.ln_g ? s.ln_src : s.act, s.K, s.act_rows, DP_MROWS)) return rc;
+    if (int rc = dp_map(&d.tmA, s.ln_g ? s.ln_src : s.act, s.K, s.act_rows, 128 / dp_mslices())) return rc;
     d.ln_src = static_cast<const __nv_bfloat16 *>(s.ln_src);
     d.ln_g = s.ln_g;
     d.ln_b = s.ln_b;
@@ -1256,6 +1270,7 @@ int auras_dpt_persist_run(void *plan, int S, const float *eps, int eps_pitch, co
     static int pf = -1;
     if (pf < 0) pf = getenv("AURAS_DPT_PF") ? atoi(getenv("AURAS_DPT_PF")) : 1;
     P.pf = pf;
+    P.mslices = dp_mslices();
     static int dbg = -1;
     if (dbg < 0) dbg = getenv("AURAS_DPT_DBG") ? atoi(getenv("AURAS_DPT_DBG")) : 0;
     P.dbg = dbg;
