@@ -664,6 +664,7 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();      // (a CTA barrier first: the metadata staging and the mbarrier inits)
   // cluster-wide: no CTA may multicast into (or arrive on) a peer's barriers before the peer
   // initialised them
   cluster_sync_all();
