@@ -356,7 +356,8 @@ typedef struct auras_dpt_gemm {
   const float *ln_g, *ln_b;
 } auras_dpt_gemm;
 typedef struct auras_dpt_op {
-  int type;                 /* 0 GEMM, 1 LayerNorm (E = 256), 2 attention, 3 scheduler update */
+  int type;                 /* 0 GEMM, 1 LayerNorm (E = 256), 2 attention, 3 scheduler update, 4 no-op,
+                               5 prep: the action tokens of every sample into out ([S T][64] bf16) */
   int gemm;                 /* GEMM: index into the gemm table */
   const void *in;           /* LN input rows / attention q */
   void *out;                /* LN output rows / attention output */
@@ -364,6 +365,9 @@ typedef struct auras_dpt_op {
   const void *k, *v;        /* attention keys / values: rows (s * nk + j) */
   int ldi, ldo, ldk, ldv, nk, mask_off, heads, dh;
   int qrows, krows;         /* attention: rows of the q buffer / of the k, v buffers (TMA bounds) */
+  const void *k2, *v2;      /* attention, gather = 1: k / v row 0 is row steps[s] of (k, v) (the time table),
+                               rows 1 .. nk - 1 are rows agents[s] * (nk - 1) .. of (k2, v2) (observation rows) */
+  int k2rows, gather;
 } auras_dpt_op;
 int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const auras_dpt_op *ops, int n_ops, int T,
                             void **plan);

@@ -52,7 +52,8 @@ class DptGemm(C.Structure):
 class DptOp(C.Structure):
     _fields_ = [("type", i32), ("gemm", i32), ("inp", vp), ("out", vp), ("g", vp), ("b", vp), ("k", vp), ("v", vp),
                 ("ldi", i32), ("ldo", i32), ("ldk", i32), ("ldv", i32), ("nk", i32), ("mask_off", i32),
-                ("heads", i32), ("dh", i32), ("qrows", i32), ("krows", i32)]
+                ("heads", i32), ("dh", i32), ("qrows", i32), ("krows", i32), ("k2", vp), ("v2", vp),
+                ("k2rows", i32), ("gather", i32)]
 
 
 class Sched(C.Structure):

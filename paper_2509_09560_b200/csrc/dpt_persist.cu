@@ -61,15 +61,17 @@ constexpr int DP_TMEM_COLS = 128;
 // phase barrier (barrier.cluster acquire) invalidates L1, so a per-phase read of the op
 // table from global memory would be an L2 round trip (~1 us) on the critical path of
 // every one of the ~67 phases.
-constexpr int DP_MAX_OPS = 96, DP_MAX_GEMMS = 56, DP_BIAS_SLAB = 3072;
+constexpr int DP_MAX_OPS = 88, DP_MAX_GEMMS = 56, DP_BIAS_SLAB = 3072;
 constexpr size_t DP_STAT_OFF = DP_BAR_OFF + 256;  // per-row (mean, rstd) of the tile a LayerNorm phase applies
-constexpr size_t DP_META_OFF = DP_STAT_OFF + 128 * 8;
-constexpr size_t DP_META_BYTES = (size_t)DP_MAX_OPS * 104 + DP_MAX_GEMMS * 96 + DP_BIAS_SLAB * 4;
+constexpr size_t DP_SAMP_OFF = DP_STAT_OFF + 128 * 8;   // agents / lanes / steps of the launch (<= 128 each)
+constexpr size_t DP_META_OFF = DP_SAMP_OFF + 3 * 128 * 4;
+constexpr size_t DP_META_BYTES = (size_t)DP_MAX_OPS * 112 + DP_MAX_GEMMS * 96 + DP_BIAS_SLAB * 4;
 constexpr size_t DP_SMEM = 1024 + DP_META_OFF + DP_META_BYTES;   // ring + LayerNorm'd A + barriers + metadata
+static_assert(DP_SMEM <= 232448, "dpt_persist shared memory");
 constexpr int DP_MAXK = 16;                   // keys per query (horizon <= 16; 3 cond tokens)
 constexpr int DP_E = 256;                     // embedding width (LayerNorm row)
 
-enum { DP_GEMM = 0, DP_LN = 1, DP_ATTN = 2, DP_UPDATE = 3, DP_NOP = 4 };
+enum { DP_GEMM = 0, DP_LN = 1, DP_ATTN = 2, DP_UPDATE = 3, DP_NOP = 4, DP_PREP = 5 };
 
 struct alignas(64) DpGemmDev {
   CUtensorMap tmA;           // activation [128][K] bf16, box {64, 128} (unless ln_g: A = LN(ln_src))
@@ -110,12 +112,16 @@ struct DpOpDev {
   // first ring job, [0] for CTAs 1.., [1] for CTA 0 (which also runs the single-CTA GEMMs);
   // host-computed so that no counter lives across phases (168 registers: it would be spilled)
   int par[2], job[2];
+  int gather;                // attention: k / v row 0 from the time table (by the sample's step), rows
+                             // 1 .. nk - 1 from the frame's observation rows (by its agent)
+  int pad_;
 };
-static_assert(sizeof(DpOpDev) == 104, "DpOpDev");
+static_assert(sizeof(DpOpDev) == 112, "DpOpDev");
 
 // Attention operand maps (128B-swizzled boxes {64, rows}: q {dh, T}, k / v {dh, nk}).
 struct alignas(64) DpAttnDev {
   CUtensorMap tq, tk, tv;
+  CUtensorMap tk2, tv2;      // gather mode: the observation rows (tk / tv: the time table, 1-row boxes)
 };
 constexpr int DP_ATT_UNIT = 3 * 2048;         // q, k, v tiles of one (sample, head) unit, <= 16 rows each
 constexpr int DP_ATT_SLOTS = 4;               // units per CTA (S * heads <= 4 * DP_CL)
@@ -612,8 +618,8 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
   uint64_t *attbar = resbar + 1;  // the attention tiles landed
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(attbar + 1);
   DpOpDev *sops = reinterpret_cast<DpOpDev *>(smem + DP_META_OFF);
-  DpGemmMeta *sgm = reinterpret_cast<DpGemmMeta *>(smem + DP_META_OFF + DP_MAX_OPS * 104);
-  float *sbias = reinterpret_cast<float *>(smem + DP_META_OFF + DP_MAX_OPS * 104 + DP_MAX_GEMMS * 96);
+  DpGemmMeta *sgm = reinterpret_cast<DpGemmMeta *>(smem + DP_META_OFF + DP_MAX_OPS * 112);
+  float *sbias = reinterpret_cast<float *>(smem + DP_META_OFF + DP_MAX_OPS * 112 + DP_MAX_GEMMS * 96);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = (int)cluster_ctarank();
 #define rows (P.S * P.T)      // (from the constant bank: not a register across the phase loop)
@@ -621,7 +627,7 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
     // ---- stage the program and this CTA's bias slices
     const uint64_t *src = reinterpret_cast<const uint64_t *>(P.ops);
     uint64_t *dst = reinterpret_cast<uint64_t *>(sops);
-    for (int i = threadIdx.x; i < P.n_ops * 13; i += DP_THREADS) dst[i] = src[i];
+    for (int i = threadIdx.x; i < P.n_ops * 14; i += DP_THREADS) dst[i] = src[i];
     for (int i = threadIdx.x; i < P.n_gemms; i += DP_THREADS) {
       const DpGemmDev &g = P.gemms[i];
       DpGemmMeta m;
@@ -640,7 +646,19 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
         sbias[g.boff + c] = n < g.N ? g.bias[n] : 0.f;
       }
     }
+    // the launch's samples, and zeroed attention tiles (a gathered k / v tile fills only its
+    // first nk rows; the masked rows must hold finite values for P V)
+    int *ssamp = reinterpret_cast<int *>(smem + DP_SAMP_OFF);
+    for (int i = threadIdx.x; i < P.S; i += DP_THREADS) {
+      ssamp[i] = P.agents[i];
+      ssamp[128 + i] = P.lanes[i];
+      ssamp[256 + i] = P.steps[i];
+    }
+    for (int i = threadIdx.x; i < DP_ATT_SLOTS * DP_ATT_UNIT / 16; i += DP_THREADS)
+      reinterpret_cast<uint4 *>(smem + DP_ATT_OFF)[i] = make_uint4(0, 0, 0, 0);
   }
+  const int *s_agent = reinterpret_cast<const int *>(smem + DP_SAMP_OFF);
+  const int *s_lane = s_agent + 128, *s_step = s_agent + 256;
   if (P.trace && rank == 0 && threadIdx.x == 0) {
     long long tn;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
@@ -717,14 +735,24 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
         const DpAttnDev &a = P.attns[o.gemm];
         const int units = P.S * o.heads;
         int bytes = 0;
-        for (int u = rank; u < units; u += DP_CL) bytes += (P.T + 2 * 16) * 128;
+        for (int u = rank; u < units; u += DP_CL) bytes += (P.T + 2 * (o.gather ? o.nk : 16)) * 128;
         mbar_expect_tx(attbar, bytes);                     // (0 bytes: a plain arrive)
         for (int u = rank, k = 0; u < units; u += DP_CL, ++k) {
           const int sidx = u / o.heads, h = u % o.heads;
           uint8_t *t = smem + DP_ATT_OFF + k * DP_ATT_UNIT;
           tma_load_2d(t, &a.tq, attbar, h * 64, sidx * P.T);
-          tma_load_2d(t + 2048, &a.tk, attbar, h * 64, sidx * o.nk);
-          tma_load_2d(t + 4096, &a.tv, attbar, h * 64, sidx * o.nk);
+          if (o.gather) {
+            // row 0: the time token of the sample's inference step; rows 1 ..: its agent's
+            // observation tokens (the 128B swizzle follows the shared-memory address)
+            const int step = s_step[sidx], obs0 = s_agent[sidx] * (o.nk - 1);
+            tma_load_2d(t + 2048, &a.tk, attbar, h * 64, step);
+            tma_load_2d(t + 2048 + 128, &a.tk2, attbar, h * 64, obs0);
+            tma_load_2d(t + 4096, &a.tv, attbar, h * 64, step);
+            tma_load_2d(t + 4096 + 128, &a.tv2, attbar, h * 64, obs0);
+          } else {
+            tma_load_2d(t + 2048, &a.tk, attbar, h * 64, sidx * o.nk);
+            tma_load_2d(t + 4096, &a.tv, attbar, h * 64, sidx * o.nk);
+          }
         }
       }
       __syncwarp();
@@ -963,13 +991,29 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
       if (warp < DP_ATT_SLOTS && u < P.S * o.heads)
         dp_attn_tile(o, smem + DP_ATT_OFF + warp * DP_ATT_UNIT, u / o.heads, u % o.heads, P.T, lane);
       if (stamp) stamp[1] = clock64();
+    } else if (o.type == DP_PREP) {
+      // ---- the action tokens of every sample from its request lane (dpt.cu dpt_prep_kernel):
+      //      out[s T + t][a] = bf16(x[t][a]) for a < adim, 0 up to 64 (the input GEMM's A)
+      const int items = P.S * P.T * 8;                     // (row, 8-column chunk)
+      for (int i = rank * DP_CT + threadIdx.x; i < items; i += DP_CL * DP_CT) {
+        const int r = i >> 3, c0 = (i & 7) * 8, sidx = r / P.T, t = r % P.T;
+        const float *x = P.x_lanes + ((int64_t)s_agent[sidx] * P.lanes_per_agent + s_lane[sidx]) * P.horizon * P.adim +
+                         t * P.adim;
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int a0 = c0 + 2 * k;
+          w[k] = dp_pack(a0 < P.adim ? x[a0] : 0.f, a0 + 1 < P.adim ? x[a0 + 1] : 0.f);
+        }
+        *reinterpret_cast<uint4 *>(o.out + (int64_t)r * 64 + c0) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
     } else if (o.type == DP_NOP) {
       // timing probe: a phase with no work (the cost of the phase boundary alone)
     } else {
       // ---- DDPM / DDIM update of sample s (dpt.cu dpt_update_kernel arithmetic)
       const auras_sched &sch = P.sched;
       for (int s = rank; s < P.S; s += DP_CL) {
-        const int agent = P.agents[s], ln = P.lanes[s], i = P.steps[s];
+        const int agent = s_agent[s], ln = s_lane[s], i = s_step[s];
         float *x = P.x_lanes + ((int64_t)agent * P.lanes_per_agent + ln) * P.horizon * P.adim;
         const float *z = P.noise_lanes ? P.noise_lanes + (((int64_t)agent * P.lanes_per_agent + ln) * sch.n_steps + i) *
                                                              P.horizon * P.adim
@@ -1150,6 +1194,7 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
     d.v = static_cast<const __nv_bfloat16 *>(s.v);
     d.ldi = s.ldi; d.ldo = s.ldo; d.ldk = s.ldk; d.ldv = s.ldv;
     d.nk = s.nk; d.mask_off = s.mask_off; d.heads = s.heads; d.dh = s.dh;
+    d.gather = s.type == DP_ATTN && s.gather;
     if (s.type == DP_ATTN) {
       d.par[0] = d.par[1] = (natt & 1) << 3;
       ++natt;
@@ -1168,7 +1213,7 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
       }
     }
     if ((s.type == DP_GEMM && (s.gemm < 0 || s.gemm >= n_gemms)) || (s.type == DP_ATTN && (s.nk > DP_MAXK || s.dh != 64)) ||
-        s.type < 0 || s.type > DP_NOP) {
+        s.type < 0 || s.type > DP_PREP) {
       set_error("dpt_persist_build: op %d", i);
       return AURAS_E_ARG;
     }
@@ -1179,16 +1224,24 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
     if (ops[i].type != DP_ATTN) continue;
     const auras_dpt_op &s = ops[i];
     if (s.qrows < 1 || s.krows < 1 || s.heads * 64 > s.ldi || s.heads * 64 > s.ldk || s.ldk != s.ldv ||
-        s.nk < 1 || s.nk > 16) {
+        s.nk < 1 || s.nk > 16 || (s.gather && (s.nk < 2 || !s.k2 || !s.v2 || s.k2rows < 1))) {
       set_error("dpt_persist_build: attention op %d (qrows %d krows %d)", i, s.qrows, s.krows);
       return AURAS_E_ARG;
     }
     DpAttnDev a;
     memset(&a, 0, sizeof(a));
     if (int rc = dp_map_pitch(&a.tq, s.in, s.heads * 64, s.ldi, s.qrows, T)) return rc;
-    // (k / v boxes of 16 rows: slots >= nk hold neighbouring rows or zero fill, masked in the kernel)
-    if (int rc = dp_map_pitch(&a.tk, s.k, s.heads * 64, s.ldk, s.krows, 16)) return rc;
-    if (int rc = dp_map_pitch(&a.tv, s.v, s.heads * 64, s.ldv, s.krows, 16)) return rc;
+    if (s.gather) {
+      // time table rows (one per sample, by inference step) + the agent's observation rows
+      if (int rc = dp_map_pitch(&a.tk, s.k, s.heads * 64, s.ldk, s.krows, 1)) return rc;
+      if (int rc = dp_map_pitch(&a.tv, s.v, s.heads * 64, s.ldv, s.krows, 1)) return rc;
+      if (int rc = dp_map_pitch(&a.tk2, s.k2, s.heads * 64, s.ldk, s.k2rows, s.nk - 1)) return rc;
+      if (int rc = dp_map_pitch(&a.tv2, s.v2, s.heads * 64, s.ldv, s.k2rows, s.nk - 1)) return rc;
+    } else {
+      // (k / v boxes of 16 rows: slots >= nk hold neighbouring rows or zero fill, masked in the kernel)
+      if (int rc = dp_map_pitch(&a.tk, s.k, s.heads * 64, s.ldk, s.krows, 16)) return rc;
+      if (int rc = dp_map_pitch(&a.tv, s.v, s.heads * 64, s.ldv, s.krows, 16)) return rc;
+    }
     ho[i].gemm = (int)ha.size();
     max_heads = std::max(max_heads, s.heads);
     ha.push_back(a);

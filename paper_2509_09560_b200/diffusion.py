@@ -898,11 +898,16 @@ class DPTDenoiser:
             gemms.append(g)
             ops.append(_lib.DptOp(type=0, gemm=len(gemms) - 1))
 
-        def attn(q, ldq, k, v, ldk, nk, mask_off, krows):
+        def attn(q, ldq, k, v, ldk, nk, mask_off, krows, k2=0, v2=0, k2rows=0):
             ops.append(_lib.DptOp(type=2, inp=q, out=self.p_att.data_ptr(), k=k, v=v, ldi=ldq, ldo=E, ldk=ldk,
                                   ldv=ldk, nk=nk, mask_off=mask_off, heads=self.H, dh=E // self.H, qrows=R,
-                                  krows=krows))
+                                  krows=krows, k2=k2, v2=v2, k2rows=k2rows, gather=int(bool(k2))))
 
+        # the action tokens from the request lanes (dpt_prep's per-iteration part), in-kernel
+        # (AURAS_DPT_INKERNEL_PREP=0: the separate dpt_prep / dpt_kv_gather launches, for A/B)
+        self.p_inprep = os.environ.get("AURAS_DPT_INKERNEL_PREP", "1") != "0"
+        if self.p_inprep:
+            ops.append(_lib.DptOp(type=5, out=self.xin.data_ptr()))
         # h = input(x) + pos; every LayerNorm runs inside the GEMM phase that consumes it
         gemm(self.xin, 64, "dpt.input", res=self.pos_rep, out=self.p_h, ldo=E, cin_pad=64)
         kv, lkv = self.kv2.data_ptr(), L * 2 * E
@@ -913,8 +918,16 @@ class DPTDenoiser:
             attn(q0, 3 * E, q0 + 2 * E, q0 + 2 * 2 * E, 3 * E, T, 0, R)
             gemm(self.p_att, E, p + ".sa_out", res=self.p_h, out=self.p_h, ldo=E)
             gemm(None, E, p + ".ca_in", rows=(0, E), out=self.p_q2, ldo=E, ln=p + ".ln2")
-            attn(self.p_q2.data_ptr(), E, kv + 2 * l * 2 * E, kv + 2 * (l * 2 * E + E), lkv, self.tc, 1,
-                 self.kv2.shape[0] * self.kv2.shape[1])
+            # cross-attention keys / values straight from the time-row table (by each sample's
+            # step) and the frame's observation rows (by agent): no per-iteration gather
+            kt, ko = self.kvt.data_ptr(), self.kvo.data_ptr()
+            if self.p_inprep:
+                attn(self.p_q2.data_ptr(), E, kt + 2 * l * 2 * E, kt + 2 * (l * 2 * E + E), lkv, self.tc, 1,
+                     self.kvt.shape[0], k2=ko + 2 * l * 2 * E, v2=ko + 2 * (l * 2 * E + E),
+                     k2rows=self.kvo.shape[0] * self.kvo.shape[1])
+            else:
+                attn(self.p_q2.data_ptr(), E, kv + 2 * l * 2 * E, kv + 2 * (l * 2 * E + E), lkv, self.tc, 1,
+                     self.kv2.shape[0] * self.kv2.shape[1])
             gemm(self.p_att, E, p + ".ca_out", res=self.p_h, out=self.p_h, ldo=E)
             gemm(None, E, p + ".ff1", out=self.p_ff, ldo=4 * E, act_fn=_lib.ACT_GELU, ln=p + ".ln3")
             gemm(self.p_ff, 4 * E, p + ".ff2", res=self.p_h, out=self.p_h, ldo=E)
@@ -952,6 +965,21 @@ class DPTDenoiser:
         cfg = self.m.cfg
         st = stream.cuda_stream
         E = self.E
+        if self.pplan and S * self.T <= 128:
+            # one launch: prep (action tokens), cross-attention rows by step / agent, the
+            # iteration's 67 phases and the scheduler update
+            if not self.p_inprep:
+                _lib.check(lib.auras_dpt_prep(agents, lanes, steps, S, x_lanes, lanes_per_agent, cfg.horizon,
+                                              cfg.action_dim, self.xin.data_ptr(), ring, ring_agent_stride,
+                                              slot_floats, fetched, self.tok_w, self.n_obs, self.gcbuf.data_ptr(),
+                                              self.gpad, self.temb.data_ptr(), E, self.c.data_ptr(),
+                                              self.cond_pos.data_ptr(), st), "dpt_prep")
+                self.memory_rows(S, agents, steps, stream)
+            _lib.check(lib.auras_dpt_persist_run(self.pplan, S, self.p_eps.data_ptr(), cfg.action_dim, agents, lanes,
+                                                 steps, x_lanes, noise_lanes, lanes_per_agent, cfg.horizon,
+                                                 cfg.action_dim, _lib.C.byref(sched), st), "dpt_persist_run")
+            self._last_persist = True
+            return
         _lib.check(lib.auras_dpt_prep(agents, lanes, steps, S, x_lanes, lanes_per_agent, cfg.horizon, cfg.action_dim,
                                       self.xin.data_ptr(), ring, ring_agent_stride, slot_floats, fetched, self.tok_w,
                                       self.n_obs, self.gcbuf.data_ptr(), self.gpad, self.temb.data_ptr(), E,
@@ -959,17 +987,19 @@ class DPTDenoiser:
         if self.hoist:
             _lib.check(lib.auras_dpt_kv_gather(self.kv2.data_ptr(), self.kvt.data_ptr(), self.kvo.data_ptr(), agents,
                                                steps, S, self.tc, self.kv2.shape[-1], st), "dpt_kv_gather")
-        if self.pplan and S * self.T <= 128:
-            _lib.check(lib.auras_dpt_persist_run(self.pplan, S, self.p_eps.data_ptr(), cfg.action_dim, agents, lanes,
-                                                 steps, x_lanes, noise_lanes, lanes_per_agent, cfg.horizon,
-                                                 cfg.action_dim, _lib.C.byref(sched), st), "dpt_persist_run")
-            self._last_persist = True
-            return
         self._run(self.prog if self.hoist else self.cond_prog + self.prog, S, st)
         self._last_persist = False
         _lib.check(lib.auras_dpt_update(self.eps_prog.data_ptr(), cfg.action_dim, agents, lanes, steps, S, x_lanes,
                                         noise_lanes, lanes_per_agent, cfg.horizon, cfg.action_dim, _lib.C.byref(sched),
                                         st), "dpt_update")
+
+    def memory_rows(self, S, agents, steps, stream):
+        """Diagnostics: the cross-attention K|V rows of S samples into kv2 (the
+        persistent kernel reads them from the tables directly)."""
+        if self.hoist:
+            _lib.check(_lib.load().auras_dpt_kv_gather(self.kv2.data_ptr(), self.kvt.data_ptr(), self.kvo.data_ptr(),
+                                                       agents, steps, S, self.tc, self.kv2.shape[-1],
+                                                       stream.cuda_stream), "dpt_kv_gather")
 
     def frame_cond(self, A, x_lanes, lanes_per_agent, ring, ring_agent_stride, slot_floats, fetched, stream):
         """Once per frame (hoisted mode): the observation rows' cross-attention

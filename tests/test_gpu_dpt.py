@@ -54,6 +54,7 @@ def _dpt_iteration(hoist, monkeypatch):
     den.iterate(S, t["agents"].data_ptr(), t["lanes"].data_ptr(), t["steps"].data_ptr(), t["x"].data_ptr(), 1,
                 t["ring"].data_ptr(), 2 * slot_floats, slot_floats, fetched.data_ptr(), t["noise"].data_ptr(), sc,
                 stream)
+    den.memory_rows(S, t["agents"].data_ptr(), t["steps"].data_ptr(), stream)
     torch.cuda.synchronize()
     return dict(cfg=cfg, w=w, S=S, steps=steps, x0=x0, noise=noise, gcs=gcs, sched=sched,
                 eps=den.eps[:S].cpu().numpy(), xs=t["x"].cpu().numpy(), kv=den.kv2[:S].float().cpu().numpy())
