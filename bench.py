@@ -303,6 +303,19 @@ def _reference_scheduler():
     return (lambda pol, env, n: osched.run_sequential(pol, env, n)), "oracle/schedule.py run_sequential"
 
 
+def _cpu_model():
+    """The host CPU model (BASELINE.md §3 asks for it beside the core count)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def cpu_oracle_sample(cfg_name, seconds, threads=None):
     """The reference CPU path for this workload on this host's cores: the
     reference scheduler driving the torch-CPU fp32 oracle network
@@ -331,6 +344,7 @@ def cpu_oracle_sample(cfg_name, seconds, threads=None):
         if el >= seconds:
             break
     return {"value": done / el, "unit": "actions/s", "cores": n, "kind": "port",
+            "cpu_model": _cpu_model(), "host_cpus": os.cpu_count(),
             "sample": f"{done} request(s) of the {cfg_name} policy (encoder + "
                       f"{cfg.num_inference_steps} denoise steps each) through {which} with the "
                       f"torch-CPU fp32 oracle network (oracle/dp_model.py), {el:.1f}s, torch "
