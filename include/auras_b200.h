@@ -357,7 +357,12 @@ typedef struct auras_dpt_gemm {
 } auras_dpt_gemm;
 typedef struct auras_dpt_op {
   int type;                 /* 0 GEMM, 1 LayerNorm (E = 256), 2 attention, 3 scheduler update, 4 no-op,
-                               5 prep: the action tokens of every sample into out ([S T][64] bf16) */
+                               5 prep: the action tokens of every sample into out ([S T][64] bf16),
+                               6 folded cross-attention block (auras_dpt_xfold tables): in = out = the
+                               residual stream [rows][ldi] bf16, updated in place, h += ca_out(MHA(LN(h), mem));
+                               k = the time-token table (float rows of ldk, row steps[s]), v = the
+                               observation table (float rows of ldv, rows agents[s] * (nk - 1) + j - 1),
+                               each pointing at the layer's block; nk <= 4 memory tokens, heads <= 4 */
   int gemm;                 /* GEMM: index into the gemm table */
   const void *in;           /* LN input rows / attention q */
   void *out;                /* LN output rows / attention output */
@@ -375,6 +380,22 @@ int auras_dpt_persist_run(void *plan, int S, const float *eps, int eps_pitch, co
                           const int *steps, float *x_lanes, const float *noise_lanes, int lanes_per_agent,
                           int horizon, int adim, const auras_sched *sched, void *stream);
 int auras_dpt_persist_trace(void *plan, long long *out, int n);   /* diagnostics (AURAS_DPT_TRACE) */
+/* Cross-attention folded into per-memory-token vectors (the memory has only
+ * 1 + n_obs tokens, so ca_in's query projection and ca_out fold into the keys
+ * and values): for every kv row r (bf16, layer l's K at l*2E, V at l*2E + E),
+ * layer l and head h, out[r][l] holds
+ *   a'[h][e] = ln_g[e] * sum_d Wq[h dh + d][e] k[h dh + d] / sqrt(dh)   (H x E)
+ *   U'[h][e] = sum_d Wo[e][h dh + d] v[h dh + d] + bo[e] / H             (H x E)
+ *   c'[h]    = sum_e ln_b[e] a[h][e] + sum_d bq[h dh + d] k[h dh + d] / sqrt(dh)
+ * (a block of xs >= 2 H E + H floats), so that with xhat the normalised
+ * residual row, score[h][j] = xhat . a'[h][j] + c'[h][j] and
+ * ca_out(attention) = sum_{h,j} p[h][j] U'[h][j].  wq: [L][E][E] (row = query
+ * channel), woT: [L][E][E] transposed (row = attention channel), bq, bo, ln_g,
+ * ln_b: [L][E]; all fp32.  Replaces the ca_in / cross-attention / ca_out
+ * GEMMs of nn.TransformerDecoderLayer (Diffusion Policy's TransformerForDiffusion). */
+int auras_dpt_xfold(const void *kv, int kv_ld, int rows, int L, int E, int H, const float *wq, const float *bq,
+                    const float *woT, const float *bo, const float *ln_g, const float *ln_b, float *out, int xs,
+                    void *stream);
 void auras_dpt_persist_free(void *plan);
 
 /* Assemble global_cond rows (the ContextStore.publish payload of the DP

@@ -114,6 +114,8 @@ _SIGNATURES = {
                                         C.POINTER(Sched), vp]),
     "auras_dpt_persist_free": (None, [vp]),
     "auras_dpt_persist_trace": (C.c_int, [vp, vp, C.c_int]),
+    "auras_dpt_xfold": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp, vp,
+                                  C.c_int, vp]),
     "auras_unet_launches_per_iter": (C.c_int, [vp]),
     "auras_conv": (C.c_int, [C.POINTER(ConvOp), C.c_int, C.c_int, vp, C.c_int, vp, i64, vp]),
     "auras_linear": (C.c_int, [C.POINTER(LinearOp), C.c_int, C.c_int, vp, C.c_int, vp, C.c_int, vp]),

@@ -71,7 +71,8 @@ static_assert(DP_SMEM <= 232448, "dpt_persist shared memory");
 constexpr int DP_MAXK = 16;                   // keys per query (horizon <= 16; 3 cond tokens)
 constexpr int DP_E = 256;                     // embedding width (LayerNorm row)
 
-enum { DP_GEMM = 0, DP_LN = 1, DP_ATTN = 2, DP_UPDATE = 3, DP_NOP = 4, DP_PREP = 5 };
+enum { DP_GEMM = 0, DP_LN = 1, DP_ATTN = 2, DP_UPDATE = 3, DP_NOP = 4, DP_PREP = 5, DP_XATTN = 6 };
+constexpr int DP_XK = 4, DP_XH = 4;           // folded cross-attention: memory tokens / heads (at most)
 
 struct alignas(64) DpGemmDev {
   CUtensorMap tmA;           // activation [128][K] bf16, box {64, 128} (unless ln_g: A = LN(ln_src))
@@ -280,6 +281,156 @@ __device__ __noinline__ void dp_attn_block(const DpOpDev &o, int q0, int q1, int
     qi += nq;
   }
   if (stamp) stamp[1] = clock64();
+}
+
+// ---- folded cross-attention block (DP_XATTN; tables from auras_dpt_xfold).
+// The decoder's memory is 1 + n_obs tokens, so the query projection folds into
+// the keys (score[h][j] = xhat . a'[h][j] + c'[h][j], the LayerNorm affine
+// included) and the output projection into the values (ca_out(attn) =
+// sum_{h,j} p[h][j] U'[h][j], ca_out's bias spread over U'): the ca_in GEMM,
+// the attention and the ca_out GEMM become one SIMT phase of 12 dot products
+// and 12 axpys per token row.  The CTA's 8 rows (one warp each) belong to one
+// sample (T % 8 == 0, checked at build): its nk table blocks are staged into
+// shared memory once (every load in flight at once: one L2 round trip after the
+// phase barrier), then each warp normalises its row, scores, softmaxes per head,
+// adds the combination to the residual in place and leaves the (mean, M2) slice
+// partials for the next LayerNorm (the GEMM epilogue's stats_out format).
+__device__ __noinline__ void dp_xattn(const DpOpDev &o, int r0, int rows, int T, const int *s_agent,
+                                      const int *s_step, float *stab, float2 *stats, int warp, int lane) {
+  const int H = o.heads, nk = o.nk;
+  const int SB = 2 * H * DP_E + 4;                   // staged floats per memory token (a', U', c', pad)
+  const int tid = warp * 32 + lane;
+  const int sidx = r0 / T;
+  const int step = s_step[sidx], obs0 = s_agent[sidx] * (nk - 1);
+  const int r = r0 + warp;
+  const bool live = r < rows;
+  const uint4 xr = live ? *reinterpret_cast<const uint4 *>(o.in + (int64_t)r * o.ldi + 8 * lane)
+                        : make_uint4(0, 0, 0, 0);
+  {
+    const int q4 = SB / 4, n4 = nk * q4;
+    constexpr int PER = (DP_XK * (2 * DP_XH * DP_E + 4) / 4 + DP_CT - 1) / DP_CT;
+    float4 tmp[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int i = tid + k * DP_CT;
+      if (i < n4) {
+        const int j = i / q4, c = i - j * q4;
+        const float *src = j == 0 ? reinterpret_cast<const float *>(o.k) + (int64_t)step * o.ldk
+                                  : reinterpret_cast<const float *>(o.v) + (int64_t)(obs0 + j - 1) * o.ldv;
+        tmp[k] = reinterpret_cast<const float4 *>(src)[c];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int i = tid + k * DP_CT;
+      if (i < n4) reinterpret_cast<float4 *>(stab)[i] = tmp[k];
+    }
+  }
+  named_sync(1, DP_CT);
+  if (!live) return;
+  const int t = r - sidx * T;
+  float x[8], xh[8];
+  {
+    const uint32_t xw[4] = {xr.x, xr.y, xr.z, xr.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&xw[i]));
+      x[2 * i] = f.x;
+      x[2 * i + 1] = f.y;
+    }
+  }
+  float sm = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sm += x[i];
+  const float mu = dp_wsum(sm) * (1.f / DP_E);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) q = fmaf(x[i] - mu, x[i] - mu, q);
+  const float rstd = rsqrtf(dp_wsum(q) * (1.f / DP_E) + 1e-5f);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) xh[i] = (x[i] - mu) * rstd;
+  // scores: lane partials over its 8 columns, then butterflies (every lane ends with all)
+  float sc[DP_XK * DP_XH];
+#pragma unroll
+  for (int j = 0; j < DP_XK; ++j)
+#pragma unroll
+    for (int h = 0; h < DP_XH; ++h) {
+      float a = 0.f;
+      if (j < nk && h < H) {
+        const float4 *ap = reinterpret_cast<const float4 *>(stab + j * SB + h * DP_E + 8 * lane);
+        const float4 a0 = ap[0], a1 = ap[1];
+        a = xh[0] * a0.x + xh[1] * a0.y + xh[2] * a0.z + xh[3] * a0.w + xh[4] * a1.x + xh[5] * a1.y + xh[6] * a1.z +
+            xh[7] * a1.w;
+      }
+      sc[j * DP_XH + h] = a;
+    }
+#pragma unroll
+  for (int off = 16; off; off >>= 1)
+#pragma unroll
+    for (int k = 0; k < DP_XK * DP_XH; ++k) sc[k] += __shfl_xor_sync(0xffffffffu, sc[k], off);
+  // per-head softmax over the visible memory tokens (key j visible iff j <= t + mask_off)
+  const int nv = min(nk, t + o.mask_off + 1);
+  float p[DP_XK * DP_XH];
+#pragma unroll
+  for (int h = 0; h < DP_XH; ++h) {
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < DP_XK; ++j) {
+      const int k = j * DP_XH + h;
+      sc[k] += (j < nk && h < H) ? stab[j * SB + 2 * H * DP_E + h] : 0.f;
+      if (j < nv) mx = fmaxf(mx, sc[k]);
+    }
+    float den = 0.f;
+#pragma unroll
+    for (int j = 0; j < DP_XK; ++j) {
+      const int k = j * DP_XH + h;
+      p[k] = (j < nv && h < H) ? __expf(sc[k] - mx) : 0.f;
+      den += p[k];
+    }
+    const float inv = h < H ? __fdividef(1.f, den) : 0.f;
+#pragma unroll
+    for (int j = 0; j < DP_XK; ++j) p[j * DP_XH + h] *= inv;
+  }
+  // h += sum p U' (bf16 residual stream, fp32 combination), in place
+  float y[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) y[i] = x[i];
+#pragma unroll
+  for (int j = 0; j < DP_XK; ++j)
+#pragma unroll
+    for (int h = 0; h < DP_XH; ++h) {
+      if (j >= nv || h >= H) continue;
+      const float pk = p[j * DP_XH + h];
+      const float4 *up = reinterpret_cast<const float4 *>(stab + j * SB + H * DP_E + h * DP_E + 8 * lane);
+      const float4 u0 = up[0], u1 = up[1];
+      y[0] = fmaf(pk, u0.x, y[0]); y[1] = fmaf(pk, u0.y, y[1]); y[2] = fmaf(pk, u0.z, y[2]); y[3] = fmaf(pk, u0.w, y[3]);
+      y[4] = fmaf(pk, u1.x, y[4]); y[5] = fmaf(pk, u1.y, y[5]); y[6] = fmaf(pk, u1.z, y[6]); y[7] = fmaf(pk, u1.w, y[7]);
+    }
+  uint32_t ow[4];
+  float f[8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __nv_bfloat162 h2 = __floats2bfloat162_rn(y[2 * i], y[2 * i + 1]);
+    ow[i] = *reinterpret_cast<const uint32_t *>(&h2);
+    const float2 g2 = __bfloat1622float2(h2);
+    f[2 * i] = g2.x;
+    f[2 * i + 1] = g2.y;
+  }
+  *reinterpret_cast<uint4 *>(o.out + (int64_t)r * o.ldo + 8 * lane) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+  // (mean, M2) of each 16-column slice of the stored row (lanes 2k, 2k + 1): the next
+  // LayerNorm'd GEMM combines them (stats_in)
+  float s8 = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s8 += f[i];
+  const float m8 = s8 * 0.125f;
+  float q8 = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) q8 = fmaf(f[i] - m8, f[i] - m8, q8);
+  const float mo = __shfl_xor_sync(0xffffffffu, m8, 1), qo = __shfl_xor_sync(0xffffffffu, q8, 1);
+  if (!(lane & 1)) {
+    const float d = mo - m8;
+    stats[r * DP_CL + (lane >> 1)] = make_float2(0.5f * (m8 + mo), q8 + qo + 4.f * d * d);
+  }
 }
 
 // Every CTA of the cluster needs the same activation block: each loads 128 / DP_CL of its rows and
@@ -1007,6 +1158,12 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
         }
         *reinterpret_cast<uint4 *>(o.out + (int64_t)r * 64 + c0) = make_uint4(w[0], w[1], w[2], w[3]);
       }
+    } else if (o.type == DP_XATTN) {
+      // table blocks staged in A-ring stages 4-5 (idle outside GEMM phases, like the attention tiles)
+      const int r0 = rank * (128 / DP_CL);
+      if (r0 < rows)
+        dp_xattn(o, r0, rows, P.T, s_agent, s_step, reinterpret_cast<float *>(smem + DP_ATT_OFF), P.stats, warp,
+                 lane);
     } else if (o.type == DP_NOP) {
       // timing probe: a phase with no work (the cost of the phase boundary alone)
     } else {
@@ -1062,6 +1219,46 @@ static int dp_mslices() {
     if (m < 1 || m > DP_CL || (DP_CL % m) || (128 % m)) m = DP_CL;
   }
   return m;
+}
+
+// ---- auras_dpt_xfold: one block per (kv row, layer, head), one thread per
+// embedding column e (coalesced reads of Wq's and Wo^T's rows).
+__global__ void dpt_xfold_kernel(const __nv_bfloat16 *kv, int kv_ld, int L, int E, int H, const float *wq,
+                                 const float *bq, const float *woT, const float *bo, const float *lng,
+                                 const float *lnb, float *out, int xs) {
+  extern __shared__ float xf_sh[];                 // k[dh], v[dh], warp partials[32]
+  const int r = blockIdx.x, l = blockIdx.y, h = blockIdx.z, e = threadIdx.x;
+  const int dh = E / H;
+  const __nv_bfloat16 *kr = kv + (int64_t)r * kv_ld + (int64_t)l * 2 * E + h * dh;
+  if (e < dh) {
+    xf_sh[e] = __bfloat162float(kr[e]);
+    xf_sh[dh + e] = __bfloat162float(kr[E + e]);
+  }
+  __syncthreads();
+  const float scale = rsqrtf((float)dh);
+  const float *wql = wq + (int64_t)l * E * E + (int64_t)h * dh * E;
+  const float *wol = woT + (int64_t)l * E * E + (int64_t)h * dh * E;
+  float a = 0.f, u = 0.f;
+  for (int d = 0; d < dh; ++d) {
+    a = fmaf(wql[(int64_t)d * E + e], xf_sh[d], a);
+    u = fmaf(wol[(int64_t)d * E + e], xf_sh[dh + d], u);
+  }
+  a *= scale;
+  float *o = out + ((int64_t)r * L + l) * xs;
+  o[h * E + e] = lng[l * E + e] * a;
+  o[H * E + h * E + e] = u + bo[l * E + e] / (float)H;
+  float c = lnb[l * E + e] * a + (e < dh ? bq[l * E + h * dh + e] * xf_sh[e] * scale : 0.f);
+  c = dp_wsum(c);
+  float *red = xf_sh + 2 * dh;
+  if ((e & 31) == 0) red[e >> 5] = c;
+  __syncthreads();
+  if (e == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (E + 31) / 32; ++w) t += red[w];
+    o[2 * H * E + h] = t;
+  }
+  if (h == 0)
+    for (int i = 2 * H * E + H + e; i < xs; i += E) o[i] = 0.f;   // pad (read by the float4 staging)
 }
 
 struct DpPlan {
@@ -1212,8 +1409,19 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
         nj[c] += gg.K / 64;
       }
     }
+    if (s.type == DP_XATTN) {
+      // one sample per CTA (8 rows), table blocks within A-ring stages 4-5, float4-aligned rows
+      const int SB = 2 * s.heads * DP_E + 4;
+      if (T % (128 / DP_CL) || s.nk < 1 || s.nk > DP_XK || s.heads < 1 || s.heads > DP_XH || s.mask_off < 0 ||
+          s.nk * SB * 4 > 2 * DP_A_BYTES || s.ldk % 4 || s.ldv % 4 || s.ldk < SB || (s.nk > 1 && s.ldv < SB) ||
+          s.ldi % 8 || s.ldo % 8 || !s.in || !s.out || !s.k || (s.nk > 1 && !s.v) ||
+          (reinterpret_cast<uintptr_t>(s.k) & 15) || (reinterpret_cast<uintptr_t>(s.v) & 15)) {
+        set_error("dpt_persist_build: folded cross-attention op %d (T=%d nk=%d heads=%d)", i, T, s.nk, s.heads);
+        return AURAS_E_ARG;
+      }
+    }
     if ((s.type == DP_GEMM && (s.gemm < 0 || s.gemm >= n_gemms)) || (s.type == DP_ATTN && (s.nk > DP_MAXK || s.dh != 64)) ||
-        s.type < 0 || s.type > DP_PREP) {
+        s.type < 0 || s.type > DP_XATTN) {
       set_error("dpt_persist_build: op %d", i);
       return AURAS_E_ARG;
     }
@@ -1345,6 +1553,22 @@ int auras_dpt_persist_run(void *plan, int S, const float *eps, int eps_pitch, co
   AURAS_CUDA(cudaLaunchKernelEx(&cfg, dpt_persist, P));
   return AURAS_OK;
 }
+
+int auras_dpt_xfold(const void *kv, int kv_ld, int rows, int L, int E, int H, const float *wq, const float *bq,
+                    const float *woT, const float *bo, const float *ln_g, const float *ln_b, float *out, int xs,
+                    void *stream) {
+  if (rows < 0 || L < 1 || H < 1 || E < 32 || E > 1024 || E % 32 || E % H || (E / H) > E || kv_ld < 2 * L * E ||
+      xs < 2 * H * E + 4 || xs % 4 || !kv || !wq || !bq || !woT || !bo || !ln_g || !ln_b || !out) {
+    set_error("dpt_xfold: bad arguments (E=%d H=%d L=%d xs=%d)", E, H, L, xs);
+    return AURAS_E_ARG;
+  }
+  if (rows == 0) return AURAS_OK;
+  const size_t sh = sizeof(float) * (2 * (E / H) + 32);
+  dpt_xfold_kernel<<<dim3(rows, L, H), E, sh, as_stream(stream)>>>(static_cast<const __nv_bfloat16 *>(kv), kv_ld, L,
+                                                                   E, H, wq, bq, woT, bo, ln_g, ln_b, out, xs);
+  return cuda_check(cudaGetLastError(), "dpt_xfold");
+}
+
 
 // Diagnostics (AURAS_DPT_TRACE set at build): per-phase globaltimer stamps of
 // the last run, n_ops + 1 values.  Returns the count copied.

@@ -818,6 +818,31 @@ class DPTDenoiser:
             self.kvo = z(s_max, self.n_obs, L * 2 * E)
             self.ar = torch.arange(s_max, dtype=torch.int32, device=dev)
             self.zr = torch.zeros(s_max, dtype=torch.int32, device=dev)
+        # Folded cross-attention (persistent path, AURAS_DPT_XFOLD=0 keeps the ca_in /
+        # attention / ca_out phases): the memory has only 1 + n_obs tokens, so per
+        # (memory token, layer, head) the query projection folds into the key and
+        # the output projection into the value (auras_dpt_xfold): the time-token
+        # vectors are tabled per inference step here, the observation tokens' once
+        # per frame (frame_cond)
+        self.xfold = (self.hoist and os.environ.get("AURAS_DPT_XFOLD", "1") == "1" and self.tc <= 4 and H <= 4
+                      and T % 8 == 0)
+        if self.xfold:
+            W = model.w
+
+            def f16(t):
+                return t.to(dev).to(td).float()
+
+            self.xs = 2 * H * E + 8
+            self.xw = dict(
+                wq=torch.stack([f16(W[f"dpt.l{l}.ca_in.w"][:E]) for l in range(L)]).contiguous(),
+                bq=torch.stack([W[f"dpt.l{l}.ca_in.b"][:E].to(dev).float() for l in range(L)]).contiguous(),
+                woT=torch.stack([f16(W[f"dpt.l{l}.ca_out.w"]).t() for l in range(L)]).contiguous(),
+                bo=torch.stack([W[f"dpt.l{l}.ca_out.b"].to(dev).float() for l in range(L)]).contiguous(),
+                g=torch.stack([W[f"dpt.l{l}.ln2.g"].to(dev).float() for l in range(L)]).contiguous(),
+                b=torch.stack([W[f"dpt.l{l}.ln2.b"].to(dev).float() for l in range(L)]).contiguous())
+            self.xt = torch.zeros(self.kvt.shape[0], L, self.xs, dtype=torch.float32, device=dev)
+            self.xo = torch.zeros(s_max * self.n_obs, L, self.xs, dtype=torch.float32, device=dev)
+            self._xfold(self.kvt, self.kvt.shape[0], self.xt, torch.cuda.current_stream(dev))
         fuse = os.environ.get("AURAS_DPT_FUSE_LN", "1") == "1"
 
         def lnp(g):
@@ -898,6 +923,13 @@ class DPTDenoiser:
             gemms.append(g)
             ops.append(_lib.DptOp(type=0, gemm=len(gemms) - 1))
 
+        def xattn(l):
+            """the folded cross-attention block of layer l (in place on the residual stream)"""
+            ops.append(_lib.DptOp(type=6, inp=self.p_h.data_ptr(), out=self.p_h.data_ptr(),
+                                  k=self.xt.data_ptr() + 4 * l * self.xs, v=self.xo.data_ptr() + 4 * l * self.xs,
+                                  ldi=E, ldo=E, ldk=L * self.xs, ldv=L * self.xs, nk=self.tc, mask_off=1,
+                                  heads=self.H, dh=E // self.H))
+
         def attn(q, ldq, k, v, ldk, nk, mask_off, krows, k2=0, v2=0, k2rows=0):
             ops.append(_lib.DptOp(type=2, inp=q, out=self.p_att.data_ptr(), k=k, v=v, ldi=ldq, ldo=E, ldk=ldk,
                                   ldv=ldk, nk=nk, mask_off=mask_off, heads=self.H, dh=E // self.H, qrows=R,
@@ -917,6 +949,11 @@ class DPTDenoiser:
             q0 = self.p_qkv.data_ptr()
             attn(q0, 3 * E, q0 + 2 * E, q0 + 2 * 2 * E, 3 * E, T, 0, R)
             gemm(self.p_att, E, p + ".sa_out", res=self.p_h, out=self.p_h, ldo=E)
+            if self.xfold and self.p_inprep:
+                xattn(l)
+                gemm(None, E, p + ".ff1", out=self.p_ff, ldo=4 * E, act_fn=_lib.ACT_GELU, ln=p + ".ln3")
+                gemm(self.p_ff, 4 * E, p + ".ff2", res=self.p_h, out=self.p_h, ldo=E)
+                continue
             gemm(None, E, p + ".ca_in", rows=(0, E), out=self.p_q2, ldo=E, ln=p + ".ln2")
             # cross-attention keys / values straight from the time-row table (by each sample's
             # step) and the frame's observation rows (by agent): no per-iteration gather
@@ -1017,6 +1054,16 @@ class DPTDenoiser:
         self._run(self.cond_prog, A, st)
         with self.m.torch.cuda.stream(stream):
             self.kvo[:A].copy_(self.kv2[:A, 1:])
+        if self.xfold:
+            self._xfold(self.kvo, A * self.n_obs, self.xo, stream)
+
+    def _xfold(self, kv, rows, out, stream):
+        """auras_dpt_xfold over `rows` K|V rows of kv into out [rows][L][xs]."""
+        x, E = self.xw, self.E
+        _lib.check(_lib.load().auras_dpt_xfold(kv.data_ptr(), kv.shape[-1], rows, self.m.cfg.dpt_layers, E, self.H,
+                                               x["wq"].data_ptr(), x["bq"].data_ptr(), x["woT"].data_ptr(),
+                                               x["bo"].data_ptr(), x["g"].data_ptr(), x["b"].data_ptr(),
+                                               out.data_ptr(), self.xs, stream.cuda_stream), "dpt_xfold")
 
     def _run(self, prog, S, st):
         lib = _lib.load()

@@ -195,3 +195,42 @@ def test_oracle_dpt_matches_torch_decoder_layers():
     h = torch.nn.functional.layer_norm(h[0], (E,), w["dpt.lnf.g"], w["dpt.lnf.b"])
     want = torch.nn.functional.linear(h, w["dpt.head.w"], w["dpt.head.b"])
     assert torch.allclose(got, want, atol=1e-4, rtol=1e-4), float((got - want).abs().max())
+
+
+def test_dpt_cross_attention_fold_algebra():
+    """The folded cross-attention of the persistent DP-T kernel (DP_XATTN phase,
+    auras_dpt_xfold tables; include/auras_b200.h) is the decoder layer's
+    h + ca_out(MHA(LN2(h), mem)) exactly, in exact arithmetic: query projection
+    and LayerNorm affine folded into per-(head, memory token) vectors a', c',
+    output projection and bias into U'.  Checked in fp64 against the oracle's
+    nn.MultiheadAttention restatement with TransformerForDiffusion's memory mask."""
+    import math
+    import torch
+    from oracle import dp_model
+    torch.manual_seed(0)
+    E, H, T, nk = 256, 4, 16, 3
+    dh = E // H
+    d = dict(dtype=torch.float64)
+    w_in, b_in = torch.randn(3 * E, E, **d) / 16, torch.randn(3 * E, **d) / 4
+    w_out, b_out = torch.randn(E, E, **d) / 16, torch.randn(E, **d) / 4
+    g, b = 1 + torch.randn(E, **d) / 4, torch.randn(E, **d) / 4
+    h = torch.randn(T, E, **d)
+    mem = torch.randn(nk, E, **d)
+    _, mmask = dp_model.dpt_masks(T, nk)
+    want = h + dp_model._mha(torch.nn.functional.layer_norm(h, (E,), g, b, 1e-5), mem, w_in, b_in, w_out, b_out, H,
+                             mmask.to(torch.float64))
+    # the fold (auras_dpt_xfold's formulas)
+    k = mem @ w_in[E:2 * E].T + b_in[E:2 * E]
+    v = mem @ w_in[2 * E:].T + b_in[2 * E:]
+    a = torch.einsum("hde,jhd->jhe", w_in[:E].reshape(H, dh, E), k.reshape(nk, H, dh)) / math.sqrt(dh)
+    a_p = a * g
+    c_p = (a * b).sum(-1) + (b_in[:E].reshape(H, dh) * k.reshape(nk, H, dh)).sum(-1) / math.sqrt(dh)
+    u_p = torch.einsum("ehd,jhd->jhe", w_out.reshape(E, H, dh), v.reshape(nk, H, dh)) + b_out / H
+    # the phase (dp_xattn): xhat, scores, masked per-head softmax, combination
+    xh = (h - h.mean(-1, keepdim=True)) / torch.sqrt(h.var(-1, unbiased=False, keepdim=True) + 1e-5)
+    sc = torch.einsum("te,jhe->thj", xh, a_p) + c_p.T[None]
+    vis = torch.arange(nk)[None, :] <= torch.arange(T)[:, None] + 1          # key j visible iff j <= t + 1
+    sc = sc.masked_fill(~vis[:, None, :], float("-inf"))
+    p = torch.softmax(sc, dim=-1)
+    got = h + torch.einsum("thj,jhe->te", p, u_p)
+    assert torch.allclose(got, want, rtol=1e-10, atol=1e-10), (got - want).abs().max()
