@@ -288,50 +288,64 @@ __device__ __noinline__ void dp_attn_block(const DpOpDev &o, int q0, int q1, int
 // the keys (score[h][j] = xhat . a'[h][j] + c'[h][j], the LayerNorm affine
 // included) and the output projection into the values (ca_out(attn) =
 // sum_{h,j} p[h][j] U'[h][j], ca_out's bias spread over U'): the ca_in GEMM,
-// the attention and the ca_out GEMM become one SIMT phase of 12 dot products
-// and 12 axpys per token row.  The CTA's 8 rows (one warp each) belong to one
-// sample (T % 8 == 0, checked at build): its nk table blocks are staged into
-// shared memory once (every load in flight at once: one L2 round trip after the
-// phase barrier), then each warp normalises its row, scores, softmaxes per head,
-// adds the combination to the residual in place and leaves the (mean, M2) slice
-// partials for the next LayerNorm (the GEMM epilogue's stats_out format).
+// the attention and the ca_out GEMM become one SIMT phase of 4 NK dot products
+// and 4 NK axpys per token row (4 heads).  The CTA's 8 rows (one warp each)
+// belong to one sample (T % 8 == 0, checked at build): its NK table blocks are
+// staged into shared memory once (every load in flight at once: one L2 round
+// trip after the phase barrier).  Lane l owns columns 4l..4l+3 and 128+4l..+3,
+// so every float4 table read of a warp is one contiguous 512-byte run (no bank
+// conflicts: 8 warps x the whole table is the phase's shared-memory traffic).
+// The 4 NK partial scores are summed by a transposing butterfly (16 shuffles:
+// lane l ends with the score of (j, h) = ((l >> 1) / 4, (l >> 1) % 4)), the
+// softmax over j runs across lanes l, l ^ 8, l ^ 16, l ^ 24, and the
+// probabilities are broadcast back for the combination.  The row is updated in
+// place; (mean, M2) slice partials go to the next LayerNorm'd GEMM (stats_in).
+template <int NK>
 __device__ __noinline__ void dp_xattn(const DpOpDev &o, int r0, int rows, int T, const int *s_agent,
-                                      const int *s_step, float *stab, float2 *stats, int warp, int lane) {
-  const int H = o.heads, nk = o.nk;
-  const int SB = 2 * H * DP_E + 4;                   // staged floats per memory token (a', U', c', pad)
+                                      const int *s_step, float *stab, float2 *stats, int warp, int lane,
+                                      long long *stamp) {
+  constexpr int H = DP_XH;                                     // (checked at build)
+  constexpr int SB = 2 * H * DP_E + 4;                         // staged floats per memory token (a', U', c', pad)
   const int tid = warp * 32 + lane;
   const int sidx = r0 / T;
-  const int step = s_step[sidx], obs0 = s_agent[sidx] * (nk - 1);
+  const int step = s_step[sidx], obs0 = s_agent[sidx] * (NK - 1);
   const int r = r0 + warp;
   const bool live = r < rows;
-  const uint4 xr = live ? *reinterpret_cast<const uint4 *>(o.in + (int64_t)r * o.ldi + 8 * lane)
-                        : make_uint4(0, 0, 0, 0);
+  const int q0 = 4 * lane, q1 = 128 + 4 * lane;
+  uint2 xa = make_uint2(0, 0), xb = make_uint2(0, 0);
+  if (live) {
+    xa = *reinterpret_cast<const uint2 *>(o.in + (int64_t)r * o.ldi + q0);
+    xb = *reinterpret_cast<const uint2 *>(o.in + (int64_t)r * o.ldi + q1);
+  }
   {
-    const int q4 = SB / 4, n4 = nk * q4;
-    constexpr int PER = (DP_XK * (2 * DP_XH * DP_E + 4) / 4 + DP_CT - 1) / DP_CT;
+    constexpr int Q4 = SB / 4, N4 = NK * Q4;
+    constexpr int PER = (N4 + DP_CT - 1) / DP_CT;
+    const float *tk = reinterpret_cast<const float *>(o.k) + (int64_t)step * o.ldk;
+    const float *tv = reinterpret_cast<const float *>(o.v) + (int64_t)obs0 * o.ldv;
     float4 tmp[PER];
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
       const int i = tid + k * DP_CT;
-      if (i < n4) {
-        const int j = i / q4, c = i - j * q4;
-        const float *src = j == 0 ? reinterpret_cast<const float *>(o.k) + (int64_t)step * o.ldk
-                                  : reinterpret_cast<const float *>(o.v) + (int64_t)(obs0 + j - 1) * o.ldv;
+      if (i < N4) {
+        const int j = i / Q4, c = i - j * Q4;
+        const float *src = j == 0 ? tk : tv + (int64_t)(j - 1) * o.ldv;
         tmp[k] = reinterpret_cast<const float4 *>(src)[c];
       }
     }
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
       const int i = tid + k * DP_CT;
-      if (i < n4) reinterpret_cast<float4 *>(stab)[i] = tmp[k];
+      if (i < N4) reinterpret_cast<float4 *>(stab)[i] = tmp[k];
     }
   }
+  if (stamp && tid == 0) stamp[0] = clock64();
   named_sync(1, DP_CT);
+  if (stamp && tid == 0) stamp[1] = clock64();
   if (!live) return;
   const int t = r - sidx * T;
   float x[8], xh[8];
   {
-    const uint32_t xw[4] = {xr.x, xr.y, xr.z, xr.w};
+    const uint32_t xw[4] = {xa.x, xa.y, xb.x, xb.y};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&xw[i]));
@@ -349,63 +363,78 @@ __device__ __noinline__ void dp_xattn(const DpOpDev &o, int r0, int rows, int T,
   const float rstd = rsqrtf(dp_wsum(q) * (1.f / DP_E) + 1e-5f);
 #pragma unroll
   for (int i = 0; i < 8; ++i) xh[i] = (x[i] - mu) * rstd;
-  // scores: lane partials over its 8 columns, then butterflies (every lane ends with all)
-  float sc[DP_XK * DP_XH];
+  // partial scores of the 16 (j, h) slots (slots j >= NK stay 0)
+  float v[16];
 #pragma unroll
-  for (int j = 0; j < DP_XK; ++j)
-#pragma unroll
-    for (int h = 0; h < DP_XH; ++h) {
-      float a = 0.f;
-      if (j < nk && h < H) {
-        const float4 *ap = reinterpret_cast<const float4 *>(stab + j * SB + h * DP_E + 8 * lane);
-        const float4 a0 = ap[0], a1 = ap[1];
-        a = xh[0] * a0.x + xh[1] * a0.y + xh[2] * a0.z + xh[3] * a0.w + xh[4] * a1.x + xh[5] * a1.y + xh[6] * a1.z +
-            xh[7] * a1.w;
-      }
-      sc[j * DP_XH + h] = a;
+  for (int k = 0; k < 16; ++k) {
+    const int j = k >> 2, h = k & 3;
+    float a = 0.f;
+    if (j < NK) {
+      const float *ap = stab + j * SB + h * DP_E;
+      const float4 a0 = *reinterpret_cast<const float4 *>(ap + q0);
+      const float4 a1 = *reinterpret_cast<const float4 *>(ap + q1);
+      a = xh[0] * a0.x + xh[1] * a0.y + xh[2] * a0.z + xh[3] * a0.w + xh[4] * a1.x + xh[5] * a1.y + xh[6] * a1.z +
+          xh[7] * a1.w;
     }
-#pragma unroll
-  for (int off = 16; off; off >>= 1)
-#pragma unroll
-    for (int k = 0; k < DP_XK * DP_XH; ++k) sc[k] += __shfl_xor_sync(0xffffffffu, sc[k], off);
-  // per-head softmax over the visible memory tokens (key j visible iff j <= t + mask_off)
-  const int nv = min(nk, t + o.mask_off + 1);
-  float p[DP_XK * DP_XH];
-#pragma unroll
-  for (int h = 0; h < DP_XH; ++h) {
-    float mx = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < DP_XK; ++j) {
-      const int k = j * DP_XH + h;
-      sc[k] += (j < nk && h < H) ? stab[j * SB + 2 * H * DP_E + h] : 0.f;
-      if (j < nv) mx = fmaxf(mx, sc[k]);
-    }
-    float den = 0.f;
-#pragma unroll
-    for (int j = 0; j < DP_XK; ++j) {
-      const int k = j * DP_XH + h;
-      p[k] = (j < nv && h < H) ? __expf(sc[k] - mx) : 0.f;
-      den += p[k];
-    }
-    const float inv = h < H ? __fdividef(1.f, den) : 0.f;
-#pragma unroll
-    for (int j = 0; j < DP_XK; ++j) p[j * DP_XH + h] *= inv;
+    v[k] = a;
   }
+  // transposing butterfly: after the xor-16/8/4/2 halvings lane l holds slot l >> 1 summed over
+  // its 16 lanes, the xor-1 step completes it
+  {
+    const bool b4 = lane & 16;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float send = b4 ? v[i] : v[i + 8];
+      const float keep = b4 ? v[i + 8] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+    const bool b3 = lane & 8;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float send = b3 ? v[i] : v[i + 4];
+      const float keep = b3 ? v[i + 4] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    const bool b2 = lane & 4;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float send = b2 ? v[i] : v[i + 2];
+      const float keep = b2 ? v[i + 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    const bool b1 = lane & 2;
+    {
+      const float send = b1 ? v[0] : v[1];
+      const float keep = b1 ? v[1] : v[0];
+      v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  }
+  if (stamp && tid == 0) stamp[2] = clock64();
+  // this lane's slot: memory token j = slot / 4 (visible iff j < NK and j <= t + mask_off), head slot % 4;
+  // the head's NK slots sit on lanes l, l ^ 8, l ^ 16, l ^ 24
+  const int slot = lane >> 1, jj = slot >> 2;
+  const bool vis = jj < NK && jj <= t + o.mask_off;
+  const float sc = vis ? v[0] + stab[jj * SB + 2 * H * DP_E + (slot & 3)] : -INFINITY;
+  float mx = fmaxf(sc, __shfl_xor_sync(0xffffffffu, sc, 8));
+  mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+  const float e = vis ? __expf(sc - mx) : 0.f;
+  float den = e + __shfl_xor_sync(0xffffffffu, e, 8);
+  den += __shfl_xor_sync(0xffffffffu, den, 16);
+  const float pr = e * __fdividef(1.f, den);                   // (den >= 1: the max contributes exp(0))
   // h += sum p U' (bf16 residual stream, fp32 combination), in place
   float y[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) y[i] = x[i];
 #pragma unroll
-  for (int j = 0; j < DP_XK; ++j)
-#pragma unroll
-    for (int h = 0; h < DP_XH; ++h) {
-      if (j >= nv || h >= H) continue;
-      const float pk = p[j * DP_XH + h];
-      const float4 *up = reinterpret_cast<const float4 *>(stab + j * SB + H * DP_E + h * DP_E + 8 * lane);
-      const float4 u0 = up[0], u1 = up[1];
-      y[0] = fmaf(pk, u0.x, y[0]); y[1] = fmaf(pk, u0.y, y[1]); y[2] = fmaf(pk, u0.z, y[2]); y[3] = fmaf(pk, u0.w, y[3]);
-      y[4] = fmaf(pk, u1.x, y[4]); y[5] = fmaf(pk, u1.y, y[5]); y[6] = fmaf(pk, u1.z, y[6]); y[7] = fmaf(pk, u1.w, y[7]);
-    }
+  for (int k = 0; k < 4 * NK; ++k) {
+    const float pk = __shfl_sync(0xffffffffu, pr, 2 * k);
+    const float *up = stab + (k >> 2) * SB + H * DP_E + (k & 3) * DP_E;
+    const float4 u0 = *reinterpret_cast<const float4 *>(up + q0);
+    const float4 u1 = *reinterpret_cast<const float4 *>(up + q1);
+    y[0] = fmaf(pk, u0.x, y[0]); y[1] = fmaf(pk, u0.y, y[1]); y[2] = fmaf(pk, u0.z, y[2]); y[3] = fmaf(pk, u0.w, y[3]);
+    y[4] = fmaf(pk, u1.x, y[4]); y[5] = fmaf(pk, u1.y, y[5]); y[6] = fmaf(pk, u1.z, y[6]); y[7] = fmaf(pk, u1.w, y[7]);
+  }
   uint32_t ow[4];
   float f[8];
 #pragma unroll
@@ -416,20 +445,30 @@ __device__ __noinline__ void dp_xattn(const DpOpDev &o, int r0, int rows, int T,
     f[2 * i] = g2.x;
     f[2 * i + 1] = g2.y;
   }
-  *reinterpret_cast<uint4 *>(o.out + (int64_t)r * o.ldo + 8 * lane) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
-  // (mean, M2) of each 16-column slice of the stored row (lanes 2k, 2k + 1): the next
-  // LayerNorm'd GEMM combines them (stats_in)
-  float s8 = 0.f;
+  *reinterpret_cast<uint2 *>(o.out + (int64_t)r * o.ldo + q0) = make_uint2(ow[0], ow[1]);
+  *reinterpret_cast<uint2 *>(o.out + (int64_t)r * o.ldo + q1) = make_uint2(ow[2], ow[3]);
+  if (stamp && tid == 0) stamp[3] = clock64();
+  // (mean, M2) of each 16-column slice of the stored row: slice lane / 4 from the first quads of
+  // lanes 4k..4k+3, slice 8 + lane / 4 from their second quads (equal-count Chan combinations)
+  float mq[2], qq[2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) s8 += f[i];
-  const float m8 = s8 * 0.125f;
-  float q8 = 0.f;
+  for (int u = 0; u < 2; ++u) {
+    const float m4 = 0.25f * (f[4 * u] + f[4 * u + 1] + f[4 * u + 2] + f[4 * u + 3]);
+    float q4 = 0.f;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) q8 = fmaf(f[i] - m8, f[i] - m8, q8);
-  const float mo = __shfl_xor_sync(0xffffffffu, m8, 1), qo = __shfl_xor_sync(0xffffffffu, q8, 1);
-  if (!(lane & 1)) {
-    const float d = mo - m8;
-    stats[r * DP_CL + (lane >> 1)] = make_float2(0.5f * (m8 + mo), q8 + qo + 4.f * d * d);
+    for (int i = 0; i < 4; ++i) q4 = fmaf(f[4 * u + i] - m4, f[4 * u + i] - m4, q4);
+    float mo = __shfl_xor_sync(0xffffffffu, m4, 1), qo = __shfl_xor_sync(0xffffffffu, q4, 1);
+    float d = mo - m4;
+    const float m8 = 0.5f * (m4 + mo), q8 = q4 + qo + 2.f * d * d;
+    mo = __shfl_xor_sync(0xffffffffu, m8, 2);
+    qo = __shfl_xor_sync(0xffffffffu, q8, 2);
+    d = mo - m8;
+    mq[u] = 0.5f * (m8 + mo);
+    qq[u] = q8 + qo + 4.f * d * d;
+  }
+  if (!(lane & 3)) {
+    stats[r * DP_CL + (lane >> 2)] = make_float2(mq[0], qq[0]);
+    stats[r * DP_CL + 8 + (lane >> 2)] = make_float2(mq[1], qq[1]);
   }
 }
 
@@ -1161,9 +1200,19 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
     } else if (o.type == DP_XATTN) {
       // table blocks staged in A-ring stages 4-5 (idle outside GEMM phases, like the attention tiles)
       const int r0 = rank * (128 / DP_CL);
-      if (r0 < rows)
-        dp_xattn(o, r0, rows, P.T, s_agent, s_step, reinterpret_cast<float *>(smem + DP_ATT_OFF), P.stats, warp,
-                 lane);
+      long long *stamp = P.trace && rank == 0 ? P.trace + 9 * P.n_ops + 1 + 64 * oi + 56 : nullptr;
+      if (stamp && threadIdx.x == 0) stamp[4] = clock64();
+      if (r0 < rows) {
+        float *stab = reinterpret_cast<float *>(smem + DP_ATT_OFF);
+        if (o.nk == 3)
+          dp_xattn<3>(o, r0, rows, P.T, s_agent, s_step, stab, P.stats, warp, lane, stamp);
+        else if (o.nk == 2)
+          dp_xattn<2>(o, r0, rows, P.T, s_agent, s_step, stab, P.stats, warp, lane, stamp);
+        else if (o.nk == 4)
+          dp_xattn<4>(o, r0, rows, P.T, s_agent, s_step, stab, P.stats, warp, lane, stamp);
+        else
+          dp_xattn<1>(o, r0, rows, P.T, s_agent, s_step, stab, P.stats, warp, lane, stamp);
+      }
     } else if (o.type == DP_NOP) {
       // timing probe: a phase with no work (the cost of the phase boundary alone)
     } else {
@@ -1412,7 +1461,7 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
     if (s.type == DP_XATTN) {
       // one sample per CTA (8 rows), table blocks within A-ring stages 4-5, float4-aligned rows
       const int SB = 2 * s.heads * DP_E + 4;
-      if (T % (128 / DP_CL) || s.nk < 1 || s.nk > DP_XK || s.heads < 1 || s.heads > DP_XH || s.mask_off < 0 ||
+      if (T % (128 / DP_CL) || s.nk < 1 || s.nk > DP_XK || s.heads != DP_XH || s.mask_off < 0 ||
           s.nk * SB * 4 > 2 * DP_A_BYTES || s.ldk % 4 || s.ldv % 4 || s.ldk < SB || (s.nk > 1 && s.ldv < SB) ||
           s.ldi % 8 || s.ldo % 8 || !s.in || !s.out || !s.k || (s.nk > 1 && !s.v) ||
           (reinterpret_cast<uintptr_t>(s.k) & 15) || (reinterpret_cast<uintptr_t>(s.v) & 15)) {

@@ -824,7 +824,7 @@ class DPTDenoiser:
         # the output projection into the value (auras_dpt_xfold): the time-token
         # vectors are tabled per inference step here, the observation tokens' once
         # per frame (frame_cond)
-        self.xfold = (self.hoist and os.environ.get("AURAS_DPT_XFOLD", "1") == "1" and self.tc <= 4 and H <= 4
+        self.xfold = (self.hoist and os.environ.get("AURAS_DPT_XFOLD", "1") == "1" and self.tc <= 4 and H == 4
                       and T % 8 == 0)
         if self.xfold:
             W = model.w

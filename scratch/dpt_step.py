@@ -64,3 +64,9 @@ if os.environ.get("AURAS_DPT_TRACE"):
     for oi in (9, 10, 12, 13, 15):
         r0 = sub[oi][0]
         print(f"  op {oi} attn-scores/attn-end/ln-landed: {ks[oi][56] - r0 if ks[oi][56] else '-'} {ks[oi][57] - r0 if ks[oi][57] else '-'}")
+    for oi in range(n_ops):
+        if ks[oi][60] and sub[oi][0]:
+            r0 = sub[oi][0]
+            print(f"  op {oi} xattn enter/staged/synced/scored/stored: " +
+                  " ".join(str(ks[oi][56 + j] - r0) if ks[oi][56 + j] else "-" for j in (4, 0, 1, 2, 3)))
+            break
