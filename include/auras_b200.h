@@ -362,7 +362,9 @@ typedef struct auras_dpt_op {
                                residual stream [rows][ldi] bf16, updated in place, h += ca_out(MHA(LN(h), mem));
                                k = the time-token table (float rows of ldk, row steps[s]), v = the
                                observation table (float rows of ldv, rows agents[s] * (nk - 1) + j - 1),
-                               each pointing at the layer's block; nk <= 4 memory tokens, heads == 4 */
+                               each pointing at the layer's block; nk <= 4 memory tokens, heads == 4;
+                               without g: out == in; with g, b: the row is written back to in and its
+                               LayerNorm(g, b) to out (bf16 [rows][ldo]), the A of a following plain GEMM */
   int gemm;                 /* GEMM: index into the gemm table */
   const void *in;           /* LN input rows / attention q */
   void *out;                /* LN output rows / attention output */

@@ -299,7 +299,9 @@ __device__ __noinline__ void dp_attn_block(const DpOpDev &o, int q0, int q1, int
 // lane l ends with the score of (j, h) = ((l >> 1) / 4, (l >> 1) % 4)), the
 // softmax over j runs across lanes l, l ^ 8, l ^ 16, l ^ 24, and the
 // probabilities are broadcast back for the combination.  The row is updated in
-// place; (mean, M2) slice partials go to the next LayerNorm'd GEMM (stats_in).
+// place; either (mean, M2) slice partials go to a following LayerNorm'd GEMM
+// (stats_in), or (o.g set) the warp, which holds the whole updated row, writes
+// its LayerNorm to o.out for a plain-A GEMM.
 template <int NK>
 __device__ __noinline__ void dp_xattn(const DpOpDev &o, int r0, int rows, int T, const int *s_agent,
                                       const int *s_step, float *stab, float2 *stats, int warp, int lane,
@@ -312,6 +314,17 @@ __device__ __noinline__ void dp_xattn(const DpOpDev &o, int r0, int rows, int T,
   const int r = r0 + warp;
   const bool live = r < rows;
   const int q0 = 4 * lane, q1 = 128 + 4 * lane;
+  // optional: the next LayerNorm (o.g, o.b) of the updated row into o.out -- the following GEMM
+  // then takes a plain A operand instead of normalising its tile in its own phase (affine loads
+  // issued now, off the critical path)
+  const bool lnout = o.g != nullptr;
+  float4 lg0 = make_float4(0.f, 0.f, 0.f, 0.f), lg1 = lg0, lb0 = lg0, lb1 = lg0;
+  if (lnout && live) {
+    lg0 = *reinterpret_cast<const float4 *>(o.g + q0);
+    lg1 = *reinterpret_cast<const float4 *>(o.g + q1);
+    lb0 = *reinterpret_cast<const float4 *>(o.b + q0);
+    lb1 = *reinterpret_cast<const float4 *>(o.b + q1);
+  }
   uint2 xa = make_uint2(0, 0), xb = make_uint2(0, 0);
   if (live) {
     xa = *reinterpret_cast<const uint2 *>(o.in + (int64_t)r * o.ldi + q0);
@@ -444,6 +457,34 @@ __device__ __noinline__ void dp_xattn(const DpOpDev &o, int r0, int rows, int T,
     const float2 g2 = __bfloat1622float2(h2);
     f[2 * i] = g2.x;
     f[2 * i + 1] = g2.y;
+  }
+  if (lnout) {
+    // the row back into the residual stream (in), its LayerNorm into out (fp32 statistics of the
+    // stored bf16 values, as the LayerNorm'd GEMM path computes them)
+    __nv_bfloat16 *hr = const_cast<__nv_bfloat16 *>(o.in) + (int64_t)r * o.ldi;
+    *reinterpret_cast<uint2 *>(hr + q0) = make_uint2(ow[0], ow[1]);
+    *reinterpret_cast<uint2 *>(hr + q1) = make_uint2(ow[2], ow[3]);
+    float s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s2 += f[i];
+    const float m2 = dp_wsum(s2) * (1.f / DP_E);
+    float v2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v2 = fmaf(f[i] - m2, f[i] - m2, v2);
+    const float rs2 = rsqrtf(dp_wsum(v2) * (1.f / DP_E) + 1e-5f);
+    const float ga[8] = {lg0.x, lg0.y, lg0.z, lg0.w, lg1.x, lg1.y, lg1.z, lg1.w};
+    const float ba[8] = {lb0.x, lb0.y, lb0.z, lb0.w, lb1.x, lb1.y, lb1.z, lb1.w};
+    uint32_t lw[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const __nv_bfloat162 h2 = __floats2bfloat162_rn((f[2 * i] - m2) * rs2 * ga[2 * i] + ba[2 * i],
+                                                      (f[2 * i + 1] - m2) * rs2 * ga[2 * i + 1] + ba[2 * i + 1]);
+      lw[i] = *reinterpret_cast<const uint32_t *>(&h2);
+    }
+    *reinterpret_cast<uint2 *>(o.out + (int64_t)r * o.ldo + q0) = make_uint2(lw[0], lw[1]);
+    *reinterpret_cast<uint2 *>(o.out + (int64_t)r * o.ldo + q1) = make_uint2(lw[2], lw[3]);
+    if (stamp && tid == 0) stamp[3] = clock64();
+    return;
   }
   *reinterpret_cast<uint2 *>(o.out + (int64_t)r * o.ldo + q0) = make_uint2(ow[0], ow[1]);
   *reinterpret_cast<uint2 *>(o.out + (int64_t)r * o.ldo + q1) = make_uint2(ow[2], ow[3]);
@@ -1463,7 +1504,8 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
       const int SB = 2 * s.heads * DP_E + 4;
       if (T % (128 / DP_CL) || s.nk < 1 || s.nk > DP_XK || s.heads != DP_XH || s.mask_off < 0 ||
           s.nk * SB * 4 > 2 * DP_A_BYTES || s.ldk % 4 || s.ldv % 4 || s.ldk < SB || (s.nk > 1 && s.ldv < SB) ||
-          s.ldi % 8 || s.ldo % 8 || !s.in || !s.out || !s.k || (s.nk > 1 && !s.v) ||
+          s.ldi % 8 || s.ldo % 8 || !s.in || !s.out || !s.k || (s.nk > 1 && !s.v) || (s.g && (!s.b || s.out == s.in)) ||
+          (!s.g && s.out != s.in) ||
           (reinterpret_cast<uintptr_t>(s.k) & 15) || (reinterpret_cast<uintptr_t>(s.v) & 15)) {
         set_error("dpt_persist_build: folded cross-attention op %d (T=%d nk=%d heads=%d)", i, T, s.nk, s.heads);
         return AURAS_E_ARG;
@@ -1514,6 +1556,11 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
     auto is_lsrc = [&](const void *q) { return std::find(lsrc.begin(), lsrc.end(), q) != lsrc.end(); };
     const void *valid = nullptr;
     for (int i = 0; i < n_ops; ++i) {
+      if (ops[i].type == DP_XATTN) {
+        // rewrites its residual rows: slice statistics only without the LayerNorm output
+        if (ops[i].g || ops[i].in != valid) valid = nullptr;
+        continue;
+      }
       if (ops[i].type != DP_GEMM) continue;
       DpGemmDev &d = hg[ops[i].gemm];
       if (d.ln_g) d.stats_in = valid && d.ln_src == valid;

@@ -923,12 +923,15 @@ class DPTDenoiser:
             gemms.append(g)
             ops.append(_lib.DptOp(type=0, gemm=len(gemms) - 1))
 
-        def xattn(l):
-            """the folded cross-attention block of layer l (in place on the residual stream)"""
-            ops.append(_lib.DptOp(type=6, inp=self.p_h.data_ptr(), out=self.p_h.data_ptr(),
-                                  k=self.xt.data_ptr() + 4 * l * self.xs, v=self.xo.data_ptr() + 4 * l * self.xs,
-                                  ldi=E, ldo=E, ldk=L * self.xs, ldv=L * self.xs, nk=self.tc, mask_off=1,
-                                  heads=self.H, dh=E // self.H))
+        def xattn(l, ln):
+            """the folded cross-attention block of layer l (in place on the residual stream),
+            with the following LayerNorm `ln` of the updated rows into p_ln"""
+            lg, lbb = lnp(ln)
+            keep.extend([lg, lbb])
+            ops.append(_lib.DptOp(type=6, inp=self.p_h.data_ptr(), out=self.p_ln.data_ptr(), g=lg.data_ptr(),
+                                  b=lbb.data_ptr(), k=self.xt.data_ptr() + 4 * l * self.xs,
+                                  v=self.xo.data_ptr() + 4 * l * self.xs, ldi=E, ldo=E, ldk=L * self.xs,
+                                  ldv=L * self.xs, nk=self.tc, mask_off=1, heads=self.H, dh=E // self.H))
 
         def attn(q, ldq, k, v, ldk, nk, mask_off, krows, k2=0, v2=0, k2rows=0):
             ops.append(_lib.DptOp(type=2, inp=q, out=self.p_att.data_ptr(), k=k, v=v, ldi=ldq, ldo=E, ldk=ldk,
@@ -950,8 +953,8 @@ class DPTDenoiser:
             attn(q0, 3 * E, q0 + 2 * E, q0 + 2 * 2 * E, 3 * E, T, 0, R)
             gemm(self.p_att, E, p + ".sa_out", res=self.p_h, out=self.p_h, ldo=E)
             if self.xfold and self.p_inprep:
-                xattn(l)
-                gemm(None, E, p + ".ff1", out=self.p_ff, ldo=4 * E, act_fn=_lib.ACT_GELU, ln=p + ".ln3")
+                xattn(l, p + ".ln3")
+                gemm(self.p_ln, E, p + ".ff1", out=self.p_ff, ldo=4 * E, act_fn=_lib.ACT_GELU)
                 gemm(self.p_ff, 4 * E, p + ".ff2", res=self.p_h, out=self.p_h, ldo=E)
                 continue
             gemm(None, E, p + ".ca_in", rows=(0, E), out=self.p_q2, ldo=E, ln=p + ".ln2")
