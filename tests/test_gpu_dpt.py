@@ -16,8 +16,9 @@ from paper_2509_09560_b200 import diffusion as D
 pytestmark = pytest.mark.gpu
 
 
-def _dpt_iteration(hoist, monkeypatch, xfold=True):
-    """One DP-T iteration of S = 5 samples at steps 0..99 on the device; returns
+def _dpt_iteration(hoist, monkeypatch, xfold=True, S=5):
+    """One DP-T iteration of S samples (5: a partial 128-row tile; 8: every
+    CTA of the persistent kernel has rows) at steps 0..99 on the device; returns
     (cfg, weights, inputs, eps, updated lanes, cross-attention time rows)."""
     monkeypatch.setenv("AURAS_DPT_HOIST", "1" if hoist else "0")
     monkeypatch.setenv("AURAS_DPT_XFOLD", "1" if xfold else "0")
@@ -25,11 +26,10 @@ def _dpt_iteration(hoist, monkeypatch, xfold=True):
                      denoiser="transformer")
     w = D.init_weights(cfg, 4, device="cpu")
     model = D.DeviceModel(cfg, w, "bf16")
-    S = 5
     den = D.DPTDenoiser(model, 8)
     rng = np.random.default_rng(1)
     T, A = cfg.horizon, cfg.action_dim
-    steps = np.array([0, 13, 50, 98, 99], dtype=np.int32)
+    steps = np.array([0, 13, 50, 98, 99, 1, 77, 42][:S], dtype=np.int32)
     agents = np.arange(S, dtype=np.int32)
     lanes = np.zeros(S, dtype=np.int32)
     x0 = rng.standard_normal((S, 1, T * A)).astype(np.float32)
@@ -73,9 +73,9 @@ def _oracle_eps(r):
     return np.stack(out)
 
 
-@pytest.mark.parametrize("xfold", [True, False])
-def test_dpt_iteration_matches_oracle(monkeypatch, xfold):
-    r = _dpt_iteration(True, monkeypatch, xfold)
+@pytest.mark.parametrize("xfold,S", [(True, 5), (False, 5), (True, 8), (False, 8)])
+def test_dpt_iteration_matches_oracle(monkeypatch, xfold, S):
+    r = _dpt_iteration(True, monkeypatch, xfold, S)
     cfg, w, S, steps, x0, noise, gcs, sched = (r[k] for k in ("cfg", "w", "S", "steps", "x0", "noise", "gcs", "sched"))
     eps, xs = r["eps"], r["xs"]
     T, A = cfg.horizon, cfg.action_dim
