@@ -1607,10 +1607,13 @@ int auras_dpt_persist_run(void *plan, int S, const float *eps, int eps_pitch, co
   }
   if (int rc = ensure_smem_attr(dpt_persist, (int)DP_SMEM)) return rc;
   if (DP_CL > 8) {
-    static bool np = false;
-    if (!np) {
+    // (a function attribute is per device: a process-wide flag would miss a second GPU)
+    static thread_local bool np[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return cuda_check(cudaGetLastError(), "dpt device");
+    if (!np[dev]) {
       AURAS_CUDA(cudaFuncSetAttribute(dpt_persist, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      np = true;
+      np[dev] = true;
     }
   }
   DpParams P;
