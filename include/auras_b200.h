@@ -354,6 +354,9 @@ typedef struct auras_dpt_gemm {
   const void *ln_src;       /* optional: A = LayerNorm(ln_src [128][256] bf16; ln_g, ln_b), computed in the
                                GEMM phase itself (act is then ignored; K = 256) */
   const float *ln_g, *ln_b;
+  int ksplit;               /* 1: K split over the cluster's two 8-CTA halves (CTA r: K half r / 8, columns
+                               [(r % 8) N/8, +N/8)), the halves' partials summed over DSMEM -- each CTA
+                               receives half the A operand (plain A, bf16 out, N / 8 % 16 == 0, K % 128 == 0) */
 } auras_dpt_gemm;
 typedef struct auras_dpt_op {
   int type;                 /* 0 GEMM, 1 LayerNorm (E = 256), 2 attention, 3 scheduler update, 4 no-op,

@@ -115,7 +115,7 @@ struct DpOpDev {
   int par[2], job[2];
   int gather;                // attention: k / v row 0 from the time table (by the sample's step), rows
                              // 1 .. nk - 1 from the frame's observation rows (by its agent)
-  int pad_;
+  int ksplit;                // GEMM: K split over the cluster halves (auras_dpt_gemm.ksplit)
 };
 static_assert(sizeof(DpOpDev) == 112, "DpOpDev");
 
@@ -520,11 +520,12 @@ constexpr int DP_MROWS = 128 / DP_CL;
 constexpr uint16_t DP_MASK = (uint16_t)((1u << DP_CL) - 1);
 static_assert(128 % DP_CL == 0, "multicast slices");
 
-__device__ __forceinline__ void dp_tma_mc(void *dst, const CUtensorMap *tm, uint64_t *bar, int c0, int c1) {
+__device__ __forceinline__ void dp_tma_mc(void *dst, const CUtensorMap *tm, uint64_t *bar, int c0, int c1,
+                                          uint16_t mask = DP_MASK) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
       " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-      "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(DP_MASK)
+      "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
       : "memory");
 }
 
@@ -573,7 +574,7 @@ __device__ __forceinline__ bool dp_issue_b(const DpParams &P, const DpOpDev *ops
                                            int rank, uint8_t *smem, uint64_t *full, uint64_t *empty, bool block) {
   while (c.op < P.n_ops) {
     const DpOpDev &o = ops[c.op];
-    if (o.type != DP_GEMM || c.kb == gm[o.gemm].K / 64) {
+    if (o.type != DP_GEMM || c.kb == (gm[o.gemm].K >> (o.ksplit ? 7 : 6))) {
       ++c.op;
       c.kb = 0;
       continue;
@@ -587,7 +588,11 @@ __device__ __forceinline__ bool dp_issue_b(const DpParams &P, const DpOpDev *ops
     }
     else if (!dp_stage_free(&empty[st], par)) return false;
     mbar_expect_tx(&full[st], g.ncta * 128);
-    tma_load_2d(smem + DP_B_OFF + st * DP_B_BYTES, &P.gemms[o.gemm].tmB, &full[st], c.kb * 64, rank * g.ncta);
+    if (o.ksplit)      // K half rank / 8, columns of CTA rank % 8
+      tma_load_2d(smem + DP_B_OFF + st * DP_B_BYTES, &P.gemms[o.gemm].tmB, &full[st],
+                  ((rank >> 3) * (g.K >> 7) + c.kb) * 64, (rank & 7) * g.ncta);
+    else
+      tma_load_2d(smem + DP_B_OFF + st * DP_B_BYTES, &P.gemms[o.gemm].tmB, &full[st], c.kb * 64, rank * g.ncta);
     ++c.kb;
     ++c.job;
     return true;
@@ -847,7 +852,9 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
   uint64_t *lnbar = done + 1;     // the LayerNorm source tile landed in sAln
   uint64_t *resbar = lnbar + 1;   // the residual slice landed
   uint64_t *attbar = resbar + 1;  // the attention tiles landed
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(attbar + 1);
+  uint64_t *rxbar = attbar + 1;   // K-split GEMM: the partner half's partial sums landed
+  uint64_t *rdybar = rxbar + 1;   // K-split GEMM: the partner's MMAs are done (its A ring may be written)
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rdybar + 1);
   DpOpDev *sops = reinterpret_cast<DpOpDev *>(smem + DP_META_OFF);
   DpGemmMeta *sgm = reinterpret_cast<DpGemmMeta *>(smem + DP_META_OFF + DP_MAX_OPS * 112);
   float *sbias = reinterpret_cast<float *>(smem + DP_META_OFF + DP_MAX_OPS * 112 + DP_MAX_GEMMS * 96);
@@ -869,11 +876,14 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
       m.stats_out = g.stats_out; m.stats_in = g.stats_in;
       sgm[i] = m;
     }
-    for (int i = warp; i < P.n_gemms; i += DP_THREADS / 32) {
-      const DpGemmDev &g = P.gemms[i];
+    for (int i = warp; i < P.n_ops; i += DP_THREADS / 32) {
+      const DpOpDev &op = P.ops[i];
+      if (op.type != DP_GEMM) continue;
+      const DpGemmDev &g = P.gemms[op.gemm];
       if (rank >= g.ctas) continue;
+      const int cb = op.ksplit ? (rank & 7) : rank;        // K split: the half's CTAs share columns
       for (int c = lane; c < g.ncta; c += 32) {
-        const int n = rank * g.ncta + c;
+        const int n = cb * g.ncta + c;
         sbias[g.boff + c] = n < g.N ? g.bias[n] : 0.f;
       }
     }
@@ -905,6 +915,8 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
     mbar_init(lnbar, 1);
     mbar_init(resbar, 1);
     mbar_init(attbar, 1);
+    mbar_init(rxbar, 1);
+    mbar_init(rdybar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -942,12 +954,18 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
               dp_tma_mc(smem + kb * DP_A_BYTES + rank * (128 / P.mslices) * 128, &P.gemms[o.gemm].tmA, lnbar,
                         kb * 64, rank * (128 / P.mslices));
         }
-        for (int kb = 0; kb < nkb; ++kb, ++ip) {
+        const int nkbx = o.ksplit ? nkb / 2 : nkb;
+        for (int kb = 0; kb < nkbx; ++kb, ++ip) {
           while (bc.job <= ip) dp_issue_b(P, sops, sgm, bc, rank, smem, full, empty, true);
           DP_KSTAMP(kb, kb < 16);
           const int st = ip % DP_STAGES;
           if (lnA) {
             mbar_arrive(&full[st]);                   // A comes from the LayerNorm warps
+          } else if (o.ksplit) {
+            // this half's k-blocks: 16 rows from each of its 8 CTAs, multicast within the half
+            mbar_expect_tx(&full[st], DP_A_BYTES);
+            dp_tma_mc(smem + st * DP_A_BYTES + (rank & 7) * 16 * 128, &P.gemms[o.gemm].tmA, &full[st],
+                      ((rank >> 3) * nkbx + kb) * 64, (rank & 7) * 16, (uint16_t)(0xFFu << (rank & 8)));
           } else {
             mbar_expect_tx(&full[st], DP_A_BYTES);     // (all DP_CL slices, from every CTA)
             if (rank < P.mslices)
@@ -1003,7 +1021,7 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
     if (o.type == DP_GEMM) {
       const DpGemmMeta &g = sgm[o.gemm];
       {
-        const int nkb = g.K / 64, ncta = g.ncta;
+        const int nkb = g.K >> (o.ksplit ? 7 : 6), ncta = g.ncta;
         const bool lnA = g.ln_g != nullptr;                // A = LayerNorm(src) computed here, not loaded
         uint8_t *sAln = smem;                              // 128 x 256 bf16, four 128B-swizzled k-blocks
         if (lnA) {
@@ -1098,7 +1116,14 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
           // ---- epilogue, all 8 warps: token row = TMEM lane (warp % 4 quadrant), warps
           //      0-3 / 4-7 take alternate 16-column chunks
           const int row = (warp & 3) * 32 + lane, grp = warp >> 2;
-          const int n0 = rank * ncta;
+          const int n0 = (o.ksplit ? (rank & 7) : rank) * ncta;
+          // K split: this CTA owns 16-column chunk kh = rank / 8 of its 32 columns (warps with grp ==
+          // kh); the other chunk's partials go to the partner CTA rank ^ 8 (which owns it) over DSMEM,
+          // into its A-ring stage 0 once the partner's MMAs are done (rdybar)
+          const bool ks = o.ksplit != 0;
+          const int kh = rank >> 3;
+          float *rx = reinterpret_cast<float *>(smem);      // [128 rows][16] fp32 partner partials
+          if (ks && threadIdx.x == 0) mbar_expect_tx(rxbar, 128 * 16 * 4);
           const uint8_t *sres = smem + DP_R_OFF + row * ncta * 2;     // this row of the TMA'd residual slice
           // the GEMM's fields in registers: g lives in shared memory behind a generic pointer, so
           // every global store below would otherwise force it to be re-read
@@ -1115,11 +1140,36 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
           if (rtma) {
             mbar_wait(resbar, (o.par[rank == 0] >> 1) & 1);
           }
+          if (ks && threadIdx.x == 0)       // my MMAs are done: the partner may write my A ring
+            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                             mapa_shared(smem_u32(rdybar), rank ^ 8))
+                         : "memory");
           DP_STAMP(5, threadIdx.x == 0);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           for (int c = 16 * grp; c < ncols; c += 32) {
             float v[16];
             tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + c, v);
+            if (ks) {
+              const uint32_t kpar = (o.par[0] >> 3) & 1;
+              if (grp != kh) {
+                // the partner's chunk: wait until its A ring is free, then push the 16 partials
+                mbar_wait_cluster(rdybar, kpar);
+                const uint32_t dst = mapa_shared(smem_u32(rx + row * 16), rank ^ 8);
+                const uint32_t rb = mapa_shared(smem_u32(rxbar), rank ^ 8);
+#pragma unroll
+                for (int i = 0; i < 16; i += 4)
+                  st_async_v4_b32(dst + 4 * i, __float_as_uint(v[i]), __float_as_uint(v[i + 1]),
+                                  __float_as_uint(v[i + 2]), __float_as_uint(v[i + 3]), rb);
+                continue;
+              }
+              mbar_wait_cluster(rxbar, kpar);
+              const float4 *rp = reinterpret_cast<const float4 *>(rx + row * 16);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float4 q = rp[i];
+                v[4 * i] += q.x; v[4 * i + 1] += q.y; v[4 * i + 2] += q.z; v[4 * i + 3] += q.w;
+              }
+            }
             DP_KSTAMP(48 + 3 * (c >> 5), threadIdx.x == 0 && c < 96);
             if (row >= rows) continue;
             const int nb = n0 + c;
@@ -1179,7 +1229,7 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
                   float m2 = 0.f;
 #pragma unroll
                   for (int i = 0; i < 16; ++i) m2 = fmaf(x[i] - mu, x[i] - mu, m2);
-                  P.stats[row * DP_CL + rank] = make_float2(mu, m2);
+                  P.stats[row * DP_CL + (nb >> 4)] = make_float2(mu, m2);
                 }
               }
               if (outf) {
@@ -1433,7 +1483,13 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
     DpGemmDev &d = hg[i];
     memset(&d, 0, sizeof(d));
     const int ctas = s.N <= 16 ? 1 : DP_CL;
-    const int ncta = ctas == 1 ? 16 : s.N / DP_CL;
+    const int ncta = ctas == 1 ? 16 : s.N / (s.ksplit ? DP_CL / 2 : DP_CL);
+    if (s.ksplit && (DP_CL != 16 || ctas != DP_CL || s.ln_g || !s.out || s.out_f32 || s.N % 128 || ncta > 64 ||
+                     ncta != 32 || s.K % 128)) {
+      // (the epilogue exchanges one 16-column chunk with the partner half: 32 columns per CTA)
+      set_error("dpt_persist_build: gemm %d K split needs a plain-A bf16 GEMM, N = 256, K %% 128 == 0", i);
+      return AURAS_E_ARG;
+    }
     if (s.K % 64 || s.act_rows != 128 || (ctas > 1 && (s.N % DP_CL || ncta % 16 || ncta * 128 > DP_B_BYTES)) ||
         (s.out && s.ldo % 8) || (s.res && s.ldr % 8) ||
         (ctas > 1 && s.out_f32 && (s.ldf % 4 || (reinterpret_cast<uintptr_t>(s.out_f32) & 15)))) {
@@ -1445,7 +1501,8 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
       return AURAS_E_ARG;
     }
     // A operand, or (LayerNorm'd A) the residual-stream rows the phase normalises in place
-    if (int rc = dp_map(&d.tmA, s.ln_g ? s.ln_src : s.act, s.K, s.act_rows, 128 / dp_mslices())) return rc;
+    if (int rc = dp_map(&d.tmA, s.ln_g ? s.ln_src : s.act, s.K, s.act_rows, s.ksplit ? 16 : 128 / dp_mslices()))
+      return rc;
     d.ln_src = static_cast<const __nv_bfloat16 *>(s.ln_src);
     d.ln_g = s.ln_g;
     d.ln_b = s.ln_b;
@@ -1468,6 +1525,7 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
   }
   std::vector<DpOpDev> ho(n_ops);
   int nln[2] = {0, 0}, nres[2] = {0, 0}, ng[2] = {0, 0}, nj[2] = {0, 0};   // [CTAs 1..] / [CTA 0]
+  int nks = 0;                                                              // K-split GEMMs so far
   int natt = 0;
   for (int i = 0; i < n_ops; ++i) {
     const auras_dpt_op &s = ops[i];
@@ -1488,16 +1546,18 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
     }
     if (s.type == DP_GEMM && s.gemm >= 0 && s.gemm < n_gemms) {
       const DpGemmDev &gg = hg[s.gemm];
+      d.ksplit = gemms[s.gemm].ksplit ? 1 : 0;
       for (int c = 0; c < 2; ++c) {
         const bool runs = true;        // every CTA streams every GEMM (multicast ring)
-        d.par[c] = (nln[c] & 1) | ((nres[c] & 1) << 1) | ((ng[c] & 1) << 2);
+        d.par[c] = (nln[c] & 1) | ((nres[c] & 1) << 1) | ((ng[c] & 1) << 2) | ((nks & 1) << 3);
         d.job[c] = nj[c];
         if (!runs) continue;
         if (gg.ln_g) ++nln[c];
         if (gg.rtma) ++nres[c];
         ++ng[c];
-        nj[c] += gg.K / 64;
+        nj[c] += gg.K / (d.ksplit ? 128 : 64);
       }
+      nks += d.ksplit;
     }
     if (s.type == DP_XATTN) {
       // one sample per CTA (8 rows), table blocks within A-ring stages 4-5, float4-aligned rows
@@ -1565,7 +1625,7 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
       DpGemmDev &d = hg[ops[i].gemm];
       if (d.ln_g) d.stats_in = valid && d.ln_src == valid;
       if (d.out && is_lsrc(d.out)) {
-        const bool ok = d.N == DP_E && d.ncta == 16 && d.ctas == DP_CL;
+        const bool ok = d.N == DP_E && d.ctas == DP_CL && (d.ncta == 16 || (gemms[ops[i].gemm].ksplit && d.ncta == 32));
         d.stats_out = ok;
         valid = ok ? d.out : nullptr;
       }

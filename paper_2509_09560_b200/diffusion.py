@@ -907,7 +907,7 @@ class DPTDenoiser:
         gemms, ops = [], []
 
         def gemm(act, K, wname, rows=None, res=None, out=None, ldo=0, out_f32=None, act_fn=0, cin_pad=None,
-                 ln=None):
+                 ln=None, ksplit=0):
             """one GEMM phase; ln = LayerNorm name: A = LN(residual stream), computed in the phase"""
             wm = model.conv_weight(lw(wname, rows), cin_pad=cin_pad)[0]
             bias = lb(wname, rows)
@@ -915,7 +915,7 @@ class DPTDenoiser:
             g = _lib.DptGemm(act=act.data_ptr() if act is not None else 0, act_rows=R, K=K, w=wm.data_ptr(),
                              N=wm.shape[0], bias=bias.data_ptr(), res=_lib.ptr(res),
                              ldr=E if res is not None else 0, out=_lib.ptr(out), ldo=ldo, out_f32=_lib.ptr(out_f32),
-                             ldf=cfg.action_dim if out_f32 is not None else 0, act_fn=act_fn)
+                             ldf=cfg.action_dim if out_f32 is not None else 0, act_fn=act_fn, ksplit=ksplit)
             if ln is not None:
                 lg, lbb = lnp(ln)
                 keep.extend([lg, lbb])
@@ -941,6 +941,7 @@ class DPTDenoiser:
         # the action tokens from the request lanes (dpt_prep's per-iteration part), in-kernel
         # (AURAS_DPT_INKERNEL_PREP=0: the separate dpt_prep / dpt_kv_gather launches, for A/B)
         self.p_inprep = os.environ.get("AURAS_DPT_INKERNEL_PREP", "1") != "0"
+        self.p_ksplit = int(os.environ.get("AURAS_DPT_KSPLIT", "1") == "1" and E == 256)
         if self.p_inprep:
             ops.append(_lib.DptOp(type=5, out=self.xin.data_ptr()))
         # h = input(x) + pos; every LayerNorm runs inside the GEMM phase that consumes it
@@ -955,7 +956,8 @@ class DPTDenoiser:
             if self.xfold and self.p_inprep:
                 xattn(l, p + ".ln3")
                 gemm(self.p_ln, E, p + ".ff1", out=self.p_ff, ldo=4 * E, act_fn=_lib.ACT_GELU)
-                gemm(self.p_ff, 4 * E, p + ".ff2", res=self.p_h, out=self.p_h, ldo=E)
+                # ff2 (K = 4E): K split over the cluster halves, each CTA receives half the A operand
+                gemm(self.p_ff, 4 * E, p + ".ff2", res=self.p_h, out=self.p_h, ldo=E, ksplit=self.p_ksplit)
                 continue
             gemm(None, E, p + ".ca_in", rows=(0, E), out=self.p_q2, ldo=E, ln=p + ".ln2")
             # cross-attention keys / values straight from the time-row table (by each sample's
