@@ -952,7 +952,8 @@ class DPTDenoiser:
             gemm(None, E, p + ".sa_in", out=self.p_qkv, ldo=3 * E, ln=p + ".ln1")
             q0 = self.p_qkv.data_ptr()
             attn(q0, 3 * E, q0 + 2 * E, q0 + 2 * 2 * E, 3 * E, T, 0, R)
-            gemm(self.p_att, E, p + ".sa_out", res=self.p_h, out=self.p_h, ldo=E)
+            gemm(self.p_att, E, p + ".sa_out", res=self.p_h, out=self.p_h, ldo=E,
+                 ksplit=self.p_ksplit if os.environ.get("AURAS_DPT_KSPLIT_SAOUT", "0") == "1" else 0)
             if self.xfold and self.p_inprep:
                 xattn(l, p + ".ln3")
                 gemm(self.p_ln, E, p + ".ff1", out=self.p_ff, ldo=4 * E, act_fn=_lib.ACT_GELU)
