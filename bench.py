@@ -678,7 +678,7 @@ def main():
     if args.disaggregated:
         out["disaggregated"] = disaggregated_leg(args, cfg, weights, A, W, K, dist)
 
-    if dist.rank == 0 and not args.no_cpu:
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu:     # (the CPU leg: rank 0 at N = 1 only)
         out["cpu_baseline"] = cpu_oracle_sample(args.config, args.cpu_seconds)
     if dist.rank == 0:
         print(json.dumps(out), flush=True)
