@@ -37,7 +37,7 @@ METRIC = "actions/sec per GPU at pipeline depth k; p99 action latency; roofline 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--steps", type=int, default=120)
     ap.add_argument("--warmup", type=int, default=6)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--depth", type=int, default=8)
@@ -137,7 +137,7 @@ class ClockSampler:
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "sw_power_cap": 0x4}
 
-    def __init__(self, device, period=0.05):
+    def __init__(self, device, period=0.02):
         self.device, self.period = device, period
         self.samples, self.masks, self.max_mhz = [], [], None
         self.stop_flag = threading.Event()
@@ -180,7 +180,7 @@ class ClockSampler:
         reasons = sorted(n for n, bit in self.REASONS.items() if any(m & bit for m in self.masks))
         return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
                 "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples),
-                "source": "NVML, 50 ms period"}
+                "source": "NVML, 20 ms period"}
 
 
 # ---------------------------------------------------------------- measurement helpers
