@@ -468,7 +468,34 @@ def _splits(M, N, Kp, target_ctas=296):
     return s
 
 
-class Encoder:
+class _GraphedProgram:
+    """Replays a fixed launch program (every pointer it reads is fixed) as one
+    CUDA graph per (layer range, stream): the first call runs eagerly (lazy
+    per-device kernel attributes), the second captures, later calls replay --
+    the encoders' ~50-100 small launches per frame stop paying a host launch
+    each (AURAS_ENC_GRAPH=0: always eager)."""
+
+    def _graph_run(self, key, stream, fn):
+        torch = self.m.torch
+        if os.environ.get("AURAS_ENC_GRAPH", "1") == "0" or not stream.cuda_stream:
+            return fn()                      # (no capture on the legacy default stream)
+        graphs = self.__dict__.setdefault("_graphs", {})
+        warm = self.__dict__.setdefault("_warm", set())
+        key = key + (stream.cuda_stream,)
+        g = graphs.get(key)
+        if g is None:
+            if key not in warm:
+                warm.add(key)
+                return fn()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                fn()
+            graphs[key] = g
+        with torch.cuda.stream(stream):
+            g.replay()
+
+
+class Encoder(_GraphedProgram):
     """ResNet-18-GN program for A frames at a time (K1 of SURVEY.md §2.4)."""
 
     GROUPS = ("stem", "layer1", "layer2", "layer3", "layer4")
@@ -551,6 +578,9 @@ class Encoder:
         self.groups[group].append(("conv", op))
 
     def run(self, lo, hi, stream):
+        self._graph_run((lo, hi), stream, lambda: self._run(lo, hi, stream))
+
+    def _run(self, lo, hi, stream):
         lib = _lib.load()
         st = stream.cuda_stream
         cfg = self.m.cfg
@@ -571,7 +601,7 @@ class Encoder:
                                                     self.m.dt, st), "maxpool")
 
 
-class ViTEncoder:
+class ViTEncoder(_GraphedProgram):
     """ViT-B/16 program for A frames at a time (BASELINE configs[3]; SURVEY.md
     §2.4 K7), same interface as Encoder.  Patch embedding and every linear
     layer are tcgen05 implicit-GEMM conv ops (16x16/s16 over the image, 1x1
@@ -678,6 +708,9 @@ class ViTEncoder:
         self.groups[group].append(("conv", op, S) if ln is None else ("conv_ln", op, S, ln[0], ln[1]))
 
     def run(self, lo, hi, stream):
+        self._graph_run((lo, hi), stream, lambda: self._run(lo, hi, stream))
+
+    def _run(self, lo, hi, stream):
         lib = _lib.load()
         st = stream.cuda_stream
         cfg = self.m.cfg
