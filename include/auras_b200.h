@@ -357,6 +357,9 @@ typedef struct auras_dpt_gemm {
   int ksplit;               /* 1: K split over the cluster's two 8-CTA halves (CTA r: K half r / 8, columns
                                [(r % 8) N/8, +N/8)), the halves' partials summed over DSMEM -- each CTA
                                receives half the A operand (plain A, bf16 out, N / 8 % 16 == 0, K % 128 == 0) */
+  int fuse_update;          /* 1 (the single-CTA action head, N = action dim <= 16, fp32 out): the DDPM / DDIM
+                               update of every sample's request lane runs in this GEMM's epilogue (the
+                               program then needs no type-3 op) */
 } auras_dpt_gemm;
 typedef struct auras_dpt_op {
   int type;                 /* 0 GEMM, 1 LayerNorm (E = 256), 2 attention, 3 scheduler update, 4 no-op,

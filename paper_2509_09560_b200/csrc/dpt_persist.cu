@@ -1255,6 +1255,30 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
                 if (out) out[(int64_t)row * ldo + nb + i] = __float2bfloat16_rn(v[i]);
                 if (outf) outf[(int64_t)row * ldf + nb + i] = v[i];
               }
+              if (o.gather == 2) {
+                // the scheduler update fused into the action head (auras_dpt_gemm.fuse_update): token
+                // row = (sample, t), its adim eps values in v (the UPDATE phase's arithmetic)
+                const auras_sched &sch = P.sched;
+                const int sm = row / P.T, t = row - sm * P.T;
+                const int agent = s_agent[sm], ln = s_lane[sm], i = s_step[sm];
+                float *x = P.x_lanes + ((int64_t)agent * P.lanes_per_agent + ln) * P.horizon * P.adim + t * P.adim;
+                const float *z = P.noise_lanes ? P.noise_lanes +
+                                                     (((int64_t)agent * P.lanes_per_agent + ln) * sch.n_steps + i) *
+                                                         P.horizon * P.adim + t * P.adim
+                                               : nullptr;
+                const float sab = sch.sqrt_ab[i], s1m = sch.sqrt_1mab[i];
+                const float cx0 = sch.c_x0[i], cxt = sch.c_xt[i], ceps = sch.c_eps[i], sig = sch.sigma[i];
+#pragma unroll
+                for (int a = 0; a < 16; ++a) {
+                  if (nb + a >= P.adim) break;
+                  const float xt = x[nb + a], ep = v[a];
+                  float x0 = (xt - s1m * ep) / sab;
+                  if (sch.clip_sample) x0 = fminf(fmaxf(x0, -1.f), 1.f);
+                  float nx = cx0 * x0 + cxt * xt + ceps * ep;
+                  if (sch.ddpm && z) nx += sig * z[nb + a];
+                  x[nb + a] = nx;
+                }
+              }
               DP_KSTAMP(50, threadIdx.x == 0);
             }
           }
@@ -1547,6 +1571,14 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
     if (s.type == DP_GEMM && s.gemm >= 0 && s.gemm < n_gemms) {
       const DpGemmDev &gg = hg[s.gemm];
       d.ksplit = gemms[s.gemm].ksplit ? 1 : 0;
+      if (gemms[s.gemm].fuse_update) {
+        const auras_dpt_gemm &gg2 = gemms[s.gemm];
+        if (gg2.N > 16 || !gg2.out_f32 || gg2.ksplit || gg2.res) {
+          set_error("dpt_persist_build: gemm %d fused update needs the single-CTA fp32 action head", s.gemm);
+          return AURAS_E_ARG;
+        }
+        d.gather = 2;
+      }
       for (int c = 0; c < 2; ++c) {
         const bool runs = true;        // every CTA streams every GEMM (multicast ring)
         d.par[c] = (nln[c] & 1) | ((nres[c] & 1) << 1) | ((ng[c] & 1) << 2) | ((nks & 1) << 3);

@@ -940,7 +940,7 @@ class DPTDenoiser:
         gemms, ops = [], []
 
         def gemm(act, K, wname, rows=None, res=None, out=None, ldo=0, out_f32=None, act_fn=0, cin_pad=None,
-                 ln=None, ksplit=0):
+                 ln=None, ksplit=0, fuse_update=0):
             """one GEMM phase; ln = LayerNorm name: A = LN(residual stream), computed in the phase"""
             wm = model.conv_weight(lw(wname, rows), cin_pad=cin_pad)[0]
             bias = lb(wname, rows)
@@ -948,7 +948,8 @@ class DPTDenoiser:
             g = _lib.DptGemm(act=act.data_ptr() if act is not None else 0, act_rows=R, K=K, w=wm.data_ptr(),
                              N=wm.shape[0], bias=bias.data_ptr(), res=_lib.ptr(res),
                              ldr=E if res is not None else 0, out=_lib.ptr(out), ldo=ldo, out_f32=_lib.ptr(out_f32),
-                             ldf=cfg.action_dim if out_f32 is not None else 0, act_fn=act_fn, ksplit=ksplit)
+                             ldf=cfg.action_dim if out_f32 is not None else 0, act_fn=act_fn, ksplit=ksplit,
+                             fuse_update=fuse_update)
             if ln is not None:
                 lg, lbb = lnp(ln)
                 keep.extend([lg, lbb])
@@ -1007,8 +1008,11 @@ class DPTDenoiser:
             gemm(self.p_att, E, p + ".ca_out", res=self.p_h, out=self.p_h, ldo=E)
             gemm(None, E, p + ".ff1", out=self.p_ff, ldo=4 * E, act_fn=_lib.ACT_GELU, ln=p + ".ln3")
             gemm(self.p_ff, 4 * E, p + ".ff2", res=self.p_h, out=self.p_h, ldo=E)
-        gemm(None, E, "dpt.head", out_f32=self.p_eps, ln="dpt.lnf")
-        ops.append(_lib.DptOp(type=3))
+        # the scheduler update in the head's epilogue (AURAS_DPT_FUSE_UPDATE=0: its own phase)
+        fuse_up = os.environ.get("AURAS_DPT_FUSE_UPDATE", "1") == "1" and cfg.action_dim <= 16
+        gemm(None, E, "dpt.head", out_f32=self.p_eps, ln="dpt.lnf", fuse_update=int(fuse_up))
+        if not fuse_up:
+            ops.append(_lib.DptOp(type=3))
         ops.extend(_lib.DptOp(type=4) for _ in range(int(os.environ.get("AURAS_DPT_NOPS", "0"))))   # timing probe
         lib = _lib.load()
         ga = (_lib.DptGemm * len(gemms))(*gemms)
