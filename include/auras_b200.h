@@ -360,6 +360,8 @@ typedef struct auras_dpt_gemm {
   int fuse_update;          /* 1 (the single-CTA action head, N = action dim <= 16, fp32 out): the DDPM / DDIM
                                update of every sample's request lane runs in this GEMM's epilogue (the
                                program then needs no type-3 op) */
+  int a_from_lanes;         /* 1 (K = 64): A = every sample's action tokens bf16(x[t][a]) read straight from
+                               its request lane into the UMMA tile (the program then needs no type-5 op) */
 } auras_dpt_gemm;
 typedef struct auras_dpt_op {
   int type;                 /* 0 GEMM, 1 LayerNorm (E = 256), 2 attention, 3 scheduler update, 4 no-op,

@@ -46,7 +46,7 @@ class LinearOp(C.Structure):
 class DptGemm(C.Structure):
     _fields_ = [("act", vp), ("act_rows", i32), ("K", i32), ("w", vp), ("N", i32), ("bias", vp), ("res", vp),
                 ("ldr", i32), ("out", vp), ("ldo", i32), ("out_f32", vp), ("ldf", i32), ("act_fn", i32),
-                ("ln_src", vp), ("ln_g", vp), ("ln_b", vp), ("ksplit", i32), ("fuse_update", i32)]
+                ("ln_src", vp), ("ln_g", vp), ("ln_b", vp), ("ksplit", i32), ("fuse_update", i32), ("a_from_lanes", i32)]
 
 
 class DptOp(C.Structure):

@@ -959,8 +959,8 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
           while (bc.job <= ip) dp_issue_b(P, sops, sgm, bc, rank, smem, full, empty, true);
           DP_KSTAMP(kb, kb < 16);
           const int st = ip % DP_STAGES;
-          if (lnA) {
-            mbar_arrive(&full[st]);                   // A comes from the LayerNorm warps
+          if (lnA || o.gather == 3) {
+            mbar_arrive(&full[st]);                   // A comes from the LayerNorm / action-token warps
           } else if (o.ksplit) {
             // this half's k-blocks: 16 rows from each of its 8 CTAs, multicast within the half
             mbar_expect_tx(&full[st], DP_A_BYTES);
@@ -1076,6 +1076,30 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           named_sync(1, DP_CT);
           DP_STAMP(2, threadIdx.x == 0);
+        } else if (o.gather == 3) {
+          // ---- the input GEMM's A (K = 64): every sample's action tokens straight from its
+          //      request lane into the UMMA tile (K-major, 128B swizzle: 16-byte chunk j of row r
+          //      at chunk j ^ (r & 7)), bf16(x[t][a]) for a < adim, zeros elsewhere -- the
+          //      separate prep phase (out[s T + t] = x[t]) and its L2 round trip are gone
+          for (int i = threadIdx.x; i < 128 * 8; i += DP_CT) {
+            const int r = i >> 3, j = i & 7;
+            uint32_t w[4] = {0u, 0u, 0u, 0u};
+            if (r < rows && 8 * j < P.adim) {
+              const int sm = r / P.T, t = r - sm * P.T;
+              const float *x = P.x_lanes +
+                               ((int64_t)s_agent[sm] * P.lanes_per_agent + s_lane[sm]) * P.horizon * P.adim +
+                               t * P.adim;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int a0 = 8 * j + 2 * k;
+                w[k] = dp_pack(a0 < P.adim ? x[a0] : 0.f, a0 + 1 < P.adim ? x[a0 + 1] : 0.f);
+              }
+            }
+            *reinterpret_cast<uint4 *>(sAln + r * 128 + ((j ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          named_sync(1, DP_CT);
+          DP_STAMP(2, threadIdx.x == 0);
         }
         if (warp == 1) {
           // ---- MMA issuer
@@ -1101,7 +1125,8 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             for (int r = 0; r < ready; ++r, ++kb) {
               const int st = (j0 + kb) % DP_STAGES;
-              const uint32_t sa = smem_u32(lnA ? sAln + kb * DP_A_BYTES : smem + st * DP_A_BYTES);
+              const uint32_t sa =
+                  smem_u32((lnA || o.gather == 3) ? sAln + kb * DP_A_BYTES : smem + st * DP_A_BYTES);
               const uint32_t sb = smem_u32(smem + DP_B_OFF + st * DP_B_BYTES);
               if (!(P.dbg & 8)) umma_kblock_warp(tmem, umma_desc(sa), umma_desc(sb), idesc, kb > 0 ? 1u : 0u);
               dp_commit_all(&empty[st]);
@@ -1571,6 +1596,14 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
     if (s.type == DP_GEMM && s.gemm >= 0 && s.gemm < n_gemms) {
       const DpGemmDev &gg = hg[s.gemm];
       d.ksplit = gemms[s.gemm].ksplit ? 1 : 0;
+      if (gemms[s.gemm].a_from_lanes) {
+        const auras_dpt_gemm &gg3 = gemms[s.gemm];
+        if (gg3.K != 64 || gg3.ln_g || gg3.ksplit || gg3.fuse_update) {
+          set_error("dpt_persist_build: gemm %d A from the request lanes needs K = 64, plain A", s.gemm);
+          return AURAS_E_ARG;
+        }
+        d.gather = 3;
+      }
       if (gemms[s.gemm].fuse_update) {
         const auras_dpt_gemm &gg2 = gemms[s.gemm];
         if (gg2.N > 16 || !gg2.out_f32 || gg2.ksplit || gg2.res) {

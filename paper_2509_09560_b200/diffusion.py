@@ -940,7 +940,7 @@ class DPTDenoiser:
         gemms, ops = [], []
 
         def gemm(act, K, wname, rows=None, res=None, out=None, ldo=0, out_f32=None, act_fn=0, cin_pad=None,
-                 ln=None, ksplit=0, fuse_update=0):
+                 ln=None, ksplit=0, fuse_update=0, a_from_lanes=0):
             """one GEMM phase; ln = LayerNorm name: A = LN(residual stream), computed in the phase"""
             wm = model.conv_weight(lw(wname, rows), cin_pad=cin_pad)[0]
             bias = lb(wname, rows)
@@ -949,7 +949,7 @@ class DPTDenoiser:
                              N=wm.shape[0], bias=bias.data_ptr(), res=_lib.ptr(res),
                              ldr=E if res is not None else 0, out=_lib.ptr(out), ldo=ldo, out_f32=_lib.ptr(out_f32),
                              ldf=cfg.action_dim if out_f32 is not None else 0, act_fn=act_fn, ksplit=ksplit,
-                             fuse_update=fuse_update)
+                             fuse_update=fuse_update, a_from_lanes=a_from_lanes)
             if ln is not None:
                 lg, lbb = lnp(ln)
                 keep.extend([lg, lbb])
@@ -976,10 +976,13 @@ class DPTDenoiser:
         # (AURAS_DPT_INKERNEL_PREP=0: the separate dpt_prep / dpt_kv_gather launches, for A/B)
         self.p_inprep = os.environ.get("AURAS_DPT_INKERNEL_PREP", "1") != "0"
         self.p_ksplit = int(os.environ.get("AURAS_DPT_KSPLIT", "1") == "1" and E == 256)
-        if self.p_inprep:
+        # the input GEMM reads the action tokens straight from the request lanes into its UMMA
+        # tile (AURAS_DPT_LANES_A=0: a prep phase writes them to xin first)
+        lanes_a = self.p_inprep and os.environ.get("AURAS_DPT_LANES_A", "1") == "1"
+        if self.p_inprep and not lanes_a:
             ops.append(_lib.DptOp(type=5, out=self.xin.data_ptr()))
         # h = input(x) + pos; every LayerNorm runs inside the GEMM phase that consumes it
-        gemm(self.xin, 64, "dpt.input", res=self.pos_rep, out=self.p_h, ldo=E, cin_pad=64)
+        gemm(self.xin, 64, "dpt.input", res=self.pos_rep, out=self.p_h, ldo=E, cin_pad=64, a_from_lanes=int(lanes_a))
         kv, lkv = self.kv2.data_ptr(), L * 2 * E
         for l in range(L):
             p = f"dpt.l{l}"
