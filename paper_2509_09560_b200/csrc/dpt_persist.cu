@@ -658,7 +658,8 @@ __device__ __forceinline__ uint32_t dp_pack(float lo, float hi) {
 // key slots), masked softmax on the accumulator fragments, O = P V with P split into bf16 hi + lo
 // parts (P V to ~2^-16, as the fp32 softmax of the launch-per-layer program).  Key slots >= nk
 // hold finite neighbouring rows (or TMA zero fill) and are masked.
-__device__ __noinline__ void dp_attn_tile(const DpOpDev &o, const uint8_t *t, int s, int h, int T, int lane) {
+__device__ __noinline__ void dp_attn_tile(const DpOpDev &o, const uint8_t *t, int s, int h, int T, int lane,
+                                          int dn0, int dn1) {
   const uint8_t *tq = t, *tk = t + 2048, *tv = t + 4096;
   const int g = lane >> 2, tq4 = lane & 3;
   const int lr = lane & 15, lc = lane >> 4;          // ldmatrix row / chunk-half of this lane
@@ -721,7 +722,7 @@ __device__ __noinline__ void dp_attn_tile(const DpOpDev &o, const uint8_t *t, in
   }
   const float inv[2] = {__fdividef(1.f, sm[0]), __fdividef(1.f, sm[1])};
 #pragma unroll
-  for (int dn = 0; dn < 4; ++dn) {                   // head dims 16 dn .. 16 dn + 15: two n-tiles
+  for (int dn = dn0; dn < dn1; ++dn) {               // head dims 16 dn .. 16 dn + 15: two n-tiles
     uint32_t b[4];
     // V^T fragments: lanes 0-7 keys 0-7 / 8-15 keys 8-15 at dims +0, 16-23 / 24-31 at dims +8
     dp_ldsm4t(b, dp_sw(tv, (lane & 7) + 8 * ((lane >> 3) & 1), 2 * dn + (lane >> 4)));
@@ -1316,10 +1317,18 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
       long long *stamp = P.trace && rank == 0 && threadIdx.x == 0 ? P.trace + 9 * P.n_ops + 1 + 64 * oi + 56 : nullptr;
       mbar_wait(attbar, (o.par[0] >> 3) & 1);
       if (stamp) stamp[0] = clock64();
-      // unit slot k (u = rank + DP_CL k) on warp k
-      const int u = rank + DP_CL * warp;
-      if (warp < DP_ATT_SLOTS && u < P.S * o.heads)
-        dp_attn_tile(o, smem + DP_ATT_OFF + warp * DP_ATT_UNIT, u / o.heads, u % o.heads, P.T, lane);
+      // unit slot k (u = rank + DP_CL k); the 8 warps split the CTA's units, each unit's P V by
+      // head-dim blocks (the scores are recomputed per warp: 8 MMAs against the 16 of P V)
+      const int units = P.S * o.heads;
+      const int nu = units > rank ? (units - rank + DP_CL - 1) / DP_CL : 0;   // this CTA's units (<= 4)
+      if (nu > 0) {
+        const int wpu = nu == 1 ? 4 : (nu == 2 ? 4 : 2);                       // warps per unit
+        const int k = warp / wpu, part = warp % wpu, nd = 4 / wpu;
+        const int u = rank + DP_CL * k;
+        if (k < nu && part * nd < 4)
+          dp_attn_tile(o, smem + DP_ATT_OFF + k * DP_ATT_UNIT, u / o.heads, u % o.heads, P.T, lane, part * nd,
+                       part * nd + nd);
+      }
       if (stamp) stamp[1] = clock64();
     } else if (o.type == DP_PREP) {
       // ---- the action tokens of every sample from its request lane (dpt.cu dpt_prep_kernel):
