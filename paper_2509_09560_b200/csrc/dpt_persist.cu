@@ -305,7 +305,7 @@ __device__ __noinline__ void dp_attn_block(const DpOpDev &o, int q0, int q1, int
 template <int NK>
 __device__ __noinline__ void dp_xattn(const DpOpDev &o, int r0, int rows, int T, const int *s_agent,
                                       const int *s_step, float *stab, float2 *stats, int warp, int lane,
-                                      long long *stamp) {
+                                      long long *stamp, uint64_t *tbar) {
   constexpr int H = DP_XH;                                     // (checked at build)
   constexpr int SB = 2 * H * DP_E + 4;                         // staged floats per memory token (a', U', c', pad)
   const int tid = warp * 32 + lane;
@@ -330,7 +330,10 @@ __device__ __noinline__ void dp_xattn(const DpOpDev &o, int r0, int rows, int T,
     xa = *reinterpret_cast<const uint2 *>(o.in + (int64_t)r * o.ldi + q0);
     xb = *reinterpret_cast<const uint2 *>(o.in + (int64_t)r * o.ldi + q1);
   }
-  {
+  if (tbar) {
+    // the tables were prefetched during the previous phase (producer warp, bulk copies)
+    mbar_wait(tbar, o.par[0] & 1);
+  } else {
     constexpr int Q4 = SB / 4, N4 = NK * Q4;
     constexpr int PER = (N4 + DP_CT - 1) / DP_CT;
     const float *tk = reinterpret_cast<const float *>(o.k) + (int64_t)step * o.ldk;
@@ -352,7 +355,7 @@ __device__ __noinline__ void dp_xattn(const DpOpDev &o, int r0, int rows, int T,
     }
   }
   if (stamp && tid == 0) stamp[0] = clock64();
-  named_sync(1, DP_CT);
+  if (!tbar) named_sync(1, DP_CT);
   if (stamp && tid == 0) stamp[1] = clock64();
   if (!live) return;
   const int t = r - sidx * T;
@@ -855,7 +858,8 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
   uint64_t *attbar = resbar + 1;  // the attention tiles landed
   uint64_t *rxbar = attbar + 1;   // K-split GEMM: the partner half's partial sums landed
   uint64_t *rdybar = rxbar + 1;   // K-split GEMM: the partner's MMAs are done (its A ring may be written)
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rdybar + 1);
+  uint64_t *tbar = rdybar + 1;    // folded cross-attention: the sample's table blocks prefetched
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tbar + 1);
   DpOpDev *sops = reinterpret_cast<DpOpDev *>(smem + DP_META_OFF);
   DpGemmMeta *sgm = reinterpret_cast<DpGemmMeta *>(smem + DP_META_OFF + DP_MAX_OPS * 112);
   float *sbias = reinterpret_cast<float *>(smem + DP_META_OFF + DP_MAX_OPS * 112 + DP_MAX_GEMMS * 96);
@@ -918,6 +922,7 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
     mbar_init(attbar, 1);
     mbar_init(rxbar, 1);
     mbar_init(rdybar, 1);
+    mbar_init(tbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -942,6 +947,25 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
     int ip = 0;
     for (int oi = 0; oi < P.n_ops; ++oi) {
       const DpOpDev &o = sops[oi];
+      if (lane == 0 && oi + 1 < P.n_ops && sops[oi + 1].type == DP_XATTN && sops[oi + 1].job[0] >= 0 &&
+          rank * (128 / DP_CL) < rows) {
+        // the next phase's folded cross-attention tables (launch constants: by the CTA's sample's
+        // step and agent) into two A-ring stages this phase's GEMM does not use (host-chosen)
+        const DpOpDev &x = sops[oi + 1];
+        const int sidx = rank * (128 / DP_CL) / P.T, sb = 2 * x.heads * DP_E + 4;
+        const uint32_t bytes = (uint32_t)sb * 4;
+        uint8_t *dst = smem + x.job[0] * DP_A_BYTES;
+        mbar_expect_tx(tbar, x.nk * bytes);
+        for (int j = 0; j < x.nk; ++j) {
+          const float *src = j == 0 ? reinterpret_cast<const float *>(x.k) + (int64_t)s_step[sidx] * x.ldk
+                                    : reinterpret_cast<const float *>(x.v) +
+                                          (int64_t)(s_agent[sidx] * (x.nk - 1) + j - 1) * x.ldv;
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           smem_u32(dst + j * bytes)),
+                       "l"(src), "r"(bytes), "r"(smem_u32(tbar))
+                       : "memory");
+        }
+      }
       if (lane == 0 && o.type == DP_GEMM) {     // (every CTA streams every GEMM: the multicast ring runs in lockstep)
         const DpGemmMeta &g = sgm[o.gemm];
         const int nkb = g.K / 64;
@@ -1352,15 +1376,16 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
       long long *stamp = P.trace && rank == 0 ? P.trace + 9 * P.n_ops + 1 + 64 * oi + 56 : nullptr;
       if (stamp && threadIdx.x == 0) stamp[4] = clock64();
       if (r0 < rows) {
-        float *stab = reinterpret_cast<float *>(smem + DP_ATT_OFF);
+        uint64_t *tb = o.job[0] >= 0 ? tbar : nullptr;
+        float *stab = reinterpret_cast<float *>(smem + (tb ? o.job[0] * DP_A_BYTES : DP_ATT_OFF));
         if (o.nk == 3)
-          dp_xattn<3>(o, r0, rows, P.T, s_agent, s_step, stab, P.stats, warp, lane, stamp);
+          dp_xattn<3>(o, r0, rows, P.T, s_agent, s_step, stab, P.stats, warp, lane, stamp, tb);
         else if (o.nk == 2)
-          dp_xattn<2>(o, r0, rows, P.T, s_agent, s_step, stab, P.stats, warp, lane, stamp);
+          dp_xattn<2>(o, r0, rows, P.T, s_agent, s_step, stab, P.stats, warp, lane, stamp, tb);
         else if (o.nk == 4)
-          dp_xattn<4>(o, r0, rows, P.T, s_agent, s_step, stab, P.stats, warp, lane, stamp);
+          dp_xattn<4>(o, r0, rows, P.T, s_agent, s_step, stab, P.stats, warp, lane, stamp, tb);
         else
-          dp_xattn<1>(o, r0, rows, P.T, s_agent, s_step, stab, P.stats, warp, lane, stamp);
+          dp_xattn<1>(o, r0, rows, P.T, s_agent, s_step, stab, P.stats, warp, lane, stamp, tb);
       }
     } else if (o.type == DP_NOP) {
       // timing probe: a phase with no work (the cost of the phase boundary alone)
@@ -1584,6 +1609,7 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
   std::vector<DpOpDev> ho(n_ops);
   int nln[2] = {0, 0}, nres[2] = {0, 0}, ng[2] = {0, 0}, nj[2] = {0, 0};   // [CTAs 1..] / [CTA 0]
   int nks = 0;                                                              // K-split GEMMs so far
+  int ntp = 0;                                                              // prefetched cross-attention tables
   int natt = 0;
   for (int i = 0; i < n_ops; ++i) {
     const auras_dpt_op &s = ops[i];
@@ -1634,6 +1660,25 @@ int auras_dpt_persist_build(const auras_dpt_gemm *gemms, int n_gemms, const aura
       nks += d.ksplit;
     }
     if (s.type == DP_XATTN) {
+      // table prefetch during the previous phase: needs a plain-A GEMM there whose ring jobs leave
+      // two adjacent A-ring stages free (the LayerNorm tile would hold stages 0-3)
+      d.job[0] = d.job[1] = -1;
+      if (i > 0 && ops[i - 1].type == DP_GEMM && !gemms[ops[i - 1].gemm].ln_g && !gemms[ops[i - 1].gemm].a_from_lanes &&
+          !getenv("AURAS_DPT_NO_TPF")) {
+        const auras_dpt_gemm &pg = gemms[ops[i - 1].gemm];
+        const int j0 = ho[i - 1].job[0], nkb = pg.K / (pg.ksplit ? 128 : 64);
+        auto used = [&](int st) {
+          for (int k = 0; k < nkb; ++k)
+            if ((j0 + k) % DP_STAGES == st) return true;
+          return false;
+        };
+        for (int st = 0; st + 1 < DP_STAGES; ++st)
+          if (!used(st) && !used(st + 1)) { d.job[0] = d.job[1] = st; break; }
+        if (d.job[0] >= 0) {
+          d.par[0] = d.par[1] = ntp & 1;
+          ++ntp;
+        }
+      }
       // one sample per CTA (8 rows), table blocks within A-ring stages 4-5, float4-aligned rows
       const int SB = 2 * s.heads * DP_E + 4;
       if (T % (128 / DP_CL) || s.nk < 1 || s.nk > DP_XK || s.heads != DP_XH || s.mask_off < 0 ||
