@@ -947,25 +947,6 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
     int ip = 0;
     for (int oi = 0; oi < P.n_ops; ++oi) {
       const DpOpDev &o = sops[oi];
-      if (lane == 0 && oi + 1 < P.n_ops && sops[oi + 1].type == DP_XATTN && sops[oi + 1].job[0] >= 0 &&
-          rank * (128 / DP_CL) < rows) {
-        // the next phase's folded cross-attention tables (launch constants: by the CTA's sample's
-        // step and agent) into two A-ring stages this phase's GEMM does not use (host-chosen)
-        const DpOpDev &x = sops[oi + 1];
-        const int sidx = rank * (128 / DP_CL) / P.T, sb = 2 * x.heads * DP_E + 4;
-        const uint32_t bytes = (uint32_t)sb * 4;
-        uint8_t *dst = smem + x.job[0] * DP_A_BYTES;
-        mbar_expect_tx(tbar, x.nk * bytes);
-        for (int j = 0; j < x.nk; ++j) {
-          const float *src = j == 0 ? reinterpret_cast<const float *>(x.k) + (int64_t)s_step[sidx] * x.ldk
-                                    : reinterpret_cast<const float *>(x.v) +
-                                          (int64_t)(s_agent[sidx] * (x.nk - 1) + j - 1) * x.ldv;
-          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                           smem_u32(dst + j * bytes)),
-                       "l"(src), "r"(bytes), "r"(smem_u32(tbar))
-                       : "memory");
-        }
-      }
       if (lane == 0 && o.type == DP_GEMM) {     // (every CTA streams every GEMM: the multicast ring runs in lockstep)
         const DpGemmMeta &g = sgm[o.gemm];
         const int nkb = g.K / 64;
@@ -1027,6 +1008,26 @@ __global__ void __launch_bounds__(DP_THREADS, 1) dpt_persist(const __grid_consta
             tma_load_2d(t + 2048, &a.tk, attbar, h * 64, sidx * o.nk);
             tma_load_2d(t + 4096, &a.tv, attbar, h * 64, sidx * o.nk);
           }
+        }
+      }
+      if (lane == 0 && oi + 1 < P.n_ops && sops[oi + 1].type == DP_XATTN && sops[oi + 1].job[0] >= 0 &&
+          rank * (128 / DP_CL) < rows) {
+        // the next phase's folded cross-attention tables (launch constants: by the CTA's sample's
+        // step and agent) into two A-ring stages this phase's GEMM does not use (host-chosen);
+        // issued after this phase's own loads so that they do not queue behind the tables
+        const DpOpDev &x = sops[oi + 1];
+        const int sidx = rank * (128 / DP_CL) / P.T, sb = 2 * x.heads * DP_E + 4;
+        const uint32_t bytes = (uint32_t)sb * 4;
+        uint8_t *dst = smem + x.job[0] * DP_A_BYTES;
+        mbar_expect_tx(tbar, x.nk * bytes);
+        for (int j = 0; j < x.nk; ++j) {
+          const float *src = j == 0 ? reinterpret_cast<const float *>(x.k) + (int64_t)s_step[sidx] * x.ldk
+                                    : reinterpret_cast<const float *>(x.v) +
+                                          (int64_t)(s_agent[sidx] * (x.nk - 1) + j - 1) * x.ldv;
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           smem_u32(dst + j * bytes)),
+                       "l"(src), "r"(bytes), "r"(smem_u32(tbar))
+                       : "memory");
         }
       }
       __syncwarp();
