@@ -52,10 +52,10 @@ if os.environ.get("AURAS_DPT_TRACE"):
     print("per phase us:", " ".join(f"{x:.1f}" for x in d))
     names = ["start", "prod", "ln", "mma0", "mmaN", "done", "epi", "fence"]
     print("sub-phase clocks (cycles after phase start; layer 2 ops + head/update):")
-    for oi in list(range(9, 17)) + [n_ops - 2, n_ops - 1]:
+    for oi in list(range(7, 13)) + [n_ops - 1]:
         r = sub[oi]
         print(f"  op {oi:3d}: " + " ".join(f"{names[k]}={(r[k] - r[0]) if r[k] else -1}" for k in range(1, 8)))
-    for oi in (9, 12, 13, 15, 16, n_ops - 2):
+    for oi in (7, 9, 11, 12, n_ops - 1):
         r0 = sub[oi][0]
         print(f"  op {oi} epilogue : " + " ".join(str(ks[oi][48 + j] - r0) if ks[oi][48 + j] else "-" for j in range(6)))
         k = ks[oi]
