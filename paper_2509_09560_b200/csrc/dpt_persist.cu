@@ -114,7 +114,9 @@ struct DpOpDev {
   // host-computed so that no counter lives across phases (168 registers: it would be spilled)
   int par[2], job[2];
   int gather;                // attention: k / v row 0 from the time table (by the sample's step), rows
-                             // 1 .. nk - 1 from the frame's observation rows (by its agent)
+                             // 1 .. nk - 1 from the frame's observation rows (by its agent);
+                             // GEMM: 2 = scheduler update in the epilogue (fuse_update), 3 = A tile
+                             // built from the request lanes (a_from_lanes)
   int ksplit;                // GEMM: K split over the cluster halves (auras_dpt_gemm.ksplit)
 };
 static_assert(sizeof(DpOpDev) == 112, "DpOpDev");
